@@ -1,0 +1,210 @@
+/*
+ * nucsim_b200.h -- C ABI of the B200-native gate-application path.
+ *
+ * The reference (arXiv 2310.17739 `nucsim` 0.1.0, /root/reference/pkg) has no
+ * FFI: its boundary is the Python API re-exported by nucsim/__init__.py:10-76.
+ * Each entry point below replaces one reference function on the hot path
+ * (SURVEY.md section 8b); the replaced reference symbol is cited per entry.
+ * The Python mirror of that API (paper_2310_17739_b200/) binds these symbols
+ * with ctypes; INTEGRATION.md shows the binding a nucsim maintainer would add.
+ *
+ * Conventions
+ *   - Complex numbers are interleaved (re, im) float64 pairs; matrices are
+ *     row-major, matrix index = sum_j bit(qubits[j]) << j (slot 0 = LSB),
+ *     exactly the reference convention (gates.py:1-17, engine.py:104-107).
+ *   - State vectors are little-endian: qubit 0 is the least significant bit
+ *     of the basis index (engine.py:1-6).
+ *   - Every call returns an int status (NSB_OK = 0).  Calls that can fail
+ *     with a reference exception also fill an nsb_status (may be NULL).
+ *     No C++ exception, callback or torch type crosses this ABI.
+ *   - Calls are synchronous: device work has completed when they return.
+ */
+#ifndef NUCSIM_B200_H
+#define NUCSIM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NSB_ABI_VERSION 1
+
+/* ---- status ------------------------------------------------------------ */
+enum {
+  NSB_OK = 0,
+  NSB_EINVAL = 1,    /* ValueError                     (engine.py:88-89, 96-97, 110-115) */
+  NSB_EASSERT = 2,   /* FilterAssertionError(step, prob) (engine.py:187-190, errors.py:27-33) */
+  NSB_EPROJECT = 3,  /* ProjectionError                (engine.py:177-178) */
+  NSB_ERESOURCE = 4, /* ResourceLimitError / out of device memory */
+  NSB_EDEVICE = 5    /* CUDA / NCCL failure -> RuntimeError */
+};
+
+typedef struct nsb_status {
+  int32_t code;
+  int32_t step; /* NSB_EASSERT: assertion step */
+  double prob;  /* NSB_EASSERT / NSB_EPROJECT: offending probability */
+  char msg[256];
+} nsb_status;
+
+/* ---- packed instruction list (the SoA-free op record) -------------------
+ * One record per reference Instruction (circuit.py:20-47).  `tag` is the
+ * gate code = position of the tag in the reference's Gate enum
+ * (gates.py:30-71); markers use NSB_OP_MEASURE / RESET / BARRIER kinds.    */
+enum { NSB_OP_GATE = 0, NSB_OP_MEASURE = 1, NSB_OP_RESET = 2, NSB_OP_BARRIER = 3 };
+
+enum {
+  NSB_GATE_U3 = 0, NSB_GATE_U2, NSB_GATE_U1, NSB_GATE_CX, NSB_GATE_ID, NSB_GATE_X,
+  NSB_GATE_Y, NSB_GATE_Z, NSB_GATE_H, NSB_GATE_S, NSB_GATE_SDG, NSB_GATE_T,
+  NSB_GATE_TDG, NSB_GATE_RX, NSB_GATE_RY, NSB_GATE_RZ, NSB_GATE_CZ, NSB_GATE_CY,
+  NSB_GATE_SWAP, NSB_GATE_CH, NSB_GATE_CCX, NSB_GATE_CSWAP, NSB_GATE_CRX,
+  NSB_GATE_CRY, NSB_GATE_CRZ, NSB_GATE_CU1, NSB_GATE_CU3, NSB_GATE_RXX,
+  NSB_GATE_RZZ, NSB_GATE_RCCX, NSB_GATE_RC3X, NSB_GATE_C3X, NSB_GATE_C3SQRTX,
+  NSB_GATE_C4X, NSB_GATE_C1, NSB_GATE_C2, NSB_GATE_MEASURE, NSB_GATE_RESET,
+  NSB_GATE_BARRIER, NSB_GATE_COUNT
+};
+
+typedef struct nsb_op {
+  int32_t kind;    /* NSB_OP_* */
+  int32_t tag;     /* NSB_GATE_* */
+  int32_t nq;      /* qubits listed in q[] (0 for barrier: see mask) */
+  int32_t cbit;    /* measure target bit, else -1 */
+  int32_t q[5];    /* qubits in slot order */
+  int32_t src;     /* input index this op was copied from unchanged, else -1 */
+  int64_t param;   /* offset into the float64 params pool, else -1 */
+  int64_t payload; /* offset in COMPLEX elements into the payload pool, else -1 */
+  uint64_t mask;   /* qubit set as a bitmask (all kinds, n <= 64) */
+} nsb_op;          /* 64 bytes */
+
+/* ---- gate vocabulary --------------------------------------------------- */
+
+/* Dense matrix of a named gate, bit-identical to reference gate_matrix
+ * (gates.py:283-291).  out: (2^k)^2 complex.  Replaces gates.gate_matrix. */
+int nsb_gate_matrix(int32_t tag, const double* params, int32_t n_params, double* out);
+
+/* ---- fusion (replaces fusion.fuse_pipeline, fusion.py:240-251) --------- */
+enum { NSB_PASS_MERGE_1Q = 1, NSB_PASS_ABSORB_1Q = 2, NSB_PASS_NORMALIZE_2Q = 4,
+       NSB_PASS_FUSE_2Q = 8, NSB_PASS_ALL = 15 };
+
+/* OpenBLAS zgemm FMA order the reference's `@` reproduces on the host
+ * (SURVEY Appendix A.3): CHAIN2 = SkylakeX/SapphireRapids cores (2x2 single
+ * chain, 4x4 four accumulators), FOUR = Haswell/Zen (four accumulators). */
+enum { NSB_BLAS_CHAIN2 = 1, NSB_BLAS_FOUR = 2 };
+
+typedef struct nsb_fused {
+  nsb_op* ops;        /* fused list, library-owned (nsb_fused_free) */
+  int64_t n_ops;
+  double* payloads;   /* complex payload pool referenced by ops[].payload */
+  int64_t n_payload;  /* complex elements */
+  int64_t gates_before;
+  int64_t pass_before[4]; /* gate counts around each pass (fusion.py:77-79) */
+  int64_t pass_after[4];
+} nsb_fused;
+
+/* Run the selected passes in the reference order merge_1q -> absorb_1q ->
+ * normalize_2q_order -> fuse_2q (fusion.py:101-237).  Unchanged input ops
+ * keep `src`; fused C1/C2 payloads live in out->payloads. */
+int nsb_fuse(const nsb_op* ops, int64_t n_ops, const double* params,
+             const double* payloads, int32_t pass_mask, int32_t blas_variant,
+             nsb_fused* out, nsb_status* st);
+void nsb_fused_free(nsb_fused* f);
+
+/* ---- native workload generator (projection.build_filter_circuit,
+ *      projection.py:191-255) ------------------------------------------- */
+/* terms: n_terms Pauli words, letters[t*n_system + q] in {0:I,1:X,2:Y,3:Z};
+ * coeffs: real coefficients (already in the reference's sorted_terms order);
+ * steps: n_steps (t_i, delta_i) pairs.  Emits the instruction stream of
+ * build_filter_circuit(h, schedule, trotter, basis trial `trial_bits`). */
+int nsb_generate_filter(int32_t n_system, const uint8_t* letters, const double* coeffs,
+                        int64_t n_terms, const double* steps, int32_t n_steps,
+                        int64_t trotter, const uint8_t* trial_bits,
+                        nsb_fused* out, double** params_out, int64_t* n_params_out,
+                        nsb_status* st);
+void nsb_free(void* p);
+
+/* ---- device context and state (replaces engine.StateVector,
+ *      engine.py:42-84) --------------------------------------------------- */
+typedef struct nsb_ctx nsb_ctx;
+
+int nsb_device_count(int32_t* n);
+int nsb_ctx_create(int32_t device, nsb_ctx** out, nsb_status* st);
+void nsb_ctx_destroy(nsb_ctx* ctx);
+/* allocate 2^n amplitudes on the device and set |0...0> */
+int nsb_state_init(nsb_ctx* ctx, int32_t n_qubits, nsb_status* st);
+int nsb_state_reset(nsb_ctx* ctx, nsb_status* st);                /* StateVector.restart */
+int nsb_state_upload(nsb_ctx* ctx, const double* amps, nsb_status* st);
+int nsb_state_download(nsb_ctx* ctx, double* amps, nsb_status* st);
+int nsb_state_norm2(nsb_ctx* ctx, double* out, nsb_status* st);
+
+/* ---- single-op kernels (apply_1q / apply_2q / apply_dense,
+ *      engine.py:92-156) --------------------------------------------------- */
+/* k = 1..5 distinct qubits; u is (2^k)^2 complex, slot j = qubits[j]. */
+int nsb_apply_matrix(nsb_ctx* ctx, const double* u, const int32_t* qubits, int32_t k,
+                     nsb_status* st);
+
+/* ---- measurement (engine.py:159-191) ---------------------------------- */
+/* P(qubit q = outcome) = sum |a_i|^2 over that half (_branch_probability) */
+int nsb_branch_probability(nsb_ctx* ctx, int32_t q, int32_t outcome, double* p,
+                           nsb_status* st);
+/* zero the other half and scale by 1/sqrt(prob) (_project) */
+int nsb_project(nsb_ctx* ctx, int32_t q, int32_t outcome, double prob, nsb_status* st);
+/* |a_i|^2 as re*re + im*im without FMA contraction (sample, engine.py:215) */
+int nsb_probabilities(nsb_ctx* ctx, double* out, nsb_status* st);
+/* <psi| sum_t c_t P_t |psi> (expectation_pauli, engine.py:225-239).
+ * Term t acts as (P_t psi)[j] = (-1)^popcount(j & zmask[t]) psi[j ^ xmask[t]]
+ * (xmask: X and Y letters, zmask: Z and Y letters); coeffs are complex
+ * (re, im) pairs with the (-i)^#Y phase of the Y letters already folded in. */
+int nsb_expectation_pauli(nsb_ctx* ctx, const uint64_t* xmask, const uint64_t* zmask,
+                          const double* coeffs, int64_t n_terms, double* out_re,
+                          double* out_im, nsb_status* st);
+
+/* ---- compiled plans: the fused gate stream resident on the device
+ *      (engine._compile + run, engine.py:295-477) ------------------------ */
+typedef struct nsb_plan nsb_plan;
+
+typedef struct nsb_plan_info {
+  int64_t n_gates;      /* gate ops in the plan */
+  int64_t n_measures;   /* mid-circuit MEASURE ops */
+  int64_t n_resets;
+  int64_t n_passes;     /* state sweeps (memory passes) the schedule needs */
+  int64_t n_segments;   /* gate segments between MEASURE/RESET ops */
+  int64_t flops;        /* FP64 flops of all gate ops (8 * nnz * 2^(n-k)) */
+  int64_t tile_qubits;  /* qubits per cache-blocked tile */
+  int64_t n_items;      /* gate segments + markers (nsb_plan_segment_marker) */
+  int64_t n_stages;     /* shared-memory round trips over all passes */
+} nsb_plan_info;
+
+/* ops: the executable part of the circuit (sampling block already removed,
+ * barriers allowed and dropped).  Matrices of named gates come from params
+ * (nsb_gate_matrix), C1/C2/k-qubit payloads from `payloads`. */
+int nsb_plan_create(nsb_ctx* ctx, const nsb_op* ops, int64_t n_ops, const double* params,
+                    const double* payloads, nsb_plan** out, nsb_status* st);
+void nsb_plan_destroy(nsb_plan* plan);
+/* Host-only dry run of the planner (no device needed): the schedule that
+ * nsb_plan_create would upload, summarised.  class_counts (6 entries, may be
+ * NULL) receives the gate count per payload class (dense 1q, diagonal 1q,
+ * dense 2q, <=2 nnz/row 2q, monomial 2q, diagonal 2q). */
+int nsb_plan_analyze(const nsb_op* ops, int64_t n_ops, const double* params,
+                     const double* payloads, int32_t n_qubits, nsb_plan_info* info,
+                     int64_t* class_counts, nsb_status* st);
+int nsb_plan_info_get(const nsb_plan* plan, nsb_plan_info* info);
+
+/* MMA mode (engine.py:414-423): execute the whole plan from the current
+ * state; each MEASURE asserts |0> (p0 < eps -> NSB_EASSERT with step/p0),
+ * records p0 into assert_probs[step] and renormalises; RESET is a no-op. */
+int nsb_plan_run_mma(nsb_ctx* ctx, nsb_plan* plan, double eps, double* assert_probs,
+                     nsb_status* st);
+/* Gate segment `seg` only (rejection mode drives MEASURE/RESET from the host,
+ * engine.py:439-459).  Segment s ends at marker op index seg_marker[s]. */
+int nsb_plan_run_segment(nsb_ctx* ctx, nsb_plan* plan, int64_t seg, nsb_status* st);
+int nsb_plan_segment_marker(const nsb_plan* plan, int64_t seg, int32_t* kind, int32_t* qubit,
+                            int32_t* step);
+
+/* Device time of the last nsb_plan_run_* call in milliseconds (CUDA events
+ * on the launching stream), and the number of kernels it launched. */
+int nsb_plan_last_timing(const nsb_plan* plan, double* ms, int64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NUCSIM_B200_H */

@@ -1,0 +1,1078 @@
+// sm_100a kernels and the device half of the C ABI.
+//
+// Reference hot path (nucsim/engine.py) and its replacement here:
+//   apply_1q / apply_2q / apply_dense (92-156)  -> k_apply1 / k_apply2 / k_applyk
+//   _branch_probability (159-161)               -> k_half_norm + k_sum_fixed
+//   _project (164-167)                          -> k_project
+//   sample's |a|^2 (215)                        -> k_probabilities (no FMA)
+//   expectation_pauli (225-239)                 -> k_pauli_term
+//   run()'s gate loop + MMA asserts (414-423)   -> k_blocked: ONE persistent
+//       cooperative launch walks the whole fused gate stream; each pass moves
+//       the state through shared memory once (global traffic 32 B/amplitude)
+//       and applies every gate of the pass in registers, stage by stage;
+//       mid-circuit assertions are epilogue reductions + prologue collapses
+//       separated by grid-wide barriers.
+// The state is complex128 in HBM as double2 (16-byte vector loads/stores).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <memory>
+#include <new>
+#include <stdexcept>
+#include <string>
+
+#include "device.cuh"
+#include "planner_host.h"
+
+namespace cg = cooperative_groups;
+
+namespace nsb {
+namespace dev {
+
+constexpr int kReduceThreads = 256;
+constexpr int kReduceBlocks = 1184;  // 8 x 148 SMs: fixed => deterministic sums
+
+// ---------------------------------------------------------------------------
+// per-op kernels
+
+__global__ void k_vacuum(double2* __restrict__ a, uint64_t n_amps) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n_amps;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    a[i] = make_double2(i == 0 ? 1.0 : 0.0, 0.0);
+}
+
+struct M2 {
+  double2 m[4];
+};
+struct M4 {
+  double2 m[16];
+};
+
+__global__ void k_apply1(double2* __restrict__ a, uint64_t n_pairs, int q, M2 u) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n_pairs;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t i0 = insert_zero(i, q), i1 = i0 | (uint64_t(1) << q);
+    const double2 x = a[i0], y = a[i1];
+    double2 o0 = make_double2(0.0, 0.0), o1 = o0;
+    cmac(o0, u.m[0], x);
+    cmac(o0, u.m[1], y);
+    cmac(o1, u.m[2], x);
+    cmac(o1, u.m[3], y);
+    a[i0] = o0;
+    a[i1] = o1;
+  }
+}
+
+// p < q; matrix index = bit(p) + 2 bit(q)  (engine.py:104-121)
+__global__ void k_apply2(double2* __restrict__ a, uint64_t n_quads, int p, int q, M4 u) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n_quads;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t b = insert_zero(insert_zero(i, p), q);
+    const uint64_t idx[4] = {b, b | (uint64_t(1) << p), b | (uint64_t(1) << q),
+                             b | (uint64_t(1) << p) | (uint64_t(1) << q)};
+    double2 x[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) x[c] = a[idx[c]];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      double2 o = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) cmac(o, u.m[4 * r + c], x[c]);
+      a[idx[r]] = o;
+    }
+  }
+}
+
+struct KQ {
+  int k;
+  int slot_q[5];    // qubit of matrix slot j
+  int sorted_q[5];  // same qubits ascending (for zero insertion)
+};
+
+// dense k-qubit matrix (k <= 5) on arbitrary qubits (engine.py:130-156)
+__global__ void k_applyk(double2* __restrict__ a, uint64_t n_groups, KQ g,
+                         const double2* __restrict__ m) {
+  const int dim = 1 << g.k;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n_groups;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    uint64_t base = i;
+    for (int j = 0; j < g.k; ++j) base = insert_zero(base, g.sorted_q[j]);
+    double2 x[32], o[32];
+    uint64_t idx[32];
+    for (int s = 0; s < dim; ++s) {
+      uint64_t e = base;
+      for (int j = 0; j < g.k; ++j)
+        if (s >> j & 1) e |= uint64_t(1) << g.slot_q[j];
+      idx[s] = e;
+      x[s] = a[e];
+    }
+    for (int r = 0; r < dim; ++r) {
+      double2 acc = make_double2(0.0, 0.0);
+      for (int c = 0; c < dim; ++c) cmac(acc, __ldg(m + r * dim + c), x[c]);
+      o[r] = acc;
+    }
+    for (int s = 0; s < dim; ++s) a[idx[s]] = o[s];
+  }
+}
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) s += red[w];
+  return s;  // valid in thread 0
+}
+
+// sum |a_i|^2 over indices with bit q == outcome, per-block partials
+__global__ void k_half_norm(const double2* __restrict__ a, uint64_t n_half, int q, int outcome,
+                            double* __restrict__ partials) {
+  __shared__ double red[32];
+  double s = 0.0;
+  const uint64_t bit = uint64_t(outcome) << q;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n_half;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const double2 v = a[insert_zero(i, q) | bit];
+    s = fma(v.x, v.x, s);
+    s = fma(v.y, v.y, s);
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+__global__ void k_norm2(const double2* __restrict__ a, uint64_t n, double* __restrict__ partials) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const double2 v = a[i];
+    s = fma(v.x, v.x, s);
+    s = fma(v.y, v.y, s);
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+// fixed-order (sequential per lane, then butterfly) sum of `count` values
+__global__ void k_sum_fixed(const double* __restrict__ in, int count, int stride_out,
+                            double* __restrict__ out) {
+  const int lane = threadIdx.x;
+  double s = 0.0;
+  for (int i = lane; i < count; i += 32) s += in[i];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) out[0] = s;
+  (void)stride_out;
+}
+
+__global__ void k_project(double2* __restrict__ a, uint64_t n, int q, int outcome, double scale) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    double2 v = a[i];
+    if (int((i >> q) & 1) != outcome) {
+      v = make_double2(0.0, 0.0);
+    } else {
+      v.x = v.x * scale;
+      v.y = v.y * scale;
+    }
+    a[i] = v;
+  }
+}
+
+// numpy: amps.real**2 + amps.imag**2 -- two roundings per product, one per
+// sum, no contraction (engine.py:215)
+__global__ void k_probabilities(const double2* __restrict__ a, uint64_t n, double* __restrict__ p) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const double2 v = a[i];
+    p[i] = __dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y));
+  }
+}
+
+// sum_j conj(a_j) (-1)^popc(j & zmask) a_{j ^ xmask}, per-block complex partials
+__global__ void k_pauli_term(const double2* __restrict__ a, uint64_t n, uint64_t xmask,
+                             uint64_t zmask, double* __restrict__ partials) {
+  __shared__ double red[32];
+  double sr = 0.0, si = 0.0;
+  for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < n;
+       j += uint64_t(gridDim.x) * blockDim.x) {
+    const double2 u = a[j], v = a[j ^ xmask];
+    double pr = fma(u.x, v.x, u.y * v.y);  // conj(u) * v
+    double pi = fma(u.x, v.y, -(u.y * v.x));
+    if (__popcll(j & zmask) & 1) {
+      pr = -pr;
+      pi = -pi;
+    }
+    sr += pr;
+    si += pi;
+  }
+  sr = block_sum(sr, red);
+  si = block_sum(si, red);
+  if (threadIdx.x == 0) {
+    partials[2 * blockIdx.x] = sr;
+    partials[2 * blockIdx.x + 1] = si;
+  }
+}
+
+__global__ void k_sum_fixed2(const double* __restrict__ in, int count, double* __restrict__ out) {
+  const int lane = threadIdx.x;
+  double sr = 0.0, si = 0.0;
+  for (int i = lane; i < count; i += 32) {
+    sr += in[2 * i];
+    si += in[2 * i + 1];
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    sr += __shfl_xor_sync(0xffffffffu, sr, off);
+    si += __shfl_xor_sync(0xffffffffu, si, off);
+  }
+  if (lane == 0) {
+    out[0] = sr;
+    out[1] = si;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// blocked gate-stream kernel
+
+struct BlockedParams {
+  double2* amps;
+  int n;
+  const PassDesc* passes;
+  int pass_begin, pass_end;
+  const StageDesc* stages;
+  const GateDesc* gates;
+  const double2* mats;
+  double* partials;  // 2 * gridDim
+  double* record;    // p0 per assertion step
+  int* fail;         // [0] flag, [1] step
+  double eps;
+};
+
+template <int P, int Q>
+struct QuadBase {  // the 4 group indices with bits P, Q clear
+  static constexpr int other0 = (P != 0 && Q != 0) ? 0 : ((P != 1 && Q != 1) ? 1 : 2);
+  static constexpr int other1 = [] {
+    for (int b = other0 + 1; b < 4; ++b)
+      if (b != P && b != Q) return b;
+    return 3;
+  }();
+  static constexpr int at(int i) { return ((i & 1) << other0) | ((i >> 1 & 1) << other1); }
+};
+
+template <int P>
+__device__ __forceinline__ void g1_dense(double2 (&a)[16], const double2* __restrict__ m) {
+  const double2 m0 = __ldg(m), m1 = __ldg(m + 1), m2 = __ldg(m + 2), m3 = __ldg(m + 3);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    if (i & (1 << P)) continue;
+    const int j = i | (1 << P);
+    const double2 x = a[i], y = a[j];
+    double2 o0 = make_double2(0.0, 0.0), o1 = o0;
+    cmac(o0, m0, x);
+    cmac(o0, m1, y);
+    cmac(o1, m2, x);
+    cmac(o1, m3, y);
+    a[i] = o0;
+    a[j] = o1;
+  }
+}
+
+template <int P>
+__device__ __forceinline__ void g1_diag(double2 (&a)[16], const double2* __restrict__ m) {
+  const double2 d0 = __ldg(m), d1 = __ldg(m + 1);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = cmul((i & (1 << P)) ? d1 : d0, a[i]);
+}
+
+template <int P, int Q>
+__device__ __forceinline__ void g2_dense(double2 (&a)[16], const double2* __restrict__ m) {
+#pragma unroll
+  for (int qd = 0; qd < 4; ++qd) {
+    const int b = QuadBase<P, Q>::at(qd);
+    const int idx[4] = {b, b | (1 << P), b | (1 << Q), b | (1 << P) | (1 << Q)};
+    const double2 x0 = a[idx[0]], x1 = a[idx[1]], x2 = a[idx[2]], x3 = a[idx[3]];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      double2 o = make_double2(0.0, 0.0);
+      cmac(o, __ldg(m + 4 * r + 0), x0);
+      cmac(o, __ldg(m + 4 * r + 1), x1);
+      cmac(o, __ldg(m + 4 * r + 2), x2);
+      cmac(o, __ldg(m + 4 * r + 3), x3);
+      a[idx[r]] = o;
+    }
+  }
+}
+
+__device__ __forceinline__ double2 pick(const double2 x0, const double2 x1, const double2 x2,
+                                        const double2 x3, int c) {
+  double2 r = x0;
+  r = c == 1 ? x1 : r;
+  r = c == 2 ? x2 : r;
+  r = c == 3 ? x3 : r;
+  return r;
+}
+
+template <int P, int Q>
+__device__ __forceinline__ void g2_sparse(double2 (&a)[16], const double2* __restrict__ m,
+                                          unsigned cols) {
+  double2 v[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) v[e] = __ldg(m + e);
+#pragma unroll
+  for (int qd = 0; qd < 4; ++qd) {
+    const int b = QuadBase<P, Q>::at(qd);
+    const int idx[4] = {b, b | (1 << P), b | (1 << Q), b | (1 << P) | (1 << Q)};
+    const double2 x0 = a[idx[0]], x1 = a[idx[1]], x2 = a[idx[2]], x3 = a[idx[3]];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      double2 o = make_double2(0.0, 0.0);
+      cmac(o, v[2 * r], pick(x0, x1, x2, x3, (cols >> (4 * r)) & 3));
+      cmac(o, v[2 * r + 1], pick(x0, x1, x2, x3, (cols >> (4 * r + 2)) & 3));
+      a[idx[r]] = o;
+    }
+  }
+}
+
+template <int P, int Q>
+__device__ __forceinline__ void g2_mono(double2 (&a)[16], const double2* __restrict__ m,
+                                        unsigned cols) {
+  const double2 v0 = __ldg(m), v1 = __ldg(m + 1), v2 = __ldg(m + 2), v3 = __ldg(m + 3);
+  const int c0 = cols & 3, c1 = (cols >> 2) & 3, c2 = (cols >> 4) & 3, c3 = (cols >> 6) & 3;
+#pragma unroll
+  for (int qd = 0; qd < 4; ++qd) {
+    const int b = QuadBase<P, Q>::at(qd);
+    const int idx[4] = {b, b | (1 << P), b | (1 << Q), b | (1 << P) | (1 << Q)};
+    const double2 x0 = a[idx[0]], x1 = a[idx[1]], x2 = a[idx[2]], x3 = a[idx[3]];
+    a[idx[0]] = cmul(v0, pick(x0, x1, x2, x3, c0));
+    a[idx[1]] = cmul(v1, pick(x0, x1, x2, x3, c1));
+    a[idx[2]] = cmul(v2, pick(x0, x1, x2, x3, c2));
+    a[idx[3]] = cmul(v3, pick(x0, x1, x2, x3, c3));
+  }
+}
+
+template <int P, int Q>
+__device__ __forceinline__ void g2_diag(double2 (&a)[16], const double2* __restrict__ m) {
+  const double2 d[4] = {__ldg(m), __ldg(m + 1), __ldg(m + 2), __ldg(m + 3)};
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = cmul(d[((i >> P) & 1) | (((i >> Q) & 1) << 1)], a[i]);
+}
+
+template <int P, int Q>
+__device__ __forceinline__ void g2(double2 (&a)[16], const GateDesc& d, const double2* m) {
+  switch (d.cls) {
+    case kDense2: g2_dense<P, Q>(a, m); break;
+    case kSparse2: g2_sparse<P, Q>(a, m, d.cols); break;
+    case kMono2: g2_mono<P, Q>(a, m, d.cols); break;
+    default: g2_diag<P, Q>(a, m); break;
+  }
+}
+
+__device__ __forceinline__ void apply_gate(double2 (&a)[16], const GateDesc& d,
+                                           const double2* __restrict__ mats) {
+  const double2* m = mats + d.mat;
+  if (d.cls <= kDiag1) {
+    const bool diag = d.cls == kDiag1;
+    switch (d.a) {
+      case 0: diag ? g1_diag<0>(a, m) : g1_dense<0>(a, m); break;
+      case 1: diag ? g1_diag<1>(a, m) : g1_dense<1>(a, m); break;
+      case 2: diag ? g1_diag<2>(a, m) : g1_dense<2>(a, m); break;
+      default: diag ? g1_diag<3>(a, m) : g1_dense<3>(a, m); break;
+    }
+    return;
+  }
+  switch (d.a * 4 + d.b) {
+    case 1: g2<0, 1>(a, d, m); break;
+    case 2: g2<0, 2>(a, d, m); break;
+    case 3: g2<0, 3>(a, d, m); break;
+    case 6: g2<1, 2>(a, d, m); break;
+    case 7: g2<1, 3>(a, d, m); break;
+    default: g2<2, 3>(a, d, m); break;
+  }
+}
+
+__global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
+  extern __shared__ __align__(16) double2 tile[];
+  __shared__ PassDesc sp;
+  __shared__ double red[32];
+  __shared__ double s_p0;
+  cg::grid_group grid = cg::this_grid();
+  const int tid = threadIdx.x;
+  double carry_p0 = 1.0;  // p0 of the previous pass's assertion (collapse input)
+
+  for (int pi = p.pass_begin; pi < p.pass_end; ++pi) {
+    __syncthreads();
+    if (tid < int(sizeof(PassDesc) / sizeof(int)))
+      reinterpret_cast<int*>(&sp)[tid] = reinterpret_cast<const int*>(p.passes + pi)[tid];
+    __syncthreads();
+    const int k = sp.k;
+    const int n_out = p.n - k;
+    const uint64_t n_tiles = uint64_t(1) << n_out;
+    const int cq = sp.collapse_q, mq = sp.measure_q;
+    const double cscale = cq >= 0 ? 1.0 / sqrt(carry_p0) : 1.0;
+
+    // tile-local -> global scatter of this thread's load/store index
+    // l = tid + 256 j  (k >= 8);  l = tid (k < 8, tid < 2^k)
+    const int lo_bits = k < 8 ? k : 8;
+    uint64_t lo = 0;
+    for (int b = 0; b < lo_bits; ++b)
+      if (tid >> b & 1) lo |= uint64_t(1) << sp.tq[b];
+    uint64_t hbit[4] = {0, 0, 0, 0};
+    for (int b = 0; b < 4; ++b)
+      if (8 + b < k) hbit[b] = uint64_t(1) << sp.tq[8 + b];
+    const int n_j = k > 8 ? 1 << (k - 8) : 1;
+    const bool loader = tid < (1 << lo_bits);
+
+    // stage-invariant thread role
+    const int n_group_threads = 1 << (k - kGroupQubits);
+    double msum = 0.0;
+
+    for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      uint64_t base = 0;
+      for (int b = 0; b < n_out; ++b)
+        if (t >> b & 1) base |= uint64_t(1) << sp.oq[b];
+      // global -> shared (+ collapse prologue)
+      if (loader) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (j >= n_j) break;
+          const uint64_t g = base | lo | ((j & 1) ? hbit[0] : 0) | ((j & 2) ? hbit[1] : 0) |
+                             ((j & 4) ? hbit[2] : 0) | ((j & 8) ? hbit[3] : 0);
+          double2 v = p.amps[g];
+          if (cq >= 0) {
+            if ((g >> cq) & 1) {
+              v = make_double2(0.0, 0.0);
+            } else {
+              v.x *= cscale;
+              v.y *= cscale;
+            }
+          }
+          tile[swz(tid + (j << 8))] = v;
+        }
+      }
+      __syncthreads();
+      // stages: shared -> registers -> gates -> shared
+      for (int s = sp.stage_begin; s < sp.stage_end; ++s) {
+        const StageDesc S = p.stages[s];
+        if (tid < n_group_threads) {
+          int tb = 0;
+          for (int b = 0; b < k - kGroupQubits; ++b)
+            if (tid >> b & 1) tb |= 1 << ((S.tperm >> (4 * b)) & 15);
+          const int r0 = 1 << S.rpos[0], r1 = 1 << S.rpos[1], r2 = 1 << S.rpos[2],
+                    r3 = 1 << S.rpos[3];
+          int addr[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            addr[i] = swz(tb | ((i & 1) ? r0 : 0) | ((i & 2) ? r1 : 0) | ((i & 4) ? r2 : 0) |
+                          ((i & 8) ? r3 : 0));
+          double2 a[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) a[i] = tile[addr[i]];
+          for (int g = S.gate_begin; g < S.gate_end; ++g) {
+            const GateDesc d = p.gates[g];
+            apply_gate(a, d, p.mats);
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) tile[addr[i]] = a[i];
+        }
+        __syncthreads();
+      }
+      // shared -> global (+ assertion epilogue partial sums)
+      if (loader) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (j >= n_j) break;
+          const uint64_t g = base | lo | ((j & 1) ? hbit[0] : 0) | ((j & 2) ? hbit[1] : 0) |
+                             ((j & 4) ? hbit[2] : 0) | ((j & 8) ? hbit[3] : 0);
+          const double2 v = tile[swz(tid + (j << 8))];
+          p.amps[g] = v;
+          if (mq >= 0 && !((g >> mq) & 1)) {
+            msum = fma(v.x, v.x, msum);
+            msum = fma(v.y, v.y, msum);
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (mq >= 0) {
+      const double bs = block_sum(msum, red);
+      if (tid == 0) p.partials[(sp.measure_slot & 1) * gridDim.x + blockIdx.x] = bs;
+    }
+    __threadfence();
+    grid.sync();
+    if (mq >= 0) {
+      if (tid < 32) {
+        const double* part = p.partials + (sp.measure_slot & 1) * gridDim.x;
+        double s = 0.0;
+        for (int i = tid; i < int(gridDim.x); i += 32) s += part[i];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (tid == 0) s_p0 = s;
+      }
+      __syncthreads();
+      carry_p0 = s_p0;
+      if (blockIdx.x == 0 && tid == 0) {
+        p.record[sp.measure_slot] = carry_p0;
+        if (carry_p0 < p.eps) {
+          p.fail[0] = 1;
+          p.fail[1] = sp.measure_slot;
+        }
+      }
+      if (carry_p0 < p.eps) return;  // every block saw the same p0
+    }
+  }
+}
+
+}  // namespace dev
+}  // namespace nsb
+
+// ===========================================================================
+// host side
+
+using namespace nsb;
+
+namespace {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define NSB_CUDA(call)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      throw CudaError(std::string(#call) + ": " + cudaGetErrorString(e_));              \
+  } while (0)
+
+template <class T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t count = 0;
+  void alloc(size_t n) {
+    release();
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMalloc(&ptr, n * sizeof(T));
+    if (e != cudaSuccess) {
+      ptr = nullptr;
+      throw std::bad_alloc();
+    }
+    count = n;
+  }
+  void upload(const T* src, size_t n, cudaStream_t s) {
+    alloc(n);
+    if (n) NSB_CUDA(cudaMemcpyAsync(ptr, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    count = 0;
+  }
+  ~DevBuf() { release(); }
+};
+
+}  // namespace
+
+struct nsb_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int sm_count = 0;
+  int blocked_grid = 0;  // co-resident CTAs of k_blocked
+  int n = 0;
+  uint64_t n_amps = 0;
+  DevBuf<double2> amps;
+  DevBuf<double> scratch;  // reductions
+  double* pinned = nullptr;
+  size_t pinned_bytes = 0;
+};
+
+struct nsb_plan {
+  nsb_ctx* ctx = nullptr;
+  HostPlan host;
+  DevBuf<PassDesc> passes, mma_passes;
+  DevBuf<StageDesc> stages;
+  DevBuf<GateDesc> gates;
+  DevBuf<double2> mats, dense;
+  DevBuf<double> record, partials;
+  DevBuf<int> fail;
+  double last_ms = 0.0;
+  int64_t last_launches = 0;
+};
+
+namespace {
+
+int fail_status(nsb_status* st, int code, const std::string& msg) {
+  set_status(st, code, msg);
+  return code;
+}
+
+template <class F>
+int guarded(nsb_status* st, F&& f) {
+  set_status(st, NSB_OK, "");
+  try {
+    f();
+  } catch (const CudaError& e) {
+    return fail_status(st, NSB_EDEVICE, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail_status(st, NSB_ERESOURCE, "out of device or host memory");
+  } catch (const std::invalid_argument& e) {
+    return fail_status(st, NSB_EINVAL, e.what());
+  } catch (const std::exception& e) {
+    return fail_status(st, NSB_EDEVICE, e.what());
+  }
+  return st ? st->code : NSB_OK;
+}
+
+unsigned grid_for(uint64_t work, int threads, const nsb_ctx* c) {
+  const uint64_t want = (work + threads - 1) / threads;
+  const uint64_t cap = uint64_t(c->sm_count) * 8;
+  return static_cast<unsigned>(std::max<uint64_t>(1, std::min(want, cap)));
+}
+
+void require_state(const nsb_ctx* c) {
+  if (!c || !c->amps.ptr) throw std::invalid_argument("state not initialised");
+}
+
+void ensure_pinned(nsb_ctx* c, size_t bytes) {
+  if (c->pinned_bytes >= bytes) return;
+  if (c->pinned) cudaFreeHost(c->pinned);
+  c->pinned = nullptr;
+  c->pinned_bytes = 0;
+  NSB_CUDA(cudaMallocHost(&c->pinned, bytes));
+  c->pinned_bytes = bytes;
+}
+
+// deterministic half-norm: fixed grid, then fixed-order sum
+double half_norm(nsb_ctx* c, int q, int outcome) {
+  const uint64_t n_half = c->n_amps >> 1;
+  dev::k_half_norm<<<dev::kReduceBlocks, dev::kReduceThreads, 0, c->stream>>>(
+      c->amps.ptr, n_half, q, outcome, c->scratch.ptr);
+  dev::k_sum_fixed<<<1, 32, 0, c->stream>>>(c->scratch.ptr, dev::kReduceBlocks, 0,
+                                             c->scratch.ptr + 2 * dev::kReduceBlocks);
+  double out = 0.0;
+  NSB_CUDA(cudaMemcpyAsync(&out, c->scratch.ptr + 2 * dev::kReduceBlocks, sizeof(double),
+                           cudaMemcpyDeviceToHost, c->stream));
+  NSB_CUDA(cudaStreamSynchronize(c->stream));
+  return out;
+}
+
+void project(nsb_ctx* c, int q, int outcome, double prob) {
+  const double scale = 1.0 / std::sqrt(prob);
+  dev::k_project<<<grid_for(c->n_amps, 256, c), 256, 0, c->stream>>>(c->amps.ptr, c->n_amps, q,
+                                                                      outcome, scale);
+  NSB_CUDA(cudaGetLastError());
+}
+
+void apply_matrix(nsb_ctx* c, const double* u, const int32_t* qubits, int k,
+                  const double2* dev_mat /* optional, for k >= 3 */) {
+  for (int j = 0; j < k; ++j) {
+    if (qubits[j] < 0 || qubits[j] >= c->n) throw std::invalid_argument("qubit out of range");
+    for (int i = 0; i < j; ++i)
+      if (qubits[i] == qubits[j]) throw std::invalid_argument("duplicate qubit");
+  }
+  if (k == 1) {
+    dev::M2 m;
+    std::memcpy(m.m, u, sizeof(m.m));
+    dev::k_apply1<<<grid_for(c->n_amps >> 1, 256, c), 256, 0, c->stream>>>(
+        c->amps.ptr, c->n_amps >> 1, qubits[0], m);
+  } else if (k == 2) {
+    dev::M4 m;
+    int p = qubits[0], q = qubits[1];
+    if (p < q) {
+      std::memcpy(m.m, u, sizeof(m.m));
+    } else {  // swap_conjugate (engine.py:124-127)
+      static const int perm[4] = {0, 2, 1, 3};
+      for (int r = 0; r < 4; ++r)
+        for (int col = 0; col < 4; ++col) {
+          m.m[4 * r + col].x = u[2 * (perm[r] * 4 + perm[col])];
+          m.m[4 * r + col].y = u[2 * (perm[r] * 4 + perm[col]) + 1];
+        }
+      std::swap(p, q);
+    }
+    dev::k_apply2<<<grid_for(c->n_amps >> 2, 256, c), 256, 0, c->stream>>>(
+        c->amps.ptr, c->n_amps >> 2, p, q, m);
+  } else {
+    if (k > 5 || k > c->n) throw std::invalid_argument("at most 5 qubits per dense gate");
+    dev::KQ g;
+    g.k = k;
+    for (int j = 0; j < k; ++j) g.slot_q[j] = g.sorted_q[j] = qubits[j];
+    std::sort(g.sorted_q, g.sorted_q + k);
+    const double2* m = dev_mat;
+    DevBuf<double2> tmp;
+    if (!m) {
+      tmp.upload(reinterpret_cast<const double2*>(u), size_t(1) << (2 * k), c->stream);
+      m = tmp.ptr;
+    }
+    dev::k_applyk<<<grid_for(c->n_amps >> k, 128, c), 128, 0, c->stream>>>(
+        c->amps.ptr, c->n_amps >> k, g, m);
+    NSB_CUDA(cudaGetLastError());
+    if (!dev_mat) NSB_CUDA(cudaStreamSynchronize(c->stream));  // tmp lifetime
+  }
+  NSB_CUDA(cudaGetLastError());
+}
+
+// launch k_blocked over [pb, pe) of `passes` cooperatively
+void launch_blocked(nsb_ctx* c, nsb_plan* P, const PassDesc* passes, int pb, int pe, double eps) {
+  dev::BlockedParams bp;
+  bp.amps = c->amps.ptr;
+  bp.n = c->n;
+  bp.passes = passes;
+  bp.pass_begin = pb;
+  bp.pass_end = pe;
+  bp.stages = P->stages.ptr;
+  bp.gates = P->gates.ptr;
+  bp.mats = P->mats.ptr;
+  bp.partials = P->partials.ptr;
+  bp.record = P->record.ptr;
+  bp.fail = P->fail.ptr;
+  bp.eps = eps;
+  void* args[] = {&bp};
+  NSB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::k_blocked),
+                                       dim3(c->blocked_grid), dim3(kPassThreads), args,
+                                       sizeof(double2) * kTileAmps, c->stream));
+  P->last_launches += 1;
+}
+
+void run_item(nsb_ctx* c, nsb_plan* P, const Item& it) {
+  if (it.kind == Item::kGates) {
+    launch_blocked(c, P, P->passes.ptr, it.pass_begin, it.pass_end, -1.0);
+  } else if (it.kind == Item::kDense) {
+    const double* u = P->host.dense_mats.data() + 2 * it.mat_off;
+    apply_matrix(c, u, it.qs, it.k, it.k >= 3 ? P->dense.ptr + it.mat_off : nullptr);
+    P->last_launches += 1;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int nsb_device_count(int32_t* n) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) c = 0;
+  if (n) *n = c;
+  return NSB_OK;
+}
+
+int nsb_ctx_create(int32_t device, nsb_ctx** out, nsb_status* st) {
+  if (!out) return fail_status(st, NSB_EINVAL, "null out pointer");
+  *out = nullptr;
+  auto ctx = std::make_unique<nsb_ctx>();
+  const int rc = guarded(st, [&] {
+    int count = 0;
+    NSB_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) throw std::invalid_argument("no such CUDA device");
+    ctx->device = device;
+    NSB_CUDA(cudaSetDevice(device));
+    NSB_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    NSB_CUDA(cudaEventCreate(&ctx->ev0));
+    NSB_CUDA(cudaEventCreate(&ctx->ev1));
+    NSB_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
+    const int smem = sizeof(double2) * kTileAmps;
+    NSB_CUDA(cudaFuncSetAttribute(dev::k_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  smem));
+    int per_sm = 0;
+    NSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_blocked,
+                                                           kPassThreads, smem));
+    if (per_sm < 1) throw std::runtime_error("k_blocked cannot be resident");
+    ctx->blocked_grid = per_sm * ctx->sm_count;
+    ctx->scratch.alloc(4 * dev::kReduceBlocks + 64);
+  });
+  if (rc == NSB_OK) *out = ctx.release();
+  return rc;
+}
+
+void nsb_ctx_destroy(nsb_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  ctx->amps.release();
+  ctx->scratch.release();
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+int nsb_state_init(nsb_ctx* c, int32_t n_qubits, nsb_status* st) {
+  if (!c) return fail_status(st, NSB_EINVAL, "null context");
+  if (n_qubits < 1 || n_qubits > kMaxQubits)
+    return fail_status(st, NSB_EINVAL, "qubit count out of range");
+  return guarded(st, [&] {
+    NSB_CUDA(cudaSetDevice(c->device));
+    const uint64_t n_amps = uint64_t(1) << n_qubits;
+    if (c->n != n_qubits || !c->amps.ptr) {
+      c->amps.release();
+      c->n = 0;
+      c->amps.alloc(n_amps);
+      c->n = n_qubits;
+      c->n_amps = n_amps;
+    }
+    dev::k_vacuum<<<grid_for(n_amps, 256, c), 256, 0, c->stream>>>(c->amps.ptr, n_amps);
+    NSB_CUDA(cudaGetLastError());
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int nsb_state_reset(nsb_ctx* c, nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    NSB_CUDA(cudaSetDevice(c->device));
+    dev::k_vacuum<<<grid_for(c->n_amps, 256, c), 256, 0, c->stream>>>(c->amps.ptr, c->n_amps);
+    NSB_CUDA(cudaGetLastError());
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int nsb_state_upload(nsb_ctx* c, const double* amps, nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    if (!amps) throw std::invalid_argument("null host buffer");
+    NSB_CUDA(cudaSetDevice(c->device));
+    NSB_CUDA(cudaMemcpyAsync(c->amps.ptr, amps, c->n_amps * sizeof(double2),
+                             cudaMemcpyHostToDevice, c->stream));
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int nsb_state_download(nsb_ctx* c, double* amps, nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    if (!amps) throw std::invalid_argument("null host buffer");
+    NSB_CUDA(cudaSetDevice(c->device));
+    NSB_CUDA(cudaMemcpyAsync(amps, c->amps.ptr, c->n_amps * sizeof(double2),
+                             cudaMemcpyDeviceToHost, c->stream));
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int nsb_state_norm2(nsb_ctx* c, double* out, nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    NSB_CUDA(cudaSetDevice(c->device));
+    dev::k_norm2<<<dev::kReduceBlocks, dev::kReduceThreads, 0, c->stream>>>(
+        c->amps.ptr, c->n_amps, c->scratch.ptr);
+    dev::k_sum_fixed<<<1, 32, 0, c->stream>>>(c->scratch.ptr, dev::kReduceBlocks, 0,
+                                               c->scratch.ptr + 2 * dev::kReduceBlocks);
+    NSB_CUDA(cudaMemcpyAsync(out, c->scratch.ptr + 2 * dev::kReduceBlocks, sizeof(double),
+                             cudaMemcpyDeviceToHost, c->stream));
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int nsb_apply_matrix(nsb_ctx* c, const double* u, const int32_t* qubits, int32_t k,
+                     nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    if (!u || !qubits || k < 1) throw std::invalid_argument("bad matrix arguments");
+    NSB_CUDA(cudaSetDevice(c->device));
+    apply_matrix(c, u, qubits, k, nullptr);
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int nsb_branch_probability(nsb_ctx* c, int32_t q, int32_t outcome, double* p, nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    if (q < 0 || q >= c->n || (outcome != 0 && outcome != 1) || !p)
+      throw std::invalid_argument("bad measurement arguments");
+    NSB_CUDA(cudaSetDevice(c->device));
+    *p = half_norm(c, q, outcome);
+  });
+}
+
+int nsb_project(nsb_ctx* c, int32_t q, int32_t outcome, double prob, nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    if (q < 0 || q >= c->n || (outcome != 0 && outcome != 1))
+      throw std::invalid_argument("bad projection arguments");
+    NSB_CUDA(cudaSetDevice(c->device));
+    project(c, q, outcome, prob);
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int nsb_probabilities(nsb_ctx* c, double* out, nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    if (!out) throw std::invalid_argument("null output");
+    NSB_CUDA(cudaSetDevice(c->device));
+    DevBuf<double> probs;
+    probs.alloc(c->n_amps);
+    dev::k_probabilities<<<grid_for(c->n_amps, 256, c), 256, 0, c->stream>>>(
+        c->amps.ptr, c->n_amps, probs.ptr);
+    NSB_CUDA(cudaGetLastError());
+    NSB_CUDA(cudaMemcpyAsync(out, probs.ptr, c->n_amps * sizeof(double), cudaMemcpyDeviceToHost,
+                             c->stream));
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int nsb_expectation_pauli(nsb_ctx* c, const uint64_t* xmask, const uint64_t* zmask,
+                          const double* coeffs, int64_t n_terms, double* out_re, double* out_im,
+                          nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    if (n_terms < 0 || (n_terms > 0 && (!xmask || !zmask || !coeffs)) || !out_re || !out_im)
+      throw std::invalid_argument("bad expectation arguments");
+    NSB_CUDA(cudaSetDevice(c->device));
+    double acc_re = 0.0, acc_im = 0.0;
+    for (int64_t t = 0; t < n_terms; ++t) {
+      dev::k_pauli_term<<<dev::kReduceBlocks, dev::kReduceThreads, 0, c->stream>>>(
+          c->amps.ptr, c->n_amps, xmask[t], zmask[t], c->scratch.ptr);
+      dev::k_sum_fixed2<<<1, 32, 0, c->stream>>>(c->scratch.ptr, dev::kReduceBlocks,
+                                                  c->scratch.ptr + 2 * dev::kReduceBlocks + 8);
+      double s[2];
+      NSB_CUDA(cudaMemcpyAsync(s, c->scratch.ptr + 2 * dev::kReduceBlocks + 8, sizeof s,
+                               cudaMemcpyDeviceToHost, c->stream));
+      NSB_CUDA(cudaStreamSynchronize(c->stream));
+      // acc += coeff * s   (coeff complex: phase of the Y letters folded in)
+      const double cr = coeffs[2 * t], ci = coeffs[2 * t + 1];
+      acc_re += cr * s[0] - ci * s[1];
+      acc_im += cr * s[1] + ci * s[0];
+    }
+    *out_re = acc_re;
+    *out_im = acc_im;
+  });
+}
+
+int nsb_plan_create(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const double* params,
+                    const double* payloads, nsb_plan** out, nsb_status* st) {
+  if (!out) return fail_status(st, NSB_EINVAL, "null out pointer");
+  *out = nullptr;
+  auto P = std::make_unique<nsb_plan>();
+  const int rc = guarded(st, [&] {
+    require_state(c);
+    if (n_ops < 0 || (n_ops > 0 && !ops)) throw std::invalid_argument("bad op list");
+    NSB_CUDA(cudaSetDevice(c->device));
+    P->ctx = c;
+    P->host.build(ops, n_ops, params, payloads, c->n);
+    HostPlan& H = P->host;
+    P->passes.upload(H.passes.data(), H.passes.size(), c->stream);
+    P->mma_passes.upload(H.mma_passes.data(), H.mma_passes.size(), c->stream);
+    P->stages.upload(H.stages.data(), H.stages.size(), c->stream);
+    P->gates.upload(H.gates.data(), H.gates.size(), c->stream);
+    P->mats.upload(reinterpret_cast<const double2*>(H.matrices.data()), H.matrices.size() / 2,
+                   c->stream);
+    P->dense.upload(reinterpret_cast<const double2*>(H.dense_mats.data()),
+                    H.dense_mats.size() / 2, c->stream);
+    P->record.alloc(std::max<int64_t>(H.n_measures, 1));
+    P->partials.alloc(2 * size_t(std::max(c->blocked_grid, 1)));
+    P->fail.alloc(2);
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+  });
+  if (rc == NSB_OK) *out = P.release();
+  return rc;
+}
+
+void nsb_plan_destroy(nsb_plan* plan) {
+  if (!plan) return;
+  if (plan->ctx) cudaSetDevice(plan->ctx->device);
+  delete plan;
+}
+
+int nsb_plan_info_get(const nsb_plan* plan, nsb_plan_info* info) {
+  if (!plan || !info) return NSB_EINVAL;
+  plan_info(plan->host, info);
+  return NSB_OK;
+}
+
+int nsb_plan_run_mma(nsb_ctx* c, nsb_plan* P, double eps, double* assert_probs,
+                     nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    if (!P || P->ctx != c) throw std::invalid_argument("plan belongs to another context");
+    NSB_CUDA(cudaSetDevice(c->device));
+    HostPlan& H = P->host;
+    P->last_launches = 0;
+    NSB_CUDA(cudaMemsetAsync(P->fail.ptr, 0, 2 * sizeof(int), c->stream));
+    NSB_CUDA(cudaEventRecord(c->ev0, c->stream));
+    if (H.mma_ok) {
+      if (!H.mma_passes.empty())
+        launch_blocked(c, P, P->mma_passes.ptr, 0, static_cast<int>(H.mma_passes.size()), eps);
+      NSB_CUDA(cudaEventRecord(c->ev1, c->stream));
+      int fail[2] = {0, 0};
+      NSB_CUDA(cudaMemcpyAsync(fail, P->fail.ptr, sizeof fail, cudaMemcpyDeviceToHost,
+                               c->stream));
+      std::vector<double> rec(std::max<int64_t>(H.n_measures, 1));
+      NSB_CUDA(cudaMemcpyAsync(rec.data(), P->record.ptr, rec.size() * sizeof(double),
+                               cudaMemcpyDeviceToHost, c->stream));
+      NSB_CUDA(cudaStreamSynchronize(c->stream));
+      float ms = 0.f;
+      NSB_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+      P->last_ms = ms;
+      const int n_ok = fail[0] ? fail[1] : static_cast<int>(H.n_measures);
+      if (assert_probs)
+        for (int s = 0; s < n_ok; ++s) assert_probs[s] = rec[s];
+      if (fail[0]) {
+        char buf[128];
+        std::snprintf(buf, sizeof buf, "assertion failed at step %d: P(|0>) = %.3e", fail[1],
+                      rec[fail[1]]);
+        set_status(st, NSB_EASSERT, buf, fail[1], rec[fail[1]]);
+      }
+      return;
+    }
+    // item-by-item: k-qubit gates or the unblocked (n < 6) path
+    for (const Item& it : H.items) {
+      if (it.kind == Item::kMeasure) {
+        const double p0 = half_norm(c, it.qubit, 0);
+        if (p0 < eps) {
+          char buf[128];
+          std::snprintf(buf, sizeof buf, "assertion failed at step %d: P(|0>) = %.3e", it.step, p0);
+          set_status(st, NSB_EASSERT, buf, it.step, p0);
+          break;
+        }
+        if (assert_probs) assert_probs[it.step] = p0;
+        project(c, it.qubit, 0, p0);
+        P->last_launches += 3;
+      } else if (it.kind != Item::kReset) {
+        run_item(c, P, it);
+      }
+    }
+    NSB_CUDA(cudaEventRecord(c->ev1, c->stream));
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+    float ms = 0.f;
+    NSB_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    P->last_ms = ms;
+  });
+}
+
+int nsb_plan_run_segment(nsb_ctx* c, nsb_plan* P, int64_t seg, nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    if (!P || P->ctx != c) throw std::invalid_argument("plan belongs to another context");
+    if (seg < 0 || seg >= static_cast<int64_t>(P->host.items.size()))
+      throw std::invalid_argument("item index out of range");
+    NSB_CUDA(cudaSetDevice(c->device));
+    run_item(c, P, P->host.items[seg]);
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int nsb_plan_segment_marker(const nsb_plan* P, int64_t seg, int32_t* kind, int32_t* qubit,
+                            int32_t* step) {
+  if (!P || seg < 0 || seg >= static_cast<int64_t>(P->host.items.size()) || !kind || !qubit ||
+      !step)
+    return NSB_EINVAL;
+  const Item& it = P->host.items[seg];
+  *kind = it.kind == Item::kMeasure ? NSB_OP_MEASURE
+                                    : (it.kind == Item::kReset ? NSB_OP_RESET : NSB_OP_GATE);
+  *qubit = it.qubit;
+  *step = it.step;
+  return NSB_OK;
+}
+
+int nsb_plan_last_timing(const nsb_plan* P, double* ms, int64_t* launches) {
+  if (!P) return NSB_EINVAL;
+  if (ms) *ms = P->last_ms;
+  if (launches) *launches = P->last_launches;
+  return NSB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,449 @@
+// Host planner: turns the fused op list (engine._compile's plan, engine.py:
+// 295-363) into the blocked device program of planner.h.
+//
+//  1. resolve every 1q/2q matrix (payload or nsb::gate_matrix), classify its
+//     sparsity by exact zeros (skipping an exact zero term is bit-identical
+//     to multiplying by it), deduplicate identical payloads by hash;
+//  2. cut the op list into items: gate runs, k>=3 dense gates, MEASURE, RESET;
+//  3. schedule each gate run into passes (tile qubit sets of <= 12 qubits)
+//     with a dependency-respecting greedy look-ahead: a gate joins the open
+//     pass if it fits the tile set and no skipped earlier gate shares a
+//     qubit with it; otherwise it is deferred to a later pass;
+//  4. inside a pass, schedule stages (4-qubit register groups) the same way;
+//  5. for MMA mode, build a single pass list in which each MEASURE becomes
+//     an epilogue reduction of the preceding pass and a collapse prologue of
+//     the next one (engine.py:183-191, 164-167).
+#include "planner_host.h"
+
+#include <algorithm>
+#include <stdexcept>
+#include <unordered_map>
+
+namespace nsb {
+namespace {
+
+inline int popc(uint64_t m) { return __builtin_popcountll(m); }
+
+inline bool is_zero(const double* m, int idx) { return m[2 * idx] == 0.0 && m[2 * idx + 1] == 0.0; }
+
+// Classify a gate matrix and write its packed form; returns class.
+// Packed layouts (complex elements):
+//   kDense1: 4, kDiag1: 2, kDense2: 16, kSparse2: 8 (row r: v0, v1),
+//   kMono2: 4 (row r value), kDiag2: 4.
+uint8_t pack_matrix(const double* m, int nq, std::vector<double>& packed, uint16_t& cols) {
+  packed.clear();
+  cols = 0;
+  auto put = [&](int idx) {
+    packed.push_back(m[2 * idx]);
+    packed.push_back(m[2 * idx + 1]);
+  };
+  auto put_zero = [&]() {
+    packed.push_back(0.0);
+    packed.push_back(0.0);
+  };
+  if (nq == 1) {
+    if (is_zero(m, 1) && is_zero(m, 2)) {
+      put(0);
+      put(3);
+      return kDiag1;
+    }
+    for (int i = 0; i < 4; ++i) put(i);
+    return kDense1;
+  }
+  int max_nnz = 0;
+  bool diag = true;
+  for (int r = 0; r < 4; ++r) {
+    int nnz = 0;
+    for (int c = 0; c < 4; ++c)
+      if (!is_zero(m, r * 4 + c)) {
+        ++nnz;
+        if (c != r) diag = false;
+      }
+    max_nnz = std::max(max_nnz, nnz);
+  }
+  if (diag) {
+    for (int r = 0; r < 4; ++r) put(r * 4 + r);
+    return kDiag2;
+  }
+  if (max_nnz <= 1) {
+    for (int r = 0; r < 4; ++r) {
+      int c0 = 0;
+      bool found = false;
+      for (int c = 0; c < 4; ++c)
+        if (!is_zero(m, r * 4 + c)) {
+          c0 = c;
+          found = true;
+        }
+      if (found)
+        put(r * 4 + c0);
+      else
+        put_zero();
+      cols |= static_cast<uint16_t>(c0 << (2 * r));
+    }
+    return kMono2;
+  }
+  if (max_nnz <= 2) {
+    for (int r = 0; r < 4; ++r) {
+      int cs[2] = {0, 1}, n = 0;
+      for (int c = 0; c < 4 && n < 2; ++c)
+        if (!is_zero(m, r * 4 + c)) cs[n++] = c;
+      if (n == 1) cs[1] = cs[0] == 0 ? 1 : 0;  // second slot multiplies an exact zero
+      for (int j = 0; j < 2; ++j) {
+        if (j < n)
+          put(r * 4 + cs[j]);
+        else
+          put_zero();
+        cols |= static_cast<uint16_t>(cs[j] << (2 * (2 * r + j)));
+      }
+    }
+    return kSparse2;
+  }
+  for (int i = 0; i < 16; ++i) put(i);
+  return kDense2;
+}
+
+// matrix with its two slots exchanged (engine.swap_conjugate, engine.py:124-127)
+void swap_slots(double* m) {
+  static const int perm[4] = {0, 2, 1, 3};
+  double t[32];
+  for (int r = 0; r < 4; ++r)
+    for (int c = 0; c < 4; ++c) {
+      t[2 * (r * 4 + c)] = m[2 * (perm[r] * 4 + perm[c])];
+      t[2 * (r * 4 + c) + 1] = m[2 * (perm[r] * 4 + perm[c]) + 1];
+    }
+  std::memcpy(m, t, sizeof t);
+}
+
+// Greedy dependency-respecting packing of gates (given by qubit masks, in
+// execution order) into groups whose qubit union has at most `cap` members
+// (`base` is always in the set).  A gate joins the open group if it fits and
+// no earlier skipped gate shares a qubit with it; skipped gates keep their
+// relative order and are retried first by the next group.  Scanning stops
+// after `lookahead` gates or once nothing else can join.
+std::vector<std::vector<int>> pack_groups(const std::vector<uint64_t>& masks, int cap,
+                                          uint64_t base, uint64_t all, int lookahead,
+                                          std::vector<uint64_t>& sets) {
+  std::vector<std::vector<int>> groups;
+  std::vector<int> pending, still;
+  size_t cursor = 0;
+  const size_t total = masks.size();
+  while (!pending.empty() || cursor < total) {
+    uint64_t set = base, blocked = 0;
+    std::vector<int> grp;
+    int scanned = 0;
+    still.clear();
+    bool stop = false;
+    auto visit = [&](int g) {
+      const uint64_t m = masks[g];
+      if (!stop && !(m & blocked) && popc(set | m) <= cap) {
+        set |= m;
+        grp.push_back(g);
+      } else {
+        blocked |= m;
+        still.push_back(g);
+      }
+      ++scanned;
+      if (scanned >= lookahead || (blocked & all) == all ||
+          (popc(set) >= cap && (set & ~blocked) == 0))
+        stop = true;
+    };
+    for (int g : pending) visit(g);
+    while (!stop && cursor < total) visit(static_cast<int>(cursor++));
+    pending.swap(still);
+    if (grp.empty()) throw std::logic_error("planner made no progress");
+    groups.push_back(std::move(grp));
+    sets.push_back(set);
+  }
+  return groups;
+}
+
+// order the non-R tile positions so that lanes 0..7 of a quarter-warp hit
+// distinct 16-byte shared-memory slots under the XOR swizzle of device.cu
+uint32_t thread_perm(const int8_t rpos[4], int k) {
+  std::vector<int> free_pos;
+  for (int p = 0; p < k; ++p) {
+    bool in_r = false;
+    for (int j = 0; j < 4; ++j) in_r |= rpos[j] == p;
+    if (!in_r) free_pos.push_back(p);
+  }
+  std::vector<int> order;
+  for (int cls = 0; cls < 3; ++cls)
+    for (size_t i = 0; i < free_pos.size(); ++i)
+      if (free_pos[i] >= 0 && free_pos[i] % 3 == cls) {
+        order.push_back(free_pos[i]);
+        free_pos[i] = -1;
+        break;
+      }
+  for (int p : free_pos)
+    if (p >= 0) order.push_back(p);
+  uint32_t packed = 0;
+  for (size_t t = 0; t < order.size() && t < 8; ++t) packed |= static_cast<uint32_t>(order[t]) << (4 * t);
+  return packed;
+}
+
+}  // namespace
+
+void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
+                     const double* payloads, int n) {
+  n_qubits = n;
+  if (n < 1 || n > kMaxQubits) throw std::invalid_argument("qubit count out of range");
+  const int k = std::min(n, kTileQubits);
+  tile_qubits = k;
+  blocked = n >= kGroupQubits + 2;
+  PoolBuilder pb{matrices, {}};
+  std::vector<GateOp> run;
+  int step = 0;
+  auto flush_run = [&]() {
+    if (run.empty()) return;
+    Item it;
+    it.kind = Item::kGates;
+    it.pass_begin = static_cast<int32_t>(passes.size());
+    schedule_run(run, pb, k);
+    it.pass_end = static_cast<int32_t>(passes.size());
+    items.push_back(it);
+    run.clear();
+  };
+  for (int64_t i = 0; i < n_ops; ++i) {
+    const nsb_op& o = ops[i];
+    if (o.kind == NSB_OP_BARRIER) continue;
+    for (int j = 0; j < o.nq; ++j)
+      if (o.q[j] < 0 || o.q[j] >= n) throw std::invalid_argument("qubit out of range in plan");
+    if (o.kind == NSB_OP_MEASURE || o.kind == NSB_OP_RESET) {
+      flush_run();
+      Item it;
+      it.kind = o.kind == NSB_OP_MEASURE ? Item::kMeasure : Item::kReset;
+      it.qubit = o.q[0];
+      it.step = o.kind == NSB_OP_MEASURE ? step++ : -1;
+      items.push_back(it);
+      continue;
+    }
+    CMat mat;
+    const int dim = 1 << o.nq;
+    if (o.payload >= 0) {
+      if (!payloads) throw std::invalid_argument("payload offset without payload pool");
+      mat.dim = dim;
+      std::memcpy(mat.v, payloads + 2 * o.payload, sizeof(double) * 2 * dim * dim);
+    } else if (!gate_matrix(o.tag, o.param >= 0 ? params + o.param : nullptr,
+                            gate_n_params(o.tag), mat) || mat.dim != dim) {
+      throw std::invalid_argument("cannot resolve gate matrix");
+    }
+    ++n_gates;
+    if (o.nq >= 3 || !blocked) {
+      flush_run();
+      Item it;
+      it.kind = Item::kDense;
+      it.k = o.nq;
+      for (int j = 0; j < o.nq; ++j) it.qs[j] = o.q[j];
+      it.mat_off = static_cast<int64_t>(dense_mats.size() / 2);
+      dense_mats.insert(dense_mats.end(), mat.v, mat.v + 2 * dim * dim);
+      items.push_back(it);
+      continue;
+    }
+    GateOp g;
+    g.nq = o.nq;
+    g.q[0] = o.q[0];
+    g.q[1] = o.nq == 2 ? o.q[1] : -1;
+    g.mask = (uint64_t(1) << o.q[0]) | (o.nq == 2 ? uint64_t(1) << o.q[1] : 0);
+    std::memcpy(g.m, mat.v, sizeof(double) * 2 * dim * dim);
+    run.push_back(g);
+  }
+  flush_run();
+  n_measures = step;
+  build_mma();
+}
+
+void HostPlan::schedule_run(std::vector<GateOp>& run, PoolBuilder& pb, int k) {
+  const int n = n_qubits;
+  const uint64_t all = (n == 64) ? ~uint64_t(0) : ((uint64_t(1) << n) - 1);
+  const uint64_t low = (uint64_t(1) << std::min(kLowQubits, n)) - 1;
+  std::vector<uint64_t> masks(run.size());
+  for (size_t i = 0; i < run.size(); ++i) masks[i] = run[i].mask;
+  std::vector<uint64_t> sets;
+  auto pass_groups = pack_groups(masks, k, low, all, 1024, sets);
+  std::vector<double> packed;
+  for (size_t pi = 0; pi < pass_groups.size(); ++pi) {
+    const auto& pg = pass_groups[pi];
+    uint64_t tset = sets[pi];
+    // pad the tile set with the lowest unused qubits up to k
+    for (int q = 0; q < n && popc(tset) < k; ++q) tset |= uint64_t(1) << q;
+    PassDesc P{};
+    P.k = k;
+    P.measure_q = P.collapse_q = -1;
+    P.measure_slot = P.collapse_slot = -1;
+    int local_of[64];
+    int t = 0, o = 0;
+    for (int q = 0; q < n; ++q) {
+      if (tset >> q & 1) {
+        local_of[q] = t;
+        P.tq[t++] = static_cast<int8_t>(q);
+      } else {
+        local_of[q] = -1;
+        P.oq[o++] = static_cast<int8_t>(q);
+      }
+    }
+    // stages on tile-local masks
+    std::vector<uint64_t> lmasks(pg.size());
+    for (size_t j = 0; j < pg.size(); ++j) {
+      const GateOp& g = run[pg[j]];
+      lmasks[j] = uint64_t(1) << local_of[g.q[0]];
+      if (g.nq == 2) lmasks[j] |= uint64_t(1) << local_of[g.q[1]];
+    }
+    std::vector<uint64_t> rsets;
+    const uint64_t lall = (uint64_t(1) << k) - 1;
+    auto stage_groups = pack_groups(lmasks, kGroupQubits, 0, lall, 256, rsets);
+    P.stage_begin = static_cast<int32_t>(stages.size());
+    for (size_t si = 0; si < stage_groups.size(); ++si) {
+      uint64_t r = rsets[si];
+      for (int p = 0; p < k && popc(r) < kGroupQubits; ++p) r |= uint64_t(1) << p;
+      StageDesc S{};
+      int gbit_of[64];
+      int j = 0;
+      for (int p = 0; p < k; ++p)
+        if (r >> p & 1) {
+          gbit_of[p] = j;
+          S.rpos[j++] = static_cast<int8_t>(p);
+        }
+      S.tperm = thread_perm(S.rpos, k);
+      S.gate_begin = static_cast<int32_t>(gates.size());
+      for (int gi : stage_groups[si]) {
+        GateOp g = run[pg[gi]];
+        GateDesc d{};
+        if (g.nq == 1) {
+          d.a = static_cast<uint8_t>(gbit_of[local_of[g.q[0]]]);
+          d.b = d.a;
+        } else {
+          int a = gbit_of[local_of[g.q[0]]], b = gbit_of[local_of[g.q[1]]];
+          if (a > b) {
+            swap_slots(g.m);
+            std::swap(a, b);
+          }
+          d.a = static_cast<uint8_t>(a);
+          d.b = static_cast<uint8_t>(b);
+        }
+        d.cls = pack_matrix(g.m, g.nq, packed, d.cols);
+        d.mat = pb.add(packed.data(), static_cast<int>(packed.size() / 2));
+        class_count[d.cls]++;
+        static const int kNnz[6] = {4, 2, 16, 8, 4, 4};
+        flops += 8ll * kNnz[d.cls] * (int64_t(1) << (n - g.nq));
+        gates.push_back(d);
+      }
+      S.gate_end = static_cast<int32_t>(gates.size());
+      stages.push_back(S);
+    }
+    P.stage_end = static_cast<int32_t>(stages.size());
+    passes.push_back(P);
+  }
+}
+
+void HostPlan::build_mma() {
+  // single-launch MMA program: possible when every item is a gate run,
+  // a measure or a reset (no k>=3 dense gates) and the blocked path is on
+  mma_ok = blocked;
+  for (const Item& it : items)
+    if (it.kind == Item::kDense) mma_ok = false;
+  if (!mma_ok) return;
+  auto fresh = [&]() {
+    PassDesc P{};
+    P.k = tile_qubits;
+    P.measure_q = P.collapse_q = -1;
+    P.measure_slot = P.collapse_slot = -1;
+    P.stage_begin = P.stage_end = 0;
+    int t = 0, o = 0;
+    for (int q = 0; q < n_qubits; ++q) {
+      if (q < tile_qubits)
+        P.tq[t++] = static_cast<int8_t>(q);
+      else
+        P.oq[o++] = static_cast<int8_t>(q);
+    }
+    return P;
+  };
+  int pending_collapse_q = -1, pending_slot = -1;
+  for (const Item& it : items) {
+    if (it.kind == Item::kGates) {
+      for (int32_t p = it.pass_begin; p < it.pass_end; ++p) {
+        PassDesc P = passes[p];
+        if (pending_collapse_q >= 0) {
+          P.collapse_q = pending_collapse_q;
+          P.collapse_slot = pending_slot;
+          pending_collapse_q = -1;
+        }
+        mma_passes.push_back(P);
+      }
+    } else if (it.kind == Item::kMeasure) {
+      if (mma_passes.empty() || mma_passes.back().measure_q >= 0 || pending_collapse_q >= 0) {
+        PassDesc P = fresh();
+        if (pending_collapse_q >= 0) {
+          P.collapse_q = pending_collapse_q;
+          P.collapse_slot = pending_slot;
+          pending_collapse_q = -1;
+        }
+        mma_passes.push_back(P);
+      }
+      mma_passes.back().measure_q = it.qubit;
+      mma_passes.back().measure_slot = it.step;
+      pending_collapse_q = it.qubit;
+      pending_slot = it.step;
+    }
+    // RESET: no-op in MMA mode (engine.py:420-421)
+  }
+  if (pending_collapse_q >= 0) {
+    PassDesc P = fresh();
+    P.collapse_q = pending_collapse_q;
+    P.collapse_slot = pending_slot;
+    mma_passes.push_back(P);
+  }
+}
+
+}  // namespace nsb
+
+namespace {
+void fill_info(const nsb::HostPlan& H, nsb_plan_info* info) {
+  using nsb::Item;
+  info->n_gates = H.n_gates;
+  info->n_measures = H.n_measures;
+  int64_t resets = 0, segs = 0;
+  for (const Item& it : H.items) {
+    resets += it.kind == Item::kReset;
+    segs += it.kind == Item::kGates || it.kind == Item::kDense;
+  }
+  info->n_resets = resets;
+  info->n_segments = segs;
+  const auto& passes = H.mma_ok ? H.mma_passes : H.passes;
+  info->n_passes = static_cast<int64_t>(passes.size());
+  info->flops = H.flops;
+  info->tile_qubits = H.tile_qubits;
+  info->n_items = static_cast<int64_t>(H.items.size());
+  int64_t n_st = 0;
+  for (const nsb::PassDesc& p : passes) n_st += p.stage_end - p.stage_begin;
+  info->n_stages = n_st;
+}
+}  // namespace
+
+namespace nsb {
+void plan_info(const HostPlan& H, nsb_plan_info* info) { fill_info(H, info); }
+}  // namespace nsb
+
+extern "C" int nsb_plan_analyze(const nsb_op* ops, int64_t n_ops, const double* params,
+                                const double* payloads, int32_t n_qubits, nsb_plan_info* info,
+                                int64_t* class_counts, nsb_status* st) {
+  if (!info || (n_ops > 0 && !ops)) {
+    nsb::set_status(st, NSB_EINVAL, "null argument");
+    return NSB_EINVAL;
+  }
+  try {
+    nsb::HostPlan H;
+    H.build(ops, n_ops, params, payloads, n_qubits);
+    fill_info(H, info);
+    if (class_counts)
+      for (int c = 0; c < 6; ++c) class_counts[c] = H.class_count[c];
+  } catch (const std::bad_alloc&) {
+    nsb::set_status(st, NSB_ERESOURCE, "host out of memory in planner");
+    return NSB_ERESOURCE;
+  } catch (const std::exception& e) {
+    nsb::set_status(st, NSB_EINVAL, e.what());
+    return NSB_EINVAL;
+  }
+  nsb::set_status(st, NSB_OK, "");
+  return NSB_OK;
+}
+

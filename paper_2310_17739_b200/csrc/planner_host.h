@@ -1,0 +1,89 @@
+// Host-side plan container (see planner.cpp for the scheduling algorithm).
+#pragma once
+
+#include <cstring>
+#include <unordered_map>
+#include <vector>
+
+#include "host_common.h"
+#include "planner.h"
+
+namespace nsb {
+
+struct Key {
+  std::vector<uint64_t> bits;
+  bool operator==(const Key& o) const { return bits == o.bits; }
+};
+struct KeyHash {
+  size_t operator()(const Key& k) const {
+    uint64_t h = 1469598103934665603ull;
+    for (uint64_t b : k.bits) {
+      h ^= b;
+      h *= 1099511628211ull;
+      h ^= h >> 29;
+    }
+    return static_cast<size_t>(h);
+  }
+};
+
+struct PoolBuilder {
+  std::vector<double>& pool;
+  std::unordered_map<Key, int32_t, KeyHash> seen;
+  int32_t add(const double* v, int n_complex) {
+    Key k;
+    k.bits.resize(2 * n_complex + 1);
+    std::memcpy(k.bits.data(), v, sizeof(double) * 2 * n_complex);
+    k.bits.back() = static_cast<uint64_t>(n_complex);
+    auto it = seen.find(k);
+    if (it != seen.end()) return it->second;
+    const int32_t off = static_cast<int32_t>(pool.size() / 2);
+    pool.insert(pool.end(), v, v + 2 * n_complex);
+    seen.emplace(std::move(k), off);
+    return off;
+  }
+};
+
+struct GateOp {
+  int nq;
+  int q[2];      // global qubits, slot order
+  uint64_t mask;
+  double m[32];  // resolved matrix (slot order)
+};
+
+
+struct Item {
+  enum Kind { kGates, kDense, kMeasure, kReset } kind;
+  int32_t pass_begin = 0, pass_end = 0;  // kGates: passes[pass_begin, pass_end)
+  int32_t k = 0, qs[5] = {0, 0, 0, 0, 0};
+  int64_t mat_off = 0;                   // kDense: offset (complex) into dense_mats
+  int32_t qubit = -1, step = -1;         // kMeasure / kReset
+};
+
+struct HostPlan {
+  int n_qubits = 0;
+  int tile_qubits = 0;
+  bool blocked = false;   // blocked pass kernel (n >= 6); else per-op kernels
+  bool mma_ok = false;    // whole MMA run fits one cooperative launch
+  int64_t n_gates = 0, n_measures = 0;
+  int64_t flops = 0;
+  int64_t class_count[6] = {0, 0, 0, 0, 0, 0};
+
+  std::vector<Item> items;
+  std::vector<PassDesc> passes;      // plain gate passes (items reference ranges)
+  std::vector<PassDesc> mma_passes;  // whole-circuit MMA program
+  std::vector<StageDesc> stages;
+  std::vector<GateDesc> gates;
+  std::vector<double> matrices;      // packed, deduplicated payload pool
+  std::vector<double> dense_mats;    // k-qubit / unblocked matrices (full)
+
+  void build(const nsb_op* ops, int64_t n_ops, const double* params, const double* payloads,
+             int n);
+
+ private:
+  void schedule_run(std::vector<GateOp>& run, PoolBuilder& pb, int k);
+  void build_mma();
+};
+
+void plan_info(const HostPlan& H, nsb_plan_info* info);
+
+}  // namespace nsb
