@@ -1,0 +1,336 @@
+"""Benchmark: input gates/s of the 21-qubit deep projection-filter circuit
+(BASELINE.json `metric`, config 3, paper P9 shape) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config deep21|rand28] [--trotter R]
+
+One step = one MMA-mode execution of the whole fused circuit from |0...0>
+(every gate, all 8 mid-circuit assertions with collapse) plus the final
+probability read-out used for sampling.  The workload is generated and fused
+natively before timing (host time reported separately in `host`).
+
+value  device-resident: the fused plan is already in HBM; timed with CUDA
+       events around each cooperative kernel launch (library stream), K steps
+       after W warm-ups; L2 flushed (256 MiB write) between steps because the
+       21-qubit state (32 MiB) would otherwise stay L2-resident across steps.
+e2e    through the C ABI with host buffers: per step the packed fused op list
+       (host) is planned + uploaded, executed, and the probabilities are read
+       back (D2H) and sampled on the host -- what `run()` does per call.
+cpu_baseline / --impl reference: the oracle port of the reference engine
+       (numpy einsum, as nucsim.engine) on a bounded prefix of the same fused
+       gate stream, single-threaded, extrapolated per gate.
+
+Multi-GPU (torchrun, N > 1): replicas -- every rank runs the same circuit on
+its own GPU (no data-path collective), value = total gates / max time over
+ranks, "scaling": "weak".  State sharding across GPUs is future work
+(DESIGN.md section 7).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+METRIC = "gates/sec on 21-qubit deep circuit; achieved GB/s vs roofline at 1/2/4/8 GPUs"
+UNIT = "input gates/s"
+FP64_DFMA_PER_CLK_PER_SM = 64  # B200: 64 FP64 FMA lanes per SM per clock (spec)
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "sm_max_mhz": float(d.get("sm_max_mhz", 1965)),
+                "source": "measured"}
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback"}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def make_workload(config: str, trotter: int | None):
+    from paper_2310_17739_b200 import workloads as W
+    t0 = time.perf_counter()
+    if config == "deep21":
+        r = trotter or 18
+        wl = W.filter_workload(20, trotter=r, n_steps=8, n_scatter=8, trial="10" * 10)
+    elif config == "rand28":
+        wl = W.layered_workload(28, layers=trotter or 20)
+    else:
+        raise SystemExit(f"unknown config {config}")
+    t_gen = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    fops, pool, stats = W.fuse_packed(wl.ops, wl.params, wl.payloads)
+    t_fuse = time.perf_counter() - t0
+    exe = wl.executable(fops)
+    return wl, exe, pool, stats, {"generate_s": round(t_gen, 3), "fuse_s": round(t_fuse, 3),
+                                  "fuse_input_gates_per_s": round(wl.input_gates / t_fuse)}
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.proc = None
+        self.path = Path(f"/tmp/nsb_clocks_{os.getpid()}.csv")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        self.path.unlink(missing_ok=True)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_reference(exe, pool, params, n, input_per_fused, budget_s=12.0):
+    """Oracle port of nucsim.engine on a prefix of the fused stream."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import nucsim_oracle as O
+    from paper_2310_17739_b200 import gate_matrix
+    from paper_2310_17739_b200.gates import BY_CODE
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    a = np.zeros(1 << n, np.complex128)
+    a[0] = 1.0
+    done = 0
+    t0 = time.perf_counter()
+    for rec in exe:
+        if rec["kind"] != 0:
+            if rec["kind"] == 1:
+                p0 = O.branch_probability(a, int(rec["q"][0]), 0)
+                O.project(a, int(rec["q"][0]), 0, p0)
+            continue
+        k = int(rec["nq"])
+        if rec["payload"] >= 0:
+            off = int(rec["payload"])
+            m = pool[off:off + 4 ** k].reshape(2 ** k, 2 ** k)
+        else:
+            g = BY_CODE[int(rec["tag"])]
+            p = tuple(params[int(rec["param"]):int(rec["param"]) + g.n_params]) if g.n_params else ()
+            m = gate_matrix(g, p)
+        a = O.apply_dense(a, m, tuple(int(x) for x in rec["q"][:k]))
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": round(done * input_per_fused / dt, 3), "unit": UNIT, "cores": 1,
+            "kind": "port",
+            "sample": f"first {done} fused gates of the same workload at {n} qubits "
+                      f"({dt:.1f} s, numpy einsum single thread), scaled by input/fused "
+                      f"gate ratio {input_per_fused:.3f}"}
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    wl, exe, pool, stats, host = make_workload(args.config, args.trotter)
+    ratio = wl.input_gates / max(stats["gates_after"], 1)
+    vals = []
+    cb = None
+    for _ in range(args.steps):
+        cb = cpu_reference(exe, pool, wl.params, wl.n_qubits, ratio, budget_s=args.ref_budget)
+        vals.append(cb["value"])
+    value = float(np.mean(vals))
+    cb["value"] = value
+    cb["cores"] = 1
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": workload_name(args), "n_qubits": wl.n_qubits,
+                       "input_gates": wl.input_gates, "fused_gates": stats["gates_after"]},
+            "cpu_baseline": cb,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_name(args) -> str:
+    if args.config == "deep21":
+        return (f"deep21: 20-mode JW shell-model projection filter + ancilla (21 qubits), "
+                f"8 filter steps x {args.trotter or 18} Trotter slices (paper P9 shape), MMA mode")
+    return f"rand28: 28-qubit random layered U3 + {{CX,CZ,RZZ}} circuit, {args.trotter or 20} layers"
+
+
+def run_ours(args, rank, world, local):
+    import ctypes
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    os.environ["NUCSIM_DEVICE"] = str(local)
+    from paper_2310_17739_b200 import _native as N
+    from paper_2310_17739_b200.engine import DeviceProgram, StateVector, _sample_from
+
+    wl, exe, pool, stats, host = make_workload(args.config, args.trotter)
+    n = wl.n_qubits
+    state = StateVector(n)
+    t0 = time.perf_counter()
+    prog = DeviceProgram(state, exe, wl.params, pool)
+    host["plan_s"] = round(time.perf_counter() - t0, 3)
+    info = prog.info
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step():
+        state.restart()
+        prog.run_mma()
+        return prog.last_timing()
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        torch.cuda.synchronize()
+        step()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    ms_list, launches = [], 0
+    wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        ms, nl = step()
+        ms_list.append(ms)
+        launches += nl + 1  # + the |0...0> reset kernel
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    if world > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop()
+    dev_s = sum(ms_list) / 1e3
+    if world > 1:
+        t = torch.tensor([dev_s], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dev_s = float(t.item())
+    total_gates = wl.input_gates * args.steps * world
+    value = total_gates / dev_s
+    ms_per_step = dev_s * 1e3 / args.steps
+
+    # e2e: the C-ABI path with host buffers, one full call per step
+    probs = np.empty(1 << n, np.float64)
+    e2e_times = []
+    rng = np.random.Generator(np.random.Philox(7))
+    for _ in range(max(1, args.e2e_steps)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        state.restart()
+        p2 = DeviceProgram(state, exe, wl.params, pool)
+        p2.run_mma()
+        state.device_call("nsb_probabilities", N.ptr(probs))
+        _sample_from(probs, n, 1024, rng)
+        e2e_times.append(time.perf_counter() - t0)
+        del p2
+    e2e_s = float(np.median(e2e_times))
+    h2d = exe.nbytes + wl.params.nbytes + pool.nbytes
+    d2h = probs.nbytes + 8 * info.n_measures
+
+    # roofline of the dominant kernel (k_blocked): algorithmic bytes =
+    # passes x (read + write) x 16 B x 2^n per launch
+    pk = peaks()
+    bytes_per_launch = info.n_passes * 2 * 16 * (1 << n)
+    kernel_s = dev_s / args.steps if world == 1 else sum(ms_list) / 1e3 / args.steps
+    achieved = bytes_per_launch / kernel_s / 1e9
+    sm_mhz = clk.get("sm_mhz") or pk["sm_max_mhz"]
+    fp64_peak = 148 * FP64_DFMA_PER_CLK_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+    fp64_ach = info.flops / kernel_s / 1e12
+    profile = ROOT / "profiles" / "r01_dram_bytes.json"
+    traffic = None
+    if profile.exists():
+        traffic = json.loads(profile.read_text()).get(args.config)
+    line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic",
+            "config": {"workload": workload_name(args), "n_qubits": n,
+                       "input_gates": wl.input_gates, "fused_gates": stats["gates_after"],
+                       "fusion_reduction": round(wl.input_gates / max(stats["gates_after"], 1), 3),
+                       "passes": info.n_passes, "stages": info.n_stages,
+                       "gates_per_pass": round(info.n_gates / max(info.n_passes, 1), 2),
+                       "tile_qubits": info.tile_qubits, "parallelism": f"replicas{world}",
+                       "l2": "flushed between steps (256 MiB write); state (2^n x 16 B) "
+                             "L2-resident within a step when it fits",
+                       **{k: v for k, v in wl.meta.items() if k != "terms"}},
+            "host": host,
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
+                         "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
+                         "traffic": traffic, "peak_source": pk["source"],
+                         "note": "algorithmic bytes = passes x 32 B x 2^n per launch; the "
+                                 "21-qubit state is L2-resident inside a launch"},
+            "fp64": {"achieved_tflops": round(fp64_ach, 3), "peak_tflops": round(fp64_peak, 2),
+                     "frac": round(fp64_ach / fp64_peak, 4),
+                     "flops_per_launch": info.flops},
+            "e2e": {"value": round(wl.input_gates / e2e_s, 1), "unit": UNIT,
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "s_per_step": round(e2e_s, 4)},
+            "wall_s": round(wall, 3), "gpu_launches": launches, "clocks": clk}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ratio = wl.input_gates / max(stats["gates_after"], 1)
+        line["cpu_baseline"] = cpu_reference(exe, pool, wl.params, n, ratio, args.ref_budget)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--config", default="deep21", choices=("deep21", "rand28"))
+    ap.add_argument("--trotter", type=int, default=None)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--ref-budget", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()
