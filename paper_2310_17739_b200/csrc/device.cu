@@ -254,33 +254,49 @@ struct BlockedParams {
   double eps;
 };
 
+// Group-local index helpers: a thread's 16 registers a[0..15] hold the
+// amplitudes whose group bits (tile-local positions rpos[0..3]) spell the
+// index.  A 2q gate on group bits P < Q works on the 4 quads; member s of
+// quad qd sits at quad_base(qd) | (s&1 ? 1<<P : 0) | (s&2 ? 1<<Q : 0).
 template <int P, int Q>
-struct QuadBase {  // the 4 group indices with bits P, Q clear
-  static constexpr int other0 = (P != 0 && Q != 0) ? 0 : ((P != 1 && Q != 1) ? 1 : 2);
-  static constexpr int other1 = [] {
-    for (int b = other0 + 1; b < 4; ++b)
-      if (b != P && b != Q) return b;
-    return 3;
-  }();
-  static constexpr int at(int i) { return ((i & 1) << other0) | ((i >> 1 & 1) << other1); }
+struct Quads {
+  static constexpr int o0 = (P != 0 && Q != 0) ? 0 : ((P != 1 && Q != 1) ? 1 : 2);
+  static constexpr int o1 = (o0 + 1 != P && o0 + 1 != Q) ? o0 + 1
+                          : ((o0 + 2 != P && o0 + 2 != Q) ? o0 + 2 : o0 + 3);
+  static constexpr int base(int qd) { return ((qd & 1) << o0) | (((qd >> 1) & 1) << o1); }
+  static constexpr int at(int qd, int s) {
+    return base(qd) | ((s & 1) << P) | (((s >> 1) & 1) << Q);
+  }
 };
+
+// Register-pressure fence: an empty volatile asm that "rewrites" v, so the
+// scheduler cannot start the work that consumes v before this point; used to
+// keep quads sequential (otherwise ptxas hoists all 16 outputs for ILP and
+// spills at 128 registers).
+__device__ __forceinline__ void fence(double2& v) {
+  asm volatile("" : "+d"(v.x), "+d"(v.y));
+}
+
+// (x, y) <- [[m0, m1], [m2, m3]] (x, y)
+__device__ __forceinline__ void mix2(double2& x, double2& y, const double2 m0, const double2 m1,
+                                     const double2 m2, const double2 m3) {
+  fence(x);
+  fence(y);
+  double2 ox = make_double2(0.0, 0.0), oy = ox;
+  cmac(ox, m0, x);
+  cmac(ox, m1, y);
+  cmac(oy, m2, x);
+  cmac(oy, m3, y);
+  x = ox;
+  y = oy;
+}
 
 template <int P>
 __device__ __forceinline__ void g1_dense(double2 (&a)[16], const double2* __restrict__ m) {
   const double2 m0 = __ldg(m), m1 = __ldg(m + 1), m2 = __ldg(m + 2), m3 = __ldg(m + 3);
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    if (i & (1 << P)) continue;
-    const int j = i | (1 << P);
-    const double2 x = a[i], y = a[j];
-    double2 o0 = make_double2(0.0, 0.0), o1 = o0;
-    cmac(o0, m0, x);
-    cmac(o0, m1, y);
-    cmac(o1, m2, x);
-    cmac(o1, m3, y);
-    a[i] = o0;
-    a[j] = o1;
-  }
+  for (int i = 0; i < 16; ++i)
+    if (!(i & (1 << P))) mix2(a[i], a[i | (1 << P)], m0, m1, m2, m3);
 }
 
 template <int P>
@@ -292,11 +308,11 @@ __device__ __forceinline__ void g1_diag(double2 (&a)[16], const double2* __restr
 
 template <int P, int Q>
 __device__ __forceinline__ void g2_dense(double2 (&a)[16], const double2* __restrict__ m) {
+  using Z = Quads<P, Q>;
 #pragma unroll
   for (int qd = 0; qd < 4; ++qd) {
-    const int b = QuadBase<P, Q>::at(qd);
-    const int idx[4] = {b, b | (1 << P), b | (1 << Q), b | (1 << P) | (1 << Q)};
-    const double2 x0 = a[idx[0]], x1 = a[idx[1]], x2 = a[idx[2]], x3 = a[idx[3]];
+    const double2 x0 = a[Z::at(qd, 0)], x1 = a[Z::at(qd, 1)], x2 = a[Z::at(qd, 2)],
+                  x3 = a[Z::at(qd, 3)];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       double2 o = make_double2(0.0, 0.0);
@@ -304,8 +320,36 @@ __device__ __forceinline__ void g2_dense(double2 (&a)[16], const double2* __rest
       cmac(o, __ldg(m + 4 * r + 1), x1);
       cmac(o, __ldg(m + 4 * r + 2), x2);
       cmac(o, __ldg(m + 4 * r + 3), x3);
-      a[idx[r]] = o;
+      a[Z::at(qd, r)] = o;
     }
+  }
+}
+
+// two 2x2 blocks on fixed member pairs (S0,S1) and (S2,S3) of every quad
+template <int P, int Q, int S0, int S1, int S2, int S3>
+__device__ __forceinline__ void g2_pairs(double2 (&a)[16], const double2* __restrict__ m) {
+  using Z = Quads<P, Q>;
+  {
+    const double2 m0 = __ldg(m), m1 = __ldg(m + 1), m2 = __ldg(m + 2), m3 = __ldg(m + 3);
+#pragma unroll
+    for (int qd = 0; qd < 4; ++qd) mix2(a[Z::at(qd, S0)], a[Z::at(qd, S1)], m0, m1, m2, m3);
+  }
+  {
+    const double2 m0 = __ldg(m + 4), m1 = __ldg(m + 5), m2 = __ldg(m + 6), m3 = __ldg(m + 7);
+#pragma unroll
+    for (int qd = 0; qd < 4; ++qd) mix2(a[Z::at(qd, S2)], a[Z::at(qd, S3)], m0, m1, m2, m3);
+  }
+}
+
+// exact CX: swap members S and T of every quad (no arithmetic)
+template <int P, int Q, int S, int T>
+__device__ __forceinline__ void g2_swap(double2 (&a)[16]) {
+  using Z = Quads<P, Q>;
+#pragma unroll
+  for (int qd = 0; qd < 4; ++qd) {
+    const double2 t = a[Z::at(qd, S)];
+    a[Z::at(qd, S)] = a[Z::at(qd, T)];
+    a[Z::at(qd, T)] = t;
   }
 }
 
@@ -321,20 +365,17 @@ __device__ __forceinline__ double2 pick(const double2 x0, const double2 x1, cons
 template <int P, int Q>
 __device__ __forceinline__ void g2_sparse(double2 (&a)[16], const double2* __restrict__ m,
                                           unsigned cols) {
-  double2 v[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) v[e] = __ldg(m + e);
+  using Z = Quads<P, Q>;
 #pragma unroll
   for (int qd = 0; qd < 4; ++qd) {
-    const int b = QuadBase<P, Q>::at(qd);
-    const int idx[4] = {b, b | (1 << P), b | (1 << Q), b | (1 << P) | (1 << Q)};
-    const double2 x0 = a[idx[0]], x1 = a[idx[1]], x2 = a[idx[2]], x3 = a[idx[3]];
+    const double2 x0 = a[Z::at(qd, 0)], x1 = a[Z::at(qd, 1)], x2 = a[Z::at(qd, 2)],
+                  x3 = a[Z::at(qd, 3)];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       double2 o = make_double2(0.0, 0.0);
-      cmac(o, v[2 * r], pick(x0, x1, x2, x3, (cols >> (4 * r)) & 3));
-      cmac(o, v[2 * r + 1], pick(x0, x1, x2, x3, (cols >> (4 * r + 2)) & 3));
-      a[idx[r]] = o;
+      cmac(o, __ldg(m + 2 * r), pick(x0, x1, x2, x3, (cols >> (4 * r)) & 3));
+      cmac(o, __ldg(m + 2 * r + 1), pick(x0, x1, x2, x3, (cols >> (4 * r + 2)) & 3));
+      a[Z::at(qd, r)] = o;
     }
   }
 }
@@ -342,34 +383,41 @@ __device__ __forceinline__ void g2_sparse(double2 (&a)[16], const double2* __res
 template <int P, int Q>
 __device__ __forceinline__ void g2_mono(double2 (&a)[16], const double2* __restrict__ m,
                                         unsigned cols) {
-  const double2 v0 = __ldg(m), v1 = __ldg(m + 1), v2 = __ldg(m + 2), v3 = __ldg(m + 3);
+  using Z = Quads<P, Q>;
   const int c0 = cols & 3, c1 = (cols >> 2) & 3, c2 = (cols >> 4) & 3, c3 = (cols >> 6) & 3;
 #pragma unroll
   for (int qd = 0; qd < 4; ++qd) {
-    const int b = QuadBase<P, Q>::at(qd);
-    const int idx[4] = {b, b | (1 << P), b | (1 << Q), b | (1 << P) | (1 << Q)};
-    const double2 x0 = a[idx[0]], x1 = a[idx[1]], x2 = a[idx[2]], x3 = a[idx[3]];
-    a[idx[0]] = cmul(v0, pick(x0, x1, x2, x3, c0));
-    a[idx[1]] = cmul(v1, pick(x0, x1, x2, x3, c1));
-    a[idx[2]] = cmul(v2, pick(x0, x1, x2, x3, c2));
-    a[idx[3]] = cmul(v3, pick(x0, x1, x2, x3, c3));
+    const double2 x0 = a[Z::at(qd, 0)], x1 = a[Z::at(qd, 1)], x2 = a[Z::at(qd, 2)],
+                  x3 = a[Z::at(qd, 3)];
+    a[Z::at(qd, 0)] = cmul(__ldg(m), pick(x0, x1, x2, x3, c0));
+    a[Z::at(qd, 1)] = cmul(__ldg(m + 1), pick(x0, x1, x2, x3, c1));
+    a[Z::at(qd, 2)] = cmul(__ldg(m + 2), pick(x0, x1, x2, x3, c2));
+    a[Z::at(qd, 3)] = cmul(__ldg(m + 3), pick(x0, x1, x2, x3, c3));
   }
 }
 
 template <int P, int Q>
 __device__ __forceinline__ void g2_diag(double2 (&a)[16], const double2* __restrict__ m) {
-  const double2 d[4] = {__ldg(m), __ldg(m + 1), __ldg(m + 2), __ldg(m + 3)};
+  const double2 d0 = __ldg(m), d1 = __ldg(m + 1), d2 = __ldg(m + 2), d3 = __ldg(m + 3);
 #pragma unroll
-  for (int i = 0; i < 16; ++i) a[i] = cmul(d[((i >> P) & 1) | (((i >> Q) & 1) << 1)], a[i]);
+  for (int i = 0; i < 16; ++i) {
+    const int s = ((i >> P) & 1) | (((i >> Q) & 1) << 1);
+    a[i] = cmul(s == 0 ? d0 : (s == 1 ? d1 : (s == 2 ? d2 : d3)), a[i]);
+  }
 }
 
 template <int P, int Q>
 __device__ __forceinline__ void g2(double2 (&a)[16], const GateDesc& d, const double2* m) {
   switch (d.cls) {
-    case kDense2: g2_dense<P, Q>(a, m); break;
-    case kSparse2: g2_sparse<P, Q>(a, m, d.cols); break;
+    case kCX01: g2_swap<P, Q, 1, 3>(a); break;
+    case kCX10: g2_swap<P, Q, 2, 3>(a); break;
+    case kPairQ: g2_pairs<P, Q, 0, 2, 1, 3>(a, m); break;
+    case kPairP: g2_pairs<P, Q, 0, 1, 2, 3>(a, m); break;
+    case kPairX: g2_pairs<P, Q, 0, 3, 1, 2>(a, m); break;
+    case kDiag2: g2_diag<P, Q>(a, m); break;
     case kMono2: g2_mono<P, Q>(a, m, d.cols); break;
-    default: g2_diag<P, Q>(a, m); break;
+    case kSparse2: g2_sparse<P, Q>(a, m, d.cols); break;
+    default: g2_dense<P, Q>(a, m); break;
   }
 }
 
@@ -396,9 +444,31 @@ __device__ __forceinline__ void apply_gate(double2 (&a)[16], const GateDesc& d,
   }
 }
 
-__global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
-  extern __shared__ __align__(16) double2 tile[];
+// Gray-code order of the 16 group members: member kGray[i] differs from
+// kGray[i-1] in group bit kFlip[i], so shared-memory addresses (XOR-linear in
+// the index, swz included) are produced with one XOR per member.
+__device__ constexpr int kGray[16] = {0, 1, 3, 2, 6, 7, 5, 4, 12, 13, 15, 14, 10, 11, 9, 8};
+__device__ constexpr int kFlip[16] = {0, 0, 1, 0, 2, 0, 1, 0, 3, 0, 1, 0, 2, 0, 1, 0};
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// One CTA per SM (254 registers, no spills: the 16-amplitude register group
+// plus in-flight matrix values do not fit the 128-register budget of two
+// CTAs).  Global-memory latency is hidden by double buffering instead: while
+// the stages of tile i run, tile i+1 of the same pass streams into the other
+// shared-memory buffer with cp.async (LDGSTS).
+__global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
+  extern __shared__ __align__(128) double2 smem[];  // 2 x kTileAmps
   __shared__ PassDesc sp;
+  __shared__ uint64_t s_hi[16];  // global offset of tile-local bits 8..11 for j = 0..15
   __shared__ double red[32];
   __shared__ double s_p0;
   cg::grid_group grid = cg::this_grid();
@@ -411,40 +481,55 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
       reinterpret_cast<int*>(&sp)[tid] = reinterpret_cast<const int*>(p.passes + pi)[tid];
     __syncthreads();
     const int k = sp.k;
-    const int n_out = p.n - k;
-    const uint64_t n_tiles = uint64_t(1) << n_out;
-    const int cq = sp.collapse_q, mq = sp.measure_q;
-    const double cscale = cq >= 0 ? 1.0 / sqrt(carry_p0) : 1.0;
-
-    // tile-local -> global scatter of this thread's load/store index
-    // l = tid + 256 j  (k >= 8);  l = tid (k < 8, tid < 2^k)
+    if (tid < 16) {
+      uint64_t h = 0;
+      for (int b = 0; b < 4; ++b)
+        if ((tid >> b & 1) && 8 + b < k) h |= uint64_t(1) << sp.tq[8 + b];
+      s_hi[tid] = h;
+    }
     const int lo_bits = k < 8 ? k : 8;
-    uint64_t lo = 0;
+    uint64_t lo = 0;  // global offset of this thread's tile-local bits 0..7
     for (int b = 0; b < lo_bits; ++b)
       if (tid >> b & 1) lo |= uint64_t(1) << sp.tq[b];
-    uint64_t hbit[4] = {0, 0, 0, 0};
-    for (int b = 0; b < 4; ++b)
-      if (8 + b < k) hbit[b] = uint64_t(1) << sp.tq[8 + b];
+    __syncthreads();
+    const int n_out = p.n - k;
+    const uint64_t n_tiles = uint64_t(1) << n_out;
     const int n_j = k > 8 ? 1 << (k - 8) : 1;
     const bool loader = tid < (1 << lo_bits);
-
-    // stage-invariant thread role
-    const int n_group_threads = 1 << (k - kGroupQubits);
+    const bool grouper = tid < (1 << (k - kGroupQubits));
+    const double cscale = sp.collapse_q >= 0 ? 1.0 / sqrt(carry_p0) : 1.0;
     double msum = 0.0;
 
-    for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-      uint64_t base = 0;
+    auto tile_base = [&](uint64_t t) {
+      uint64_t base = lo;
       for (int b = 0; b < n_out; ++b)
         if (t >> b & 1) base |= uint64_t(1) << sp.oq[b];
-      // global -> shared (+ collapse prologue)
-      if (loader) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          if (j >= n_j) break;
-          const uint64_t g = base | lo | ((j & 1) ? hbit[0] : 0) | ((j & 2) ? hbit[1] : 0) |
-                             ((j & 4) ? hbit[2] : 0) | ((j & 8) ? hbit[3] : 0);
-          double2 v = p.amps[g];
-          if (cq >= 0) {
+      return base;
+    };
+    auto issue_load = [&](uint64_t t, double2* buf) {
+      if (!loader) return;
+      const uint64_t base = tile_base(t);
+      for (int j = 0; j < n_j; ++j) cp_async16(buf + swz(tid + (j << 8)), p.amps + (base | s_hi[j]));
+    };
+
+    uint64_t t = blockIdx.x;
+    int cur = 0;
+    if (t < n_tiles) issue_load(t, smem);
+    cp_async_commit();
+    for (; t < n_tiles; t += gridDim.x, cur ^= 1) {
+      double2* tile = smem + cur * kTileAmps;
+      const uint64_t t_next = t + gridDim.x;
+      if (t_next < n_tiles) issue_load(t_next, smem + (cur ^ 1) * kTileAmps);
+      cp_async_commit();
+      cp_async_wait<1>();  // this tile's group has landed (next may be in flight)
+      __syncthreads();
+      const uint64_t base = tile_base(t);
+      if (sp.collapse_q >= 0) {  // pending collapse (engine.py:164-167)
+        const int cq = sp.collapse_q;
+        if (loader)
+          for (int j = 0; j < n_j; ++j) {
+            const uint64_t g = base | s_hi[j];
+            double2& v = tile[swz(tid + (j << 8))];
             if ((g >> cq) & 1) {
               v = make_double2(0.0, 0.0);
             } else {
@@ -452,43 +537,43 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
               v.y *= cscale;
             }
           }
-          tile[swz(tid + (j << 8))] = v;
-        }
+        __syncthreads();
       }
-      __syncthreads();
       // stages: shared -> registers -> gates -> shared
       for (int s = sp.stage_begin; s < sp.stage_end; ++s) {
-        const StageDesc S = p.stages[s];
-        if (tid < n_group_threads) {
+        if (grouper) {
+          const StageDesc S = p.stages[s];
           int tb = 0;
           for (int b = 0; b < k - kGroupQubits; ++b)
             if (tid >> b & 1) tb |= 1 << ((S.tperm >> (4 * b)) & 15);
-          const int r0 = 1 << S.rpos[0], r1 = 1 << S.rpos[1], r2 = 1 << S.rpos[2],
-                    r3 = 1 << S.rpos[3];
-          int addr[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            addr[i] = swz(tb | ((i & 1) ? r0 : 0) | ((i & 2) ? r1 : 0) | ((i & 4) ? r2 : 0) |
-                          ((i & 8) ? r3 : 0));
+          const int x0 = swz(1 << S.rpos[0]), x1 = swz(1 << S.rpos[1]),
+                    x2 = swz(1 << S.rpos[2]), x3 = swz(1 << S.rpos[3]);
           double2 a[16];
+          int addr = swz(tb);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) a[i] = tile[addr[i]];
+          for (int i = 0; i < 16; ++i) {
+            if (i) addr ^= kFlip[i] == 0 ? x0 : (kFlip[i] == 1 ? x1 : (kFlip[i] == 2 ? x2 : x3));
+            a[kGray[i]] = tile[addr];
+          }
           for (int g = S.gate_begin; g < S.gate_end; ++g) {
             const GateDesc d = p.gates[g];
             apply_gate(a, d, p.mats);
           }
+          addr = swz(tb);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) tile[addr[i]] = a[i];
+          for (int i = 0; i < 16; ++i) {
+            if (i) addr ^= kFlip[i] == 0 ? x0 : (kFlip[i] == 1 ? x1 : (kFlip[i] == 2 ? x2 : x3));
+            tile[addr] = a[kGray[i]];
+          }
         }
         __syncthreads();
       }
       // shared -> global (+ assertion epilogue partial sums)
       if (loader) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          if (j >= n_j) break;
-          const uint64_t g = base | lo | ((j & 1) ? hbit[0] : 0) | ((j & 2) ? hbit[1] : 0) |
-                             ((j & 4) ? hbit[2] : 0) | ((j & 8) ? hbit[3] : 0);
+        const int mq = sp.measure_q;
+#pragma unroll 4
+        for (int j = 0; j < n_j; ++j) {
+          const uint64_t g = base | s_hi[j];
           const double2 v = tile[swz(tid + (j << 8))];
           p.amps[g] = v;
           if (mq >= 0 && !((g >> mq) & 1)) {
@@ -497,17 +582,20 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
           }
         }
       }
-      __syncthreads();
+      __syncthreads();  // buffer `cur` is free for the load issued next iteration
     }
+    cp_async_wait<0>();
+    const int mq = sp.measure_q;
+    const int mslot = sp.measure_slot;
     if (mq >= 0) {
       const double bs = block_sum(msum, red);
-      if (tid == 0) p.partials[(sp.measure_slot & 1) * gridDim.x + blockIdx.x] = bs;
+      if (tid == 0) p.partials[(mslot & 1) * gridDim.x + blockIdx.x] = bs;
     }
     __threadfence();
     grid.sync();
     if (mq >= 0) {
       if (tid < 32) {
-        const double* part = p.partials + (sp.measure_slot & 1) * gridDim.x;
+        const double* part = p.partials + (mslot & 1) * gridDim.x;
         double s = 0.0;
         for (int i = tid; i < int(gridDim.x); i += 32) s += part[i];
 #pragma unroll
@@ -517,10 +605,10 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
       __syncthreads();
       carry_p0 = s_p0;
       if (blockIdx.x == 0 && tid == 0) {
-        p.record[sp.measure_slot] = carry_p0;
+        p.record[mslot] = carry_p0;
         if (carry_p0 < p.eps) {
           p.fail[0] = 1;
-          p.fail[1] = sp.measure_slot;
+          p.fail[1] = mslot;
         }
       }
       if (carry_p0 < p.eps) return;  // every block saw the same p0
@@ -734,7 +822,7 @@ void launch_blocked(nsb_ctx* c, nsb_plan* P, const PassDesc* passes, int pb, int
   void* args[] = {&bp};
   NSB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::k_blocked),
                                        dim3(c->blocked_grid), dim3(kPassThreads), args,
-                                       sizeof(double2) * kTileAmps, c->stream));
+                                       2 * sizeof(double2) * kTileAmps, c->stream));
   P->last_launches += 1;
 }
 
@@ -773,7 +861,7 @@ int nsb_ctx_create(int32_t device, nsb_ctx** out, nsb_status* st) {
     NSB_CUDA(cudaEventCreate(&ctx->ev0));
     NSB_CUDA(cudaEventCreate(&ctx->ev1));
     NSB_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
-    const int smem = sizeof(double2) * kTileAmps;
+    const int smem = 2 * sizeof(double2) * kTileAmps;
     NSB_CUDA(cudaFuncSetAttribute(dev::k_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   smem));
     int per_sm = 0;

@@ -27,9 +27,8 @@ inline int popc(uint64_t m) { return __builtin_popcountll(m); }
 inline bool is_zero(const double* m, int idx) { return m[2 * idx] == 0.0 && m[2 * idx + 1] == 0.0; }
 
 // Classify a gate matrix and write its packed form; returns class.
-// Packed layouts (complex elements):
-//   kDense1: 4, kDiag1: 2, kDense2: 16, kSparse2: 8 (row r: v0, v1),
-//   kMono2: 4 (row r value), kDiag2: 4.
+// Packed layouts (complex elements) are listed with GateClass in planner.h;
+// kPair* store the two 2x2 blocks row-major, block 0 first.
 uint8_t pack_matrix(const double* m, int nq, std::vector<double>& packed, uint16_t& cols) {
   packed.clear();
   cols = 0;
@@ -50,27 +49,65 @@ uint8_t pack_matrix(const double* m, int nq, std::vector<double>& packed, uint16
     for (int i = 0; i < 4; ++i) put(i);
     return kDense1;
   }
+  bool nz[4][4];
   int max_nnz = 0;
   bool diag = true;
   for (int r = 0; r < 4; ++r) {
     int nnz = 0;
-    for (int c = 0; c < 4; ++c)
-      if (!is_zero(m, r * 4 + c)) {
+    for (int c = 0; c < 4; ++c) {
+      nz[r][c] = !is_zero(m, r * 4 + c);
+      if (nz[r][c]) {
         ++nnz;
         if (c != r) diag = false;
       }
+    }
     max_nnz = std::max(max_nnz, nnz);
   }
   if (diag) {
     for (int r = 0; r < 4; ++r) put(r * 4 + r);
     return kDiag2;
   }
+  auto is_one = [&](int idx) { return m[2 * idx] == 1.0 && m[2 * idx + 1] == 0.0; };
+  auto exact_perm = [&](const int* sigma) {
+    for (int r = 0; r < 4; ++r)
+      for (int c = 0; c < 4; ++c)
+        if (c == sigma[r] ? !is_one(r * 4 + c) : nz[r][c]) return false;
+    return true;
+  };
+  static const int kCxA[4] = {0, 3, 2, 1}, kCxB[4] = {0, 1, 3, 2};
+  if (exact_perm(kCxA)) return kCX01;
+  if (exact_perm(kCxB)) return kCX10;
+  // two independent 2x2 blocks on fixed index pairs
+  struct PairPattern {
+    uint8_t cls;
+    int pair[2][2];
+  };
+  static const PairPattern kPairs[3] = {{kPairQ, {{0, 2}, {1, 3}}},
+                                        {kPairP, {{0, 1}, {2, 3}}},
+                                        {kPairX, {{0, 3}, {1, 2}}}};
+  for (const PairPattern& pp : kPairs) {
+    bool fits = true;
+    for (int r = 0; r < 4 && fits; ++r) {
+      const int* blk = (pp.pair[0][0] == r || pp.pair[0][1] == r) ? pp.pair[0] : pp.pair[1];
+      for (int c = 0; c < 4; ++c)
+        if (nz[r][c] && c != blk[0] && c != blk[1]) fits = false;
+    }
+    if (!fits) continue;
+    for (int b = 0; b < 2; ++b) {
+      const int x = pp.pair[b][0], y = pp.pair[b][1];
+      put(x * 4 + x);
+      put(x * 4 + y);
+      put(y * 4 + x);
+      put(y * 4 + y);
+    }
+    return pp.cls;
+  }
   if (max_nnz <= 1) {
     for (int r = 0; r < 4; ++r) {
       int c0 = 0;
       bool found = false;
       for (int c = 0; c < 4; ++c)
-        if (!is_zero(m, r * 4 + c)) {
+        if (nz[r][c]) {
           c0 = c;
           found = true;
         }
@@ -86,7 +123,7 @@ uint8_t pack_matrix(const double* m, int nq, std::vector<double>& packed, uint16
     for (int r = 0; r < 4; ++r) {
       int cs[2] = {0, 1}, n = 0;
       for (int c = 0; c < 4 && n < 2; ++c)
-        if (!is_zero(m, r * 4 + c)) cs[n++] = c;
+        if (nz[r][c]) cs[n++] = c;
       if (n == 1) cs[1] = cs[0] == 0 ? 1 : 0;  // second slot multiplies an exact zero
       for (int j = 0; j < 2; ++j) {
         if (j < n)
@@ -323,7 +360,7 @@ void HostPlan::schedule_run(std::vector<GateOp>& run, PoolBuilder& pb, int k) {
         d.cls = pack_matrix(g.m, g.nq, packed, d.cols);
         d.mat = pb.add(packed.data(), static_cast<int>(packed.size() / 2));
         class_count[d.cls]++;
-        static const int kNnz[6] = {4, 2, 16, 8, 4, 4};
+        static const int kNnz[kNumClasses] = {4, 2, 16, 8, 4, 4, 0, 0, 8, 8, 8};
         flops += 8ll * kNnz[d.cls] * (int64_t(1) << (n - g.nq));
         gates.push_back(d);
       }
@@ -435,7 +472,7 @@ extern "C" int nsb_plan_analyze(const nsb_op* ops, int64_t n_ops, const double* 
     H.build(ops, n_ops, params, payloads, n_qubits);
     fill_info(H, info);
     if (class_counts)
-      for (int c = 0; c < 6; ++c) class_counts[c] = H.class_count[c];
+      for (int c = 0; c < nsb::kNumClasses; ++c) class_counts[c] = H.class_count[c];
   } catch (const std::bad_alloc&) {
     nsb::set_status(st, NSB_ERESOURCE, "host out of memory in planner");
     return NSB_ERESOURCE;

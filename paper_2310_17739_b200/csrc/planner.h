@@ -28,13 +28,21 @@ constexpr int kPassThreads = kTileAmps / kGroupAmps;  // 256
 constexpr int kLowQubits = 3;                    // always-tiled qubits 0..2 (128 B runs)
 constexpr int kMaxQubits = 40;
 
+// Payload classes, chosen by exact-zero structure (skipping an exact zero
+// term is bit-identical to multiplying by it).  Ordered cheapest first.
 enum GateClass : uint8_t {
-  kDense1 = 0,    // 2x2
-  kDiag1 = 1,     // 2x2 diagonal
-  kDense2 = 2,    // 4x4 dense
-  kSparse2 = 3,   // 4x4, <= 2 nonzeros per row
-  kMono2 = 4,     // 4x4, <= 1 nonzero per row
-  kDiag2 = 5,     // 4x4 diagonal
+  kDense1 = 0,    // 2x2                                  (4 complex values)
+  kDiag1 = 1,     // 2x2 diagonal                         (2)
+  kDense2 = 2,    // 4x4 dense                            (16)
+  kSparse2 = 3,   // 4x4, <= 2 nonzeros per row, any cols (8 + column codes)
+  kMono2 = 4,     // 4x4, <= 1 nonzero per row            (4 + column codes)
+  kDiag2 = 5,     // 4x4 diagonal                         (4)
+  kCX01 = 6,      // exact CX, slot 0 controls slot 1: swaps |01>,|11>  (0)
+  kCX10 = 7,      // exact CX, slot 1 controls slot 0: swaps |10>,|11>  (0)
+  kPairQ = 8,     // 2x2 on slot 1 selected by slot 0: (0,2) and (1,3)  (8)
+  kPairP = 9,     // 2x2 on slot 0 selected by slot 1: (0,1) and (2,3)  (8)
+  kPairX = 10,    // 2x2 on the anti-diagonal pairs (0,3) and (1,2)     (8)
+  kNumClasses = 11
 };
 
 struct GateDesc {     // 16 bytes

@@ -66,7 +66,7 @@ struct HostPlan {
   bool mma_ok = false;    // whole MMA run fits one cooperative launch
   int64_t n_gates = 0, n_measures = 0;
   int64_t flops = 0;
-  int64_t class_count[6] = {0, 0, 0, 0, 0, 0};
+  int64_t class_count[kNumClasses] = {};
 
   std::vector<Item> items;
   std::vector<PassDesc> passes;      // plain gate passes (items reference ranges)

@@ -224,15 +224,18 @@ def layered_workload(n: int, layers: int, seed: int = 28) -> Workload:
                     np.zeros(1, np.complex128), i, {"layers": layers})
 
 
+CLASS_NAMES = ("dense1", "diag1", "dense2", "sparse2", "mono2", "diag2", "cx01", "cx10",
+               "pair_q", "pair_p", "pair_x")
+
+
 def plan_analyze(ops: np.ndarray, params: np.ndarray, payloads: np.ndarray, n: int) -> dict:
     """Host-only planner dry run (nsb_plan_analyze)."""
     info = N.PlanInfo()
-    classes = np.zeros(6, np.int64)
+    classes = np.zeros(len(CLASS_NAMES), np.int64)
     st = N.Status()
     N.check(N.lib().nsb_plan_analyze(N.ptr(ops), len(ops), N.ptr(params),
                                      N.ptr(payloads.view(np.float64)), n, ctypes.byref(info),
                                      N.ptr(classes), ctypes.byref(st)), st)
     out = {k: int(getattr(info, k)) for k, _ in N.PlanInfo._fields_}
-    out["classes"] = dict(zip(("dense1", "diag1", "dense2", "sparse2", "mono2", "diag2"),
-                              map(int, classes)))
+    out["classes"] = dict(zip(CLASS_NAMES, map(int, classes)))
     return out
