@@ -285,7 +285,10 @@ def run_ours(args, rank, world, local):
             "config": {"workload": workload_name(args), "n_qubits": n,
                        "input_gates": wl.input_gates, "fused_gates": stats["gates_after"],
                        "fusion_reduction": round(wl.input_gates / max(stats["gates_after"], 1), 3),
-                       "passes": info.n_passes, "stages": info.n_stages,
+                       "passes": info.n_passes,
+                       "device_gate_sweeps": info.n_device_gates,
+                       "frame_absorbed_gates": info.n_frame_gates,
+                       "frame_flush_gates": info.n_flush_gates,
                        "gates_per_pass": round(info.n_gates / max(info.n_passes, 1), 2),
                        "tile_qubits": info.tile_qubits, "parallelism": f"replicas{world}",
                        "l2": "flushed between steps (256 MiB write); state (2^n x 16 B) "

@@ -171,7 +171,9 @@ typedef struct nsb_plan_info {
   int64_t flops;        /* FP64 flops of all gate ops (8 * nnz * 2^(n-k)) */
   int64_t tile_qubits;  /* qubits per cache-blocked tile */
   int64_t n_items;      /* gate segments + markers (nsb_plan_segment_marker) */
-  int64_t n_stages;     /* shared-memory round trips over all passes */
+  int64_t n_frame_gates; /* exact CX/SWAP absorbed by the relabeling frame */
+  int64_t n_flush_gates; /* physical CX emitted to flush the frame */
+  int64_t n_device_gates;/* gate sweeps executed on the device per run */
 } nsb_plan_info;
 
 /* ops: the executable part of the circuit (sampling block already removed,
@@ -184,8 +186,8 @@ void nsb_plan_destroy(nsb_plan* plan);
  * nsb_plan_create would upload, summarised.  class_counts (NSB_N_CLASSES
  * entries, may be NULL) receives the gate count per payload class: dense 1q,
  * diagonal 1q, dense 2q, <=2 nnz/row 2q, monomial 2q, diagonal 2q, exact CX
- * (two orientations), two-block 2x2 patterns (three pairings). */
-#define NSB_N_CLASSES 11
+ * (two orientations), two-block 2x2 patterns (three pairings), exact SWAP. */
+#define NSB_N_CLASSES 12
 int nsb_plan_analyze(const nsb_op* ops, int64_t n_ops, const double* params,
                      const double* payloads, int32_t n_qubits, nsb_plan_info* info,
                      int64_t* class_counts, nsb_status* st);

@@ -48,7 +48,8 @@ class PlanInfo(ctypes.Structure):
                 ("n_resets", ctypes.c_int64), ("n_passes", ctypes.c_int64),
                 ("n_segments", ctypes.c_int64), ("flops", ctypes.c_int64),
                 ("tile_qubits", ctypes.c_int64), ("n_items", ctypes.c_int64),
-                ("n_stages", ctypes.c_int64)]
+                ("n_frame_gates", ctypes.c_int64), ("n_flush_gates", ctypes.c_int64),
+                ("n_device_gates", ctypes.c_int64)]
 
 
 _P = ctypes.c_void_p

@@ -245,7 +245,6 @@ struct BlockedParams {
   int n;
   const PassDesc* passes;
   int pass_begin, pass_end;
-  const StageDesc* stages;
   const GateDesc* gates;
   const double2* mats;
   double* partials;  // 2 * gridDim
@@ -254,34 +253,21 @@ struct BlockedParams {
   double eps;
 };
 
-// Group-local index helpers: a thread's 16 registers a[0..15] hold the
-// amplitudes whose group bits (tile-local positions rpos[0..3]) spell the
-// index.  A 2q gate on group bits P < Q works on the 4 quads; member s of
-// quad qd sits at quad_base(qd) | (s&1 ? 1<<P : 0) | (s&2 ? 1<<Q : 0).
-template <int P, int Q>
-struct Quads {
-  static constexpr int o0 = (P != 0 && Q != 0) ? 0 : ((P != 1 && Q != 1) ? 1 : 2);
-  static constexpr int o1 = (o0 + 1 != P && o0 + 1 != Q) ? o0 + 1
-                          : ((o0 + 2 != P && o0 + 2 != Q) ? o0 + 2 : o0 + 3);
-  static constexpr int base(int qd) { return ((qd & 1) << o0) | (((qd >> 1) & 1) << o1); }
-  static constexpr int at(int qd, int s) {
-    return base(qd) | ((s & 1) << P) | (((s >> 1) & 1) << Q);
-  }
-};
+// ---- gate sweeps over a shared-memory tile --------------------------------
+// A 2q gate with tile-local XOR masks (ma, mb) acts on the quads
+// {v, v^ma, v^mb, v^ma^mb}; quad representatives are the indices with both
+// pivot bits clear, enumerated by inserting zeros at plo < phi into the quad
+// number.  Member s of a quad (s = bit(slot0) + 2 bit(slot1), the reference's
+// matrix index) lives at swz(base) ^ (s&1 ? swz(ma) : 0) ^ (s&2 ? swz(mb) : 0)
+// because the swizzle is linear over XOR.  1q gates use pairs {v, v^ma}.
 
-// Register-pressure fence: an empty volatile asm that "rewrites" v, so the
-// scheduler cannot start the work that consumes v before this point; used to
-// keep quads sequential (otherwise ptxas hoists all 16 outputs for ILP and
-// spills at 128 registers).
-__device__ __forceinline__ void fence(double2& v) {
-  asm volatile("" : "+d"(v.x), "+d"(v.y));
+__device__ __forceinline__ int ins0(int j, int pos) {
+  return ((j >> pos) << (pos + 1)) | (j & ((1 << pos) - 1));
 }
 
 // (x, y) <- [[m0, m1], [m2, m3]] (x, y)
 __device__ __forceinline__ void mix2(double2& x, double2& y, const double2 m0, const double2 m1,
                                      const double2 m2, const double2 m3) {
-  fence(x);
-  fence(y);
   double2 ox = make_double2(0.0, 0.0), oy = ox;
   cmac(ox, m0, x);
   cmac(ox, m1, y);
@@ -289,68 +275,6 @@ __device__ __forceinline__ void mix2(double2& x, double2& y, const double2 m0, c
   cmac(oy, m3, y);
   x = ox;
   y = oy;
-}
-
-template <int P>
-__device__ __forceinline__ void g1_dense(double2 (&a)[16], const double2* __restrict__ m) {
-  const double2 m0 = __ldg(m), m1 = __ldg(m + 1), m2 = __ldg(m + 2), m3 = __ldg(m + 3);
-#pragma unroll
-  for (int i = 0; i < 16; ++i)
-    if (!(i & (1 << P))) mix2(a[i], a[i | (1 << P)], m0, m1, m2, m3);
-}
-
-template <int P>
-__device__ __forceinline__ void g1_diag(double2 (&a)[16], const double2* __restrict__ m) {
-  const double2 d0 = __ldg(m), d1 = __ldg(m + 1);
-#pragma unroll
-  for (int i = 0; i < 16; ++i) a[i] = cmul((i & (1 << P)) ? d1 : d0, a[i]);
-}
-
-template <int P, int Q>
-__device__ __forceinline__ void g2_dense(double2 (&a)[16], const double2* __restrict__ m) {
-  using Z = Quads<P, Q>;
-#pragma unroll
-  for (int qd = 0; qd < 4; ++qd) {
-    const double2 x0 = a[Z::at(qd, 0)], x1 = a[Z::at(qd, 1)], x2 = a[Z::at(qd, 2)],
-                  x3 = a[Z::at(qd, 3)];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      double2 o = make_double2(0.0, 0.0);
-      cmac(o, __ldg(m + 4 * r + 0), x0);
-      cmac(o, __ldg(m + 4 * r + 1), x1);
-      cmac(o, __ldg(m + 4 * r + 2), x2);
-      cmac(o, __ldg(m + 4 * r + 3), x3);
-      a[Z::at(qd, r)] = o;
-    }
-  }
-}
-
-// two 2x2 blocks on fixed member pairs (S0,S1) and (S2,S3) of every quad
-template <int P, int Q, int S0, int S1, int S2, int S3>
-__device__ __forceinline__ void g2_pairs(double2 (&a)[16], const double2* __restrict__ m) {
-  using Z = Quads<P, Q>;
-  {
-    const double2 m0 = __ldg(m), m1 = __ldg(m + 1), m2 = __ldg(m + 2), m3 = __ldg(m + 3);
-#pragma unroll
-    for (int qd = 0; qd < 4; ++qd) mix2(a[Z::at(qd, S0)], a[Z::at(qd, S1)], m0, m1, m2, m3);
-  }
-  {
-    const double2 m0 = __ldg(m + 4), m1 = __ldg(m + 5), m2 = __ldg(m + 6), m3 = __ldg(m + 7);
-#pragma unroll
-    for (int qd = 0; qd < 4; ++qd) mix2(a[Z::at(qd, S2)], a[Z::at(qd, S3)], m0, m1, m2, m3);
-  }
-}
-
-// exact CX: swap members S and T of every quad (no arithmetic)
-template <int P, int Q, int S, int T>
-__device__ __forceinline__ void g2_swap(double2 (&a)[16]) {
-  using Z = Quads<P, Q>;
-#pragma unroll
-  for (int qd = 0; qd < 4; ++qd) {
-    const double2 t = a[Z::at(qd, S)];
-    a[Z::at(qd, S)] = a[Z::at(qd, T)];
-    a[Z::at(qd, T)] = t;
-  }
 }
 
 __device__ __forceinline__ double2 pick(const double2 x0, const double2 x1, const double2 x2,
@@ -362,93 +286,151 @@ __device__ __forceinline__ double2 pick(const double2 x0, const double2 x1, cons
   return r;
 }
 
-template <int P, int Q>
-__device__ __forceinline__ void g2_sparse(double2 (&a)[16], const double2* __restrict__ m,
-                                          unsigned cols) {
-  using Z = Quads<P, Q>;
-#pragma unroll
-  for (int qd = 0; qd < 4; ++qd) {
-    const double2 x0 = a[Z::at(qd, 0)], x1 = a[Z::at(qd, 1)], x2 = a[Z::at(qd, 2)],
-                  x3 = a[Z::at(qd, 3)];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      double2 o = make_double2(0.0, 0.0);
-      cmac(o, __ldg(m + 2 * r), pick(x0, x1, x2, x3, (cols >> (4 * r)) & 3));
-      cmac(o, __ldg(m + 2 * r + 1), pick(x0, x1, x2, x3, (cols >> (4 * r + 2)) & 3));
-      a[Z::at(qd, r)] = o;
-    }
+struct Sweep {
+  double2* tile;
+  int n_items;  // quads (2q) or pairs (1q) in the tile
+  int plo, phi;
+  int sa, sb;   // swizzled masks
+};
+
+template <class F>
+__device__ __forceinline__ void for_quads(const Sweep& w, F f) {
+  for (int j = threadIdx.x; j < w.n_items; j += kPassThreads) {
+    const int a0 = swz(ins0(ins0(j, w.plo), w.phi));
+    f(a0, a0 ^ w.sa, a0 ^ w.sb, a0 ^ w.sa ^ w.sb);
   }
 }
 
-template <int P, int Q>
-__device__ __forceinline__ void g2_mono(double2 (&a)[16], const double2* __restrict__ m,
-                                        unsigned cols) {
-  using Z = Quads<P, Q>;
-  const int c0 = cols & 3, c1 = (cols >> 2) & 3, c2 = (cols >> 4) & 3, c3 = (cols >> 6) & 3;
-#pragma unroll
-  for (int qd = 0; qd < 4; ++qd) {
-    const double2 x0 = a[Z::at(qd, 0)], x1 = a[Z::at(qd, 1)], x2 = a[Z::at(qd, 2)],
-                  x3 = a[Z::at(qd, 3)];
-    a[Z::at(qd, 0)] = cmul(__ldg(m), pick(x0, x1, x2, x3, c0));
-    a[Z::at(qd, 1)] = cmul(__ldg(m + 1), pick(x0, x1, x2, x3, c1));
-    a[Z::at(qd, 2)] = cmul(__ldg(m + 2), pick(x0, x1, x2, x3, c2));
-    a[Z::at(qd, 3)] = cmul(__ldg(m + 3), pick(x0, x1, x2, x3, c3));
+template <class F>
+__device__ __forceinline__ void for_pairs(const Sweep& w, F f) {
+  for (int j = threadIdx.x; j < w.n_items; j += kPassThreads) {
+    const int a0 = swz(ins0(j, w.plo));
+    f(a0, a0 ^ w.sa);
   }
 }
 
-template <int P, int Q>
-__device__ __forceinline__ void g2_diag(double2 (&a)[16], const double2* __restrict__ m) {
-  const double2 d0 = __ldg(m), d1 = __ldg(m + 1), d2 = __ldg(m + 2), d3 = __ldg(m + 3);
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int s = ((i >> P) & 1) | (((i >> Q) & 1) << 1);
-    a[i] = cmul(s == 0 ? d0 : (s == 1 ? d1 : (s == 2 ? d2 : d3)), a[i]);
-  }
-}
-
-template <int P, int Q>
-__device__ __forceinline__ void g2(double2 (&a)[16], const GateDesc& d, const double2* m) {
-  switch (d.cls) {
-    case kCX01: g2_swap<P, Q, 1, 3>(a); break;
-    case kCX10: g2_swap<P, Q, 2, 3>(a); break;
-    case kPairQ: g2_pairs<P, Q, 0, 2, 1, 3>(a, m); break;
-    case kPairP: g2_pairs<P, Q, 0, 1, 2, 3>(a, m); break;
-    case kPairX: g2_pairs<P, Q, 0, 3, 1, 2>(a, m); break;
-    case kDiag2: g2_diag<P, Q>(a, m); break;
-    case kMono2: g2_mono<P, Q>(a, m, d.cols); break;
-    case kSparse2: g2_sparse<P, Q>(a, m, d.cols); break;
-    default: g2_dense<P, Q>(a, m); break;
-  }
-}
-
-__device__ __forceinline__ void apply_gate(double2 (&a)[16], const GateDesc& d,
-                                           const double2* __restrict__ mats) {
-  const double2* m = mats + d.mat;
-  if (d.cls <= kDiag1) {
-    const bool diag = d.cls == kDiag1;
-    switch (d.a) {
-      case 0: diag ? g1_diag<0>(a, m) : g1_dense<0>(a, m); break;
-      case 1: diag ? g1_diag<1>(a, m) : g1_dense<1>(a, m); break;
-      case 2: diag ? g1_diag<2>(a, m) : g1_dense<2>(a, m); break;
-      default: diag ? g1_diag<3>(a, m) : g1_dense<3>(a, m); break;
+__device__ __forceinline__ void apply_gate(double2* __restrict__ tile, int k, const GateDesc& d,
+                                           const double2* __restrict__ m) {
+  Sweep w;
+  w.tile = tile;
+  w.plo = d.plo;
+  w.phi = d.phi;
+  w.sa = swz(d.ma);
+  w.sb = swz(d.mb);
+  if (d.nq == 1) {
+    w.n_items = 1 << (k - 1);
+    if (d.cls == kDiag1) {
+      const double2 d0 = __ldg(m), d1 = __ldg(m + 1);
+      for_pairs(w, [&](int i0, int i1) {
+        tile[i0] = cmul(d0, tile[i0]);
+        tile[i1] = cmul(d1, tile[i1]);
+      });
+    } else {
+      const double2 m0 = __ldg(m), m1 = __ldg(m + 1), m2 = __ldg(m + 2), m3 = __ldg(m + 3);
+      for_pairs(w, [&](int i0, int i1) {
+        double2 x = tile[i0], y = tile[i1];
+        mix2(x, y, m0, m1, m2, m3);
+        tile[i0] = x;
+        tile[i1] = y;
+      });
     }
     return;
   }
-  switch (d.a * 4 + d.b) {
-    case 1: g2<0, 1>(a, d, m); break;
-    case 2: g2<0, 2>(a, d, m); break;
-    case 3: g2<0, 3>(a, d, m); break;
-    case 6: g2<1, 2>(a, d, m); break;
-    case 7: g2<1, 3>(a, d, m); break;
-    default: g2<2, 3>(a, d, m); break;
+  w.n_items = 1 << (k - 2);
+  switch (d.cls) {
+    case kCX01:
+    case kCX10:
+    case kSwap: {
+      const int s = d.cls == kCX01 ? 1 : 2, t = d.cls == kSwap ? 2 : 3;
+      const int os = d.cls == kCX01 ? 1 : (d.cls == kCX10 ? 2 : 1);
+      (void)s;
+      for_quads(w, [&](int i0, int i1, int i2, int i3) {
+        const int x = os == 1 ? i1 : i2, y = t == 3 ? i3 : i2;
+        const double2 a = tile[x], b = tile[y];
+        tile[x] = b;
+        tile[y] = a;
+        (void)i0;
+      });
+      break;
+    }
+    case kPairQ:
+    case kPairP:
+    case kPairX: {
+      const double2 m0 = __ldg(m), m1 = __ldg(m + 1), m2 = __ldg(m + 2), m3 = __ldg(m + 3);
+      const double2 n0 = __ldg(m + 4), n1 = __ldg(m + 5), n2 = __ldg(m + 6), n3 = __ldg(m + 7);
+      const int cls = d.cls;
+      for_quads(w, [&](int i0, int i1, int i2, int i3) {
+        // block 0 on members (u0,u1), block 1 on (u2,u3)
+        const int u0 = i0;
+        const int u1 = cls == kPairQ ? i2 : (cls == kPairP ? i1 : i3);
+        const int u2 = cls == kPairP ? i2 : i1;
+        const int u3 = cls == kPairQ ? i3 : (cls == kPairP ? i3 : i2);
+        double2 x = tile[u0], y = tile[u1], z = tile[u2], v = tile[u3];
+        mix2(x, y, m0, m1, m2, m3);
+        mix2(z, v, n0, n1, n2, n3);
+        tile[u0] = x;
+        tile[u1] = y;
+        tile[u2] = z;
+        tile[u3] = v;
+      });
+      break;
+    }
+    case kDiag2: {
+      const double2 d0 = __ldg(m), d1 = __ldg(m + 1), d2 = __ldg(m + 2), d3 = __ldg(m + 3);
+      for_quads(w, [&](int i0, int i1, int i2, int i3) {
+        tile[i0] = cmul(d0, tile[i0]);
+        tile[i1] = cmul(d1, tile[i1]);
+        tile[i2] = cmul(d2, tile[i2]);
+        tile[i3] = cmul(d3, tile[i3]);
+      });
+      break;
+    }
+    case kMono2: {
+      const double2 v0 = __ldg(m), v1 = __ldg(m + 1), v2 = __ldg(m + 2), v3 = __ldg(m + 3);
+      const int c0 = d.cols & 3, c1 = (d.cols >> 2) & 3, c2 = (d.cols >> 4) & 3,
+                c3 = (d.cols >> 6) & 3;
+      for_quads(w, [&](int i0, int i1, int i2, int i3) {
+        const double2 x0 = tile[i0], x1 = tile[i1], x2 = tile[i2], x3 = tile[i3];
+        tile[i0] = cmul(v0, pick(x0, x1, x2, x3, c0));
+        tile[i1] = cmul(v1, pick(x0, x1, x2, x3, c1));
+        tile[i2] = cmul(v2, pick(x0, x1, x2, x3, c2));
+        tile[i3] = cmul(v3, pick(x0, x1, x2, x3, c3));
+      });
+      break;
+    }
+    case kSparse2: {
+      const unsigned cols = d.cols;
+      for_quads(w, [&](int i0, int i1, int i2, int i3) {
+        const double2 x0 = tile[i0], x1 = tile[i1], x2 = tile[i2], x3 = tile[i3];
+        const int idx[4] = {i0, i1, i2, i3};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          double2 o = make_double2(0.0, 0.0);
+          cmac(o, __ldg(m + 2 * r), pick(x0, x1, x2, x3, (cols >> (4 * r)) & 3));
+          cmac(o, __ldg(m + 2 * r + 1), pick(x0, x1, x2, x3, (cols >> (4 * r + 2)) & 3));
+          tile[idx[r]] = o;
+        }
+      });
+      break;
+    }
+    default: {  // kDense2
+      for_quads(w, [&](int i0, int i1, int i2, int i3) {
+        const double2 x0 = tile[i0], x1 = tile[i1], x2 = tile[i2], x3 = tile[i3];
+        const int idx[4] = {i0, i1, i2, i3};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          double2 o = make_double2(0.0, 0.0);
+          cmac(o, __ldg(m + 4 * r + 0), x0);
+          cmac(o, __ldg(m + 4 * r + 1), x1);
+          cmac(o, __ldg(m + 4 * r + 2), x2);
+          cmac(o, __ldg(m + 4 * r + 3), x3);
+          tile[idx[r]] = o;
+        }
+      });
+      break;
+    }
   }
 }
-
-// Gray-code order of the 16 group members: member kGray[i] differs from
-// kGray[i-1] in group bit kFlip[i], so shared-memory addresses (XOR-linear in
-// the index, swz included) are produced with one XOR per member.
-__device__ constexpr int kGray[16] = {0, 1, 3, 2, 6, 7, 5, 4, 12, 13, 15, 14, 10, 11, 9, 8};
-__device__ constexpr int kFlip[16] = {0, 0, 1, 0, 2, 0, 1, 0, 3, 0, 1, 0, 2, 0, 1, 0};
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
@@ -460,13 +442,10 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// One CTA per SM (254 registers, no spills: the 16-amplitude register group
-// plus in-flight matrix values do not fit the 128-register budget of two
-// CTAs).  Global-memory latency is hidden by double buffering instead: while
-// the stages of tile i run, tile i+1 of the same pass streams into the other
-// shared-memory buffer with cp.async (LDGSTS).
+// One persistent CTA per SM; while the gate sweeps of tile i run, tile i+1 of
+// the same pass streams into the other shared-memory buffer with cp.async.
 __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
-  extern __shared__ __align__(128) double2 smem[];  // 2 x kTileAmps
+  extern __shared__ __align__(128) double2 smem[];  // 2 x kTileAmpsMax
   __shared__ PassDesc sp;
   __shared__ uint64_t s_hi[16];  // global offset of tile-local bits 8..11 for j = 0..15
   __shared__ double red[32];
@@ -496,8 +475,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
     const uint64_t n_tiles = uint64_t(1) << n_out;
     const int n_j = k > 8 ? 1 << (k - 8) : 1;
     const bool loader = tid < (1 << lo_bits);
-    const bool grouper = tid < (1 << (k - kGroupQubits));
     const double cscale = sp.collapse_q >= 0 ? 1.0 / sqrt(carry_p0) : 1.0;
+    const int g_begin = sp.gate_begin, g_end = sp.gate_end;
     double msum = 0.0;
 
     auto tile_base = [&](uint64_t t) {
@@ -517,9 +496,9 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
     if (t < n_tiles) issue_load(t, smem);
     cp_async_commit();
     for (; t < n_tiles; t += gridDim.x, cur ^= 1) {
-      double2* tile = smem + cur * kTileAmps;
+      double2* tile = smem + cur * kTileAmpsMax;
       const uint64_t t_next = t + gridDim.x;
-      if (t_next < n_tiles) issue_load(t_next, smem + (cur ^ 1) * kTileAmps);
+      if (t_next < n_tiles) issue_load(t_next, smem + (cur ^ 1) * kTileAmpsMax);
       cp_async_commit();
       cp_async_wait<1>();  // this tile's group has landed (next may be in flight)
       __syncthreads();
@@ -539,33 +518,9 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
           }
         __syncthreads();
       }
-      // stages: shared -> registers -> gates -> shared
-      for (int s = sp.stage_begin; s < sp.stage_end; ++s) {
-        if (grouper) {
-          const StageDesc S = p.stages[s];
-          int tb = 0;
-          for (int b = 0; b < k - kGroupQubits; ++b)
-            if (tid >> b & 1) tb |= 1 << ((S.tperm >> (4 * b)) & 15);
-          const int x0 = swz(1 << S.rpos[0]), x1 = swz(1 << S.rpos[1]),
-                    x2 = swz(1 << S.rpos[2]), x3 = swz(1 << S.rpos[3]);
-          double2 a[16];
-          int addr = swz(tb);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            if (i) addr ^= kFlip[i] == 0 ? x0 : (kFlip[i] == 1 ? x1 : (kFlip[i] == 2 ? x2 : x3));
-            a[kGray[i]] = tile[addr];
-          }
-          for (int g = S.gate_begin; g < S.gate_end; ++g) {
-            const GateDesc d = p.gates[g];
-            apply_gate(a, d, p.mats);
-          }
-          addr = swz(tb);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            if (i) addr ^= kFlip[i] == 0 ? x0 : (kFlip[i] == 1 ? x1 : (kFlip[i] == 2 ? x2 : x3));
-            tile[addr] = a[kGray[i]];
-          }
-        }
+      for (int g = g_begin; g < g_end; ++g) {
+        const GateDesc d = p.gates[g];
+        apply_gate(tile, k, d, p.mats + d.mat);
         __syncthreads();
       }
       // shared -> global (+ assertion epilogue partial sums)
@@ -683,7 +638,6 @@ struct nsb_plan {
   nsb_ctx* ctx = nullptr;
   HostPlan host;
   DevBuf<PassDesc> passes, mma_passes;
-  DevBuf<StageDesc> stages;
   DevBuf<GateDesc> gates;
   DevBuf<double2> mats, dense;
   DevBuf<double> record, partials;
@@ -812,7 +766,6 @@ void launch_blocked(nsb_ctx* c, nsb_plan* P, const PassDesc* passes, int pb, int
   bp.passes = passes;
   bp.pass_begin = pb;
   bp.pass_end = pe;
-  bp.stages = P->stages.ptr;
   bp.gates = P->gates.ptr;
   bp.mats = P->mats.ptr;
   bp.partials = P->partials.ptr;
@@ -822,7 +775,7 @@ void launch_blocked(nsb_ctx* c, nsb_plan* P, const PassDesc* passes, int pb, int
   void* args[] = {&bp};
   NSB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::k_blocked),
                                        dim3(c->blocked_grid), dim3(kPassThreads), args,
-                                       2 * sizeof(double2) * kTileAmps, c->stream));
+                                       2 * sizeof(double2) * kTileAmpsMax, c->stream));
   P->last_launches += 1;
 }
 
@@ -861,7 +814,7 @@ int nsb_ctx_create(int32_t device, nsb_ctx** out, nsb_status* st) {
     NSB_CUDA(cudaEventCreate(&ctx->ev0));
     NSB_CUDA(cudaEventCreate(&ctx->ev1));
     NSB_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
-    const int smem = 2 * sizeof(double2) * kTileAmps;
+    const int smem = 2 * sizeof(double2) * kTileAmpsMax;
     NSB_CUDA(cudaFuncSetAttribute(dev::k_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   smem));
     int per_sm = 0;
@@ -1040,11 +993,10 @@ int nsb_plan_create(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const double* 
     if (n_ops < 0 || (n_ops > 0 && !ops)) throw std::invalid_argument("bad op list");
     NSB_CUDA(cudaSetDevice(c->device));
     P->ctx = c;
-    P->host.build(ops, n_ops, params, payloads, c->n);
+    P->host.build(ops, n_ops, params, payloads, c->n, c->blocked_grid);
     HostPlan& H = P->host;
     P->passes.upload(H.passes.data(), H.passes.size(), c->stream);
     P->mma_passes.upload(H.mma_passes.data(), H.mma_passes.size(), c->stream);
-    P->stages.upload(H.stages.data(), H.stages.size(), c->stream);
     P->gates.upload(H.gates.data(), H.gates.size(), c->stream);
     P->mats.upload(reinterpret_cast<const double2*>(H.matrices.data()), H.matrices.size() / 2,
                    c->stream);

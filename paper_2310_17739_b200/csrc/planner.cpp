@@ -74,9 +74,10 @@ uint8_t pack_matrix(const double* m, int nq, std::vector<double>& packed, uint16
         if (c == sigma[r] ? !is_one(r * 4 + c) : nz[r][c]) return false;
     return true;
   };
-  static const int kCxA[4] = {0, 3, 2, 1}, kCxB[4] = {0, 1, 3, 2};
+  static const int kCxA[4] = {0, 3, 2, 1}, kCxB[4] = {0, 1, 3, 2}, kSw[4] = {0, 2, 1, 3};
   if (exact_perm(kCxA)) return kCX01;
   if (exact_perm(kCxB)) return kCX10;
+  if (exact_perm(kSw)) return kSwap;
   // two independent 2x2 blocks on fixed index pairs
   struct PairPattern {
     uint8_t cls;
@@ -194,52 +195,97 @@ std::vector<std::vector<int>> pack_groups(const std::vector<uint64_t>& masks, in
   return groups;
 }
 
-// order the non-R tile positions so that lanes 0..7 of a quarter-warp hit
-// distinct 16-byte shared-memory slots under the XOR swizzle of device.cu
-uint32_t thread_perm(const int8_t rpos[4], int k) {
-  std::vector<int> free_pos;
-  for (int p = 0; p < k; ++p) {
-    bool in_r = false;
-    for (int j = 0; j < 4; ++j) in_r |= rpos[j] == p;
-    if (!in_r) free_pos.push_back(p);
-  }
-  std::vector<int> order;
-  for (int cls = 0; cls < 3; ++cls)
-    for (size_t i = 0; i < free_pos.size(); ++i)
-      if (free_pos[i] >= 0 && free_pos[i] % 3 == cls) {
-        order.push_back(free_pos[i]);
-        free_pos[i] = -1;
-        break;
-      }
-  for (int p : free_pos)
-    if (p >= 0) order.push_back(p);
-  uint32_t packed = 0;
-  for (size_t t = 0; t < order.size() && t < 8; ++t) packed |= static_cast<uint32_t>(order[t]) << (4 * t);
-  return packed;
-}
-
 }  // namespace
 
+// compress the bits of `m` that lie in `set` into consecutive positions
+static inline uint32_t pext64(uint64_t m, uint64_t set) {
+  uint32_t out = 0;
+  int j = 0;
+  for (uint64_t s = set; s; s &= s - 1, ++j)
+    if (m & (s & -s)) out |= 1u << j;
+  return out;
+}
+
+static inline int lowest_bit(uint64_t m) { return __builtin_ctzll(m); }
+
+// tile size: the largest k <= 12 whose tile count spreads over the persistent
+// CTAs with >= 95% balance (2^(n-k) tiles over `workers` CTAs)
+// physical support (bits of ma | mb) above which the frame is flushed first
+constexpr int kMaxSupport = 6;
+
+static int choose_tile_qubits(int n, int workers) {
+  if (n <= kTileQubitsMax) return n;
+  for (int k = kTileQubitsMax; k >= 9; --k) {
+    const double tiles = std::ldexp(1.0, n - k);
+    const double rounds = std::ceil(tiles / workers);
+    if (tiles / (rounds * workers) >= 0.95) return k;
+  }
+  return kTileQubitsMax;
+}
+
 void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
-                     const double* payloads, int n) {
+                     const double* payloads, int n, int workers) {
   n_qubits = n;
   if (n < 1 || n > kMaxQubits) throw std::invalid_argument("qubit count out of range");
-  const int k = std::min(n, kTileQubits);
+  const int k = choose_tile_qubits(n, workers);
   tile_qubits = k;
-  blocked = n >= kGroupQubits + 2;
+  blocked = n >= 6;
   PoolBuilder pb{matrices, {}};
-  std::vector<GateOp> run;
+  std::vector<PhysGate> run;
+  uint64_t col[64];  // frame: physical mask of logical bit j (M e_j)
+  for (int j = 0; j < 64; ++j) col[j] = uint64_t(1) << j;
+  std::vector<double> packed;
   int step = 0;
+
+  auto emit_cx = [&](int c, int t) {  // physical CX(control c, target t)
+    PhysGate g{};
+    g.cls = kCX01;
+    g.nq = 2;
+    g.ma = uint64_t(1) << c;
+    g.mb = uint64_t(1) << t;
+    g.mat = 0;
+    run.push_back(g);
+    ++n_flush_gates;
+  };
+  // Bring the frame back to the identity: reduce M to I by column additions
+  // col[c] ^= col[t] (= M * CX(c, t)), then M = C_k ... C_1, applied
+  // physically in the reverse of the recording order.
+  auto flush_frame = [&]() {
+    bool identity = true;
+    for (int j = 0; j < n; ++j) identity &= col[j] == (uint64_t(1) << j);
+    if (identity) return;
+    uint64_t m[64];
+    std::memcpy(m, col, sizeof m);
+    std::vector<std::pair<int, int>> ops_rec;
+    for (int b = 0; b < n; ++b) {
+      if (!(m[b] >> b & 1)) {
+        int j = b + 1;
+        while (j < n && !(m[j] >> b & 1)) ++j;
+        if (j >= n) throw std::logic_error("relabeling frame is singular");
+        m[b] ^= m[j];
+        ops_rec.emplace_back(b, j);
+      }
+      for (int j = 0; j < n; ++j)
+        if (j != b && (m[j] >> b & 1)) {
+          m[j] ^= m[b];
+          ops_rec.emplace_back(j, b);
+        }
+    }
+    for (size_t i = ops_rec.size(); i-- > 0;) emit_cx(ops_rec[i].first, ops_rec[i].second);
+    for (int j = 0; j < 64; ++j) col[j] = uint64_t(1) << j;
+  };
   auto flush_run = [&]() {
+    flush_frame();
     if (run.empty()) return;
     Item it;
     it.kind = Item::kGates;
     it.pass_begin = static_cast<int32_t>(passes.size());
-    schedule_run(run, pb, k);
+    schedule_run(run, k);
     it.pass_end = static_cast<int32_t>(passes.size());
     items.push_back(it);
     run.clear();
   };
+
   for (int64_t i = 0; i < n_ops; ++i) {
     const nsb_op& o = ops[i];
     if (o.kind == NSB_OP_BARRIER) continue;
@@ -273,15 +319,39 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
       for (int j = 0; j < o.nq; ++j) it.qs[j] = o.q[j];
       it.mat_off = static_cast<int64_t>(dense_mats.size() / 2);
       dense_mats.insert(dense_mats.end(), mat.v, mat.v + 2 * dim * dim);
+      flops += 8ll * dim * dim * (int64_t(1) << (n - o.nq));
       items.push_back(it);
       continue;
     }
-    GateOp g;
+    PhysGate g{};
     g.nq = o.nq;
-    g.q[0] = o.q[0];
-    g.q[1] = o.nq == 2 ? o.q[1] : -1;
-    g.mask = (uint64_t(1) << o.q[0]) | (o.nq == 2 ? uint64_t(1) << o.q[1] : 0);
-    std::memcpy(g.m, mat.v, sizeof(double) * 2 * dim * dim);
+    g.cls = pack_matrix(mat.v, o.nq, packed, g.cols);
+    class_count[g.cls]++;
+    const int a = o.q[0], b = o.nq == 2 ? o.q[1] : -1;
+    if (g.cls == kCX01) {  // logical CX(a -> b): M <- M CX  (column a += column b)
+      col[a] ^= col[b];
+      ++n_frame_gates;
+      continue;
+    }
+    if (g.cls == kCX10) {
+      col[b] ^= col[a];
+      ++n_frame_gates;
+      continue;
+    }
+    if (g.cls == kSwap) {
+      std::swap(col[a], col[b]);
+      ++n_frame_gates;
+      continue;
+    }
+    if (popc(col[a] | (o.nq == 2 ? col[b] : 0)) > kMaxSupport) {
+      flush_frame();  // keep physical supports small so passes stay dense
+      ++n_frame_flushes;
+    }
+    g.ma = col[a];
+    g.mb = o.nq == 2 ? col[b] : 0;
+    g.mat = pb.add(packed.data(), static_cast<int>(packed.size() / 2));
+    static const int kNnz[kNumClasses] = {4, 2, 16, 8, 4, 4, 0, 0, 8, 8, 8, 0};
+    flops += 8ll * kNnz[g.cls] * (int64_t(1) << (n - g.nq));
     run.push_back(g);
   }
   flush_run();
@@ -289,85 +359,55 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
   build_mma();
 }
 
-void HostPlan::schedule_run(std::vector<GateOp>& run, PoolBuilder& pb, int k) {
+void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
   const int n = n_qubits;
   const uint64_t all = (n == 64) ? ~uint64_t(0) : ((uint64_t(1) << n) - 1);
   const uint64_t low = (uint64_t(1) << std::min(kLowQubits, n)) - 1;
   std::vector<uint64_t> masks(run.size());
-  for (size_t i = 0; i < run.size(); ++i) masks[i] = run[i].mask;
+  for (size_t i = 0; i < run.size(); ++i) {
+    masks[i] = run[i].ma | run[i].mb;
+    if (popc(masks[i] | low) > k) throw std::logic_error("gate support exceeds the tile");
+  }
   std::vector<uint64_t> sets;
-  auto pass_groups = pack_groups(masks, k, low, all, 1024, sets);
-  std::vector<double> packed;
+  auto pass_groups = pack_groups(masks, k, low, all, 2048, sets);
   for (size_t pi = 0; pi < pass_groups.size(); ++pi) {
-    const auto& pg = pass_groups[pi];
     uint64_t tset = sets[pi];
-    // pad the tile set with the lowest unused qubits up to k
     for (int q = 0; q < n && popc(tset) < k; ++q) tset |= uint64_t(1) << q;
     PassDesc P{};
     P.k = k;
     P.measure_q = P.collapse_q = -1;
     P.measure_slot = P.collapse_slot = -1;
-    int local_of[64];
     int t = 0, o = 0;
     for (int q = 0; q < n; ++q) {
-      if (tset >> q & 1) {
-        local_of[q] = t;
+      if (tset >> q & 1)
         P.tq[t++] = static_cast<int8_t>(q);
-      } else {
-        local_of[q] = -1;
+      else
         P.oq[o++] = static_cast<int8_t>(q);
+    }
+    P.gate_begin = static_cast<int32_t>(gates.size());
+    for (int gi : pass_groups[pi]) {
+      const PhysGate& g = run[gi];
+      GateDesc d{};
+      d.mat = g.mat;
+      d.cls = g.cls;
+      d.nq = static_cast<uint8_t>(g.nq);
+      d.cols = g.cols;
+      const uint32_t ma = pext64(g.ma, tset), mb = pext64(g.mb, tset);
+      d.ma = static_cast<uint16_t>(ma);
+      d.mb = static_cast<uint16_t>(mb);
+      const int pa = lowest_bit(ma);
+      if (g.nq == 1) {
+        d.plo = d.phi = static_cast<uint8_t>(pa);
+      } else {
+        const uint32_t mr = (mb >> pa & 1) ? (mb ^ ma) : mb;
+        if (!mr) throw std::logic_error("degenerate gate masks");
+        const int pbit = lowest_bit(mr);
+        d.plo = static_cast<uint8_t>(std::min(pa, pbit));
+        d.phi = static_cast<uint8_t>(std::max(pa, pbit));
       }
+      gates.push_back(d);
     }
-    // stages on tile-local masks
-    std::vector<uint64_t> lmasks(pg.size());
-    for (size_t j = 0; j < pg.size(); ++j) {
-      const GateOp& g = run[pg[j]];
-      lmasks[j] = uint64_t(1) << local_of[g.q[0]];
-      if (g.nq == 2) lmasks[j] |= uint64_t(1) << local_of[g.q[1]];
-    }
-    std::vector<uint64_t> rsets;
-    const uint64_t lall = (uint64_t(1) << k) - 1;
-    auto stage_groups = pack_groups(lmasks, kGroupQubits, 0, lall, 256, rsets);
-    P.stage_begin = static_cast<int32_t>(stages.size());
-    for (size_t si = 0; si < stage_groups.size(); ++si) {
-      uint64_t r = rsets[si];
-      for (int p = 0; p < k && popc(r) < kGroupQubits; ++p) r |= uint64_t(1) << p;
-      StageDesc S{};
-      int gbit_of[64];
-      int j = 0;
-      for (int p = 0; p < k; ++p)
-        if (r >> p & 1) {
-          gbit_of[p] = j;
-          S.rpos[j++] = static_cast<int8_t>(p);
-        }
-      S.tperm = thread_perm(S.rpos, k);
-      S.gate_begin = static_cast<int32_t>(gates.size());
-      for (int gi : stage_groups[si]) {
-        GateOp g = run[pg[gi]];
-        GateDesc d{};
-        if (g.nq == 1) {
-          d.a = static_cast<uint8_t>(gbit_of[local_of[g.q[0]]]);
-          d.b = d.a;
-        } else {
-          int a = gbit_of[local_of[g.q[0]]], b = gbit_of[local_of[g.q[1]]];
-          if (a > b) {
-            swap_slots(g.m);
-            std::swap(a, b);
-          }
-          d.a = static_cast<uint8_t>(a);
-          d.b = static_cast<uint8_t>(b);
-        }
-        d.cls = pack_matrix(g.m, g.nq, packed, d.cols);
-        d.mat = pb.add(packed.data(), static_cast<int>(packed.size() / 2));
-        class_count[d.cls]++;
-        static const int kNnz[kNumClasses] = {4, 2, 16, 8, 4, 4, 0, 0, 8, 8, 8};
-        flops += 8ll * kNnz[d.cls] * (int64_t(1) << (n - g.nq));
-        gates.push_back(d);
-      }
-      S.gate_end = static_cast<int32_t>(gates.size());
-      stages.push_back(S);
-    }
-    P.stage_end = static_cast<int32_t>(stages.size());
+    P.gate_end = static_cast<int32_t>(gates.size());
     passes.push_back(P);
   }
 }
@@ -384,7 +424,7 @@ void HostPlan::build_mma() {
     P.k = tile_qubits;
     P.measure_q = P.collapse_q = -1;
     P.measure_slot = P.collapse_slot = -1;
-    P.stage_begin = P.stage_end = 0;
+    P.gate_begin = P.gate_end = 0;
     int t = 0, o = 0;
     for (int q = 0; q < n_qubits; ++q) {
       if (q < tile_qubits)
@@ -450,9 +490,9 @@ void fill_info(const nsb::HostPlan& H, nsb_plan_info* info) {
   info->flops = H.flops;
   info->tile_qubits = H.tile_qubits;
   info->n_items = static_cast<int64_t>(H.items.size());
-  int64_t n_st = 0;
-  for (const nsb::PassDesc& p : passes) n_st += p.stage_end - p.stage_begin;
-  info->n_stages = n_st;
+  info->n_frame_gates = H.n_frame_gates;
+  info->n_flush_gates = H.n_flush_gates;
+  info->n_device_gates = static_cast<int64_t>(H.gates.size());
 }
 }  // namespace
 
@@ -469,7 +509,7 @@ extern "C" int nsb_plan_analyze(const nsb_op* ops, int64_t n_ops, const double* 
   }
   try {
     nsb::HostPlan H;
-    H.build(ops, n_ops, params, payloads, n_qubits);
+    H.build(ops, n_ops, params, payloads, n_qubits, 148);
     fill_info(H, info);
     if (class_counts)
       for (int c = 0; c < nsb::kNumClasses; ++c) class_counts[c] = H.class_count[c];

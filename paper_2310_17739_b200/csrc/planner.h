@@ -1,17 +1,23 @@
 // Device program produced by the host planner (planner.cpp) and executed by
 // the blocked gate-stream kernel (device.cu).
 //
-// Hierarchy:
-//   pass   = one sweep of the state through shared memory: the state is cut
-//            into 2^(n-k) tiles of 2^k amplitudes over a tile qubit set T
-//            (|T| = k <= kTileQubits, always containing qubits 0..2 so every
-//            global access is a full 128-byte line);
-//   stage  = one shared-memory round trip inside a pass: every thread pulls a
-//            16-amplitude group spanned by 4 tile-local qubits R into registers
-//            and applies all stage gates (on qubits of R) there;
-//   gate   = a 1q / 2q payload in group-local bit positions plus its sparsity
-//            class (dense, <=2 nnz per row, monomial, diagonal).
-// Mid-circuit measurements end a pass: the pass epilogue writes per-tile
+// Two ideas carry the design:
+//  1. Relabeling frame.  Exact CX and SWAP payloads are permutations that are
+//     linear over GF(2) on basis indices.  The planner does not move data for
+//     them: it keeps a linear map M with psi(v) = phi(M v) between the
+//     logical state psi and the physical array phi, and rewrites every later
+//     gate on logical qubit j to act along the physical XOR mask M e_j.  At
+//     every measurement / reset / dense k-qubit gate and at the end of the
+//     program the frame is flushed back to the identity with a short
+//     sequence of physical CX gates (exact data movement), so everything
+//     outside a gate run sees the reference's ordinary little-endian state.
+//  2. Passes.  The state is cut into 2^(n-k) tiles of 2^k amplitudes over a
+//     physical tile qubit set T (|T| = k <= kTileQubitsMax, always holding
+//     qubits 0..2 so global accesses are whole 128-byte lines).  A pass
+//     streams every tile through shared memory once and applies each of its
+//     gates as one shared-memory sweep (pairs / quads along the gate's
+//     tile-local XOR masks).  Global traffic is 32 B per amplitude per pass.
+// Mid-circuit measurements end a pass: the pass epilogue writes per-CTA
 // partial sums of |a|^2 over the |0> half, the grid agrees on p0 after the
 // barrier, and the next pass's prologue applies the collapse.
 #pragma once
@@ -20,16 +26,14 @@
 
 namespace nsb {
 
-constexpr int kTileQubits = 12;                  // 4096 amplitudes = 64 KiB tile
-constexpr int kTileAmps = 1 << kTileQubits;
-constexpr int kGroupQubits = 4;                  // 16 amplitudes per thread
-constexpr int kGroupAmps = 1 << kGroupQubits;
-constexpr int kPassThreads = kTileAmps / kGroupAmps;  // 256
+constexpr int kTileQubitsMax = 12;               // 4096 amplitudes = 64 KiB per buffer
+constexpr int kTileAmpsMax = 1 << kTileQubitsMax;
+constexpr int kPassThreads = 256;
 constexpr int kLowQubits = 3;                    // always-tiled qubits 0..2 (128 B runs)
 constexpr int kMaxQubits = 40;
 
 // Payload classes, chosen by exact-zero structure (skipping an exact zero
-// term is bit-identical to multiplying by it).  Ordered cheapest first.
+// term is bit-identical to multiplying by it).
 enum GateClass : uint8_t {
   kDense1 = 0,    // 2x2                                  (4 complex values)
   kDiag1 = 1,     // 2x2 diagonal                         (2)
@@ -37,40 +41,35 @@ enum GateClass : uint8_t {
   kSparse2 = 3,   // 4x4, <= 2 nonzeros per row, any cols (8 + column codes)
   kMono2 = 4,     // 4x4, <= 1 nonzero per row            (4 + column codes)
   kDiag2 = 5,     // 4x4 diagonal                         (4)
-  kCX01 = 6,      // exact CX, slot 0 controls slot 1: swaps |01>,|11>  (0)
-  kCX10 = 7,      // exact CX, slot 1 controls slot 0: swaps |10>,|11>  (0)
-  kPairQ = 8,     // 2x2 on slot 1 selected by slot 0: (0,2) and (1,3)  (8)
-  kPairP = 9,     // 2x2 on slot 0 selected by slot 1: (0,1) and (2,3)  (8)
-  kPairX = 10,    // 2x2 on the anti-diagonal pairs (0,3) and (1,2)     (8)
-  kNumClasses = 11
+  kCX01 = 6,      // exact CX, slot 0 controls slot 1: swaps members 1,3  (0)
+  kCX10 = 7,      // exact CX, slot 1 controls slot 0: swaps members 2,3  (0)
+  kPairQ = 8,     // 2x2 blocks on members (0,2) and (1,3)                (8)
+  kPairP = 9,     // 2x2 blocks on members (0,1) and (2,3)                (8)
+  kPairX = 10,    // 2x2 blocks on members (0,3) and (1,2)                (8)
+  kSwap = 11,     // exact SWAP: swaps members 1,2                        (0)
+  kNumClasses = 12
 };
 
 struct GateDesc {     // 16 bytes
   int32_t mat;        // offset (complex elements) into the matrix pool
   uint8_t cls;        // GateClass
-  uint8_t a, b;       // group bit of slot 0 / slot 1 (a < b after planning)
-  uint8_t pad;
-  uint16_t cols;      // sparse classes: 2 bits per (row, nz#) column index
-  uint16_t pad2;
-  int32_t pad3;
+  uint8_t plo, phi;   // pivot bits (ascending) removed from the quad/pair index
+  uint8_t nq;         // 1 or 2
+  uint16_t ma, mb;    // tile-local XOR masks of slot 0 / slot 1
+  uint16_t cols;      // kSparse2 / kMono2: 2-bit column codes
+  uint16_t pad;
 };
 
-struct StageDesc {    // 16 bytes
-  int32_t gate_begin, gate_end;
-  int8_t rpos[kGroupQubits];                  // tile-local bit of group bit j
-  uint32_t tperm;                             // packed 4-bit tile-local positions
-};                                            // of thread bits 0..7 (non-R)
-
 struct PassDesc {
-  int32_t stage_begin, stage_end;
-  int32_t k;              // tile qubits used (<= kTileQubits)
+  int32_t gate_begin, gate_end;
+  int32_t k;              // tile qubits used (<= kTileQubitsMax)
   int32_t measure_q;      // epilogue: partial P(q=0) sums (-1: none)
   int32_t measure_slot;   // index into the probability record
-  int32_t collapse_q;     // prologue: collapse onto q=0 using record[collapse_slot]
+  int32_t collapse_q;     // prologue: collapse onto q=0 using the carried p0
   int32_t collapse_slot;
   int32_t pad;
-  int8_t tq[16];          // tile-local bit i -> global qubit (ascending)
-  int8_t oq[48];          // tile-index bit j -> global qubit (ascending)
+  int8_t tq[16];          // tile-local bit i -> physical qubit (ascending)
+  int8_t oq[48];          // tile-index bit j -> physical qubit (ascending)
 };
 
 }  // namespace nsb

@@ -43,13 +43,13 @@ struct PoolBuilder {
   }
 };
 
-struct GateOp {
-  int nq;
-  int q[2];      // global qubits, slot order
-  uint64_t mask;
-  double m[32];  // resolved matrix (slot order)
+struct PhysGate {
+  uint8_t cls = 0;
+  int nq = 0;
+  uint64_t ma = 0, mb = 0;  // physical XOR masks of slot 0 / slot 1
+  int32_t mat = 0;          // packed payload offset in the pool
+  uint16_t cols = 0;
 };
-
 
 struct Item {
   enum Kind { kGates, kDense, kMeasure, kReset } kind;
@@ -65,22 +65,25 @@ struct HostPlan {
   bool blocked = false;   // blocked pass kernel (n >= 6); else per-op kernels
   bool mma_ok = false;    // whole MMA run fits one cooperative launch
   int64_t n_gates = 0, n_measures = 0;
+  int64_t n_frame_gates = 0;  // exact CX/SWAP absorbed by the relabeling frame
+  int64_t n_flush_gates = 0;  // physical CX emitted to flush the frame
+  int64_t n_frame_flushes = 0;  // flushes forced by a wide support
   int64_t flops = 0;
   int64_t class_count[kNumClasses] = {};
 
   std::vector<Item> items;
   std::vector<PassDesc> passes;      // plain gate passes (items reference ranges)
   std::vector<PassDesc> mma_passes;  // whole-circuit MMA program
-  std::vector<StageDesc> stages;
   std::vector<GateDesc> gates;
   std::vector<double> matrices;      // packed, deduplicated payload pool
   std::vector<double> dense_mats;    // k-qubit / unblocked matrices (full)
 
+  // workers: persistent CTAs of the pass kernel (tile-size choice)
   void build(const nsb_op* ops, int64_t n_ops, const double* params, const double* payloads,
-             int n);
+             int n, int workers);
 
  private:
-  void schedule_run(std::vector<GateOp>& run, PoolBuilder& pb, int k);
+  void schedule_run(std::vector<PhysGate>& run, int k);
   void build_mma();
 };
 

@@ -348,3 +348,66 @@ def test_blocked_kernel_against_oracle(n):
     rep = run(fused, "mma", shots=128, seed=5, ancilla=n - 1)
     assert rep.assert_probs == pytest.approx(probs, abs=1e-12)
     assert rep.samples == samples
+
+
+def ladder_circuit(rng, n, terms, blocks=2):
+    """JW-ladder rotations (the filter-circuit body, projection.py:191-212)
+    with random Pauli words: long CX chains that the relabeling frame absorbs."""
+    anc = n - 1
+    c = Circuit(n, [("c", blocks), ("r", n)])
+    for b in range(blocks):
+        for _ in range(terms):
+            inv = sorted(int(x) for x in rng.choice(n - 1, int(rng.integers(1, n - 1)),
+                                                    replace=False))
+            letters = {q: "XYZ"[int(rng.integers(3))] for q in inv}
+            for q in inv:
+                if letters[q] == "X":
+                    c.h(q)
+                elif letters[q] == "Y":
+                    c.sdg(q)
+                    c.h(q)
+            c.sdg(anc)
+            c.h(anc)
+            chain = inv + [anc]
+            for x, y in zip(chain, chain[1:]):
+                c.cx(x, y)
+            c.rz(float(rng.uniform(-1, 1)), anc)
+            for x, y in reversed(list(zip(chain, chain[1:]))):
+                c.cx(x, y)
+            c.h(anc)
+            c.gate_op(Gate.S, (anc,))
+            for q in reversed(inv):
+                if letters[q] == "X":
+                    c.h(q)
+                elif letters[q] == "Y":
+                    c.h(q)
+                    c.gate_op(Gate.S, (q,))
+            if rng.random() < 0.2:  # stray swaps and reversed CX exercise the frame
+                x, y = (int(v) for v in rng.choice(n - 1, 2, replace=False))
+                c.gate_op(Gate.SWAP, (x, y))
+                c.cx(y, x)
+        c.measure(anc, b)
+        c.barrier()
+        c.reset(anc)
+        c.barrier()
+    for q in range(n):
+        c.measure(q, blocks + q)
+    return c
+
+
+@pytest.mark.parametrize("n,terms", [(7, 30), (12, 40), (14, 60), (18, 40)])
+def test_relabeling_frame_against_oracle(n, terms):
+    rng = np.random.default_rng(50 + n)
+    c = ladder_circuit(rng, n, terms)
+    for circ in (c, fuse_pipeline(c)[0]):
+        instrs = oracle_from_circuit(circ)
+        try:
+            probs, samples, state, _ = O.run_mma(instrs, n, 256, 9)
+        except O.OracleAssertion:
+            pytest.skip("dead assertion branch")
+        rep = run(circ, "mma", shots=256, seed=9, ancilla=n - 1)
+        assert rep.assert_probs == pytest.approx(probs, abs=1e-12)
+        assert rep.samples == samples
+        rej = run(circ, "rejection", shots=3, seed=4, ancilla=None)
+        acc, steps, counts = O.run_rejection(instrs, n, 3, 4)
+        assert (rej.accepted, rej.step_rejections, rej.samples) == (acc, steps, counts)
