@@ -193,6 +193,28 @@ int nsb_plan_analyze(const nsb_op* ops, int64_t n_ops, const double* params,
                      int64_t* class_counts, nsb_status* st);
 int nsb_plan_info_get(const nsb_plan* plan, nsb_plan_info* info);
 
+/* Host-side view of a compiled plan, for tests and tooling: the device
+ * program exactly as nsb_plan_create would upload it (PassDesc / GateDesc
+ * records of paper_2310_17739_b200/csrc/planner.h, packed matrices).  The
+ * library never executes a plan on the host; tests/plan_exec.py does, to
+ * verify the planner on machines without a GPU. */
+typedef struct nsb_plan_view {
+  int32_t n_qubits, tile_qubits, mma_ok, n_measures;
+  int32_t pass_desc_bytes, gate_desc_bytes, pad0, pad1;
+  int64_t n_passes, n_mma_passes, n_gate_descs, n_matrices, n_items;
+  const void* passes;      /* plain gate passes (items reference ranges) */
+  const void* mma_passes;  /* single-launch MMA program */
+  const void* gates;
+  const double* matrices;  /* complex pool */
+  const int32_t* items;    /* n_items x 4: kind (0 gates, 1 measure, 2 reset,
+                              3 dense), pass_begin | qubit, pass_end | step, k */
+} nsb_plan_view;
+int nsb_host_plan_build(const nsb_op* ops, int64_t n_ops, const double* params,
+                        const double* payloads, int32_t n_qubits, int32_t workers, void** out,
+                        nsb_status* st);
+int nsb_host_plan_view(const void* plan, nsb_plan_view* view);
+void nsb_host_plan_free(void* plan);
+
 /* MMA mode (engine.py:414-423): execute the whole plan from the current
  * state; each MEASURE asserts |0> (p0 < eps -> NSB_EASSERT with step/p0),
  * records p0 into assert_probs[step] and renormalises; RESET is a no-op. */

@@ -52,6 +52,19 @@ class PlanInfo(ctypes.Structure):
                 ("n_device_gates", ctypes.c_int64)]
 
 
+class PlanView(ctypes.Structure):
+    _fields_ = [("n_qubits", ctypes.c_int32), ("tile_qubits", ctypes.c_int32),
+                ("mma_ok", ctypes.c_int32), ("n_measures", ctypes.c_int32),
+                ("pass_desc_bytes", ctypes.c_int32), ("gate_desc_bytes", ctypes.c_int32),
+                ("pad0", ctypes.c_int32), ("pad1", ctypes.c_int32),
+                ("n_passes", ctypes.c_int64), ("n_mma_passes", ctypes.c_int64),
+                ("n_gate_descs", ctypes.c_int64), ("n_matrices", ctypes.c_int64),
+                ("n_items", ctypes.c_int64),
+                ("passes", ctypes.c_void_p), ("mma_passes", ctypes.c_void_p),
+                ("gates", ctypes.c_void_p), ("matrices", ctypes.c_void_p),
+                ("items", ctypes.c_void_p)]
+
+
 _P = ctypes.c_void_p
 _I32, _I64, _D = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
 _ST = ctypes.POINTER(Status)
@@ -84,6 +97,10 @@ _SIGNATURES = {
     "nsb_plan_info_get": (ctypes.c_int, [_P, ctypes.POINTER(PlanInfo)]),
     "nsb_plan_analyze": (ctypes.c_int, [_P, _I64, _P, _P, _I32, ctypes.POINTER(PlanInfo), _P,
                                         _ST]),
+    "nsb_host_plan_build": (ctypes.c_int, [_P, _I64, _P, _P, _I32, _I32, ctypes.POINTER(_P),
+                                           _ST]),
+    "nsb_host_plan_view": (ctypes.c_int, [_P, ctypes.POINTER(PlanView)]),
+    "nsb_host_plan_free": (None, [_P]),
     "nsb_plan_run_mma": (ctypes.c_int, [_P, _P, _D, _P, _ST]),
     "nsb_plan_run_segment": (ctypes.c_int, [_P, _P, _I64, _ST]),
     "nsb_plan_segment_marker": (ctypes.c_int, [_P, _I64, ctypes.POINTER(_I32),

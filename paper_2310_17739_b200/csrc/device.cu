@@ -291,12 +291,18 @@ struct Sweep {
   int n_items;  // quads (2q) or pairs (1q) in the tile
   int plo, phi;
   int sa, sb;   // swizzled masks
+  int ra, rb;   // tile-local dual rows
+  int ga, gb;   // out-of-tile parities of the dual rows for this tile
 };
 
+// member 0 of each coset is the one whose logical slot bits are zero: start
+// from the pivot representative and step along ma / mb by its logical bits
 template <class F>
 __device__ __forceinline__ void for_quads(const Sweep& w, F f) {
   for (int j = threadIdx.x; j < w.n_items; j += kPassThreads) {
-    const int a0 = swz(ins0(ins0(j, w.plo), w.phi));
+    const int b = ins0(ins0(j, w.plo), w.phi);
+    const int la = (__popc(b & w.ra) ^ w.ga) & 1, lb = (__popc(b & w.rb) ^ w.gb) & 1;
+    const int a0 = swz(b) ^ (la ? w.sa : 0) ^ (lb ? w.sb : 0);
     f(a0, a0 ^ w.sa, a0 ^ w.sb, a0 ^ w.sa ^ w.sb);
   }
 }
@@ -304,19 +310,25 @@ __device__ __forceinline__ void for_quads(const Sweep& w, F f) {
 template <class F>
 __device__ __forceinline__ void for_pairs(const Sweep& w, F f) {
   for (int j = threadIdx.x; j < w.n_items; j += kPassThreads) {
-    const int a0 = swz(ins0(j, w.plo));
+    const int b = ins0(j, w.plo);
+    const int la = (__popc(b & w.ra) ^ w.ga) & 1;
+    const int a0 = swz(b) ^ (la ? w.sa : 0);
     f(a0, a0 ^ w.sa);
   }
 }
 
 __device__ __forceinline__ void apply_gate(double2* __restrict__ tile, int k, const GateDesc& d,
-                                           const double2* __restrict__ m) {
+                                           const double2* __restrict__ m, uint64_t tile_base) {
   Sweep w;
   w.tile = tile;
   w.plo = d.plo;
   w.phi = d.phi;
   w.sa = swz(d.ma);
   w.sb = swz(d.mb);
+  w.ra = d.ra;
+  w.rb = d.rb;
+  w.ga = __popcll(tile_base & d.ra_out);
+  w.gb = __popcll(tile_base & d.rb_out);
   if (d.nq == 1) {
     w.n_items = 1 << (k - 1);
     if (d.cls == kDiag1) {
@@ -479,15 +491,15 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
     const int g_begin = sp.gate_begin, g_end = sp.gate_end;
     double msum = 0.0;
 
-    auto tile_base = [&](uint64_t t) {
-      uint64_t base = lo;
+    auto tile_base = [&](uint64_t t) {  // physical index bits of tile t (no tile-local bits)
+      uint64_t base = 0;
       for (int b = 0; b < n_out; ++b)
         if (t >> b & 1) base |= uint64_t(1) << sp.oq[b];
       return base;
     };
     auto issue_load = [&](uint64_t t, double2* buf) {
       if (!loader) return;
-      const uint64_t base = tile_base(t);
+      const uint64_t base = tile_base(t) | lo;
       for (int j = 0; j < n_j; ++j) cp_async16(buf + swz(tid + (j << 8)), p.amps + (base | s_hi[j]));
     };
 
@@ -502,7 +514,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
       cp_async_commit();
       cp_async_wait<1>();  // this tile's group has landed (next may be in flight)
       __syncthreads();
-      const uint64_t base = tile_base(t);
+      const uint64_t tbase = tile_base(t);
+      const uint64_t base = tbase | lo;
       if (sp.collapse_q >= 0) {  // pending collapse (engine.py:164-167)
         const int cq = sp.collapse_q;
         if (loader)
@@ -520,7 +533,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
       }
       for (int g = g_begin; g < g_end; ++g) {
         const GateDesc d = p.gates[g];
-        apply_gate(tile, k, d, p.mats + d.mat);
+        apply_gate(tile, k, d, p.mats + d.mat, tbase);
         __syncthreads();
       }
       // shared -> global (+ assertion epilogue partial sums)

@@ -158,9 +158,14 @@ void swap_slots(double* m) {
 // no earlier skipped gate shares a qubit with it; skipped gates keep their
 // relative order and are retried first by the next group.  Scanning stops
 // after `lookahead` gates or once nothing else can join.
+//
+// `masks` are the qubits a gate needs inside the group; `deps` (optional,
+// defaults to `masks`) are all qubits it reads or writes -- a relabeled gate
+// also reads the bits of its dual rows -- and decide ordering conflicts.
 std::vector<std::vector<int>> pack_groups(const std::vector<uint64_t>& masks, int cap,
                                           uint64_t base, uint64_t all, int lookahead,
-                                          std::vector<uint64_t>& sets) {
+                                          std::vector<uint64_t>& sets,
+                                          const std::vector<uint64_t>* deps = nullptr) {
   std::vector<std::vector<int>> groups;
   std::vector<int> pending, still;
   size_t cursor = 0;
@@ -173,11 +178,12 @@ std::vector<std::vector<int>> pack_groups(const std::vector<uint64_t>& masks, in
     bool stop = false;
     auto visit = [&](int g) {
       const uint64_t m = masks[g];
-      if (!stop && !(m & blocked) && popc(set | m) <= cap) {
+      const uint64_t dm = deps ? (*deps)[g] : m;
+      if (!stop && !(dm & blocked) && popc(set | m) <= cap) {
         set |= m;
         grp.push_back(g);
       } else {
-        blocked |= m;
+        blocked |= dm;
         still.push_back(g);
       }
       ++scanned;
@@ -233,7 +239,8 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
   PoolBuilder pb{matrices, {}};
   std::vector<PhysGate> run;
   uint64_t col[64];  // frame: physical mask of logical bit j (M e_j)
-  for (int j = 0; j < 64; ++j) col[j] = uint64_t(1) << j;
+  uint64_t row[64];  // inverse frame: logical bit j = parity(p & row[j]) (M^-1)
+  for (int j = 0; j < 64; ++j) col[j] = row[j] = uint64_t(1) << j;
   std::vector<double> packed;
   int step = 0;
 
@@ -241,8 +248,8 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
     PhysGate g{};
     g.cls = kCX01;
     g.nq = 2;
-    g.ma = uint64_t(1) << c;
-    g.mb = uint64_t(1) << t;
+    g.ma = g.ra = uint64_t(1) << c;
+    g.mb = g.rb = uint64_t(1) << t;
     g.mat = 0;
     run.push_back(g);
     ++n_flush_gates;
@@ -272,7 +279,7 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
         }
     }
     for (size_t i = ops_rec.size(); i-- > 0;) emit_cx(ops_rec[i].first, ops_rec[i].second);
-    for (int j = 0; j < 64; ++j) col[j] = uint64_t(1) << j;
+    for (int j = 0; j < 64; ++j) col[j] = row[j] = uint64_t(1) << j;
   };
   auto flush_run = [&]() {
     flush_frame();
@@ -328,18 +335,23 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
     g.cls = pack_matrix(mat.v, o.nq, packed, g.cols);
     class_count[g.cls]++;
     const int a = o.q[0], b = o.nq == 2 ? o.q[1] : -1;
-    if (g.cls == kCX01) {  // logical CX(a -> b): M <- M CX  (column a += column b)
+    // logical CX(c -> t): M <- M C, i.e. column c += column t and, for
+    // M^-1 <- C M^-1, row t += row c
+    if (g.cls == kCX01) {
       col[a] ^= col[b];
+      row[b] ^= row[a];
       ++n_frame_gates;
       continue;
     }
     if (g.cls == kCX10) {
       col[b] ^= col[a];
+      row[a] ^= row[b];
       ++n_frame_gates;
       continue;
     }
     if (g.cls == kSwap) {
       std::swap(col[a], col[b]);
+      std::swap(row[a], row[b]);
       ++n_frame_gates;
       continue;
     }
@@ -349,6 +361,8 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
     }
     g.ma = col[a];
     g.mb = o.nq == 2 ? col[b] : 0;
+    g.ra = row[a];
+    g.rb = o.nq == 2 ? row[b] : 0;
     g.mat = pb.add(packed.data(), static_cast<int>(packed.size() / 2));
     static const int kNnz[kNumClasses] = {4, 2, 16, 8, 4, 4, 0, 0, 8, 8, 8, 0};
     flops += 8ll * kNnz[g.cls] * (int64_t(1) << (n - g.nq));
@@ -363,13 +377,14 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
   const int n = n_qubits;
   const uint64_t all = (n == 64) ? ~uint64_t(0) : ((uint64_t(1) << n) - 1);
   const uint64_t low = (uint64_t(1) << std::min(kLowQubits, n)) - 1;
-  std::vector<uint64_t> masks(run.size());
+  std::vector<uint64_t> masks(run.size()), deps(run.size());
   for (size_t i = 0; i < run.size(); ++i) {
     masks[i] = run[i].ma | run[i].mb;
+    deps[i] = masks[i] | run[i].ra | run[i].rb;
     if (popc(masks[i] | low) > k) throw std::logic_error("gate support exceeds the tile");
   }
   std::vector<uint64_t> sets;
-  auto pass_groups = pack_groups(masks, k, low, all, 2048, sets);
+  auto pass_groups = pack_groups(masks, k, low, all, 2048, sets, &deps);
   for (size_t pi = 0; pi < pass_groups.size(); ++pi) {
     uint64_t tset = sets[pi];
     for (int q = 0; q < n && popc(tset) < k; ++q) tset |= uint64_t(1) << q;
@@ -395,6 +410,10 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
       const uint32_t ma = pext64(g.ma, tset), mb = pext64(g.mb, tset);
       d.ma = static_cast<uint16_t>(ma);
       d.mb = static_cast<uint16_t>(mb);
+      d.ra = static_cast<uint16_t>(pext64(g.ra, tset));
+      d.rb = static_cast<uint16_t>(pext64(g.rb, tset));
+      d.ra_out = g.ra & ~tset;
+      d.rb_out = g.rb & ~tset;
       const int pa = lowest_bit(ma);
       if (g.nq == 1) {
         d.plo = d.phi = static_cast<uint8_t>(pa);
@@ -524,3 +543,65 @@ extern "C" int nsb_plan_analyze(const nsb_op* ops, int64_t n_ops, const double* 
   return NSB_OK;
 }
 
+
+extern "C" int nsb_host_plan_build(const nsb_op* ops, int64_t n_ops, const double* params,
+                                   const double* payloads, int32_t n_qubits, int32_t workers,
+                                   void** out, nsb_status* st) {
+  if (!out || (n_ops > 0 && !ops) || workers < 1) {
+    nsb::set_status(st, NSB_EINVAL, "bad arguments");
+    return NSB_EINVAL;
+  }
+  *out = nullptr;
+  try {
+    auto* H = new nsb::HostPlan();
+    try {
+      H->build(ops, n_ops, params, payloads, n_qubits, workers);
+    } catch (...) {
+      delete H;
+      throw;
+    }
+    for (const nsb::Item& it : H->items) {
+      const int kind = it.kind == nsb::Item::kGates ? 0
+                       : it.kind == nsb::Item::kMeasure ? 1
+                       : it.kind == nsb::Item::kReset ? 2 : 3;
+      H->items_flat.push_back(kind);
+      H->items_flat.push_back(kind == 0 ? it.pass_begin : it.qubit);
+      H->items_flat.push_back(kind == 0 ? it.pass_end : it.step);
+      H->items_flat.push_back(it.k);
+    }
+    *out = H;
+  } catch (const std::bad_alloc&) {
+    nsb::set_status(st, NSB_ERESOURCE, "host out of memory in planner");
+    return NSB_ERESOURCE;
+  } catch (const std::exception& e) {
+    nsb::set_status(st, NSB_EINVAL, e.what());
+    return NSB_EINVAL;
+  }
+  nsb::set_status(st, NSB_OK, "");
+  return NSB_OK;
+}
+
+extern "C" int nsb_host_plan_view(const void* plan, nsb_plan_view* v) {
+  if (!plan || !v) return NSB_EINVAL;
+  const auto* H = static_cast<const nsb::HostPlan*>(plan);
+  std::memset(v, 0, sizeof(*v));
+  v->n_qubits = H->n_qubits;
+  v->tile_qubits = H->tile_qubits;
+  v->mma_ok = H->mma_ok;
+  v->n_measures = static_cast<int32_t>(H->n_measures);
+  v->pass_desc_bytes = sizeof(nsb::PassDesc);
+  v->gate_desc_bytes = sizeof(nsb::GateDesc);
+  v->n_passes = static_cast<int64_t>(H->passes.size());
+  v->n_mma_passes = static_cast<int64_t>(H->mma_passes.size());
+  v->n_gate_descs = static_cast<int64_t>(H->gates.size());
+  v->n_matrices = static_cast<int64_t>(H->matrices.size() / 2);
+  v->n_items = static_cast<int64_t>(H->items.size());
+  v->passes = H->passes.data();
+  v->mma_passes = H->mma_passes.data();
+  v->gates = H->gates.data();
+  v->matrices = H->matrices.data();
+  v->items = H->items_flat.data();
+  return NSB_OK;
+}
+
+extern "C" void nsb_host_plan_free(void* plan) { delete static_cast<nsb::HostPlan*>(plan); }

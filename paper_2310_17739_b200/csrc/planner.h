@@ -50,14 +50,21 @@ enum GateClass : uint8_t {
   kNumClasses = 12
 };
 
-struct GateDesc {     // 16 bytes
+// A gate on logical qubits (a, b) acts on physical cosets of span{ma, mb}
+// (ma = M e_a, mb = M e_b).  The coset member whose LOGICAL bits a, b are
+// zero is found with the dual rows ra, rb of M^-1 (logical bit a of physical
+// index p = parity(p & ra)); the tile-local and out-of-tile parts of the rows
+// are stored separately so the out-of-tile parity is one popcount per tile.
+struct GateDesc {     // 40 bytes
   int32_t mat;        // offset (complex elements) into the matrix pool
   uint8_t cls;        // GateClass
   uint8_t plo, phi;   // pivot bits (ascending) removed from the quad/pair index
   uint8_t nq;         // 1 or 2
   uint16_t ma, mb;    // tile-local XOR masks of slot 0 / slot 1
+  uint16_t ra, rb;    // tile-local parts of the dual rows
   uint16_t cols;      // kSparse2 / kMono2: 2-bit column codes
   uint16_t pad;
+  uint64_t ra_out, rb_out;  // out-of-tile parts of the dual rows (physical bits)
 };
 
 struct PassDesc {

@@ -47,6 +47,7 @@ struct PhysGate {
   uint8_t cls = 0;
   int nq = 0;
   uint64_t ma = 0, mb = 0;  // physical XOR masks of slot 0 / slot 1
+  uint64_t ra = 0, rb = 0;  // dual rows: logical slot bits as physical parities
   int32_t mat = 0;          // packed payload offset in the pool
   uint16_t cols = 0;
 };
@@ -77,6 +78,7 @@ struct HostPlan {
   std::vector<GateDesc> gates;
   std::vector<double> matrices;      // packed, deduplicated payload pool
   std::vector<double> dense_mats;    // k-qubit / unblocked matrices (full)
+  std::vector<int32_t> items_flat;   // nsb_host_plan_view export
 
   // workers: persistent CTAs of the pass kernel (tile-size choice)
   void build(const nsb_op* ops, int64_t n_ops, const double* params, const double* payloads,

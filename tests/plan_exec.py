@@ -1,0 +1,170 @@
+"""Host executor of an exported device plan (test infrastructure).
+
+Runs the PassDesc / GateDesc program that nsb_plan_create would upload
+(exported by nsb_host_plan_view) with numpy, following the kernel's
+semantics in csrc/device.cu line by line except the shared-memory swizzle,
+which is a storage detail.  Lets the CPU suite verify the planner -- the
+relabeling frame, pivots, dual rows, pass tiling, measurement epilogues --
+against the oracle without a GPU.  Small qubit counts only.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from paper_2310_17739_b200 import _native as N
+
+PASS_DT = np.dtype([("gate_begin", "<i4"), ("gate_end", "<i4"), ("k", "<i4"),
+                    ("measure_q", "<i4"), ("measure_slot", "<i4"), ("collapse_q", "<i4"),
+                    ("collapse_slot", "<i4"), ("pad", "<i4"), ("tq", "i1", (16,)),
+                    ("oq", "i1", (48,))])
+GATE_DT = np.dtype([("mat", "<i4"), ("cls", "u1"), ("plo", "u1"), ("phi", "u1"), ("nq", "u1"),
+                    ("ma", "<u2"), ("mb", "<u2"), ("ra", "<u2"), ("rb", "<u2"),
+                    ("cols", "<u2"), ("pad", "<u2"), ("ra_out", "<u8"), ("rb_out", "<u8")],
+                   align=True)
+(DENSE1, DIAG1, DENSE2, SPARSE2, MONO2, DIAG2, CX01, CX10, PAIRQ, PAIRP, PAIRX, SWAP) = range(12)
+
+
+class HostPlan:
+    def __init__(self, ops, params, payloads, n, workers=148):
+        h = ctypes.c_void_p()
+        st = N.Status()
+        N.check(N.lib().nsb_host_plan_build(N.ptr(ops), len(ops), N.ptr(params),
+                                            N.ptr(payloads.view(np.float64)), n, workers,
+                                            ctypes.byref(h), ctypes.byref(st)), st)
+        self.h = h
+        v = N.PlanView()
+        N.lib().nsb_host_plan_view(h, ctypes.byref(v))
+        assert v.pass_desc_bytes == PASS_DT.itemsize and v.gate_desc_bytes == GATE_DT.itemsize
+        self.n, self.k, self.mma_ok, self.n_measures = v.n_qubits, v.tile_qubits, v.mma_ok, v.n_measures
+
+        def arr(p, count, dt):
+            if count == 0:
+                return np.zeros(0, dt)
+            raw = (ctypes.c_uint8 * (count * dt.itemsize)).from_address(p)
+            return np.frombuffer(bytes(raw), dtype=dt)
+
+        self.passes = arr(v.passes, v.n_passes, PASS_DT)
+        self.mma_passes = arr(v.mma_passes, v.n_mma_passes, PASS_DT)
+        self.gates = arr(v.gates, v.n_gate_descs, GATE_DT)
+        self.mats = arr(v.matrices, v.n_matrices, np.dtype(np.complex128))
+        self.items = arr(v.items, 4 * v.n_items, np.dtype(np.int32)).reshape(-1, 4)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            N.lib().nsb_host_plan_free(self.h)
+            self.h = None
+
+
+def _scatter(values: np.ndarray, bits) -> np.ndarray:
+    out = np.zeros_like(values)
+    for j, b in enumerate(bits):
+        out |= ((values >> j) & 1) << int(b)
+    return out
+
+
+def _ins0(j, pos):
+    return ((j >> pos) << (pos + 1)) | (j & ((1 << pos) - 1))
+
+
+def _parity(x):
+    x = np.asarray(x, dtype=np.uint64)
+    p = np.zeros(x.shape, np.uint64)
+    while np.any(x):
+        p ^= x & np.uint64(1)
+        x = x >> np.uint64(1)
+    return p.astype(np.int64)
+
+
+def _mix2(x, y, m):
+    return m[0] * x + m[1] * y, m[2] * x + m[3] * y
+
+
+def _apply(T, g, mats, tbases, k):
+    """One gate sweep on all tiles T (tiles x 2^k), as k_blocked's apply_gate."""
+    m = mats[int(g["mat"]):]
+    ga = _parity(tbases & np.uint64(g["ra_out"]))[:, None]
+    gb = _parity(tbases & np.uint64(g["rb_out"]))[:, None]
+    ma, mb = int(g["ma"]), int(g["mb"])
+    if g["nq"] == 1:
+        j = np.arange(1 << (k - 1), dtype=np.int64)
+        b = _ins0(j, int(g["plo"]))[None, :]
+        la = (_parity(b & int(g["ra"])) ^ ga) & 1
+        i0 = b ^ (la * ma)
+        i1 = i0 ^ ma
+        r = np.arange(T.shape[0])[:, None]
+        x, y = T[r, i0], T[r, i1]
+        if g["cls"] == DIAG1:
+            x, y = m[0] * x, m[1] * y
+        else:
+            x, y = _mix2(x, y, m[:4])
+        T[r, i0], T[r, i1] = x, y
+        return
+    j = np.arange(1 << (k - 2), dtype=np.int64)
+    b = _ins0(_ins0(j, int(g["plo"])), int(g["phi"]))[None, :]
+    la = (_parity(b & int(g["ra"])) ^ ga) & 1
+    lb = (_parity(b & int(g["rb"])) ^ gb) & 1
+    i0 = b ^ (la * ma) ^ (lb * mb)
+    idx = [i0, i0 ^ ma, i0 ^ mb, i0 ^ ma ^ mb]
+    r = np.arange(T.shape[0])[:, None]
+    x = [T[r, i] for i in idx]
+    c = int(g["cls"])
+    out = list(x)
+    if c in (CX01, CX10, SWAP):
+        s, t = {CX01: (1, 3), CX10: (2, 3), SWAP: (1, 2)}[c]
+        out[s], out[t] = x[t], x[s]
+    elif c in (PAIRQ, PAIRP, PAIRX):
+        (u0, u1), (u2, u3) = {PAIRQ: ((0, 2), (1, 3)), PAIRP: ((0, 1), (2, 3)),
+                              PAIRX: ((0, 3), (1, 2))}[c]
+        out[u0], out[u1] = _mix2(x[u0], x[u1], m[:4])
+        out[u2], out[u3] = _mix2(x[u2], x[u3], m[4:8])
+    elif c == DIAG2:
+        out = [m[s] * x[s] for s in range(4)]
+    elif c == MONO2:
+        cols = int(g["cols"])
+        out = [m[s] * x[(cols >> (2 * s)) & 3] for s in range(4)]
+    elif c == SPARSE2:
+        cols = int(g["cols"])
+        out = [m[2 * s] * x[(cols >> (4 * s)) & 3] + m[2 * s + 1] * x[(cols >> (4 * s + 2)) & 3]
+               for s in range(4)]
+    else:
+        out = [sum(m[4 * s + t] * x[t] for t in range(4)) for s in range(4)]
+    for i, v in zip(idx, out):
+        T[r, i] = v
+
+
+def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12):
+    """Execute a pass list on `state` in place; returns {step: p0} and the carry."""
+    n = plan.n
+    rec = {}
+    for P in passes:
+        k = int(P["k"])
+        lidx = _scatter(np.arange(1 << k, dtype=np.int64), P["tq"][:k])
+        tb = _scatter(np.arange(1 << (n - k), dtype=np.int64), P["oq"][:n - k])
+        idx = tb[:, None] | lidx[None, :]
+        T = state[idx]
+        cq = int(P["collapse_q"])
+        if cq >= 0:
+            scale = 1.0 / np.sqrt(carry_p0)
+            T = np.where((idx >> cq) & 1, 0.0, T * scale)
+        for g in plan.gates[int(P["gate_begin"]):int(P["gate_end"])]:
+            _apply(T, g, plan.mats, tb.astype(np.uint64), k)
+        state[idx] = T
+        mq = int(P["measure_q"])
+        if mq >= 0:
+            keep = ((np.arange(state.size) >> mq) & 1) == 0
+            carry_p0 = float(np.sum(np.abs(state[keep]) ** 2))
+            rec[int(P["measure_slot"])] = carry_p0
+            if carry_p0 < eps:
+                break
+    return rec, carry_p0
+
+
+def run_mma(plan: HostPlan, eps=1e-12):
+    assert plan.mma_ok
+    state = np.zeros(1 << plan.n, np.complex128)
+    state[0] = 1.0
+    rec, _ = run_passes(plan, plan.mma_passes, state, eps=eps)
+    return [rec[s] for s in sorted(rec)], state

@@ -1,0 +1,69 @@
+"""Planner verification on the CPU: the exported device program (relabeling
+frame, pivots, dual rows, pass tiling, measurement epilogues) executed by
+tests/plan_exec.py must reproduce the oracle's final state and assertion
+probabilities.  The GPU tests then check that k_blocked executes the same
+program faithfully."""
+
+import numpy as np
+import pytest
+
+import nucsim_oracle as O
+import plan_exec as PE
+from circuit_io import oracle_from_circuit, to_circuit
+from paper_2310_17739_b200 import fuse_pipeline
+from paper_2310_17739_b200._pack import pack
+from test_engine_gpu import ladder_circuit, random_filter_like
+
+
+def executable(c):
+    end = len(c.instructions)
+    while end and c.instructions[end - 1].gate.value in ("measure", "barrier"):
+        end -= 1
+    return pack(c, c.instructions[:end])
+
+
+def check(c, workers=148):
+    n = c.n_qubits
+    pk = executable(c)
+    plan = PE.HostPlan(pk.ops, pk.params, pk.payloads, n, workers)
+    try:
+        want_p, _, want_state, _ = O.run_mma(oracle_from_circuit(c), n, 1, 0)
+    except O.OracleAssertion:
+        pytest.skip("dead assertion branch")
+    probs, state = PE.run_mma(plan)
+    assert probs == pytest.approx(want_p, abs=1e-12)
+    err = np.linalg.norm(state - want_state) / np.linalg.norm(want_state)
+    assert err < 1e-10, err
+    return plan
+
+
+@pytest.mark.parametrize("n", [6, 8, 11, 13])
+def test_random_filter_like(n):
+    rng = np.random.default_rng(1000 + n)
+    c = random_filter_like(rng, n, blocks=3, per_block=50)
+    check(c)
+    check(fuse_pipeline(c)[0])
+
+
+@pytest.mark.parametrize("n,terms", [(7, 30), (10, 30), (13, 25)])
+def test_ladders_through_the_frame(n, terms):
+    rng = np.random.default_rng(50 + n)
+    c = ladder_circuit(rng, n, terms)
+    for circ in (c, fuse_pipeline(c)[0]):
+        plan = check(circ)
+        info_frame = int(np.sum(plan.gates["cls"] == PE.CX01))
+        assert info_frame >= 0
+
+
+@pytest.mark.parametrize("workers", [1, 3, 148])
+def test_small_tiles_multi_pass(workers):
+    """n = 14 > 12 forces several tiles and multiple passes per run."""
+    rng = np.random.default_rng(7)
+    c = ladder_circuit(rng, 14, 12, blocks=2)
+    check(fuse_pipeline(c)[0], workers)
+
+
+def test_golden_filter8_plan(golden):
+    d = golden("filter8")
+    for pre in ("fused_", "in_"):
+        check(to_circuit(d, pre))
