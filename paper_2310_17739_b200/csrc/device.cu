@@ -332,13 +332,13 @@ __device__ __forceinline__ void apply_gate(double2* __restrict__ tile, int k, co
   if (d.nq == 1) {
     w.n_items = 1 << (k - 1);
     if (d.cls == kDiag1) {
-      const double2 d0 = __ldg(m), d1 = __ldg(m + 1);
+      const double2 d0 = *(m), d1 = *(m + 1);
       for_pairs(w, [&](int i0, int i1) {
         tile[i0] = cmul(d0, tile[i0]);
         tile[i1] = cmul(d1, tile[i1]);
       });
     } else {
-      const double2 m0 = __ldg(m), m1 = __ldg(m + 1), m2 = __ldg(m + 2), m3 = __ldg(m + 3);
+      const double2 m0 = *(m), m1 = *(m + 1), m2 = *(m + 2), m3 = *(m + 3);
       for_pairs(w, [&](int i0, int i1) {
         double2 x = tile[i0], y = tile[i1];
         mix2(x, y, m0, m1, m2, m3);
@@ -368,8 +368,8 @@ __device__ __forceinline__ void apply_gate(double2* __restrict__ tile, int k, co
     case kPairQ:
     case kPairP:
     case kPairX: {
-      const double2 m0 = __ldg(m), m1 = __ldg(m + 1), m2 = __ldg(m + 2), m3 = __ldg(m + 3);
-      const double2 n0 = __ldg(m + 4), n1 = __ldg(m + 5), n2 = __ldg(m + 6), n3 = __ldg(m + 7);
+      const double2 m0 = *(m), m1 = *(m + 1), m2 = *(m + 2), m3 = *(m + 3);
+      const double2 n0 = *(m + 4), n1 = *(m + 5), n2 = *(m + 6), n3 = *(m + 7);
       const int cls = d.cls;
       for_quads(w, [&](int i0, int i1, int i2, int i3) {
         // block 0 on members (u0,u1), block 1 on (u2,u3)
@@ -388,7 +388,7 @@ __device__ __forceinline__ void apply_gate(double2* __restrict__ tile, int k, co
       break;
     }
     case kDiag2: {
-      const double2 d0 = __ldg(m), d1 = __ldg(m + 1), d2 = __ldg(m + 2), d3 = __ldg(m + 3);
+      const double2 d0 = *(m), d1 = *(m + 1), d2 = *(m + 2), d3 = *(m + 3);
       for_quads(w, [&](int i0, int i1, int i2, int i3) {
         tile[i0] = cmul(d0, tile[i0]);
         tile[i1] = cmul(d1, tile[i1]);
@@ -398,7 +398,7 @@ __device__ __forceinline__ void apply_gate(double2* __restrict__ tile, int k, co
       break;
     }
     case kMono2: {
-      const double2 v0 = __ldg(m), v1 = __ldg(m + 1), v2 = __ldg(m + 2), v3 = __ldg(m + 3);
+      const double2 v0 = *(m), v1 = *(m + 1), v2 = *(m + 2), v3 = *(m + 3);
       const int c0 = d.cols & 3, c1 = (d.cols >> 2) & 3, c2 = (d.cols >> 4) & 3,
                 c3 = (d.cols >> 6) & 3;
       for_quads(w, [&](int i0, int i1, int i2, int i3) {
@@ -418,8 +418,8 @@ __device__ __forceinline__ void apply_gate(double2* __restrict__ tile, int k, co
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           double2 o = make_double2(0.0, 0.0);
-          cmac(o, __ldg(m + 2 * r), pick(x0, x1, x2, x3, (cols >> (4 * r)) & 3));
-          cmac(o, __ldg(m + 2 * r + 1), pick(x0, x1, x2, x3, (cols >> (4 * r + 2)) & 3));
+          cmac(o, *(m + 2 * r), pick(x0, x1, x2, x3, (cols >> (4 * r)) & 3));
+          cmac(o, *(m + 2 * r + 1), pick(x0, x1, x2, x3, (cols >> (4 * r + 2)) & 3));
           tile[idx[r]] = o;
         }
       });
@@ -432,10 +432,10 @@ __device__ __forceinline__ void apply_gate(double2* __restrict__ tile, int k, co
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           double2 o = make_double2(0.0, 0.0);
-          cmac(o, __ldg(m + 4 * r + 0), x0);
-          cmac(o, __ldg(m + 4 * r + 1), x1);
-          cmac(o, __ldg(m + 4 * r + 2), x2);
-          cmac(o, __ldg(m + 4 * r + 3), x3);
+          cmac(o, *(m + 4 * r + 0), x0);
+          cmac(o, *(m + 4 * r + 1), x1);
+          cmac(o, *(m + 4 * r + 2), x2);
+          cmac(o, *(m + 4 * r + 3), x3);
           tile[idx[r]] = o;
         }
       });
@@ -456,8 +456,14 @@ __device__ __forceinline__ void cp_async_wait() {
 
 // One persistent CTA per SM; while the gate sweeps of tile i run, tile i+1 of
 // the same pass streams into the other shared-memory buffer with cp.async.
+constexpr size_t kBlockedSmemBytes = sizeof(double2) * (2 * kTileAmpsMax + kMaxPassMats) +
+                                     sizeof(GateDesc) * kMaxPassGates;
+
 __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
-  extern __shared__ __align__(128) double2 smem[];  // 2 x kTileAmpsMax
+  // dynamic shared memory: 2 tile buffers | pass matrices | pass gate descriptors
+  extern __shared__ __align__(128) double2 smem[];
+  double2* s_mats = smem + 2 * kTileAmpsMax;
+  GateDesc* s_gates = reinterpret_cast<GateDesc*>(s_mats + kMaxPassMats);
   __shared__ PassDesc sp;
   __shared__ uint64_t s_hi[16];  // global offset of tile-local bits 8..11 for j = 0..15
   __shared__ double red[32];
@@ -472,6 +478,14 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
       reinterpret_cast<int*>(&sp)[tid] = reinterpret_cast<const int*>(p.passes + pi)[tid];
     __syncthreads();
     const int k = sp.k;
+    {  // stage the pass's gates and matrices (the previous pass is done with them)
+      const int n_mat = sp.mat_count;
+      for (int i = tid; i < n_mat; i += kPassThreads) s_mats[i] = p.mats[sp.mat_begin + i];
+      const int n_words = (sp.gate_end - sp.gate_begin) * int(sizeof(GateDesc) / 8);
+      const uint64_t* src = reinterpret_cast<const uint64_t*>(p.gates + sp.gate_begin);
+      uint64_t* dst = reinterpret_cast<uint64_t*>(s_gates);
+      for (int i = tid; i < n_words; i += kPassThreads) dst[i] = src[i];
+    }
     if (tid < 16) {
       uint64_t h = 0;
       for (int b = 0; b < 4; ++b)
@@ -488,7 +502,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
     const int n_j = k > 8 ? 1 << (k - 8) : 1;
     const bool loader = tid < (1 << lo_bits);
     const double cscale = sp.collapse_q >= 0 ? 1.0 / sqrt(carry_p0) : 1.0;
-    const int g_begin = sp.gate_begin, g_end = sp.gate_end;
+    const int n_gates = sp.gate_end - sp.gate_begin;
     double msum = 0.0;
 
     auto tile_base = [&](uint64_t t) {  // physical index bits of tile t (no tile-local bits)
@@ -531,9 +545,9 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
           }
         __syncthreads();
       }
-      for (int g = g_begin; g < g_end; ++g) {
-        const GateDesc d = p.gates[g];
-        apply_gate(tile, k, d, p.mats + d.mat, tbase);
+      for (int g = 0; g < n_gates; ++g) {
+        const GateDesc d = s_gates[g];
+        apply_gate(tile, k, d, s_mats + d.mat, tbase);
         __syncthreads();
       }
       // shared -> global (+ assertion epilogue partial sums)
@@ -788,7 +802,7 @@ void launch_blocked(nsb_ctx* c, nsb_plan* P, const PassDesc* passes, int pb, int
   void* args[] = {&bp};
   NSB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::k_blocked),
                                        dim3(c->blocked_grid), dim3(kPassThreads), args,
-                                       2 * sizeof(double2) * kTileAmpsMax, c->stream));
+                                       dev::kBlockedSmemBytes, c->stream));
   P->last_launches += 1;
 }
 
@@ -827,7 +841,7 @@ int nsb_ctx_create(int32_t device, nsb_ctx** out, nsb_status* st) {
     NSB_CUDA(cudaEventCreate(&ctx->ev0));
     NSB_CUDA(cudaEventCreate(&ctx->ev1));
     NSB_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
-    const int smem = 2 * sizeof(double2) * kTileAmpsMax;
+    const int smem = static_cast<int>(dev::kBlockedSmemBytes);
     NSB_CUDA(cudaFuncSetAttribute(dev::k_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   smem));
     int per_sm = 0;

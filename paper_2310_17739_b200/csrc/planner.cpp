@@ -165,7 +165,9 @@ void swap_slots(double* m) {
 std::vector<std::vector<int>> pack_groups(const std::vector<uint64_t>& masks, int cap,
                                           uint64_t base, uint64_t all, int lookahead,
                                           std::vector<uint64_t>& sets,
-                                          const std::vector<uint64_t>* deps = nullptr) {
+                                          const std::vector<uint64_t>* deps = nullptr,
+                                          const std::vector<int>* weights = nullptr,
+                                          int max_count = 1 << 30, int max_weight = 1 << 30) {
   std::vector<std::vector<int>> groups;
   std::vector<int> pending, still;
   size_t cursor = 0;
@@ -173,14 +175,17 @@ std::vector<std::vector<int>> pack_groups(const std::vector<uint64_t>& masks, in
   while (!pending.empty() || cursor < total) {
     uint64_t set = base, blocked = 0;
     std::vector<int> grp;
-    int scanned = 0;
+    int scanned = 0, weight = 0;
     still.clear();
     bool stop = false;
     auto visit = [&](int g) {
       const uint64_t m = masks[g];
       const uint64_t dm = deps ? (*deps)[g] : m;
-      if (!stop && !(dm & blocked) && popc(set | m) <= cap) {
+      const int wg = weights ? (*weights)[g] : 0;
+      if (!stop && !(dm & blocked) && popc(set | m) <= cap &&
+          static_cast<int>(grp.size()) < max_count && weight + wg <= max_weight) {
         set |= m;
+        weight += wg;
         grp.push_back(g);
       } else {
         blocked |= dm;
@@ -188,7 +193,8 @@ std::vector<std::vector<int>> pack_groups(const std::vector<uint64_t>& masks, in
       }
       ++scanned;
       if (scanned >= lookahead || (blocked & all) == all ||
-          (popc(set) >= cap && (set & ~blocked) == 0))
+          (popc(set) >= cap && (set & ~blocked) == 0) ||
+          static_cast<int>(grp.size()) >= max_count)
         stop = true;
     };
     for (int g : pending) visit(g);
@@ -236,7 +242,6 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
   const int k = choose_tile_qubits(n, workers);
   tile_qubits = k;
   blocked = n >= 6;
-  PoolBuilder pb{matrices, {}};
   std::vector<PhysGate> run;
   uint64_t col[64];  // frame: physical mask of logical bit j (M e_j)
   uint64_t row[64];  // inverse frame: logical bit j = parity(p & row[j]) (M^-1)
@@ -251,6 +256,7 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
     g.ma = g.ra = uint64_t(1) << c;
     g.mb = g.rb = uint64_t(1) << t;
     g.mat = 0;
+    g.n_mat = 0;
     run.push_back(g);
     ++n_flush_gates;
   };
@@ -291,6 +297,7 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
     it.pass_end = static_cast<int32_t>(passes.size());
     items.push_back(it);
     run.clear();
+    packed_all.clear();
   };
 
   for (int64_t i = 0; i < n_ops; ++i) {
@@ -363,7 +370,9 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
     g.mb = o.nq == 2 ? col[b] : 0;
     g.ra = row[a];
     g.rb = o.nq == 2 ? row[b] : 0;
-    g.mat = pb.add(packed.data(), static_cast<int>(packed.size() / 2));
+    g.mat = static_cast<int32_t>(packed_all.size() / 2);
+    g.n_mat = static_cast<int32_t>(packed.size() / 2);
+    packed_all.insert(packed_all.end(), packed.begin(), packed.end());
     static const int kNnz[kNumClasses] = {4, 2, 16, 8, 4, 4, 0, 0, 8, 8, 8, 0};
     flops += 8ll * kNnz[g.cls] * (int64_t(1) << (n - g.nq));
     run.push_back(g);
@@ -378,13 +387,16 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
   const uint64_t all = (n == 64) ? ~uint64_t(0) : ((uint64_t(1) << n) - 1);
   const uint64_t low = (uint64_t(1) << std::min(kLowQubits, n)) - 1;
   std::vector<uint64_t> masks(run.size()), deps(run.size());
+  std::vector<int> weights(run.size());
   for (size_t i = 0; i < run.size(); ++i) {
     masks[i] = run[i].ma | run[i].mb;
     deps[i] = masks[i] | run[i].ra | run[i].rb;
+    weights[i] = run[i].n_mat;
     if (popc(masks[i] | low) > k) throw std::logic_error("gate support exceeds the tile");
   }
   std::vector<uint64_t> sets;
-  auto pass_groups = pack_groups(masks, k, low, all, 2048, sets, &deps);
+  auto pass_groups = pack_groups(masks, k, low, all, 2048, sets, &deps, &weights, kMaxPassGates,
+                                 kMaxPassMats);
   for (size_t pi = 0; pi < pass_groups.size(); ++pi) {
     uint64_t tset = sets[pi];
     for (int q = 0; q < n && popc(tset) < k; ++q) tset |= uint64_t(1) << q;
@@ -400,10 +412,13 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
         P.oq[o++] = static_cast<int8_t>(q);
     }
     P.gate_begin = static_cast<int32_t>(gates.size());
+    P.mat_begin = static_cast<int32_t>(matrices.size() / 2);
     for (int gi : pass_groups[pi]) {
       const PhysGate& g = run[gi];
       GateDesc d{};
-      d.mat = g.mat;
+      d.mat = static_cast<int32_t>(matrices.size() / 2) - P.mat_begin;
+      matrices.insert(matrices.end(), packed_all.begin() + 2 * g.mat,
+                      packed_all.begin() + 2 * (g.mat + g.n_mat));
       d.cls = g.cls;
       d.nq = static_cast<uint8_t>(g.nq);
       d.cols = g.cols;
@@ -427,6 +442,7 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
       gates.push_back(d);
     }
     P.gate_end = static_cast<int32_t>(gates.size());
+    P.mat_count = static_cast<int32_t>(matrices.size() / 2) - P.mat_begin;
     passes.push_back(P);
   }
 }
@@ -444,6 +460,7 @@ void HostPlan::build_mma() {
     P.measure_q = P.collapse_q = -1;
     P.measure_slot = P.collapse_slot = -1;
     P.gate_begin = P.gate_end = 0;
+    P.mat_begin = P.mat_count = 0;
     int t = 0, o = 0;
     for (int q = 0; q < n_qubits; ++q) {
       if (q < tile_qubits)

@@ -56,7 +56,7 @@ enum GateClass : uint8_t {
 // index p = parity(p & ra)); the tile-local and out-of-tile parts of the rows
 // are stored separately so the out-of-tile parity is one popcount per tile.
 struct GateDesc {     // 40 bytes
-  int32_t mat;        // offset (complex elements) into the matrix pool
+  int32_t mat;        // offset (complex elements) in the pass's matrix block
   uint8_t cls;        // GateClass
   uint8_t plo, phi;   // pivot bits (ascending) removed from the quad/pair index
   uint8_t nq;         // 1 or 2
@@ -67,14 +67,20 @@ struct GateDesc {     // 40 bytes
   uint64_t ra_out, rb_out;  // out-of-tile parts of the dual rows (physical bits)
 };
 
-struct PassDesc {
+// Per pass the kernel stages the gate descriptors and the pass's own block
+// of packed matrices in shared memory (bounded by these limits).
+constexpr int kMaxPassGates = 64;
+constexpr int kMaxPassMats = 1024;  // complex elements (16 KiB)
+
+struct PassDesc {         // 112 bytes
   int32_t gate_begin, gate_end;
+  int32_t mat_begin, mat_count;  // the pass's matrix block (complex elements)
   int32_t k;              // tile qubits used (<= kTileQubitsMax)
   int32_t measure_q;      // epilogue: partial P(q=0) sums (-1: none)
   int32_t measure_slot;   // index into the probability record
   int32_t collapse_q;     // prologue: collapse onto q=0 using the carried p0
   int32_t collapse_slot;
-  int32_t pad;
+  int32_t pad[3];
   int8_t tq[16];          // tile-local bit i -> physical qubit (ascending)
   int8_t oq[48];          // tile-index bit j -> physical qubit (ascending)
 };

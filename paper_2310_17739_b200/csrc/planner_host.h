@@ -48,7 +48,8 @@ struct PhysGate {
   int nq = 0;
   uint64_t ma = 0, mb = 0;  // physical XOR masks of slot 0 / slot 1
   uint64_t ra = 0, rb = 0;  // dual rows: logical slot bits as physical parities
-  int32_t mat = 0;          // packed payload offset in the pool
+  int32_t mat = 0;          // packed payload: offset into HostPlan::packed_all
+  int32_t n_mat = 0;        // complex elements
   uint16_t cols = 0;
 };
 
@@ -76,7 +77,8 @@ struct HostPlan {
   std::vector<PassDesc> passes;      // plain gate passes (items reference ranges)
   std::vector<PassDesc> mma_passes;  // whole-circuit MMA program
   std::vector<GateDesc> gates;
-  std::vector<double> matrices;      // packed, deduplicated payload pool
+  std::vector<double> matrices;      // packed payloads, one block per pass
+  std::vector<double> packed_all;    // packed payloads of the current run
   std::vector<double> dense_mats;    // k-qubit / unblocked matrices (full)
   std::vector<int32_t> items_flat;   // nsb_host_plan_view export
 

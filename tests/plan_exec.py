@@ -16,10 +16,10 @@ import numpy as np
 
 from paper_2310_17739_b200 import _native as N
 
-PASS_DT = np.dtype([("gate_begin", "<i4"), ("gate_end", "<i4"), ("k", "<i4"),
-                    ("measure_q", "<i4"), ("measure_slot", "<i4"), ("collapse_q", "<i4"),
-                    ("collapse_slot", "<i4"), ("pad", "<i4"), ("tq", "i1", (16,)),
-                    ("oq", "i1", (48,))])
+PASS_DT = np.dtype([("gate_begin", "<i4"), ("gate_end", "<i4"), ("mat_begin", "<i4"),
+                    ("mat_count", "<i4"), ("k", "<i4"), ("measure_q", "<i4"),
+                    ("measure_slot", "<i4"), ("collapse_q", "<i4"), ("collapse_slot", "<i4"),
+                    ("pad", "<i4", (3,)), ("tq", "i1", (16,)), ("oq", "i1", (48,))])
 GATE_DT = np.dtype([("mat", "<i4"), ("cls", "u1"), ("plo", "u1"), ("phi", "u1"), ("nq", "u1"),
                     ("ma", "<u2"), ("mb", "<u2"), ("ra", "<u2"), ("rb", "<u2"),
                     ("cols", "<u2"), ("pad", "<u2"), ("ra_out", "<u8"), ("rb_out", "<u8")],
@@ -83,7 +83,8 @@ def _mix2(x, y, m):
 
 
 def _apply(T, g, mats, tbases, k):
-    """One gate sweep on all tiles T (tiles x 2^k), as k_blocked's apply_gate."""
+    """One gate sweep on all tiles T (tiles x 2^k), as k_blocked's apply_gate;
+    `mats` is the pass's matrix block."""
     m = mats[int(g["mat"]):]
     ga = _parity(tbases & np.uint64(g["ra_out"]))[:, None]
     gb = _parity(tbases & np.uint64(g["rb_out"]))[:, None]
@@ -149,8 +150,10 @@ def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12):
         if cq >= 0:
             scale = 1.0 / np.sqrt(carry_p0)
             T = np.where((idx >> cq) & 1, 0.0, T * scale)
+        block = plan.mats[int(P["mat_begin"]):int(P["mat_begin"]) + int(P["mat_count"])]
+        assert int(P["gate_end"]) - int(P["gate_begin"]) <= 64 and len(block) <= 1024
         for g in plan.gates[int(P["gate_begin"]):int(P["gate_end"])]:
-            _apply(T, g, plan.mats, tb.astype(np.uint64), k)
+            _apply(T, g, block, tb.astype(np.uint64), k)
         state[idx] = T
         mq = int(P["measure_q"])
         if mq >= 0:
