@@ -258,8 +258,10 @@ struct BlockedParams {
 // {v, v^ma, v^mb, v^ma^mb}; quad representatives are the indices with both
 // pivot bits clear, enumerated by inserting zeros at plo < phi into the quad
 // number.  Member s of a quad (s = bit(slot0) + 2 bit(slot1), the reference's
-// matrix index) lives at swz(base) ^ (s&1 ? swz(ma) : 0) ^ (s&2 ? swz(mb) : 0)
-// because the swizzle is linear over XOR.  1q gates use pairs {v, v^ma}.
+// matrix index) lives at base ^ (s&1 ? ma : 0) ^ (s&2 ? mb : 0).  1q gates use
+// pairs {v, v^ma}.  Tiles are stored unswizzled: a quarter-warp's 8 bases
+// differ in their low non-pivot bits, so 16-byte accesses are conflict-free
+// unless a pivot sits in bits 0..2.
 
 __device__ __forceinline__ int ins0(int j, int pos) {
   return ((j >> pos) << (pos + 1)) | (j & ((1 << pos) - 1));
@@ -286,51 +288,96 @@ __device__ __forceinline__ double2 pick(const double2 x0, const double2 x1, cons
   return r;
 }
 
+// Quad q of thread t is j = t + 256 i.  Inserting the pivot zeros is linear
+// over disjoint bit-ORs, so base(j) = base(t) | base(256 i) and the logical
+// parities la = parity(base & ra) ^ g_a split the same way: everything per
+// quad is a handful of XORs on values computed once per gate.
 struct Sweep {
-  double2* tile;
-  int n_items;  // quads (2q) or pairs (1q) in the tile
-  int plo, phi;
-  int sa, sb;   // swizzled masks
-  int ra, rb;   // tile-local dual rows
-  int ga, gb;   // out-of-tile parities of the dual rows for this tile
+  int n_iter;       // quads (2q) / pairs (1q) per thread
+  bool active;      // this thread owns work (tiles smaller than 256 items)
+  int bt;           // pivot-expanded thread part of the index
+  int st1, st2, st3;        // pivot-expanded 256, 512, 1024
+  int la_t, lb_t;           // logical parities of bt (incl. out-of-tile part)
+  int la1, lb1, la2, lb2, la3;  // parities of st1 / st2 / st3
+  int ma, mb;
 };
 
-// member 0 of each coset is the one whose logical slot bits are zero: start
-// from the pivot representative and step along ma / mb by its logical bits
+__device__ __forceinline__ int parity(int x) { return __popc(x) & 1; }
+
+__device__ __forceinline__ Sweep make_sweep(int k, const GateDesc& d, uint64_t tile_base) {
+  Sweep w;
+  const int two = d.nq == 2;
+  const int items = 1 << (k - 1 - two);
+  const int t = threadIdx.x;
+  w.active = t < items;
+  w.n_iter = items > kPassThreads ? items / kPassThreads : 1;
+  auto expand = [&](int j) { return two ? ins0(ins0(j, d.plo), d.phi) : ins0(j, d.plo); };
+  w.bt = expand(t);
+  w.st1 = expand(kPassThreads);
+  w.st2 = expand(2 * kPassThreads);
+  w.st3 = expand(4 * kPassThreads);
+  const int ga = __popcll(tile_base & d.ra_out) & 1, gb = __popcll(tile_base & d.rb_out) & 1;
+  w.la_t = parity(w.bt & d.ra) ^ ga;
+  w.lb_t = parity(w.bt & d.rb) ^ gb;
+  w.la1 = parity(w.st1 & d.ra);
+  w.lb1 = parity(w.st1 & d.rb);
+  w.la2 = parity(w.st2 & d.ra);
+  w.lb2 = parity(w.st2 & d.rb);
+  w.la3 = parity(w.st3 & d.ra);
+  w.ma = d.ma;
+  w.mb = d.mb;
+  return w;
+}
+
+// member 0 of each coset is the one whose logical slot bits are zero
 template <class F>
 __device__ __forceinline__ void for_quads(const Sweep& w, F f) {
-  for (int j = threadIdx.x; j < w.n_items; j += kPassThreads) {
-    const int b = ins0(ins0(j, w.plo), w.phi);
-    const int la = (__popc(b & w.ra) ^ w.ga) & 1, lb = (__popc(b & w.rb) ^ w.gb) & 1;
-    const int a0 = swz(b) ^ (la ? w.sa : 0) ^ (lb ? w.sb : 0);
-    f(a0, a0 ^ w.sa, a0 ^ w.sb, a0 ^ w.sa ^ w.sb);
+  if (!w.active) return;
+#pragma unroll 4
+  for (int i = 0; i < w.n_iter; ++i) {
+    int b = w.bt, la = w.la_t, lb = w.lb_t;
+    if (i & 1) {
+      b |= w.st1;
+      la ^= w.la1;
+      lb ^= w.lb1;
+    }
+    if (i & 2) {
+      b |= w.st2;
+      la ^= w.la2;
+      lb ^= w.lb2;
+    }
+    const int a0 = b ^ (la ? w.ma : 0) ^ (lb ? w.mb : 0);
+    f(a0, a0 ^ w.ma, a0 ^ w.mb, a0 ^ w.ma ^ w.mb);
   }
 }
 
 template <class F>
 __device__ __forceinline__ void for_pairs(const Sweep& w, F f) {
-  for (int j = threadIdx.x; j < w.n_items; j += kPassThreads) {
-    const int b = ins0(j, w.plo);
-    const int la = (__popc(b & w.ra) ^ w.ga) & 1;
-    const int a0 = swz(b) ^ (la ? w.sa : 0);
-    f(a0, a0 ^ w.sa);
+  if (!w.active) return;
+#pragma unroll 4
+  for (int i = 0; i < w.n_iter; ++i) {
+    int b = w.bt, la = w.la_t;
+    if (i & 1) {
+      b |= w.st1;
+      la ^= w.la1;
+    }
+    if (i & 2) {
+      b |= w.st2;
+      la ^= w.la2;
+    }
+    if (i & 4) {
+      b |= w.st3;
+      la ^= w.la3;
+    }
+    const int a0 = b ^ (la ? w.ma : 0);
+    f(a0, a0 ^ w.ma);
   }
 }
 
 __device__ __forceinline__ void apply_gate(double2* __restrict__ tile, int k, const GateDesc& d,
                                            const double2* __restrict__ m, uint64_t tile_base) {
-  Sweep w;
-  w.tile = tile;
-  w.plo = d.plo;
-  w.phi = d.phi;
-  w.sa = swz(d.ma);
-  w.sb = swz(d.mb);
-  w.ra = d.ra;
-  w.rb = d.rb;
-  w.ga = __popcll(tile_base & d.ra_out);
-  w.gb = __popcll(tile_base & d.rb_out);
+  const Sweep w = make_sweep(k, d, tile_base);
   if (d.nq == 1) {
-    w.n_items = 1 << (k - 1);
     if (d.cls == kDiag1) {
       const double2 d0 = *(m), d1 = *(m + 1);
       for_pairs(w, [&](int i0, int i1) {
@@ -348,7 +395,6 @@ __device__ __forceinline__ void apply_gate(double2* __restrict__ tile, int k, co
     }
     return;
   }
-  w.n_items = 1 << (k - 2);
   switch (d.cls) {
     case kCX01:
     case kCX10:
@@ -514,7 +560,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
     auto issue_load = [&](uint64_t t, double2* buf) {
       if (!loader) return;
       const uint64_t base = tile_base(t) | lo;
-      for (int j = 0; j < n_j; ++j) cp_async16(buf + swz(tid + (j << 8)), p.amps + (base | s_hi[j]));
+      for (int j = 0; j < n_j; ++j) cp_async16(buf + tid + (j << 8), p.amps + (base | s_hi[j]));
     };
 
     uint64_t t = blockIdx.x;
@@ -535,7 +581,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
         if (loader)
           for (int j = 0; j < n_j; ++j) {
             const uint64_t g = base | s_hi[j];
-            double2& v = tile[swz(tid + (j << 8))];
+            double2& v = tile[tid + (j << 8)];
             if ((g >> cq) & 1) {
               v = make_double2(0.0, 0.0);
             } else {
@@ -556,7 +602,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
 #pragma unroll 4
         for (int j = 0; j < n_j; ++j) {
           const uint64_t g = base | s_hi[j];
-          const double2 v = tile[swz(tid + (j << 8))];
+          const double2 v = tile[tid + (j << 8)];
           p.amps[g] = v;
           if (mq >= 0 && !((g >> mq) & 1)) {
             msum = fma(v.x, v.x, msum);
