@@ -310,20 +310,19 @@ __device__ __forceinline__ Sweep make_sweep(int k, const GateDesc& d, uint64_t t
   const int items = 1 << (k - 1 - two);
   const int t = threadIdx.x;
   w.active = t < items;
-  w.n_iter = items > kPassThreads ? items / kPassThreads : 1;
-  auto expand = [&](int j) { return two ? ins0(ins0(j, d.plo), d.phi) : ins0(j, d.plo); };
-  w.bt = expand(t);
-  w.st1 = expand(kPassThreads);
-  w.st2 = expand(2 * kPassThreads);
-  w.st3 = expand(4 * kPassThreads);
-  const int ga = __popcll(tile_base & d.ra_out) & 1, gb = __popcll(tile_base & d.rb_out) & 1;
-  w.la_t = parity(w.bt & d.ra) ^ ga;
-  w.lb_t = parity(w.bt & d.rb) ^ gb;
-  w.la1 = parity(w.st1 & d.ra);
-  w.lb1 = parity(w.st1 & d.rb);
-  w.la2 = parity(w.st2 & d.ra);
-  w.lb2 = parity(w.st2 & d.rb);
-  w.la3 = parity(w.st3 & d.ra);
+  w.n_iter = items > kPassThreads ? items >> 8 : 1;
+  w.bt = two ? ins0(ins0(t, d.plo), d.phi) : ins0(t, d.plo);
+  w.st1 = d.st1;
+  w.st2 = d.st2;
+  w.st3 = d.st3;
+  const int sp = d.spar;
+  w.la_t = (__popc(w.bt & d.ra) ^ __popcll(tile_base & d.ra_out)) & 1;
+  w.lb_t = (__popc(w.bt & d.rb) ^ __popcll(tile_base & d.rb_out)) & 1;
+  w.la1 = sp & 1;
+  w.lb1 = (sp >> 1) & 1;
+  w.la2 = (sp >> 2) & 1;
+  w.lb2 = (sp >> 3) & 1;
+  w.la3 = (sp >> 4) & 1;
   w.ma = d.ma;
   w.mb = d.mb;
   return w;

@@ -439,6 +439,17 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
         d.plo = static_cast<uint8_t>(std::min(pa, pbit));
         d.phi = static_cast<uint8_t>(std::max(pa, pbit));
       }
+      auto ins0 = [](uint32_t j, int pos) { return ((j >> pos) << (pos + 1)) | (j & ((1u << pos) - 1)); };
+      auto expand = [&](uint32_t j) { return g.nq == 2 ? ins0(ins0(j, d.plo), d.phi) : ins0(j, d.plo); };
+      const uint32_t st[3] = {expand(256), expand(512), expand(1024)};
+      d.st1 = static_cast<uint16_t>(st[0]);
+      d.st2 = static_cast<uint16_t>(st[1]);
+      d.st3 = static_cast<uint16_t>(st[2]);
+      d.spar = 0;
+      for (int i = 0; i < 3; ++i) {
+        d.spar |= static_cast<uint8_t>((popc(st[i] & d.ra) & 1) << (2 * i));
+        d.spar |= static_cast<uint8_t>((popc(st[i] & d.rb) & 1) << (2 * i + 1));
+      }
       gates.push_back(d);
     }
     P.gate_end = static_cast<int32_t>(gates.size());

@@ -55,7 +55,11 @@ enum GateClass : uint8_t {
 // zero is found with the dual rows ra, rb of M^-1 (logical bit a of physical
 // index p = parity(p & ra)); the tile-local and out-of-tile parts of the rows
 // are stored separately so the out-of-tile parity is one popcount per tile.
-struct GateDesc {     // 40 bytes
+//
+// Thread t handles quad numbers j = t + 256 i; the planner precomputes the
+// pivot expansion of 256, 512, 1024 (st1..st3) and their logical parities
+// (spar bits: la1 lb1 la2 lb2 la3 lb3) so the kernel's per-quad work is XORs.
+struct GateDesc {     // 48 bytes
   int32_t mat;        // offset (complex elements) in the pass's matrix block
   uint8_t cls;        // GateClass
   uint8_t plo, phi;   // pivot bits (ascending) removed from the quad/pair index
@@ -63,7 +67,9 @@ struct GateDesc {     // 40 bytes
   uint16_t ma, mb;    // tile-local XOR masks of slot 0 / slot 1
   uint16_t ra, rb;    // tile-local parts of the dual rows
   uint16_t cols;      // kSparse2 / kMono2: 2-bit column codes
-  uint16_t pad;
+  uint16_t st1, st2, st3;   // pivot-expanded 256, 512, 1024
+  uint8_t spar;       // parities of st1..st3 against ra / rb
+  uint8_t pad[7];
   uint64_t ra_out, rb_out;  // out-of-tile parts of the dual rows (physical bits)
 };
 

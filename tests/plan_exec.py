@@ -22,7 +22,8 @@ PASS_DT = np.dtype([("gate_begin", "<i4"), ("gate_end", "<i4"), ("mat_begin", "<
                     ("pad", "<i4", (3,)), ("tq", "i1", (16,)), ("oq", "i1", (48,))])
 GATE_DT = np.dtype([("mat", "<i4"), ("cls", "u1"), ("plo", "u1"), ("phi", "u1"), ("nq", "u1"),
                     ("ma", "<u2"), ("mb", "<u2"), ("ra", "<u2"), ("rb", "<u2"),
-                    ("cols", "<u2"), ("pad", "<u2"), ("ra_out", "<u8"), ("rb_out", "<u8")],
+                    ("cols", "<u2"), ("st1", "<u2"), ("st2", "<u2"), ("st3", "<u2"),
+                    ("spar", "u1"), ("pad", "u1", (7,)), ("ra_out", "<u8"), ("rb_out", "<u8")],
                    align=True)
 (DENSE1, DIAG1, DENSE2, SPARSE2, MONO2, DIAG2, CX01, CX10, PAIRQ, PAIRP, PAIRX, SWAP) = range(12)
 
@@ -89,10 +90,28 @@ def _apply(T, g, mats, tbases, k):
     ga = _parity(tbases & np.uint64(g["ra_out"]))[:, None]
     gb = _parity(tbases & np.uint64(g["rb_out"]))[:, None]
     ma, mb = int(g["ma"]), int(g["mb"])
+    sp = int(g["spar"])
+    steps = [(int(g["st1"]), sp & 1, (sp >> 1) & 1), (int(g["st2"]), (sp >> 2) & 1, (sp >> 3) & 1),
+             (int(g["st3"]), (sp >> 4) & 1, (sp >> 5) & 1)]
+
+    def enumerate_items(nq):
+        """The kernel's enumeration: item j = t + 256 i, base and parities
+        assembled from the thread part and the planner's precomputed steps."""
+        items = 1 << (k - nq)
+        j = np.arange(items, dtype=np.int64)
+        t, i = j & 255, j >> 8
+        bt = _ins0(_ins0(t, int(g["plo"])), int(g["phi"])) if nq == 2 else _ins0(t, int(g["plo"]))
+        b, la, lb = bt.copy(), _parity(bt & int(g["ra"])), _parity(bt & int(g["rb"]))
+        for bit, (st, pa, pb) in enumerate(steps):
+            on = ((i >> bit) & 1).astype(bool)
+            b = np.where(on, b | st, b)
+            la = np.where(on, la ^ pa, la)
+            lb = np.where(on, lb ^ pb, lb)
+        return b[None, :], la[None, :], lb[None, :]
+
     if g["nq"] == 1:
-        j = np.arange(1 << (k - 1), dtype=np.int64)
-        b = _ins0(j, int(g["plo"]))[None, :]
-        la = (_parity(b & int(g["ra"])) ^ ga) & 1
+        b, la, _ = enumerate_items(1)
+        la = (la ^ ga) & 1
         i0 = b ^ (la * ma)
         i1 = i0 ^ ma
         r = np.arange(T.shape[0])[:, None]
@@ -103,10 +122,9 @@ def _apply(T, g, mats, tbases, k):
             x, y = _mix2(x, y, m[:4])
         T[r, i0], T[r, i1] = x, y
         return
-    j = np.arange(1 << (k - 2), dtype=np.int64)
-    b = _ins0(_ins0(j, int(g["plo"])), int(g["phi"]))[None, :]
-    la = (_parity(b & int(g["ra"])) ^ ga) & 1
-    lb = (_parity(b & int(g["rb"])) ^ gb) & 1
+    b, la, lb = enumerate_items(2)
+    la = (la ^ ga) & 1
+    lb = (lb ^ gb) & 1
     i0 = b ^ (la * ma) ^ (lb * mb)
     idx = [i0, i0 ^ ma, i0 ^ mb, i0 ^ ma ^ mb]
     r = np.arange(T.shape[0])[:, None]
