@@ -288,94 +288,106 @@ __device__ __forceinline__ double2 pick(const double2 x0, const double2 x1, cons
   return r;
 }
 
-// Quad q of thread t is j = t + 256 i.  Inserting the pivot zeros is linear
-// over disjoint bit-ORs, so base(j) = base(t) | base(256 i) and the logical
-// parities la = parity(base & ra) ^ g_a split the same way: everything per
-// quad is a handful of XORs on values computed once per gate.
+// A sweep covers one batch of up to 4096 amplitudes: nb tiles of 2^k stored
+// back to back (batch index bits k.. act as extra tile bits no gate touches).
+// Item j = t + 256 i of thread t; inserting the pivot zeros is linear over
+// disjoint bit-ORs, so base(j) = base(t) | base(256 i) and the logical
+// parities split the same way: per item only XORs remain.  The out-of-tile
+// parity of each tile in the batch is a bit of gmask.
 struct Sweep {
-  int n_iter;       // quads (2q) / pairs (1q) per thread
-  bool active;      // this thread owns work (tiles smaller than 256 items)
-  int bt;           // pivot-expanded thread part of the index
-  int st1, st2, st3;        // pivot-expanded 256, 512, 1024
-  int la_t, lb_t;           // logical parities of bt (incl. out-of-tile part)
-  int la1, lb1, la2, lb2, la3;  // parities of st1 / st2 / st3
+  int n_iter;           // valid items per thread
+  bool active;          // this thread owns work (batches smaller than 256 items)
+  int bt;               // pivot-expanded thread part of the index
+  int st1, st2, st3;    // pivot-expanded 256, 512, 1024
+  int la_t, lb_t;       // logical parities of bt (tile-local part)
+  int spar;             // parities of st1..st3
+  int tshift;           // item iteration i belongs to tile i >> tshift
+  unsigned gma, gmb;    // out-of-tile parities per tile of the batch
   int ma, mb;
 };
 
 __device__ __forceinline__ int parity(int x) { return __popc(x) & 1; }
 
-__device__ __forceinline__ Sweep make_sweep(int k, const GateDesc& d, uint64_t tile_base) {
+__device__ __forceinline__ Sweep make_sweep(int k, int nb, const GateDesc& d,
+                                            const uint64_t* tile_base) {
   Sweep w;
   const int two = d.nq == 2;
-  const int items = 1 << (k - 1 - two);
+  const int per_tile = 1 << (k - 1 - two);  // items per tile
+  const int items = per_tile * nb;
   const int t = threadIdx.x;
   w.active = t < items;
   w.n_iter = items > kPassThreads ? items >> 8 : 1;
+  w.tshift = per_tile > kPassThreads ? __ffs(per_tile >> 8) - 1 : 0;
   w.bt = two ? ins0(ins0(t, d.plo), d.phi) : ins0(t, d.plo);
   w.st1 = d.st1;
   w.st2 = d.st2;
   w.st3 = d.st3;
-  const int sp = d.spar;
-  w.la_t = (__popc(w.bt & d.ra) ^ __popcll(tile_base & d.ra_out)) & 1;
-  w.lb_t = (__popc(w.bt & d.rb) ^ __popcll(tile_base & d.rb_out)) & 1;
-  w.la1 = sp & 1;
-  w.lb1 = (sp >> 1) & 1;
-  w.la2 = (sp >> 2) & 1;
-  w.lb2 = (sp >> 3) & 1;
-  w.la3 = (sp >> 4) & 1;
+  w.spar = d.spar;
+  w.la_t = parity(w.bt & d.ra);
+  w.lb_t = parity(w.bt & d.rb);
+  w.gma = w.gmb = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    if (b < nb) {
+      w.gma |= (__popcll(tile_base[b] & d.ra_out) & 1u) << b;
+      w.gmb |= (__popcll(tile_base[b] & d.rb_out) & 1u) << b;
+    }
+  }
+  if (per_tile < kPassThreads) {  // small tiles: thread t sits in tile t / per_tile
+    const int b = t / per_tile;
+    w.gma = (w.gma >> b) & 1u;
+    w.gmb = (w.gmb >> b) & 1u;
+  }
   w.ma = d.ma;
   w.mb = d.mb;
   return w;
 }
 
 // member 0 of each coset is the one whose logical slot bits are zero
-template <class F>
-__device__ __forceinline__ void for_quads(const Sweep& w, F f) {
+template <int MAXI, class F>
+__device__ __forceinline__ void for_items(const Sweep& w, bool two, F f) {
   if (!w.active) return;
-#pragma unroll 4
-  for (int i = 0; i < w.n_iter; ++i) {
+#pragma unroll
+  for (int i = 0; i < MAXI; ++i) {
+    if (i >= w.n_iter) break;
     int b = w.bt, la = w.la_t, lb = w.lb_t;
     if (i & 1) {
       b |= w.st1;
-      la ^= w.la1;
-      lb ^= w.lb1;
+      la ^= w.spar & 1;
+      lb ^= (w.spar >> 1) & 1;
     }
     if (i & 2) {
       b |= w.st2;
-      la ^= w.la2;
-      lb ^= w.lb2;
+      la ^= (w.spar >> 2) & 1;
+      lb ^= (w.spar >> 3) & 1;
     }
-    const int a0 = b ^ (la ? w.ma : 0) ^ (lb ? w.mb : 0);
-    f(a0, a0 ^ w.ma, a0 ^ w.mb, a0 ^ w.ma ^ w.mb);
+    if (i & 4) {
+      b |= w.st3;
+      la ^= (w.spar >> 4) & 1;
+      lb ^= (w.spar >> 5) & 1;
+    }
+    const int tb = i >> w.tshift;
+    la ^= (w.gma >> tb) & 1;
+    lb ^= (w.gmb >> tb) & 1;
+    const int a0 = b ^ (la ? w.ma : 0) ^ (two && lb ? w.mb : 0);
+    f(a0);
   }
+}
+
+template <class F>
+__device__ __forceinline__ void for_quads(const Sweep& w, F f) {
+  for_items<4>(w, true, [&](int a0) { f(a0, a0 ^ w.ma, a0 ^ w.mb, a0 ^ w.ma ^ w.mb); });
 }
 
 template <class F>
 __device__ __forceinline__ void for_pairs(const Sweep& w, F f) {
-  if (!w.active) return;
-#pragma unroll 4
-  for (int i = 0; i < w.n_iter; ++i) {
-    int b = w.bt, la = w.la_t;
-    if (i & 1) {
-      b |= w.st1;
-      la ^= w.la1;
-    }
-    if (i & 2) {
-      b |= w.st2;
-      la ^= w.la2;
-    }
-    if (i & 4) {
-      b |= w.st3;
-      la ^= w.la3;
-    }
-    const int a0 = b ^ (la ? w.ma : 0);
-    f(a0, a0 ^ w.ma);
-  }
+  for_items<8>(w, false, [&](int a0) { f(a0, a0 ^ w.ma); });
 }
 
-__device__ __forceinline__ void apply_gate(double2* __restrict__ tile, int k, const GateDesc& d,
-                                           const double2* __restrict__ m, uint64_t tile_base) {
-  const Sweep w = make_sweep(k, d, tile_base);
+__device__ __forceinline__ void apply_gate(double2* __restrict__ tile, int k, int nb,
+                                           const GateDesc& d, const double2* __restrict__ m,
+                                           const uint64_t* tile_base) {
+  const Sweep w = make_sweep(k, nb, d, tile_base);
   if (d.nq == 1) {
     if (d.cls == kDiag1) {
       const double2 d0 = *(m), d1 = *(m + 1);
@@ -556,60 +568,74 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
         if (t >> b & 1) base |= uint64_t(1) << sp.oq[b];
       return base;
     };
-    auto issue_load = [&](uint64_t t, double2* buf) {
+    // contiguous tile range of this CTA, processed in batches of nb tiles
+    const int nb = k >= kTileQubitsMax ? 1 : min(1 << (kTileQubitsMax - k), 4);
+    const uint64_t per = n_tiles / gridDim.x, extra = n_tiles % gridDim.x;
+    const uint64_t t_begin = blockIdx.x * per + (blockIdx.x < extra ? blockIdx.x : extra);
+    const uint64_t t_end = t_begin + per + (blockIdx.x < extra ? 1 : 0);
+    auto issue_batch = [&](uint64_t t0, double2* buf) {
       if (!loader) return;
-      const uint64_t base = tile_base(t) | lo;
-      for (int j = 0; j < n_j; ++j) cp_async16(buf + tid + (j << 8), p.amps + (base | s_hi[j]));
+      for (int b = 0; b < nb && t0 + b < t_end; ++b) {
+        const uint64_t base = tile_base(t0 + b) | lo;
+        double2* dst = buf + (b << k);
+        for (int j = 0; j < n_j; ++j) cp_async16(dst + tid + (j << 8), p.amps + (base | s_hi[j]));
+      }
     };
 
-    uint64_t t = blockIdx.x;
     int cur = 0;
-    if (t < n_tiles) issue_load(t, smem);
+    if (t_begin < t_end) issue_batch(t_begin, smem);
     cp_async_commit();
-    for (; t < n_tiles; t += gridDim.x, cur ^= 1) {
+    for (uint64_t t0 = t_begin; t0 < t_end; t0 += nb, cur ^= 1) {
       double2* tile = smem + cur * kTileAmpsMax;
-      const uint64_t t_next = t + gridDim.x;
-      if (t_next < n_tiles) issue_load(t_next, smem + (cur ^ 1) * kTileAmpsMax);
+      const int nvalid = t_end - t0 < uint64_t(nb) ? static_cast<int>(t_end - t0) : nb;
+      uint64_t tbase[4];
+      for (int b = 0; b < 4; ++b) tbase[b] = b < nvalid ? tile_base(t0 + b) : 0;
+      if (t0 + nb < t_end) issue_batch(t0 + nb, smem + (cur ^ 1) * kTileAmpsMax);
       cp_async_commit();
-      cp_async_wait<1>();  // this tile's group has landed (next may be in flight)
+      cp_async_wait<1>();  // this batch has landed (the next may be in flight)
       __syncthreads();
-      const uint64_t tbase = tile_base(t);
-      const uint64_t base = tbase | lo;
       if (sp.collapse_q >= 0) {  // pending collapse (engine.py:164-167)
         const int cq = sp.collapse_q;
         if (loader)
-          for (int j = 0; j < n_j; ++j) {
-            const uint64_t g = base | s_hi[j];
-            double2& v = tile[tid + (j << 8)];
-            if ((g >> cq) & 1) {
-              v = make_double2(0.0, 0.0);
-            } else {
-              v.x *= cscale;
-              v.y *= cscale;
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            for (int j = 0; j < n_j && b < nvalid; ++j) {
+              const uint64_t g = tbase[b] | lo | s_hi[j];
+              double2& v = tile[(b << k) + tid + (j << 8)];
+              if ((g >> cq) & 1) {
+                v = make_double2(0.0, 0.0);
+              } else {
+                v.x *= cscale;
+                v.y *= cscale;
+              }
             }
-          }
         __syncthreads();
       }
       for (int g = 0; g < n_gates; ++g) {
         const GateDesc d = s_gates[g];
-        apply_gate(tile, k, d, s_mats + d.mat, tbase);
+        apply_gate(tile, k, nvalid, d, s_mats + d.mat, tbase);
         __syncthreads();
       }
       // shared -> global (+ assertion epilogue partial sums)
       if (loader) {
         const int mq = sp.measure_q;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if (b >= nvalid) break;
+          const uint64_t base = tbase[b] | lo;
 #pragma unroll 4
-        for (int j = 0; j < n_j; ++j) {
-          const uint64_t g = base | s_hi[j];
-          const double2 v = tile[tid + (j << 8)];
-          p.amps[g] = v;
-          if (mq >= 0 && !((g >> mq) & 1)) {
-            msum = fma(v.x, v.x, msum);
-            msum = fma(v.y, v.y, msum);
+          for (int j = 0; j < n_j; ++j) {
+            const uint64_t g = base | s_hi[j];
+            const double2 v = tile[(b << k) + tid + (j << 8)];
+            p.amps[g] = v;
+            if (mq >= 0 && !((g >> mq) & 1)) {
+              msum = fma(v.x, v.x, msum);
+              msum = fma(v.y, v.y, msum);
+            }
           }
         }
       }
-      __syncthreads();  // buffer `cur` is free for the load issued next iteration
+      __syncthreads();  // buffer `cur` is free for the batch issued next iteration
     }
     cp_async_wait<0>();
     const int mq = sp.measure_q;

@@ -83,57 +83,47 @@ def _mix2(x, y, m):
     return m[0] * x + m[1] * y, m[2] * x + m[3] * y
 
 
-def _apply(T, g, mats, tbases, k):
-    """One gate sweep on all tiles T (tiles x 2^k), as k_blocked's apply_gate;
-    `mats` is the pass's matrix block."""
+def _apply(B, g, mats, tbases, k, nvalid):
+    """One gate sweep over a batch B (nvalid tiles of 2^k stored back to back),
+    enumerated exactly as k_blocked's make_sweep / for_items."""
     m = mats[int(g["mat"]):]
-    ga = _parity(tbases & np.uint64(g["ra_out"]))[:, None]
-    gb = _parity(tbases & np.uint64(g["rb_out"]))[:, None]
+    nq = int(g["nq"])
     ma, mb = int(g["ma"]), int(g["mb"])
     sp = int(g["spar"])
-    steps = [(int(g["st1"]), sp & 1, (sp >> 1) & 1), (int(g["st2"]), (sp >> 2) & 1, (sp >> 3) & 1),
-             (int(g["st3"]), (sp >> 4) & 1, (sp >> 5) & 1)]
-
-    def enumerate_items(nq):
-        """The kernel's enumeration: item j = t + 256 i, base and parities
-        assembled from the thread part and the planner's precomputed steps."""
-        items = 1 << (k - nq)
-        j = np.arange(items, dtype=np.int64)
-        t, i = j & 255, j >> 8
-        bt = _ins0(_ins0(t, int(g["plo"])), int(g["phi"])) if nq == 2 else _ins0(t, int(g["plo"]))
-        b, la, lb = bt.copy(), _parity(bt & int(g["ra"])), _parity(bt & int(g["rb"]))
-        for bit, (st, pa, pb) in enumerate(steps):
-            on = ((i >> bit) & 1).astype(bool)
-            b = np.where(on, b | st, b)
-            la = np.where(on, la ^ pa, la)
-            lb = np.where(on, lb ^ pb, lb)
-        return b[None, :], la[None, :], lb[None, :]
-
-    if g["nq"] == 1:
-        b, la, _ = enumerate_items(1)
-        la = (la ^ ga) & 1
-        i0 = b ^ (la * ma)
+    per_tile = 1 << (k - nq)
+    items = per_tile * nvalid
+    j = np.arange(items, dtype=np.int64)
+    t, i = j & 255, j >> 8
+    bt = _ins0(_ins0(t, int(g["plo"])), int(g["phi"])) if nq == 2 else _ins0(t, int(g["plo"]))
+    base, la, lb = bt.copy(), _parity(bt & int(g["ra"])), _parity(bt & int(g["rb"]))
+    for bit, st in enumerate((int(g["st1"]), int(g["st2"]), int(g["st3"]))):
+        on = ((i >> bit) & 1).astype(bool)
+        base = np.where(on, base | st, base)
+        la = np.where(on, la ^ ((sp >> (2 * bit)) & 1), la)
+        lb = np.where(on, lb ^ ((sp >> (2 * bit + 1)) & 1), lb)
+    # tile of each item: the kernel uses i >> tshift (or t // per_tile for small tiles)
+    tile = j // per_tile
+    ga = _parity(tbases[tile].astype(np.uint64) & np.uint64(g["ra_out"]))
+    gb = _parity(tbases[tile].astype(np.uint64) & np.uint64(g["rb_out"]))
+    la, lb = (la ^ ga) & 1, (lb ^ gb) & 1
+    if nq == 1:
+        i0 = base ^ (la * ma)
         i1 = i0 ^ ma
-        r = np.arange(T.shape[0])[:, None]
-        x, y = T[r, i0], T[r, i1]
+        x, y = B[i0], B[i1]
         if g["cls"] == DIAG1:
             x, y = m[0] * x, m[1] * y
         else:
             x, y = _mix2(x, y, m[:4])
-        T[r, i0], T[r, i1] = x, y
+        B[i0], B[i1] = x, y
         return
-    b, la, lb = enumerate_items(2)
-    la = (la ^ ga) & 1
-    lb = (lb ^ gb) & 1
-    i0 = b ^ (la * ma) ^ (lb * mb)
+    i0 = base ^ (la * ma) ^ (lb * mb)
     idx = [i0, i0 ^ ma, i0 ^ mb, i0 ^ ma ^ mb]
-    r = np.arange(T.shape[0])[:, None]
-    x = [T[r, i] for i in idx]
+    x = [B[ix] for ix in idx]
     c = int(g["cls"])
     out = list(x)
     if c in (CX01, CX10, SWAP):
-        s, t = {CX01: (1, 3), CX10: (2, 3), SWAP: (1, 2)}[c]
-        out[s], out[t] = x[t], x[s]
+        s, tt = {CX01: (1, 3), CX10: (2, 3), SWAP: (1, 2)}[c]
+        out[s], out[tt] = x[tt], x[s]
     elif c in (PAIRQ, PAIRP, PAIRX):
         (u0, u1), (u2, u3) = {PAIRQ: ((0, 2), (1, 3)), PAIRP: ((0, 1), (2, 3)),
                               PAIRX: ((0, 3), (1, 2))}[c]
@@ -149,30 +139,40 @@ def _apply(T, g, mats, tbases, k):
         out = [m[2 * s] * x[(cols >> (4 * s)) & 3] + m[2 * s + 1] * x[(cols >> (4 * s + 2)) & 3]
                for s in range(4)]
     else:
-        out = [sum(m[4 * s + t] * x[t] for t in range(4)) for s in range(4)]
-    for i, v in zip(idx, out):
-        T[r, i] = v
+        out = [sum(m[4 * s + u] * x[u] for u in range(4)) for s in range(4)]
+    for ix, v in zip(idx, out):
+        B[ix] = v
 
 
-def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12):
-    """Execute a pass list on `state` in place; returns {step: p0} and the carry."""
+def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12, workers=148):
+    """Execute a pass list on `state` in place, with k_blocked's per-CTA
+    contiguous tile ranges and batches; returns {step: p0} and the carry."""
     n = plan.n
     rec = {}
     for P in passes:
         k = int(P["k"])
         lidx = _scatter(np.arange(1 << k, dtype=np.int64), P["tq"][:k])
-        tb = _scatter(np.arange(1 << (n - k), dtype=np.int64), P["oq"][:n - k])
-        idx = tb[:, None] | lidx[None, :]
-        T = state[idx]
-        cq = int(P["collapse_q"])
-        if cq >= 0:
-            scale = 1.0 / np.sqrt(carry_p0)
-            T = np.where((idx >> cq) & 1, 0.0, T * scale)
+        n_tiles = 1 << (n - k)
+        tb_all = _scatter(np.arange(n_tiles, dtype=np.int64), P["oq"][:n - k])
+        nb = 1 if k >= 12 else min(1 << (12 - k), 4)
         block = plan.mats[int(P["mat_begin"]):int(P["mat_begin"]) + int(P["mat_count"])]
-        assert int(P["gate_end"]) - int(P["gate_begin"]) <= 64 and len(block) <= 1024
-        for g in plan.gates[int(P["gate_begin"]):int(P["gate_end"])]:
-            _apply(T, g, block, tb.astype(np.uint64), k)
-        state[idx] = T
+        gates = plan.gates[int(P["gate_begin"]):int(P["gate_end"])]
+        assert len(gates) <= 64 and len(block) <= 1024
+        cq = int(P["collapse_q"])
+        per, extra = divmod(n_tiles, workers)
+        for cta in range(min(workers, n_tiles)):
+            t_begin = cta * per + min(cta, extra)
+            t_end = t_begin + per + (1 if cta < extra else 0)
+            for t0 in range(t_begin, t_end, nb):
+                nvalid = min(nb, t_end - t0)
+                tbs = tb_all[t0:t0 + nvalid]
+                idx = (tbs[:, None] | lidx[None, :]).reshape(-1)
+                B = state[idx]
+                if cq >= 0:
+                    B = np.where((idx >> cq) & 1, 0.0, B * (1.0 / np.sqrt(carry_p0)))
+                for g in gates:
+                    _apply(B, g, block, tbs, k, nvalid)
+                state[idx] = B
         mq = int(P["measure_q"])
         if mq >= 0:
             keep = ((np.arange(state.size) >> mq) & 1) == 0
@@ -183,9 +183,9 @@ def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12):
     return rec, carry_p0
 
 
-def run_mma(plan: HostPlan, eps=1e-12):
+def run_mma(plan: HostPlan, eps=1e-12, workers=148):
     assert plan.mma_ok
     state = np.zeros(1 << plan.n, np.complex128)
     state[0] = 1.0
-    rec, _ = run_passes(plan, plan.mma_passes, state, eps=eps)
+    rec, _ = run_passes(plan, plan.mma_passes, state, eps=eps, workers=workers)
     return [rec[s] for s in sorted(rec)], state

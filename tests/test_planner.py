@@ -30,7 +30,7 @@ def check(c, workers=148):
         want_p, _, want_state, _ = O.run_mma(oracle_from_circuit(c), n, 1, 0)
     except O.OracleAssertion:
         pytest.skip("dead assertion branch")
-    probs, state = PE.run_mma(plan)
+    probs, state = PE.run_mma(plan, workers=workers)
     assert probs == pytest.approx(want_p, abs=1e-12)
     err = np.linalg.norm(state - want_state) / np.linalg.norm(want_state)
     assert err < 1e-10, err
@@ -55,11 +55,11 @@ def test_ladders_through_the_frame(n, terms):
         assert info_frame >= 0
 
 
-@pytest.mark.parametrize("workers", [1, 3, 148])
-def test_small_tiles_multi_pass(workers):
-    """n = 14 > 12 forces several tiles and multiple passes per run."""
-    rng = np.random.default_rng(7)
-    c = ladder_circuit(rng, 14, 12, blocks=2)
+@pytest.mark.parametrize("n,workers", [(14, 1), (14, 3), (14, 148), (15, 5), (16, 3)])
+def test_small_tiles_multi_pass(n, workers):
+    """n > 12 forces several tiles, batches of tiles and multiple passes."""
+    rng = np.random.default_rng(7 + n)
+    c = ladder_circuit(rng, n, 12, blocks=2)
     check(fuse_pipeline(c)[0], workers)
 
 
