@@ -290,7 +290,7 @@ __device__ __forceinline__ double2 pick(const double2 x0, const double2 x1, cons
 
 // A sweep covers one batch of up to 4096 amplitudes: nb tiles of 2^k stored
 // back to back (batch index bits k.. act as extra tile bits no gate touches).
-// Item j = t + 256 i of thread t; inserting the pivot zeros is linear over
+// Item j = t + T i of thread t (T = kPassThreads); inserting the pivot zeros is linear over
 // disjoint bit-ORs, so base(j) = base(t) | base(256 i) and the logical
 // parities split the same way: per item only XORs remain.  The out-of-tile
 // parity of each tile in the batch is a bit of gmask.
@@ -308,16 +308,15 @@ struct Sweep {
 
 __device__ __forceinline__ int parity(int x) { return __popc(x) & 1; }
 
-__device__ __forceinline__ Sweep make_sweep(int k, int nb, const GateDesc& d,
-                                            const uint64_t* tile_base) {
+__device__ __forceinline__ Sweep make_sweep(int k, int nb, const GateDesc& d, unsigned gm) {
   Sweep w;
   const int two = d.nq == 2;
   const int per_tile = 1 << (k - 1 - two);  // items per tile
   const int items = per_tile * nb;
   const int t = threadIdx.x;
   w.active = t < items;
-  w.n_iter = items > kPassThreads ? items >> 8 : 1;
-  w.tshift = per_tile > kPassThreads ? __ffs(per_tile >> 8) - 1 : 0;
+  w.n_iter = items > kPassThreads ? items >> kThreadBits : 1;
+  w.tshift = per_tile > kPassThreads ? __ffs(per_tile >> kThreadBits) - 1 : 0;
   w.bt = two ? ins0(ins0(t, d.plo), d.phi) : ins0(t, d.plo);
   w.st1 = d.st1;
   w.st2 = d.st2;
@@ -325,14 +324,8 @@ __device__ __forceinline__ Sweep make_sweep(int k, int nb, const GateDesc& d,
   w.spar = d.spar;
   w.la_t = parity(w.bt & d.ra);
   w.lb_t = parity(w.bt & d.rb);
-  w.gma = w.gmb = 0;
-#pragma unroll
-  for (int b = 0; b < 4; ++b) {
-    if (b < nb) {
-      w.gma |= (__popcll(tile_base[b] & d.ra_out) & 1u) << b;
-      w.gmb |= (__popcll(tile_base[b] & d.rb_out) & 1u) << b;
-    }
-  }
+  w.gma = gm & 15u;
+  w.gmb = gm >> 4;
   if (per_tile < kPassThreads) {  // small tiles: thread t sits in tile t / per_tile
     const int b = t / per_tile;
     w.gma = (w.gma >> b) & 1u;
@@ -386,8 +379,8 @@ __device__ __forceinline__ void for_pairs(const Sweep& w, F f) {
 
 __device__ __forceinline__ void apply_gate(double2* __restrict__ tile, int k, int nb,
                                            const GateDesc& d, const double2* __restrict__ m,
-                                           const uint64_t* tile_base) {
-  const Sweep w = make_sweep(k, nb, d, tile_base);
+                                           unsigned gm) {
+  const Sweep w = make_sweep(k, nb, d, gm);
   if (d.nq == 1) {
     if (d.cls == kDiag1) {
       const double2 d0 = *(m), d1 = *(m + 1);
@@ -522,7 +515,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
   double2* s_mats = smem + 2 * kTileAmpsMax;
   GateDesc* s_gates = reinterpret_cast<GateDesc*>(s_mats + kMaxPassMats);
   __shared__ PassDesc sp;
-  __shared__ uint64_t s_hi[16];  // global offset of tile-local bits 8..11 for j = 0..15
+  __shared__ uint64_t s_hi[1 << (kTileQubitsMax - kThreadBits)];  // offsets of tile bits >= kThreadBits
+  __shared__ unsigned s_gm[kMaxPassGates];  // per gate: out-of-tile row parities of the batch tiles
   __shared__ double red[32];
   __shared__ double s_p0;
   cg::grid_group grid = cg::this_grid();
@@ -543,20 +537,21 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
       uint64_t* dst = reinterpret_cast<uint64_t*>(s_gates);
       for (int i = tid; i < n_words; i += kPassThreads) dst[i] = src[i];
     }
-    if (tid < 16) {
+    constexpr int kHi = kTileQubitsMax - kThreadBits;
+    if (tid < (1 << kHi)) {
       uint64_t h = 0;
-      for (int b = 0; b < 4; ++b)
-        if ((tid >> b & 1) && 8 + b < k) h |= uint64_t(1) << sp.tq[8 + b];
+      for (int b = 0; b < kHi; ++b)
+        if ((tid >> b & 1) && kThreadBits + b < k) h |= uint64_t(1) << sp.tq[kThreadBits + b];
       s_hi[tid] = h;
     }
-    const int lo_bits = k < 8 ? k : 8;
-    uint64_t lo = 0;  // global offset of this thread's tile-local bits 0..7
+    const int lo_bits = k < kThreadBits ? k : kThreadBits;
+    uint64_t lo = 0;  // global offset of this thread's low tile-local bits
     for (int b = 0; b < lo_bits; ++b)
       if (tid >> b & 1) lo |= uint64_t(1) << sp.tq[b];
     __syncthreads();
     const int n_out = p.n - k;
     const uint64_t n_tiles = uint64_t(1) << n_out;
-    const int n_j = k > 8 ? 1 << (k - 8) : 1;
+    const int n_j = k > kThreadBits ? 1 << (k - kThreadBits) : 1;
     const bool loader = tid < (1 << lo_bits);
     const double cscale = sp.collapse_q >= 0 ? 1.0 / sqrt(carry_p0) : 1.0;
     const int n_gates = sp.gate_end - sp.gate_begin;
@@ -578,7 +573,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
       for (int b = 0; b < nb && t0 + b < t_end; ++b) {
         const uint64_t base = tile_base(t0 + b) | lo;
         double2* dst = buf + (b << k);
-        for (int j = 0; j < n_j; ++j) cp_async16(dst + tid + (j << 8), p.amps + (base | s_hi[j]));
+        for (int j = 0; j < n_j; ++j)
+          cp_async16(dst + tid + (j << kThreadBits), p.amps + (base | s_hi[j]));
       }
     };
 
@@ -593,6 +589,18 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
       if (t0 + nb < t_end) issue_batch(t0 + nb, smem + (cur ^ 1) * kTileAmpsMax);
       cp_async_commit();
       cp_async_wait<1>();  // this batch has landed (the next may be in flight)
+      if (tid < n_gates) {  // out-of-tile dual-row parities per (gate, tile of the batch)
+        const GateDesc& d = s_gates[tid];
+        unsigned gm = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if (b < nvalid) {
+            gm |= (__popcll(tbase[b] & d.ra_out) & 1u) << b;
+            gm |= (__popcll(tbase[b] & d.rb_out) & 1u) << (4 + b);
+          }
+        }
+        s_gm[tid] = gm;
+      }
       __syncthreads();
       if (sp.collapse_q >= 0) {  // pending collapse (engine.py:164-167)
         const int cq = sp.collapse_q;
@@ -601,7 +609,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
           for (int b = 0; b < 4; ++b)
             for (int j = 0; j < n_j && b < nvalid; ++j) {
               const uint64_t g = tbase[b] | lo | s_hi[j];
-              double2& v = tile[(b << k) + tid + (j << 8)];
+              double2& v = tile[(b << k) + tid + (j << kThreadBits)];
               if ((g >> cq) & 1) {
                 v = make_double2(0.0, 0.0);
               } else {
@@ -613,7 +621,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
       }
       for (int g = 0; g < n_gates; ++g) {
         const GateDesc d = s_gates[g];
-        apply_gate(tile, k, nvalid, d, s_mats + d.mat, tbase);
+        apply_gate(tile, k, nvalid, d, s_mats + d.mat, s_gm[g]);
         __syncthreads();
       }
       // shared -> global (+ assertion epilogue partial sums)
@@ -626,7 +634,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
 #pragma unroll 4
           for (int j = 0; j < n_j; ++j) {
             const uint64_t g = base | s_hi[j];
-            const double2 v = tile[(b << k) + tid + (j << 8)];
+            const double2 v = tile[(b << k) + tid + (j << kThreadBits)];
             p.amps[g] = v;
             if (mq >= 0 && !((g >> mq) & 1)) {
               msum = fma(v.x, v.x, msum);

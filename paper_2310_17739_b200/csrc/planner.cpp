@@ -441,7 +441,8 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
       }
       auto ins0 = [](uint32_t j, int pos) { return ((j >> pos) << (pos + 1)) | (j & ((1u << pos) - 1)); };
       auto expand = [&](uint32_t j) { return g.nq == 2 ? ins0(ins0(j, d.plo), d.phi) : ins0(j, d.plo); };
-      const uint32_t st[3] = {expand(256), expand(512), expand(1024)};
+      const uint32_t st[3] = {expand(kPassThreads), expand(2 * kPassThreads),
+                              expand(4 * kPassThreads)};
       d.st1 = static_cast<uint16_t>(st[0]);
       d.st2 = static_cast<uint16_t>(st[1]);
       d.st3 = static_cast<uint16_t>(st[2]);

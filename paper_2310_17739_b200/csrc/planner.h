@@ -28,7 +28,8 @@ namespace nsb {
 
 constexpr int kTileQubitsMax = 12;               // 4096 amplitudes = 64 KiB per buffer
 constexpr int kTileAmpsMax = 1 << kTileQubitsMax;
-constexpr int kPassThreads = 256;
+constexpr int kThreadBits = 9;
+constexpr int kPassThreads = 1 << kThreadBits;  // 16 warps per CTA, one CTA per SM
 constexpr int kLowQubits = 3;                    // always-tiled qubits 0..2 (128 B runs)
 constexpr int kMaxQubits = 40;
 
@@ -56,9 +57,9 @@ enum GateClass : uint8_t {
 // index p = parity(p & ra)); the tile-local and out-of-tile parts of the rows
 // are stored separately so the out-of-tile parity is one popcount per tile.
 //
-// Thread t handles quad numbers j = t + 256 i; the planner precomputes the
-// pivot expansion of 256, 512, 1024 (st1..st3) and their logical parities
-// (spar bits: la1 lb1 la2 lb2 la3 lb3) so the kernel's per-quad work is XORs.
+// Thread t handles quad numbers j = t + T i (T = kPassThreads); the planner
+// precomputes the pivot expansion of T, 2T, 4T (st1..st3) and their logical
+// parities (spar bits: la1 lb1 la2 lb2 la3 lb3) so per-quad work is XORs.
 struct GateDesc {     // 48 bytes
   int32_t mat;        // offset (complex elements) in the pass's matrix block
   uint8_t cls;        // GateClass
@@ -67,7 +68,7 @@ struct GateDesc {     // 48 bytes
   uint16_t ma, mb;    // tile-local XOR masks of slot 0 / slot 1
   uint16_t ra, rb;    // tile-local parts of the dual rows
   uint16_t cols;      // kSparse2 / kMono2: 2-bit column codes
-  uint16_t st1, st2, st3;   // pivot-expanded 256, 512, 1024
+  uint16_t st1, st2, st3;   // pivot-expanded T, 2T, 4T
   uint8_t spar;       // parities of st1..st3 against ra / rb
   uint8_t pad[7];
   uint64_t ra_out, rb_out;  // out-of-tile parts of the dual rows (physical bits)

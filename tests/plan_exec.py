@@ -25,6 +25,7 @@ GATE_DT = np.dtype([("mat", "<i4"), ("cls", "u1"), ("plo", "u1"), ("phi", "u1"),
                     ("cols", "<u2"), ("st1", "<u2"), ("st2", "<u2"), ("st3", "<u2"),
                     ("spar", "u1"), ("pad", "u1", (7,)), ("ra_out", "<u8"), ("rb_out", "<u8")],
                    align=True)
+THREADS = 512  # kPassThreads
 (DENSE1, DIAG1, DENSE2, SPARSE2, MONO2, DIAG2, CX01, CX10, PAIRQ, PAIRP, PAIRX, SWAP) = range(12)
 
 
@@ -93,7 +94,7 @@ def _apply(B, g, mats, tbases, k, nvalid):
     per_tile = 1 << (k - nq)
     items = per_tile * nvalid
     j = np.arange(items, dtype=np.int64)
-    t, i = j & 255, j >> 8
+    t, i = j % THREADS, j // THREADS
     bt = _ins0(_ins0(t, int(g["plo"])), int(g["phi"])) if nq == 2 else _ins0(t, int(g["plo"]))
     base, la, lb = bt.copy(), _parity(bt & int(g["ra"])), _parity(bt & int(g["rb"]))
     for bit, st in enumerate((int(g["st1"]), int(g["st2"]), int(g["st3"]))):
