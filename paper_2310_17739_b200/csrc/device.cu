@@ -288,7 +288,7 @@ __device__ __forceinline__ double2 pick(const double2 x0, const double2 x1, cons
   return r;
 }
 
-// A sweep covers one batch of up to 4096 amplitudes: nb tiles of 2^k stored
+// A sweep covers one batch of up to 2^kTileQubitsMax amplitudes: nb tiles of 2^k stored
 // back to back (batch index bits k.. act as extra tile bits no gate touches).
 // Item j = t + T i of thread t (T = kPassThreads); inserting the pivot zeros is linear over
 // disjoint bit-ORs, so base(j) = base(t) | base(256 i) and the logical
@@ -509,7 +509,7 @@ __device__ __forceinline__ void cp_async_wait() {
 constexpr size_t kBlockedSmemBytes = sizeof(double2) * (2 * kTileAmpsMax + kMaxPassMats) +
                                      sizeof(GateDesc) * kMaxPassGates;
 
-__global__ void __launch_bounds__(kPassThreads, 1) k_blocked(BlockedParams p) {
+__global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
   // dynamic shared memory: 2 tile buffers | pass matrices | pass gate descriptors
   extern __shared__ __align__(128) double2 smem[];
   double2* s_mats = smem + 2 * kTileAmpsMax;

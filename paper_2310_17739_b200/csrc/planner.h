@@ -26,10 +26,10 @@
 
 namespace nsb {
 
-constexpr int kTileQubitsMax = 12;               // 4096 amplitudes = 64 KiB per buffer
+constexpr int kTileQubitsMax = 11;               // 2048 amplitudes = 32 KiB per buffer
 constexpr int kTileAmpsMax = 1 << kTileQubitsMax;
-constexpr int kThreadBits = 9;
-constexpr int kPassThreads = 1 << kThreadBits;  // 16 warps per CTA, one CTA per SM
+constexpr int kThreadBits = 8;
+constexpr int kPassThreads = 1 << kThreadBits;  // 8 warps per CTA, two CTAs per SM
 constexpr int kLowQubits = 3;                    // always-tiled qubits 0..2 (128 B runs)
 constexpr int kMaxQubits = 40;
 

@@ -25,7 +25,8 @@ GATE_DT = np.dtype([("mat", "<i4"), ("cls", "u1"), ("plo", "u1"), ("phi", "u1"),
                     ("cols", "<u2"), ("st1", "<u2"), ("st2", "<u2"), ("st3", "<u2"),
                     ("spar", "u1"), ("pad", "u1", (7,)), ("ra_out", "<u8"), ("rb_out", "<u8")],
                    align=True)
-THREADS = 512  # kPassThreads
+THREADS = 256  # kPassThreads
+TILE_MAX = 11  # kTileQubitsMax
 (DENSE1, DIAG1, DENSE2, SPARSE2, MONO2, DIAG2, CX01, CX10, PAIRQ, PAIRP, PAIRX, SWAP) = range(12)
 
 
@@ -155,7 +156,7 @@ def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12, workers=1
         lidx = _scatter(np.arange(1 << k, dtype=np.int64), P["tq"][:k])
         n_tiles = 1 << (n - k)
         tb_all = _scatter(np.arange(n_tiles, dtype=np.int64), P["oq"][:n - k])
-        nb = 1 if k >= 12 else min(1 << (12 - k), 4)
+        nb = 1 if k >= TILE_MAX else min(1 << (TILE_MAX - k), 4)
         block = plan.mats[int(P["mat_begin"]):int(P["mat_begin"]) + int(P["mat_count"])]
         gates = plan.gates[int(P["gate_begin"]):int(P["gate_end"])]
         assert len(gates) <= 64 and len(block) <= 1024
