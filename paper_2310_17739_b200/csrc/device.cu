@@ -336,45 +336,118 @@ __device__ __forceinline__ Sweep make_sweep(int k, int nb, const GateDesc& d, un
   return w;
 }
 
-// member 0 of each coset is the one whose logical slot bits are zero
-template <int MAXI, class F>
-__device__ __forceinline__ void for_items(const Sweep& w, bool two, F f) {
+// Items per thread of one batch (2^kTileQubitsMax amplitudes).
+constexpr int kQuadsPerThread = (1 << kTileQubitsMax) / 4 / kPassThreads;
+constexpr int kPairsPerThread = (1 << kTileQubitsMax) / 2 / kPassThreads;
+static_assert(kQuadsPerThread >= 1 && kQuadsPerThread <= 4, "quad items per thread");
+static_assert(kPairsPerThread <= 8, "pair items per thread");
+
+// Base address (member 0 = logical slot bits zero) of item i of this thread.
+__device__ __forceinline__ int item_base(const Sweep& w, int i, bool two) {
+  int b = w.bt, la = w.la_t, lb = w.lb_t;
+  if (i & 1) {
+    b |= w.st1;
+    la ^= w.spar & 1;
+    lb ^= (w.spar >> 1) & 1;
+  }
+  if (i & 2) {
+    b |= w.st2;
+    la ^= (w.spar >> 2) & 1;
+    lb ^= (w.spar >> 3) & 1;
+  }
+  if (i & 4) {
+    b |= w.st3;
+    la ^= (w.spar >> 4) & 1;
+    lb ^= (w.spar >> 5) & 1;
+  }
+  const int tb = i >> w.tshift;
+  la ^= (w.gma >> tb) & 1;
+  lb ^= (w.gmb >> tb) & 1;
+  return b ^ (la ? w.ma : 0) ^ (two && lb ? w.mb : 0);
+}
+
+// All items are loaded before any is stored: shared-memory stores would
+// otherwise serialise every item's load -> math -> store chain (the compiler
+// cannot prove the item addresses disjoint).
+template <class Compute>
+__device__ __forceinline__ void sweep_quads(double2* __restrict__ tile, const Sweep& w,
+                                            Compute op) {
   if (!w.active) return;
+  int a[kQuadsPerThread];
+  double2 x[kQuadsPerThread][4];
 #pragma unroll
-  for (int i = 0; i < MAXI; ++i) {
-    if (i >= w.n_iter) break;
-    int b = w.bt, la = w.la_t, lb = w.lb_t;
-    if (i & 1) {
-      b |= w.st1;
-      la ^= w.spar & 1;
-      lb ^= (w.spar >> 1) & 1;
+  for (int i = 0; i < kQuadsPerThread; ++i) {
+    a[i] = item_base(w, i, true);
+    if (i < w.n_iter) {
+      x[i][0] = tile[a[i]];
+      x[i][1] = tile[a[i] ^ w.ma];
+      x[i][2] = tile[a[i] ^ w.mb];
+      x[i][3] = tile[a[i] ^ w.ma ^ w.mb];
     }
-    if (i & 2) {
-      b |= w.st2;
-      la ^= (w.spar >> 2) & 1;
-      lb ^= (w.spar >> 3) & 1;
+  }
+#pragma unroll
+  for (int i = 0; i < kQuadsPerThread; ++i)
+    if (i < w.n_iter) op(x[i]);
+#pragma unroll
+  for (int i = 0; i < kQuadsPerThread; ++i) {
+    if (i < w.n_iter) {
+      tile[a[i]] = x[i][0];
+      tile[a[i] ^ w.ma] = x[i][1];
+      tile[a[i] ^ w.mb] = x[i][2];
+      tile[a[i] ^ w.ma ^ w.mb] = x[i][3];
     }
-    if (i & 4) {
-      b |= w.st3;
-      la ^= (w.spar >> 4) & 1;
-      lb ^= (w.spar >> 5) & 1;
-    }
-    const int tb = i >> w.tshift;
-    la ^= (w.gma >> tb) & 1;
-    lb ^= (w.gmb >> tb) & 1;
-    const int a0 = b ^ (la ? w.ma : 0) ^ (two && lb ? w.mb : 0);
-    f(a0);
   }
 }
 
-template <class F>
-__device__ __forceinline__ void for_quads(const Sweep& w, F f) {
-  for_items<4>(w, true, [&](int a0) { f(a0, a0 ^ w.ma, a0 ^ w.mb, a0 ^ w.ma ^ w.mb); });
+// exact permutation: swap members S and T of every quad
+template <int S, int T>
+__device__ __forceinline__ void sweep_swap(double2* __restrict__ tile, const Sweep& w) {
+  if (!w.active) return;
+  int as[kQuadsPerThread], at[kQuadsPerThread];
+  double2 xs[kQuadsPerThread], xt[kQuadsPerThread];
+#pragma unroll
+  for (int i = 0; i < kQuadsPerThread; ++i) {
+    const int a0 = item_base(w, i, true);
+    as[i] = a0 ^ ((S & 1) ? w.ma : 0) ^ ((S & 2) ? w.mb : 0);
+    at[i] = a0 ^ ((T & 1) ? w.ma : 0) ^ ((T & 2) ? w.mb : 0);
+    if (i < w.n_iter) {
+      xs[i] = tile[as[i]];
+      xt[i] = tile[at[i]];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kQuadsPerThread; ++i) {
+    if (i < w.n_iter) {
+      tile[as[i]] = xt[i];
+      tile[at[i]] = xs[i];
+    }
+  }
 }
 
-template <class F>
-__device__ __forceinline__ void for_pairs(const Sweep& w, F f) {
-  for_items<8>(w, false, [&](int a0) { f(a0, a0 ^ w.ma); });
+template <class Compute>
+__device__ __forceinline__ void sweep_pairs(double2* __restrict__ tile, const Sweep& w,
+                                            Compute op) {
+  if (!w.active) return;
+  int a[kPairsPerThread];
+  double2 x[kPairsPerThread], y[kPairsPerThread];
+#pragma unroll
+  for (int i = 0; i < kPairsPerThread; ++i) {
+    a[i] = item_base(w, i, false);
+    if (i < w.n_iter) {
+      x[i] = tile[a[i]];
+      y[i] = tile[a[i] ^ w.ma];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kPairsPerThread; ++i)
+    if (i < w.n_iter) op(x[i], y[i]);
+#pragma unroll
+  for (int i = 0; i < kPairsPerThread; ++i) {
+    if (i < w.n_iter) {
+      tile[a[i]] = x[i];
+      tile[a[i] ^ w.ma] = y[i];
+    }
+  }
 }
 
 __device__ __forceinline__ void apply_gate(double2* __restrict__ tile, int k, int nb,
@@ -383,110 +456,92 @@ __device__ __forceinline__ void apply_gate(double2* __restrict__ tile, int k, in
   const Sweep w = make_sweep(k, nb, d, gm);
   if (d.nq == 1) {
     if (d.cls == kDiag1) {
-      const double2 d0 = *(m), d1 = *(m + 1);
-      for_pairs(w, [&](int i0, int i1) {
-        tile[i0] = cmul(d0, tile[i0]);
-        tile[i1] = cmul(d1, tile[i1]);
+      const double2 d0 = m[0], d1 = m[1];
+      sweep_pairs(tile, w, [&](double2& x, double2& y) {
+        x = cmul(d0, x);
+        y = cmul(d1, y);
       });
     } else {
-      const double2 m0 = *(m), m1 = *(m + 1), m2 = *(m + 2), m3 = *(m + 3);
-      for_pairs(w, [&](int i0, int i1) {
-        double2 x = tile[i0], y = tile[i1];
-        mix2(x, y, m0, m1, m2, m3);
-        tile[i0] = x;
-        tile[i1] = y;
-      });
+      const double2 m0 = m[0], m1 = m[1], m2 = m[2], m3 = m[3];
+      sweep_pairs(tile, w, [&](double2& x, double2& y) { mix2(x, y, m0, m1, m2, m3); });
     }
     return;
   }
   switch (d.cls) {
-    case kCX01:
-    case kCX10:
-    case kSwap: {
-      const int s = d.cls == kCX01 ? 1 : 2, t = d.cls == kSwap ? 2 : 3;
-      const int os = d.cls == kCX01 ? 1 : (d.cls == kCX10 ? 2 : 1);
-      (void)s;
-      for_quads(w, [&](int i0, int i1, int i2, int i3) {
-        const int x = os == 1 ? i1 : i2, y = t == 3 ? i3 : i2;
-        const double2 a = tile[x], b = tile[y];
-        tile[x] = b;
-        tile[y] = a;
-        (void)i0;
-      });
-      break;
-    }
+    case kCX01: sweep_swap<1, 3>(tile, w); break;
+    case kCX10: sweep_swap<2, 3>(tile, w); break;
+    case kSwap: sweep_swap<1, 2>(tile, w); break;
     case kPairQ:
     case kPairP:
     case kPairX: {
-      const double2 m0 = *(m), m1 = *(m + 1), m2 = *(m + 2), m3 = *(m + 3);
-      const double2 n0 = *(m + 4), n1 = *(m + 5), n2 = *(m + 6), n3 = *(m + 7);
-      const int cls = d.cls;
-      for_quads(w, [&](int i0, int i1, int i2, int i3) {
-        // block 0 on members (u0,u1), block 1 on (u2,u3)
-        const int u0 = i0;
-        const int u1 = cls == kPairQ ? i2 : (cls == kPairP ? i1 : i3);
-        const int u2 = cls == kPairP ? i2 : i1;
-        const int u3 = cls == kPairQ ? i3 : (cls == kPairP ? i3 : i2);
-        double2 x = tile[u0], y = tile[u1], z = tile[u2], v = tile[u3];
-        mix2(x, y, m0, m1, m2, m3);
-        mix2(z, v, n0, n1, n2, n3);
-        tile[u0] = x;
-        tile[u1] = y;
-        tile[u2] = z;
-        tile[u3] = v;
-      });
+      const double2 m0 = m[0], m1 = m[1], m2 = m[2], m3 = m[3];
+      const double2 n0 = m[4], n1 = m[5], n2 = m[6], n3 = m[7];
+      if (d.cls == kPairQ) {
+        sweep_quads(tile, w, [&](double2 (&x)[4]) {
+          mix2(x[0], x[2], m0, m1, m2, m3);
+          mix2(x[1], x[3], n0, n1, n2, n3);
+        });
+      } else if (d.cls == kPairP) {
+        sweep_quads(tile, w, [&](double2 (&x)[4]) {
+          mix2(x[0], x[1], m0, m1, m2, m3);
+          mix2(x[2], x[3], n0, n1, n2, n3);
+        });
+      } else {
+        sweep_quads(tile, w, [&](double2 (&x)[4]) {
+          mix2(x[0], x[3], m0, m1, m2, m3);
+          mix2(x[1], x[2], n0, n1, n2, n3);
+        });
+      }
       break;
     }
     case kDiag2: {
-      const double2 d0 = *(m), d1 = *(m + 1), d2 = *(m + 2), d3 = *(m + 3);
-      for_quads(w, [&](int i0, int i1, int i2, int i3) {
-        tile[i0] = cmul(d0, tile[i0]);
-        tile[i1] = cmul(d1, tile[i1]);
-        tile[i2] = cmul(d2, tile[i2]);
-        tile[i3] = cmul(d3, tile[i3]);
+      const double2 d0 = m[0], d1 = m[1], d2 = m[2], d3 = m[3];
+      sweep_quads(tile, w, [&](double2 (&x)[4]) {
+        x[0] = cmul(d0, x[0]);
+        x[1] = cmul(d1, x[1]);
+        x[2] = cmul(d2, x[2]);
+        x[3] = cmul(d3, x[3]);
       });
       break;
     }
     case kMono2: {
-      const double2 v0 = *(m), v1 = *(m + 1), v2 = *(m + 2), v3 = *(m + 3);
+      const double2 v0 = m[0], v1 = m[1], v2 = m[2], v3 = m[3];
       const int c0 = d.cols & 3, c1 = (d.cols >> 2) & 3, c2 = (d.cols >> 4) & 3,
                 c3 = (d.cols >> 6) & 3;
-      for_quads(w, [&](int i0, int i1, int i2, int i3) {
-        const double2 x0 = tile[i0], x1 = tile[i1], x2 = tile[i2], x3 = tile[i3];
-        tile[i0] = cmul(v0, pick(x0, x1, x2, x3, c0));
-        tile[i1] = cmul(v1, pick(x0, x1, x2, x3, c1));
-        tile[i2] = cmul(v2, pick(x0, x1, x2, x3, c2));
-        tile[i3] = cmul(v3, pick(x0, x1, x2, x3, c3));
+      sweep_quads(tile, w, [&](double2 (&x)[4]) {
+        const double2 x0 = x[0], x1 = x[1], x2 = x[2], x3 = x[3];
+        x[0] = cmul(v0, pick(x0, x1, x2, x3, c0));
+        x[1] = cmul(v1, pick(x0, x1, x2, x3, c1));
+        x[2] = cmul(v2, pick(x0, x1, x2, x3, c2));
+        x[3] = cmul(v3, pick(x0, x1, x2, x3, c3));
       });
       break;
     }
     case kSparse2: {
       const unsigned cols = d.cols;
-      for_quads(w, [&](int i0, int i1, int i2, int i3) {
-        const double2 x0 = tile[i0], x1 = tile[i1], x2 = tile[i2], x3 = tile[i3];
-        const int idx[4] = {i0, i1, i2, i3};
+      sweep_quads(tile, w, [&](double2 (&x)[4]) {
+        const double2 x0 = x[0], x1 = x[1], x2 = x[2], x3 = x[3];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           double2 o = make_double2(0.0, 0.0);
-          cmac(o, *(m + 2 * r), pick(x0, x1, x2, x3, (cols >> (4 * r)) & 3));
-          cmac(o, *(m + 2 * r + 1), pick(x0, x1, x2, x3, (cols >> (4 * r + 2)) & 3));
-          tile[idx[r]] = o;
+          cmac(o, m[2 * r], pick(x0, x1, x2, x3, (cols >> (4 * r)) & 3));
+          cmac(o, m[2 * r + 1], pick(x0, x1, x2, x3, (cols >> (4 * r + 2)) & 3));
+          x[r] = o;
         }
       });
       break;
     }
-    default: {  // kDense2
-      for_quads(w, [&](int i0, int i1, int i2, int i3) {
-        const double2 x0 = tile[i0], x1 = tile[i1], x2 = tile[i2], x3 = tile[i3];
-        const int idx[4] = {i0, i1, i2, i3};
+    default: {  // kDense2: matrix rows streamed from shared memory
+      sweep_quads(tile, w, [&](double2 (&x)[4]) {
+        const double2 x0 = x[0], x1 = x[1], x2 = x[2], x3 = x[3];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           double2 o = make_double2(0.0, 0.0);
-          cmac(o, *(m + 4 * r + 0), x0);
-          cmac(o, *(m + 4 * r + 1), x1);
-          cmac(o, *(m + 4 * r + 2), x2);
-          cmac(o, *(m + 4 * r + 3), x3);
-          tile[idx[r]] = o;
+          cmac(o, m[4 * r + 0], x0);
+          cmac(o, m[4 * r + 1], x1);
+          cmac(o, m[4 * r + 2], x2);
+          cmac(o, m[4 * r + 3], x3);
+          x[r] = o;
         }
       });
       break;
