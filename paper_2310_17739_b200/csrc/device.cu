@@ -336,212 +336,174 @@ __device__ __forceinline__ Sweep make_sweep(int k, int nb, const GateDesc& d, un
   return w;
 }
 
-// Items per thread of one batch (2^kTileQubitsMax amplitudes).
-constexpr int kQuadsPerThread = (1 << kTileQubitsMax) / 4 / kPassThreads;
-constexpr int kPairsPerThread = (1 << kTileQubitsMax) / 2 / kPassThreads;
-static_assert(kQuadsPerThread >= 1 && kQuadsPerThread <= 4, "quad items per thread");
-static_assert(kPairsPerThread <= 8, "pair items per thread");
-
-// Base address (member 0 = logical slot bits zero) of item i of this thread.
-__device__ __forceinline__ int item_base(const Sweep& w, int i, bool two) {
-  int b = w.bt, la = w.la_t, lb = w.lb_t;
-  if (i & 1) {
-    b |= w.st1;
-    la ^= w.spar & 1;
-    lb ^= (w.spar >> 1) & 1;
-  }
-  if (i & 2) {
-    b |= w.st2;
-    la ^= (w.spar >> 2) & 1;
-    lb ^= (w.spar >> 3) & 1;
-  }
-  if (i & 4) {
-    b |= w.st3;
-    la ^= (w.spar >> 4) & 1;
-    lb ^= (w.spar >> 5) & 1;
-  }
-  const int tb = i >> w.tshift;
-  la ^= (w.gma >> tb) & 1;
-  lb ^= (w.gmb >> tb) & 1;
-  return b ^ (la ? w.ma : 0) ^ (two && lb ? w.mb : 0);
-}
-
-// All items are loaded before any is stored: shared-memory stores would
-// otherwise serialise every item's load -> math -> store chain (the compiler
-// cannot prove the item addresses disjoint).
-template <class Compute>
-__device__ __forceinline__ void sweep_quads(double2* __restrict__ tile, const Sweep& w,
-                                            Compute op) {
+// member 0 of each coset is the one whose logical slot bits are zero
+template <int MAXI, class F>
+__device__ __forceinline__ void for_items(const Sweep& w, bool two, F f) {
   if (!w.active) return;
-  int a[kQuadsPerThread];
-  double2 x[kQuadsPerThread][4];
 #pragma unroll
-  for (int i = 0; i < kQuadsPerThread; ++i) {
-    a[i] = item_base(w, i, true);
-    if (i < w.n_iter) {
-      x[i][0] = tile[a[i]];
-      x[i][1] = tile[a[i] ^ w.ma];
-      x[i][2] = tile[a[i] ^ w.mb];
-      x[i][3] = tile[a[i] ^ w.ma ^ w.mb];
+  for (int i = 0; i < MAXI; ++i) {
+    if (i >= w.n_iter) break;
+    int b = w.bt, la = w.la_t, lb = w.lb_t;
+    if (i & 1) {
+      b |= w.st1;
+      la ^= w.spar & 1;
+      lb ^= (w.spar >> 1) & 1;
     }
-  }
-#pragma unroll
-  for (int i = 0; i < kQuadsPerThread; ++i)
-    if (i < w.n_iter) op(x[i]);
-#pragma unroll
-  for (int i = 0; i < kQuadsPerThread; ++i) {
-    if (i < w.n_iter) {
-      tile[a[i]] = x[i][0];
-      tile[a[i] ^ w.ma] = x[i][1];
-      tile[a[i] ^ w.mb] = x[i][2];
-      tile[a[i] ^ w.ma ^ w.mb] = x[i][3];
+    if (i & 2) {
+      b |= w.st2;
+      la ^= (w.spar >> 2) & 1;
+      lb ^= (w.spar >> 3) & 1;
     }
-  }
-}
-
-// exact permutation: swap members S and T of every quad
-template <int S, int T>
-__device__ __forceinline__ void sweep_swap(double2* __restrict__ tile, const Sweep& w) {
-  if (!w.active) return;
-  int as[kQuadsPerThread], at[kQuadsPerThread];
-  double2 xs[kQuadsPerThread], xt[kQuadsPerThread];
-#pragma unroll
-  for (int i = 0; i < kQuadsPerThread; ++i) {
-    const int a0 = item_base(w, i, true);
-    as[i] = a0 ^ ((S & 1) ? w.ma : 0) ^ ((S & 2) ? w.mb : 0);
-    at[i] = a0 ^ ((T & 1) ? w.ma : 0) ^ ((T & 2) ? w.mb : 0);
-    if (i < w.n_iter) {
-      xs[i] = tile[as[i]];
-      xt[i] = tile[at[i]];
+    if (i & 4) {
+      b |= w.st3;
+      la ^= (w.spar >> 4) & 1;
+      lb ^= (w.spar >> 5) & 1;
     }
-  }
-#pragma unroll
-  for (int i = 0; i < kQuadsPerThread; ++i) {
-    if (i < w.n_iter) {
-      tile[as[i]] = xt[i];
-      tile[at[i]] = xs[i];
-    }
+    const int tb = i >> w.tshift;
+    la ^= (w.gma >> tb) & 1;
+    lb ^= (w.gmb >> tb) & 1;
+    const int a0 = b ^ (la ? w.ma : 0) ^ (two && lb ? w.mb : 0);
+    f(a0);
   }
 }
 
-template <class Compute>
-__device__ __forceinline__ void sweep_pairs(double2* __restrict__ tile, const Sweep& w,
-                                            Compute op) {
-  if (!w.active) return;
-  int a[kPairsPerThread];
-  double2 x[kPairsPerThread], y[kPairsPerThread];
-#pragma unroll
-  for (int i = 0; i < kPairsPerThread; ++i) {
-    a[i] = item_base(w, i, false);
-    if (i < w.n_iter) {
-      x[i] = tile[a[i]];
-      y[i] = tile[a[i] ^ w.ma];
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < kPairsPerThread; ++i)
-    if (i < w.n_iter) op(x[i], y[i]);
-#pragma unroll
-  for (int i = 0; i < kPairsPerThread; ++i) {
-    if (i < w.n_iter) {
-      tile[a[i]] = x[i];
-      tile[a[i] ^ w.ma] = y[i];
-    }
-  }
+template <class F>
+__device__ __forceinline__ void for_quads(const Sweep& w, F f) {
+  for_items<4>(w, true, [&](int a0) { f(a0, a0 ^ w.ma, a0 ^ w.mb, a0 ^ w.ma ^ w.mb); });
 }
 
-__device__ __forceinline__ void apply_gate(double2* __restrict__ tile, int k, int nb,
+template <class F>
+__device__ __forceinline__ void for_pairs(const Sweep& w, F f) {
+  for_items<8>(w, false, [&](int a0) { f(a0, a0 ^ w.ma); });
+}
+
+// Out of place: every gate reads `src` and writes all members to `dst`
+// (different buffers, both __restrict__), so the next item's loads never wait
+// on this item's stores -- in place, the compiler must keep each item's
+// load -> math -> store chain in order because the addresses may alias.
+__device__ __forceinline__ void apply_gate(const double2* __restrict__ src,
+                                           double2* __restrict__ dst, int k, int nb,
                                            const GateDesc& d, const double2* __restrict__ m,
                                            unsigned gm) {
   const Sweep w = make_sweep(k, nb, d, gm);
   if (d.nq == 1) {
     if (d.cls == kDiag1) {
-      const double2 d0 = m[0], d1 = m[1];
-      sweep_pairs(tile, w, [&](double2& x, double2& y) {
-        x = cmul(d0, x);
-        y = cmul(d1, y);
+      const double2 d0 = *(m), d1 = *(m + 1);
+      for_pairs(w, [&](int i0, int i1) {
+        dst[i0] = cmul(d0, src[i0]);
+        dst[i1] = cmul(d1, src[i1]);
       });
     } else {
-      const double2 m0 = m[0], m1 = m[1], m2 = m[2], m3 = m[3];
-      sweep_pairs(tile, w, [&](double2& x, double2& y) { mix2(x, y, m0, m1, m2, m3); });
+      const double2 m0 = *(m), m1 = *(m + 1), m2 = *(m + 2), m3 = *(m + 3);
+      for_pairs(w, [&](int i0, int i1) {
+        double2 x = src[i0], y = src[i1];
+        mix2(x, y, m0, m1, m2, m3);
+        dst[i0] = x;
+        dst[i1] = y;
+      });
     }
     return;
   }
   switch (d.cls) {
-    case kCX01: sweep_swap<1, 3>(tile, w); break;
-    case kCX10: sweep_swap<2, 3>(tile, w); break;
-    case kSwap: sweep_swap<1, 2>(tile, w); break;
+    case kCX01:  // swaps members 1, 3
+      for_quads(w, [&](int i0, int i1, int i2, int i3) {
+        const double2 x0 = src[i0], x1 = src[i1], x2 = src[i2], x3 = src[i3];
+        dst[i0] = x0;
+        dst[i1] = x3;
+        dst[i2] = x2;
+        dst[i3] = x1;
+      });
+      break;
+    case kCX10:  // swaps members 2, 3
+      for_quads(w, [&](int i0, int i1, int i2, int i3) {
+        const double2 x0 = src[i0], x1 = src[i1], x2 = src[i2], x3 = src[i3];
+        dst[i0] = x0;
+        dst[i1] = x1;
+        dst[i2] = x3;
+        dst[i3] = x2;
+      });
+      break;
+    case kSwap:  // swaps members 1, 2
+      for_quads(w, [&](int i0, int i1, int i2, int i3) {
+        const double2 x0 = src[i0], x1 = src[i1], x2 = src[i2], x3 = src[i3];
+        dst[i0] = x0;
+        dst[i1] = x2;
+        dst[i2] = x1;
+        dst[i3] = x3;
+      });
+      break;
     case kPairQ:
     case kPairP:
     case kPairX: {
-      const double2 m0 = m[0], m1 = m[1], m2 = m[2], m3 = m[3];
-      const double2 n0 = m[4], n1 = m[5], n2 = m[6], n3 = m[7];
-      if (d.cls == kPairQ) {
-        sweep_quads(tile, w, [&](double2 (&x)[4]) {
-          mix2(x[0], x[2], m0, m1, m2, m3);
-          mix2(x[1], x[3], n0, n1, n2, n3);
-        });
-      } else if (d.cls == kPairP) {
-        sweep_quads(tile, w, [&](double2 (&x)[4]) {
-          mix2(x[0], x[1], m0, m1, m2, m3);
-          mix2(x[2], x[3], n0, n1, n2, n3);
-        });
-      } else {
-        sweep_quads(tile, w, [&](double2 (&x)[4]) {
-          mix2(x[0], x[3], m0, m1, m2, m3);
-          mix2(x[1], x[2], n0, n1, n2, n3);
-        });
-      }
+      const double2 m0 = *(m), m1 = *(m + 1), m2 = *(m + 2), m3 = *(m + 3);
+      const double2 n0 = *(m + 4), n1 = *(m + 5), n2 = *(m + 6), n3 = *(m + 7);
+      const int cls = d.cls;
+      for_quads(w, [&](int i0, int i1, int i2, int i3) {
+        // block 0 on members (u0,u1), block 1 on (u2,u3)
+        const int u0 = i0;
+        const int u1 = cls == kPairQ ? i2 : (cls == kPairP ? i1 : i3);
+        const int u2 = cls == kPairP ? i2 : i1;
+        const int u3 = cls == kPairQ ? i3 : (cls == kPairP ? i3 : i2);
+        double2 x = src[u0], y = src[u1], z = src[u2], v = src[u3];
+        mix2(x, y, m0, m1, m2, m3);
+        mix2(z, v, n0, n1, n2, n3);
+        dst[u0] = x;
+        dst[u1] = y;
+        dst[u2] = z;
+        dst[u3] = v;
+      });
       break;
     }
     case kDiag2: {
-      const double2 d0 = m[0], d1 = m[1], d2 = m[2], d3 = m[3];
-      sweep_quads(tile, w, [&](double2 (&x)[4]) {
-        x[0] = cmul(d0, x[0]);
-        x[1] = cmul(d1, x[1]);
-        x[2] = cmul(d2, x[2]);
-        x[3] = cmul(d3, x[3]);
+      const double2 d0 = *(m), d1 = *(m + 1), d2 = *(m + 2), d3 = *(m + 3);
+      for_quads(w, [&](int i0, int i1, int i2, int i3) {
+        dst[i0] = cmul(d0, src[i0]);
+        dst[i1] = cmul(d1, src[i1]);
+        dst[i2] = cmul(d2, src[i2]);
+        dst[i3] = cmul(d3, src[i3]);
       });
       break;
     }
     case kMono2: {
-      const double2 v0 = m[0], v1 = m[1], v2 = m[2], v3 = m[3];
+      const double2 v0 = *(m), v1 = *(m + 1), v2 = *(m + 2), v3 = *(m + 3);
       const int c0 = d.cols & 3, c1 = (d.cols >> 2) & 3, c2 = (d.cols >> 4) & 3,
                 c3 = (d.cols >> 6) & 3;
-      sweep_quads(tile, w, [&](double2 (&x)[4]) {
-        const double2 x0 = x[0], x1 = x[1], x2 = x[2], x3 = x[3];
-        x[0] = cmul(v0, pick(x0, x1, x2, x3, c0));
-        x[1] = cmul(v1, pick(x0, x1, x2, x3, c1));
-        x[2] = cmul(v2, pick(x0, x1, x2, x3, c2));
-        x[3] = cmul(v3, pick(x0, x1, x2, x3, c3));
+      for_quads(w, [&](int i0, int i1, int i2, int i3) {
+        const double2 x0 = src[i0], x1 = src[i1], x2 = src[i2], x3 = src[i3];
+        dst[i0] = cmul(v0, pick(x0, x1, x2, x3, c0));
+        dst[i1] = cmul(v1, pick(x0, x1, x2, x3, c1));
+        dst[i2] = cmul(v2, pick(x0, x1, x2, x3, c2));
+        dst[i3] = cmul(v3, pick(x0, x1, x2, x3, c3));
       });
       break;
     }
     case kSparse2: {
       const unsigned cols = d.cols;
-      sweep_quads(tile, w, [&](double2 (&x)[4]) {
-        const double2 x0 = x[0], x1 = x[1], x2 = x[2], x3 = x[3];
+      for_quads(w, [&](int i0, int i1, int i2, int i3) {
+        const double2 x0 = src[i0], x1 = src[i1], x2 = src[i2], x3 = src[i3];
+        const int idx[4] = {i0, i1, i2, i3};
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           double2 o = make_double2(0.0, 0.0);
-          cmac(o, m[2 * r], pick(x0, x1, x2, x3, (cols >> (4 * r)) & 3));
-          cmac(o, m[2 * r + 1], pick(x0, x1, x2, x3, (cols >> (4 * r + 2)) & 3));
-          x[r] = o;
+          cmac(o, *(m + 2 * r), pick(x0, x1, x2, x3, (cols >> (4 * r)) & 3));
+          cmac(o, *(m + 2 * r + 1), pick(x0, x1, x2, x3, (cols >> (4 * r + 2)) & 3));
+          dst[idx[r]] = o;
         }
       });
       break;
     }
-    default: {  // kDense2: matrix rows streamed from shared memory
-      sweep_quads(tile, w, [&](double2 (&x)[4]) {
-        const double2 x0 = x[0], x1 = x[1], x2 = x[2], x3 = x[3];
+    default: {  // kDense2
+      for_quads(w, [&](int i0, int i1, int i2, int i3) {
+        const double2 x0 = src[i0], x1 = src[i1], x2 = src[i2], x3 = src[i3];
+        const int idx[4] = {i0, i1, i2, i3};
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           double2 o = make_double2(0.0, 0.0);
-          cmac(o, m[4 * r + 0], x0);
-          cmac(o, m[4 * r + 1], x1);
-          cmac(o, m[4 * r + 2], x2);
-          cmac(o, m[4 * r + 3], x3);
-          x[r] = o;
+          cmac(o, *(m + 4 * r + 0), x0);
+          cmac(o, *(m + 4 * r + 1), x1);
+          cmac(o, *(m + 4 * r + 2), x2);
+          cmac(o, *(m + 4 * r + 3), x3);
+          dst[idx[r]] = o;
         }
       });
       break;
@@ -561,13 +523,14 @@ __device__ __forceinline__ void cp_async_wait() {
 
 // One persistent CTA per SM; while the gate sweeps of tile i run, tile i+1 of
 // the same pass streams into the other shared-memory buffer with cp.async.
-constexpr size_t kBlockedSmemBytes = sizeof(double2) * (2 * kTileAmpsMax + kMaxPassMats) +
+constexpr size_t kBlockedSmemBytes = sizeof(double2) * (3 * kTileAmpsMax + kMaxPassMats) +
                                      sizeof(GateDesc) * kMaxPassGates;
 
 __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
-  // dynamic shared memory: 2 tile buffers | pass matrices | pass gate descriptors
+  // dynamic shared memory: 3 batch buffers (current, gate-sweep target,
+  // prefetch) | pass matrices | pass gate descriptors
   extern __shared__ __align__(128) double2 smem[];
-  double2* s_mats = smem + 2 * kTileAmpsMax;
+  double2* s_mats = smem + 3 * kTileAmpsMax;
   GateDesc* s_gates = reinterpret_cast<GateDesc*>(s_mats + kMaxPassMats);
   __shared__ PassDesc sp;
   __shared__ uint64_t s_hi[1 << (kTileQubitsMax - kThreadBits)];  // offsets of tile bits >= kThreadBits
@@ -625,23 +588,25 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
     const uint64_t t_end = t_begin + per + (blockIdx.x < extra ? 1 : 0);
     auto issue_batch = [&](uint64_t t0, double2* buf) {
       if (!loader) return;
+#pragma unroll 1
       for (int b = 0; b < nb && t0 + b < t_end; ++b) {
         const uint64_t base = tile_base(t0 + b) | lo;
         double2* dst = buf + (b << k);
+#pragma unroll 2
         for (int j = 0; j < n_j; ++j)
           cp_async16(dst + tid + (j << kThreadBits), p.amps + (base | s_hi[j]));
       }
     };
 
-    int cur = 0;
+    int cur = 0, pre = 1, spare = 2;  // buffer roles (rotate)
     if (t_begin < t_end) issue_batch(t_begin, smem);
     cp_async_commit();
-    for (uint64_t t0 = t_begin; t0 < t_end; t0 += nb, cur ^= 1) {
+    for (uint64_t t0 = t_begin; t0 < t_end; t0 += nb) {
       double2* tile = smem + cur * kTileAmpsMax;
       const int nvalid = t_end - t0 < uint64_t(nb) ? static_cast<int>(t_end - t0) : nb;
       uint64_t tbase[4];
       for (int b = 0; b < 4; ++b) tbase[b] = b < nvalid ? tile_base(t0 + b) : 0;
-      if (t0 + nb < t_end) issue_batch(t0 + nb, smem + (cur ^ 1) * kTileAmpsMax);
+      if (t0 + nb < t_end) issue_batch(t0 + nb, smem + pre * kTileAmpsMax);
       cp_async_commit();
       cp_async_wait<1>();  // this batch has landed (the next may be in flight)
       if (tid < n_gates) {  // out-of-tile dual-row parities per (gate, tile of the batch)
@@ -660,8 +625,9 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
       if (sp.collapse_q >= 0) {  // pending collapse (engine.py:164-167)
         const int cq = sp.collapse_q;
         if (loader)
-#pragma unroll
+#pragma unroll 1
           for (int b = 0; b < 4; ++b)
+#pragma unroll 1
             for (int j = 0; j < n_j && b < nvalid; ++j) {
               const uint64_t g = tbase[b] | lo | s_hi[j];
               double2& v = tile[(b << k) + tid + (j << kThreadBits)];
@@ -674,19 +640,25 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
             }
         __syncthreads();
       }
+#pragma unroll 1
       for (int g = 0; g < n_gates; ++g) {
         const GateDesc d = s_gates[g];
-        apply_gate(tile, k, nvalid, d, s_mats + d.mat, s_gm[g]);
+        double2* out = smem + spare * kTileAmpsMax;
+        apply_gate(tile, out, k, nvalid, d, s_mats + d.mat, s_gm[g]);
+        const int tmp = cur;
+        cur = spare;
+        spare = tmp;
+        tile = out;
         __syncthreads();
       }
       // shared -> global (+ assertion epilogue partial sums)
       if (loader) {
         const int mq = sp.measure_q;
-#pragma unroll
+#pragma unroll 1
         for (int b = 0; b < 4; ++b) {
           if (b >= nvalid) break;
           const uint64_t base = tbase[b] | lo;
-#pragma unroll 4
+#pragma unroll 2
           for (int j = 0; j < n_j; ++j) {
             const uint64_t g = base | s_hi[j];
             const double2 v = tile[(b << k) + tid + (j << kThreadBits)];
@@ -699,6 +671,9 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
         }
       }
       __syncthreads();  // buffer `cur` is free for the batch issued next iteration
+      const int done = cur;  // next batch lives in `pre`; `done` takes the next prefetch
+      cur = pre;
+      pre = done;
     }
     cp_async_wait<0>();
     const int mq = sp.measure_q;

@@ -76,8 +76,8 @@ struct GateDesc {     // 48 bytes
 
 // Per pass the kernel stages the gate descriptors and the pass's own block
 // of packed matrices in shared memory (bounded by these limits).
-constexpr int kMaxPassGates = 64;
-constexpr int kMaxPassMats = 1024;  // complex elements (16 KiB)
+constexpr int kMaxPassGates = 48;
+constexpr int kMaxPassMats = 512;   // complex elements (8 KiB)
 
 struct PassDesc {         // 112 bytes
   int32_t gate_begin, gate_end;

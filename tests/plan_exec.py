@@ -159,7 +159,7 @@ def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12, workers=1
         nb = 1 if k >= TILE_MAX else min(1 << (TILE_MAX - k), 4)
         block = plan.mats[int(P["mat_begin"]):int(P["mat_begin"]) + int(P["mat_count"])]
         gates = plan.gates[int(P["gate_begin"]):int(P["gate_end"])]
-        assert len(gates) <= 64 and len(block) <= 1024
+        assert len(gates) <= 48 and len(block) <= 512
         cq = int(P["collapse_q"])
         per, extra = divmod(n_tiles, workers)
         for cta in range(min(workers, n_tiles)):
