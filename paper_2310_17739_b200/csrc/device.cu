@@ -255,13 +255,11 @@ struct BlockedParams {
 
 // ---- gate sweeps over a shared-memory tile --------------------------------
 // A 2q gate with tile-local XOR masks (ma, mb) acts on the quads
-// {v, v^ma, v^mb, v^ma^mb}; quad representatives are the indices with both
-// pivot bits clear, enumerated by inserting zeros at plo < phi into the quad
-// number.  Member s of a quad (s = bit(slot0) + 2 bit(slot1), the reference's
-// matrix index) lives at base ^ (s&1 ? ma : 0) ^ (s&2 ? mb : 0).  1q gates use
-// pairs {v, v^ma}.  Tiles are stored unswizzled: a quarter-warp's 8 bases
-// differ in their low non-pivot bits, so 16-byte accesses are conflict-free
-// unless a pivot sits in bits 0..2.
+// {v, v^ma, v^mb, v^ma^mb}; 1q gates on pairs {v, v^ma}.  Member s of a quad
+// (s = bit(slot0) + 2 bit(slot1), the reference's matrix index) is the one
+// whose logical slot bits spell s.  Batches live in shared memory under the
+// XOR swizzle swz (device.cuh), which is linear over XOR, so every address is
+// formed from swizzled per-bit offsets precomputed by the planner.
 
 __device__ __forceinline__ int ins0(int j, int pos) {
   return ((j >> pos) << (pos + 1)) | (j & ((1 << pos) - 1));
@@ -288,93 +286,91 @@ __device__ __forceinline__ double2 pick(const double2 x0, const double2 x1, cons
   return r;
 }
 
-// A sweep covers one batch of up to 2^kTileQubitsMax amplitudes: nb tiles of 2^k stored
-// back to back (batch index bits k.. act as extra tile bits no gate touches).
-// Item j = t + T i of thread t (T = kPassThreads); inserting the pivot zeros is linear over
-// disjoint bit-ORs, so base(j) = base(t) | base(256 i) and the logical
-// parities split the same way: per item only XORs remain.  The out-of-tile
-// parity of each tile in the batch is a bit of gmask.
+// A sweep covers one batch (nb tiles of 2^k back to back).  Item j = t + T i
+// of thread t; the planner's per-bit tables (GateDesc.tcol / st*, tla / tlb /
+// spar) give the swizzled representative address and its logical parities as
+// XORs over the bits of t and i (see planner.h).  The out-of-tile parity of
+// each tile of the batch is a bit of gm.
 struct Sweep {
   int n_iter;           // valid items per thread
-  bool active;          // this thread owns work (batches smaller than 256 items)
-  int bt;               // pivot-expanded thread part of the index
-  int st1, st2, st3;    // pivot-expanded 256, 512, 1024
-  int la_t, lb_t;       // logical parities of bt (tile-local part)
-  int spar;             // parities of st1..st3
-  int tshift;           // item iteration i belongs to tile i >> tshift
+  bool active;          // this thread owns work (batches smaller than T items)
+  int bt;               // swizzled offset of the thread bits
+  int la_t, lb_t;       // logical parities of the thread bits
+  int st1, st2, st3, spar;
+  int tile_shift;       // item j lies in tile j >> tile_shift of the batch
   unsigned gma, gmb;    // out-of-tile parities per tile of the batch
-  int ma, mb;
+  int sa, sb;
 };
-
-__device__ __forceinline__ int parity(int x) { return __popc(x) & 1; }
 
 __device__ __forceinline__ Sweep make_sweep(int k, int nb, const GateDesc& d, unsigned gm) {
   Sweep w;
   const int two = d.nq == 2;
-  const int per_tile = 1 << (k - 1 - two);  // items per tile
-  const int items = per_tile * nb;
+  const int lpt = k - 1 - two;  // log2 items per tile
+  const int items = nb << lpt;
   const int t = threadIdx.x;
   w.active = t < items;
   w.n_iter = items > kPassThreads ? items >> kThreadBits : 1;
-  w.tshift = per_tile > kPassThreads ? __ffs(per_tile >> kThreadBits) - 1 : 0;
-  w.bt = two ? ins0(ins0(t, d.plo), d.phi) : ins0(t, d.plo);
+  w.tile_shift = lpt;
+  int bt = 0;
+#pragma unroll
+  for (int b = 0; b < kThreadBits; ++b)
+    if (t >> b & 1) bt ^= d.tcol[b];
+  w.bt = bt;
+  w.la_t = __popc(t & d.tla) & 1;
+  w.lb_t = __popc(t & d.tlb) & 1;
   w.st1 = d.st1;
   w.st2 = d.st2;
   w.st3 = d.st3;
   w.spar = d.spar;
-  w.la_t = parity(w.bt & d.ra);
-  w.lb_t = parity(w.bt & d.rb);
   w.gma = gm & 15u;
   w.gmb = gm >> 4;
-  if (per_tile < kPassThreads) {  // small tiles: thread t sits in tile t / per_tile
-    const int b = t / per_tile;
-    w.gma = (w.gma >> b) & 1u;
-    w.gmb = (w.gmb >> b) & 1u;
-  }
-  w.ma = d.ma;
-  w.mb = d.mb;
+  w.sa = d.sa;
+  w.sb = d.sb;
   return w;
 }
 
-// member 0 of each coset is the one whose logical slot bits are zero
-template <int MAXI, class F>
-__device__ __forceinline__ void for_items(const Sweep& w, bool two, F f) {
-  if (!w.active) return;
-#pragma unroll
-  for (int i = 0; i < MAXI; ++i) {
-    if (i >= w.n_iter) break;
-    int b = w.bt, la = w.la_t, lb = w.lb_t;
-    if (i & 1) {
-      b |= w.st1;
-      la ^= w.spar & 1;
-      lb ^= (w.spar >> 1) & 1;
-    }
-    if (i & 2) {
-      b |= w.st2;
-      la ^= (w.spar >> 2) & 1;
-      lb ^= (w.spar >> 3) & 1;
-    }
-    if (i & 4) {
-      b |= w.st3;
-      la ^= (w.spar >> 4) & 1;
-      lb ^= (w.spar >> 5) & 1;
-    }
-    const int tb = i >> w.tshift;
-    la ^= (w.gma >> tb) & 1;
-    lb ^= (w.gmb >> tb) & 1;
-    const int a0 = b ^ (la ? w.ma : 0) ^ (two && lb ? w.mb : 0);
-    f(a0);
+// swizzled address of member 0 (logical slot bits zero) of item i of this thread
+__device__ __forceinline__ int item_addr(const Sweep& w, int i, bool two) {
+  int a = w.bt, la = w.la_t, lb = w.lb_t;
+  if (i & 1) {
+    a ^= w.st1;
+    la ^= w.spar & 1;
+    lb ^= (w.spar >> 1) & 1;
   }
+  if (i & 2) {
+    a ^= w.st2;
+    la ^= (w.spar >> 2) & 1;
+    lb ^= (w.spar >> 3) & 1;
+  }
+  if (i & 4) {
+    a ^= w.st3;
+    la ^= (w.spar >> 4) & 1;
+    lb ^= (w.spar >> 5) & 1;
+  }
+  const int tile = (threadIdx.x + (i << kThreadBits)) >> w.tile_shift;
+  la ^= (w.gma >> tile) & 1;
+  lb ^= (w.gmb >> tile) & 1;
+  return a ^ (la ? w.sa : 0) ^ (two && lb ? w.sb : 0);
 }
 
 template <class F>
 __device__ __forceinline__ void for_quads(const Sweep& w, F f) {
-  for_items<4>(w, true, [&](int a0) { f(a0, a0 ^ w.ma, a0 ^ w.mb, a0 ^ w.ma ^ w.mb); });
+  if (!w.active) return;
+#pragma unroll 4
+  for (int i = 0; i < w.n_iter; ++i) {
+    const int a0 = item_addr(w, i, true);
+    f(a0, a0 ^ w.sa, a0 ^ w.sb, a0 ^ w.sa ^ w.sb);
+  }
 }
 
 template <class F>
 __device__ __forceinline__ void for_pairs(const Sweep& w, F f) {
-  for_items<8>(w, false, [&](int a0) { f(a0, a0 ^ w.ma); });
+  if (!w.active) return;
+#pragma unroll 4
+  for (int i = 0; i < w.n_iter; ++i) {
+    const int a0 = item_addr(w, i, false);
+    f(a0, a0 ^ w.sa);
+  }
 }
 
 // Out of place: every gate reads `src` and writes all members to `dst`
@@ -591,10 +587,10 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
 #pragma unroll 1
       for (int b = 0; b < nb && t0 + b < t_end; ++b) {
         const uint64_t base = tile_base(t0 + b) | lo;
-        double2* dst = buf + (b << k);
+        double2* dst = buf;
 #pragma unroll 2
         for (int j = 0; j < n_j; ++j)
-          cp_async16(dst + tid + (j << kThreadBits), p.amps + (base | s_hi[j]));
+          cp_async16(dst + swz(tid + (j << kThreadBits) + (b << k)), p.amps + (base | s_hi[j]));
       }
     };
 
@@ -630,7 +626,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
 #pragma unroll 1
             for (int j = 0; j < n_j && b < nvalid; ++j) {
               const uint64_t g = tbase[b] | lo | s_hi[j];
-              double2& v = tile[(b << k) + tid + (j << kThreadBits)];
+              double2& v = tile[swz((b << k) + tid + (j << kThreadBits))];
               if ((g >> cq) & 1) {
                 v = make_double2(0.0, 0.0);
               } else {
@@ -661,7 +657,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
 #pragma unroll 2
           for (int j = 0; j < n_j; ++j) {
             const uint64_t g = base | s_hi[j];
-            const double2 v = tile[(b << k) + tid + (j << kThreadBits)];
+            const double2 v = tile[swz((b << k) + tid + (j << kThreadBits))];
             p.amps[g] = v;
             if (mq >= 0 && !((g >> mq) & 1)) {
               msum = fma(v.x, v.x, msum);

@@ -423,33 +423,53 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
       d.nq = static_cast<uint8_t>(g.nq);
       d.cols = g.cols;
       const uint32_t ma = pext64(g.ma, tset), mb = pext64(g.mb, tset);
-      d.ma = static_cast<uint16_t>(ma);
-      d.mb = static_cast<uint16_t>(mb);
-      d.ra = static_cast<uint16_t>(pext64(g.ra, tset));
-      d.rb = static_cast<uint16_t>(pext64(g.rb, tset));
+      const uint32_t ra = pext64(g.ra, tset), rb = pext64(g.rb, tset);
       d.ra_out = g.ra & ~tset;
       d.rb_out = g.rb & ~tset;
+      // pivots: one bit of ma, and one of mb reduced against ma
       const int pa = lowest_bit(ma);
-      if (g.nq == 1) {
-        d.plo = d.phi = static_cast<uint8_t>(pa);
-      } else {
+      int pbit = -1;
+      if (g.nq == 2) {
         const uint32_t mr = (mb >> pa & 1) ? (mb ^ ma) : mb;
         if (!mr) throw std::logic_error("degenerate gate masks");
-        const int pbit = lowest_bit(mr);
-        d.plo = static_cast<uint8_t>(std::min(pa, pbit));
-        d.phi = static_cast<uint8_t>(std::max(pa, pbit));
+        pbit = lowest_bit(mr);
       }
-      auto ins0 = [](uint32_t j, int pos) { return ((j >> pos) << (pos + 1)) | (j & ((1u << pos) - 1)); };
-      auto expand = [&](uint32_t j) { return g.nq == 2 ? ins0(ins0(j, d.plo), d.phi) : ins0(j, d.plo); };
-      const uint32_t st[3] = {expand(kPassThreads), expand(2 * kPassThreads),
-                              expand(4 * kPassThreads)};
-      d.st1 = static_cast<uint16_t>(st[0]);
-      d.st2 = static_cast<uint16_t>(st[1]);
-      d.st3 = static_cast<uint16_t>(st[2]);
+      // free positions: tile-local non-pivot bits (first three with distinct
+      // residues mod 3 for conflict-free quarter-warps), then batch bits
+      std::vector<int> local, pos;
+      for (int p = 0; p < k; ++p)
+        if (p != pa && p != pbit) local.push_back(p);
+      for (int r = 0; r < 3; ++r)
+        for (size_t i = 0; i < local.size(); ++i)
+          if (local[i] >= 0 && local[i] % 3 == r) {
+            pos.push_back(local[i]);
+            local[i] = -1;
+            break;
+          }
+      for (int p : local)
+        if (p >= 0) pos.push_back(p);
+      for (int b = 0; b < 8; ++b) pos.push_back(k + b);  // tile-in-batch bits (+ padding)
+      auto sw = [](uint32_t l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u); };
+      d.sa = static_cast<uint16_t>(sw(ma));
+      d.sb = static_cast<uint16_t>(sw(mb));
+      d.tla = d.tlb = 0;
+      for (int b = 0; b < 8; ++b) {
+        const int p = pos[b];
+        d.tcol[b] = static_cast<uint16_t>(sw(1u << p));
+        if (p < k) {
+          d.tla |= static_cast<uint8_t>(((ra >> p) & 1) << b);
+          d.tlb |= static_cast<uint8_t>(((rb >> p) & 1) << b);
+        }
+      }
+      uint16_t* st[3] = {&d.st1, &d.st2, &d.st3};
       d.spar = 0;
       for (int i = 0; i < 3; ++i) {
-        d.spar |= static_cast<uint8_t>((popc(st[i] & d.ra) & 1) << (2 * i));
-        d.spar |= static_cast<uint8_t>((popc(st[i] & d.rb) & 1) << (2 * i + 1));
+        const int p = pos[8 + i];
+        *st[i] = static_cast<uint16_t>(sw(1u << p));
+        if (p < k) {
+          d.spar |= static_cast<uint8_t>(((ra >> p) & 1) << (2 * i));
+          d.spar |= static_cast<uint8_t>(((rb >> p) & 1) << (2 * i + 1));
+        }
       }
       gates.push_back(d);
     }

@@ -54,23 +54,29 @@ enum GateClass : uint8_t {
 // A gate on logical qubits (a, b) acts on physical cosets of span{ma, mb}
 // (ma = M e_a, mb = M e_b).  The coset member whose LOGICAL bits a, b are
 // zero is found with the dual rows ra, rb of M^-1 (logical bit a of physical
-// index p = parity(p & ra)); the tile-local and out-of-tile parts of the rows
-// are stored separately so the out-of-tile parity is one popcount per tile.
+// index p = parity(p & ra)).
 //
-// Thread t handles quad numbers j = t + T i (T = kPassThreads); the planner
-// precomputes the pivot expansion of T, 2T, 4T (st1..st3) and their logical
-// parities (spar bits: la1 lb1 la2 lb2 la3 lb3) so per-quad work is XORs.
-struct GateDesc {     // 48 bytes
+// Work split: a sweep covers one batch (nb tiles stored back to back, batch
+// index = tile-local index | tile-in-batch << k).  Item j (a quad or a pair)
+// of the batch is j = t + T i (thread t, iteration i, T = kPassThreads); its
+// representative is the batch index whose bits at the pivot positions are
+// zero and whose other bits are j's bits, placed at the planner-chosen free
+// positions pos[0..].  pos[0..2] are picked with distinct residues mod 3, so
+// the 8 lanes of a quarter-warp hit 8 different 16-byte bank groups under
+// the shared-memory swizzle swz(l) = l ^ ((l>>3 ^ l>>6 ^ l>>9) & 7).  Because
+// swz, the placement and the parities are all linear over XOR, the planner
+// stores swizzled per-bit offsets and parity masks and the kernel only XORs.
+struct GateDesc {     // 64 bytes
   int32_t mat;        // offset (complex elements) in the pass's matrix block
   uint8_t cls;        // GateClass
-  uint8_t plo, phi;   // pivot bits (ascending) removed from the quad/pair index
   uint8_t nq;         // 1 or 2
-  uint16_t ma, mb;    // tile-local XOR masks of slot 0 / slot 1
-  uint16_t ra, rb;    // tile-local parts of the dual rows
+  uint8_t tla, tlb;   // thread bits whose position carries a ra / rb bit
+  uint16_t sa, sb;    // swizzled masks of slot 0 / slot 1
+  uint16_t st1, st2, st3;   // swizzled offsets of iteration bits 0, 1, 2
   uint16_t cols;      // kSparse2 / kMono2: 2-bit column codes
-  uint16_t st1, st2, st3;   // pivot-expanded T, 2T, 4T
-  uint8_t spar;       // parities of st1..st3 against ra / rb
-  uint8_t pad[7];
+  uint8_t spar;       // ra / rb parities of iteration bits (la1 lb1 la2 lb2 la3 lb3)
+  uint8_t pad0[3];
+  uint16_t tcol[8];   // swizzled offsets of thread bits 0..7
   uint64_t ra_out, rb_out;  // out-of-tile parts of the dual rows (physical bits)
 };
 

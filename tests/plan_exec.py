@@ -20,11 +20,10 @@ PASS_DT = np.dtype([("gate_begin", "<i4"), ("gate_end", "<i4"), ("mat_begin", "<
                     ("mat_count", "<i4"), ("k", "<i4"), ("measure_q", "<i4"),
                     ("measure_slot", "<i4"), ("collapse_q", "<i4"), ("collapse_slot", "<i4"),
                     ("pad", "<i4", (3,)), ("tq", "i1", (16,)), ("oq", "i1", (48,))])
-GATE_DT = np.dtype([("mat", "<i4"), ("cls", "u1"), ("plo", "u1"), ("phi", "u1"), ("nq", "u1"),
-                    ("ma", "<u2"), ("mb", "<u2"), ("ra", "<u2"), ("rb", "<u2"),
-                    ("cols", "<u2"), ("st1", "<u2"), ("st2", "<u2"), ("st3", "<u2"),
-                    ("spar", "u1"), ("pad", "u1", (7,)), ("ra_out", "<u8"), ("rb_out", "<u8")],
-                   align=True)
+GATE_DT = np.dtype([("mat", "<i4"), ("cls", "u1"), ("nq", "u1"), ("tla", "u1"), ("tlb", "u1"),
+                    ("sa", "<u2"), ("sb", "<u2"), ("st1", "<u2"), ("st2", "<u2"), ("st3", "<u2"),
+                    ("cols", "<u2"), ("spar", "u1"), ("pad0", "u1", (3,)), ("tcol", "<u2", (8,)),
+                    ("ra_out", "<u8"), ("rb_out", "<u8")], align=True)
 THREADS = 256  # kPassThreads
 TILE_MAX = 11  # kTileQubitsMax
 (DENSE1, DIAG1, DENSE2, SPARSE2, MONO2, DIAG2, CX01, CX10, PAIRQ, PAIRP, PAIRX, SWAP) = range(12)
@@ -85,32 +84,40 @@ def _mix2(x, y, m):
     return m[0] * x + m[1] * y, m[2] * x + m[3] * y
 
 
+def _swz(l):
+    return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7)
+
+
 def _apply(B, g, mats, tbases, k, nvalid):
     """One gate sweep over a batch B (nvalid tiles of 2^k stored back to back),
-    enumerated exactly as k_blocked's make_sweep / for_items."""
+    enumerated exactly as k_blocked's make_sweep / item_addr: swizzled
+    shared-memory addresses, un-swizzled here (swz is an involution) to index B."""
     m = mats[int(g["mat"]):]
     nq = int(g["nq"])
-    ma, mb = int(g["ma"]), int(g["mb"])
-    sp = int(g["spar"])
     per_tile = 1 << (k - nq)
     items = per_tile * nvalid
     j = np.arange(items, dtype=np.int64)
     t, i = j % THREADS, j // THREADS
-    bt = _ins0(_ins0(t, int(g["plo"])), int(g["phi"])) if nq == 2 else _ins0(t, int(g["plo"]))
-    base, la, lb = bt.copy(), _parity(bt & int(g["ra"])), _parity(bt & int(g["rb"]))
+    a = np.zeros(items, np.int64)
+    for b in range(8):
+        a ^= np.where((t >> b) & 1, int(g["tcol"][b]), 0)
+    la = _parity(t & int(g["tla"]))
+    lb = _parity(t & int(g["tlb"]))
+    sp = int(g["spar"])
     for bit, st in enumerate((int(g["st1"]), int(g["st2"]), int(g["st3"]))):
         on = ((i >> bit) & 1).astype(bool)
-        base = np.where(on, base | st, base)
+        a = np.where(on, a ^ st, a)
         la = np.where(on, la ^ ((sp >> (2 * bit)) & 1), la)
         lb = np.where(on, lb ^ ((sp >> (2 * bit + 1)) & 1), lb)
-    # tile of each item: the kernel uses i >> tshift (or t // per_tile for small tiles)
-    tile = j // per_tile
+    tile = j >> (k - nq)
     ga = _parity(tbases[tile].astype(np.uint64) & np.uint64(g["ra_out"]))
     gb = _parity(tbases[tile].astype(np.uint64) & np.uint64(g["rb_out"]))
     la, lb = (la ^ ga) & 1, (lb ^ gb) & 1
+    sa, sb = int(g["sa"]), int(g["sb"])
+    a0 = a ^ (la * sa) ^ ((lb * sb) if nq == 2 else 0)
+    U = _swz  # swizzled address -> batch index
     if nq == 1:
-        i0 = base ^ (la * ma)
-        i1 = i0 ^ ma
+        i0, i1 = U(a0), U(a0 ^ sa)
         x, y = B[i0], B[i1]
         if g["cls"] == DIAG1:
             x, y = m[0] * x, m[1] * y
@@ -118,8 +125,8 @@ def _apply(B, g, mats, tbases, k, nvalid):
             x, y = _mix2(x, y, m[:4])
         B[i0], B[i1] = x, y
         return
-    i0 = base ^ (la * ma) ^ (lb * mb)
-    idx = [i0, i0 ^ ma, i0 ^ mb, i0 ^ ma ^ mb]
+    idx = [U(a0), U(a0 ^ sa), U(a0 ^ sb), U(a0 ^ sa ^ sb)]
+    assert len(np.unique(np.concatenate(idx))) == 4 * items  # items partition the batch
     x = [B[ix] for ix in idx]
     c = int(g["cls"])
     out = list(x)

@@ -37,8 +37,11 @@ def measure(n, pairs, reps=3):
     return ms, info.n_passes, info.n_device_gates
 
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 21
-for label, pairs in [
+if __name__ != "__main__":
+    pass
+else:
+  n = int(sys.argv[1]) if len(sys.argv) > 1 else 21
+  for label, pairs in [
     ("local x640", [(i % 5, i % 5 + 1) for i in range(640)]),
     ("local x6400", [(i % 5, i % 5 + 1) for i in range(6400)]),
     ("chain x640", [(i % (n - 1), i % (n - 1) + 1) for i in range(640)]),
