@@ -302,7 +302,24 @@ struct Sweep {
   int sa, sb;
 };
 
-__device__ __forceinline__ Sweep make_sweep(int k, int nb, const GateDesc& d, unsigned gm) {
+// Per pass, the thread part of every gate's item address is tabulated: entry
+// e of table 0 (table 1) is the XOR of the swizzled offsets of thread bits
+// 0..3 (4..7) set in e, with the ra / rb parities in bits 12 / 13.
+__device__ __forceinline__ uint16_t thread_table_entry(const GateDesc& d, int e) {
+  const int half = e >> 4, bits = e & 15;
+  unsigned v = 0;
+  for (int b = 0; b < 4; ++b)
+    if (bits >> b & 1) {
+      const int tb = 4 * half + b;
+      v ^= d.tcol[tb];
+      v ^= ((d.tla >> tb) & 1u) << 12;
+      v ^= ((d.tlb >> tb) & 1u) << 13;
+    }
+  return static_cast<uint16_t>(v);
+}
+
+__device__ __forceinline__ Sweep make_sweep(int k, int nb, const GateDesc& d, unsigned gm,
+                                            const uint16_t* ttab) {
   Sweep w;
   const int two = d.nq == 2;
   const int lpt = k - 1 - two;  // log2 items per tile
@@ -311,13 +328,10 @@ __device__ __forceinline__ Sweep make_sweep(int k, int nb, const GateDesc& d, un
   w.active = t < items;
   w.n_iter = items > kPassThreads ? items >> kThreadBits : 1;
   w.tile_shift = lpt;
-  int bt = 0;
-#pragma unroll
-  for (int b = 0; b < kThreadBits; ++b)
-    if (t >> b & 1) bt ^= d.tcol[b];
-  w.bt = bt;
-  w.la_t = __popc(t & d.tla) & 1;
-  w.lb_t = __popc(t & d.tlb) & 1;
+  const unsigned v = ttab[t & 15] ^ ttab[16 + (t >> 4)];
+  w.bt = v & 0xfffu;
+  w.la_t = (v >> 12) & 1;
+  w.lb_t = (v >> 13) & 1;
   w.st1 = d.st1;
   w.st2 = d.st2;
   w.st3 = d.st3;
@@ -380,8 +394,8 @@ __device__ __forceinline__ void for_pairs(const Sweep& w, F f) {
 __device__ __forceinline__ void apply_gate(const double2* __restrict__ src,
                                            double2* __restrict__ dst, int k, int nb,
                                            const GateDesc& d, const double2* __restrict__ m,
-                                           unsigned gm) {
-  const Sweep w = make_sweep(k, nb, d, gm);
+                                           unsigned gm, const uint16_t* ttab) {
+  const Sweep w = make_sweep(k, nb, d, gm, ttab);
   if (d.nq == 1) {
     if (d.cls == kDiag1) {
       const double2 d0 = *(m), d1 = *(m + 1);
@@ -531,6 +545,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
   __shared__ PassDesc sp;
   __shared__ uint64_t s_hi[1 << (kTileQubitsMax - kThreadBits)];  // offsets of tile bits >= kThreadBits
   __shared__ unsigned s_gm[kMaxPassGates];  // per gate: out-of-tile row parities of the batch tiles
+  __shared__ uint16_t s_ttab[kMaxPassGates][32];  // per gate: thread-address tables
   __shared__ double red[32];
   __shared__ double s_p0;
   cg::grid_group grid = cg::this_grid();
@@ -550,6 +565,12 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
       const uint64_t* src = reinterpret_cast<const uint64_t*>(p.gates + sp.gate_begin);
       uint64_t* dst = reinterpret_cast<uint64_t*>(s_gates);
       for (int i = tid; i < n_words; i += kPassThreads) dst[i] = src[i];
+    }
+    __syncthreads();
+    {
+      const int n_entries = (sp.gate_end - sp.gate_begin) * 32;
+      for (int e = tid; e < n_entries; e += kPassThreads)
+        s_ttab[e >> 5][e & 31] = thread_table_entry(s_gates[e >> 5], e & 31);
     }
     constexpr int kHi = kTileQubitsMax - kThreadBits;
     if (tid < (1 << kHi)) {
@@ -640,7 +661,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
       for (int g = 0; g < n_gates; ++g) {
         const GateDesc d = s_gates[g];
         double2* out = smem + spare * kTileAmpsMax;
-        apply_gate(tile, out, k, nvalid, d, s_mats + d.mat, s_gm[g]);
+        apply_gate(tile, out, k, nvalid, d, s_mats + d.mat, s_gm[g], s_ttab[g]);
         const int tmp = cur;
         cur = spare;
         spare = tmp;
