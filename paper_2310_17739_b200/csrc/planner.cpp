@@ -220,17 +220,19 @@ static inline uint32_t pext64(uint64_t m, uint64_t set) {
 
 static inline int lowest_bit(uint64_t m) { return __builtin_ctzll(m); }
 
-// tile size: the largest k <= 12 whose tile count spreads over the persistent
-// CTAs with >= 95% balance (2^(n-k) tiles over `workers` CTAs)
+// tile size: the largest k <= kTileQubitsMax whose tile count spreads over
+// the persistent CTAs with >= 85% balance (2^(n-k) tiles over `workers`
+// CTAs); bigger tiles mean fewer passes, whose fixed cost dominates a lost
+// balance of a few percent.
 // physical support (bits of ma | mb) above which the frame is flushed first
-constexpr int kMaxSupport = 6;
+constexpr int kMaxSupport = 4;
 
 static int choose_tile_qubits(int n, int workers) {
   if (n <= kTileQubitsMax) return n;
   for (int k = kTileQubitsMax; k >= 9; --k) {
     const double tiles = std::ldexp(1.0, n - k);
     const double rounds = std::ceil(tiles / workers);
-    if (tiles / (rounds * workers) >= 0.95) return k;
+    if (tiles / (rounds * workers) >= 0.85) return k;
   }
   return kTileQubitsMax;
 }
@@ -286,6 +288,22 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
     }
     for (size_t i = ops_rec.size(); i-- > 0;) emit_cx(ops_rec[i].first, ops_rec[i].second);
     for (int j = 0; j < 64; ++j) col[j] = row[j] = uint64_t(1) << j;
+  };
+  // A physical CX(c -> t) gives M <- P M: every column holding bit c toggles
+  // bit t; M^-1 <- M^-1 P: every row holding bit t toggles bit c.  Clearing
+  // the non-pivot bits of one column costs |col| - 1 such gates.
+  auto physical_cx = [&](int c, int t) {
+    emit_cx(c, t);
+    for (int j = 0; j < n; ++j) {
+      if (col[j] >> c & 1) col[j] ^= uint64_t(1) << t;
+      if (row[j] >> t & 1) row[j] ^= uint64_t(1) << c;
+    }
+  };
+  auto reduce_column = [&](int j) {
+    const uint64_t m = col[j];
+    if (popc(m) <= 1) return;
+    const int pivot = __builtin_ctzll(m);
+    for (uint64_t r = m & (m - 1); r; r &= r - 1) physical_cx(pivot, __builtin_ctzll(r));
   };
   auto flush_run = [&]() {
     flush_frame();
@@ -363,7 +381,10 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
       continue;
     }
     if (popc(col[a] | (o.nq == 2 ? col[b] : 0)) > kMaxSupport) {
-      flush_frame();  // keep physical supports small so passes stay dense
+      // keep physical supports small so passes stay dense: reduce just this
+      // gate's columns to unit vectors with physical CXs (row operations)
+      reduce_column(a);
+      if (o.nq == 2) reduce_column(b);
       ++n_frame_flushes;
     }
     g.ma = col[a];
@@ -577,7 +598,7 @@ extern "C" int nsb_plan_analyze(const nsb_op* ops, int64_t n_ops, const double* 
   }
   try {
     nsb::HostPlan H;
-    H.build(ops, n_ops, params, payloads, n_qubits, 148);
+    H.build(ops, n_ops, params, payloads, n_qubits, 296);  // 2 CTAs x 148 SMs (B200)
     fill_info(H, info);
     if (class_counts)
       for (int c = 0; c < nsb::kNumClasses; ++c) class_counts[c] = H.class_count[c];
