@@ -294,9 +294,10 @@ __device__ __forceinline__ double2 pick(const double2 x0, const double2 x1, cons
 struct Sweep {
   int n_iter;           // valid items per thread
   bool active;          // this thread owns work (batches smaller than T items)
-  int bt;               // swizzled offset of the thread bits
+  int bt, rbt;          // swizzled offset of the thread bits (store / load side)
   int la_t, lb_t;       // logical parities of the thread bits
   int st1, st2, st3, spar;
+  int rst1, rst2, rst3, rsa, rsb;  // load side: offsets through the read map
   int tile_shift;       // item j lies in tile j >> tile_shift of the batch
   unsigned gma, gmb;    // out-of-tile parities per tile of the batch
   int sa, sb;
@@ -304,22 +305,24 @@ struct Sweep {
 
 // Per pass, the thread part of every gate's item address is tabulated: entry
 // e of table 0 (table 1) is the XOR of the swizzled offsets of thread bits
-// 0..3 (4..7) set in e, with the ra / rb parities in bits 12 / 13.
-__device__ __forceinline__ uint16_t thread_table_entry(const GateDesc& d, int e) {
+// 0..3 (4..7) set in e -- store side in bits 0..11 with the ra / rb parities
+// in bits 12 / 13, load side (through the read map) in bits 16..27.
+__device__ __forceinline__ uint32_t thread_table_entry(const GateDesc& d, int e) {
   const int half = e >> 4, bits = e & 15;
-  unsigned v = 0;
+  uint32_t v = 0;
   for (int b = 0; b < 4; ++b)
     if (bits >> b & 1) {
       const int tb = 4 * half + b;
       v ^= d.tcol[tb];
       v ^= ((d.tla >> tb) & 1u) << 12;
       v ^= ((d.tlb >> tb) & 1u) << 13;
+      v ^= static_cast<uint32_t>(d.rtcol[tb]) << 16;
     }
-  return static_cast<uint16_t>(v);
+  return v;
 }
 
 __device__ __forceinline__ Sweep make_sweep(int k, int nb, const GateDesc& d, unsigned gm,
-                                            const uint16_t* ttab) {
+                                            const uint32_t* ttab) {
   Sweep w;
   const int two = d.nq == 2;
   const int lpt = k - 1 - two;  // log2 items per tile
@@ -328,8 +331,14 @@ __device__ __forceinline__ Sweep make_sweep(int k, int nb, const GateDesc& d, un
   w.active = t < items;
   w.n_iter = items > kPassThreads ? items >> kThreadBits : 1;
   w.tile_shift = lpt;
-  const unsigned v = ttab[t & 15] ^ ttab[16 + (t >> 4)];
+  const uint32_t v = ttab[t & 15] ^ ttab[16 + (t >> 4)];
   w.bt = v & 0xfffu;
+  w.rbt = v >> 16;
+  w.rst1 = d.rst1;
+  w.rst2 = d.rst2;
+  w.rst3 = d.rst3;
+  w.rsa = d.rsa;
+  w.rsb = d.rsb;
   w.la_t = (v >> 12) & 1;
   w.lb_t = (v >> 13) & 1;
   w.st1 = d.st1;
@@ -343,37 +352,43 @@ __device__ __forceinline__ Sweep make_sweep(int k, int nb, const GateDesc& d, un
   return w;
 }
 
-// swizzled address of member 0 (logical slot bits zero) of item i of this thread
-__device__ __forceinline__ int item_addr(const Sweep& w, int i, bool two) {
-  int a = w.bt, la = w.la_t, lb = w.lb_t;
+// swizzled addresses of member 0 (logical slot bits zero) of item i of this
+// thread: store side in .x, load side (through the read map) in .y
+__device__ __forceinline__ int2 item_addr(const Sweep& w, int i, bool two) {
+  int a = w.bt, r = w.rbt, la = w.la_t, lb = w.lb_t;
   if (i & 1) {
     a ^= w.st1;
+    r ^= w.rst1;
     la ^= w.spar & 1;
     lb ^= (w.spar >> 1) & 1;
   }
   if (i & 2) {
     a ^= w.st2;
+    r ^= w.rst2;
     la ^= (w.spar >> 2) & 1;
     lb ^= (w.spar >> 3) & 1;
   }
   if (i & 4) {
     a ^= w.st3;
+    r ^= w.rst3;
     la ^= (w.spar >> 4) & 1;
     lb ^= (w.spar >> 5) & 1;
   }
   const int tile = (threadIdx.x + (i << kThreadBits)) >> w.tile_shift;
   la ^= (w.gma >> tile) & 1;
-  lb ^= (w.gmb >> tile) & 1;
-  return a ^ (la ? w.sa : 0) ^ (two && lb ? w.sb : 0);
+  lb = two ? lb ^ ((w.gmb >> tile) & 1) : 0;
+  return make_int2(a ^ (la ? w.sa : 0) ^ (lb ? w.sb : 0), r ^ (la ? w.rsa : 0) ^ (lb ? w.rsb : 0));
 }
 
+// f(load addresses l0..l3, store addresses s0..s3)
 template <class F>
 __device__ __forceinline__ void for_quads(const Sweep& w, F f) {
   if (!w.active) return;
 #pragma unroll 4
   for (int i = 0; i < w.n_iter; ++i) {
-    const int a0 = item_addr(w, i, true);
-    f(a0, a0 ^ w.sa, a0 ^ w.sb, a0 ^ w.sa ^ w.sb);
+    const int2 a = item_addr(w, i, true);
+    f(a.y, a.y ^ w.rsa, a.y ^ w.rsb, a.y ^ w.rsa ^ w.rsb, a.x, a.x ^ w.sa, a.x ^ w.sb,
+      a.x ^ w.sa ^ w.sb);
   }
 }
 
@@ -382,8 +397,8 @@ __device__ __forceinline__ void for_pairs(const Sweep& w, F f) {
   if (!w.active) return;
 #pragma unroll 4
   for (int i = 0; i < w.n_iter; ++i) {
-    const int a0 = item_addr(w, i, false);
-    f(a0, a0 ^ w.sa);
+    const int2 a = item_addr(w, i, false);
+    f(a.y, a.y ^ w.rsa, a.x, a.x ^ w.sa);
   }
 }
 
@@ -394,19 +409,27 @@ __device__ __forceinline__ void for_pairs(const Sweep& w, F f) {
 __device__ __forceinline__ void apply_gate(const double2* __restrict__ src,
                                            double2* __restrict__ dst, int k, int nb,
                                            const GateDesc& d, const double2* __restrict__ m,
-                                           unsigned gm, const uint16_t* ttab) {
+                                           unsigned gm, const uint32_t* ttab) {
   const Sweep w = make_sweep(k, nb, d, gm, ttab);
+  if (d.cls == kPermute) {  // pure read-map sweep
+    for_pairs(w, [&](int l0, int l1, int i0, int i1) {
+      const double2 x = src[l0], y = src[l1];
+      dst[i0] = x;
+      dst[i1] = y;
+    });
+    return;
+  }
   if (d.nq == 1) {
     if (d.cls == kDiag1) {
       const double2 d0 = *(m), d1 = *(m + 1);
-      for_pairs(w, [&](int i0, int i1) {
-        dst[i0] = cmul(d0, src[i0]);
-        dst[i1] = cmul(d1, src[i1]);
+      for_pairs(w, [&](int l0, int l1, int i0, int i1) {
+        dst[i0] = cmul(d0, src[l0]);
+        dst[i1] = cmul(d1, src[l1]);
       });
     } else {
       const double2 m0 = *(m), m1 = *(m + 1), m2 = *(m + 2), m3 = *(m + 3);
-      for_pairs(w, [&](int i0, int i1) {
-        double2 x = src[i0], y = src[i1];
+      for_pairs(w, [&](int l0, int l1, int i0, int i1) {
+        double2 x = src[l0], y = src[l1];
         mix2(x, y, m0, m1, m2, m3);
         dst[i0] = x;
         dst[i1] = y;
@@ -416,8 +439,8 @@ __device__ __forceinline__ void apply_gate(const double2* __restrict__ src,
   }
   switch (d.cls) {
     case kCX01:  // swaps members 1, 3
-      for_quads(w, [&](int i0, int i1, int i2, int i3) {
-        const double2 x0 = src[i0], x1 = src[i1], x2 = src[i2], x3 = src[i3];
+      for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
+        const double2 x0 = src[l0], x1 = src[l1], x2 = src[l2], x3 = src[l3];
         dst[i0] = x0;
         dst[i1] = x3;
         dst[i2] = x2;
@@ -425,8 +448,8 @@ __device__ __forceinline__ void apply_gate(const double2* __restrict__ src,
       });
       break;
     case kCX10:  // swaps members 2, 3
-      for_quads(w, [&](int i0, int i1, int i2, int i3) {
-        const double2 x0 = src[i0], x1 = src[i1], x2 = src[i2], x3 = src[i3];
+      for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
+        const double2 x0 = src[l0], x1 = src[l1], x2 = src[l2], x3 = src[l3];
         dst[i0] = x0;
         dst[i1] = x1;
         dst[i2] = x3;
@@ -434,8 +457,8 @@ __device__ __forceinline__ void apply_gate(const double2* __restrict__ src,
       });
       break;
     case kSwap:  // swaps members 1, 2
-      for_quads(w, [&](int i0, int i1, int i2, int i3) {
-        const double2 x0 = src[i0], x1 = src[i1], x2 = src[i2], x3 = src[i3];
+      for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
+        const double2 x0 = src[l0], x1 = src[l1], x2 = src[l2], x3 = src[l3];
         dst[i0] = x0;
         dst[i1] = x2;
         dst[i2] = x1;
@@ -448,7 +471,7 @@ __device__ __forceinline__ void apply_gate(const double2* __restrict__ src,
       const double2 m0 = *(m), m1 = *(m + 1), m2 = *(m + 2), m3 = *(m + 3);
       const double2 n0 = *(m + 4), n1 = *(m + 5), n2 = *(m + 6), n3 = *(m + 7);
       const int cls = d.cls;
-      for_quads(w, [&](int i0, int i1, int i2, int i3) {
+      for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
         // block 0 on members (u0,u1), block 1 on (u2,u3)
         const int u0 = i0;
         const int u1 = cls == kPairQ ? i2 : (cls == kPairP ? i1 : i3);
@@ -466,11 +489,11 @@ __device__ __forceinline__ void apply_gate(const double2* __restrict__ src,
     }
     case kDiag2: {
       const double2 d0 = *(m), d1 = *(m + 1), d2 = *(m + 2), d3 = *(m + 3);
-      for_quads(w, [&](int i0, int i1, int i2, int i3) {
-        dst[i0] = cmul(d0, src[i0]);
-        dst[i1] = cmul(d1, src[i1]);
-        dst[i2] = cmul(d2, src[i2]);
-        dst[i3] = cmul(d3, src[i3]);
+      for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
+        dst[i0] = cmul(d0, src[l0]);
+        dst[i1] = cmul(d1, src[l1]);
+        dst[i2] = cmul(d2, src[l2]);
+        dst[i3] = cmul(d3, src[l3]);
       });
       break;
     }
@@ -478,8 +501,8 @@ __device__ __forceinline__ void apply_gate(const double2* __restrict__ src,
       const double2 v0 = *(m), v1 = *(m + 1), v2 = *(m + 2), v3 = *(m + 3);
       const int c0 = d.cols & 3, c1 = (d.cols >> 2) & 3, c2 = (d.cols >> 4) & 3,
                 c3 = (d.cols >> 6) & 3;
-      for_quads(w, [&](int i0, int i1, int i2, int i3) {
-        const double2 x0 = src[i0], x1 = src[i1], x2 = src[i2], x3 = src[i3];
+      for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
+        const double2 x0 = src[l0], x1 = src[l1], x2 = src[l2], x3 = src[l3];
         dst[i0] = cmul(v0, pick(x0, x1, x2, x3, c0));
         dst[i1] = cmul(v1, pick(x0, x1, x2, x3, c1));
         dst[i2] = cmul(v2, pick(x0, x1, x2, x3, c2));
@@ -489,8 +512,8 @@ __device__ __forceinline__ void apply_gate(const double2* __restrict__ src,
     }
     case kSparse2: {
       const unsigned cols = d.cols;
-      for_quads(w, [&](int i0, int i1, int i2, int i3) {
-        const double2 x0 = src[i0], x1 = src[i1], x2 = src[i2], x3 = src[i3];
+      for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
+        const double2 x0 = src[l0], x1 = src[l1], x2 = src[l2], x3 = src[l3];
         const int idx[4] = {i0, i1, i2, i3};
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
@@ -503,8 +526,8 @@ __device__ __forceinline__ void apply_gate(const double2* __restrict__ src,
       break;
     }
     default: {  // kDense2
-      for_quads(w, [&](int i0, int i1, int i2, int i3) {
-        const double2 x0 = src[i0], x1 = src[i1], x2 = src[i2], x3 = src[i3];
+      for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
+        const double2 x0 = src[l0], x1 = src[l1], x2 = src[l2], x3 = src[l3];
         const int idx[4] = {i0, i1, i2, i3};
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
@@ -545,7 +568,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
   __shared__ PassDesc sp;
   __shared__ uint64_t s_hi[1 << (kTileQubitsMax - kThreadBits)];  // offsets of tile bits >= kThreadBits
   __shared__ unsigned s_gm[kMaxPassGates];  // per gate: out-of-tile row parities of the batch tiles
-  __shared__ uint16_t s_ttab[kMaxPassGates][32];  // per gate: thread-address tables
+  __shared__ uint32_t s_ttab[kMaxPassGates][32];  // per gate: thread-address tables
   __shared__ double red[32];
   __shared__ double s_p0;
   cg::grid_group grid = cg::this_grid();

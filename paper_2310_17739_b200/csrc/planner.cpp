@@ -237,6 +237,72 @@ static int choose_tile_qubits(int n, int workers) {
   return kTileQubitsMax;
 }
 
+// pivots, free positions, swizzled per-bit offsets (plain and through the read
+// map R) and parity masks of one gate in tile-local coordinates (planner.h)
+void describe_gate(const PhysGate& g, uint64_t tset, int k, const uint32_t* rcol, GateDesc& d) {
+  const uint32_t ma = pext64(g.ma, tset), mb = pext64(g.mb, tset);
+  const uint32_t ra = pext64(g.ra, tset), rb = pext64(g.rb, tset);
+  d.ra_out = g.ra & ~tset;
+  d.rb_out = g.rb & ~tset;
+  // pivots: one bit of ma, and one of mb reduced against ma
+  const int pa = lowest_bit(ma);
+  int pbit = -1;
+  if (g.nq == 2) {
+    const uint32_t mr = (mb >> pa & 1) ? (mb ^ ma) : mb;
+    if (!mr) throw std::logic_error("degenerate gate masks");
+    pbit = lowest_bit(mr);
+  }
+  // free positions: tile-local non-pivot bits (first three with distinct
+  // residues mod 3 for conflict-free quarter-warps), then batch bits
+  std::vector<int> local, pos;
+  for (int p = 0; p < k; ++p)
+    if (p != pa && p != pbit) local.push_back(p);
+  for (int r = 0; r < 3; ++r)
+    for (size_t i = 0; i < local.size(); ++i)
+      if (local[i] >= 0 && local[i] % 3 == r) {
+        pos.push_back(local[i]);
+        local[i] = -1;
+        break;
+      }
+  for (int p : local)
+    if (p >= 0) pos.push_back(p);
+  for (int b = 0; b < 8; ++b) pos.push_back(k + b);  // tile-in-batch bits (+ padding)
+  auto sw = [](uint32_t l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u); };
+  d.sa = static_cast<uint16_t>(sw(ma));
+  d.sb = static_cast<uint16_t>(sw(mb));
+  d.tla = d.tlb = 0;
+  for (int b = 0; b < 8; ++b) {
+    const int p = pos[b];
+    d.tcol[b] = static_cast<uint16_t>(sw(1u << p));
+    if (p < k) {
+      d.tla |= static_cast<uint8_t>(((ra >> p) & 1) << b);
+      d.tlb |= static_cast<uint8_t>(((rb >> p) & 1) << b);
+    }
+  }
+  uint16_t* st[3] = {&d.st1, &d.st2, &d.st3};
+  d.spar = 0;
+  for (int i = 0; i < 3; ++i) {
+    const int p = pos[8 + i];
+    *st[i] = static_cast<uint16_t>(sw(1u << p));
+    if (p < k) {
+      d.spar |= static_cast<uint8_t>(((ra >> p) & 1) << (2 * i));
+      d.spar |= static_cast<uint8_t>(((rb >> p) & 1) << (2 * i + 1));
+    }
+  }
+  auto rmap = [&](uint32_t u) {  // R u on tile-local bits; batch bits pass through
+    uint32_t out = u & ~((1u << k) - 1);
+    for (int i = 0; i < k; ++i)
+      if (u >> i & 1) out ^= rcol[i];
+    return out;
+  };
+  d.rsa = static_cast<uint16_t>(sw(rmap(ma)));
+  d.rsb = static_cast<uint16_t>(sw(rmap(mb)));
+  for (int b = 0; b < 8; ++b) d.rtcol[b] = static_cast<uint16_t>(sw(rmap(1u << pos[b])));
+  d.rst1 = static_cast<uint16_t>(sw(rmap(1u << pos[8])));
+  d.rst2 = static_cast<uint16_t>(sw(rmap(1u << pos[9])));
+  d.rst3 = static_cast<uint16_t>(sw(rmap(1u << pos[10])));
+}
+
 void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
                      const double* payloads, int n, int workers) {
   n_qubits = n;
@@ -434,8 +500,10 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
     }
     P.gate_begin = static_cast<int32_t>(gates.size());
     P.mat_begin = static_cast<int32_t>(matrices.size() / 2);
-    for (int gi : pass_groups[pi]) {
-      const PhysGate& g = run[gi];
+    uint32_t rcol[16];  // pending read map R (tile-local columns), product of CXs
+    for (int i = 0; i < 16; ++i) rcol[i] = 1u << i;
+    bool r_identity = true;
+    auto emit = [&](const PhysGate& g) {
       GateDesc d{};
       d.mat = static_cast<int32_t>(matrices.size() / 2) - P.mat_begin;
       matrices.insert(matrices.end(), packed_all.begin() + 2 * g.mat,
@@ -443,56 +511,36 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
       d.cls = g.cls;
       d.nq = static_cast<uint8_t>(g.nq);
       d.cols = g.cols;
-      const uint32_t ma = pext64(g.ma, tset), mb = pext64(g.mb, tset);
-      const uint32_t ra = pext64(g.ra, tset), rb = pext64(g.rb, tset);
-      d.ra_out = g.ra & ~tset;
-      d.rb_out = g.rb & ~tset;
-      // pivots: one bit of ma, and one of mb reduced against ma
-      const int pa = lowest_bit(ma);
-      int pbit = -1;
-      if (g.nq == 2) {
-        const uint32_t mr = (mb >> pa & 1) ? (mb ^ ma) : mb;
-        if (!mr) throw std::logic_error("degenerate gate masks");
-        pbit = lowest_bit(mr);
-      }
-      // free positions: tile-local non-pivot bits (first three with distinct
-      // residues mod 3 for conflict-free quarter-warps), then batch bits
-      std::vector<int> local, pos;
-      for (int p = 0; p < k; ++p)
-        if (p != pa && p != pbit) local.push_back(p);
-      for (int r = 0; r < 3; ++r)
-        for (size_t i = 0; i < local.size(); ++i)
-          if (local[i] >= 0 && local[i] % 3 == r) {
-            pos.push_back(local[i]);
-            local[i] = -1;
-            break;
-          }
-      for (int p : local)
-        if (p >= 0) pos.push_back(p);
-      for (int b = 0; b < 8; ++b) pos.push_back(k + b);  // tile-in-batch bits (+ padding)
-      auto sw = [](uint32_t l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u); };
-      d.sa = static_cast<uint16_t>(sw(ma));
-      d.sb = static_cast<uint16_t>(sw(mb));
-      d.tla = d.tlb = 0;
-      for (int b = 0; b < 8; ++b) {
-        const int p = pos[b];
-        d.tcol[b] = static_cast<uint16_t>(sw(1u << p));
-        if (p < k) {
-          d.tla |= static_cast<uint8_t>(((ra >> p) & 1) << b);
-          d.tlb |= static_cast<uint8_t>(((rb >> p) & 1) << b);
-        }
-      }
-      uint16_t* st[3] = {&d.st1, &d.st2, &d.st3};
-      d.spar = 0;
-      for (int i = 0; i < 3; ++i) {
-        const int p = pos[8 + i];
-        *st[i] = static_cast<uint16_t>(sw(1u << p));
-        if (p < k) {
-          d.spar |= static_cast<uint8_t>(((ra >> p) & 1) << (2 * i));
-          d.spar |= static_cast<uint8_t>(((rb >> p) & 1) << (2 * i + 1));
-        }
-      }
+      describe_gate(g, tset, k, rcol, d);
       gates.push_back(d);
+      for (int i = 0; i < 16; ++i) rcol[i] = 1u << i;
+      r_identity = true;
+    };
+    for (int gi : pass_groups[pi]) {
+      const PhysGate& g = run[gi];
+      const bool perm = g.cls == kCX01 || g.cls == kCX10 || g.cls == kSwap;
+      if (perm && popc(g.ma) == 1 && popc(g.mb) == 1) {
+        // fold into the read map: R <- R C  (R e_c ^= R e_t for CX(c -> t))
+        const int a = lowest_bit(pext64(g.ma, tset)), b = lowest_bit(pext64(g.mb, tset));
+        if (g.cls == kCX01) {
+          rcol[a] ^= rcol[b];
+        } else if (g.cls == kCX10) {
+          rcol[b] ^= rcol[a];
+        } else {
+          std::swap(rcol[a], rcol[b]);
+        }
+        r_identity = false;
+        ++n_folded_gates;
+        continue;
+      }
+      emit(g);
+    }
+    if (!r_identity) {  // trailing permutation: one identity sweep through R
+      PhysGate id{};
+      id.cls = kPermute;
+      id.nq = 1;
+      id.ma = id.ra = uint64_t(1) << P.tq[0];
+      emit(id);
     }
     P.gate_end = static_cast<int32_t>(gates.size());
     P.mat_count = static_cast<int32_t>(matrices.size() / 2) - P.mat_begin;

@@ -48,7 +48,8 @@ enum GateClass : uint8_t {
   kPairP = 9,     // 2x2 blocks on members (0,1) and (2,3)                (8)
   kPairX = 10,    // 2x2 blocks on members (0,3) and (1,2)                (8)
   kSwap = 11,     // exact SWAP: swaps members 1,2                        (0)
-  kNumClasses = 12
+  kPermute = 12,  // identity sweep that only applies its read map      (0)
+  kNumClasses = 13
 };
 
 // A gate on logical qubits (a, b) acts on physical cosets of span{ma, mb}
@@ -66,7 +67,13 @@ enum GateClass : uint8_t {
 // the shared-memory swizzle swz(l) = l ^ ((l>>3 ^ l>>6 ^ l>>9) & 7).  Because
 // swz, the placement and the parities are all linear over XOR, the planner
 // stores swizzled per-bit offsets and parity masks and the kernel only XORs.
-struct GateDesc {     // 64 bytes
+//
+// Read maps: physical permutations (the CX gates that shrink the relabeling
+// frame) are not executed as sweeps of their own.  A gate that follows them in
+// a pass reads its members through their composition R (a linear map of
+// tile-local indices) and writes in place order, so the r* fields hold the
+// same offsets mapped through R (equal to the plain ones when R = I).
+struct GateDesc {     // 96 bytes
   int32_t mat;        // offset (complex elements) in the pass's matrix block
   uint8_t cls;        // GateClass
   uint8_t nq;         // 1 or 2
@@ -77,13 +84,17 @@ struct GateDesc {     // 64 bytes
   uint8_t spar;       // ra / rb parities of iteration bits (la1 lb1 la2 lb2 la3 lb3)
   uint8_t pad0[3];
   uint16_t tcol[8];   // swizzled offsets of thread bits 0..7
+  uint16_t rsa, rsb, rst1, rst2, rst3;  // the same, read through R
+  uint16_t rtcol[8];
+  uint8_t pad1[14];
   uint64_t ra_out, rb_out;  // out-of-tile parts of the dual rows (physical bits)
 };
+static_assert(sizeof(GateDesc) == 96, "GateDesc layout");
 
 // Per pass the kernel stages the gate descriptors and the pass's own block
 // of packed matrices in shared memory (bounded by these limits).
-constexpr int kMaxPassGates = 48;
-constexpr int kMaxPassMats = 512;   // complex elements (8 KiB)
+constexpr int kMaxPassGates = 40;
+constexpr int kMaxPassMats = 384;   // complex elements (6 KiB)
 
 struct PassDesc {         // 112 bytes
   int32_t gate_begin, gate_end;

@@ -70,6 +70,7 @@ struct HostPlan {
   int64_t n_frame_gates = 0;  // exact CX/SWAP absorbed by the relabeling frame
   int64_t n_flush_gates = 0;  // physical CX emitted to flush the frame
   int64_t n_frame_flushes = 0;  // flushes forced by a wide support
+  int64_t n_folded_gates = 0;   // physical CXs folded into read maps
   int64_t flops = 0;
   int64_t class_count[kNumClasses] = {};
 
@@ -92,5 +93,6 @@ struct HostPlan {
 };
 
 void plan_info(const HostPlan& H, nsb_plan_info* info);
+void describe_gate(const PhysGate& g, uint64_t tset, int k, const uint32_t* rcol, GateDesc& d);
 
 }  // namespace nsb

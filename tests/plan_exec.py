@@ -23,10 +23,13 @@ PASS_DT = np.dtype([("gate_begin", "<i4"), ("gate_end", "<i4"), ("mat_begin", "<
 GATE_DT = np.dtype([("mat", "<i4"), ("cls", "u1"), ("nq", "u1"), ("tla", "u1"), ("tlb", "u1"),
                     ("sa", "<u2"), ("sb", "<u2"), ("st1", "<u2"), ("st2", "<u2"), ("st3", "<u2"),
                     ("cols", "<u2"), ("spar", "u1"), ("pad0", "u1", (3,)), ("tcol", "<u2", (8,)),
+                    ("rsa", "<u2"), ("rsb", "<u2"), ("rst1", "<u2"), ("rst2", "<u2"),
+                    ("rst3", "<u2"), ("rtcol", "<u2", (8,)), ("pad1", "u1", (14,)),
                     ("ra_out", "<u8"), ("rb_out", "<u8")], align=True)
 THREADS = 256  # kPassThreads
 TILE_MAX = 11  # kTileQubitsMax
-(DENSE1, DIAG1, DENSE2, SPARSE2, MONO2, DIAG2, CX01, CX10, PAIRQ, PAIRP, PAIRX, SWAP) = range(12)
+(DENSE1, DIAG1, DENSE2, SPARSE2, MONO2, DIAG2, CX01, CX10, PAIRQ, PAIRP, PAIRX, SWAP,
+ PERMUTE) = range(13)
 
 
 class HostPlan:
@@ -99,26 +102,38 @@ def _apply(B, g, mats, tbases, k, nvalid):
     j = np.arange(items, dtype=np.int64)
     t, i = j % THREADS, j // THREADS
     a = np.zeros(items, np.int64)
+    r = np.zeros(items, np.int64)  # load side, through the read map
     for b in range(8):
         a ^= np.where((t >> b) & 1, int(g["tcol"][b]), 0)
+        r ^= np.where((t >> b) & 1, int(g["rtcol"][b]), 0)
     la = _parity(t & int(g["tla"]))
     lb = _parity(t & int(g["tlb"]))
     sp = int(g["spar"])
-    for bit, st in enumerate((int(g["st1"]), int(g["st2"]), int(g["st3"]))):
+    for bit, (st, rst) in enumerate(((int(g["st1"]), int(g["rst1"])), (int(g["st2"]), int(g["rst2"])),
+                                     (int(g["st3"]), int(g["rst3"])))):
         on = ((i >> bit) & 1).astype(bool)
         a = np.where(on, a ^ st, a)
+        r = np.where(on, r ^ rst, r)
         la = np.where(on, la ^ ((sp >> (2 * bit)) & 1), la)
         lb = np.where(on, lb ^ ((sp >> (2 * bit + 1)) & 1), lb)
     tile = j >> (k - nq)
     ga = _parity(tbases[tile].astype(np.uint64) & np.uint64(g["ra_out"]))
     gb = _parity(tbases[tile].astype(np.uint64) & np.uint64(g["rb_out"]))
     la, lb = (la ^ ga) & 1, (lb ^ gb) & 1
+    if nq == 1:
+        lb = lb * 0
     sa, sb = int(g["sa"]), int(g["sb"])
-    a0 = a ^ (la * sa) ^ ((lb * sb) if nq == 2 else 0)
+    rsa, rsb = int(g["rsa"]), int(g["rsb"])
+    a0 = a ^ (la * sa) ^ (lb * sb)
+    r0 = r ^ (la * rsa) ^ (lb * rsb)
     U = _swz  # swizzled address -> batch index
+    S = B.copy()  # the kernel sweeps out of place: loads see the pre-gate batch
     if nq == 1:
         i0, i1 = U(a0), U(a0 ^ sa)
-        x, y = B[i0], B[i1]
+        x, y = S[U(r0)], S[U(r0 ^ rsa)]
+        if g["cls"] == PERMUTE:
+            B[i0], B[i1] = x, y
+            return
         if g["cls"] == DIAG1:
             x, y = m[0] * x, m[1] * y
         else:
@@ -126,8 +141,10 @@ def _apply(B, g, mats, tbases, k, nvalid):
         B[i0], B[i1] = x, y
         return
     idx = [U(a0), U(a0 ^ sa), U(a0 ^ sb), U(a0 ^ sa ^ sb)]
+    ridx = [U(r0), U(r0 ^ rsa), U(r0 ^ rsb), U(r0 ^ rsa ^ rsb)]
     assert len(np.unique(np.concatenate(idx))) == 4 * items  # items partition the batch
-    x = [B[ix] for ix in idx]
+    assert len(np.unique(np.concatenate(ridx))) == 4 * items
+    x = [S[ix] for ix in ridx]
     c = int(g["cls"])
     out = list(x)
     if c in (CX01, CX10, SWAP):
