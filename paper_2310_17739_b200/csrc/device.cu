@@ -470,21 +470,29 @@ __device__ __forceinline__ void apply_gate(const double2* __restrict__ src,
     case kPairX: {
       const double2 m0 = *(m), m1 = *(m + 1), m2 = *(m + 2), m3 = *(m + 3);
       const double2 n0 = *(m + 4), n1 = *(m + 5), n2 = *(m + 6), n3 = *(m + 7);
-      const int cls = d.cls;
-      for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
-        // block 0 on members (u0,u1), block 1 on (u2,u3)
-        const int u0 = i0;
-        const int u1 = cls == kPairQ ? i2 : (cls == kPairP ? i1 : i3);
-        const int u2 = cls == kPairP ? i2 : i1;
-        const int u3 = cls == kPairQ ? i3 : (cls == kPairP ? i3 : i2);
-        double2 x = src[u0], y = src[u1], z = src[u2], v = src[u3];
+      // two 2x2 blocks: PairQ on members (0,2),(1,3); PairP (0,1),(2,3); PairX (0,3),(1,2)
+      auto blocks = [&](int la, int lb, int lc, int ld, int sa_, int sb_, int sc, int sd) {
+        double2 x = src[la], y = src[lb], z = src[lc], v = src[ld];
         mix2(x, y, m0, m1, m2, m3);
         mix2(z, v, n0, n1, n2, n3);
-        dst[u0] = x;
-        dst[u1] = y;
-        dst[u2] = z;
-        dst[u3] = v;
-      });
+        dst[sa_] = x;
+        dst[sb_] = y;
+        dst[sc] = z;
+        dst[sd] = v;
+      };
+      if (d.cls == kPairQ) {
+        for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
+          blocks(l0, l2, l1, l3, i0, i2, i1, i3);
+        });
+      } else if (d.cls == kPairP) {
+        for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
+          blocks(l0, l1, l2, l3, i0, i1, i2, i3);
+        });
+      } else {
+        for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
+          blocks(l0, l3, l1, l2, i0, i3, i1, i2);
+        });
+      }
       break;
     }
     case kDiag2: {
