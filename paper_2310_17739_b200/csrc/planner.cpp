@@ -14,12 +14,14 @@
 //     an epilogue reduction of the preceding pass and a collapse prologue of
 //     the next one (engine.py:183-191, 164-167).
 #include "planner_host.h"
+#include "../../include/nucsim_b200.h"
 
 #include <algorithm>
 #include <stdexcept>
 #include <unordered_map>
 
 namespace nsb {
+static_assert(kNumClasses == NSB_N_CLASSES, "class count exported by the C ABI");
 namespace {
 
 inline int popc(uint64_t m) { return __builtin_popcountll(m); }
@@ -460,7 +462,7 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
     g.mat = static_cast<int32_t>(packed_all.size() / 2);
     g.n_mat = static_cast<int32_t>(packed.size() / 2);
     packed_all.insert(packed_all.end(), packed.begin(), packed.end());
-    static const int kNnz[kNumClasses] = {4, 2, 16, 8, 4, 4, 0, 0, 8, 8, 8, 0};
+    static const int kNnz[kNumClasses] = {4, 2, 16, 8, 4, 4, 0, 0, 8, 8, 8, 0, 0};
     flops += 8ll * kNnz[g.cls] * (int64_t(1) << (n - g.nq));
     run.push_back(g);
   }

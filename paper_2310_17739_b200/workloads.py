@@ -225,7 +225,7 @@ def layered_workload(n: int, layers: int, seed: int = 28) -> Workload:
 
 
 CLASS_NAMES = ("dense1", "diag1", "dense2", "sparse2", "mono2", "diag2", "cx01", "cx10",
-               "pair_q", "pair_p", "pair_x", "swap")
+               "pair_q", "pair_p", "pair_x", "swap", "permute")
 
 
 def plan_analyze(ops: np.ndarray, params: np.ndarray, payloads: np.ndarray, n: int) -> dict:
