@@ -20,10 +20,14 @@ cpu_baseline / --impl reference: the oracle port of the reference engine
        (numpy einsum, as nucsim.engine) on a bounded prefix of the same fused
        gate stream, single-threaded, extrapolated per gate.
 
-Multi-GPU (torchrun, N > 1): replicas -- every rank runs the same circuit on
-its own GPU (no data-path collective), value = total gates / max time over
-ranks, "scaling": "weak".  State sharding across GPUs is future work
-(DESIGN.md section 7).
+Multi-GPU (torchrun, N > 1), default configs: replicas -- every rank runs
+the same circuit on its own GPU (no data-path collective), value = total
+gates / max time over ranks, "scaling": "weak".
+
+--config shard [--qubits Q] (BASELINE config 5, default Q = 34): ONE layered
+random circuit whose state is split over the N ranks (sharded.py: 2^(Q-g)
+amplitudes per GPU, NCCL qubit swaps over NVLink, "scaling": "strong").
+value = input gates / max-over-ranks device time of one full execution.
 """
 
 from __future__ import annotations
@@ -192,6 +196,109 @@ def workload_name(args) -> str:
     return f"rand28: 28-qubit random layered U3 + {{CX,CZ,RZZ}} circuit, {args.trotter or 20} layers"
 
 
+def run_sharded(args, rank, world, local):
+    """BASELINE config 5: one state split over all ranks (sharded.py)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2310_17739_b200 import workloads as W
+    from paper_2310_17739_b200.sharded import ShardedState
+
+    n = args.qubits
+    if world > 1:
+        dist.init_process_group("gloo")
+    torch.cuda.set_device(local)
+    t0 = time.perf_counter()
+    wl = W.layered_workload(n, layers=args.trotter or 10, seed=34)
+    fops, pool, stats = W.fuse_packed(wl.ops, wl.params, wl.payloads)
+    host = {"generate_fuse_s": round(time.perf_counter() - t0, 3)}
+    if world > 1:
+        st = ShardedState.from_torch_distributed(n, device=local)
+    else:
+        st = ShardedState(n, 0, 1, local, ShardedState.unique_id())
+    t0 = time.perf_counter()
+    prog = st.compile(fops, wl.params, pool)
+    host["schedule_plan_s"] = round(time.perf_counter() - t0, 3)
+    tot = prog.plan_totals()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def one():
+        st.reset()
+        barrier()
+        st.timer_start()
+        prog.run()
+        return st.timer_stop()
+
+    for _ in range(args.warmup):
+        one()
+    barrier()
+    clocks = Clocks(local)
+    ms = [one() for _ in range(args.steps)]
+    clk = clocks.stop()
+    dev_s = sum(ms) / 1e3
+    if world > 1:
+        box = [None] * world
+        dist.all_gather_object(box, dev_s)
+        dev_s = max(box)
+    # one extra profiled execution (per-step device events; outside the timed region)
+    st.reset()
+    barrier()
+    times: dict = {}
+    prog.run(times=times)
+    t0 = time.perf_counter()
+    st.reset()
+    p2 = st.compile(fops, wl.params, pool)
+    p2.run()
+    norm = st.norm()
+    e2e_s = time.perf_counter() - t0
+    p2.close()
+    nl = st.nl
+    pk = peaks()
+    gate_bytes = tot["n_passes"] * 32 * (1 << nl)
+    swap_bytes = prog.n_swaps * 16 * (1 << (nl - 1))  # sent (= received) per rank
+    gate_s = times.get("gates", 0.0) / 1e3
+    swap_s = times.get("swap", 0.0) / 1e3
+    achieved = gate_bytes / gate_s / 1e9 if gate_s else 0.0
+    line = {"metric": METRIC, "value": round(wl.input_gates * args.steps / dev_s, 1),
+            "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dev_s * 1e3 / args.steps, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": {"workload": f"shard{n}: {n}-qubit random layered U3 + {{CX,CZ,RZZ}} "
+                                   f"circuit, {args.trotter or 10} layers, state split over "
+                                   f"{world} GPU(s)",
+                       "n_qubits": n, "local_qubits": nl, "input_gates": wl.input_gates,
+                       "fused_gates": stats["gates_after"], "passes_per_rank": tot["n_passes"],
+                       "device_gate_sweeps": tot["n_device_gates"], "qubit_swaps": prog.n_swaps,
+                       "parallelism": f"shard{world}",
+                       "l2": f"state shard 2^{nl} x 16 B >> L2; no flush needed"},
+            "host": host,
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
+                         "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
+                         "traffic": None, "peak_source": pk["source"],
+                         "note": "k_blocked only: passes x 32 B x 2^local per rank over the "
+                                 "summed gate-group device time of one profiled execution"},
+            "breakdown_ms": {k: round(v, 3) for k, v in times.items()},
+            "nvlink": {"bytes_sent_per_rank": swap_bytes,
+                       "achieved_gbs": round(swap_bytes / swap_s / 1e9, 1) if swap_s else None,
+                       "note": "per qubit swap each rank sends and receives half its shard"},
+            "e2e": {"value": round(wl.input_gates / e2e_s, 1), "unit": UNIT,
+                    "h2d_bytes_per_step": int(fops.nbytes + wl.params.nbytes + pool.nbytes),
+                    "d2h_bytes_per_step": 8, "s_per_step": round(e2e_s, 4),
+                    "note": "schedule + plan upload from host op arrays + run + norm read-back"},
+            "norm": norm, "gpu_launches": None, "clocks": clk,
+            "cpu_baseline": {"value": None, "unit": UNIT, "cores": 1, "kind": "port",
+                             "sample": f"infeasible: the reference holds 2 x 2^{n} x 16 B "
+                                       "on one host (engine.py:51, 68-71)"}}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    prog.close()
+    st.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def run_ours(args, rank, world, local):
     import ctypes
     import torch
@@ -322,7 +429,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--config", default="deep21", choices=("deep21", "rand28"))
+    ap.add_argument("--config", default="deep21", choices=("deep21", "rand28", "shard"))
+    ap.add_argument("--qubits", type=int, default=34, help="--config shard: total qubits")
     ap.add_argument("--trotter", type=int, default=None)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--ref-budget", type=float, default=12.0)
@@ -330,7 +438,16 @@ def main():
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":
+        if args.config == "shard":
+            if rank == 0:
+                print(json.dumps({"impl": "reference", "metric": METRIC, "value": None,
+                                  "unit": UNIT, "unavailable": f"the reference keeps 2 x 2^"
+                                  f"{args.qubits} x 16 B in one host process"}), flush=True)
+            return
         run_reference(args, rank)
+        return
+    if args.config == "shard":
+        run_sharded(args, rank, world, local)
         return
     run_ours(args, rank, world, local)
 

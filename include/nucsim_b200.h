@@ -231,6 +231,41 @@ int nsb_plan_segment_marker(const nsb_plan* plan, int64_t seg, int32_t* kind, in
  * on the launching stream), and the number of kernels it launched. */
 int nsb_plan_last_timing(const nsb_plan* plan, double* ms, int64_t* launches);
 
+/* Device-side timer on the context's stream (CUDA events): the elapsed
+ * device time of everything the context enqueued between the two calls. */
+int nsb_timer_start(nsb_ctx* ctx, nsb_status* st);
+int nsb_timer_stop(nsb_ctx* ctx, double* ms, nsb_status* st);
+
+/* ---- Sharded state (one process per GPU, NCCL over NVLink) -------------
+ * A state of n qubits is split on its top g = log2(nranks) qubits: rank r
+ * keeps the 2^(n-g) amplitudes whose top bits equal r, as the ordinary
+ * (n-g)-qubit state of its context.  Gates on the local qubits run through
+ * the single-GPU calls above; paper_2310_17739_b200/sharded.py schedules the
+ * qubit swaps that bring a global qubit into the local range (SURVEY.md
+ * 8(e); the reference has no multi-device path -- it replaces engine.py's
+ * full-state loops for states larger than one GPU).
+ *
+ * nsb_comm_unique_id: 128-byte NCCL id, made on one rank and shared with the
+ * others through any host channel.  nsb_comm_init: bind the context to rank
+ * `rank` of `nranks` (a power of two).
+ * nsb_shard_swap: global qubit `global_bit` (rank bit) and local qubit
+ * `local_q` trade places.  The half of the shard whose bit local_q differs
+ * from this rank's bit is exchanged element for element with the partner
+ * rank (rank ^ 1 << global_bit), in chunks of chunk_amps (<= 0: 2^26).
+ * Collective: both partners must call it.
+ * nsb_shard_reset: the shard of |0...0> (rank 0: amplitude 1 at index 0;
+ * other ranks: zeros), on the device.
+ * nsb_shard_allgather: every rank contributes `count` (<= 64) doubles; `out`
+ * receives nranks * count values in rank order (deterministic sums). */
+int nsb_comm_unique_id(uint8_t* id, nsb_status* st);
+int nsb_comm_init(nsb_ctx* ctx, const uint8_t* id, int32_t nranks, int32_t rank,
+                  nsb_status* st);
+int nsb_shard_swap(nsb_ctx* ctx, int32_t global_bit, int32_t local_q, int64_t chunk_amps,
+                   nsb_status* st);
+int nsb_shard_reset(nsb_ctx* ctx, nsb_status* st);
+int nsb_shard_allgather(nsb_ctx* ctx, const double* in, int32_t count, double* out,
+                        nsb_status* st);
+
 #ifdef __cplusplus
 }
 #endif

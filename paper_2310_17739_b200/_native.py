@@ -106,6 +106,13 @@ _SIGNATURES = {
     "nsb_plan_segment_marker": (ctypes.c_int, [_P, _I64, ctypes.POINTER(_I32),
                                                ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
     "nsb_plan_last_timing": (ctypes.c_int, [_P, ctypes.POINTER(_D), ctypes.POINTER(_I64)]),
+    "nsb_timer_start": (ctypes.c_int, [_P, _ST]),
+    "nsb_timer_stop": (ctypes.c_int, [_P, ctypes.POINTER(_D), _ST]),
+    "nsb_comm_unique_id": (ctypes.c_int, [_P, _ST]),
+    "nsb_comm_init": (ctypes.c_int, [_P, _P, _I32, _I32, _ST]),
+    "nsb_shard_swap": (ctypes.c_int, [_P, _I32, _I32, _I64, _ST]),
+    "nsb_shard_reset": (ctypes.c_int, [_P, _ST]),
+    "nsb_shard_allgather": (ctypes.c_int, [_P, _P, _I32, _P, _ST]),
 }
 
 EXPORTS = tuple(_SIGNATURES)

@@ -14,9 +14,12 @@
 //       separated by grid-wide barriers.
 // The state is complex128 in HBM as double2 (16-byte vector loads/stores).
 #include <cooperative_groups.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl is resolved at run time (shard_nccl)
 
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 #include <memory>
 #include <new>
 #include <stdexcept>
@@ -755,6 +758,26 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// sharded state: the half of the local shard that changes owner when a global
+// qubit and local qubit L trade places (bit L == v), packed in index order.
+
+__global__ void k_shard_pack(const double2* __restrict__ a, double2* __restrict__ out,
+                             uint64_t off, uint64_t count, int L, int v) {
+  const uint64_t vb = uint64_t(v) << L;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    out[i] = a[insert_zero(off + i, L) | vb];
+}
+
+__global__ void k_shard_unpack(double2* __restrict__ a, const double2* __restrict__ in,
+                               uint64_t off, uint64_t count, int L, int v) {
+  const uint64_t vb = uint64_t(v) << L;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < count;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    a[insert_zero(off + i, L) | vb] = in[i];
+}
+
 }  // namespace dev
 }  // namespace nsb
 
@@ -808,6 +831,7 @@ struct nsb_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t tev0 = nullptr, tev1 = nullptr;  // nsb_timer_start / stop
   int sm_count = 0;
   int blocked_grid = 0;  // co-resident CTAs of k_blocked
   int n = 0;
@@ -816,6 +840,10 @@ struct nsb_ctx {
   DevBuf<double> scratch;  // reductions
   double* pinned = nullptr;
   size_t pinned_bytes = 0;
+  // sharded state (nsb_comm_init): this process holds rank `rank` of `nranks`
+  void* comm = nullptr;  // ncclComm_t
+  int rank = 0, nranks = 1;
+  DevBuf<double2> stage_send, stage_recv;
 };
 
 struct nsb_plan {
@@ -831,6 +859,64 @@ struct nsb_plan {
 };
 
 namespace {
+
+// NCCL is resolved at run time from the process's libnccl.so.2 (torch's copy
+// when torch is loaded, else the system library), so the library keeps
+// loading on machines without NCCL and never carries a second NCCL instance.
+struct NcclApi {
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclAllGather) all_gather = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+  std::string error;
+};
+
+const NcclApi& shard_nccl() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.error = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return a;
+    }
+#define NSB_NCCL_SYM(field, name)                                     \
+  a.field = reinterpret_cast<decltype(a.field)>(dlsym(h, #name));     \
+  if (!a.field) a.error = "libnccl lacks " #name;
+    NSB_NCCL_SYM(get_unique_id, ncclGetUniqueId)
+    NSB_NCCL_SYM(comm_init_rank, ncclCommInitRank)
+    NSB_NCCL_SYM(comm_destroy, ncclCommDestroy)
+    NSB_NCCL_SYM(send, ncclSend)
+    NSB_NCCL_SYM(recv, ncclRecv)
+    NSB_NCCL_SYM(all_gather, ncclAllGather)
+    NSB_NCCL_SYM(group_start, ncclGroupStart)
+    NSB_NCCL_SYM(group_end, ncclGroupEnd)
+    NSB_NCCL_SYM(error_string, ncclGetErrorString)
+#undef NSB_NCCL_SYM
+    return a;
+  }();
+  if (!api.error.empty()) throw CudaError(api.error);
+  return api;
+}
+
+#define NSB_NCCL(call)                                                                 \
+  do {                                                                                 \
+    const ncclResult_t r_ = (call);                                                    \
+    if (r_ != ncclSuccess)                                                             \
+      throw CudaError(std::string(#call) + ": " + shard_nccl().error_string(r_));      \
+  } while (0)
+
+void shard_comm_destroy(nsb_ctx* c) {
+  if (c->comm) shard_nccl().comm_destroy(static_cast<ncclComm_t>(c->comm));
+  c->comm = nullptr;
+  c->rank = 0;
+  c->nranks = 1;
+}
 
 int fail_status(nsb_status* st, int code, const std::string& msg) {
   set_status(st, code, msg);
@@ -997,6 +1083,8 @@ int nsb_ctx_create(int32_t device, nsb_ctx** out, nsb_status* st) {
     NSB_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     NSB_CUDA(cudaEventCreate(&ctx->ev0));
     NSB_CUDA(cudaEventCreate(&ctx->ev1));
+    NSB_CUDA(cudaEventCreate(&ctx->tev0));
+    NSB_CUDA(cudaEventCreate(&ctx->tev1));
     NSB_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
     const int smem = static_cast<int>(dev::kBlockedSmemBytes);
     NSB_CUDA(cudaFuncSetAttribute(dev::k_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1016,11 +1104,16 @@ void nsb_ctx_destroy(nsb_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->comm) shard_comm_destroy(ctx);
   ctx->amps.release();
   ctx->scratch.release();
+  ctx->stage_send.release();
+  ctx->stage_recv.release();
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->tev0) cudaEventDestroy(ctx->tev0);
+  if (ctx->tev1) cudaEventDestroy(ctx->tev1);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -1297,6 +1390,125 @@ int nsb_plan_last_timing(const nsb_plan* P, double* ms, int64_t* launches) {
   if (ms) *ms = P->last_ms;
   if (launches) *launches = P->last_launches;
   return NSB_OK;
+}
+
+int nsb_timer_start(nsb_ctx* c, nsb_status* st) {
+  return guarded(st, [&] {
+    if (!c) throw std::invalid_argument("null context");
+    NSB_CUDA(cudaSetDevice(c->device));
+    NSB_CUDA(cudaEventRecord(c->tev0, c->stream));
+  });
+}
+
+int nsb_timer_stop(nsb_ctx* c, double* ms, nsb_status* st) {
+  return guarded(st, [&] {
+    if (!c || !ms) throw std::invalid_argument("null argument");
+    NSB_CUDA(cudaSetDevice(c->device));
+    NSB_CUDA(cudaEventRecord(c->tev1, c->stream));
+    NSB_CUDA(cudaEventSynchronize(c->tev1));
+    float f = 0.f;
+    NSB_CUDA(cudaEventElapsedTime(&f, c->tev0, c->tev1));
+    *ms = f;
+  });
+}
+
+// ---------------------------------------------------------------------------
+// sharded state
+
+int nsb_comm_unique_id(uint8_t* id, nsb_status* st) {
+  return guarded(st, [&] {
+    if (!id) throw std::invalid_argument("null id buffer");
+    ncclUniqueId u;
+    NSB_NCCL(shard_nccl().get_unique_id(&u));
+    std::memcpy(id, u.internal, NCCL_UNIQUE_ID_BYTES);
+  });
+}
+
+int nsb_comm_init(nsb_ctx* c, const uint8_t* id, int32_t nranks, int32_t rank, nsb_status* st) {
+  if (!c || !id) return fail_status(st, NSB_EINVAL, "null argument");
+  if (nranks < 1 || (nranks & (nranks - 1)) || rank < 0 || rank >= nranks)
+    return fail_status(st, NSB_EINVAL, "rank count must be a power of two and rank < count");
+  return guarded(st, [&] {
+    NSB_CUDA(cudaSetDevice(c->device));
+    if (c->comm) shard_comm_destroy(c);
+    ncclUniqueId u;
+    std::memcpy(u.internal, id, NCCL_UNIQUE_ID_BYTES);
+    ncclComm_t comm = nullptr;
+    NSB_NCCL(shard_nccl().comm_init_rank(&comm, nranks, u, rank));
+    c->comm = comm;
+    c->rank = rank;
+    c->nranks = nranks;
+  });
+}
+
+int nsb_shard_swap(nsb_ctx* c, int32_t global_bit, int32_t local_q, int64_t chunk_amps,
+                   nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    if (!c->comm) throw std::invalid_argument("no communicator (nsb_comm_init)");
+    if (global_bit < 0 || (1 << global_bit) >= c->nranks || local_q < 0 || local_q >= c->n)
+      throw std::invalid_argument("bad shard swap qubits");
+    NSB_CUDA(cudaSetDevice(c->device));
+    const NcclApi& api = shard_nccl();
+    const int peer = c->rank ^ (1 << global_bit);
+    const int v = 1 - ((c->rank >> global_bit) & 1);  // the half that changes owner
+    const uint64_t half = c->n_amps >> 1;
+    const uint64_t chunk =
+        std::min<uint64_t>(half, chunk_amps > 0 ? uint64_t(chunk_amps) : (uint64_t(1) << 26));
+    if (c->stage_send.count < chunk) {
+      c->stage_send.alloc(chunk);
+      c->stage_recv.alloc(chunk);
+    }
+    auto comm = static_cast<ncclComm_t>(c->comm);
+    for (uint64_t off = 0; off < half; off += chunk) {
+      const uint64_t cnt = std::min(chunk, half - off);
+      const unsigned grid = grid_for(cnt, 256, c);
+      dev::k_shard_pack<<<grid, 256, 0, c->stream>>>(c->amps.ptr, c->stage_send.ptr, off, cnt,
+                                                     local_q, v);
+      NSB_CUDA(cudaGetLastError());
+      NSB_NCCL(api.group_start());
+      NSB_NCCL(api.send(c->stage_send.ptr, 2 * cnt, ncclFloat64, peer, comm, c->stream));
+      NSB_NCCL(api.recv(c->stage_recv.ptr, 2 * cnt, ncclFloat64, peer, comm, c->stream));
+      NSB_NCCL(api.group_end());
+      dev::k_shard_unpack<<<grid, 256, 0, c->stream>>>(c->amps.ptr, c->stage_recv.ptr, off,
+                                                       cnt, local_q, v);
+      NSB_CUDA(cudaGetLastError());
+    }
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int nsb_shard_reset(nsb_ctx* c, nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    NSB_CUDA(cudaSetDevice(c->device));
+    if (c->rank == 0) {
+      dev::k_vacuum<<<grid_for(c->n_amps, 256, c), 256, 0, c->stream>>>(c->amps.ptr, c->n_amps);
+      NSB_CUDA(cudaGetLastError());
+    } else {
+      NSB_CUDA(cudaMemsetAsync(c->amps.ptr, 0, c->n_amps * sizeof(double2), c->stream));
+    }
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int nsb_shard_allgather(nsb_ctx* c, const double* in, int32_t count, double* out,
+                        nsb_status* st) {
+  return guarded(st, [&] {
+    if (!c || !c->comm) throw std::invalid_argument("no communicator (nsb_comm_init)");
+    if (!in || !out || count < 1 || count > 64) throw std::invalid_argument("bad gather size");
+    NSB_CUDA(cudaSetDevice(c->device));
+    if (c->scratch.count < size_t(2 * dev::kReduceBlocks + 8 + 64 * (c->nranks + 1)))
+      throw std::invalid_argument("gather exceeds scratch");
+    double* d_in = c->scratch.ptr + 2 * dev::kReduceBlocks + 8;
+    double* d_out = d_in + 64;
+    NSB_CUDA(cudaMemcpyAsync(d_in, in, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    NSB_NCCL(shard_nccl().all_gather(d_in, d_out, count, ncclFloat64,
+                                     static_cast<ncclComm_t>(c->comm), c->stream));
+    NSB_CUDA(cudaMemcpyAsync(out, d_out, size_t(count) * c->nranks * sizeof(double),
+                             cudaMemcpyDeviceToHost, c->stream));
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+  });
 }
 
 }  // extern "C"

@@ -1,0 +1,361 @@
+"""State vectors larger than one GPU: one process per GPU, state split on its
+top qubits, NCCL qubit swaps.
+
+The reference keeps the whole 2^n state in one host array
+(nucsim/engine.py:42-84) and applies every gate to it (engine.py:92-156,
+383-430).  Here a state of n qubits lives on P = 2^g ranks: rank r holds the
+2^(n-g) amplitudes whose top g index bits equal r, as the ordinary
+(n-g)-qubit state of its own context.  The logical-to-physical qubit layout
+is a permutation: a gate runs through the single-GPU plan (k_blocked) when
+all its qubits sit at local positions; otherwise a *qubit swap* trades a
+global position with a local one (nsb_shard_swap: each rank exchanges half
+its shard with one partner over NVLink).
+
+`schedule` is the host half: it walks the op stream in a dependency-
+respecting order (an op may run ahead of earlier ops on disjoint qubits,
+measurements stay in their order), emits maximal local gate groups, and
+when no op can proceed swaps in the qubits of the oldest waiting op,
+evicting the local qubits whose next use is furthest away (Belady).  At the
+end the layout is restored to the identity so every rank's shard is the
+canonical slice of the state.
+
+MMA measurements (engine.py:183-191, 414-423) are collective: every rank
+computes its partial P(q=0) with the fixed-order device reduction, the
+partials are all-gathered and summed in rank order (identical on every
+rank), and every rank collapses with the same p0.  Resets are no-ops in MMA
+mode as in the reference; rejection mode is single-GPU only.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .errors import FilterAssertionError
+from .gates import Gate
+
+EPS_MMA = 1e-12
+
+
+@dataclass
+class Step:
+    kind: str                        # "gates" | "swap" | "measure"
+    ops: np.ndarray | None = None    # "gates": op records on LOCAL positions
+    global_bit: int = -1             # "swap": rank bit that trades places ...
+    local_q: int = -1                # ... with this local position
+    step: int = -1                   # "measure": reference step index
+
+
+def _qubits(rec) -> tuple[int, ...]:
+    return tuple(int(q) for q in rec["q"][: int(rec["nq"])])
+
+
+def _translate(ops: np.ndarray, idx: list[int], pos: list[int]) -> np.ndarray:
+    out = ops[np.asarray(idx, np.int64)].copy()
+    lut = np.asarray(pos, np.int32)
+    q = out["q"]
+    for j in range(q.shape[1]):
+        live = out["nq"] > j
+        q[live, j] = lut[q[live, j]]
+    out["q"] = q
+    mask = np.zeros(len(out), np.uint64)
+    for j in range(q.shape[1]):
+        live = out["nq"] > j
+        mask[live] |= np.left_shift(np.uint64(1), q[live, j].astype(np.uint64))
+    out["mask"] = mask
+    return out
+
+
+def schedule(ops: np.ndarray, n: int, g: int, window: int = 4096) -> list[Step]:
+    """Split an MMA op stream (gates, measures, resets, barriers; no trailing
+    sampling block) into local gate groups, qubit swaps and collective
+    measurements for 2^g ranks.  Pure host logic (tested on CPU)."""
+    if g < 0 or g >= n:
+        raise ValueError("need 0 <= g < n")
+    nl = n - g
+    kinds = ops["kind"]
+    step_of = {}
+    pending = []
+    s = 0
+    for i in range(len(ops)):
+        k = int(kinds[i])
+        if k == N.OP_MEASURE:
+            step_of[i] = s
+            s += 1
+            pending.append(i)
+        elif k == N.OP_GATE:
+            pending.append(i)
+        elif k not in (N.OP_RESET, N.OP_BARRIER):
+            raise ValueError(f"op {i}: unknown kind {k}")
+    qs = {i: _qubits(ops[i]) for i in pending}
+    pos = list(range(n))   # logical qubit -> position
+    at = list(range(n))    # position -> logical qubit
+    steps: list[Step] = []
+    group: list[int] = []
+
+    def flush():
+        if group:
+            steps.append(Step("gates", ops=_translate(ops, group, pos)))
+            group.clear()
+
+    def swap(gpos: int, lpos: int):
+        flush()
+        steps.append(Step("swap", global_bit=gpos - nl, local_q=lpos))
+        a, b = at[gpos], at[lpos]
+        at[gpos], at[lpos] = b, a
+        pos[a], pos[b] = lpos, gpos
+
+    while pending:
+        blocked: set[int] = set()
+        measure_waiting = False
+        waiting: list[int] = []
+        for j, i in enumerate(pending):
+            if j >= window or len(blocked) == n:
+                waiting.extend(pending[j:])
+                break
+            q = qs[i]
+            is_m = int(kinds[i]) == N.OP_MEASURE
+            if (all(pos[x] < nl for x in q) and blocked.isdisjoint(q)
+                    and not (is_m and measure_waiting)):
+                if is_m:
+                    flush()
+                    steps.append(Step("measure", local_q=pos[q[0]], step=step_of[i]))
+                else:
+                    group.append(i)
+            else:
+                waiting.append(i)
+                blocked.update(q)
+                measure_waiting |= is_m
+        pending = waiting
+        if not pending:
+            break
+        head = qs[pending[0]]
+        if all(pos[x] < nl for x in head):
+            continue  # the scan stopped at the window; keep going
+        nxt = {}
+        for j, i in enumerate(pending[:window]):
+            for x in qs[i]:
+                nxt.setdefault(x, j)
+        for x in head:
+            if pos[x] < nl:
+                continue
+            victims = [p for p in range(nl) if at[p] not in head]
+            if not victims:
+                raise ValueError("op needs more qubits than the local range holds")
+            far = max(victims, key=lambda p: (nxt.get(at[p], 1 << 62), p))
+            swap(pos[x], far)
+    flush()
+    # restore the identity layout: global positions first, then a local
+    # permutation as exact SWAP gates (the planner's frame makes them free)
+    for gp in range(nl, n):
+        if at[gp] == gp:
+            continue
+        if pos[gp] >= nl:  # wanted qubit sits in another global position
+            p = max(p for p in range(nl))
+            swap(pos[gp], p)
+        swap(gp, pos[gp])
+    perm_ops = []
+    for p in range(nl):
+        while at[p] != p:
+            t = at[p]
+            perm_ops.append((p, t))
+            a, b = at[p], at[t]
+            at[p], at[t] = b, a
+            pos[a], pos[b] = t, p
+    if perm_ops:
+        rec = np.zeros(len(perm_ops), N.OP_DTYPE)
+        rec["kind"], rec["tag"], rec["nq"], rec["cbit"] = N.OP_GATE, Gate.SWAP.code, 2, -1
+        rec["q"] = -1
+        rec["src"], rec["param"], rec["payload"] = -1, -1, -1
+        for j, (a, b) in enumerate(perm_ops):
+            rec["q"][j, 0], rec["q"][j, 1] = a, b
+            rec["mask"][j] = (1 << a) | (1 << b)
+        steps.append(Step("gates", ops=rec))
+    assert pos == list(range(n))
+    return steps
+
+
+def swap_count(steps: list[Step]) -> int:
+    return sum(1 for s in steps if s.kind == "swap")
+
+
+class ShardedState:
+    """The local shard of an n-qubit state on this rank (torch.distributed
+    supplies rank / world size and carries the NCCL id; the data path is the
+    library's own NCCL communicator on the context's stream)."""
+
+    def __init__(self, n_qubits: int, rank: int, world: int, device: int, nccl_id: bytes):
+        g = world.bit_length() - 1
+        if world < 1 or (1 << g) != world:
+            raise ValueError("rank count must be a power of two")
+        if n_qubits - g < 2:
+            raise ValueError("need at least 2 local qubits per rank")
+        self.n, self.g, self.nl = n_qubits, g, n_qubits - g
+        self.rank, self.world = rank, world
+        self.dev = N.Device(device)
+        self.dev.call("nsb_state_init", self.nl)
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
+        self.dev.call("nsb_comm_init", buf, world, rank)
+        self.reset()
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (ctypes.c_uint8 * 128)()
+        st = N.Status()
+        N.check(N.lib().nsb_comm_unique_id(buf, ctypes.byref(st)), st)
+        return bytes(buf)
+
+    @classmethod
+    def from_torch_distributed(cls, n_qubits: int, device: int | None = None):
+        """Collective: rank 0 makes the NCCL id, torch.distributed broadcasts it."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        box = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        if device is None:
+            import os
+            device = int(os.environ.get("LOCAL_RANK", rank))
+        return cls(n_qubits, rank, world, device, box[0])
+
+    def close(self):
+        self.dev.close()
+
+    # -- collectives -----------------------------------------------------------
+    def allgather(self, values) -> np.ndarray:
+        v = np.ascontiguousarray(values, np.float64).reshape(-1)
+        out = np.zeros(v.size * self.world, np.float64)
+        self.dev.call("nsb_shard_allgather", N.ptr(v), v.size, N.ptr(out))
+        return out.reshape(self.world, v.size)
+
+    def _sum(self, local: float) -> float:
+        total = 0.0
+        for x in self.allgather([local])[:, 0]:  # rank order on every rank
+            total += float(x)
+        return total
+
+    def norm(self) -> float:
+        out = ctypes.c_double(0.0)
+        self.dev.call("nsb_state_norm2", ctypes.byref(out))
+        return float(np.sqrt(self._sum(out.value)))
+
+    def reset(self):
+        """|0...0>: amplitude 1 on rank 0, zeros elsewhere (on the device)."""
+        self.dev.call("nsb_shard_reset")
+
+    def upload(self, full: np.ndarray):
+        """Load this rank's slice of a full host state (tests, small n)."""
+        lo = self.rank << self.nl
+        sl = np.ascontiguousarray(full[lo: lo + (1 << self.nl)], np.complex128)
+        self.dev.call("nsb_state_upload", N.ptr(sl))
+
+    def download(self) -> np.ndarray:
+        host = np.empty(1 << self.nl, np.complex128)
+        self.dev.call("nsb_state_download", N.ptr(host))
+        return host
+
+    # -- execution --------------------------------------------------------------
+    def compile(self, ops, params, payloads, window: int = 4096) -> "ShardedProgram":
+        """Schedule an MMA op stream and upload one device plan per gate group."""
+        return ShardedProgram(self, schedule(ops, self.n, self.g, window), params, payloads)
+
+    def run_mma(self, ops, params, payloads, eps: float = EPS_MMA, window: int = 4096):
+        prog = self.compile(ops, params, payloads, window)
+        try:
+            probs = prog.run(eps)
+        finally:
+            prog.close()
+        return [probs[k] for k in sorted(probs)], prog.steps
+
+    def timer_start(self):
+        self.dev.call("nsb_timer_start")
+
+    def timer_stop(self) -> float:
+        ms = ctypes.c_double(0.0)
+        self.dev.call("nsb_timer_stop", ctypes.byref(ms))
+        return float(ms.value)
+
+
+class ShardedProgram:
+    """A schedule with its gate groups compiled into device plans (nsb_plan)
+    bound to one rank's context."""
+
+    def __init__(self, state: ShardedState, steps: list[Step], params, payloads):
+        self.state, self.steps = state, steps
+        self.plans: list[tuple[ctypes.c_void_p, int] | None] = []
+        st = N.Status()
+        try:
+            for s in steps:
+                if s.kind != "gates":
+                    self.plans.append(None)
+                    continue
+                h = ctypes.c_void_p()
+                N.check(N.lib().nsb_plan_create(state.dev.handle, N.ptr(s.ops), len(s.ops),
+                                                N.ptr(params), N.ptr(payloads.view(np.float64)),
+                                                ctypes.byref(h), ctypes.byref(st)), st)
+                info = N.PlanInfo()
+                N.lib().nsb_plan_info_get(h, ctypes.byref(info))
+                self.plans.append((h, int(info.n_items)))
+        except Exception:
+            self.close()
+            raise
+        self.n_swaps = swap_count(steps)
+
+    def close(self):
+        for e in self.plans:
+            if e is not None:
+                N.lib().nsb_plan_destroy(e[0])
+        self.plans = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def run(self, eps: float = EPS_MMA, chunk_amps: int = 0,
+            times: dict | None = None) -> dict[int, float]:
+        """Execute on this rank (collective with the other ranks); returns
+        {step: p0}.  Raises FilterAssertionError on every rank when a
+        post-selection probability falls below eps.  With `times`, each step
+        is bracketed by device events and its time (ms) is added under its
+        kind ("gates" / "swap" / "measure")."""
+        S = self.state
+        probs: dict[int, float] = {}
+        st = N.Status()
+        for s, plan in zip(self.steps, self.plans):
+            if times is not None:
+                S.timer_start()
+            if s.kind == "gates":
+                h, n_items = plan
+                for i in range(n_items):
+                    N.check(N.lib().nsb_plan_run_segment(S.dev.handle, h, i, ctypes.byref(st)),
+                            st)
+            elif s.kind == "swap":
+                S.dev.call("nsb_shard_swap", s.global_bit, s.local_q, chunk_amps)
+            else:
+                p = ctypes.c_double(0.0)
+                S.dev.call("nsb_branch_probability", s.local_q, 0, ctypes.byref(p))
+                p0 = S._sum(p.value)
+                probs[s.step] = p0
+                if p0 < eps:
+                    raise FilterAssertionError(s.step, p0)
+                S.dev.call("nsb_project", s.local_q, 0, p0)
+            if times is not None:
+                times[s.kind] = times.get(s.kind, 0.0) + S.timer_stop()
+        return probs
+
+    def plan_totals(self) -> dict:
+        """Summed nsb_plan_info counters over the gate groups."""
+        tot: dict[str, int] = {}
+        for e in self.plans:
+            if e is None:
+                continue
+            info = N.PlanInfo()
+            N.lib().nsb_plan_info_get(e[0], ctypes.byref(info))
+            for k, _ in N.PlanInfo._fields_:
+                if k != "tile_qubits":
+                    tot[k] = tot.get(k, 0) + int(getattr(info, k))
+        return tot

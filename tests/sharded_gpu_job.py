@@ -1,0 +1,56 @@
+"""torchrun job for tests/test_sharded.py::test_nccl_sharded_matches_oracle:
+every rank runs the sharded NCCL executor on its GPU, rank 0 gathers the
+shards and stores them next to the full-state oracle run."""
+
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch.distributed as dist
+
+ROOT = Path(__file__).resolve().parents[1]
+for p in (ROOT, ROOT / "tests", ROOT / "oracle"):
+    sys.path.insert(0, str(p))
+
+import shard_exec as SE  # noqa: E402
+from paper_2310_17739_b200 import sharded as S  # noqa: E402
+from paper_2310_17739_b200 import workloads as W  # noqa: E402
+
+
+def cases():
+    wl = W.filter_workload(11, 1, n_steps=3, seed=5, hop_range=8)
+    fops, pool, _ = W.fuse_packed(wl.ops, wl.params, wl.payloads)
+    yield "filter12", wl.executable(fops), wl.params, pool, wl.n_qubits
+    wl = W.layered_workload(14, 6, 14)
+    fops, pool, _ = W.fuse_packed(wl.ops, wl.params, wl.payloads)
+    yield "layered14", fops, wl.params, pool, 14
+
+
+def main(out):
+    dist.init_process_group("gloo")
+    rank = dist.get_rank()
+    res = {}
+    for tag, ops, params, pool, n in cases():
+        st = S.ShardedState.from_torch_distributed(n, device=int(os.environ["LOCAL_RANK"]))
+        probs, steps = st.run_mma(ops, params, pool)
+        shard = st.download()
+        norm = st.norm()
+        st.close()
+        shards = [None] * dist.get_world_size()
+        dist.all_gather_object(shards, shard)
+        if rank == 0:
+            want_p, want = SE.full_mma(ops, params, pool, n)
+            res["got_" + tag] = np.concatenate(shards)
+            res["want_" + tag] = want
+            res["gotp_" + tag] = np.asarray(probs)
+            res["wantp_" + tag] = np.asarray(want_p)
+            print(tag, "swaps", S.swap_count(steps), "norm", norm, flush=True)
+    if rank == 0:
+        np.savez(out, **res)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])

@@ -1,0 +1,196 @@
+"""Sharded state (paper_2310_17739_b200/sharded.py).
+
+CPU: the schedule (qubit swaps, reordered local groups, collective
+measurements, layout restore) is executed on numpy shards with the oracle's
+primitives and must reproduce the full-state reference run; a world_size-2
+gloo job runs the same steps with one shard per process and real
+point-to-point exchanges.  GPU (>= 2 devices): the NCCL path against the
+oracle."""
+
+from __future__ import annotations
+
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import shard_exec as SE
+from paper_2310_17739_b200 import _native as N
+from paper_2310_17739_b200 import sharded as S
+from paper_2310_17739_b200 import workloads as W
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _filter(n_sys=7, trotter=1, n_steps=3, seed=5):
+    wl = W.filter_workload(n_sys, trotter, n_steps=n_steps, seed=seed, hop_range=6)
+    fops, pool, _ = W.fuse_packed(wl.ops, wl.params, wl.payloads)
+    return wl.executable(fops), wl.params, pool, wl.n_qubits
+
+
+def _layered(n, layers, seed):
+    wl = W.layered_workload(n, layers, seed)
+    fops, pool, _ = W.fuse_packed(wl.ops, wl.params, wl.payloads)
+    return fops, wl.params, pool, n
+
+
+def _close(got, want, tol=1e-10):
+    assert np.linalg.norm(got - want) <= tol * max(np.linalg.norm(want), 1e-300)
+
+
+@pytest.mark.parametrize("g", [1, 2, 3])
+def test_schedule_filter_matches_full_state(g):
+    ops, params, pool, n = _filter()
+    want_p, want = SE.full_mma(ops, params, pool, n)
+    steps = S.schedule(ops, n, g)
+    assert S.swap_count(steps) > 0
+    got_p, got = SE.run_steps_all(steps, params, pool, n, g)
+    assert [got_p[k] for k in sorted(got_p)] == pytest.approx(want_p, rel=1e-10, abs=1e-14)
+    _close(got, want)
+
+
+@pytest.mark.parametrize("n,g,seed", [(7, 1, 1), (8, 2, 2), (9, 3, 3), (10, 1, 4)])
+def test_schedule_layered_matches_full_state(n, g, seed):
+    ops, params, pool, n = _layered(n, 4, seed)
+    _, want = SE.full_mma(ops, params, pool, n)
+    steps = S.schedule(ops, n, g)
+    _, got = SE.run_steps_all(steps, params, pool, n, g)
+    _close(got, want)
+
+
+def test_schedule_small_window_and_order():
+    ops, params, pool, n = _filter(seed=9)
+    want_p, want = SE.full_mma(ops, params, pool, n)
+    for window in (1, 3, 17):
+        steps = S.schedule(ops, n, 2, window=window)
+        got_p, got = SE.run_steps_all(steps, params, pool, n, 2)
+        # measurements keep their reference order
+        order = [s.step for s in steps if s.kind == "measure"]
+        assert order == sorted(order) == list(range(len(want_p)))
+        _close(got, want)
+
+
+def test_schedule_lookahead_saves_swaps():
+    ops, _, _, n = _layered(12, 6, 7)
+    eager = S.swap_count(S.schedule(ops, n, 2, window=1))
+    ahead = S.swap_count(S.schedule(ops, n, 2))
+    assert ahead <= eager
+
+
+def test_schedule_g0_is_one_group():
+    ops, params, pool, n = _filter()
+    steps = S.schedule(ops, n, 0)
+    assert S.swap_count(steps) == 0
+    assert all(s.kind in ("gates", "measure") for s in steps)
+
+
+def test_schedule_rejects_bad_args():
+    ops, _, _, n = _filter()
+    with pytest.raises(ValueError):
+        S.schedule(ops, n, n)
+
+
+# ---------------------------------------------------------------------------
+# world_size-2 gloo: one shard per process, real exchanges
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gloo_worker(rank, world, port, n, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ops, params, pool, n = _filter()
+        g = world.bit_length() - 1
+        nl = n - g
+        steps = S.schedule(ops, n, g)
+        a = np.zeros(1 << nl, np.complex128)
+        if rank == 0:
+            a[0] = 1.0
+        probs = {}
+        for s in steps:
+            if s.kind == "gates":
+                a = SE.apply_ops(a, s.ops, params, pool)
+            elif s.kind == "swap":
+                b = (rank >> s.global_bit) & 1
+                half = SE.half_index(nl, s.local_q, 1 - b)
+                send = torch.from_numpy(a[half].view(np.float64).copy())
+                recv = torch.empty_like(send)
+                peer = rank ^ (1 << s.global_bit)
+                reqs = [dist.isend(send, peer), dist.irecv(recv, peer)]
+                for r in reqs:
+                    r.wait()
+                a[half] = recv.numpy().view(np.complex128)
+            else:
+                part = torch.tensor([SE.O.branch_probability(a, s.local_q, 0)], dtype=torch.float64)
+                parts = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+                dist.all_gather(parts, part)
+                p0 = 0.0
+                for t in parts:
+                    p0 += float(t[0])
+                probs[s.step] = p0
+                SE.O.project(a, s.local_q, 0, p0)
+        shards = [None] * world
+        dist.all_gather_object(shards, a)
+        if rank == 0:
+            q.put((probs, np.concatenate(shards)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_world2_matches_full_state(world):
+    ops, params, pool, n = _filter()
+    want_p, want = SE.full_mma(ops, params, pool, n)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    probs, got = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [probs[k] for k in sorted(probs)] == pytest.approx(want_p, rel=1e-10, abs=1e-14)
+    _close(got, want)
+
+
+# ---------------------------------------------------------------------------
+# GPU: NCCL exchange on >= 2 devices (run under gpurun --gpus 2)
+
+
+def _gpu_count():
+    try:
+        return N.device_count()
+    except Exception:
+        return 0
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(_gpu_count() < 2, reason="needs two GPUs")
+def test_nccl_sharded_matches_oracle(tmp_path):
+    port = _free_port()
+    out = tmp_path / "sharded.npz"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           str(ROOT / "tests" / "sharded_gpu_job.py"), str(out)]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    d = np.load(out)
+    for name in d.files:
+        if name.startswith("want_"):
+            tag = name[5:]
+            _close(d["got_" + tag], d[name])
+            assert np.allclose(d["gotp_" + tag], d["wantp_" + tag], rtol=1e-10, atol=1e-14)
