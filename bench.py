@@ -270,7 +270,8 @@ def run_sharded(args, rank, world, local):
                                    f"{world} GPU(s)",
                        "n_qubits": n, "local_qubits": nl, "input_gates": wl.input_gates,
                        "fused_gates": stats["gates_after"], "passes_per_rank": tot["n_passes"],
-                       "device_gate_sweeps": tot["n_device_gates"], "qubit_swaps": prog.n_swaps,
+                       "device_gate_ops": tot["n_device_gates"], "octet_sweeps": tot["n_sweeps"],
+                       "qubit_swaps": prog.n_swaps,
                        "parallelism": f"shard{world}",
                        "l2": f"state shard 2^{nl} x 16 B >> L2; no flush needed"},
             "host": host,
@@ -393,7 +394,8 @@ def run_ours(args, rank, world, local):
                        "input_gates": wl.input_gates, "fused_gates": stats["gates_after"],
                        "fusion_reduction": round(wl.input_gates / max(stats["gates_after"], 1), 3),
                        "passes": info.n_passes,
-                       "device_gate_sweeps": info.n_device_gates,
+                       "device_gate_ops": info.n_device_gates,
+                       "octet_sweeps": info.n_sweeps,
                        "frame_absorbed_gates": info.n_frame_gates,
                        "frame_flush_gates": info.n_flush_gates,
                        "gates_per_pass": round(info.n_gates / max(info.n_passes, 1), 2),

@@ -173,7 +173,8 @@ typedef struct nsb_plan_info {
   int64_t n_items;      /* gate segments + markers (nsb_plan_segment_marker) */
   int64_t n_frame_gates; /* exact CX/SWAP absorbed by the relabeling frame */
   int64_t n_flush_gates; /* physical CX emitted to flush the frame */
-  int64_t n_device_gates;/* gate sweeps executed on the device per run */
+  int64_t n_device_gates;/* gate ops executed on the device per run */
+  int64_t n_sweeps;      /* shared-memory octet sweeps (gate groups) per run */
 } nsb_plan_info;
 
 /* ops: the executable part of the circuit (sampling block already removed,
@@ -195,17 +196,18 @@ int nsb_plan_analyze(const nsb_op* ops, int64_t n_ops, const double* params,
 int nsb_plan_info_get(const nsb_plan* plan, nsb_plan_info* info);
 
 /* Host-side view of a compiled plan, for tests and tooling: the device
- * program exactly as nsb_plan_create would upload it (PassDesc / GateDesc
+ * program exactly as nsb_plan_create would upload it (PassDesc / GroupDesc / GateOp
  * records of paper_2310_17739_b200/csrc/planner.h, packed matrices).  The
  * library never executes a plan on the host; tests/plan_exec.py does, to
  * verify the planner on machines without a GPU. */
 typedef struct nsb_plan_view {
   int32_t n_qubits, tile_qubits, mma_ok, n_measures;
-  int32_t pass_desc_bytes, gate_desc_bytes, pad0, pad1;
-  int64_t n_passes, n_mma_passes, n_gate_descs, n_matrices, n_items;
+  int32_t pass_desc_bytes, group_desc_bytes, gate_op_bytes, pad0;
+  int64_t n_passes, n_mma_passes, n_groups, n_gate_ops, n_matrices, n_items;
   const void* passes;      /* plain gate passes (items reference ranges) */
   const void* mma_passes;  /* single-launch MMA program */
-  const void* gates;
+  const void* groups;      /* GroupDesc records */
+  const void* gate_ops;    /* GateOp records */
   const double* matrices;  /* complex pool */
   const int32_t* items;    /* n_items x 4: kind (0 gates, 1 measure, 2 reset,
                               3 dense), pass_begin | qubit, pass_end | step, k */

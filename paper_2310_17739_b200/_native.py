@@ -49,20 +49,20 @@ class PlanInfo(ctypes.Structure):
                 ("n_segments", ctypes.c_int64), ("flops", ctypes.c_int64),
                 ("tile_qubits", ctypes.c_int64), ("n_items", ctypes.c_int64),
                 ("n_frame_gates", ctypes.c_int64), ("n_flush_gates", ctypes.c_int64),
-                ("n_device_gates", ctypes.c_int64)]
+                ("n_device_gates", ctypes.c_int64), ("n_sweeps", ctypes.c_int64)]
 
 
 class PlanView(ctypes.Structure):
     _fields_ = [("n_qubits", ctypes.c_int32), ("tile_qubits", ctypes.c_int32),
                 ("mma_ok", ctypes.c_int32), ("n_measures", ctypes.c_int32),
-                ("pass_desc_bytes", ctypes.c_int32), ("gate_desc_bytes", ctypes.c_int32),
-                ("pad0", ctypes.c_int32), ("pad1", ctypes.c_int32),
+                ("pass_desc_bytes", ctypes.c_int32), ("group_desc_bytes", ctypes.c_int32),
+                ("gate_op_bytes", ctypes.c_int32), ("pad0", ctypes.c_int32),
                 ("n_passes", ctypes.c_int64), ("n_mma_passes", ctypes.c_int64),
-                ("n_gate_descs", ctypes.c_int64), ("n_matrices", ctypes.c_int64),
-                ("n_items", ctypes.c_int64),
+                ("n_groups", ctypes.c_int64), ("n_gate_ops", ctypes.c_int64),
+                ("n_matrices", ctypes.c_int64), ("n_items", ctypes.c_int64),
                 ("passes", ctypes.c_void_p), ("mma_passes", ctypes.c_void_p),
-                ("gates", ctypes.c_void_p), ("matrices", ctypes.c_void_p),
-                ("items", ctypes.c_void_p)]
+                ("groups", ctypes.c_void_p), ("gate_ops", ctypes.c_void_p),
+                ("matrices", ctypes.c_void_p), ("items", ctypes.c_void_p)]
 
 
 _P = ctypes.c_void_p

@@ -248,7 +248,8 @@ struct BlockedParams {
   int n;
   const PassDesc* passes;
   int pass_begin, pass_end;
-  const GateDesc* gates;
+  const GroupDesc* groups;
+  const GateOp* ops;
   const double2* mats;
   double* partials;  // 2 * gridDim
   double* record;    // p0 per assertion step
@@ -256,17 +257,14 @@ struct BlockedParams {
   double eps;
 };
 
-// ---- gate sweeps over a shared-memory tile --------------------------------
-// A 2q gate with tile-local XOR masks (ma, mb) acts on the quads
-// {v, v^ma, v^mb, v^ma^mb}; 1q gates on pairs {v, v^ma}.  Member s of a quad
-// (s = bit(slot0) + 2 bit(slot1), the reference's matrix index) is the one
-// whose logical slot bits spell s.  Batches live in shared memory under the
-// XOR swizzle swz (device.cuh), which is linear over XOR, so every address is
-// formed from swizzled per-bit offsets precomputed by the planner.
-
-__device__ __forceinline__ int ins0(int j, int pos) {
-  return ((j >> pos) << (pos + 1)) | (j & ((1 << pos) - 1));
-}
+// ---- octet sweeps over a shared-memory batch -------------------------------
+// A group (planner.h) is applied in one sweep: thread t loads the octet
+// {A_t ^ c0 m0 ^ c1 m1 ^ c2 m2} into x[c] (through the read map on the load
+// side), applies the group's gates in registers -- x's index c spells the
+// octet's logical axis bits, so every gate touches compile-time register
+// indices for its axis pattern -- and stores the octet.  Batches live in
+// shared memory under the XOR swizzle swz (device.cuh); all offsets are
+// swizzled per-bit values precomputed by the planner, combined by XOR.
 
 // (x, y) <- [[m0, m1], [m2, m3]] (x, y)
 __device__ __forceinline__ void mix2(double2& x, double2& y, const double2 m0, const double2 m1,
@@ -289,270 +287,228 @@ __device__ __forceinline__ double2 pick(const double2 x0, const double2 x1, cons
   return r;
 }
 
-// A sweep covers one batch (nb tiles of 2^k back to back).  Item j = t + T i
-// of thread t; the planner's per-bit tables (GateDesc.tcol / st*, tla / tlb /
-// spar) give the swizzled representative address and its logical parities as
-// XORs over the bits of t and i (see planner.h).  The out-of-tile parity of
-// each tile of the batch is a bit of gm.
-struct Sweep {
-  int n_iter;           // valid items per thread
-  bool active;          // this thread owns work (batches smaller than T items)
-  int bt, rbt;          // swizzled offset of the thread bits (store / load side)
-  int la_t, lb_t;       // logical parities of the thread bits
-  int st1, st2, st3, spar;
-  int rst1, rst2, rst3, rsa, rsb;  // load side: offsets through the read map
-  int tile_shift;       // item j lies in tile j >> tile_shift of the batch
-  unsigned gma, gmb;    // out-of-tile parities per tile of the batch
-  int sa, sb;
-};
+// 2q gate with slot 0 on axis P and slot 1 on axis Q (P < Q): two quads,
+// member s of quad h at register h | bit(s,0) << P | bit(s,1) << Q
+template <int P, int Q>
+__device__ __forceinline__ void gate2(double2 (&x)[8], const GateOp o,
+                                      const double2* __restrict__ m) {
+  constexpr int R = 3 - P - Q;
+  constexpr int A = 1 << P, B = 1 << Q, H = 1 << R;
+  switch (o.cls) {
+    case kCX01:  // swaps members 1, 3
+#pragma unroll
+      for (int h = 0; h <= H; h += H) {
+        const double2 t = x[h | A];
+        x[h | A] = x[h | A | B];
+        x[h | A | B] = t;
+      }
+      break;
+    case kCX10:  // swaps members 2, 3
+#pragma unroll
+      for (int h = 0; h <= H; h += H) {
+        const double2 t = x[h | B];
+        x[h | B] = x[h | A | B];
+        x[h | A | B] = t;
+      }
+      break;
+    case kSwap:  // swaps members 1, 2
+#pragma unroll
+      for (int h = 0; h <= H; h += H) {
+        const double2 t = x[h | A];
+        x[h | A] = x[h | B];
+        x[h | B] = t;
+      }
+      break;
+    case kPairQ: {  // blocks on members (0,2), (1,3)
+      const double2 m0 = m[0], m1 = m[1], m2 = m[2], m3 = m[3];
+      const double2 n0 = m[4], n1 = m[5], n2 = m[6], n3 = m[7];
+#pragma unroll
+      for (int h = 0; h <= H; h += H) {
+        mix2(x[h], x[h | B], m0, m1, m2, m3);
+        mix2(x[h | A], x[h | A | B], n0, n1, n2, n3);
+      }
+      break;
+    }
+    case kPairP: {  // blocks on members (0,1), (2,3)
+      const double2 m0 = m[0], m1 = m[1], m2 = m[2], m3 = m[3];
+      const double2 n0 = m[4], n1 = m[5], n2 = m[6], n3 = m[7];
+#pragma unroll
+      for (int h = 0; h <= H; h += H) {
+        mix2(x[h], x[h | A], m0, m1, m2, m3);
+        mix2(x[h | B], x[h | A | B], n0, n1, n2, n3);
+      }
+      break;
+    }
+    case kPairX: {  // blocks on members (0,3), (1,2)
+      const double2 m0 = m[0], m1 = m[1], m2 = m[2], m3 = m[3];
+      const double2 n0 = m[4], n1 = m[5], n2 = m[6], n3 = m[7];
+#pragma unroll
+      for (int h = 0; h <= H; h += H) {
+        mix2(x[h], x[h | A | B], m0, m1, m2, m3);
+        mix2(x[h | A], x[h | B], n0, n1, n2, n3);
+      }
+      break;
+    }
+    case kDiag2: {
+      const double2 d0 = m[0], d1 = m[1], d2 = m[2], d3 = m[3];
+#pragma unroll
+      for (int h = 0; h <= H; h += H) {
+        x[h] = cmul(d0, x[h]);
+        x[h | A] = cmul(d1, x[h | A]);
+        x[h | B] = cmul(d2, x[h | B]);
+        x[h | A | B] = cmul(d3, x[h | A | B]);
+      }
+      break;
+    }
+    case kMono2: {
+      const double2 v0 = m[0], v1 = m[1], v2 = m[2], v3 = m[3];
+      const int c0 = o.cols & 3, c1 = (o.cols >> 2) & 3, c2 = (o.cols >> 4) & 3,
+                c3 = (o.cols >> 6) & 3;
+#pragma unroll
+      for (int h = 0; h <= H; h += H) {
+        const double2 x0 = x[h], x1 = x[h | A], x2 = x[h | B], x3 = x[h | A | B];
+        x[h] = cmul(v0, pick(x0, x1, x2, x3, c0));
+        x[h | A] = cmul(v1, pick(x0, x1, x2, x3, c1));
+        x[h | B] = cmul(v2, pick(x0, x1, x2, x3, c2));
+        x[h | A | B] = cmul(v3, pick(x0, x1, x2, x3, c3));
+      }
+      break;
+    }
+    case kSparse2: {
+      const unsigned cols = o.cols;
+      double2 out[2][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const double2 ma = m[2 * r], mb = m[2 * r + 1];
+        const int ca = (cols >> (4 * r)) & 3, cb = (cols >> (4 * r + 2)) & 3;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int h = hh * H;
+          const double2 x0 = x[h], x1 = x[h | A], x2 = x[h | B], x3 = x[h | A | B];
+          double2 acc = make_double2(0.0, 0.0);
+          cmac(acc, ma, pick(x0, x1, x2, x3, ca));
+          cmac(acc, mb, pick(x0, x1, x2, x3, cb));
+          out[hh][r] = acc;
+        }
+      }
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int h = hh * H;
+        x[h] = out[hh][0];
+        x[h | A] = out[hh][1];
+        x[h | B] = out[hh][2];
+        x[h | A | B] = out[hh][3];
+      }
+      break;
+    }
+    default: {  // kDense2
+      double2 out[2][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const double2 w0 = m[4 * r], w1 = m[4 * r + 1], w2 = m[4 * r + 2], w3 = m[4 * r + 3];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int h = hh * H;
+          double2 acc = make_double2(0.0, 0.0);
+          cmac(acc, w0, x[h]);
+          cmac(acc, w1, x[h | A]);
+          cmac(acc, w2, x[h | B]);
+          cmac(acc, w3, x[h | A | B]);
+          out[hh][r] = acc;
+        }
+      }
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int h = hh * H;
+        x[h] = out[hh][0];
+        x[h | A] = out[hh][1];
+        x[h | B] = out[hh][2];
+        x[h | A | B] = out[hh][3];
+      }
+      break;
+    }
+  }
+}
 
-// Per pass, the thread part of every gate's item address is tabulated: entry
-// e of table 0 (table 1) is the XOR of the swizzled offsets of thread bits
-// 0..3 (4..7) set in e -- store side in bits 0..11 with the ra / rb parities
-// in bits 12 / 13, load side (through the read map) in bits 16..27.
-__device__ __forceinline__ uint32_t thread_table_entry(const GateDesc& d, int e) {
+// 1q gate on axis P: pairs (c, c | 1 << P)
+template <int P>
+__device__ __forceinline__ void gate1(double2 (&x)[8], const GateOp o,
+                                      const double2* __restrict__ m) {
+  constexpr int A = 1 << P;
+  constexpr int L0 = P == 0 ? 2 : 1, L1 = P == 2 ? 2 : 4;  // the other two axes
+  if (o.cls == kDiag1) {
+    const double2 d0 = m[0], d1 = m[1];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int c = ((i & 1) ? L0 : 0) | ((i & 2) ? L1 : 0);
+      x[c] = cmul(d0, x[c]);
+      x[c | A] = cmul(d1, x[c | A]);
+    }
+  } else {
+    const double2 m0 = m[0], m1 = m[1], m2 = m[2], m3 = m[3];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int c = ((i & 1) ? L0 : 0) | ((i & 2) ? L1 : 0);
+      mix2(x[c], x[c | A], m0, m1, m2, m3);
+    }
+  }
+}
+
+// Per pass, the thread part of every group's octet address is tabulated:
+// entry e of table 0 (table 1) is the XOR of the swizzled offsets of thread
+// bits 0..3 (4..7) set in e -- store side in bits 0..15, load side (through
+// the read map) in bits 16..31.
+__device__ __forceinline__ uint32_t thread_table_entry(const GroupDesc& d, int e) {
   const int half = e >> 4, bits = e & 15;
   uint32_t v = 0;
   for (int b = 0; b < 4; ++b)
     if (bits >> b & 1) {
       const int tb = 4 * half + b;
       v ^= d.tcol[tb];
-      v ^= ((d.tla >> tb) & 1u) << 12;
-      v ^= ((d.tlb >> tb) & 1u) << 13;
       v ^= static_cast<uint32_t>(d.rtcol[tb]) << 16;
     }
   return v;
 }
 
-__device__ __forceinline__ Sweep make_sweep(int k, int nb, const GateDesc& d, unsigned gm,
+// One octet sweep: src -> registers -> dst (different buffers).  `kap` holds
+// 3 parity bits per tile of the batch (the axes' out-of-tile rows).
+__device__ __forceinline__ void apply_group(const double2* __restrict__ src,
+                                            double2* __restrict__ dst, int k, int nvalid,
+                                            const GroupDesc& G, const GateOp* __restrict__ ops,
+                                            const double2* __restrict__ mats, unsigned kap,
                                             const uint32_t* ttab) {
-  Sweep w;
-  const int two = d.nq == 2;
-  const int lpt = k - 1 - two;  // log2 items per tile
-  const int items = nb << lpt;
   const int t = threadIdx.x;
-  w.active = t < items;
-  w.n_iter = items > kPassThreads ? items >> kThreadBits : 1;
-  w.tile_shift = lpt;
+  const int cb = k - 3;
+  if (t >= (nvalid << cb)) return;
   const uint32_t v = ttab[t & 15] ^ ttab[16 + (t >> 4)];
-  w.bt = v & 0xfffu;
-  w.rbt = v >> 16;
-  w.rst1 = d.rst1;
-  w.rst2 = d.rst2;
-  w.rst3 = d.rst3;
-  w.rsa = d.rsa;
-  w.rsb = d.rsb;
-  w.la_t = (v >> 12) & 1;
-  w.lb_t = (v >> 13) & 1;
-  w.st1 = d.st1;
-  w.st2 = d.st2;
-  w.st3 = d.st3;
-  w.spar = d.spar;
-  w.gma = gm & 15u;
-  w.gmb = gm >> 4;
-  w.sa = d.sa;
-  w.sb = d.sb;
-  return w;
-}
-
-// swizzled addresses of member 0 (logical slot bits zero) of item i of this
-// thread: store side in .x, load side (through the read map) in .y
-__device__ __forceinline__ int2 item_addr(const Sweep& w, int i, bool two) {
-  int a = w.bt, r = w.rbt, la = w.la_t, lb = w.lb_t;
-  if (i & 1) {
-    a ^= w.st1;
-    r ^= w.rst1;
-    la ^= w.spar & 1;
-    lb ^= (w.spar >> 1) & 1;
-  }
-  if (i & 2) {
-    a ^= w.st2;
-    r ^= w.rst2;
-    la ^= (w.spar >> 2) & 1;
-    lb ^= (w.spar >> 3) & 1;
-  }
-  if (i & 4) {
-    a ^= w.st3;
-    r ^= w.rst3;
-    la ^= (w.spar >> 4) & 1;
-    lb ^= (w.spar >> 5) & 1;
-  }
-  const int tile = (threadIdx.x + (i << kThreadBits)) >> w.tile_shift;
-  la ^= (w.gma >> tile) & 1;
-  lb = two ? lb ^ ((w.gmb >> tile) & 1) : 0;
-  return make_int2(a ^ (la ? w.sa : 0) ^ (lb ? w.sb : 0), r ^ (la ? w.rsa : 0) ^ (lb ? w.rsb : 0));
-}
-
-// f(load addresses l0..l3, store addresses s0..s3)
-template <class F>
-__device__ __forceinline__ void for_quads(const Sweep& w, F f) {
-  if (!w.active) return;
-#pragma unroll 4
-  for (int i = 0; i < w.n_iter; ++i) {
-    const int2 a = item_addr(w, i, true);
-    f(a.y, a.y ^ w.rsa, a.y ^ w.rsb, a.y ^ w.rsa ^ w.rsb, a.x, a.x ^ w.sa, a.x ^ w.sb,
-      a.x ^ w.sa ^ w.sb);
-  }
-}
-
-template <class F>
-__device__ __forceinline__ void for_pairs(const Sweep& w, F f) {
-  if (!w.active) return;
-#pragma unroll 4
-  for (int i = 0; i < w.n_iter; ++i) {
-    const int2 a = item_addr(w, i, false);
-    f(a.y, a.y ^ w.rsa, a.x, a.x ^ w.sa);
-  }
-}
-
-// Out of place: every gate reads `src` and writes all members to `dst`
-// (different buffers, both __restrict__), so the next item's loads never wait
-// on this item's stores -- in place, the compiler must keep each item's
-// load -> math -> store chain in order because the addresses may alias.
-__device__ __forceinline__ void apply_gate(const double2* __restrict__ src,
-                                           double2* __restrict__ dst, int k, int nb,
-                                           const GateDesc& d, const double2* __restrict__ m,
-                                           unsigned gm, const uint32_t* ttab) {
-  const Sweep w = make_sweep(k, nb, d, gm, ttab);
-  if (d.cls == kPermute) {  // pure read-map sweep
-    for_pairs(w, [&](int l0, int l1, int i0, int i1) {
-      const double2 x = src[l0], y = src[l1];
-      dst[i0] = x;
-      dst[i1] = y;
-    });
-    return;
-  }
-  if (d.nq == 1) {
-    if (d.cls == kDiag1) {
-      const double2 d0 = *(m), d1 = *(m + 1);
-      for_pairs(w, [&](int l0, int l1, int i0, int i1) {
-        dst[i0] = cmul(d0, src[l0]);
-        dst[i1] = cmul(d1, src[l1]);
-      });
-    } else {
-      const double2 m0 = *(m), m1 = *(m + 1), m2 = *(m + 2), m3 = *(m + 3);
-      for_pairs(w, [&](int l0, int l1, int i0, int i1) {
-        double2 x = src[l0], y = src[l1];
-        mix2(x, y, m0, m1, m2, m3);
-        dst[i0] = x;
-        dst[i1] = y;
-      });
-    }
-    return;
-  }
-  switch (d.cls) {
-    case kCX01:  // swaps members 1, 3
-      for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
-        const double2 x0 = src[l0], x1 = src[l1], x2 = src[l2], x3 = src[l3];
-        dst[i0] = x0;
-        dst[i1] = x3;
-        dst[i2] = x2;
-        dst[i3] = x1;
-      });
-      break;
-    case kCX10:  // swaps members 2, 3
-      for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
-        const double2 x0 = src[l0], x1 = src[l1], x2 = src[l2], x3 = src[l3];
-        dst[i0] = x0;
-        dst[i1] = x1;
-        dst[i2] = x3;
-        dst[i3] = x2;
-      });
-      break;
-    case kSwap:  // swaps members 1, 2
-      for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
-        const double2 x0 = src[l0], x1 = src[l1], x2 = src[l2], x3 = src[l3];
-        dst[i0] = x0;
-        dst[i1] = x2;
-        dst[i2] = x1;
-        dst[i3] = x3;
-      });
-      break;
-    case kPairQ:
-    case kPairP:
-    case kPairX: {
-      const double2 m0 = *(m), m1 = *(m + 1), m2 = *(m + 2), m3 = *(m + 3);
-      const double2 n0 = *(m + 4), n1 = *(m + 5), n2 = *(m + 6), n3 = *(m + 7);
-      // two 2x2 blocks: PairQ on members (0,2),(1,3); PairP (0,1),(2,3); PairX (0,3),(1,2)
-      auto blocks = [&](int la, int lb, int lc, int ld, int sa_, int sb_, int sc, int sd) {
-        double2 x = src[la], y = src[lb], z = src[lc], v = src[ld];
-        mix2(x, y, m0, m1, m2, m3);
-        mix2(z, v, n0, n1, n2, n3);
-        dst[sa_] = x;
-        dst[sb_] = y;
-        dst[sc] = z;
-        dst[sd] = v;
-      };
-      if (d.cls == kPairQ) {
-        for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
-          blocks(l0, l2, l1, l3, i0, i2, i1, i3);
-        });
-      } else if (d.cls == kPairP) {
-        for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
-          blocks(l0, l1, l2, l3, i0, i1, i2, i3);
-        });
-      } else {
-        for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
-          blocks(l0, l3, l1, l2, i0, i3, i1, i2);
-        });
-      }
-      break;
-    }
-    case kDiag2: {
-      const double2 d0 = *(m), d1 = *(m + 1), d2 = *(m + 2), d3 = *(m + 3);
-      for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
-        dst[i0] = cmul(d0, src[l0]);
-        dst[i1] = cmul(d1, src[l1]);
-        dst[i2] = cmul(d2, src[l2]);
-        dst[i3] = cmul(d3, src[l3]);
-      });
-      break;
-    }
-    case kMono2: {
-      const double2 v0 = *(m), v1 = *(m + 1), v2 = *(m + 2), v3 = *(m + 3);
-      const int c0 = d.cols & 3, c1 = (d.cols >> 2) & 3, c2 = (d.cols >> 4) & 3,
-                c3 = (d.cols >> 6) & 3;
-      for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
-        const double2 x0 = src[l0], x1 = src[l1], x2 = src[l2], x3 = src[l3];
-        dst[i0] = cmul(v0, pick(x0, x1, x2, x3, c0));
-        dst[i1] = cmul(v1, pick(x0, x1, x2, x3, c1));
-        dst[i2] = cmul(v2, pick(x0, x1, x2, x3, c2));
-        dst[i3] = cmul(v3, pick(x0, x1, x2, x3, c3));
-      });
-      break;
-    }
-    case kSparse2: {
-      const unsigned cols = d.cols;
-      for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
-        const double2 x0 = src[l0], x1 = src[l1], x2 = src[l2], x3 = src[l3];
-        const int idx[4] = {i0, i1, i2, i3};
+  int a = v & 0xffffu, r = v >> 16;
+  const unsigned kp = (kap >> (3 * (t >> cb))) & 7u;
+  const int m0 = G.am[0], m1 = G.am[1], m2 = G.am[2];
+  const int r0 = G.ram[0], r1 = G.ram[1], r2 = G.ram[2];
+  if (kp & 1) { a ^= m0; r ^= r0; }
+  if (kp & 2) { a ^= m1; r ^= r1; }
+  if (kp & 4) { a ^= m2; r ^= r2; }
+  double2 x[8];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          double2 o = make_double2(0.0, 0.0);
-          cmac(o, *(m + 2 * r), pick(x0, x1, x2, x3, (cols >> (4 * r)) & 3));
-          cmac(o, *(m + 2 * r + 1), pick(x0, x1, x2, x3, (cols >> (4 * r + 2)) & 3));
-          dst[idx[r]] = o;
-        }
-      });
-      break;
-    }
-    default: {  // kDense2
-      for_quads(w, [&](int l0, int l1, int l2, int l3, int i0, int i1, int i2, int i3) {
-        const double2 x0 = src[l0], x1 = src[l1], x2 = src[l2], x3 = src[l3];
-        const int idx[4] = {i0, i1, i2, i3};
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          double2 o = make_double2(0.0, 0.0);
-          cmac(o, *(m + 4 * r + 0), x0);
-          cmac(o, *(m + 4 * r + 1), x1);
-          cmac(o, *(m + 4 * r + 2), x2);
-          cmac(o, *(m + 4 * r + 3), x3);
-          dst[idx[r]] = o;
-        }
-      });
-      break;
+  for (int c = 0; c < 8; ++c)
+    x[c] = src[r ^ ((c & 1) ? r0 : 0) ^ ((c & 2) ? r1 : 0) ^ ((c & 4) ? r2 : 0)];
+  const int n_ops = G.n_ops;
+#pragma unroll 1
+  for (int i = 0; i < n_ops; ++i) {
+    const GateOp o = ops[i];
+    const double2* m = mats + o.mat;
+    switch (o.pat) {
+      case kPat01: gate2<0, 1>(x, o, m); break;
+      case kPat02: gate2<0, 2>(x, o, m); break;
+      case kPat12: gate2<1, 2>(x, o, m); break;
+      case kPat0: gate1<0>(x, o, m); break;
+      case kPat1: gate1<1>(x, o, m); break;
+      default: gate1<2>(x, o, m); break;
     }
   }
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    dst[a ^ ((c & 1) ? m0 : 0) ^ ((c & 2) ? m1 : 0) ^ ((c & 4) ? m2 : 0)] = x[c];
 }
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
@@ -568,18 +524,20 @@ __device__ __forceinline__ void cp_async_wait() {
 // One persistent CTA per SM; while the gate sweeps of tile i run, tile i+1 of
 // the same pass streams into the other shared-memory buffer with cp.async.
 constexpr size_t kBlockedSmemBytes = sizeof(double2) * (3 * kTileAmpsMax + kMaxPassMats) +
-                                     sizeof(GateDesc) * kMaxPassGates;
+                                     sizeof(GroupDesc) * kMaxPassGates +
+                                     sizeof(GateOp) * kMaxPassGates;
 
 __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
   // dynamic shared memory: 3 batch buffers (current, gate-sweep target,
-  // prefetch) | pass matrices | pass gate descriptors
+  // prefetch) | pass matrices | pass group descriptors | gate ops
   extern __shared__ __align__(128) double2 smem[];
   double2* s_mats = smem + 3 * kTileAmpsMax;
-  GateDesc* s_gates = reinterpret_cast<GateDesc*>(s_mats + kMaxPassMats);
+  GroupDesc* s_groups = reinterpret_cast<GroupDesc*>(s_mats + kMaxPassMats);
+  GateOp* s_ops = reinterpret_cast<GateOp*>(s_groups + kMaxPassGates);
   __shared__ PassDesc sp;
   __shared__ uint64_t s_hi[1 << (kTileQubitsMax - kThreadBits)];  // offsets of tile bits >= kThreadBits
-  __shared__ unsigned s_gm[kMaxPassGates];  // per gate: out-of-tile row parities of the batch tiles
-  __shared__ uint32_t s_ttab[kMaxPassGates][32];  // per gate: thread-address tables
+  __shared__ unsigned s_gm[kMaxPassGates];  // per group: out-of-tile axis parities per batch tile
+  __shared__ uint32_t s_ttab[kMaxPassGates][32];  // per group: thread-address tables
   __shared__ double red[32];
   __shared__ double s_p0;
   cg::grid_group grid = cg::this_grid();
@@ -592,19 +550,23 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
       reinterpret_cast<int*>(&sp)[tid] = reinterpret_cast<const int*>(p.passes + pi)[tid];
     __syncthreads();
     const int k = sp.k;
-    {  // stage the pass's gates and matrices (the previous pass is done with them)
+    {  // stage the pass's groups, ops and matrices (the previous pass is done with them)
       const int n_mat = sp.mat_count;
       for (int i = tid; i < n_mat; i += kPassThreads) s_mats[i] = p.mats[sp.mat_begin + i];
-      const int n_words = (sp.gate_end - sp.gate_begin) * int(sizeof(GateDesc) / 8);
-      const uint64_t* src = reinterpret_cast<const uint64_t*>(p.gates + sp.gate_begin);
-      uint64_t* dst = reinterpret_cast<uint64_t*>(s_gates);
+      const int n_words = (sp.group_end - sp.group_begin) * int(sizeof(GroupDesc) / 8);
+      const uint64_t* src = reinterpret_cast<const uint64_t*>(p.groups + sp.group_begin);
+      uint64_t* dst = reinterpret_cast<uint64_t*>(s_groups);
       for (int i = tid; i < n_words; i += kPassThreads) dst[i] = src[i];
+      const int n_ow = sp.op_end - sp.op_begin;
+      const uint64_t* osrc = reinterpret_cast<const uint64_t*>(p.ops + sp.op_begin);
+      uint64_t* odst = reinterpret_cast<uint64_t*>(s_ops);
+      for (int i = tid; i < n_ow; i += kPassThreads) odst[i] = osrc[i];
     }
     __syncthreads();
     {
-      const int n_entries = (sp.gate_end - sp.gate_begin) * 32;
+      const int n_entries = (sp.group_end - sp.group_begin) * 32;
       for (int e = tid; e < n_entries; e += kPassThreads)
-        s_ttab[e >> 5][e & 31] = thread_table_entry(s_gates[e >> 5], e & 31);
+        s_ttab[e >> 5][e & 31] = thread_table_entry(s_groups[e >> 5], e & 31);
     }
     constexpr int kHi = kTileQubitsMax - kThreadBits;
     if (tid < (1 << kHi)) {
@@ -623,7 +585,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
     const int n_j = k > kThreadBits ? 1 << (k - kThreadBits) : 1;
     const bool loader = tid < (1 << lo_bits);
     const double cscale = sp.collapse_q >= 0 ? 1.0 / sqrt(carry_p0) : 1.0;
-    const int n_gates = sp.gate_end - sp.gate_begin;
+    const int n_groups = sp.group_end - sp.group_begin;
     double msum = 0.0;
 
     auto tile_base = [&](uint64_t t) {  // physical index bits of tile t (no tile-local bits)
@@ -660,14 +622,14 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
       if (t0 + nb < t_end) issue_batch(t0 + nb, smem + pre * kTileAmpsMax);
       cp_async_commit();
       cp_async_wait<1>();  // this batch has landed (the next may be in flight)
-      if (tid < n_gates) {  // out-of-tile dual-row parities per (gate, tile of the batch)
-        const GateDesc& d = s_gates[tid];
+      if (tid < n_groups) {  // out-of-tile axis parities per (group, tile of the batch)
+        const GroupDesc& d = s_groups[tid];
         unsigned gm = 0;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           if (b < nvalid) {
-            gm |= (__popcll(tbase[b] & d.ra_out) & 1u) << b;
-            gm |= (__popcll(tbase[b] & d.rb_out) & 1u) << (4 + b);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) gm |= (__popcll(tbase[b] & d.r_out[i]) & 1u) << (3 * b + i);
           }
         }
         s_gm[tid] = gm;
@@ -692,10 +654,10 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
         __syncthreads();
       }
 #pragma unroll 1
-      for (int g = 0; g < n_gates; ++g) {
-        const GateDesc d = s_gates[g];
+      for (int g = 0; g < n_groups; ++g) {
+        const GroupDesc& d = s_groups[g];
         double2* out = smem + spare * kTileAmpsMax;
-        apply_gate(tile, out, k, nvalid, d, s_mats + d.mat, s_gm[g], s_ttab[g]);
+        apply_group(tile, out, k, nvalid, d, s_ops + d.op_begin, s_mats, s_gm[g], s_ttab[g]);
         const int tmp = cur;
         cur = spare;
         spare = tmp;
@@ -850,7 +812,8 @@ struct nsb_plan {
   nsb_ctx* ctx = nullptr;
   HostPlan host;
   DevBuf<PassDesc> passes, mma_passes;
-  DevBuf<GateDesc> gates;
+  DevBuf<GroupDesc> groups;
+  DevBuf<GateOp> ops;
   DevBuf<double2> mats, dense;
   DevBuf<double> record, partials;
   DevBuf<int> fail;
@@ -1036,7 +999,8 @@ void launch_blocked(nsb_ctx* c, nsb_plan* P, const PassDesc* passes, int pb, int
   bp.passes = passes;
   bp.pass_begin = pb;
   bp.pass_end = pe;
-  bp.gates = P->gates.ptr;
+  bp.groups = P->groups.ptr;
+  bp.ops = P->ops.ptr;
   bp.mats = P->mats.ptr;
   bp.partials = P->partials.ptr;
   bp.record = P->record.ptr;
@@ -1274,7 +1238,8 @@ int nsb_plan_create(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const double* 
     HostPlan& H = P->host;
     P->passes.upload(H.passes.data(), H.passes.size(), c->stream);
     P->mma_passes.upload(H.mma_passes.data(), H.mma_passes.size(), c->stream);
-    P->gates.upload(H.gates.data(), H.gates.size(), c->stream);
+    P->groups.upload(H.groups.data(), H.groups.size(), c->stream);
+    P->ops.upload(H.gate_ops.data(), H.gate_ops.size(), c->stream);
     P->mats.upload(reinterpret_cast<const double2*>(H.matrices.data()), H.matrices.size() / 2,
                    c->stream);
     P->dense.upload(reinterpret_cast<const double2*>(H.dense_mats.data()),

@@ -239,71 +239,193 @@ static int choose_tile_qubits(int n, int workers) {
   return kTileQubitsMax;
 }
 
-// pivots, free positions, swizzled per-bit offsets (plain and through the read
-// map R) and parity masks of one gate in tile-local coordinates (planner.h)
-void describe_gate(const PhysGate& g, uint64_t tset, int k, const uint32_t* rcol, GateDesc& d) {
-  const uint32_t ma = pext64(g.ma, tset), mb = pext64(g.mb, tset);
-  const uint32_t ra = pext64(g.ra, tset), rb = pext64(g.rb, tset);
-  d.ra_out = g.ra & ~tset;
-  d.rb_out = g.rb & ~tset;
-  // pivots: one bit of ma, and one of mb reduced against ma
-  const int pa = lowest_bit(ma);
-  int pbit = -1;
-  if (g.nq == 2) {
-    const uint32_t mr = (mb >> pa & 1) ? (mb ^ ma) : mb;
-    if (!mr) throw std::logic_error("degenerate gate masks");
-    pbit = lowest_bit(mr);
+// ---- octet groups (planner.h) ----------------------------------------------
+
+namespace {
+
+inline int parity32(uint32_t x) { return __builtin_popcount(x) & 1; }
+inline uint32_t swz11(uint32_t l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u); }
+
+// basis of {v in GF(2)^k : parity(f_i & v) = 0 for all i}
+std::vector<uint32_t> kernel_basis(const uint32_t* f, int nf, int k) {
+  uint32_t rows[8];
+  int piv[8], nr = 0;
+  for (int i = 0; i < nf; ++i) {  // reduced row echelon form
+    uint32_t r = f[i];
+    for (int j = 0; j < nr; ++j)
+      if (r >> piv[j] & 1) r ^= rows[j];
+    if (!r) continue;
+    const int p = __builtin_ctz(r);
+    for (int j = 0; j < nr; ++j)
+      if (rows[j] >> p & 1) rows[j] ^= r;
+    rows[nr] = r;
+    piv[nr++] = p;
   }
-  // free positions: tile-local non-pivot bits (first three with distinct
-  // residues mod 3 for conflict-free quarter-warps), then batch bits
-  std::vector<int> local, pos;
-  for (int p = 0; p < k; ++p)
-    if (p != pa && p != pbit) local.push_back(p);
-  for (int r = 0; r < 3; ++r)
-    for (size_t i = 0; i < local.size(); ++i)
-      if (local[i] >= 0 && local[i] % 3 == r) {
-        pos.push_back(local[i]);
-        local[i] = -1;
-        break;
+  std::vector<uint32_t> basis;
+  for (int c = 0; c < k; ++c) {
+    bool pivot = false;
+    for (int j = 0; j < nr; ++j) pivot |= piv[j] == c;
+    if (pivot) continue;
+    uint32_t v = 1u << c;
+    for (int j = 0; j < nr; ++j)
+      if (rows[j] >> c & 1) v |= 1u << piv[j];
+    basis.push_back(v);
+  }
+  return basis;
+}
+
+// Exchange the two slots of a packed 2q payload (engine.swap_conjugate):
+// an exact permutation of values and column codes (no arithmetic).
+void swap_packed_slots(uint8_t& cls, double* v, uint16_t& cols) {
+  static const int pi[4] = {0, 2, 1, 3};
+  double t[32];
+  switch (cls) {
+    case kDense2:
+      swap_slots(v);
+      break;
+    case kDiag2:
+      for (int i = 0; i < 2; ++i) std::swap(v[2 + i], v[4 + i]);
+      break;
+    case kMono2: {
+      std::memcpy(t, v, 8 * sizeof(double));
+      uint16_t c2 = 0;
+      for (int s = 0; s < 4; ++s) {
+        const int ns = pi[s];
+        v[2 * ns] = t[2 * s];
+        v[2 * ns + 1] = t[2 * s + 1];
+        c2 |= static_cast<uint16_t>(pi[(cols >> (2 * s)) & 3] << (2 * ns));
       }
-  for (int p : local)
-    if (p >= 0) pos.push_back(p);
-  for (int b = 0; b < 8; ++b) pos.push_back(k + b);  // tile-in-batch bits (+ padding)
-  auto sw = [](uint32_t l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u); };
-  d.sa = static_cast<uint16_t>(sw(ma));
-  d.sb = static_cast<uint16_t>(sw(mb));
-  d.tla = d.tlb = 0;
-  for (int b = 0; b < 8; ++b) {
-    const int p = pos[b];
-    d.tcol[b] = static_cast<uint16_t>(sw(1u << p));
-    if (p < k) {
-      d.tla |= static_cast<uint8_t>(((ra >> p) & 1) << b);
-      d.tlb |= static_cast<uint8_t>(((rb >> p) & 1) << b);
+      cols = c2;
+      break;
     }
+    case kSparse2: {
+      std::memcpy(t, v, 16 * sizeof(double));
+      uint16_t c2 = 0;
+      for (int s = 0; s < 4; ++s) {
+        const int ns = pi[s];
+        for (int j = 0; j < 2; ++j) {
+          v[2 * (2 * ns + j)] = t[2 * (2 * s + j)];
+          v[2 * (2 * ns + j) + 1] = t[2 * (2 * s + j) + 1];
+          c2 |= static_cast<uint16_t>(pi[(cols >> (2 * (2 * s + j))) & 3] << (2 * (2 * ns + j)));
+        }
+      }
+      cols = c2;
+      break;
+    }
+    case kCX01:
+      cls = kCX10;
+      break;
+    case kCX10:
+      cls = kCX01;
+      break;
+    case kPairQ:
+      cls = kPairP;
+      break;
+    case kPairP:
+      cls = kPairQ;
+      break;
+    case kPairX:  // second block acts on (2, 1) afterwards: reverse its entries
+      std::memcpy(t, v + 8, 8 * sizeof(double));
+      for (int e = 0; e < 4; ++e) {
+        v[8 + 2 * e] = t[2 * (3 - e)];
+        v[8 + 2 * e + 1] = t[2 * (3 - e) + 1];
+      }
+      break;
+    default:  // kSwap: symmetric
+      break;
   }
-  uint16_t* st[3] = {&d.st1, &d.st2, &d.st3};
-  d.spar = 0;
-  for (int i = 0; i < 3; ++i) {
-    const int p = pos[8 + i];
-    *st[i] = static_cast<uint16_t>(sw(1u << p));
-    if (p < k) {
-      d.spar |= static_cast<uint8_t>(((ra >> p) & 1) << (2 * i));
-      d.spar |= static_cast<uint8_t>(((rb >> p) & 1) << (2 * i + 1));
+}
+
+struct Axis {
+  uint32_t m = 0;     // tile-local physical mask
+  uint32_t rin = 0;   // tile-local part of the dual row
+  uint64_t rout = 0;  // out-of-tile part
+  bool operator==(const Axis& o) const { return m == o.m && rin == o.rin && rout == o.rout; }
+};
+
+struct OpenGroup {
+  int nax = 0;
+  Axis ax[3];
+  uint32_t rcol[16];       // read map of the group's loads
+  std::vector<GateOp> ops;
+  std::vector<double> mats;  // packed payloads of the ops (complex, back to back)
+};
+
+// axis slots of the gate's qubits in the group (adding axes if allowed);
+// false if the gate needs a fourth axis or clashes with the group's frame
+bool join_axes(OpenGroup& G, const Axis* ga, int nq, int* slot) {
+  Axis tmp[3];
+  int n = G.nax;
+  for (int i = 0; i < n; ++i) tmp[i] = G.ax[i];
+  for (int a = 0; a < nq; ++a) {
+    int found = -1;
+    for (int i = 0; i < n; ++i)
+      if (tmp[i] == ga[a]) found = i;
+    if (found < 0) {
+      for (int i = 0; i < n; ++i)
+        if (parity32(ga[a].rin & tmp[i].m) || parity32(tmp[i].rin & ga[a].m)) return false;
+      if (n == 3) return false;
+      tmp[n] = ga[a];
+      found = n++;
     }
+    slot[a] = found;
+  }
+  for (int i = 0; i < n; ++i) G.ax[i] = tmp[i];
+  G.nax = n;
+  return true;
+}
+
+void finish_group(OpenGroup& G, int k, GroupDesc& d) {
+  while (G.nax < 3) {  // pad with a free axis of the tile
+    uint32_t f[3];
+    for (int i = 0; i < G.nax; ++i) f[i] = G.ax[i].rin;
+    const std::vector<uint32_t> ker = kernel_basis(f, G.nax, k);
+    if (ker.empty()) throw std::logic_error("no free axis in the tile");
+    Axis a;
+    a.m = ker[0];
+    const int p = __builtin_ctz(a.m);
+    a.rin = 1u << p;
+    for (int j = 0; j < G.nax; ++j)
+      if (G.ax[j].m >> p & 1) a.rin ^= G.ax[j].rin;
+    G.ax[G.nax++] = a;
+  }
+  uint32_t f[3] = {G.ax[0].rin, G.ax[1].rin, G.ax[2].rin};
+  std::vector<uint32_t> C = kernel_basis(f, 3, k);
+  if (static_cast<int>(C.size()) != k - 3) throw std::logic_error("group axes are not dual");
+  // thread bits 0..2 first: basis vectors whose swizzled bank groups are independent
+  uint32_t phis[3];
+  int placed = 0;
+  for (size_t j = 0; j < C.size() && placed < 3; ++j) {
+    uint32_t ph = swz11(C[j]) & 7u;
+    for (int i = 0; i < placed; ++i)
+      if (ph >> __builtin_ctz(phis[i]) & 1) ph ^= phis[i];
+    if (!ph) continue;
+    for (int i = 0; i < placed; ++i)
+      if (phis[i] >> __builtin_ctz(ph) & 1) phis[i] ^= ph;
+    phis[placed] = ph;
+    std::swap(C[placed], C[j]);
+    ++placed;
   }
   auto rmap = [&](uint32_t u) {  // R u on tile-local bits; batch bits pass through
     uint32_t out = u & ~((1u << k) - 1);
     for (int i = 0; i < k; ++i)
-      if (u >> i & 1) out ^= rcol[i];
+      if (u >> i & 1) out ^= G.rcol[i];
     return out;
   };
-  d.rsa = static_cast<uint16_t>(sw(rmap(ma)));
-  d.rsb = static_cast<uint16_t>(sw(rmap(mb)));
-  for (int b = 0; b < 8; ++b) d.rtcol[b] = static_cast<uint16_t>(sw(rmap(1u << pos[b])));
-  d.rst1 = static_cast<uint16_t>(sw(rmap(1u << pos[8])));
-  d.rst2 = static_cast<uint16_t>(sw(rmap(1u << pos[9])));
-  d.rst3 = static_cast<uint16_t>(sw(rmap(1u << pos[10])));
+  for (int i = 0; i < 3; ++i) {
+    d.am[i] = static_cast<uint16_t>(swz11(G.ax[i].m));
+    d.ram[i] = static_cast<uint16_t>(swz11(rmap(G.ax[i].m)));
+    d.r_out[i] = G.ax[i].rout;
+  }
+  const int cb = k - 3;
+  for (int b = 0; b < 8; ++b) {
+    const uint32_t v = b < cb ? C[b] : (1u << (k + b - cb));  // then tile-in-batch bits
+    d.tcol[b] = static_cast<uint16_t>(swz11(v));
+    d.rtcol[b] = static_cast<uint16_t>(swz11(rmap(v)));
+  }
 }
+
+}  // namespace
 
 void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
                      const double* payloads, int n, int workers) {
@@ -484,8 +606,9 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
     if (popc(masks[i] | low) > k) throw std::logic_error("gate support exceeds the tile");
   }
   std::vector<uint64_t> sets;
-  auto pass_groups = pack_groups(masks, k, low, all, 2048, sets, &deps, &weights, kMaxPassGates,
-                                 kMaxPassMats);
+  // one group slot stays free for a trailing read-map sweep
+  auto pass_groups = pack_groups(masks, k, low, all, 2048, sets, &deps, &weights,
+                                 kMaxPassGates - 1, kMaxPassMats);
   for (size_t pi = 0; pi < pass_groups.size(); ++pi) {
     uint64_t tset = sets[pi];
     for (int q = 0; q < n && popc(tset) < k; ++q) tset |= uint64_t(1) << q;
@@ -500,29 +623,42 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
       else
         P.oq[o++] = static_cast<int8_t>(q);
     }
-    P.gate_begin = static_cast<int32_t>(gates.size());
+    P.group_begin = static_cast<int32_t>(groups.size());
+    P.op_begin = static_cast<int32_t>(gate_ops.size());
     P.mat_begin = static_cast<int32_t>(matrices.size() / 2);
     uint32_t rcol[16];  // pending read map R (tile-local columns), product of CXs
     for (int i = 0; i < 16; ++i) rcol[i] = 1u << i;
     bool r_identity = true;
-    auto emit = [&](const PhysGate& g) {
-      GateDesc d{};
-      d.mat = static_cast<int32_t>(matrices.size() / 2) - P.mat_begin;
-      matrices.insert(matrices.end(), packed_all.begin() + 2 * g.mat,
-                      packed_all.begin() + 2 * (g.mat + g.n_mat));
-      d.cls = g.cls;
-      d.nq = static_cast<uint8_t>(g.nq);
-      d.cols = g.cols;
-      describe_gate(g, tset, k, rcol, d);
-      gates.push_back(d);
+    OpenGroup G;
+    bool open = false;
+    auto close = [&]() {
+      if (!open) return;
+      GroupDesc d{};
+      d.op_begin = static_cast<uint8_t>(gate_ops.size() - P.op_begin);
+      d.n_ops = static_cast<uint8_t>(G.ops.size());
+      const int32_t mat0 = static_cast<int32_t>(matrices.size() / 2) - P.mat_begin;
+      for (GateOp op : G.ops) {
+        op.mat = static_cast<int16_t>(op.mat + mat0);
+        gate_ops.push_back(op);
+      }
+      matrices.insert(matrices.end(), G.mats.begin(), G.mats.end());
+      finish_group(G, k, d);
+      groups.push_back(d);
+      open = false;
+    };
+    auto start = [&]() {
+      G = OpenGroup();
+      std::memcpy(G.rcol, rcol, sizeof rcol);
       for (int i = 0; i < 16; ++i) rcol[i] = 1u << i;
       r_identity = true;
+      open = true;
     };
     for (int gi : pass_groups[pi]) {
       const PhysGate& g = run[gi];
       const bool perm = g.cls == kCX01 || g.cls == kCX10 || g.cls == kSwap;
       if (perm && popc(g.ma) == 1 && popc(g.mb) == 1) {
-        // fold into the read map: R <- R C  (R e_c ^= R e_t for CX(c -> t))
+        // fold into the read map of the next group: R <- R C
+        close();
         const int a = lowest_bit(pext64(g.ma, tset)), b = lowest_bit(pext64(g.mb, tset));
         if (g.cls == kCX01) {
           rcol[a] ^= rcol[b];
@@ -535,16 +671,48 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
         ++n_folded_gates;
         continue;
       }
-      emit(g);
+      Axis ga[2];
+      ga[0].m = pext64(g.ma, tset);
+      ga[0].rin = pext64(g.ra, tset);
+      ga[0].rout = g.ra & ~tset;
+      if (g.nq == 2) {
+        ga[1].m = pext64(g.mb, tset);
+        ga[1].rin = pext64(g.rb, tset);
+        ga[1].rout = g.rb & ~tset;
+      }
+      int slot[2] = {0, 0};
+      if (!open || !join_axes(G, ga, g.nq, slot)) {
+        close();
+        start();
+        if (!join_axes(G, ga, g.nq, slot)) throw std::logic_error("gate does not fit a group");
+      }
+      GateOp op{};
+      op.cls = g.cls;
+      op.cols = g.cols;
+      op.mat = static_cast<int16_t>(G.mats.size() / 2);
+      const size_t m0 = G.mats.size();
+      G.mats.insert(G.mats.end(), packed_all.begin() + 2 * g.mat,
+                    packed_all.begin() + 2 * (g.mat + g.n_mat));
+      if (g.nq == 1) {
+        op.pat = static_cast<uint8_t>(kPat0 + slot[0]);
+      } else {
+        if (slot[0] > slot[1]) {
+          swap_packed_slots(op.cls, G.mats.data() + m0, op.cols);
+          std::swap(slot[0], slot[1]);
+        }
+        op.pat = static_cast<uint8_t>(slot[0] == 0 ? (slot[1] == 1 ? kPat01 : kPat02) : kPat12);
+      }
+      G.ops.push_back(op);
+      ++n_ops;
     }
-    if (!r_identity) {  // trailing permutation: one identity sweep through R
-      PhysGate id{};
-      id.cls = kPermute;
-      id.nq = 1;
-      id.ma = id.ra = uint64_t(1) << P.tq[0];
-      emit(id);
+    close();
+    if (!r_identity) {  // trailing permutation: one sweep through R without gates
+      start();
+      close();
+      class_count[kPermute]++;
     }
-    P.gate_end = static_cast<int32_t>(gates.size());
+    P.group_end = static_cast<int32_t>(groups.size());
+    P.op_end = static_cast<int32_t>(gate_ops.size());
     P.mat_count = static_cast<int32_t>(matrices.size() / 2) - P.mat_begin;
     passes.push_back(P);
   }
@@ -562,7 +730,8 @@ void HostPlan::build_mma() {
     P.k = tile_qubits;
     P.measure_q = P.collapse_q = -1;
     P.measure_slot = P.collapse_slot = -1;
-    P.gate_begin = P.gate_end = 0;
+    P.group_begin = P.group_end = 0;
+    P.op_begin = P.op_end = 0;
     P.mat_begin = P.mat_count = 0;
     int t = 0, o = 0;
     for (int q = 0; q < n_qubits; ++q) {
@@ -631,7 +800,8 @@ void fill_info(const nsb::HostPlan& H, nsb_plan_info* info) {
   info->n_items = static_cast<int64_t>(H.items.size());
   info->n_frame_gates = H.n_frame_gates;
   info->n_flush_gates = H.n_flush_gates;
-  info->n_device_gates = static_cast<int64_t>(H.gates.size());
+  info->n_device_gates = H.n_ops;
+  info->n_sweeps = static_cast<int64_t>(H.groups.size());
 }
 }  // namespace
 
@@ -710,15 +880,18 @@ extern "C" int nsb_host_plan_view(const void* plan, nsb_plan_view* v) {
   v->mma_ok = H->mma_ok;
   v->n_measures = static_cast<int32_t>(H->n_measures);
   v->pass_desc_bytes = sizeof(nsb::PassDesc);
-  v->gate_desc_bytes = sizeof(nsb::GateDesc);
+  v->group_desc_bytes = sizeof(nsb::GroupDesc);
+  v->gate_op_bytes = sizeof(nsb::GateOp);
   v->n_passes = static_cast<int64_t>(H->passes.size());
   v->n_mma_passes = static_cast<int64_t>(H->mma_passes.size());
-  v->n_gate_descs = static_cast<int64_t>(H->gates.size());
+  v->n_groups = static_cast<int64_t>(H->groups.size());
+  v->n_gate_ops = static_cast<int64_t>(H->gate_ops.size());
   v->n_matrices = static_cast<int64_t>(H->matrices.size() / 2);
   v->n_items = static_cast<int64_t>(H->items.size());
   v->passes = H->passes.data();
   v->mma_passes = H->mma_passes.data();
-  v->gates = H->gates.data();
+  v->groups = H->groups.data();
+  v->gate_ops = H->gate_ops.data();
   v->matrices = H->matrices.data();
   v->items = H->items_flat.data();
   return NSB_OK;

@@ -14,9 +14,10 @@
 //  2. Passes.  The state is cut into 2^(n-k) tiles of 2^k amplitudes over a
 //     physical tile qubit set T (|T| = k <= kTileQubitsMax, always holding
 //     qubits 0..2 so global accesses are whole 128-byte lines).  A pass
-//     streams every tile through shared memory once and applies each of its
-//     gates as one shared-memory sweep (pairs / quads along the gate's
-//     tile-local XOR masks).  Global traffic is 32 B per amplitude per pass.
+//     streams every tile through shared memory once and applies its gates as
+//     octet sweeps (below): each sweep moves the tile through registers once
+//     and applies a group of up to three-axis gates there.  Global traffic is
+//     32 B per amplitude per pass.
 // Mid-circuit measurements end a pass: the pass epilogue writes per-CTA
 // partial sums of |a|^2 over the |0> half, the grid agrees on p0 after the
 // barrier, and the next pass's prologue applies the collapse.
@@ -57,56 +58,73 @@ enum GateClass : uint8_t {
 // zero is found with the dual rows ra, rb of M^-1 (logical bit a of physical
 // index p = parity(p & ra)).
 //
-// Work split: a sweep covers one batch (nb tiles stored back to back, batch
-// index = tile-local index | tile-in-batch << k).  Item j (a quad or a pair)
-// of the batch is j = t + T i (thread t, iteration i, T = kPassThreads); its
-// representative is the batch index whose bits at the pivot positions are
-// zero and whose other bits are j's bits, placed at the planner-chosen free
-// positions pos[0..].  pos[0..2] are picked with distinct residues mod 3, so
-// the 8 lanes of a quarter-warp hit 8 different 16-byte bank groups under
-// the shared-memory swizzle swz(l) = l ^ ((l>>3 ^ l>>6 ^ l>>9) & 7).  Because
-// swz, the placement and the parities are all linear over XOR, the planner
-// stores swizzled per-bit offsets and parity masks and the kernel only XORs.
+// Octet sweeps.  Consecutive gates of a pass that together touch at most
+// three logical axes (m_i, r_i) -- tile-local physical masks with their dual
+// rows, r_i(m_j) = delta_ij -- form a GROUP, executed as ONE shared-memory
+// sweep: every thread loads one octet {A ^ c0 m0 ^ c1 m1 ^ c2 m2} into eight
+// registers, applies all of the group's gates there (register index c = the
+// octet's logical bits, fixed at compile time per axis pattern) and stores
+// it back.  The octet bases A range over C = ker(r_0) ^ ker(r_1) ^ ker(r_2)
+// inside the tile, so the logical bits of an octet member never depend on A
+// -- only on the tile (out-of-tile parts of the rows, folded into A per tile
+// as the parity bits kappa).  Groups with fewer than three axes are padded
+// with a free tile axis.  The planner orders C's basis so the first three
+// thread bits hit different 16-byte bank groups under the shared-memory
+// swizzle swz(l) = l ^ ((l>>3 ^ l>>6 ^ l>>9) & 7); because swz and all maps
+// are linear over XOR, the planner stores swizzled per-bit offsets and the
+// kernel only XORs.
 //
 // Read maps: physical permutations (the CX gates that shrink the relabeling
-// frame) are not executed as sweeps of their own.  A gate that follows them in
-// a pass reads its members through their composition R (a linear map of
-// tile-local indices) and writes in place order, so the r* fields hold the
-// same offsets mapped through R (equal to the plain ones when R = I).
-struct GateDesc {     // 96 bytes
-  int32_t mat;        // offset (complex elements) in the pass's matrix block
-  uint8_t cls;        // GateClass
-  uint8_t nq;         // 1 or 2
-  uint8_t tla, tlb;   // thread bits whose position carries a ra / rb bit
-  uint16_t sa, sb;    // swizzled masks of slot 0 / slot 1
-  uint16_t st1, st2, st3;   // swizzled offsets of iteration bits 0, 1, 2
-  uint16_t cols;      // kSparse2 / kMono2: 2-bit column codes
-  uint8_t spar;       // ra / rb parities of iteration bits (la1 lb1 la2 lb2 la3 lb3)
-  uint8_t pad0[3];
-  uint16_t tcol[8];   // swizzled offsets of thread bits 0..7
-  uint16_t rsa, rsb, rst1, rst2, rst3;  // the same, read through R
-  uint16_t rtcol[8];
-  uint8_t pad1[14];
-  uint64_t ra_out, rb_out;  // out-of-tile parts of the dual rows (physical bits)
+// frame) are not executed as sweeps of their own.  The group that follows
+// them in a pass reads its octets through their composition R (a linear map
+// of tile-local indices) and writes in place order, so the r* fields hold
+// the same offsets mapped through R (equal to the plain ones when R = I).
+struct GroupDesc {        // 80 bytes
+  uint16_t am[3];         // swizzled axis masks (store side)
+  uint16_t ram[3];        // the same through the read map R (load side)
+  uint16_t tcol[8];       // swizzled offsets of thread bits 0..7 (store side)
+  uint16_t rtcol[8];      // load side
+  uint8_t op_begin;       // first GateOp (relative to the pass's op_begin)
+  uint8_t n_ops;          // 0: a pure read-map sweep
+  uint8_t pad[10];
+  uint64_t r_out[3];      // out-of-tile parts of the axes' dual rows
 };
-static_assert(sizeof(GateDesc) == 96, "GateDesc layout");
+static_assert(sizeof(GroupDesc) == 80, "GroupDesc layout");
 
-// Per pass the kernel stages the gate descriptors and the pass's own block
-// of packed matrices in shared memory (bounded by these limits).
-constexpr int kMaxPassGates = 40;
+// One gate of a group: class, axis pattern, payload.  Two-qubit gates are
+// stored with slot 0 on the lower axis (the planner exchanges the slots of
+// the payload when needed).
+enum AxisPattern : uint8_t {
+  kPat01 = 0, kPat02 = 1, kPat12 = 2,  // 2q: (slot0 axis, slot1 axis)
+  kPat0 = 3, kPat1 = 4, kPat2 = 5      // 1q: axis
+};
+struct GateOp {           // 8 bytes
+  int16_t mat;            // offset (complex elements) in the pass's matrix block
+  uint8_t cls;            // GateClass
+  uint8_t pat;            // AxisPattern
+  uint16_t cols;          // kSparse2 / kMono2: 2-bit column codes
+  uint16_t pad;
+};
+static_assert(sizeof(GateOp) == 8, "GateOp layout");
+
+// Per pass the kernel stages the group descriptors, gate ops and the pass's
+// own block of packed matrices in shared memory (bounded by these limits).
+constexpr int kMaxPassGates = 40;   // gate ops per pass (and groups per pass)
 constexpr int kMaxPassMats = 384;   // complex elements (6 KiB)
 
 struct PassDesc {         // 112 bytes
-  int32_t gate_begin, gate_end;
+  int32_t group_begin, group_end;
+  int32_t op_begin, op_end;
   int32_t mat_begin, mat_count;  // the pass's matrix block (complex elements)
   int32_t k;              // tile qubits used (<= kTileQubitsMax)
   int32_t measure_q;      // epilogue: partial P(q=0) sums (-1: none)
   int32_t measure_slot;   // index into the probability record
   int32_t collapse_q;     // prologue: collapse onto q=0 using the carried p0
   int32_t collapse_slot;
-  int32_t pad[3];
+  int32_t pad;
   int8_t tq[16];          // tile-local bit i -> physical qubit (ascending)
   int8_t oq[48];          // tile-index bit j -> physical qubit (ascending)
 };
+static_assert(sizeof(PassDesc) == 112, "PassDesc layout");
 
 }  // namespace nsb

@@ -71,13 +71,15 @@ struct HostPlan {
   int64_t n_flush_gates = 0;  // physical CX emitted to flush the frame
   int64_t n_frame_flushes = 0;  // flushes forced by a wide support
   int64_t n_folded_gates = 0;   // physical CXs folded into read maps
+  int64_t n_ops = 0;            // gate ops executed on the device (all groups)
   int64_t flops = 0;
   int64_t class_count[kNumClasses] = {};
 
   std::vector<Item> items;
   std::vector<PassDesc> passes;      // plain gate passes (items reference ranges)
   std::vector<PassDesc> mma_passes;  // whole-circuit MMA program
-  std::vector<GateDesc> gates;
+  std::vector<GroupDesc> groups;    // octet sweeps
+  std::vector<GateOp> gate_ops;     // their gates
   std::vector<double> matrices;      // packed payloads, one block per pass
   std::vector<double> packed_all;    // packed payloads of the current run
   std::vector<double> dense_mats;    // k-qubit / unblocked matrices (full)
@@ -93,6 +95,5 @@ struct HostPlan {
 };
 
 void plan_info(const HostPlan& H, nsb_plan_info* info);
-void describe_gate(const PhysGate& g, uint64_t tset, int k, const uint32_t* rcol, GateDesc& d);
 
 }  // namespace nsb

@@ -51,8 +51,7 @@ def test_ladders_through_the_frame(n, terms):
     c = ladder_circuit(rng, n, terms)
     for circ in (c, fuse_pipeline(c)[0]):
         plan = check(circ)
-        info_frame = int(np.sum(plan.gates["cls"] == PE.CX01))
-        assert info_frame >= 0
+        assert len(plan.groups) <= len(plan.ops) + len(plan.passes)
 
 
 @pytest.mark.parametrize("n,workers", [(14, 1), (14, 3), (14, 148), (15, 5), (16, 3)])
