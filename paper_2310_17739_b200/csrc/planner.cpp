@@ -17,6 +17,7 @@
 #include "../../include/nucsim_b200.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
 #include <unordered_map>
 
@@ -433,6 +434,8 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
   if (n < 1 || n > kMaxQubits) throw std::invalid_argument("qubit count out of range");
   const int k = choose_tile_qubits(n, workers);
   tile_qubits = k;
+  low_qubits = n <= kL2ResidentQubits ? 1 : kLowQubits;
+  if (const char* e = std::getenv("NSB_LOW_QUBITS")) low_qubits = std::atoi(e);  // tuning
   blocked = n >= 6;
   std::vector<PhysGate> run;
   uint64_t col[64];  // frame: physical mask of logical bit j (M e_j)
@@ -596,7 +599,7 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
 void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
   const int n = n_qubits;
   const uint64_t all = (n == 64) ? ~uint64_t(0) : ((uint64_t(1) << n) - 1);
-  const uint64_t low = (uint64_t(1) << std::min(kLowQubits, n)) - 1;
+  const uint64_t low = (uint64_t(1) << std::min(low_qubits, n)) - 1;
   std::vector<uint64_t> masks(run.size()), deps(run.size());
   std::vector<int> weights(run.size());
   for (size_t i = 0; i < run.size(); ++i) {

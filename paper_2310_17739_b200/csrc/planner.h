@@ -32,6 +32,10 @@ constexpr int kTileAmpsMax = 1 << kTileQubitsMax;
 constexpr int kThreadBits = 8;
 constexpr int kPassThreads = 1 << kThreadBits;  // 8 warps per CTA, two CTAs per SM
 constexpr int kLowQubits = 3;                    // always-tiled qubits 0..2 (128 B runs)
+// States up to this many qubits stay L2-resident inside a launch: their
+// tiles need not hold qubits 0..2 (sector efficiency matters less than the
+// extra free tile qubit slots, which cut the pass count by a third).
+constexpr int kL2ResidentQubits = 22;
 constexpr int kMaxQubits = 40;
 
 // Payload classes, chosen by exact-zero structure (skipping an exact zero

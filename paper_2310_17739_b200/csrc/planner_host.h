@@ -64,6 +64,7 @@ struct Item {
 struct HostPlan {
   int n_qubits = 0;
   int tile_qubits = 0;
+  int low_qubits = kLowQubits;  // qubits 0..low-1 are in every pass's tile
   bool blocked = false;   // blocked pass kernel (n >= 6); else per-op kernels
   bool mma_ok = false;    // whole MMA run fits one cooperative launch
   int64_t n_gates = 0, n_measures = 0;
