@@ -289,12 +289,12 @@ __device__ __forceinline__ double2 pick(const double2 x0, const double2 x1, cons
 
 // 2q gate with slot 0 on axis P and slot 1 on axis Q (P < Q): two quads,
 // member s of quad h at register h | bit(s,0) << P | bit(s,1) << Q
-template <int P, int Q>
+template <int P, int Q, int C>
 __device__ __forceinline__ void gate2(double2 (&x)[8], const GateOp o,
                                       const double2* __restrict__ m) {
   constexpr int R = 3 - P - Q;
   constexpr int A = 1 << P, B = 1 << Q, H = 1 << R;
-  switch (o.cls) {
+  switch (C) {
     case kCX01:  // swaps members 1, 3
 #pragma unroll
       for (int h = 0; h <= H; h += H) {
@@ -431,12 +431,12 @@ __device__ __forceinline__ void gate2(double2 (&x)[8], const GateOp o,
 }
 
 // 1q gate on axis P: pairs (c, c | 1 << P)
-template <int P>
-__device__ __forceinline__ void gate1(double2 (&x)[8], const GateOp o,
+template <int P, int C>
+__device__ __forceinline__ void gate1(double2 (&x)[8], const GateOp,
                                       const double2* __restrict__ m) {
   constexpr int A = 1 << P;
   constexpr int L0 = P == 0 ? 2 : 1, L1 = P == 2 ? 2 : 4;  // the other two axes
-  if (o.cls == kDiag1) {
+  if (C == kDiag1) {
     const double2 d0 = m[0], d1 = m[1];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -497,13 +497,30 @@ __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
   for (int i = 0; i < n_ops; ++i) {
     const GateOp o = ops[i];
     const double2* m = mats + o.mat;
-    switch (o.pat) {
-      case kPat01: gate2<0, 1>(x, o, m); break;
-      case kPat02: gate2<0, 2>(x, o, m); break;
-      case kPat12: gate2<1, 2>(x, o, m); break;
-      case kPat0: gate1<0>(x, o, m); break;
-      case kPat1: gate1<1>(x, o, m); break;
-      default: gate1<2>(x, o, m); break;
+    switch (o.kind) {  // pattern * 16 + class: one flat dispatch
+#define NSB_G2(P, Q, PAT)                                            \
+  case PAT * 16 + kDense2: gate2<P, Q, kDense2>(x, o, m); break;     \
+  case PAT * 16 + kSparse2: gate2<P, Q, kSparse2>(x, o, m); break;   \
+  case PAT * 16 + kMono2: gate2<P, Q, kMono2>(x, o, m); break;       \
+  case PAT * 16 + kDiag2: gate2<P, Q, kDiag2>(x, o, m); break;       \
+  case PAT * 16 + kCX01: gate2<P, Q, kCX01>(x, o, m); break;         \
+  case PAT * 16 + kCX10: gate2<P, Q, kCX10>(x, o, m); break;         \
+  case PAT * 16 + kPairQ: gate2<P, Q, kPairQ>(x, o, m); break;       \
+  case PAT * 16 + kPairP: gate2<P, Q, kPairP>(x, o, m); break;       \
+  case PAT * 16 + kPairX: gate2<P, Q, kPairX>(x, o, m); break;       \
+  case PAT * 16 + kSwap: gate2<P, Q, kSwap>(x, o, m); break;
+#define NSB_G1(P, PAT)                                               \
+  case PAT * 16 + kDense1: gate1<P, kDense1>(x, o, m); break;        \
+  case PAT * 16 + kDiag1: gate1<P, kDiag1>(x, o, m); break;
+      NSB_G2(0, 1, kPat01)
+      NSB_G2(0, 2, kPat02)
+      NSB_G2(1, 2, kPat12)
+      NSB_G1(0, kPat0)
+      NSB_G1(1, kPat1)
+      NSB_G1(2, kPat2)
+#undef NSB_G1
+#undef NSB_G2
+      default: break;
     }
   }
 #pragma unroll

@@ -656,25 +656,7 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
       r_identity = true;
       open = true;
     };
-    for (int gi : pass_groups[pi]) {
-      const PhysGate& g = run[gi];
-      const bool perm = g.cls == kCX01 || g.cls == kCX10 || g.cls == kSwap;
-      if (perm && popc(g.ma) == 1 && popc(g.mb) == 1) {
-        // fold into the read map of the next group: R <- R C
-        close();
-        const int a = lowest_bit(pext64(g.ma, tset)), b = lowest_bit(pext64(g.mb, tset));
-        if (g.cls == kCX01) {
-          rcol[a] ^= rcol[b];
-        } else if (g.cls == kCX10) {
-          rcol[b] ^= rcol[a];
-        } else {
-          std::swap(rcol[a], rcol[b]);
-        }
-        r_identity = false;
-        ++n_folded_gates;
-        continue;
-      }
-      Axis ga[2];
+    auto axes_of = [&](const PhysGate& g, Axis* ga) {
       ga[0].m = pext64(g.ma, tset);
       ga[0].rin = pext64(g.ra, tset);
       ga[0].rout = g.ra & ~tset;
@@ -683,12 +665,8 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
         ga[1].rin = pext64(g.rb, tset);
         ga[1].rout = g.rb & ~tset;
       }
-      int slot[2] = {0, 0};
-      if (!open || !join_axes(G, ga, g.nq, slot)) {
-        close();
-        start();
-        if (!join_axes(G, ga, g.nq, slot)) throw std::logic_error("gate does not fit a group");
-      }
+    };
+    auto add_op = [&](const PhysGate& g, int* slot) {
       GateOp op{};
       op.cls = g.cls;
       op.cols = g.cols;
@@ -705,9 +683,61 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
         }
         op.pat = static_cast<uint8_t>(slot[0] == 0 ? (slot[1] == 1 ? kPat01 : kPat02) : kPat12);
       }
+      op.kind = static_cast<uint8_t>(op.pat * 16 + op.cls);
       G.ops.push_back(op);
       ++n_ops;
+    };
+    // Gates between two folded permutations are grouped greedily with
+    // look-ahead: a gate may join the open group ahead of skipped gates it
+    // commutes with (disjoint physical supports and dual rows).
+    std::vector<int> seg;
+    auto flush_segment = [&]() {
+      std::vector<int> rest, still;
+      rest.swap(seg);
+      while (!rest.empty()) {
+        close();
+        start();
+        uint64_t blocked = 0;
+        still.clear();
+        for (int gi : rest) {
+          const PhysGate& g = run[gi];
+          const uint64_t dm = g.ma | g.mb | g.ra | g.rb;
+          Axis ga[2];
+          axes_of(g, ga);
+          int slot[2] = {0, 0};
+          if (!(dm & blocked) && join_axes(G, ga, g.nq, slot)) {
+            add_op(g, slot);
+          } else {
+            blocked |= dm;
+            still.push_back(gi);
+          }
+        }
+        if (G.ops.empty()) throw std::logic_error("grouping made no progress");
+        rest.swap(still);
+      }
+    };
+    for (int gi : pass_groups[pi]) {
+      const PhysGate& g = run[gi];
+      const bool perm = g.cls == kCX01 || g.cls == kCX10 || g.cls == kSwap;
+      if (perm && popc(g.ma) == 1 && popc(g.mb) == 1) {
+        // fold into the read map of the next group: R <- R C
+        flush_segment();
+        close();
+        const int a = lowest_bit(pext64(g.ma, tset)), b = lowest_bit(pext64(g.mb, tset));
+        if (g.cls == kCX01) {
+          rcol[a] ^= rcol[b];
+        } else if (g.cls == kCX10) {
+          rcol[b] ^= rcol[a];
+        } else {
+          std::swap(rcol[a], rcol[b]);
+        }
+        r_identity = false;
+        ++n_folded_gates;
+        continue;
+      }
+      seg.push_back(gi);
     }
+    flush_segment();
     close();
     if (!r_identity) {  // trailing permutation: one sweep through R without gates
       start();

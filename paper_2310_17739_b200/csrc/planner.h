@@ -107,7 +107,8 @@ struct GateOp {           // 8 bytes
   uint8_t cls;            // GateClass
   uint8_t pat;            // AxisPattern
   uint16_t cols;          // kSparse2 / kMono2: 2-bit column codes
-  uint16_t pad;
+  uint8_t kind;           // pat * 16 + cls (the kernel's dispatch key)
+  uint8_t pad;
 };
 static_assert(sizeof(GateOp) == 8, "GateOp layout");
 
