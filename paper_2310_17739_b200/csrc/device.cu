@@ -822,7 +822,10 @@ struct nsb_ctx {
   // sharded state (nsb_comm_init): this process holds rank `rank` of `nranks`
   void* comm = nullptr;  // ncclComm_t
   int rank = 0, nranks = 1;
-  DevBuf<double2> stage_send, stage_recv;
+  // qubit swaps: pack / unpack on `stream`, NCCL on `xfer`, double-buffered
+  cudaStream_t xfer = nullptr;
+  cudaEvent_t ev_packed[2] = {}, ev_moved[2] = {}, ev_unpacked[2] = {};
+  DevBuf<double2> stage_send[2], stage_recv[2];
 };
 
 struct nsb_plan {
@@ -1088,8 +1091,14 @@ void nsb_ctx_destroy(nsb_ctx* ctx) {
   if (ctx->comm) shard_comm_destroy(ctx);
   ctx->amps.release();
   ctx->scratch.release();
-  ctx->stage_send.release();
-  ctx->stage_recv.release();
+  for (int b = 0; b < 2; ++b) {
+    ctx->stage_send[b].release();
+    ctx->stage_recv[b].release();
+    if (ctx->ev_packed[b]) cudaEventDestroy(ctx->ev_packed[b]);
+    if (ctx->ev_moved[b]) cudaEventDestroy(ctx->ev_moved[b]);
+    if (ctx->ev_unpacked[b]) cudaEventDestroy(ctx->ev_unpacked[b]);
+  }
+  if (ctx->xfer) cudaStreamDestroy(ctx->xfer);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -1420,6 +1429,14 @@ int nsb_comm_init(nsb_ctx* c, const uint8_t* id, int32_t nranks, int32_t rank, n
     c->comm = comm;
     c->rank = rank;
     c->nranks = nranks;
+    if (!c->xfer) {
+      NSB_CUDA(cudaStreamCreateWithFlags(&c->xfer, cudaStreamNonBlocking));
+      for (int b = 0; b < 2; ++b) {
+        NSB_CUDA(cudaEventCreateWithFlags(&c->ev_packed[b], cudaEventDisableTiming));
+        NSB_CUDA(cudaEventCreateWithFlags(&c->ev_moved[b], cudaEventDisableTiming));
+        NSB_CUDA(cudaEventCreateWithFlags(&c->ev_unpacked[b], cudaEventDisableTiming));
+      }
+    }
   });
 }
 
@@ -1436,27 +1453,53 @@ int nsb_shard_swap(nsb_ctx* c, int32_t global_bit, int32_t local_q, int64_t chun
     const int v = 1 - ((c->rank >> global_bit) & 1);  // the half that changes owner
     const uint64_t half = c->n_amps >> 1;
     const uint64_t chunk =
-        std::min<uint64_t>(half, chunk_amps > 0 ? uint64_t(chunk_amps) : (uint64_t(1) << 26));
-    if (c->stage_send.count < chunk) {
-      c->stage_send.alloc(chunk);
-      c->stage_recv.alloc(chunk);
-    }
+        std::min<uint64_t>(half, chunk_amps > 0 ? uint64_t(chunk_amps) : (uint64_t(1) << 25));
+    // pack / unpack run beside NCCL's copy kernels: leave most SMs to them
+    const unsigned pgrid = static_cast<unsigned>(std::max(1, c->sm_count / 2));
+    for (int b = 0; b < 2; ++b)
+      if (c->stage_send[b].count < chunk) {
+        c->stage_send[b].alloc(chunk);
+        c->stage_recv[b].alloc(chunk);
+      }
     auto comm = static_cast<ncclComm_t>(c->comm);
-    for (uint64_t off = 0; off < half; off += chunk) {
-      const uint64_t cnt = std::min(chunk, half - off);
-      const unsigned grid = grid_for(cnt, 256, c);
-      dev::k_shard_pack<<<grid, 256, 0, c->stream>>>(c->amps.ptr, c->stage_send.ptr, off, cnt,
-                                                     local_q, v);
+    // Pipeline over chunks j: pack(j) and unpack(j) on the compute stream,
+    // the exchange of j on the transfer stream, so pack(j+1) and unpack(j-1)
+    // overlap the NVLink transfer of j.  Staging buffers alternate (j & 1).
+    const uint64_t n_chunks = (half + chunk - 1) / chunk;
+    auto count = [&](uint64_t j) { return std::min(chunk, half - j * chunk); };
+    auto pack = [&](uint64_t j) {
+      const int b = static_cast<int>(j & 1);
+      const uint64_t cnt = count(j);
+      dev::k_shard_pack<<<pgrid, 512, 0, c->stream>>>(c->amps.ptr, c->stage_send[b].ptr,
+                                                      j * chunk, cnt, local_q, v);
       NSB_CUDA(cudaGetLastError());
+      NSB_CUDA(cudaEventRecord(c->ev_packed[b], c->stream));
+    };
+    NSB_CUDA(cudaEventRecord(c->ev_unpacked[0], c->stream));  // buffers free
+    NSB_CUDA(cudaEventRecord(c->ev_unpacked[1], c->stream));
+    pack(0);
+    for (uint64_t j = 0; j < n_chunks; ++j) {
+      const int b = static_cast<int>(j & 1);
+      const uint64_t cnt = count(j);
+      NSB_CUDA(cudaStreamWaitEvent(c->xfer, c->ev_packed[b], 0));
+      NSB_CUDA(cudaStreamWaitEvent(c->xfer, c->ev_unpacked[b], 0));
       NSB_NCCL(api.group_start());
-      NSB_NCCL(api.send(c->stage_send.ptr, 2 * cnt, ncclFloat64, peer, comm, c->stream));
-      NSB_NCCL(api.recv(c->stage_recv.ptr, 2 * cnt, ncclFloat64, peer, comm, c->stream));
+      NSB_NCCL(api.send(c->stage_send[b].ptr, 2 * cnt, ncclFloat64, peer, comm, c->xfer));
+      NSB_NCCL(api.recv(c->stage_recv[b].ptr, 2 * cnt, ncclFloat64, peer, comm, c->xfer));
       NSB_NCCL(api.group_end());
-      dev::k_shard_unpack<<<grid, 256, 0, c->stream>>>(c->amps.ptr, c->stage_recv.ptr, off,
-                                                       cnt, local_q, v);
+      NSB_CUDA(cudaEventRecord(c->ev_moved[b], c->xfer));
+      if (j + 1 < n_chunks) {  // the send buffer of j+1 was last read by exchange j-1
+        NSB_CUDA(cudaStreamWaitEvent(c->stream, c->ev_moved[b ^ 1], 0));
+        pack(j + 1);
+      }
+      NSB_CUDA(cudaStreamWaitEvent(c->stream, c->ev_moved[b], 0));
+      dev::k_shard_unpack<<<pgrid, 512, 0, c->stream>>>(c->amps.ptr, c->stage_recv[b].ptr,
+                                                        j * chunk, cnt, local_q, v);
       NSB_CUDA(cudaGetLastError());
+      NSB_CUDA(cudaEventRecord(c->ev_unpacked[b], c->stream));
     }
     NSB_CUDA(cudaStreamSynchronize(c->stream));
+    NSB_CUDA(cudaStreamSynchronize(c->xfer));
   });
 }
 
