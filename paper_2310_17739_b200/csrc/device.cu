@@ -287,77 +287,73 @@ __device__ __forceinline__ double2 pick(const double2 x0, const double2 x1, cons
   return r;
 }
 
-// 2q gate with slot 0 on axis P and slot 1 on axis Q (P < Q): two quads,
-// member s of quad h at register h | bit(s,0) << P | bit(s,1) << Q
-template <int P, int Q, int C>
-__device__ __forceinline__ void gate2(double2 (&x)[8], const GateOp o,
+// 2q gate with slot 0 on axis P and slot 1 on axis Q (P < Q) on each of the
+// thread's NO octets: two quads per octet, member s of quad h at register
+// h | bit(s,0) << P | bit(s,1) << Q.  Matrix entries are read once per gate.
+template <int P, int Q, int C, int NO>
+__device__ __forceinline__ void gate2(double2 (&xs)[NO][8], const GateOp o,
                                       const double2* __restrict__ m) {
   constexpr int R = 3 - P - Q;
   constexpr int A = 1 << P, B = 1 << Q, H = 1 << R;
   switch (C) {
     case kCX01:  // swaps members 1, 3
 #pragma unroll
-      for (int h = 0; h <= H; h += H) {
-        const double2 t = x[h | A];
-        x[h | A] = x[h | A | B];
-        x[h | A | B] = t;
-      }
+      for (int q = 0; q < NO; ++q)
+#pragma unroll
+        for (int h = 0; h <= H; h += H) {
+          const double2 t = xs[q][h | A];
+          xs[q][h | A] = xs[q][h | A | B];
+          xs[q][h | A | B] = t;
+        }
       break;
     case kCX10:  // swaps members 2, 3
 #pragma unroll
-      for (int h = 0; h <= H; h += H) {
-        const double2 t = x[h | B];
-        x[h | B] = x[h | A | B];
-        x[h | A | B] = t;
-      }
+      for (int q = 0; q < NO; ++q)
+#pragma unroll
+        for (int h = 0; h <= H; h += H) {
+          const double2 t = xs[q][h | B];
+          xs[q][h | B] = xs[q][h | A | B];
+          xs[q][h | A | B] = t;
+        }
       break;
     case kSwap:  // swaps members 1, 2
 #pragma unroll
-      for (int h = 0; h <= H; h += H) {
-        const double2 t = x[h | A];
-        x[h | A] = x[h | B];
-        x[h | B] = t;
-      }
+      for (int q = 0; q < NO; ++q)
+#pragma unroll
+        for (int h = 0; h <= H; h += H) {
+          const double2 t = xs[q][h | A];
+          xs[q][h | A] = xs[q][h | B];
+          xs[q][h | B] = t;
+        }
       break;
-    case kPairQ: {  // blocks on members (0,2), (1,3)
+    case kPairQ:
+    case kPairP:
+    case kPairX: {  // blocks: Q (0,2),(1,3); P (0,1),(2,3); X (0,3),(1,2)
+      constexpr int u1 = C == kPairQ ? B : (C == kPairP ? A : A | B);
+      constexpr int u2 = C == kPairQ ? A : (C == kPairP ? B : A);
+      constexpr int u3 = C == kPairQ ? A | B : (C == kPairP ? A | B : B);
       const double2 m0 = m[0], m1 = m[1], m2 = m[2], m3 = m[3];
       const double2 n0 = m[4], n1 = m[5], n2 = m[6], n3 = m[7];
 #pragma unroll
-      for (int h = 0; h <= H; h += H) {
-        mix2(x[h], x[h | B], m0, m1, m2, m3);
-        mix2(x[h | A], x[h | A | B], n0, n1, n2, n3);
-      }
-      break;
-    }
-    case kPairP: {  // blocks on members (0,1), (2,3)
-      const double2 m0 = m[0], m1 = m[1], m2 = m[2], m3 = m[3];
-      const double2 n0 = m[4], n1 = m[5], n2 = m[6], n3 = m[7];
+      for (int q = 0; q < NO; ++q)
 #pragma unroll
-      for (int h = 0; h <= H; h += H) {
-        mix2(x[h], x[h | A], m0, m1, m2, m3);
-        mix2(x[h | B], x[h | A | B], n0, n1, n2, n3);
-      }
-      break;
-    }
-    case kPairX: {  // blocks on members (0,3), (1,2)
-      const double2 m0 = m[0], m1 = m[1], m2 = m[2], m3 = m[3];
-      const double2 n0 = m[4], n1 = m[5], n2 = m[6], n3 = m[7];
-#pragma unroll
-      for (int h = 0; h <= H; h += H) {
-        mix2(x[h], x[h | A | B], m0, m1, m2, m3);
-        mix2(x[h | A], x[h | B], n0, n1, n2, n3);
-      }
+        for (int h = 0; h <= H; h += H) {
+          mix2(xs[q][h], xs[q][h | u1], m0, m1, m2, m3);
+          mix2(xs[q][h | u2], xs[q][h | u3], n0, n1, n2, n3);
+        }
       break;
     }
     case kDiag2: {
       const double2 d0 = m[0], d1 = m[1], d2 = m[2], d3 = m[3];
 #pragma unroll
-      for (int h = 0; h <= H; h += H) {
-        x[h] = cmul(d0, x[h]);
-        x[h | A] = cmul(d1, x[h | A]);
-        x[h | B] = cmul(d2, x[h | B]);
-        x[h | A | B] = cmul(d3, x[h | A | B]);
-      }
+      for (int q = 0; q < NO; ++q)
+#pragma unroll
+        for (int h = 0; h <= H; h += H) {
+          xs[q][h] = cmul(d0, xs[q][h]);
+          xs[q][h | A] = cmul(d1, xs[q][h | A]);
+          xs[q][h | B] = cmul(d2, xs[q][h | B]);
+          xs[q][h | A | B] = cmul(d3, xs[q][h | A | B]);
+        }
       break;
     }
     case kMono2: {
@@ -365,92 +361,108 @@ __device__ __forceinline__ void gate2(double2 (&x)[8], const GateOp o,
       const int c0 = o.cols & 3, c1 = (o.cols >> 2) & 3, c2 = (o.cols >> 4) & 3,
                 c3 = (o.cols >> 6) & 3;
 #pragma unroll
-      for (int h = 0; h <= H; h += H) {
-        const double2 x0 = x[h], x1 = x[h | A], x2 = x[h | B], x3 = x[h | A | B];
-        x[h] = cmul(v0, pick(x0, x1, x2, x3, c0));
-        x[h | A] = cmul(v1, pick(x0, x1, x2, x3, c1));
-        x[h | B] = cmul(v2, pick(x0, x1, x2, x3, c2));
-        x[h | A | B] = cmul(v3, pick(x0, x1, x2, x3, c3));
-      }
+      for (int q = 0; q < NO; ++q)
+#pragma unroll
+        for (int h = 0; h <= H; h += H) {
+          const double2 x0 = xs[q][h], x1 = xs[q][h | A], x2 = xs[q][h | B],
+                        x3 = xs[q][h | A | B];
+          xs[q][h] = cmul(v0, pick(x0, x1, x2, x3, c0));
+          xs[q][h | A] = cmul(v1, pick(x0, x1, x2, x3, c1));
+          xs[q][h | B] = cmul(v2, pick(x0, x1, x2, x3, c2));
+          xs[q][h | A | B] = cmul(v3, pick(x0, x1, x2, x3, c3));
+        }
       break;
     }
     case kSparse2: {
       const unsigned cols = o.cols;
-      double2 out[2][4];
+      double2 out[NO][2][4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const double2 ma = m[2 * r], mb = m[2 * r + 1];
         const int ca = (cols >> (4 * r)) & 3, cb = (cols >> (4 * r + 2)) & 3;
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int h = hh * H;
-          const double2 x0 = x[h], x1 = x[h | A], x2 = x[h | B], x3 = x[h | A | B];
-          double2 acc = make_double2(0.0, 0.0);
-          cmac(acc, ma, pick(x0, x1, x2, x3, ca));
-          cmac(acc, mb, pick(x0, x1, x2, x3, cb));
-          out[hh][r] = acc;
-        }
+        for (int q = 0; q < NO; ++q)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int h = hh * H;
+            const double2 x0 = xs[q][h], x1 = xs[q][h | A], x2 = xs[q][h | B],
+                          x3 = xs[q][h | A | B];
+            double2 acc = make_double2(0.0, 0.0);
+            cmac(acc, ma, pick(x0, x1, x2, x3, ca));
+            cmac(acc, mb, pick(x0, x1, x2, x3, cb));
+            out[q][hh][r] = acc;
+          }
       }
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const int h = hh * H;
-        x[h] = out[hh][0];
-        x[h | A] = out[hh][1];
-        x[h | B] = out[hh][2];
-        x[h | A | B] = out[hh][3];
-      }
+      for (int q = 0; q < NO; ++q)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int h = hh * H;
+          xs[q][h] = out[q][hh][0];
+          xs[q][h | A] = out[q][hh][1];
+          xs[q][h | B] = out[q][hh][2];
+          xs[q][h | A | B] = out[q][hh][3];
+        }
       break;
     }
     default: {  // kDense2
-      double2 out[2][4];
+      double2 out[NO][2][4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const double2 w0 = m[4 * r], w1 = m[4 * r + 1], w2 = m[4 * r + 2], w3 = m[4 * r + 3];
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int h = hh * H;
-          double2 acc = make_double2(0.0, 0.0);
-          cmac(acc, w0, x[h]);
-          cmac(acc, w1, x[h | A]);
-          cmac(acc, w2, x[h | B]);
-          cmac(acc, w3, x[h | A | B]);
-          out[hh][r] = acc;
-        }
+        for (int q = 0; q < NO; ++q)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int h = hh * H;
+            double2 acc = make_double2(0.0, 0.0);
+            cmac(acc, w0, xs[q][h]);
+            cmac(acc, w1, xs[q][h | A]);
+            cmac(acc, w2, xs[q][h | B]);
+            cmac(acc, w3, xs[q][h | A | B]);
+            out[q][hh][r] = acc;
+          }
       }
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const int h = hh * H;
-        x[h] = out[hh][0];
-        x[h | A] = out[hh][1];
-        x[h | B] = out[hh][2];
-        x[h | A | B] = out[hh][3];
-      }
+      for (int q = 0; q < NO; ++q)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int h = hh * H;
+          xs[q][h] = out[q][hh][0];
+          xs[q][h | A] = out[q][hh][1];
+          xs[q][h | B] = out[q][hh][2];
+          xs[q][h | A | B] = out[q][hh][3];
+        }
       break;
     }
   }
 }
 
-// 1q gate on axis P: pairs (c, c | 1 << P)
-template <int P, int C>
-__device__ __forceinline__ void gate1(double2 (&x)[8], const GateOp,
+// 1q gate on axis P: pairs (c, c | 1 << P) of each octet
+template <int P, int C, int NO>
+__device__ __forceinline__ void gate1(double2 (&xs)[NO][8], const GateOp,
                                       const double2* __restrict__ m) {
   constexpr int A = 1 << P;
   constexpr int L0 = P == 0 ? 2 : 1, L1 = P == 2 ? 2 : 4;  // the other two axes
   if (C == kDiag1) {
     const double2 d0 = m[0], d1 = m[1];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int c = ((i & 1) ? L0 : 0) | ((i & 2) ? L1 : 0);
-      x[c] = cmul(d0, x[c]);
-      x[c | A] = cmul(d1, x[c | A]);
-    }
+    for (int q = 0; q < NO; ++q)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int c = ((i & 1) ? L0 : 0) | ((i & 2) ? L1 : 0);
+        xs[q][c] = cmul(d0, xs[q][c]);
+        xs[q][c | A] = cmul(d1, xs[q][c | A]);
+      }
   } else {
     const double2 m0 = m[0], m1 = m[1], m2 = m[2], m3 = m[3];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int c = ((i & 1) ? L0 : 0) | ((i & 2) ? L1 : 0);
-      mix2(x[c], x[c | A], m0, m1, m2, m3);
-    }
+    for (int q = 0; q < NO; ++q)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int c = ((i & 1) ? L0 : 0) | ((i & 2) ? L1 : 0);
+        mix2(xs[q][c], xs[q][c | A], m0, m1, m2, m3);
+      }
   }
 }
 
@@ -470,48 +482,63 @@ __device__ __forceinline__ uint32_t thread_table_entry(const GroupDesc& d, int e
   return v;
 }
 
-// One octet sweep: src -> registers -> dst (different buffers).  `kap` holds
-// 3 parity bits per tile of the batch (the axes' out-of-tile rows).
+// One octet sweep: src -> registers -> dst (different buffers).  Thread t
+// owns octets t + j T (j < kOctets, T = kPassThreads; octet-index bit
+// kThreadBits selects the second octet).  `kap` holds 3 parity bits per
+// tile of the batch (the axes' out-of-tile rows).
 __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
                                             double2* __restrict__ dst, int k, int nvalid,
                                             const GroupDesc& G, const GateOp* __restrict__ ops,
                                             const double2* __restrict__ mats, unsigned kap,
                                             const uint32_t* ttab) {
+  constexpr int NO = kOctets;
   const int t = threadIdx.x;
   const int cb = k - 3;
-  if (t >= (nvalid << cb)) return;
+  const int n_act = nvalid << cb;  // octets in the batch
+  if (t >= n_act) return;
   const uint32_t v = ttab[t & 15] ^ ttab[16 + (t >> 4)];
-  int a = v & 0xffffu, r = v >> 16;
-  const unsigned kp = (kap >> (3 * (t >> cb))) & 7u;
   const int m0 = G.am[0], m1 = G.am[1], m2 = G.am[2];
   const int r0 = G.ram[0], r1 = G.ram[1], r2 = G.ram[2];
-  if (kp & 1) { a ^= m0; r ^= r0; }
-  if (kp & 2) { a ^= m1; r ^= r1; }
-  if (kp & 4) { a ^= m2; r ^= r2; }
-  double2 x[8];
+  int a[NO], r[NO];
+  bool live[NO];
 #pragma unroll
-  for (int c = 0; c < 8; ++c)
-    x[c] = src[r ^ ((c & 1) ? r0 : 0) ^ ((c & 2) ? r1 : 0) ^ ((c & 4) ? r2 : 0)];
+  for (int q = 0; q < NO; ++q) {
+    const int oi = t + (q << kThreadBits);
+    live[q] = oi < n_act;
+    a[q] = (v & 0xffffu) ^ (q ? G.tcol[kThreadBits] : 0);
+    r[q] = (v >> 16) ^ (q ? G.rtcol[kThreadBits] : 0);
+    const unsigned kp = (kap >> (3 * (oi >> cb))) & 7u;
+    if (kp & 1) { a[q] ^= m0; r[q] ^= r0; }
+    if (kp & 2) { a[q] ^= m1; r[q] ^= r1; }
+    if (kp & 4) { a[q] ^= m2; r[q] ^= r2; }
+  }
+  double2 x[NO][8];
+#pragma unroll
+  for (int q = 0; q < NO; ++q)
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      x[q][c] = live[q] ? src[r[q] ^ ((c & 1) ? r0 : 0) ^ ((c & 2) ? r1 : 0) ^ ((c & 4) ? r2 : 0)]
+                        : make_double2(0.0, 0.0);
   const int n_ops = G.n_ops;
 #pragma unroll 1
   for (int i = 0; i < n_ops; ++i) {
     const GateOp o = ops[i];
     const double2* m = mats + o.mat;
     switch (o.kind) {  // pattern * 16 + class: one flat dispatch
-#define NSB_G2(P, Q, PAT)                                            \
-  case PAT * 16 + kDense2: gate2<P, Q, kDense2>(x, o, m); break;     \
-  case PAT * 16 + kSparse2: gate2<P, Q, kSparse2>(x, o, m); break;   \
-  case PAT * 16 + kMono2: gate2<P, Q, kMono2>(x, o, m); break;       \
-  case PAT * 16 + kDiag2: gate2<P, Q, kDiag2>(x, o, m); break;       \
-  case PAT * 16 + kCX01: gate2<P, Q, kCX01>(x, o, m); break;         \
-  case PAT * 16 + kCX10: gate2<P, Q, kCX10>(x, o, m); break;         \
-  case PAT * 16 + kPairQ: gate2<P, Q, kPairQ>(x, o, m); break;       \
-  case PAT * 16 + kPairP: gate2<P, Q, kPairP>(x, o, m); break;       \
-  case PAT * 16 + kPairX: gate2<P, Q, kPairX>(x, o, m); break;       \
-  case PAT * 16 + kSwap: gate2<P, Q, kSwap>(x, o, m); break;
-#define NSB_G1(P, PAT)                                               \
-  case PAT * 16 + kDense1: gate1<P, kDense1>(x, o, m); break;        \
-  case PAT * 16 + kDiag1: gate1<P, kDiag1>(x, o, m); break;
+#define NSB_G2(P, Q, PAT)                                                \
+  case PAT * 16 + kDense2: gate2<P, Q, kDense2, NO>(x, o, m); break;     \
+  case PAT * 16 + kSparse2: gate2<P, Q, kSparse2, NO>(x, o, m); break;   \
+  case PAT * 16 + kMono2: gate2<P, Q, kMono2, NO>(x, o, m); break;       \
+  case PAT * 16 + kDiag2: gate2<P, Q, kDiag2, NO>(x, o, m); break;       \
+  case PAT * 16 + kCX01: gate2<P, Q, kCX01, NO>(x, o, m); break;         \
+  case PAT * 16 + kCX10: gate2<P, Q, kCX10, NO>(x, o, m); break;         \
+  case PAT * 16 + kPairQ: gate2<P, Q, kPairQ, NO>(x, o, m); break;       \
+  case PAT * 16 + kPairP: gate2<P, Q, kPairP, NO>(x, o, m); break;       \
+  case PAT * 16 + kPairX: gate2<P, Q, kPairX, NO>(x, o, m); break;       \
+  case PAT * 16 + kSwap: gate2<P, Q, kSwap, NO>(x, o, m); break;
+#define NSB_G1(P, PAT)                                                   \
+  case PAT * 16 + kDense1: gate1<P, kDense1, NO>(x, o, m); break;        \
+  case PAT * 16 + kDiag1: gate1<P, kDiag1, NO>(x, o, m); break;
       NSB_G2(0, 1, kPat01)
       NSB_G2(0, 2, kPat02)
       NSB_G2(1, 2, kPat12)
@@ -524,8 +551,11 @@ __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
     }
   }
 #pragma unroll
-  for (int c = 0; c < 8; ++c)
-    dst[a ^ ((c & 1) ? m0 : 0) ^ ((c & 2) ? m1 : 0) ^ ((c & 4) ? m2 : 0)] = x[c];
+  for (int q = 0; q < NO; ++q)
+    if (live[q])
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        dst[a[q] ^ ((c & 1) ? m0 : 0) ^ ((c & 2) ? m1 : 0) ^ ((c & 4) ? m2 : 0)] = x[q][c];
 }
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {

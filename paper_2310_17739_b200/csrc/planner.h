@@ -29,8 +29,9 @@ namespace nsb {
 
 constexpr int kTileQubitsMax = 11;               // 2048 amplitudes = 32 KiB per buffer
 constexpr int kTileAmpsMax = 1 << kTileQubitsMax;
-constexpr int kThreadBits = 8;
-constexpr int kPassThreads = 1 << kThreadBits;  // 8 warps per CTA, two CTAs per SM
+constexpr int kThreadBits = 7;
+constexpr int kPassThreads = 1 << kThreadBits;  // 4 warps per CTA, two CTAs per SM
+constexpr int kOctets = 2;                       // octets per thread per sweep
 constexpr int kLowQubits = 3;                    // always-tiled qubits 0..2 (128 B runs)
 // States up to this many qubits stay L2-resident inside a launch: their
 // tiles need not hold qubits 0..2 (sector efficiency matters less than the

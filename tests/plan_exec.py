@@ -25,7 +25,7 @@ GROUP_DT = np.dtype([("am", "<u2", (3,)), ("ram", "<u2", (3,)), ("tcol", "<u2", 
                      ("rtcol", "<u2", (8,)), ("op_begin", "u1"), ("n_ops", "u1"),
                      ("pad", "u1", (10,)), ("r_out", "<u8", (3,))], align=True)
 OP_DT = np.dtype([("mat", "<i2"), ("cls", "u1"), ("pat", "u1"), ("cols", "<u2"), ("kind", "u1"), ("pad", "u1")])
-THREADS = 256  # kPassThreads
+THREADS = 128  # kPassThreads
 TILE_MAX = 11  # kTileQubitsMax
 (DENSE1, DIAG1, DENSE2, SPARSE2, MONO2, DIAG2, CX01, CX10, PAIRQ, PAIRP, PAIRX, SWAP,
  PERMUTE) = range(13)
