@@ -709,7 +709,10 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
         cur = spare;
         spare = tmp;
         tile = out;
-        __syncthreads();
+        if (d.sync)
+          __syncthreads();
+        else
+          __syncwarp();  // the next sweep reads only this warp's amplitudes
       }
       // shared -> global (+ assertion epilogue partial sums)
       if (loader) {

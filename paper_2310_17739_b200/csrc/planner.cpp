@@ -376,11 +376,32 @@ bool join_axes(OpenGroup& G, const Axis* ga, int nq, int* slot) {
   return true;
 }
 
-void finish_group(OpenGroup& G, int k, GroupDesc& d) {
-  while (G.nax < 3) {  // pad with a free axis of the tile
-    uint32_t f[3];
-    for (int i = 0; i < G.nax; ++i) f[i] = G.ax[i].rin;
-    const std::vector<uint32_t> ker = kernel_basis(f, G.nax, k);
+// Warp-local sweeps: with warp positions (p1, p2) a group whose axes avoid
+// both tile positions (and whose read map keeps them) can give warp w exactly
+// the amplitudes with (bit p1, bit p2) = w -- its octets never leave that set,
+// so consecutive warp-local sweeps need only __syncwarp.
+bool warp_local(const OpenGroup& G, int p1, int p2) {
+  const uint32_t wm = (1u << p1) | (1u << p2);
+  for (int i = 0; i < G.nax; ++i)
+    if (G.ax[i].m & wm) return false;
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t want = (i == p1 ? 1u << p1 : 0u) | (i == p2 ? 1u << p2 : 0u);
+    if ((G.rcol[i] & wm) != want) return false;
+  }
+  return true;
+}
+
+void finish_group(OpenGroup& G, int k, GroupDesc& d, int p1, int p2) {
+  const bool local = p1 >= 0;
+  while (G.nax < 3) {  // pad with a free axis of the tile (outside the warp positions)
+    uint32_t f[5];
+    int nf = 0;
+    for (int i = 0; i < G.nax; ++i) f[nf++] = G.ax[i].rin;
+    if (local) {
+      f[nf++] = 1u << p1;
+      f[nf++] = 1u << p2;
+    }
+    const std::vector<uint32_t> ker = kernel_basis(f, nf, k);
     if (ker.empty()) throw std::logic_error("no free axis in the tile");
     Axis a;
     a.m = ker[0];
@@ -390,9 +411,28 @@ void finish_group(OpenGroup& G, int k, GroupDesc& d) {
       if (G.ax[j].m >> p & 1) a.rin ^= G.ax[j].rin;
     G.ax[G.nax++] = a;
   }
-  uint32_t f[3] = {G.ax[0].rin, G.ax[1].rin, G.ax[2].rin};
+  uint32_t f[5] = {G.ax[0].rin, G.ax[1].rin, G.ax[2].rin, 0, 0};
   std::vector<uint32_t> C = kernel_basis(f, 3, k);
   if (static_cast<int>(C.size()) != k - 3) throw std::logic_error("group axes are not dual");
+  uint32_t c5 = 0, c6 = 0;
+  if (local) {  // octet-index bits 5, 6 (the warp bits) pick the warp's (p1, p2) coset
+    f[3] = 1u << p1;
+    f[4] = 1u << p2;
+    std::vector<uint32_t> K = kernel_basis(f, 5, k);
+    for (uint32_t v : C) {
+      const int w = (v >> p1 & 1) | ((v >> p2 & 1) << 1);
+      if (w == 1 && !c5) c5 = v;
+      if (w == 2 && !c6) c6 = v;
+    }
+    for (uint32_t v : C) {  // mixed vectors give the missing one
+      const int w = (v >> p1 & 1) | ((v >> p2 & 1) << 1);
+      if (w == 3 && !c5 && c6) c5 = v ^ c6;
+      if (w == 3 && !c6 && c5) c6 = v ^ c5;
+    }
+    if (!c5 || !c6 || static_cast<int>(K.size()) != k - 5)
+      throw std::logic_error("warp positions do not split the group");
+    C = K;
+  }
   // thread bits 0..2 first: basis vectors whose swizzled bank groups are independent
   uint32_t phis[3];
   int placed = 0;
@@ -406,6 +446,10 @@ void finish_group(OpenGroup& G, int k, GroupDesc& d) {
     phis[placed] = ph;
     std::swap(C[placed], C[j]);
     ++placed;
+  }
+  if (local) {
+    C.insert(C.begin() + 5, c6);
+    C.insert(C.begin() + 5, c5);
   }
   auto rmap = [&](uint32_t u) {  // R u on tile-local bits; batch bits pass through
     uint32_t out = u & ~((1u << k) - 1);
@@ -634,19 +678,10 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
     bool r_identity = true;
     OpenGroup G;
     bool open = false;
+    std::vector<OpenGroup> closed;  // the pass's groups, finalised at the end
     auto close = [&]() {
       if (!open) return;
-      GroupDesc d{};
-      d.op_begin = static_cast<uint8_t>(gate_ops.size() - P.op_begin);
-      d.n_ops = static_cast<uint8_t>(G.ops.size());
-      const int32_t mat0 = static_cast<int32_t>(matrices.size() / 2) - P.mat_begin;
-      for (GateOp op : G.ops) {
-        op.mat = static_cast<int16_t>(op.mat + mat0);
-        gate_ops.push_back(op);
-      }
-      matrices.insert(matrices.end(), G.mats.begin(), G.mats.end());
-      finish_group(G, k, d);
-      groups.push_back(d);
+      closed.push_back(G);
       open = false;
     };
     auto start = [&]() {
@@ -743,6 +778,43 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
       start();
       close();
       class_count[kPermute]++;
+    }
+    // warp positions: the pair of tile positions that lets the most
+    // consecutive sweeps run warp-locally (kThreadBits + 1 octet-index bits
+    // must be tile-local for the warp bits 5, 6 to be C vectors: k >= 10)
+    int w1 = -1, w2 = -1;
+    if (k >= 10 && kPassThreads == 128) {
+      int best = 0;
+      std::vector<char> loc(closed.size());
+      for (int p1 = 0; p1 < k; ++p1)
+        for (int p2 = p1 + 1; p2 < k; ++p2) {
+          for (size_t g = 0; g < closed.size(); ++g) loc[g] = warp_local(closed[g], p1, p2);
+          int score = 0;
+          for (size_t g = 0; g + 1 < closed.size(); ++g) score += loc[g] && loc[g + 1];
+          if (score > best) {
+            best = score;
+            w1 = p1;
+            w2 = p2;
+          }
+        }
+    }
+    for (size_t g = 0; g < closed.size(); ++g) {
+      OpenGroup& H = closed[g];
+      GroupDesc d{};
+      d.op_begin = static_cast<uint8_t>(gate_ops.size() - P.op_begin);
+      d.n_ops = static_cast<uint8_t>(H.ops.size());
+      const int32_t mat0 = static_cast<int32_t>(matrices.size() / 2) - P.mat_begin;
+      for (GateOp op : H.ops) {
+        op.mat = static_cast<int16_t>(op.mat + mat0);
+        gate_ops.push_back(op);
+      }
+      matrices.insert(matrices.end(), H.mats.begin(), H.mats.end());
+      const bool here = w1 >= 0 && warp_local(H, w1, w2);
+      const bool next = g + 1 < closed.size() && w1 >= 0 && warp_local(closed[g + 1], w1, w2);
+      finish_group(H, k, d, here ? w1 : -1, here ? w2 : -1);
+      d.sync = (here && next) ? 0 : 1;
+      if (!d.sync) ++n_warp_syncs;
+      groups.push_back(d);
     }
     P.group_end = static_cast<int32_t>(groups.size());
     P.op_end = static_cast<int32_t>(gate_ops.size());

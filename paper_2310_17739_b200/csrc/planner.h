@@ -91,7 +91,8 @@ struct GroupDesc {        // 80 bytes
   uint16_t rtcol[8];      // load side
   uint8_t op_begin;       // first GateOp (relative to the pass's op_begin)
   uint8_t n_ops;          // 0: a pure read-map sweep
-  uint8_t pad[10];
+  uint8_t sync;           // 1: CTA barrier after this sweep; 0: warp-local, __syncwarp
+  uint8_t pad[9];
   uint64_t r_out[3];      // out-of-tile parts of the axes' dual rows
 };
 static_assert(sizeof(GroupDesc) == 80, "GroupDesc layout");

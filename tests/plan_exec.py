@@ -23,7 +23,7 @@ PASS_DT = np.dtype([("group_begin", "<i4"), ("group_end", "<i4"), ("op_begin", "
                     ("oq", "i1", (48,))])
 GROUP_DT = np.dtype([("am", "<u2", (3,)), ("ram", "<u2", (3,)), ("tcol", "<u2", (8,)),
                      ("rtcol", "<u2", (8,)), ("op_begin", "u1"), ("n_ops", "u1"),
-                     ("pad", "u1", (10,)), ("r_out", "<u8", (3,))], align=True)
+                     ("sync", "u1"), ("pad", "u1", (9,)), ("r_out", "<u8", (3,))], align=True)
 OP_DT = np.dtype([("mat", "<i2"), ("cls", "u1"), ("pat", "u1"), ("cols", "<u2"), ("kind", "u1"), ("pad", "u1")])
 THREADS = 128  # kPassThreads
 TILE_MAX = 11  # kTileQubitsMax
@@ -161,12 +161,16 @@ def _apply_group(B, G, ops, mats, tbases, k, nvalid):
     assert len(np.unique(np.concatenate(st))) == 8 * n_act  # octets partition the batch
     assert len(np.unique(np.concatenate(ld))) == 8 * n_act
     S = B.copy()  # out of place: loads see the pre-sweep batch
+    warp = (t >> 5) & 3  # octet index bits 5, 6 (kThreadBits = 7 threads per CTA)
+    loads = [np.sort(np.concatenate([U(l)[warp == w] for l in ld])) for w in range(4)]
+    stores = [np.sort(np.concatenate([U(s_)[warp == w] for s_ in st])) for w in range(4)]
     x = [S[U(l)] for l in ld]
     o0 = int(G["op_begin"])
     for op in ops[o0:o0 + int(G["n_ops"])]:
         _gate(x, op, mats[int(op["mat"]):])
     for s, v in zip(st, x):
         B[U(s)] = v
+    return loads, stores
 
 
 def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12, workers=148):
@@ -196,8 +200,13 @@ def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12, workers=1
                 B = state[idx]
                 if cq >= 0:
                     B = np.where((idx >> cq) & 1, 0.0, B * (1.0 / np.sqrt(carry_p0)))
+                prev = None
                 for G in groups:
-                    _apply_group(B, G, pops, block, tbs, k, nvalid)
+                    loads, stores = _apply_group(B, G, pops, block, tbs, k, nvalid)
+                    if prev is not None:  # __syncwarp only: each warp reads its own writes
+                        for w in range(4):
+                            assert np.array_equal(loads[w], prev[w])
+                    prev = stores if int(G["sync"]) == 0 else None
                 state[idx] = B
         mq = int(P["measure_q"])
         if mq >= 0:
