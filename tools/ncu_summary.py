@@ -2,6 +2,7 @@
 metrics of one --set full capture.  Usage:
     python tools/ncu_summary.py launches gpurun_out/launches.csv
     python tools/ncu_summary.py full gpurun_out/prof_full.ncu-rep
+    python tools/ncu_summary.py dram gpurun_out  > profiles/r01_dram_bytes.json
 """
 import csv
 import io
@@ -79,5 +80,27 @@ def full(path):
         print(f"| {h} | {100 * s / tot:.1f} % |")
 
 
+def dram(folder):
+    """JSON {config: DRAM bytes (read + write) of one k_blocked launch}."""
+    import json
+    import pathlib
+    out = {}
+    for f in sorted(pathlib.Path(folder).glob("dram_*.csv")):
+        rows = list(csv.reader(open(f)))
+        try:
+            start = next(i for i, r in enumerate(rows) if "Metric Name" in r)
+        except StopIteration:
+            continue
+        hdr = rows[start]
+        iname, ival, iunit = hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+        tot = 0.0
+        for r in rows[start + 1:]:
+            if len(r) > ival and r[iname].startswith("dram__bytes"):
+                tot += float(r[ival].replace(",", "")) * scale.get(r[iunit], 1)
+        out[f.stem[len("dram_"):]] = int(tot)
+    print(json.dumps(out))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "full": full, "dram": dram}[sys.argv[1]](sys.argv[2])
