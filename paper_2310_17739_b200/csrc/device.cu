@@ -520,42 +520,58 @@ __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
       x[q][c] = live[q] ? src[r[q] ^ ((c & 1) ? r0 : 0) ^ ((c & 2) ? r1 : 0) ^ ((c & 4) ? r2 : 0)]
                         : make_double2(0.0, 0.0);
   const int n_ops = G.n_ops;
-#pragma unroll 1
-  for (int i = 0; i < n_ops; ++i) {
-    const GateOp o = ops[i];
+  auto store = [&]() {
+#pragma unroll
+    for (int q = 0; q < NO; ++q)
+      if (live[q])
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          dst[a[q] ^ ((c & 1) ? m0 : 0) ^ ((c & 2) ? m1 : 0) ^ ((c & 4) ? m2 : 0)] = x[q][c];
+  };
+  // Gate dispatch: pattern * 16 + class selects straight-line register code.
+  // The LAST gate of a group stores its octets from inside its own case, so
+  // the common one-gate group never merges the 64-register octet pair across
+  // the dispatch (the merge costs the allocator a full copy).
+  auto dispatch = [&](const GateOp o, bool last) {
     const double2* m = mats + o.mat;
-    switch (o.kind) {  // pattern * 16 + class: one flat dispatch
-#define NSB_G2(P, Q, PAT)                                                \
-  case PAT * 16 + kDense2: gate2<P, Q, kDense2, NO>(x, o, m); break;     \
-  case PAT * 16 + kSparse2: gate2<P, Q, kSparse2, NO>(x, o, m); break;   \
-  case PAT * 16 + kMono2: gate2<P, Q, kMono2, NO>(x, o, m); break;       \
-  case PAT * 16 + kDiag2: gate2<P, Q, kDiag2, NO>(x, o, m); break;       \
-  case PAT * 16 + kCX01: gate2<P, Q, kCX01, NO>(x, o, m); break;         \
-  case PAT * 16 + kCX10: gate2<P, Q, kCX10, NO>(x, o, m); break;         \
-  case PAT * 16 + kPairQ: gate2<P, Q, kPairQ, NO>(x, o, m); break;       \
-  case PAT * 16 + kPairP: gate2<P, Q, kPairP, NO>(x, o, m); break;       \
-  case PAT * 16 + kPairX: gate2<P, Q, kPairX, NO>(x, o, m); break;       \
-  case PAT * 16 + kSwap: gate2<P, Q, kSwap, NO>(x, o, m); break;
-#define NSB_G1(P, PAT)                                                   \
-  case PAT * 16 + kDense1: gate1<P, kDense1, NO>(x, o, m); break;        \
-  case PAT * 16 + kDiag1: gate1<P, kDiag1, NO>(x, o, m); break;
-      NSB_G2(0, 1, kPat01)
-      NSB_G2(0, 2, kPat02)
-      NSB_G2(1, 2, kPat12)
-      NSB_G1(0, kPat0)
-      NSB_G1(1, kPat1)
-      NSB_G1(2, kPat2)
+    switch (o.kind) {
+#define NSB_G2(P, Q, PAT, C)                                             \
+  case PAT * 16 + C:                                                     \
+    gate2<P, Q, C, NO>(x, o, m);                                         \
+    if (last) store();                                                   \
+    break;
+#define NSB_G2ALL(P, Q, PAT)                                             \
+  NSB_G2(P, Q, PAT, kDense2) NSB_G2(P, Q, PAT, kSparse2)                 \
+  NSB_G2(P, Q, PAT, kMono2) NSB_G2(P, Q, PAT, kDiag2)                    \
+  NSB_G2(P, Q, PAT, kCX01) NSB_G2(P, Q, PAT, kCX10)                      \
+  NSB_G2(P, Q, PAT, kPairQ) NSB_G2(P, Q, PAT, kPairP)                    \
+  NSB_G2(P, Q, PAT, kPairX) NSB_G2(P, Q, PAT, kSwap)
+#define NSB_G1(P, PAT, C)                                                \
+  case PAT * 16 + C:                                                     \
+    gate1<P, C, NO>(x, o, m);                                            \
+    if (last) store();                                                   \
+    break;
+      NSB_G2ALL(0, 1, kPat01)
+      NSB_G2ALL(0, 2, kPat02)
+      NSB_G2ALL(1, 2, kPat12)
+      NSB_G1(0, kPat0, kDense1) NSB_G1(0, kPat0, kDiag1)
+      NSB_G1(1, kPat1, kDense1) NSB_G1(1, kPat1, kDiag1)
+      NSB_G1(2, kPat2, kDense1) NSB_G1(2, kPat2, kDiag1)
 #undef NSB_G1
+#undef NSB_G2ALL
 #undef NSB_G2
-      default: break;
+      default:
+        if (last) store();
+        break;
     }
+  };
+  if (n_ops == 0) {
+    store();
+    return;
   }
-#pragma unroll
-  for (int q = 0; q < NO; ++q)
-    if (live[q])
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        dst[a[q] ^ ((c & 1) ? m0 : 0) ^ ((c & 2) ? m1 : 0) ^ ((c & 4) ? m2 : 0)] = x[q][c];
+#pragma unroll 1
+  for (int i = 0; i + 1 < n_ops; ++i) dispatch(ops[i], false);
+  dispatch(ops[n_ops - 1], true);
 }
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
