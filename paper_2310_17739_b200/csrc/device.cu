@@ -607,37 +607,40 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
   const int tid = threadIdx.x;
   double carry_p0 = 1.0;  // p0 of the previous pass's assertion (collapse input)
 
-  for (int pi = p.pass_begin; pi < p.pass_end; ++pi) {
-    __syncthreads();
+  // Stage pass pi's descriptors in shared memory.  Called for the next pass
+  // right before the grid barrier, so the copy overlaps the wait.
+  auto stage = [&](int pi) {
+    __syncthreads();  // the previous pass is done with sp and the tables
     if (tid < int(sizeof(PassDesc) / sizeof(int)))
       reinterpret_cast<int*>(&sp)[tid] = reinterpret_cast<const int*>(p.passes + pi)[tid];
     __syncthreads();
-    const int k = sp.k;
-    {  // stage the pass's groups, ops and matrices (the previous pass is done with them)
-      const int n_mat = sp.mat_count;
-      for (int i = tid; i < n_mat; i += kPassThreads) s_mats[i] = p.mats[sp.mat_begin + i];
-      const int n_words = (sp.group_end - sp.group_begin) * int(sizeof(GroupDesc) / 8);
-      const uint64_t* src = reinterpret_cast<const uint64_t*>(p.groups + sp.group_begin);
-      uint64_t* dst = reinterpret_cast<uint64_t*>(s_groups);
-      for (int i = tid; i < n_words; i += kPassThreads) dst[i] = src[i];
-      const int n_ow = sp.op_end - sp.op_begin;
-      const uint64_t* osrc = reinterpret_cast<const uint64_t*>(p.ops + sp.op_begin);
-      uint64_t* odst = reinterpret_cast<uint64_t*>(s_ops);
-      for (int i = tid; i < n_ow; i += kPassThreads) odst[i] = osrc[i];
-    }
+    const int n_mat = sp.mat_count;
+    for (int i = tid; i < n_mat; i += kPassThreads) s_mats[i] = p.mats[sp.mat_begin + i];
+    const int n_words = (sp.group_end - sp.group_begin) * int(sizeof(GroupDesc) / 8);
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(p.groups + sp.group_begin);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(s_groups);
+    for (int i = tid; i < n_words; i += kPassThreads) dst[i] = src[i];
+    const int n_ow = sp.op_end - sp.op_begin;
+    const uint64_t* osrc = reinterpret_cast<const uint64_t*>(p.ops + sp.op_begin);
+    uint64_t* odst = reinterpret_cast<uint64_t*>(s_ops);
+    for (int i = tid; i < n_ow; i += kPassThreads) odst[i] = osrc[i];
     __syncthreads();
-    {
-      const int n_entries = (sp.group_end - sp.group_begin) * 32;
-      for (int e = tid; e < n_entries; e += kPassThreads)
-        s_ttab[e >> 5][e & 31] = thread_table_entry(s_groups[e >> 5], e & 31);
-    }
+    const int n_entries = (sp.group_end - sp.group_begin) * 32;
+    for (int e = tid; e < n_entries; e += kPassThreads)
+      s_ttab[e >> 5][e & 31] = thread_table_entry(s_groups[e >> 5], e & 31);
     constexpr int kHi = kTileQubitsMax - kThreadBits;
     if (tid < (1 << kHi)) {
       uint64_t h = 0;
       for (int b = 0; b < kHi; ++b)
-        if ((tid >> b & 1) && kThreadBits + b < k) h |= uint64_t(1) << sp.tq[kThreadBits + b];
+        if ((tid >> b & 1) && kThreadBits + b < sp.k) h |= uint64_t(1) << sp.tq[kThreadBits + b];
       s_hi[tid] = h;
     }
+    __syncthreads();
+  };
+  if (p.pass_begin < p.pass_end) stage(p.pass_begin);
+
+  for (int pi = p.pass_begin; pi < p.pass_end; ++pi) {
+    const int k = sp.k;
     const int lo_bits = k < kThreadBits ? k : kThreadBits;
     uint64_t lo = 0;  // global offset of this thread's low tile-local bits
     for (int b = 0; b < lo_bits; ++b)
@@ -761,6 +764,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
       const double bs = block_sum(msum, red);
       if (tid == 0) p.partials[(mslot & 1) * gridDim.x + blockIdx.x] = bs;
     }
+    if (pi + 1 < p.pass_end) stage(pi + 1);  // overlaps the barrier wait
     __threadfence();
     grid.sync();
     if (mq >= 0) {
