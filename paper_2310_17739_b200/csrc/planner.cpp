@@ -17,6 +17,9 @@
 #include "../../include/nucsim_b200.h"
 
 #include <algorithm>
+#include <atomic>
+#include <exception>
+#include <thread>
 #include <cstdlib>
 #include <stdexcept>
 #include <unordered_map>
@@ -248,7 +251,22 @@ inline int parity32(uint32_t x) { return __builtin_popcount(x) & 1; }
 inline uint32_t swz11(uint32_t l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u); }
 
 // basis of {v in GF(2)^k : parity(f_i & v) = 0 for all i}
-std::vector<uint32_t> kernel_basis(const uint32_t* f, int nf, int k) {
+struct Basis {
+  uint32_t v[16];
+  int n = 0;
+  bool empty() const { return n == 0; }
+  size_t size() const { return static_cast<size_t>(n); }
+  uint32_t& operator[](size_t i) { return v[i]; }
+  uint32_t* begin() { return v; }
+  uint32_t* end() { return v + n; }
+  void insert_at(int pos, uint32_t x) {
+    for (int i = n; i > pos; --i) v[i] = v[i - 1];
+    v[pos] = x;
+    ++n;
+  }
+};
+
+Basis kernel_basis(const uint32_t* f, int nf, int k) {
   uint32_t rows[8];
   int piv[8], nr = 0;
   for (int i = 0; i < nf; ++i) {  // reduced row echelon form
@@ -262,15 +280,15 @@ std::vector<uint32_t> kernel_basis(const uint32_t* f, int nf, int k) {
     rows[nr] = r;
     piv[nr++] = p;
   }
-  std::vector<uint32_t> basis;
+  uint32_t pivmask = 0;
+  for (int j = 0; j < nr; ++j) pivmask |= 1u << piv[j];
+  Basis basis;
   for (int c = 0; c < k; ++c) {
-    bool pivot = false;
-    for (int j = 0; j < nr; ++j) pivot |= piv[j] == c;
-    if (pivot) continue;
+    if (pivmask >> c & 1) continue;
     uint32_t v = 1u << c;
     for (int j = 0; j < nr; ++j)
       if (rows[j] >> c & 1) v |= 1u << piv[j];
-    basis.push_back(v);
+    basis.v[basis.n++] = v;
   }
   return basis;
 }
@@ -348,6 +366,8 @@ struct OpenGroup {
   int nax = 0;
   Axis ax[3];
   uint32_t rcol[16];       // read map of the group's loads
+  uint32_t axm = 0;        // union of the (unpadded) axis masks
+  bool r_id = true;        // read map is the identity
   std::vector<GateOp> ops;
   std::vector<double> mats;  // packed payloads of the ops (complex, back to back)
 };
@@ -382,8 +402,8 @@ bool join_axes(OpenGroup& G, const Axis* ga, int nq, int* slot) {
 // so consecutive warp-local sweeps need only __syncwarp.
 bool warp_local(const OpenGroup& G, int p1, int p2) {
   const uint32_t wm = (1u << p1) | (1u << p2);
-  for (int i = 0; i < G.nax; ++i)
-    if (G.ax[i].m & wm) return false;
+  if (G.axm & wm) return false;
+  if (G.r_id) return true;
   for (int i = 0; i < 16; ++i) {
     const uint32_t want = (i == p1 ? 1u << p1 : 0u) | (i == p2 ? 1u << p2 : 0u);
     if ((G.rcol[i] & wm) != want) return false;
@@ -401,7 +421,7 @@ void finish_group(OpenGroup& G, int k, GroupDesc& d, int p1, int p2) {
       f[nf++] = 1u << p1;
       f[nf++] = 1u << p2;
     }
-    const std::vector<uint32_t> ker = kernel_basis(f, nf, k);
+    Basis ker = kernel_basis(f, nf, k);
     if (ker.empty()) throw std::logic_error("no free axis in the tile");
     Axis a;
     a.m = ker[0];
@@ -412,13 +432,13 @@ void finish_group(OpenGroup& G, int k, GroupDesc& d, int p1, int p2) {
     G.ax[G.nax++] = a;
   }
   uint32_t f[5] = {G.ax[0].rin, G.ax[1].rin, G.ax[2].rin, 0, 0};
-  std::vector<uint32_t> C = kernel_basis(f, 3, k);
+  Basis C = kernel_basis(f, 3, k);
   if (static_cast<int>(C.size()) != k - 3) throw std::logic_error("group axes are not dual");
   uint32_t c5 = 0, c6 = 0;
   if (local) {  // octet-index bits 5, 6 (the warp bits) pick the warp's (p1, p2) coset
     f[3] = 1u << p1;
     f[4] = 1u << p2;
-    std::vector<uint32_t> K = kernel_basis(f, 5, k);
+    Basis K = kernel_basis(f, 5, k);
     for (uint32_t v : C) {
       const int w = (v >> p1 & 1) | ((v >> p2 & 1) << 1);
       if (w == 1 && !c5) c5 = v;
@@ -436,7 +456,7 @@ void finish_group(OpenGroup& G, int k, GroupDesc& d, int p1, int p2) {
   // thread bits 0..2 first: basis vectors whose swizzled bank groups are independent
   uint32_t phis[3];
   int placed = 0;
-  for (size_t j = 0; j < C.size() && placed < 3; ++j) {
+  for (int j = 0; j < C.n && placed < 3; ++j) {
     uint32_t ph = swz11(C[j]) & 7u;
     for (int i = 0; i < placed; ++i)
       if (ph >> __builtin_ctz(phis[i]) & 1) ph ^= phis[i];
@@ -448,8 +468,8 @@ void finish_group(OpenGroup& G, int k, GroupDesc& d, int p1, int p2) {
     ++placed;
   }
   if (local) {
-    C.insert(C.begin() + 5, c6);
-    C.insert(C.begin() + 5, c5);
+    C.insert_at(5, c6);
+    C.insert_at(5, c5);
   }
   auto rmap = [&](uint32_t u) {  // R u on tile-local bits; batch bits pass through
     uint32_t out = u & ~((1u << k) - 1);
@@ -472,8 +492,102 @@ void finish_group(OpenGroup& G, int k, GroupDesc& d, int p1, int p2) {
 
 }  // namespace
 
+// Gate runs between two MEASURE / RESET ops are independent planning problems
+// (the relabeling frame is flushed at every marker), so long circuits are
+// planned on several host threads and the parts concatenated in order.
 void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
                      const double* payloads, int n, int workers) {
+  std::vector<int64_t> marks;
+  for (int64_t i = 0; i < n_ops; ++i)
+    if (ops[i].kind == NSB_OP_MEASURE || ops[i].kind == NSB_OP_RESET) marks.push_back(i);
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  if (marks.empty() || n_ops < 20000 || hw == 1 || std::getenv("NSB_PLAN_SERIAL")) {
+    build_serial(ops, n_ops, params, payloads, n, workers);
+    build_mma();
+    return;
+  }
+  // parts: [0, m0), [m0 + 1, m1), ..., [m_last + 1, n_ops)
+  const size_t n_parts = marks.size() + 1;
+  std::vector<HostPlan> parts(n_parts);
+  std::vector<std::exception_ptr> errors(n_parts);
+  auto range = [&](size_t s, int64_t& b, int64_t& e) {
+    b = s == 0 ? 0 : marks[s - 1] + 1;
+    e = s < marks.size() ? marks[s] : n_ops;
+  };
+  std::atomic<size_t> next{0};
+  auto worker = [&]() {
+    for (size_t s; (s = next.fetch_add(1)) < n_parts;) {
+      int64_t b, e;
+      range(s, b, e);
+      try {
+        parts[s].build_serial(ops + b, e - b, params, payloads, n, workers);
+      } catch (...) {
+        errors[s] = std::current_exception();
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < std::min<size_t>(hw, n_parts); ++t) pool.emplace_back(worker);
+  worker();
+  for (std::thread& t : pool) t.join();
+  for (auto& e : errors)
+    if (e) std::rethrow_exception(e);
+  // concatenate: each part's items, then the marker that ended it
+  build_serial(ops, 0, params, payloads, n, workers);  // header fields, no ops
+  int step = 0;
+  for (size_t s = 0; s < n_parts; ++s) {
+    HostPlan& H = parts[s];
+    const int32_t pass0 = static_cast<int32_t>(passes.size());
+    const int32_t group0 = static_cast<int32_t>(groups.size());
+    const int32_t op0 = static_cast<int32_t>(gate_ops.size());
+    const int32_t mat0 = static_cast<int32_t>(matrices.size() / 2);
+    const int64_t dense0 = static_cast<int64_t>(dense_mats.size() / 2);
+    for (PassDesc P : H.passes) {
+      P.group_begin += group0;
+      P.group_end += group0;
+      P.op_begin += op0;
+      P.op_end += op0;
+      P.mat_begin += mat0;
+      passes.push_back(P);
+    }
+    groups.insert(groups.end(), H.groups.begin(), H.groups.end());
+    gate_ops.insert(gate_ops.end(), H.gate_ops.begin(), H.gate_ops.end());
+    matrices.insert(matrices.end(), H.matrices.begin(), H.matrices.end());
+    dense_mats.insert(dense_mats.end(), H.dense_mats.begin(), H.dense_mats.end());
+    for (Item it : H.items) {
+      if (it.kind == Item::kGates) {
+        it.pass_begin += pass0;
+        it.pass_end += pass0;
+      } else if (it.kind == Item::kDense) {
+        it.mat_off += dense0;
+      }
+      items.push_back(it);
+    }
+    n_gates += H.n_gates;
+    n_frame_gates += H.n_frame_gates;
+    n_flush_gates += H.n_flush_gates;
+    n_frame_flushes += H.n_frame_flushes;
+    n_folded_gates += H.n_folded_gates;
+    n_ops += H.n_ops;
+    n_warp_syncs += H.n_warp_syncs;
+    flops += H.flops;
+    for (int c = 0; c < kNumClasses; ++c) class_count[c] += H.class_count[c];
+    if (s < marks.size()) {
+      const nsb_op& o = ops[marks[s]];
+      if (o.q[0] < 0 || o.q[0] >= n) throw std::invalid_argument("qubit out of range in plan");
+      Item it;
+      it.kind = o.kind == NSB_OP_MEASURE ? Item::kMeasure : Item::kReset;
+      it.qubit = o.q[0];
+      it.step = o.kind == NSB_OP_MEASURE ? step++ : -1;
+      items.push_back(it);
+    }
+  }
+  n_measures = step;
+  build_mma();
+}
+
+void HostPlan::build_serial(const nsb_op* ops, int64_t n_ops, const double* params,
+                            const double* payloads, int n, int workers) {
   n_qubits = n;
   if (n < 1 || n > kMaxQubits) throw std::invalid_argument("qubit count out of range");
   const int k = choose_tile_qubits(n, workers);
@@ -637,7 +751,6 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
   }
   flush_run();
   n_measures = step;
-  build_mma();
 }
 
 void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
@@ -654,7 +767,7 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
   }
   std::vector<uint64_t> sets;
   // one group slot stays free for a trailing read-map sweep
-  auto pass_groups = pack_groups(masks, k, low, all, 2048, sets, &deps, &weights,
+  auto pass_groups = pack_groups(masks, k, low, all, 256, sets, &deps, &weights,
                                  kMaxPassGates - 1, kMaxPassMats);
   for (size_t pi = 0; pi < pass_groups.size(); ++pi) {
     uint64_t tset = sets[pi];
@@ -681,7 +794,11 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
     std::vector<OpenGroup> closed;  // the pass's groups, finalised at the end
     auto close = [&]() {
       if (!open) return;
-      closed.push_back(G);
+      G.axm = 0;
+      for (int i = 0; i < G.nax; ++i) G.axm |= G.ax[i].m;
+      G.r_id = true;
+      for (int i = 0; i < 16; ++i) G.r_id &= G.rcol[i] == (1u << i);
+      closed.push_back(std::move(G));
       open = false;
     };
     auto start = [&]() {
@@ -784,13 +901,18 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
     // must be tile-local for the warp bits 5, 6 to be C vectors: k >= 10)
     int w1 = -1, w2 = -1;
     if (k >= 10 && kPassThreads == 128) {
+      // positions a group keeps out of the warp split: its axes (all of them
+      // when its read map is not the identity -- exact check below)
+      std::vector<uint32_t> blocked(closed.size());
+      for (size_t g = 0; g < closed.size(); ++g)
+        blocked[g] = closed[g].r_id ? closed[g].axm : ~0u;
       int best = 0;
-      std::vector<char> loc(closed.size());
       for (int p1 = 0; p1 < k; ++p1)
         for (int p2 = p1 + 1; p2 < k; ++p2) {
-          for (size_t g = 0; g < closed.size(); ++g) loc[g] = warp_local(closed[g], p1, p2);
+          const uint32_t wm = (1u << p1) | (1u << p2);
           int score = 0;
-          for (size_t g = 0; g + 1 < closed.size(); ++g) score += loc[g] && loc[g + 1];
+          for (size_t g = 0; g + 1 < closed.size(); ++g)
+            score += !((blocked[g] | blocked[g + 1]) & wm);
           if (score > best) {
             best = score;
             w1 = p1;

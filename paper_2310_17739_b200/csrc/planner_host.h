@@ -92,6 +92,8 @@ struct HostPlan {
              int n, int workers);
 
  private:
+  void build_serial(const nsb_op* ops, int64_t n_ops, const double* params,
+                    const double* payloads, int n, int workers);
   void schedule_run(std::vector<PhysGate>& run, int k);
   void build_mma();
 };

@@ -66,3 +66,23 @@ def test_golden_filter8_plan(golden):
     d = golden("filter8")
     for pre in ("fused_", "in_"):
         check(to_circuit(d, pre))
+
+
+def test_parallel_planning_matches_serial(monkeypatch):
+    """Gate runs between markers are planned on host threads; the merged
+    program must be byte-identical to the serial one."""
+    from paper_2310_17739_b200 import workloads as W
+    wl = W.filter_workload(11, 6, n_steps=4, seed=3, hop_range=8)
+    fops, pool, _ = W.fuse_packed(wl.ops, wl.params, wl.payloads)
+    exe = wl.executable(fops)
+    assert len(exe) >= 20000
+
+    def view():
+        hp = PE.HostPlan(exe, wl.params, pool, wl.n_qubits, workers=296)
+        return (hp.passes.tobytes(), hp.mma_passes.tobytes(), hp.groups.tobytes(),
+                hp.ops.tobytes(), hp.mats.tobytes(), hp.items.tobytes())
+
+    par = view()
+    monkeypatch.setenv("NSB_PLAN_SERIAL", "1")
+    ser = view()
+    assert par == ser
