@@ -568,7 +568,7 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
     n_flush_gates += H.n_flush_gates;
     n_frame_flushes += H.n_frame_flushes;
     n_folded_gates += H.n_folded_gates;
-    n_ops += H.n_ops;
+    this->n_ops += H.n_ops;
     n_warp_syncs += H.n_warp_syncs;
     flops += H.flops;
     for (int c = 0; c < kNumClasses; ++c) class_count[c] += H.class_count[c];
