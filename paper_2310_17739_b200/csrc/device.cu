@@ -870,6 +870,7 @@ struct nsb_ctx {
   uint64_t n_amps = 0;
   DevBuf<double2> amps;
   DevBuf<double> scratch;  // reductions
+  DevBuf<double> probs;    // nsb_probabilities (kept between calls)
   double* pinned = nullptr;
   size_t pinned_bytes = 0;
   // sharded state (nsb_comm_init): this process holds rank `rank` of `nranks`
@@ -993,6 +994,34 @@ void ensure_pinned(nsb_ctx* c, size_t bytes) {
   c->pinned_bytes = 0;
   NSB_CUDA(cudaMallocHost(&c->pinned, bytes));
   c->pinned_bytes = bytes;
+}
+
+// Host <-> device through the context's pinned staging buffer (16 MiB chunks):
+// pageable copies make the driver stage and pin on every call, with erratic
+// latency (observed 5 ms .. 0.9 s for 16 MiB on the same box).
+void copy_d2h(nsb_ctx* c, void* dst, const void* src, size_t bytes) {
+  const size_t chunk = size_t(16) << 20;
+  ensure_pinned(c, std::min(bytes, chunk));
+  for (size_t off = 0; off < bytes; off += chunk) {
+    const size_t nb = std::min(chunk, bytes - off);
+    NSB_CUDA(cudaMemcpyAsync(c->pinned, static_cast<const char*>(src) + off, nb,
+                             cudaMemcpyDeviceToHost, c->stream));
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+    std::memcpy(static_cast<char*>(dst) + off, c->pinned, nb);
+  }
+}
+
+void copy_h2d(nsb_ctx* c, void* dst, const void* src, size_t bytes) {
+  const size_t chunk = size_t(16) << 20;
+  ensure_pinned(c, std::min(bytes, chunk));
+  for (size_t off = 0; off < bytes; off += chunk) {
+    const size_t nb = std::min(chunk, bytes - off);
+    NSB_CUDA(cudaStreamSynchronize(c->stream));  // staging free again
+    std::memcpy(c->pinned, static_cast<const char*>(src) + off, nb);
+    NSB_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, c->pinned, nb,
+                             cudaMemcpyHostToDevice, c->stream));
+  }
+  NSB_CUDA(cudaStreamSynchronize(c->stream));
 }
 
 // deterministic half-norm: fixed grid, then fixed-order sum
@@ -1144,6 +1173,7 @@ void nsb_ctx_destroy(nsb_ctx* ctx) {
   if (ctx->comm) shard_comm_destroy(ctx);
   ctx->amps.release();
   ctx->scratch.release();
+  ctx->probs.release();
   for (int b = 0; b < 2; ++b) {
     ctx->stage_send[b].release();
     ctx->stage_recv[b].release();
@@ -1196,9 +1226,7 @@ int nsb_state_upload(nsb_ctx* c, const double* amps, nsb_status* st) {
     require_state(c);
     if (!amps) throw std::invalid_argument("null host buffer");
     NSB_CUDA(cudaSetDevice(c->device));
-    NSB_CUDA(cudaMemcpyAsync(c->amps.ptr, amps, c->n_amps * sizeof(double2),
-                             cudaMemcpyHostToDevice, c->stream));
-    NSB_CUDA(cudaStreamSynchronize(c->stream));
+    copy_h2d(c, c->amps.ptr, amps, c->n_amps * sizeof(double2));
   });
 }
 
@@ -1207,9 +1235,7 @@ int nsb_state_download(nsb_ctx* c, double* amps, nsb_status* st) {
     require_state(c);
     if (!amps) throw std::invalid_argument("null host buffer");
     NSB_CUDA(cudaSetDevice(c->device));
-    NSB_CUDA(cudaMemcpyAsync(amps, c->amps.ptr, c->n_amps * sizeof(double2),
-                             cudaMemcpyDeviceToHost, c->stream));
-    NSB_CUDA(cudaStreamSynchronize(c->stream));
+    copy_d2h(c, amps, c->amps.ptr, c->n_amps * sizeof(double2));
   });
 }
 
@@ -1264,14 +1290,11 @@ int nsb_probabilities(nsb_ctx* c, double* out, nsb_status* st) {
     require_state(c);
     if (!out) throw std::invalid_argument("null output");
     NSB_CUDA(cudaSetDevice(c->device));
-    DevBuf<double> probs;
-    probs.alloc(c->n_amps);
+    if (c->probs.count < c->n_amps) c->probs.alloc(c->n_amps);
     dev::k_probabilities<<<grid_for(c->n_amps, 256, c), 256, 0, c->stream>>>(
-        c->amps.ptr, c->n_amps, probs.ptr);
+        c->amps.ptr, c->n_amps, c->probs.ptr);
     NSB_CUDA(cudaGetLastError());
-    NSB_CUDA(cudaMemcpyAsync(out, probs.ptr, c->n_amps * sizeof(double), cudaMemcpyDeviceToHost,
-                             c->stream));
-    NSB_CUDA(cudaStreamSynchronize(c->stream));
+    copy_d2h(c, out, c->probs.ptr, c->n_amps * sizeof(double));
   });
 }
 
