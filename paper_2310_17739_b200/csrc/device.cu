@@ -494,20 +494,22 @@ __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
   constexpr int NO = kOctets;
   const int t = threadIdx.x;
   const int cb = k - 3;
-  const int n_act = nvalid << cb;  // octets in the batch
-  if (t >= n_act) return;
+  // Every thread sweeps both of its octets.  Octets past the batch's valid
+  // tiles (a short last batch, or k < 8) address the unused part of the
+  // 2^11-amplitude buffer: they move garbage that is never stored to global
+  // memory, which is cheaper than predicating every load and store.
+  (void)nvalid;
   const uint32_t v = ttab[t & 15] ^ ttab[16 + (t >> 4)];
   const int m0 = G.am[0], m1 = G.am[1], m2 = G.am[2];
   const int r0 = G.ram[0], r1 = G.ram[1], r2 = G.ram[2];
   int a[NO], r[NO];
-  bool live[NO];
 #pragma unroll
   for (int q = 0; q < NO; ++q) {
     const int oi = t + (q << kThreadBits);
-    live[q] = oi < n_act;
     a[q] = (v & 0xffffu) ^ (q ? G.tcol[kThreadBits] : 0);
     r[q] = (v >> 16) ^ (q ? G.rtcol[kThreadBits] : 0);
-    const unsigned kp = (kap >> (3 * (oi >> cb))) & 7u;
+    const int sh = 3 * (oi >> cb);  // tiles >= 4 exist only as garbage octets
+    const unsigned kp = sh < 12 ? (kap >> sh) & 7u : 0u;
     if (kp & 1) { a[q] ^= m0; r[q] ^= r0; }
     if (kp & 2) { a[q] ^= m1; r[q] ^= r1; }
     if (kp & 4) { a[q] ^= m2; r[q] ^= r2; }
@@ -517,16 +519,14 @@ __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
   for (int q = 0; q < NO; ++q)
 #pragma unroll
     for (int c = 0; c < 8; ++c)
-      x[q][c] = live[q] ? src[r[q] ^ ((c & 1) ? r0 : 0) ^ ((c & 2) ? r1 : 0) ^ ((c & 4) ? r2 : 0)]
-                        : make_double2(0.0, 0.0);
+      x[q][c] = src[r[q] ^ ((c & 1) ? r0 : 0) ^ ((c & 2) ? r1 : 0) ^ ((c & 4) ? r2 : 0)];
   const int n_ops = G.n_ops;
   auto store = [&]() {
 #pragma unroll
     for (int q = 0; q < NO; ++q)
-      if (live[q])
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
-          dst[a[q] ^ ((c & 1) ? m0 : 0) ^ ((c & 2) ? m1 : 0) ^ ((c & 4) ? m2 : 0)] = x[q][c];
+      for (int c = 0; c < 8; ++c)
+        dst[a[q] ^ ((c & 1) ? m0 : 0) ^ ((c & 2) ? m1 : 0) ^ ((c & 4) ? m2 : 0)] = x[q][c];
   };
   // Gate dispatch: pattern * 16 + class selects straight-line register code.
   // The LAST gate of a group stores its octets from inside its own case, so
