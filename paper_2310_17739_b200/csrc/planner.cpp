@@ -590,7 +590,8 @@ void HostPlan::build_serial(const nsb_op* ops, int64_t n_ops, const double* para
                             const double* payloads, int n, int workers) {
   n_qubits = n;
   if (n < 1 || n > kMaxQubits) throw std::invalid_argument("qubit count out of range");
-  const int k = choose_tile_qubits(n, workers);
+  int k = choose_tile_qubits(n, workers);
+  if (const char* e = std::getenv("NSB_TILE_QUBITS")) k = std::min(std::atoi(e), n);  // tuning
   tile_qubits = k;
   low_qubits = n <= kL2ResidentQubits ? 1 : kLowQubits;
   if (const char* e = std::getenv("NSB_LOW_QUBITS")) low_qubits = std::atoi(e);  // tuning
