@@ -396,31 +396,29 @@ bool join_axes(OpenGroup& G, const Axis* ga, int nq, int* slot) {
   return true;
 }
 
-// Warp-local sweeps: with warp positions (p1, p2) a group whose axes avoid
-// both tile positions (and whose read map keeps them) can give warp w exactly
-// the amplitudes with (bit p1, bit p2) = w -- its octets never leave that set,
-// so consecutive warp-local sweeps need only __syncwarp.
-bool warp_local(const OpenGroup& G, int p1, int p2) {
-  const uint32_t wm = (1u << p1) | (1u << p2);
+// Warp-local sweeps: with warp positions W (kWarpBits tile positions, mask
+// wm) a group whose axes avoid them (and whose read map keeps them) can give
+// warp w exactly the amplitudes whose bits at W spell w -- its octets never
+// leave that set, so consecutive warp-local sweeps need only __syncwarp.
+constexpr int kWarpBits = kThreadBits - 5;
+
+bool warp_local(const OpenGroup& G, uint32_t wm) {
   if (G.axm & wm) return false;
   if (G.r_id) return true;
   for (int i = 0; i < 16; ++i) {
-    const uint32_t want = (i == p1 ? 1u << p1 : 0u) | (i == p2 ? 1u << p2 : 0u);
+    const uint32_t want = (wm >> i & 1) ? (1u << i) : 0u;
     if ((G.rcol[i] & wm) != want) return false;
   }
   return true;
 }
 
-void finish_group(OpenGroup& G, int k, GroupDesc& d, int p1, int p2) {
-  const bool local = p1 >= 0;
+void finish_group(OpenGroup& G, int k, GroupDesc& d, uint32_t wm) {
+  const bool local = wm != 0;
   while (G.nax < 3) {  // pad with a free axis of the tile (outside the warp positions)
-    uint32_t f[5];
+    uint32_t f[3 + kWarpBits];
     int nf = 0;
     for (int i = 0; i < G.nax; ++i) f[nf++] = G.ax[i].rin;
-    if (local) {
-      f[nf++] = 1u << p1;
-      f[nf++] = 1u << p2;
-    }
+    for (uint32_t w = wm; w; w &= w - 1) f[nf++] = w & (0u - w);
     Basis ker = kernel_basis(f, nf, k);
     if (ker.empty()) throw std::logic_error("no free axis in the tile");
     Axis a;
@@ -431,26 +429,36 @@ void finish_group(OpenGroup& G, int k, GroupDesc& d, int p1, int p2) {
       if (G.ax[j].m >> p & 1) a.rin ^= G.ax[j].rin;
     G.ax[G.nax++] = a;
   }
-  uint32_t f[5] = {G.ax[0].rin, G.ax[1].rin, G.ax[2].rin, 0, 0};
+  uint32_t f[3] = {G.ax[0].rin, G.ax[1].rin, G.ax[2].rin};
   Basis C = kernel_basis(f, 3, k);
   if (static_cast<int>(C.size()) != k - 3) throw std::logic_error("group axes are not dual");
-  uint32_t c5 = 0, c6 = 0;
-  if (local) {  // octet-index bits 5, 6 (the warp bits) pick the warp's (p1, p2) coset
-    f[3] = 1u << p1;
-    f[4] = 1u << p2;
-    Basis K = kernel_basis(f, 5, k);
-    for (uint32_t v : C) {
-      const int w = (v >> p1 & 1) | ((v >> p2 & 1) << 1);
-      if (w == 1 && !c5) c5 = v;
-      if (w == 2 && !c6) c6 = v;
+  uint32_t cw[kWarpBits > 0 ? kWarpBits : 1] = {};
+  if (local) {  // index bits 5.. (the warp bits) pick the warp's coset of W
+    int wp[kWarpBits], nw = 0;
+    for (uint32_t w = wm; w; w &= w - 1) wp[nw++] = __builtin_ctz(w);
+    auto phi = [&](uint32_t v) {
+      uint32_t o = 0;
+      for (int j = 0; j < nw; ++j) o |= (v >> wp[j] & 1) << j;
+      return o;
+    };
+    // reduce C so that kWarpBits vectors have unit images under phi, the rest 0
+    int np = 0;
+    for (int j = 0; j < nw; ++j) {
+      int piv = -1;
+      for (int i = np; i < C.n; ++i)
+        if (phi(C.v[i]) >> j & 1) {
+          piv = i;
+          break;
+        }
+      if (piv < 0) throw std::logic_error("warp positions do not split the group");
+      std::swap(C.v[np], C.v[piv]);
+      for (int i = 0; i < C.n; ++i)
+        if (i != np && (phi(C.v[i]) >> j & 1)) C.v[i] ^= C.v[np];
+      ++np;
     }
-    for (uint32_t v : C) {  // mixed vectors give the missing one
-      const int w = (v >> p1 & 1) | ((v >> p2 & 1) << 1);
-      if (w == 3 && !c5 && c6) c5 = v ^ c6;
-      if (w == 3 && !c6 && c5) c6 = v ^ c5;
-    }
-    if (!c5 || !c6 || static_cast<int>(K.size()) != k - 5)
-      throw std::logic_error("warp positions do not split the group");
+    for (int j = 0; j < nw; ++j) cw[j] = C.v[j];  // phi(cw[j]) = e_j
+    Basis K;
+    for (int i = nw; i < C.n; ++i) K.v[K.n++] = C.v[i];
     C = K;
   }
   // thread bits 0..2 first: basis vectors whose swizzled bank groups are independent
@@ -467,10 +475,8 @@ void finish_group(OpenGroup& G, int k, GroupDesc& d, int p1, int p2) {
     std::swap(C[placed], C[j]);
     ++placed;
   }
-  if (local) {
-    C.insert_at(5, c6);
-    C.insert_at(5, c5);
-  }
+  if (local)
+    for (int j = kWarpBits - 1; j >= 0; --j) C.insert_at(5, cw[j]);
   auto rmap = [&](uint32_t u) {  // R u on tile-local bits; batch bits pass through
     uint32_t out = u & ~((1u << k) - 1);
     for (int i = 0; i < k; ++i)
@@ -483,7 +489,7 @@ void finish_group(OpenGroup& G, int k, GroupDesc& d, int p1, int p2) {
     d.r_out[i] = G.ax[i].rout;
   }
   const int cb = k - 3;
-  for (int b = 0; b < 8; ++b) {
+  for (int b = 0; b < kIndexBits; ++b) {
     const uint32_t v = b < cb ? C[b] : (1u << (k + b - cb));  // then tile-in-batch bits
     d.tcol[b] = static_cast<uint16_t>(swz11(v));
     d.rtcol[b] = static_cast<uint16_t>(swz11(rmap(v)));
@@ -900,26 +906,24 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
     // warp positions: the pair of tile positions that lets the most
     // consecutive sweeps run warp-locally (kThreadBits + 1 octet-index bits
     // must be tile-local for the warp bits 5, 6 to be C vectors: k >= 10)
-    int w1 = -1, w2 = -1;
-    if (k >= 10 && kPassThreads == 128) {
+    uint32_t wsel = 0;  // chosen warp positions
+    if (k - 3 >= kThreadBits) {  // the warp bits of the octet index are tile-local C vectors
       // positions a group keeps out of the warp split: its axes (all of them
       // when its read map is not the identity -- exact check below)
       std::vector<uint32_t> blocked(closed.size());
       for (size_t g = 0; g < closed.size(); ++g)
         blocked[g] = closed[g].r_id ? closed[g].axm : ~0u;
       int best = 0;
-      for (int p1 = 0; p1 < k; ++p1)
-        for (int p2 = p1 + 1; p2 < k; ++p2) {
-          const uint32_t wm = (1u << p1) | (1u << p2);
-          int score = 0;
-          for (size_t g = 0; g + 1 < closed.size(); ++g)
-            score += !((blocked[g] | blocked[g + 1]) & wm);
-          if (score > best) {
-            best = score;
-            w1 = p1;
-            w2 = p2;
-          }
+      for (uint32_t wm = 1; wm < (1u << k); ++wm) {
+        if (__builtin_popcount(wm) != kWarpBits) continue;
+        int score = 0;
+        for (size_t g = 0; g + 1 < closed.size(); ++g)
+          score += !((blocked[g] | blocked[g + 1]) & wm);
+        if (score > best) {
+          best = score;
+          wsel = wm;
         }
+      }
     }
     for (size_t g = 0; g < closed.size(); ++g) {
       OpenGroup& H = closed[g];
@@ -932,9 +936,9 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
         gate_ops.push_back(op);
       }
       matrices.insert(matrices.end(), H.mats.begin(), H.mats.end());
-      const bool here = w1 >= 0 && warp_local(H, w1, w2);
-      const bool next = g + 1 < closed.size() && w1 >= 0 && warp_local(closed[g + 1], w1, w2);
-      finish_group(H, k, d, here ? w1 : -1, here ? w2 : -1);
+      const bool here = wsel && warp_local(H, wsel);
+      const bool next = g + 1 < closed.size() && wsel && warp_local(closed[g + 1], wsel);
+      finish_group(H, k, d, here ? wsel : 0u);
       d.sync = (here && next) ? 0 : 1;
       if (!d.sync) ++n_warp_syncs;
       groups.push_back(d);

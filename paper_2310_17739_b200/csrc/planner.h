@@ -32,6 +32,8 @@ constexpr int kTileAmpsMax = 1 << kTileQubitsMax;
 constexpr int kThreadBits = 7;
 constexpr int kPassThreads = 1 << kThreadBits;  // 4 warps per CTA, two CTAs per SM
 constexpr int kOctets = 2;                       // octets per thread per sweep
+constexpr int kIndexBits = kThreadBits + 1;      // octet-index bits of a full batch
+static_assert(kIndexBits <= 9, "GroupDesc holds 9 index-bit offsets");
 constexpr int kLowQubits = 3;                    // always-tiled qubits 0..2 (128 B runs)
 // States up to this many qubits stay L2-resident inside a launch: their
 // tiles need not hold qubits 0..2 (sector efficiency matters less than the
@@ -87,12 +89,13 @@ enum GateClass : uint8_t {
 struct GroupDesc {        // 80 bytes
   uint16_t am[3];         // swizzled axis masks (store side)
   uint16_t ram[3];        // the same through the read map R (load side)
-  uint16_t tcol[8];       // swizzled offsets of thread bits 0..7 (store side)
-  uint16_t rtcol[8];      // load side
+  uint16_t tcol[9];       // swizzled offsets of octet-index bits (store side):
+                          // thread bits, then the thread's second-octet bit
+  uint16_t rtcol[9];      // load side
   uint8_t op_begin;       // first GateOp (relative to the pass's op_begin)
   uint8_t n_ops;          // 0: a pure read-map sweep
   uint8_t sync;           // 1: CTA barrier after this sweep; 0: warp-local, __syncwarp
-  uint8_t pad[9];
+  uint8_t pad[5];
   uint64_t r_out[3];      // out-of-tile parts of the axes' dual rows
 };
 static_assert(sizeof(GroupDesc) == 80, "GroupDesc layout");

@@ -21,11 +21,12 @@ PASS_DT = np.dtype([("group_begin", "<i4"), ("group_end", "<i4"), ("op_begin", "
                     ("measure_q", "<i4"), ("measure_slot", "<i4"), ("collapse_q", "<i4"),
                     ("collapse_slot", "<i4"), ("pad", "<i4"), ("tq", "i1", (16,)),
                     ("oq", "i1", (48,))])
-GROUP_DT = np.dtype([("am", "<u2", (3,)), ("ram", "<u2", (3,)), ("tcol", "<u2", (8,)),
-                     ("rtcol", "<u2", (8,)), ("op_begin", "u1"), ("n_ops", "u1"),
-                     ("sync", "u1"), ("pad", "u1", (9,)), ("r_out", "<u8", (3,))], align=True)
+GROUP_DT = np.dtype([("am", "<u2", (3,)), ("ram", "<u2", (3,)), ("tcol", "<u2", (9,)),
+                     ("rtcol", "<u2", (9,)), ("op_begin", "u1"), ("n_ops", "u1"),
+                     ("sync", "u1"), ("pad", "u1", (5,)), ("r_out", "<u8", (3,))], align=True)
 OP_DT = np.dtype([("mat", "<i2"), ("cls", "u1"), ("pat", "u1"), ("cols", "<u2"), ("kind", "u1"), ("pad", "u1")])
-THREADS = 128  # kPassThreads
+THREAD_BITS = 7  # kThreadBits
+THREADS = 1 << THREAD_BITS  # kPassThreads
 TILE_MAX = 11  # kTileQubitsMax
 (DENSE1, DIAG1, DENSE2, SPARSE2, MONO2, DIAG2, CX01, CX10, PAIRQ, PAIRP, PAIRX, SWAP,
  PERMUTE) = range(13)
@@ -143,7 +144,7 @@ def _apply_group(B, G, ops, mats, tbases, k, nvalid):
     t = np.arange(n_act, dtype=np.int64)
     a = np.zeros(n_act, np.int64)
     r = np.zeros(n_act, np.int64)
-    for b in range(8):
+    for b in range(THREAD_BITS + 1):
         a ^= np.where((t >> b) & 1, int(G["tcol"][b]), 0)
         r ^= np.where((t >> b) & 1, int(G["rtcol"][b]), 0)
     tile = t >> cb
@@ -161,9 +162,10 @@ def _apply_group(B, G, ops, mats, tbases, k, nvalid):
     assert len(np.unique(np.concatenate(st))) == 8 * n_act  # octets partition the batch
     assert len(np.unique(np.concatenate(ld))) == 8 * n_act
     S = B.copy()  # out of place: loads see the pre-sweep batch
-    warp = (t >> 5) & 3  # octet index bits 5, 6 (kThreadBits = 7 threads per CTA)
-    loads = [np.sort(np.concatenate([U(l)[warp == w] for l in ld])) for w in range(4)]
-    stores = [np.sort(np.concatenate([U(s_)[warp == w] for s_ in st])) for w in range(4)]
+    n_warps = THREADS // 32
+    warp = (t >> 5) & (n_warps - 1)  # octet-index bits 5 .. kThreadBits-1
+    loads = [np.sort(np.concatenate([U(l)[warp == w] for l in ld])) for w in range(n_warps)]
+    stores = [np.sort(np.concatenate([U(s_)[warp == w] for s_ in st])) for w in range(n_warps)]
     x = [S[U(l)] for l in ld]
     o0 = int(G["op_begin"])
     for op in ops[o0:o0 + int(G["n_ops"])]:
@@ -204,7 +206,7 @@ def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12, workers=1
                 for G in groups:
                     loads, stores = _apply_group(B, G, pops, block, tbs, k, nvalid)
                     if prev is not None:  # __syncwarp only: each warp reads its own writes
-                        for w in range(4):
+                        for w in range(len(loads)):
                             assert np.array_equal(loads[w], prev[w])
                     prev = stores if int(G["sync"]) == 0 else None
                 state[idx] = B
