@@ -411,3 +411,29 @@ def test_relabeling_frame_against_oracle(n, terms):
         rej = run(circ, "rejection", shots=3, seed=4, ancilla=None)
         acc, steps, counts = O.run_rejection(instrs, n, 3, 4)
         assert (rej.accepted, rej.step_rejections, rej.samples) == (acc, steps, counts)
+
+
+@pytest.mark.gpu
+def test_rejection_replay_equals_explicit_shots(golden):
+    """The replay fast path gives the same tallies, samples and accepted
+    count as simulating every shot (same seed, same Philox stream)."""
+    from paper_2310_17739_b200 import engine as E
+    d = golden("filter8")
+    fused = to_circuit(d, "fused_")
+    instrs = fused.instructions
+    end = E._sampling_start(instrs)
+    packed = E.pack(fused, instrs[:end])
+    n_steps = sum(1 for ins in instrs[:end] if ins.gate is E.Gate.MEASURE)
+    state = E.StateVector(fused.n_qubits)
+    prog = E.DeviceProgram(state, packed.ops, packed.params, packed.payloads)
+    items = prog.items()
+    assert E._replayable(items)
+    fast = E._rejection(state, prog, items, n_steps, 200, E._as_rng(11), False)
+    # explicit path: force the non-replay branch
+    saved = E._replayable
+    try:
+        E._replayable = lambda items: False
+        slow = E._rejection(state, prog, items, n_steps, 200, E._as_rng(11), False)
+    finally:
+        E._replayable = saved
+    assert fast[0] == slow[0] and fast[2] == slow[2] and fast[1] == slow[1]
