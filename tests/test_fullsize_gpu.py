@@ -1,0 +1,129 @@
+"""Full-size (BASELINE config 3, 21 qubits) properties of the device path,
+where the oracle is too slow to compare amplitude by amplitude:
+
+* the fused gate stream of the P9-shaped filter circuit followed by its
+  adjoint (reversed, conjugate-transposed payloads) returns |0...0>;
+* the single-launch MMA program and the host-driven item path (per-op
+  measurement kernels) agree on every assertion probability;
+* edge cases: empty programs, one-qubit states, marker-only circuits."""
+
+import numpy as np
+import pytest
+
+from paper_2310_17739_b200 import _native as N
+from paper_2310_17739_b200 import workloads as W
+from paper_2310_17739_b200.engine import DeviceProgram, StateVector, _branch_probability, _project
+from paper_2310_17739_b200.gates import BY_CODE, Gate, gate_matrix
+
+pytestmark = pytest.mark.gpu
+
+
+def _matrix(rec, params, pool):
+    nq = int(rec["nq"])
+    if int(rec["payload"]) >= 0:
+        d = 1 << nq
+        off = int(rec["payload"])
+        return pool[off: off + d * d].reshape(d, d)
+    g = BY_CODE[int(rec["tag"])]
+    p0 = int(rec["param"])
+    return gate_matrix(g, tuple(params[p0: p0 + g.n_params]) if g.n_params else ())
+
+
+def _adjoint(ops, params, pool):
+    """Reversed stream of payload gates U^dagger (C1 / C2 tags)."""
+    gates = ops[ops["kind"] == N.OP_GATE][::-1]
+    out = np.zeros(len(gates), N.OP_DTYPE)
+    mats = []
+    off = 0
+    for i, rec in enumerate(gates):
+        u = np.conj(_matrix(rec, params, pool)).T
+        nq = int(rec["nq"])
+        out[i]["kind"], out[i]["nq"], out[i]["cbit"] = N.OP_GATE, nq, -1
+        out[i]["tag"] = (Gate.C1 if nq == 1 else Gate.C2).code
+        out[i]["q"] = rec["q"]
+        out[i]["mask"] = rec["mask"]
+        out[i]["src"], out[i]["param"], out[i]["payload"] = -1, -1, off
+        mats.append(np.ascontiguousarray(u).reshape(-1))
+        off += u.size
+    return out, np.concatenate(mats)
+
+
+def test_filter21_stream_then_adjoint_is_identity():
+    wl = W.filter_workload(20, trotter=1, n_steps=2, n_scatter=8, trial="10" * 10)
+    fops, pool, _ = W.fuse_packed(wl.ops, wl.params, wl.payloads)
+    gates = fops[fops["kind"] == N.OP_GATE]
+    inv, inv_pool = _adjoint(gates, wl.params, pool)
+    state = StateVector(wl.n_qubits)
+    fwd = DeviceProgram(state, gates, wl.params, pool)
+    assert fwd.info.n_passes > 100
+    fwd.run_mma()
+    mid = state.amps.copy()
+    assert abs(np.linalg.norm(mid) - 1.0) < 1e-10
+    assert abs(mid[0]) < 0.99  # the stream moved the state
+    back = DeviceProgram(state, inv, np.zeros(1), inv_pool)
+    back.run_mma()
+    a = state.amps
+    assert abs(a[0] - 1.0) < 1e-9
+    assert np.linalg.norm(a[1:]) < 1e-9
+
+
+def test_filter21_mma_launch_matches_item_path():
+    wl = W.filter_workload(20, trotter=1, n_steps=8, n_scatter=8, trial="10" * 10)
+    fops, pool, _ = W.fuse_packed(wl.ops, wl.params, wl.payloads)
+    exe = wl.executable(fops)
+    state = StateVector(wl.n_qubits)
+    prog = DeviceProgram(state, exe, wl.params, pool)
+    p_mma = prog.run_mma()
+    final_mma = state.amps.copy()
+    state.restart()
+    p_items = []
+    for i, (kind, q, step) in enumerate(prog.items()):
+        if kind == N.OP_MEASURE:
+            p0 = _branch_probability(state, q, 0)
+            p_items.append(p0)
+            _project(state, q, 0, p0)
+        elif kind == N.OP_GATE:
+            prog.run_item(i)
+    assert len(p_mma) == 8
+    np.testing.assert_allclose(p_mma, p_items, rtol=1e-12, atol=0)
+    a = state.amps
+    assert np.linalg.norm(a - final_mma) <= 1e-10 * np.linalg.norm(a)
+
+
+def test_empty_and_marker_only_programs():
+    state = StateVector(8)
+    empty = np.zeros(0, N.OP_DTYPE)
+    prog = DeviceProgram(state, empty, np.zeros(1), np.zeros(1, np.complex128))
+    assert prog.run_mma() == []
+    assert state.amps[0] == 1.0
+    ops = np.zeros(2, N.OP_DTYPE)
+    ops["kind"] = (N.OP_MEASURE, N.OP_RESET)
+    ops["nq"], ops["cbit"], ops["src"], ops["param"], ops["payload"] = 1, -1, -1, -1, -1
+    ops["q"] = -1
+    ops["q"][:, 0] = 3
+    prog = DeviceProgram(state, ops, np.zeros(1), np.zeros(1, np.complex128))
+    assert prog.run_mma() == [1.0]
+
+
+@pytest.mark.parametrize("n", [1, 2, 5])
+def test_tiny_states_through_the_plan(n):
+    """n < 6 takes the per-op path of the same plan API."""
+    rng = np.random.default_rng(n)
+    ops = np.zeros(6, N.OP_DTYPE)
+    params = []
+    for i in range(6):
+        ops[i]["kind"], ops[i]["tag"], ops[i]["nq"], ops[i]["cbit"] = N.OP_GATE, Gate.U3.code, 1, -1
+        ops[i]["q"] = (i % n, -1, -1, -1, -1)
+        ops[i]["src"], ops[i]["payload"], ops[i]["param"] = -1, -1, len(params)
+        params.extend(rng.uniform(-3, 3, 3))
+    params = np.asarray(params)
+    state = StateVector(n)
+    DeviceProgram(state, ops, params, np.zeros(1, np.complex128)).run_mma()
+    want = np.zeros(1 << n, complex)
+    want[0] = 1
+    for rec in ops:
+        u = gate_matrix(Gate.U3, tuple(params[int(rec["param"]): int(rec["param"]) + 3]))
+        q = int(rec["q"][0])
+        want = want.reshape(-1, 2, 1 << q)
+        want = np.einsum("ab,rbt->rat", u, want).reshape(-1)
+    np.testing.assert_allclose(state.amps, want, atol=1e-13)
