@@ -382,6 +382,8 @@ def run_ours(args, rank, world, local):
     sm_mhz = clk.get("sm_mhz") or pk["sm_max_mhz"]
     fp64_peak = 148 * FP64_DFMA_PER_CLK_PER_SM * 2 * sm_mhz * 1e6 / 1e12
     fp64_ach = info.flops / kernel_s / 1e12
+    smem_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
+    smem_ach = info.n_sweeps * 32 * (1 << n) / kernel_s / 1e12
     profile = ROOT / "profiles" / "r01_dram_bytes.json"
     traffic = None
     if profile.exists():
@@ -409,6 +411,11 @@ def run_ours(args, rank, world, local):
                          "traffic": traffic, "peak_source": pk["source"],
                          "note": "algorithmic bytes = passes x 32 B x 2^n per launch; the "
                                  "21-qubit state is L2-resident inside a launch"},
+            "smem": {"achieved_tbs": round(smem_ach, 2), "peak_tbs": round(smem_peak, 2),
+                     "frac": round(smem_ach / smem_peak, 4),
+                     "note": "octet sweeps x 32 B x 2^n (each sweep reads and writes the "
+                             "state in shared memory) over kernel time; peak = 148 SMs x "
+                             "128 B/clk at the sampled SM clock"},
             "fp64": {"achieved_tflops": round(fp64_ach, 3), "peak_tflops": round(fp64_peak, 2),
                      "frac": round(fp64_ach / fp64_peak, 4),
                      "flops_per_launch": info.flops},
