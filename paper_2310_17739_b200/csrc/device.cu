@@ -18,6 +18,7 @@
 #include <nccl.h>  // types only: libnccl is resolved at run time (shard_nccl)
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -254,7 +255,10 @@ struct BlockedParams {
   double* partials;  // 2 * gridDim
   double* record;    // p0 per assertion step
   int* fail;         // [0] flag, [1] step
+  unsigned* bar;     // grid-barrier arrival counter (zeroed before each launch)
   double eps;
+  int debug;         // timing experiments only (NSB_DEBUG_BLOCKED): 1 skip sweeps, 2 skip HBM,
+                     // 4 no CTA rotation
 };
 
 // ---- octet sweeps over a shared-memory batch -------------------------------
@@ -603,9 +607,10 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
   __shared__ uint32_t s_ttab[kMaxPassGates][32];  // per group: thread-address tables
   __shared__ double red[32];
   __shared__ double s_p0;
-  cg::grid_group grid = cg::this_grid();
+  __shared__ uint64_t s_omask;  // physical mask of the pass's out-of-tile qubits
   const int tid = threadIdx.x;
   double carry_p0 = 1.0;  // p0 of the previous pass's assertion (collapse input)
+  unsigned n_bar = 0;     // grid barriers passed in this launch
 
   // Stage pass pi's descriptors in shared memory.  Called for the next pass
   // right before the grid barrier, so the copy overlaps the wait.
@@ -628,6 +633,11 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
     const int n_entries = (sp.group_end - sp.group_begin) * 32;
     for (int e = tid; e < n_entries; e += kPassThreads)
       s_ttab[e >> 5][e & 31] = thread_table_entry(s_groups[e >> 5], e & 31);
+    if (tid == 0) {
+      uint64_t m = 0;
+      for (int b = 0; b < p.n - sp.k; ++b) m |= uint64_t(1) << sp.oq[b];
+      s_omask = m;
+    }
     constexpr int kHi = kTileQubitsMax - kThreadBits;
     if (tid < (1 << kHi)) {
       uint64_t h = 0;
@@ -663,29 +673,43 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
     // contiguous tile range of this CTA, processed in batches of nb tiles
     const int nb = k >= kTileQubitsMax ? 1 : min(1 << (kTileQubitsMax - k), 4);
     const uint64_t per = n_tiles / gridDim.x, extra = n_tiles % gridDim.x;
-    const uint64_t t_begin = blockIdx.x * per + (blockIdx.x < extra ? blockIdx.x : extra);
-    const uint64_t t_end = t_begin + per + (blockIdx.x < extra ? 1 : 0);
-    auto issue_batch = [&](uint64_t t0, double2* buf) {
-      if (!loader) return;
+    // the CTAs holding the extra tiles alternate between passes, so the CTA
+    // that arrived last at a barrier (and stages after arriving) is not
+    // again the slowest in the next pass
+    const unsigned vb = (p.debug & 4) ? blockIdx.x
+                                      : (blockIdx.x + ((pi & 1) ? gridDim.x / 2 : 0)) % gridDim.x;
+    const uint64_t t_begin = vb * per + (vb < extra ? vb : extra);
+    const uint64_t t_end = t_begin + per + (vb < extra ? 1 : 0);
+    // tile t+1's base from tile t's: increment within the out-of-tile mask
+    const uint64_t omask = s_omask;
+    auto next_base = [&](uint64_t b) { return ((b | ~omask) + 1) & omask; };
+    auto issue_batch = [&](uint64_t t0, uint64_t base0, double2* buf) {
+      if (!loader || (p.debug & 2)) return;
+      uint64_t base = base0 | lo;
 #pragma unroll 1
       for (int b = 0; b < nb && t0 + b < t_end; ++b) {
-        const uint64_t base = tile_base(t0 + b) | lo;
         double2* dst = buf;
 #pragma unroll 2
         for (int j = 0; j < n_j; ++j)
           cp_async16(dst + swz(tid + (j << kThreadBits) + (b << k)), p.amps + (base | s_hi[j]));
+        base = next_base(base & omask) | lo;
       }
     };
 
     int cur = 0, pre = 1, spare = 2;  // buffer roles (rotate)
-    if (t_begin < t_end) issue_batch(t_begin, smem);
+    uint64_t bnext = t_begin < t_end ? tile_base(t_begin) : 0;  // base of the batch's first tile
+    if (t_begin < t_end) issue_batch(t_begin, bnext, smem);
     cp_async_commit();
     for (uint64_t t0 = t_begin; t0 < t_end; t0 += nb) {
       double2* tile = smem + cur * kTileAmpsMax;
       const int nvalid = t_end - t0 < uint64_t(nb) ? static_cast<int>(t_end - t0) : nb;
       uint64_t tbase[4];
-      for (int b = 0; b < 4; ++b) tbase[b] = b < nvalid ? tile_base(t0 + b) : 0;
-      if (t0 + nb < t_end) issue_batch(t0 + nb, smem + pre * kTileAmpsMax);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        tbase[b] = b < nvalid ? bnext : 0;
+        if (b < nb) bnext = next_base(bnext);  // ends as the next batch's first base
+      }
+      if (t0 + nb < t_end) issue_batch(t0 + nb, bnext, smem + pre * kTileAmpsMax);
       cp_async_commit();
       cp_async_wait<1>();  // this batch has landed (the next may be in flight)
       if (tid < n_groups) {  // out-of-tile axis parities per (group, tile of the batch)
@@ -720,7 +744,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
         __syncthreads();
       }
 #pragma unroll 1
-      for (int g = 0; g < n_groups; ++g) {
+      for (int g = 0; g < ((p.debug & 1) ? 0 : n_groups); ++g) {
         const GroupDesc& d = s_groups[g];
         double2* out = smem + spare * kTileAmpsMax;
         apply_group(tile, out, k, nvalid, d, s_ops + d.op_begin, s_mats, s_gm[g], s_ttab[g]);
@@ -734,7 +758,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
           __syncwarp();  // the next sweep reads only this warp's amplitudes
       }
       // shared -> global (+ assertion epilogue partial sums)
-      if (loader) {
+      if (loader && !(p.debug & 2)) {
         const int mq = sp.measure_q;
 #pragma unroll 1
         for (int b = 0; b < 4; ++b) {
@@ -764,9 +788,21 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
       const double bs = block_sum(msum, red);
       if (tid == 0) p.partials[(mslot & 1) * gridDim.x + blockIdx.x] = bs;
     }
-    if (pi + 1 < p.pass_end) stage(pi + 1);  // overlaps the barrier wait
+    // split grid barrier: arrive, stage the next pass's descriptors while the
+    // other CTAs finish, then wait (co-residency from the cooperative launch)
     __threadfence();
-    grid.sync();
+    __syncthreads();
+    ++n_bar;
+    if (tid == 0) atomicAdd(p.bar, 1u);
+    if (pi + 1 < p.pass_end) stage(pi + 1);
+    if (tid == 0) {
+      const unsigned target = n_bar * gridDim.x;
+      unsigned seen;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(p.bar) : "memory");
+      } while (seen < target);
+    }
+    __syncthreads();
     if (mq >= 0) {
       if (tid < 32) {
         const double* part = p.partials + (mslot & 1) * gridDim.x;
@@ -780,12 +816,12 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
       carry_p0 = s_p0;
       if (blockIdx.x == 0 && tid == 0) {
         p.record[mslot] = carry_p0;
-        if (carry_p0 < p.eps) {
+        if (carry_p0 < p.eps && !p.debug) {
           p.fail[0] = 1;
           p.fail[1] = mslot;
         }
       }
-      if (carry_p0 < p.eps) return;  // every block saw the same p0
+      if (carry_p0 < p.eps && !p.debug) return;  // every block saw the same p0
     }
   }
 }
@@ -891,6 +927,7 @@ struct nsb_plan {
   DevBuf<double2> mats, dense;
   DevBuf<double> record, partials;
   DevBuf<int> fail;
+  DevBuf<unsigned> bar;
   double last_ms = 0.0;
   int64_t last_launches = 0;
 };
@@ -1107,7 +1144,14 @@ void launch_blocked(nsb_ctx* c, nsb_plan* P, const PassDesc* passes, int pb, int
   bp.partials = P->partials.ptr;
   bp.record = P->record.ptr;
   bp.fail = P->fail.ptr;
+  bp.bar = P->bar.ptr;
+  NSB_CUDA(cudaMemsetAsync(P->bar.ptr, 0, sizeof(unsigned), c->stream));
   bp.eps = eps;
+  static const int debug = [] {
+    const char* e = std::getenv("NSB_DEBUG_BLOCKED");
+    return e ? std::atoi(e) : 0;
+  }();
+  bp.debug = debug;
   void* args[] = {&bp};
   NSB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::k_blocked),
                                        dim3(c->blocked_grid), dim3(kPassThreads), args,
@@ -1349,6 +1393,7 @@ int nsb_plan_create(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const double* 
     P->record.alloc(std::max<int64_t>(H.n_measures, 1));
     P->partials.alloc(2 * size_t(std::max(c->blocked_grid, 1)));
     P->fail.alloc(2);
+    P->bar.alloc(1);
     NSB_CUDA(cudaStreamSynchronize(c->stream));
   });
   if (rc == NSB_OK) *out = P.release();
