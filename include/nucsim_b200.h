@@ -150,6 +150,13 @@ int nsb_branch_probability(nsb_ctx* ctx, int32_t q, int32_t outcome, double* p,
 int nsb_project(nsb_ctx* ctx, int32_t q, int32_t outcome, double prob, nsb_status* st);
 /* |a_i|^2 as re*re + im*im without FMA contraction (sample, engine.py:215) */
 int nsb_probabilities(nsb_ctx* ctx, double* out, nsb_status* st);
+/* Sampling a sharded state (sample, engine.py:207-222, at scale): sums of
+ * |a_i|^2 over consecutive chunks of 2^chunk_log2 local amplitudes
+ * (deterministic fixed-order device reduction; out has 2^(n - chunk_log2)
+ * entries), and |a_i|^2 of one local index range [offset, offset + count). */
+int nsb_prob_chunk_sums(nsb_ctx* ctx, int32_t chunk_log2, double* out, nsb_status* st);
+int nsb_probabilities_range(nsb_ctx* ctx, uint64_t offset, uint64_t count, double* out,
+                            nsb_status* st);
 /* <psi| sum_t c_t P_t |psi> (expectation_pauli, engine.py:225-239).
  * Term t acts as (P_t psi)[j] = (-1)^popcount(j & zmask[t]) psi[j ^ xmask[t]]
  * (xmask: X and Y letters, zmask: Z and Y letters); coeffs are complex

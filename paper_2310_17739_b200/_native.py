@@ -90,6 +90,8 @@ _SIGNATURES = {
     "nsb_branch_probability": (ctypes.c_int, [_P, _I32, _I32, ctypes.POINTER(_D), _ST]),
     "nsb_project": (ctypes.c_int, [_P, _I32, _I32, _D, _ST]),
     "nsb_probabilities": (ctypes.c_int, [_P, _P, _ST]),
+    "nsb_prob_chunk_sums": (ctypes.c_int, [_P, _I32, _P, _ST]),
+    "nsb_probabilities_range": (ctypes.c_int, [_P, ctypes.c_uint64, ctypes.c_uint64, _P, _ST]),
     "nsb_expectation_pauli": (ctypes.c_int, [_P, _P, _P, _P, _I64, ctypes.POINTER(_D),
                                              ctypes.POINTER(_D), _ST]),
     "nsb_plan_create": (ctypes.c_int, [_P, _P, _I64, _P, _P, ctypes.POINTER(_P), _ST]),

@@ -199,6 +199,29 @@ __global__ void k_probabilities(const double2* __restrict__ a, uint64_t n, doubl
 }
 
 // sum_j conj(a_j) (-1)^popc(j & zmask) a_{j ^ xmask}, per-block complex partials
+// Per-chunk sums of |a_i|^2 (chunks of 2^clog amplitudes) for sampling a
+// sharded state (sample, engine.py:207-222): one warp per chunk, each lane a
+// sequential sum of its strided slice, then a fixed shuffle tree, so the sums
+// are deterministic.  Probabilities as in k_probabilities (no contraction).
+__global__ void k_prob_chunk_sums(const double2* __restrict__ a, uint64_t n_chunks, int clog,
+                                  double* __restrict__ out) {
+  const uint64_t lane = threadIdx.x & 31;
+  const uint64_t w0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t len = uint64_t(1) << clog;
+  for (uint64_t c = w0; c < n_chunks; c += nw) {
+    const double2* base = a + (c << clog);
+    double s = 0.0;
+    for (uint64_t i = lane; i < len; i += 32) {
+      const double2 v = base[i];
+      s = __dadd_rn(s, __dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y)));
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
+    if (lane == 0) out[c] = s;
+  }
+}
+
 __global__ void k_pauli_term(const double2* __restrict__ a, uint64_t n, uint64_t xmask,
                              uint64_t zmask, double* __restrict__ partials) {
   __shared__ double red[32];
@@ -1339,6 +1362,39 @@ int nsb_probabilities(nsb_ctx* c, double* out, nsb_status* st) {
         c->amps.ptr, c->n_amps, c->probs.ptr);
     NSB_CUDA(cudaGetLastError());
     copy_d2h(c, out, c->probs.ptr, c->n_amps * sizeof(double));
+  });
+}
+
+int nsb_prob_chunk_sums(nsb_ctx* c, int32_t chunk_log2, double* out, nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    if (!out) throw std::invalid_argument("null output");
+    if (chunk_log2 < 0 || chunk_log2 > c->n) throw std::invalid_argument("bad chunk size");
+    NSB_CUDA(cudaSetDevice(c->device));
+    const uint64_t n_chunks = c->n_amps >> chunk_log2;
+    if (c->probs.count < n_chunks) c->probs.alloc(n_chunks);
+    const uint64_t warps = std::min<uint64_t>(n_chunks, uint64_t(c->sm_count) * 64);
+    dev::k_prob_chunk_sums<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, c->stream>>>(
+        c->amps.ptr, n_chunks, chunk_log2, c->probs.ptr);
+    NSB_CUDA(cudaGetLastError());
+    copy_d2h(c, out, c->probs.ptr, n_chunks * sizeof(double));
+  });
+}
+
+int nsb_probabilities_range(nsb_ctx* c, uint64_t offset, uint64_t count, double* out,
+                            nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    if (!out && count) throw std::invalid_argument("null output");
+    if (offset > c->n_amps || count > c->n_amps - offset)
+      throw std::invalid_argument("range outside the state");
+    if (!count) return;
+    NSB_CUDA(cudaSetDevice(c->device));
+    if (c->probs.count < count) c->probs.alloc(count);
+    dev::k_probabilities<<<grid_for(count, 256, c), 256, 0, c->stream>>>(c->amps.ptr + offset,
+                                                                         count, c->probs.ptr);
+    NSB_CUDA(cudaGetLastError());
+    copy_d2h(c, out, c->probs.ptr, count * sizeof(double));
   });
 }
 

@@ -178,6 +178,71 @@ def schedule(ops: np.ndarray, n: int, g: int, window: int = 4096) -> list[Step]:
     return steps
 
 
+def sample_shard(rank: int, nl: int, draws: np.ndarray, starts: np.ndarray, last: bool,
+                 chunk_sums: np.ndarray, chunk_log2: int, probs_range) -> np.ndarray:
+    """This rank's part of `sample` (engine.py:207-222) on a sharded state.
+
+    The reference draws u * cum[-1] and takes searchsorted(cum, ., "right")
+    on the sequential cumulative sum of |a_i|^2 over the whole state.  Here
+    `starts` are the global cumulative masses before each rank (rank-order
+    sums of the ranks' totals), `chunk_sums` this rank's fixed-order sums
+    over chunks of 2^chunk_log2 local amplitudes.  A draw belongs to the
+    rank whose mass interval holds it; inside the rank the chunk prefix
+    finds its chunk, whose probabilities are fetched (`probs_range(offset,
+    count)`) and summed sequentially from the carried prefix exactly as
+    np.cumsum, then searched with side="right".  With one rank and one chunk
+    this is the reference's arithmetic; otherwise the chunk and rank carries
+    are regrouped sums, so a draw within ~1e-16 (relative) of a cumulative
+    boundary may land on the neighbouring index -- the same caveat as the
+    amplitudes' own rounding.  Returns the global index of
+    every owned draw, -1 elsewhere.
+    """
+    out = np.full(draws.size, -1, np.int64)
+    lo = float(starts[rank])
+    own = draws >= lo
+    if not last:
+        own &= draws < float(starts[rank + 1])
+    if not own.any():
+        return out
+    sums = np.asarray(chunk_sums, np.float64)
+    n_chunks = sums.size
+    clen = 1 << chunk_log2
+    excl = np.empty(n_chunks, np.float64)
+    excl[0] = 0.0
+    if n_chunks > 1:
+        np.cumsum(sums[:-1], out=excl[1:])
+    incl = lo + np.cumsum(sums)          # approximate global chunk ends
+    cache: dict[int, np.ndarray] = {}
+
+    def chunk_cum(c: int, carry: float) -> np.ndarray:
+        p = cache.get(c)
+        if p is None:
+            p = np.empty(clen, np.float64)
+            probs_range(c * clen, clen, p)
+            cache[c] = p
+        return np.cumsum(np.concatenate(([carry], p)))[1:]
+
+    base = rank << nl
+    for j in np.nonzero(own)[0]:
+        x = float(draws[j])
+        c = min(int(np.searchsorted(incl, x, side="right")), n_chunks - 1)
+        carry = lo + excl[c] if c else lo
+        while c > 0 and x < carry:         # regrouped carry overshot: step back
+            c -= 1
+            carry = lo + excl[c] if c else lo
+        local = clen * n_chunks - 1        # past every cumulative value: clip
+        while c < n_chunks:
+            cum = chunk_cum(c, carry)
+            pos = int(np.searchsorted(cum, x, side="right"))
+            if pos < clen:
+                local = c * clen + pos
+                break
+            carry = float(cum[-1])
+            c += 1
+        out[j] = base + local
+    return out
+
+
 def swap_count(steps: list[Step]) -> int:
     return sum(1 for s in steps if s.kind == "swap")
 
@@ -240,6 +305,38 @@ class ShardedState:
         out = ctypes.c_double(0.0)
         self.dev.call("nsb_state_norm2", ctypes.byref(out))
         return float(np.sqrt(self._sum(out.value)))
+
+    def sample(self, shots: int, seed, chunk_log2: int = 13) -> dict[str, int]:
+        """Collective `sample` (engine.py:194-222) of the full n-qubit state:
+        every rank draws the same Philox stream, owns the draws inside its
+        probability mass, locates them from device chunk sums plus one
+        fetched chunk per hit, and the indices are all-gathered; returns the
+        reference's {bitstring: count} on every rank (sample_shard)."""
+        from .engine import _as_rng, bitstring
+        if shots < 0:
+            raise ValueError("shots must be nonnegative")
+        rng = _as_rng(seed)
+        if shots == 0:
+            return {}
+        clog = max(0, min(int(chunk_log2), self.nl))
+        sums = np.empty(1 << (self.nl - clog), np.float64)
+        self.dev.call("nsb_prob_chunk_sums", clog, N.ptr(sums))
+        total_local = float(np.cumsum(sums)[-1])
+        totals = self.allgather([total_local])[:, 0]
+        starts = np.zeros(self.world + 1, np.float64)
+        for r in range(self.world):  # rank order on every rank
+            starts[r + 1] = starts[r] + totals[r]
+        draws = rng.random(shots) * starts[-1]
+
+        def fetch(off, count, out):
+            self.dev.call("nsb_probabilities_range", off, count, N.ptr(out))
+
+        mine = sample_shard(self.rank, self.nl, draws, starts, self.rank == self.world - 1,
+                            sums, clog, fetch)
+        idx = self.allgather(mine.astype(np.float64)).max(axis=0).astype(np.int64)
+        np.clip(idx, 0, (1 << self.n) - 1, out=idx)
+        values, counts = np.unique(idx, return_counts=True)
+        return {bitstring(int(v), self.n): int(c) for v, c in zip(values, counts)}
 
     def reset(self):
         """|0...0>: amplitude 1 on rank 0, zeros elsewhere (on the device)."""

@@ -93,3 +93,36 @@ def run_steps_all(steps, params, payloads, n, g):
             for a in shards:
                 O.project(a, s.local_q, 0, p0)
     return probs, np.concatenate(shards)
+
+
+def chunk_sums(a: np.ndarray, clog: int) -> np.ndarray:
+    """Per-chunk sums of |a_i|^2 (the values only steer the search; any
+    fixed order is valid -- the device uses a warp tree)."""
+    p = a.real ** 2 + a.imag ** 2
+    return p.reshape(-1, 1 << clog).sum(axis=1)
+
+
+def sample_all(shards, nl, shots, seed, clog):
+    """ShardedState.sample for every rank at once (single-process emulation)."""
+    from paper_2310_17739_b200.sharded import sample_shard
+    world = len(shards)
+    sums = [chunk_sums(a, clog) for a in shards]
+    starts = np.zeros(world + 1)
+    for r in range(world):
+        starts[r + 1] = starts[r] + float(np.cumsum(sums[r])[-1])
+    draws = O.as_rng(seed).random(shots) * starts[-1]
+    idx = np.full(shots, -1, np.int64)
+    for r, a in enumerate(shards):
+        p = a.real ** 2 + a.imag ** 2
+
+        def fetch(off, count, out, p=p):
+            out[:] = p[off: off + count]
+
+        got = sample_shard(r, nl, draws, starts, r == world - 1, sums[r], clog, fetch)
+        assert np.all((got < 0) | (idx < 0)), "a draw owned by two ranks"
+        idx = np.maximum(idx, got)
+    assert np.all(idx >= 0), "a draw owned by no rank"
+    n = nl + world.bit_length() - 1
+    np.clip(idx, 0, (1 << n) - 1, out=idx)
+    values, counts = np.unique(idx, return_counts=True)
+    return {O.bitstring(int(v), n): int(c) for v, c in zip(values, counts)}

@@ -36,6 +36,7 @@ def main(out):
         probs, steps = st.run_mma(ops, params, pool)
         shard = st.download()
         norm = st.norm()
+        samples = {clog: st.sample(1024, 2310, chunk_log2=clog) for clog in (4, 13)}
         st.close()
         shards = [None] * dist.get_world_size()
         dist.all_gather_object(shards, shard)
@@ -45,6 +46,8 @@ def main(out):
             res["want_" + tag] = want
             res["gotp_" + tag] = np.asarray(probs)
             res["wantp_" + tag] = np.asarray(want_p)
+            ref = SE.O.sample(res["got_" + tag], n, 1024, 2310)
+            res["samples_ok_" + tag] = np.asarray([samples[c] == ref for c in sorted(samples)])
             print(tag, "swaps", S.swap_count(steps), "norm", norm, flush=True)
     if rank == 0:
         np.savez(out, **res)

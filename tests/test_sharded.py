@@ -98,6 +98,53 @@ def test_schedule_rejects_bad_args():
 
 
 # ---------------------------------------------------------------------------
+# sampling a sharded state (sample_shard) against the reference's sample
+
+
+def _random_state(n, seed, concentrate=False):
+    rng = np.random.default_rng(seed)
+    a = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    if concentrate:  # all mass in the first quarter: ranks with zero mass
+        a[1 << (n - 2):] = 0.0
+    return a / np.linalg.norm(a)
+
+
+@pytest.mark.parametrize("seed", [3, 11, 1234])
+def test_sample_one_rank_one_chunk_is_reference(seed):
+    n = 9
+    a = _random_state(n, seed)
+    assert SE.sample_all([a], n, 2048, seed, n) == SE.O.sample(a, n, 2048, seed)
+
+
+@pytest.mark.parametrize("g,clog", [(0, 0), (0, 4), (1, 3), (2, 0), (2, 5), (3, 2)])
+@pytest.mark.parametrize("concentrate", [False, True])
+def test_sample_shards_match_reference(g, clog, concentrate):
+    n = 10
+    a = _random_state(n, 100 + g + clog, concentrate)
+    nl = n - g
+    shards = [a[r << nl:(r + 1) << nl].copy() for r in range(1 << g)]
+    for seed in (7, 42):
+        assert SE.sample_all(shards, nl, 1024, seed, clog) == SE.O.sample(a, n, 1024, seed)
+
+
+def test_sample_shard_edge_draws():
+    """Draws at 0, inside zero-mass chunks' boundaries and at the total."""
+    from paper_2310_17739_b200.sharded import sample_shard
+    nl = 4
+    p = np.array([0, 0, .25, 0, 0, .25, 0, 0, 0, 0, .5, 0, 0, 0, 0, 0], np.float64)
+    sums = p.reshape(-1, 4).sum(axis=1)
+    starts = np.array([0.0, 1.0])
+
+    def fetch(off, count, out):
+        out[:] = p[off: off + count]
+
+    draws = np.array([0.0, 0.2499, 0.25, 0.5, 0.75, 0.999, 1.0])
+    got = sample_shard(0, nl, draws, starts, True, sums, 2, fetch)
+    want = np.clip(np.searchsorted(np.cumsum(p), draws, side="right"), 0, 15)
+    assert got.tolist() == want.tolist()
+
+
+# ---------------------------------------------------------------------------
 # world_size-2 gloo: one shard per process, real exchanges
 
 
@@ -141,10 +188,30 @@ def _gloo_worker(rank, world, port, n, q):
                     p0 += float(t[0])
                 probs[s.step] = p0
                 SE.O.project(a, s.local_q, 0, p0)
+        # collective sampling (ShardedState.sample with gloo collectives)
+        clog = 3
+        sums = SE.chunk_sums(a, clog)
+        tot = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(tot, torch.tensor([float(np.cumsum(sums)[-1])], dtype=torch.float64))
+        starts = np.zeros(world + 1)
+        for r in range(world):
+            starts[r + 1] = starts[r] + float(tot[r][0])
+        draws = SE.O.as_rng(99).random(512) * starts[-1]
+        pr = a.real ** 2 + a.imag ** 2
+
+        def fetch(off, count, out):
+            out[:] = pr[off: off + count]
+
+        mine = S.sample_shard(rank, nl, draws, starts, rank == world - 1, sums, clog, fetch)
+        parts = [torch.zeros(512, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(mine))
+        idx = torch.stack(parts).max(dim=0).values.numpy()
+        values, counts = np.unique(idx, return_counts=True)
+        samples = {SE.O.bitstring(int(v), n): int(c) for v, c in zip(values, counts)}
         shards = [None] * world
         dist.all_gather_object(shards, a)
         if rank == 0:
-            q.put((probs, np.concatenate(shards)))
+            q.put((probs, np.concatenate(shards), samples))
     finally:
         dist.destroy_process_group()
 
@@ -159,12 +226,13 @@ def test_gloo_world2_matches_full_state(world):
     procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, n, q)) for r in range(world)]
     for p in procs:
         p.start()
-    probs, got = q.get(timeout=240)
+    probs, got, samples = q.get(timeout=240)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     assert [probs[k] for k in sorted(probs)] == pytest.approx(want_p, rel=1e-10, abs=1e-14)
     _close(got, want)
+    assert samples == SE.O.sample(got, n, 512, 99)
 
 
 # ---------------------------------------------------------------------------
@@ -194,3 +262,4 @@ def test_nccl_sharded_matches_oracle(tmp_path):
             tag = name[5:]
             _close(d["got_" + tag], d[name])
             assert np.allclose(d["gotp_" + tag], d["wantp_" + tag], rtol=1e-10, atol=1e-14)
+            assert d["samples_ok_" + tag].all(), tag  # ShardedState.sample == reference sample
