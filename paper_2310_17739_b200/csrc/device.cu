@@ -1698,12 +1698,16 @@ int nsb_shard_allgather(nsb_ctx* c, const double* in, int32_t count, double* out
                         nsb_status* st) {
   return guarded(st, [&] {
     if (!c || !c->comm) throw std::invalid_argument("no communicator (nsb_comm_init)");
-    if (!in || !out || count < 1 || count > 64) throw std::invalid_argument("bad gather size");
+    if (!in || !out || count < 1) throw std::invalid_argument("bad gather size");
     NSB_CUDA(cudaSetDevice(c->device));
-    if (c->scratch.count < size_t(2 * dev::kReduceBlocks + 8 + 64 * (c->nranks + 1)))
-      throw std::invalid_argument("gather exceeds scratch");
+    const size_t need = size_t(count) * (c->nranks + 1);
+    DevBuf<double> big;  // large gathers (sampled indices): a temporary buffer
     double* d_in = c->scratch.ptr + 2 * dev::kReduceBlocks + 8;
-    double* d_out = d_in + 64;
+    if (count > 64 || c->scratch.count < size_t(2 * dev::kReduceBlocks + 8) + need) {
+      big.alloc(need);
+      d_in = big.ptr;
+    }
+    double* d_out = d_in + count;
     NSB_CUDA(cudaMemcpyAsync(d_in, in, count * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     NSB_NCCL(shard_nccl().all_gather(d_in, d_out, count, ncclFloat64,
                                      static_cast<ncclComm_t>(c->comm), c->stream));
