@@ -254,6 +254,10 @@ def run_sharded(args, rank, world, local):
     norm = st.norm()
     e2e_s = time.perf_counter() - t0
     p2.close()
+    barrier()
+    t0 = time.perf_counter()
+    smp = st.sample(1024, 2310)  # collective sampling of the full 2^n state (sharded.py)
+    sample_s = time.perf_counter() - t0
     nl = st.nl
     pk = peaks()
     gate_bytes = tot["n_passes"] * 32 * (1 << nl)
@@ -288,6 +292,9 @@ def run_sharded(args, rank, world, local):
                     "h2d_bytes_per_step": int(fops.nbytes + wl.params.nbytes + pool.nbytes),
                     "d2h_bytes_per_step": 8, "s_per_step": round(e2e_s, 4),
                     "note": "schedule + plan upload from host op arrays + run + norm read-back"},
+            "sampling": {"shots": 1024, "s": round(sample_s, 4), "distinct": len(smp),
+                         "note": "ShardedState.sample after the last run: device chunk sums, "
+                                 "one fetched chunk per hit, indices all-gathered"},
             "norm": norm, "gpu_launches": None, "clocks": clk,
             "cpu_baseline": {"value": None, "unit": UNIT, "cores": 1, "kind": "port",
                              "sample": f"infeasible: the reference holds 2 x 2^{n} x 16 B "
