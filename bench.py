@@ -59,6 +59,28 @@ def peaks() -> dict:
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback"}
 
 
+def l2_copy_gbs(state_bytes: int, reps: int = 200) -> float | None:
+    """Measured L2-resident copy bandwidth (read + write bytes per second) for
+    a buffer of the state's size: the roof for a state that stays in the
+    126 MB L2 inside a launch.  None if the source and
+    destination together would not fit in half the L2."""
+    import torch
+    if 2 * state_bytes > 64 << 20:
+        return None
+    a = torch.ones(state_bytes // 8, dtype=torch.float64, device="cuda")
+    b = torch.empty_like(a)
+    for _ in range(20):
+        b.copy_(a)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        b.copy_(a)
+    e1.record()
+    torch.cuda.synchronize()
+    return 2 * state_bytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -391,6 +413,7 @@ def run_ours(args, rank, world, local):
     fp64_ach = info.flops / kernel_s / 1e12
     smem_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
     smem_ach = info.n_sweeps * 32 * (1 << n) / kernel_s / 1e12
+    l2_gbs = l2_copy_gbs(16 << n)
     profile = ROOT / "profiles" / "r01_dram_bytes.json"
     traffic = None
     if profile.exists():
@@ -418,6 +441,12 @@ def run_ours(args, rank, world, local):
                          "traffic": traffic, "peak_source": pk["source"],
                          "note": "algorithmic bytes = passes x 32 B x 2^n per launch; the "
                                  "21-qubit state is L2-resident inside a launch"},
+            "l2": None if l2_gbs is None else {
+                "achieved_gbs": round(achieved, 1), "copy_gbs_measured": round(l2_gbs, 1),
+                "frac": round(achieved / l2_gbs, 4),
+                "note": "same algorithmic bytes over the measured L2-resident copy bandwidth "
+                        "(torch copy of a state-sized buffer, 200 reps): the state never "
+                        "leaves L2 within a launch"},
             "smem": {"achieved_tbs": round(smem_ach, 2), "peak_tbs": round(smem_peak, 2),
                      "frac": round(smem_ach / smem_peak, 4),
                      "note": "octet sweeps x 32 B x 2^n (each sweep reads and writes the "

@@ -750,12 +750,13 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
       __syncthreads();
       if (sp.collapse_q >= 0) {  // pending collapse (engine.py:164-167)
         const int cq = sp.collapse_q;
+        uint64_t bb = tbase[0];
         if (loader)
 #pragma unroll 1
-          for (int b = 0; b < 4; ++b)
+          for (int b = 0; b < 4; ++b, bb = next_base(bb))
 #pragma unroll 1
             for (int j = 0; j < n_j && b < nvalid; ++j) {
-              const uint64_t g = tbase[b] | lo | s_hi[j];
+              const uint64_t g = bb | lo | s_hi[j];
               double2& v = tile[swz((b << k) + tid + (j << kThreadBits))];
               if ((g >> cq) & 1) {
                 v = make_double2(0.0, 0.0);
@@ -769,13 +770,14 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
 #pragma unroll 1
       for (int g = 0; g < ((p.debug & 1) ? 0 : n_groups); ++g) {
         const GroupDesc& d = s_groups[g];
+        const bool cta_sync = d.sync;  // read before the sweep: no load latency after it
         double2* out = smem + spare * kTileAmpsMax;
         apply_group(tile, out, k, nvalid, d, s_ops + d.op_begin, s_mats, s_gm[g], s_ttab[g]);
         const int tmp = cur;
         cur = spare;
         spare = tmp;
         tile = out;
-        if (d.sync)
+        if (cta_sync)
           __syncthreads();
         else
           __syncwarp();  // the next sweep reads only this warp's amplitudes
@@ -783,10 +785,11 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
       // shared -> global (+ assertion epilogue partial sums)
       if (loader && !(p.debug & 2)) {
         const int mq = sp.measure_q;
+        uint64_t bb = tbase[0];  // advanced in registers (no dynamic index into tbase)
 #pragma unroll 1
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < 4; ++b, bb = next_base(bb)) {
           if (b >= nvalid) break;
-          const uint64_t base = tbase[b] | lo;
+          const uint64_t base = bb | lo;
 #pragma unroll 2
           for (int j = 0; j < n_j; ++j) {
             const uint64_t g = base | s_hi[j];
@@ -821,9 +824,11 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
     if (tid == 0) {
       const unsigned target = n_bar * gridDim.x;
       unsigned seen;
+      // relaxed polling (no L1 invalidation per iteration), one acquire fence after
       do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(p.bar) : "memory");
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(p.bar) : "memory");
       } while (seen < target);
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
     __syncthreads();
     if (mq >= 0) {
