@@ -196,7 +196,7 @@ void nsb_plan_destroy(nsb_plan* plan);
  * diagonal 1q, dense 2q, <=2 nnz/row 2q, monomial 2q, diagonal 2q, exact CX
  * (two orientations), two-block 2x2 patterns (three pairings), exact SWAP,
  * read-map-only permutation sweeps. */
-#define NSB_N_CLASSES 13
+#define NSB_N_CLASSES 16
 int nsb_plan_analyze(const nsb_op* ops, int64_t n_ops, const double* params,
                      const double* payloads, int32_t n_qubits, nsb_plan_info* info,
                      int64_t* class_counts, nsb_status* st);

@@ -305,6 +305,16 @@ __device__ __forceinline__ void mix2(double2& x, double2& y, const double2 m0, c
   y = oy;
 }
 
+// (x, y) <- [[a0, a1], [a2, a3]] (x, y) with real a: the imaginary parts of
+// the payload are exact zeros (kPair*r), two multiply-adds per output part
+__device__ __forceinline__ void mix2r(double2& x, double2& y, const double a0, const double a1,
+                                      const double a2, const double a3) {
+  const double2 ox = make_double2(fma(a0, x.x, a1 * y.x), fma(a0, x.y, a1 * y.y));
+  const double2 oy = make_double2(fma(a2, x.x, a3 * y.x), fma(a2, x.y, a3 * y.y));
+  x = ox;
+  y = oy;
+}
+
 __device__ __forceinline__ double2 pick(const double2 x0, const double2 x1, const double2 x2,
                                         const double2 x3, int c) {
   double2 r = x0;
@@ -367,6 +377,23 @@ __device__ __forceinline__ void gate2(double2 (&xs)[NO][8], const GateOp o,
         for (int h = 0; h <= H; h += H) {
           mix2(xs[q][h], xs[q][h | u1], m0, m1, m2, m3);
           mix2(xs[q][h | u2], xs[q][h | u3], n0, n1, n2, n3);
+        }
+      break;
+    }
+    case kPairQr:
+    case kPairPr:
+    case kPairXr: {
+      constexpr int u1 = C == kPairQr ? B : (C == kPairPr ? A : A | B);
+      constexpr int u2 = C == kPairQr ? A : (C == kPairPr ? B : A);
+      constexpr int u3 = C == kPairQr ? A | B : (C == kPairPr ? A | B : B);
+      const double a0 = m[0].x, a1 = m[1].x, a2 = m[2].x, a3 = m[3].x;
+      const double b0 = m[4].x, b1 = m[5].x, b2 = m[6].x, b3 = m[7].x;
+#pragma unroll
+      for (int q = 0; q < NO; ++q)
+#pragma unroll
+        for (int h = 0; h <= H; h += H) {
+          mix2r(xs[q][h], xs[q][h | u1], a0, a1, a2, a3);
+          mix2r(xs[q][h | u2], xs[q][h | u3], b0, b1, b2, b3);
         }
       break;
     }
@@ -572,7 +599,9 @@ __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
   NSB_G2(P, Q, PAT, kMono2) NSB_G2(P, Q, PAT, kDiag2)                    \
   NSB_G2(P, Q, PAT, kCX01) NSB_G2(P, Q, PAT, kCX10)                      \
   NSB_G2(P, Q, PAT, kPairQ) NSB_G2(P, Q, PAT, kPairP)                    \
-  NSB_G2(P, Q, PAT, kPairX) NSB_G2(P, Q, PAT, kSwap)
+  NSB_G2(P, Q, PAT, kPairX) NSB_G2(P, Q, PAT, kSwap)                    \
+  NSB_G2(P, Q, PAT, kPairQr) NSB_G2(P, Q, PAT, kPairPr)                  \
+  NSB_G2(P, Q, PAT, kPairXr)
 #define NSB_G1(P, PAT, C)                                                \
   case PAT * 16 + C:                                                     \
     gate1<P, C, NO>(x, o, m);                                            \

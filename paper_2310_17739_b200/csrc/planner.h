@@ -57,7 +57,10 @@ enum GateClass : uint8_t {
   kPairX = 10,    // 2x2 blocks on members (0,3) and (1,2)                (8)
   kSwap = 11,     // exact SWAP: swaps members 1,2                        (0)
   kPermute = 12,  // identity sweep that only applies its read map      (0)
-  kNumClasses = 13
+  kPairQr = 13,   // kPairQ with real entries (imaginary parts exactly 0)  (8)
+  kPairPr = 14,   // kPairP, real                                          (8)
+  kPairXr = 15,   // kPairX, real                                          (8)
+  kNumClasses = 16
 };
 
 // A gate on logical qubits (a, b) acts on physical cosets of span{ma, mb}

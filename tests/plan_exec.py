@@ -29,7 +29,7 @@ THREAD_BITS = 7  # kThreadBits
 THREADS = 1 << THREAD_BITS  # kPassThreads
 TILE_MAX = 11  # kTileQubitsMax
 (DENSE1, DIAG1, DENSE2, SPARSE2, MONO2, DIAG2, CX01, CX10, PAIRQ, PAIRP, PAIRX, SWAP,
- PERMUTE) = range(13)
+ PERMUTE, PAIRQR, PAIRPR, PAIRXR) = range(16)
 PATTERNS = {0: (0, 1), 1: (0, 2), 2: (1, 2), 3: (0,), 4: (1,), 5: (2,)}
 
 
@@ -115,9 +115,10 @@ def _gate(x, op, m):
         if c in (CX01, CX10, SWAP):
             s, t = {CX01: (1, 3), CX10: (2, 3), SWAP: (1, 2)}[c]
             out[s], out[t] = v[t], v[s]
-        elif c in (PAIRQ, PAIRP, PAIRX):
+        elif c in (PAIRQ, PAIRP, PAIRX, PAIRQR, PAIRPR, PAIRXR):
             (u0, u1), (u2, u3) = {PAIRQ: ((0, 2), (1, 3)), PAIRP: ((0, 1), (2, 3)),
-                                  PAIRX: ((0, 3), (1, 2))}[c]
+                                  PAIRX: ((0, 3), (1, 2)), PAIRQR: ((0, 2), (1, 3)),
+                                  PAIRPR: ((0, 1), (2, 3)), PAIRXR: ((0, 3), (1, 2))}[c]
             out[u0], out[u1] = _mix2(v[u0], v[u1], m[:4])
             out[u2], out[u3] = _mix2(v[u2], v[u3], m[4:8])
         elif c == DIAG2:
