@@ -428,6 +428,7 @@ def run_ours(args, rank, world, local):
                        "passes": info.n_passes,
                        "device_gate_ops": info.n_device_gates,
                        "octet_sweeps": info.n_sweeps,
+                       "group_fused_ops": info.n_fused_group_ops,
                        "frame_absorbed_gates": info.n_frame_gates,
                        "frame_flush_gates": info.n_flush_gates,
                        "gates_per_pass": round(info.n_gates / max(info.n_passes, 1), 2),

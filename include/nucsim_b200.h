@@ -182,6 +182,7 @@ typedef struct nsb_plan_info {
   int64_t n_flush_gates; /* physical CX emitted to flush the frame */
   int64_t n_device_gates;/* gate ops executed on the device per run */
   int64_t n_sweeps;      /* shared-memory octet sweeps (gate groups) per run */
+  int64_t n_fused_group_ops; /* gate ops merged away by group fusion (whole-octet ops) */
 } nsb_plan_info;
 
 /* ops: the executable part of the circuit (sampling block already removed,

@@ -49,7 +49,8 @@ class PlanInfo(ctypes.Structure):
                 ("n_segments", ctypes.c_int64), ("flops", ctypes.c_int64),
                 ("tile_qubits", ctypes.c_int64), ("n_items", ctypes.c_int64),
                 ("n_frame_gates", ctypes.c_int64), ("n_flush_gates", ctypes.c_int64),
-                ("n_device_gates", ctypes.c_int64), ("n_sweeps", ctypes.c_int64)]
+                ("n_device_gates", ctypes.c_int64), ("n_sweeps", ctypes.c_int64),
+                ("n_fused_group_ops", ctypes.c_int64)]
 
 
 class PlanView(ctypes.Structure):

@@ -520,6 +520,33 @@ __device__ __forceinline__ void gate1(double2 (&xs)[NO][8], const GateOp,
   }
 }
 
+// Whole-octet ops (planner group fusion, planner.h kPatT* / kPatAll).
+// 2x2 on axis T with one block per value of the other two axes (L0 lower).
+template <int T, int NO>
+__device__ __forceinline__ void gate_octet_axis(double2 (&xs)[NO][8],
+                                                const double2* __restrict__ m) {
+  constexpr int A = 1 << T;
+  constexpr int L0 = T == 0 ? 2 : 1, L1 = T == 2 ? 2 : 4;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const int c = ((b & 1) ? L0 : 0) | ((b & 2) ? L1 : 0);
+    const double2 m0 = m[4 * b], m1 = m[4 * b + 1], m2 = m[4 * b + 2], m3 = m[4 * b + 3];
+#pragma unroll
+    for (int q = 0; q < NO; ++q) mix2(xs[q][c], xs[q][c | A], m0, m1, m2, m3);
+  }
+}
+
+template <int NO>
+__device__ __forceinline__ void gate_octet_diag(double2 (&xs)[NO][8],
+                                                const double2* __restrict__ m) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const double2 d = m[c];
+#pragma unroll
+    for (int q = 0; q < NO; ++q) xs[q][c] = cmul(d, xs[q][c]);
+  }
+}
+
 // Per pass, the thread part of every group's octet address is tabulated:
 // entry e of table 0 (table 1) is the XOR of the swizzled offsets of thread
 // bits 0..3 (4..7) set in e -- store side in bits 0..15, load side (through
@@ -613,6 +640,17 @@ __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
       NSB_G1(0, kPat0, kDense1) NSB_G1(0, kPat0, kDiag1)
       NSB_G1(1, kPat1, kDense1) NSB_G1(1, kPat1, kDiag1)
       NSB_G1(2, kPat2, kDense1) NSB_G1(2, kPat2, kDiag1)
+#define NSB_GT(T)                                                        \
+  case (kPatT0 + T) * 16 + kDense1:                                      \
+    gate_octet_axis<T, NO>(x, m);                                        \
+    if (last) store();                                                   \
+    break;
+      NSB_GT(0) NSB_GT(1) NSB_GT(2)
+      case kPatAll * 16 + kDiag1:
+        gate_octet_diag<NO>(x, m);
+        if (last) store();
+        break;
+#undef NSB_GT
 #undef NSB_G1
 #undef NSB_G2ALL
 #undef NSB_G2

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <complex>
 #include <atomic>
 #include <exception>
 #include <thread>
@@ -394,6 +395,137 @@ void swap_packed_slots(uint8_t& cls, double* v, uint16_t& cols) {
   }
 }
 
+// ---- group fusion ----------------------------------------------------------
+// A group's gates act on the eight octet registers (register index = the
+// octet's logical axis bits).  apply_octet mirrors gate1 / gate2 of
+// csrc/device.cu on complex registers; fuse_group multiplies the group's
+// gates into one 8x8 matrix and, when that product is an axis-targeted
+// block op or a diagonal, replaces the gates by ONE whole-octet op
+// (kPatT* / kPatAll): one dispatch, no intermediate register copies, and
+// for the common (diagonal, two-block) pairs of deep circuits 8 instead of
+// 12 multiply-adds per amplitude.  The product is rounded once per entry
+// (within the 1e-10 parity bound; components below half an ulp of the
+// largest are zeroed as in pack_matrix).
+using cplx = std::complex<double>;
+
+void apply_octet(const GateOp& op, const double* m2, cplx* x) {
+  auto M = [&](int i) { return cplx(m2[2 * i], m2[2 * i + 1]); };
+  auto mix = [&](int i, int j, int e) {
+    const cplx a = x[i], b = x[j];
+    x[i] = M(e) * a + M(e + 1) * b;
+    x[j] = M(e + 2) * a + M(e + 3) * b;
+  };
+  const int c = op.cls;
+  if (op.pat >= kPat0 && op.pat <= kPat2) {
+    const int A = 1 << (op.pat - kPat0);
+    for (int b = 0; b < 8; ++b) {
+      if (b & A) continue;
+      if (c == kDiag1) {
+        x[b] *= M(0);
+        x[b | A] *= M(1);
+      } else {
+        mix(b, b | A, 0);
+      }
+    }
+    return;
+  }
+  static const int kAx[3][2] = {{0, 1}, {0, 2}, {1, 2}};
+  const int P = kAx[op.pat][0], Q = kAx[op.pat][1], R = 3 - P - Q;
+  const int A = 1 << P, B = 1 << Q, H = 1 << R;
+  for (int h = 0; h <= H; h += H) {
+    const int idx[4] = {h, h | A, h | B, h | A | B};
+    cplx v[4], out[4];
+    for (int s = 0; s < 4; ++s) out[s] = v[s] = x[idx[s]];
+    switch (c) {
+      case kCX01: std::swap(out[1], out[3]); break;
+      case kCX10: std::swap(out[2], out[3]); break;
+      case kSwap: std::swap(out[1], out[2]); break;
+      case kPermute: break;
+      case kPairQ: case kPairP: case kPairX: case kPairQr: case kPairPr: case kPairXr: {
+        const int k = (c == kPairQ || c == kPairQr) ? 0 : (c == kPairP || c == kPairPr) ? 1 : 2;
+        static const int kU[3][4] = {{0, 2, 1, 3}, {0, 1, 2, 3}, {0, 3, 1, 2}};
+        const int* u = kU[k];
+        out[u[0]] = M(0) * v[u[0]] + M(1) * v[u[1]];
+        out[u[1]] = M(2) * v[u[0]] + M(3) * v[u[1]];
+        out[u[2]] = M(4) * v[u[2]] + M(5) * v[u[3]];
+        out[u[3]] = M(6) * v[u[2]] + M(7) * v[u[3]];
+        break;
+      }
+      case kDiag2:
+        for (int s = 0; s < 4; ++s) out[s] = M(s) * v[s];
+        break;
+      case kMono2:
+        for (int s = 0; s < 4; ++s) out[s] = M(s) * v[(op.cols >> (2 * s)) & 3];
+        break;
+      case kSparse2:
+        for (int s = 0; s < 4; ++s)
+          out[s] = M(2 * s) * v[(op.cols >> (4 * s)) & 3] +
+                   M(2 * s + 1) * v[(op.cols >> (4 * s + 2)) & 3];
+        break;
+      default:  // kDense2
+        for (int s = 0; s < 4; ++s)
+          out[s] = M(4 * s) * v[0] + M(4 * s + 1) * v[1] + M(4 * s + 2) * v[2] + M(4 * s + 3) * v[3];
+        break;
+    }
+    for (int s = 0; s < 4; ++s) x[idx[s]] = out[s];
+  }
+}
+
+// The fused replacement of a group's ops (op + packed values), or false.
+bool fuse_group(const std::vector<GateOp>& ops, const std::vector<double>& mats, GateOp& fused,
+                std::vector<double>& packed) {
+  if (ops.size() < 2) return false;
+  for (const GateOp& op : ops)
+    if (op.pat > kPat2) return false;
+  cplx Mx[8][8];
+  for (int j = 0; j < 8; ++j) {
+    cplx x[8];
+    for (int i = 0; i < 8; ++i) x[i] = i == j ? 1.0 : 0.0;
+    for (const GateOp& op : ops) apply_octet(op, mats.data() + 2 * op.mat, x);
+    for (int i = 0; i < 8; ++i) Mx[i][j] = x[i];
+  }
+  double mx = 0.0;
+  for (auto& row : Mx)
+    for (const cplx& v : row) mx = std::max({mx, std::fabs(v.real()), std::fabs(v.imag())});
+  const double thr = std::ldexp(mx, -53);
+  uint8_t reach = 0;  // bit d: some nonzero entry couples registers r, r ^ d
+  for (int r = 0; r < 8; ++r)
+    for (int c = 0; c < 8; ++c) {
+      cplx& v = Mx[r][c];
+      v = cplx(std::fabs(v.real()) <= thr ? 0.0 : v.real(), std::fabs(v.imag()) <= thr ? 0.0 : v.imag());
+      if (v != cplx(0.0, 0.0)) reach |= static_cast<uint8_t>(1u << (r ^ c));
+    }
+  packed.clear();
+  auto put = [&](const cplx& v) {
+    packed.push_back(v.real());
+    packed.push_back(v.imag());
+  };
+  fused = GateOp{};
+  if ((reach & ~1u) == 0) {
+    for (int c = 0; c < 8; ++c) put(Mx[c][c]);
+    fused.cls = kDiag1;
+    fused.pat = kPatAll;
+  } else {
+    int t = -1;
+    for (int a = 0; a < 3; ++a)
+      if ((reach & ~(1u | (1u << (1 << a)))) == 0) t = a;
+    if (t < 0) return false;
+    const int T = 1 << t;
+    const int L0 = t == 0 ? 2 : 1, L1 = t == 2 ? 2 : 4;  // the other two axes
+    for (int b = 0; b < 4; ++b) {
+      const int h = ((b & 1) ? L0 : 0) | ((b & 2) ? L1 : 0);
+      put(Mx[h][h]);
+      put(Mx[h][h | T]);
+      put(Mx[h | T][h]);
+      put(Mx[h | T][h | T]);
+    }
+    fused.cls = kDense1;
+    fused.pat = static_cast<uint8_t>(kPatT0 + t);
+  }
+  fused.kind = static_cast<uint8_t>(fused.pat * 16 + fused.cls);
+  return true;
+}
+
 struct Axis {
   uint32_t m = 0;     // tile-local physical mask
   uint32_t rin = 0;   // tile-local part of the dual row
@@ -615,6 +747,7 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
     n_folded_gates += H.n_folded_gates;
     this->n_ops += H.n_ops;
     n_warp_syncs += H.n_warp_syncs;
+    n_fused_group_ops += H.n_fused_group_ops;
     flops += H.flops;
     for (int c = 0; c < kNumClasses; ++c) class_count[c] += H.class_count[c];
     if (s < marks.size()) {
@@ -640,6 +773,7 @@ void HostPlan::build_serial(const nsb_op* ops, int64_t n_ops, const double* para
   tile_qubits = k;
   low_qubits = n <= kL2ResidentQubits ? 1 : kLowQubits;
   if (const char* e = std::getenv("NSB_LOW_QUBITS")) low_qubits = std::atoi(e);  // tuning
+  if (const char* e = std::getenv("NSB_NO_GROUP_FUSION")) fuse_groups = std::atoi(e) == 0;
   blocked = n >= 6;
   std::vector<PhysGate> run;
   uint64_t col[64];  // frame: physical mask of logical bit j (M e_j)
@@ -964,6 +1098,24 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
         }
       }
     }
+    // group fusion, within the pass's matrix budget (kMaxPassMats)
+    if (fuse_groups) {
+      size_t used = 0;
+      for (const OpenGroup& H : closed) used += H.mats.size() / 2;
+      for (OpenGroup& H : closed) {
+        GateOp f;
+        std::vector<double> pk;
+        if (!fuse_group(H.ops, H.mats, f, pk)) continue;
+        const size_t after = used - H.mats.size() / 2 + pk.size() / 2;
+        if (after > size_t(kMaxPassMats)) continue;
+        used = after;
+        n_fused_group_ops += static_cast<int64_t>(H.ops.size()) - 1;
+        n_ops -= static_cast<int64_t>(H.ops.size()) - 1;
+        f.mat = 0;
+        H.ops.assign(1, f);
+        H.mats = std::move(pk);
+      }
+    }
     for (size_t g = 0; g < closed.size(); ++g) {
       OpenGroup& H = closed[g];
       GroupDesc d{};
@@ -1073,6 +1225,7 @@ void fill_info(const nsb::HostPlan& H, nsb_plan_info* info) {
   info->n_flush_gates = H.n_flush_gates;
   info->n_device_gates = H.n_ops;
   info->n_sweeps = static_cast<int64_t>(H.groups.size());
+  info->n_fused_group_ops = H.n_fused_group_ops;
 }
 }  // namespace
 

@@ -108,7 +108,12 @@ static_assert(sizeof(GroupDesc) == 80, "GroupDesc layout");
 // the payload when needed).
 enum AxisPattern : uint8_t {
   kPat01 = 0, kPat02 = 1, kPat12 = 2,  // 2q: (slot0 axis, slot1 axis)
-  kPat0 = 3, kPat1 = 4, kPat2 = 5      // 1q: axis
+  kPat0 = 3, kPat1 = 4, kPat2 = 5,     // 1q: axis
+  // Whole-octet ops, the product of a group's gates (planner group fusion):
+  // kPatT0..T2 with class kDense1 = a 2x2 on axis t whose matrix depends on
+  // the other two axes (four blocks, block index = their bits, lower axis
+  // first; 16 complex values); kPatAll with class kDiag1 = 8x8 diagonal (8).
+  kPatT0 = 6, kPatT1 = 7, kPatT2 = 8, kPatAll = 9
 };
 struct GateOp {           // 8 bytes
   int16_t mat;            // offset (complex elements) in the pass's matrix block

@@ -74,6 +74,8 @@ struct HostPlan {
   int64_t n_folded_gates = 0;   // physical CXs folded into read maps
   int64_t n_ops = 0;            // gate ops executed on the device (all groups)
   int64_t n_warp_syncs = 0;     // sweeps followed by __syncwarp instead of a CTA barrier
+  int64_t n_fused_group_ops = 0;  // gate ops removed by group fusion (fuse_group)
+  bool fuse_groups = true;      // NSB_NO_GROUP_FUSION=1 turns group fusion off
   int64_t flops = 0;
   int64_t class_count[kNumClasses] = {};
 

@@ -31,6 +31,7 @@ TILE_MAX = 11  # kTileQubitsMax
 (DENSE1, DIAG1, DENSE2, SPARSE2, MONO2, DIAG2, CX01, CX10, PAIRQ, PAIRP, PAIRX, SWAP,
  PERMUTE, PAIRQR, PAIRPR, PAIRXR) = range(16)
 PATTERNS = {0: (0, 1), 1: (0, 2), 2: (1, 2), 3: (0,), 4: (1,), 5: (2,)}
+PAT_T, PAT_ALL = (6, 7, 8), 9  # whole-octet ops (planner.h kPatT0..T2, kPatAll)
 
 
 class HostPlan:
@@ -93,8 +94,21 @@ def _swz(l):
 def _gate(x, op, m):
     """One GateOp on the octet registers x[0..7] (arrays over threads),
     as gate2 / gate1 in csrc/device.cu."""
-    axes = PATTERNS[int(op["pat"])]
+    pat = int(op["pat"])
     c = int(op["cls"])
+    if pat == PAT_ALL:  # whole-octet diagonal (planner group fusion)
+        for r in range(8):
+            x[r] = m[r] * x[r]
+        return
+    if pat in PAT_T:  # 2x2 on axis t, one block per value of the other two axes
+        t = pat - PAT_T[0]
+        A = 1 << t
+        L0, L1 = (2 if t == 0 else 1), (2 if t == 2 else 4)
+        for b in range(4):
+            h = (L0 if b & 1 else 0) | (L1 if b & 2 else 0)
+            x[h], x[h | A] = _mix2(x[h], x[h | A], m[4 * b: 4 * b + 4])
+        return
+    axes = PATTERNS[pat]
     if len(axes) == 1:
         A = 1 << axes[0]
         for base in range(8):

@@ -86,3 +86,26 @@ def test_parallel_planning_matches_serial(monkeypatch):
     monkeypatch.setenv("NSB_PLAN_SERIAL", "1")
     ser = view()
     assert par == ser
+
+
+@pytest.mark.parametrize("fusion", [True, False])
+def test_group_fusion_whole_octet_ops(monkeypatch, fusion):
+    """Planner group fusion (fuse_group): on a deep-circuit-shaped workload
+    the product of a group's gates replaces them by one whole-octet op
+    (axis-targeted blocks or an octet diagonal); the program must still
+    reproduce the full-state oracle."""
+    import shard_exec as SE
+    from paper_2310_17739_b200 import workloads as W
+    if not fusion:
+        monkeypatch.setenv("NSB_NO_GROUP_FUSION", "1")
+    wl = W.filter_workload(9, trotter=1, n_steps=2, n_scatter=4, trial="10" * 5)
+    fops, pool, _ = W.fuse_packed(wl.ops, wl.params, wl.payloads)
+    exe = wl.executable(fops)
+    n = wl.n_qubits
+    plan = PE.HostPlan(exe, wl.params, pool, n, 148)
+    whole = int((plan.ops["pat"] >= 6).sum())
+    assert (whole > 0) == fusion
+    want_p, want = SE.full_mma(exe, wl.params, pool, n)
+    probs, state = PE.run_mma(plan)
+    assert probs == pytest.approx(want_p, abs=1e-12)
+    assert np.linalg.norm(state - want) / np.linalg.norm(want) < 1e-10
