@@ -17,6 +17,8 @@ import numpy as np
 from .errors import FilterAssertionError, ProjectionError, ResourceLimitError
 
 LIB_PATH = Path(__file__).resolve().parent / "libnucsim_b200.so"
+if os.environ.get("NSB_LIB_VARIANT"):  # tuning experiments: an in-tree build variant
+    LIB_PATH = LIB_PATH.with_name(f"libnucsim_b200_{os.environ['NSB_LIB_VARIANT']}.so")
 
 NSB_OK, NSB_EINVAL, NSB_EASSERT, NSB_EPROJECT, NSB_ERESOURCE, NSB_EDEVICE = range(6)
 OP_GATE, OP_MEASURE, OP_RESET, OP_BARRIER = range(4)

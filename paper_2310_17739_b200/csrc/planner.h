@@ -29,10 +29,13 @@ namespace nsb {
 
 constexpr int kTileQubitsMax = 11;               // 2048 amplitudes = 32 KiB per buffer
 constexpr int kTileAmpsMax = 1 << kTileQubitsMax;
-constexpr int kThreadBits = 7;
-constexpr int kPassThreads = 1 << kThreadBits;  // 4 warps per CTA, two CTAs per SM
-constexpr int kOctets = 2;                       // octets per thread per sweep
-constexpr int kIndexBits = kThreadBits + 1;      // octet-index bits of a full batch
+#ifndef NSB_OCTETS
+#define NSB_OCTETS 2
+#endif
+constexpr int kOctets = NSB_OCTETS;              // octets per thread per sweep (1 or 2)
+constexpr int kThreadBits = kOctets == 2 ? 7 : 8;
+constexpr int kPassThreads = 1 << kThreadBits;  // 4 (8) warps per CTA, two CTAs per SM
+constexpr int kIndexBits = kThreadBits + (kOctets == 2 ? 1 : 0);  // octet-index bits of a batch
 static_assert(kIndexBits <= 9, "GroupDesc holds 9 index-bit offsets");
 constexpr int kLowQubits = 3;                    // always-tiled qubits 0..2 (128 B runs)
 // States up to this many qubits stay L2-resident inside a launch: their

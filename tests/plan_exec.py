@@ -11,6 +11,7 @@ against the oracle without a GPU.  Small qubit counts only.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -25,7 +26,9 @@ GROUP_DT = np.dtype([("am", "<u2", (3,)), ("ram", "<u2", (3,)), ("tcol", "<u2", 
                      ("rtcol", "<u2", (9,)), ("op_begin", "u1"), ("n_ops", "u1"),
                      ("sync", "u1"), ("pad", "u1", (5,)), ("r_out", "<u8", (3,))], align=True)
 OP_DT = np.dtype([("mat", "<i2"), ("cls", "u1"), ("pat", "u1"), ("cols", "<u2"), ("kind", "u1"), ("pad", "u1")])
-THREAD_BITS = 7  # kThreadBits
+OCTETS = 1 if os.environ.get("NSB_LIB_VARIANT") == "o1" else 2  # kOctets (build variant)
+THREAD_BITS = 7 if OCTETS == 2 else 8  # kThreadBits
+INDEX_BITS = THREAD_BITS + (1 if OCTETS == 2 else 0)  # kIndexBits
 THREADS = 1 << THREAD_BITS  # kPassThreads
 TILE_MAX = 11  # kTileQubitsMax
 (DENSE1, DIAG1, DENSE2, SPARSE2, MONO2, DIAG2, CX01, CX10, PAIRQ, PAIRP, PAIRX, SWAP,
@@ -159,7 +162,7 @@ def _apply_group(B, G, ops, mats, tbases, k, nvalid):
     t = np.arange(n_act, dtype=np.int64)
     a = np.zeros(n_act, np.int64)
     r = np.zeros(n_act, np.int64)
-    for b in range(THREAD_BITS + 1):
+    for b in range(INDEX_BITS):
         a ^= np.where((t >> b) & 1, int(G["tcol"][b]), 0)
         r ^= np.where((t >> b) & 1, int(G["rtcol"][b]), 0)
     tile = t >> cb
