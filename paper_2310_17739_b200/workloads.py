@@ -225,7 +225,8 @@ def layered_workload(n: int, layers: int, seed: int = 28) -> Workload:
 
 
 CLASS_NAMES = ("dense1", "diag1", "dense2", "sparse2", "mono2", "diag2", "cx01", "cx10",
-               "pair_q", "pair_p", "pair_x", "swap", "permute")
+               "pair_q", "pair_p", "pair_x", "swap", "permute", "pair_q_real", "pair_p_real",
+               "pair_x_real")  # planner.h GateClass order; NSB_N_CLASSES entries
 
 
 def plan_analyze(ops: np.ndarray, params: np.ndarray, payloads: np.ndarray, n: int) -> dict:

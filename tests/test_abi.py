@@ -60,3 +60,11 @@ def test_gate_matrix_rejects_bad_tags():
     out = np.zeros(64, np.float64)
     assert N.lib().nsb_gate_matrix(999, None, 0, N.ptr(out)) == N.NSB_EINVAL
     assert N.lib().nsb_gate_matrix(0, None, 0, N.ptr(out)) == N.NSB_EINVAL  # u3 needs 3 params
+
+
+def test_class_names_match_header():
+    """nsb_plan_analyze writes NSB_N_CLASSES counts into the caller's buffer."""
+    from paper_2310_17739_b200.workloads import CLASS_NAMES
+    text = (ROOT / "include" / "nucsim_b200.h").read_text()
+    n = int(re.search(r"#define NSB_N_CLASSES (\d+)", text).group(1))
+    assert len(CLASS_NAMES) == n
