@@ -771,7 +771,7 @@ void HostPlan::build_serial(const nsb_op* ops, int64_t n_ops, const double* para
   int k = choose_tile_qubits(n, workers);
   if (const char* e = std::getenv("NSB_TILE_QUBITS")) k = std::min(std::atoi(e), n);  // tuning
   tile_qubits = k;
-  low_qubits = n <= kL2ResidentQubits ? 1 : kLowQubits;
+  low_qubits = n <= kL2ResidentQubits ? kLowQubitsL2 : kLowQubits;
   if (const char* e = std::getenv("NSB_LOW_QUBITS")) low_qubits = std::atoi(e);  // tuning
   if (const char* e = std::getenv("NSB_NO_GROUP_FUSION")) fuse_groups = std::atoi(e) == 0;
   blocked = n >= 6;

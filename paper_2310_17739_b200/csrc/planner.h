@@ -42,6 +42,9 @@ constexpr int kLowQubits = 3;                    // always-tiled qubits 0..2 (12
 // tiles need not hold qubits 0..2 (sector efficiency matters less than the
 // extra free tile qubit slots, which cut the pass count by a third).
 constexpr int kL2ResidentQubits = 22;
+// ... but qubits 0, 1 (64-byte runs: half the L2 requests of 32-byte runs)
+// still pay: deep21 measured 862 ms with 2, 878 ms with 1, 924 ms with 3.
+constexpr int kLowQubitsL2 = 2;
 constexpr int kMaxQubits = 40;
 
 // Payload classes, chosen by exact-zero structure (skipping an exact zero
