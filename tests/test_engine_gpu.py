@@ -437,3 +437,29 @@ def test_rejection_replay_equals_explicit_shots(golden):
     finally:
         E._replayable = saved
     assert fast[0] == slow[0] and fast[2] == slow[2] and fast[1] == slow[1]
+
+
+@pytest.mark.parametrize("env", [{}, {"NSB_NO_GROUP_FUSION": "1"}, {"NSB_EXACT_CLASSES": "1"}])
+def test_deep_filter_workload_classes_and_group_fusion(monkeypatch, env):
+    """The deep-circuit shape (JW shell-model filter, natively generated and
+    fused) through the blocked kernel with the planner's near-zero cleaning,
+    real two-block classes and group fusion on (default) and off: final
+    state within 1e-10 relative L2 and assertion probabilities within 1e-12
+    of the full-state oracle."""
+    import shard_exec as SE
+    from paper_2310_17739_b200 import workloads as W
+    from paper_2310_17739_b200.engine import DeviceProgram, StateVector
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    wl = W.filter_workload(11, trotter=2, n_steps=3, n_scatter=6, trial="10" * 6)
+    fops, pool, _ = W.fuse_packed(wl.ops, wl.params, wl.payloads)
+    exe = wl.executable(fops)
+    n = wl.n_qubits
+    want_p, want = SE.full_mma(exe, wl.params, pool, n)
+    state = StateVector(n)
+    prog = DeviceProgram(state, exe, wl.params, pool)
+    got_p = prog.run_mma()
+    assert got_p == pytest.approx(want_p, abs=1e-12)
+    assert rel_l2(state.amps, want) < 1e-10
+    if not env:
+        assert prog.info.n_fused_group_ops > 0
