@@ -298,6 +298,8 @@ def run_sharded(args, rank, world, local):
                        "fused_gates": stats["gates_after"], "passes_per_rank": tot["n_passes"],
                        "device_gate_ops": tot["n_device_gates"], "octet_sweeps": tot["n_sweeps"],
                        "qubit_swaps": prog.n_swaps,
+                       "qubit_swap_path": "peer-memory kernel (nsb_shard_swap_p2p)"
+                       if st.peer_swaps else "pack + NCCL send/recv + unpack",
                        "parallelism": f"shard{world}",
                        "l2": f"state shard 2^{nl} x 16 B >> L2; no flush needed"},
             "host": host,

@@ -265,8 +265,16 @@ int nsb_timer_stop(nsb_ctx* ctx, double* ms, nsb_status* st);
  * Collective: both partners must call it.
  * nsb_shard_reset: the shard of |0...0> (rank 0: amplitude 1 at index 0;
  * other ranks: zeros), on the device.
- * nsb_shard_allgather: every rank contributes `count` (<= 64) doubles; `out`
- * receives nranks * count values in rank order (deterministic sums). */
+ * nsb_shard_allgather: every rank contributes `count` doubles; `out`
+ * receives nranks * count values in rank order (deterministic sums).
+ * nsb_shard_ipc_handle: 64-byte CUDA IPC handle of this rank's shard;
+ * nsb_shard_open_peers: map every other rank's shard (handles: nranks x 64
+ * bytes in rank order, own entry ignored) into this context.
+ * nsb_shard_swap_p2p: nsb_shard_swap through peer memory over NVLink: the
+ * element pairs are split in chunks, this rank swaps the chunks of its
+ * parity with one kernel that reads and writes both shards directly (no
+ * staging copies, no pack / unpack), between two stream-ordered barriers.
+ * Collective: both partners must call it (after nsb_shard_open_peers). */
 int nsb_comm_unique_id(uint8_t* id, nsb_status* st);
 int nsb_comm_init(nsb_ctx* ctx, const uint8_t* id, int32_t nranks, int32_t rank,
                   nsb_status* st);
@@ -275,6 +283,9 @@ int nsb_shard_swap(nsb_ctx* ctx, int32_t global_bit, int32_t local_q, int64_t ch
 int nsb_shard_reset(nsb_ctx* ctx, nsb_status* st);
 int nsb_shard_allgather(nsb_ctx* ctx, const double* in, int32_t count, double* out,
                         nsb_status* st);
+int nsb_shard_ipc_handle(nsb_ctx* ctx, uint8_t* handle, nsb_status* st);
+int nsb_shard_open_peers(nsb_ctx* ctx, const uint8_t* handles, nsb_status* st);
+int nsb_shard_swap_p2p(nsb_ctx* ctx, int32_t global_bit, int32_t local_q, nsb_status* st);
 
 #ifdef __cplusplus
 }

@@ -118,6 +118,9 @@ _SIGNATURES = {
     "nsb_shard_swap": (ctypes.c_int, [_P, _I32, _I32, _I64, _ST]),
     "nsb_shard_reset": (ctypes.c_int, [_P, _ST]),
     "nsb_shard_allgather": (ctypes.c_int, [_P, _P, _I32, _P, _ST]),
+    "nsb_shard_ipc_handle": (ctypes.c_int, [_P, _P, _ST]),
+    "nsb_shard_open_peers": (ctypes.c_int, [_P, _P, _ST]),
+    "nsb_shard_swap_p2p": (ctypes.c_int, [_P, _I32, _I32, _ST]),
 }
 
 EXPORTS = tuple(_SIGNATURES)

@@ -941,6 +941,48 @@ __global__ void k_shard_unpack(double2* __restrict__ a, const double2* __restric
     a[insert_zero(off + i, L) | vb] = in[i];
 }
 
+// Qubit swap through peer memory (NVLink): element k of this rank's outgoing
+// half (bit L == v_mine) trades places with element k of the partner's
+// (bit L == v_peer).  Chunks of 2^clog element pairs alternate between the
+// two ranks (chunk parity), so every pair is read and written by exactly one
+// GPU: one local and one remote load, one local and one remote store, four
+// independent pairs in flight per thread.
+__global__ void k_shard_swap_p2p(double2* __restrict__ mine, double2* __restrict__ peer,
+                                 uint64_t half, int L, int v_mine, int v_peer, int parity,
+                                 int clog) {
+  const uint64_t clen = uint64_t(1) << clog;
+  const uint64_t n_chunks = (half + clen - 1) >> clog;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  // owned elements, enumerated densely: e -> chunk 2 * (e >> clog) + parity
+  const uint64_t owned_chunks = (n_chunks + 1 - parity) >> 1;
+  const uint64_t n_owned = owned_chunks << clog;
+  for (uint64_t e0 = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e0 < n_owned;
+       e0 += 4 * stride) {
+    uint64_t km[4], kp[4];
+    double2 x[4], y[4];
+    bool ok[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t e = e0 + u * stride;
+      const uint64_t k = ((2 * (e >> clog) + parity) << clog) | (e & (clen - 1));
+      ok[u] = e < n_owned && k < half;
+      km[u] = insert_zero(k, L) | (uint64_t(v_mine) << L);
+      kp[u] = insert_zero(k, L) | (uint64_t(v_peer) << L);
+      if (ok[u]) {
+        x[u] = mine[km[u]];
+        y[u] = peer[kp[u]];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (ok[u]) {
+        mine[km[u]] = y[u];
+        peer[kp[u]] = x[u];
+      }
+  }
+  __threadfence_system();
+}
+
 }  // namespace dev
 }  // namespace nsb
 
@@ -1006,6 +1048,7 @@ struct nsb_ctx {
   size_t pinned_bytes = 0;
   // sharded state (nsb_comm_init): this process holds rank `rank` of `nranks`
   void* comm = nullptr;  // ncclComm_t
+  double2* peers[64] = {};  // IPC-mapped shards of the other ranks (nsb_shard_open_peers)
   int rank = 0, nranks = 1;
   // qubit swaps: pack / unpack on `stream`, NCCL on `xfer`, double-buffered
   cudaStream_t xfer = nullptr;
@@ -1081,6 +1124,11 @@ const NcclApi& shard_nccl() {
   } while (0)
 
 void shard_comm_destroy(nsb_ctx* c) {
+  for (double2*& p : c->peers)
+    if (p) {
+      cudaIpcCloseMemHandle(p);
+      p = nullptr;
+    }
   if (c->comm) shard_nccl().comm_destroy(static_cast<ncclComm_t>(c->comm));
   c->comm = nullptr;
   c->rank = 0;
@@ -1749,6 +1797,66 @@ int nsb_shard_swap(nsb_ctx* c, int32_t global_bit, int32_t local_q, int64_t chun
     }
     NSB_CUDA(cudaStreamSynchronize(c->stream));
     NSB_CUDA(cudaStreamSynchronize(c->xfer));
+  });
+}
+
+int nsb_shard_ipc_handle(nsb_ctx* c, uint8_t* handle, nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    if (!handle) throw std::invalid_argument("null handle");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    NSB_CUDA(cudaSetDevice(c->device));
+    cudaIpcMemHandle_t h;
+    NSB_CUDA(cudaIpcGetMemHandle(&h, c->amps.ptr));
+    std::memcpy(handle, &h, sizeof h);
+  });
+}
+
+int nsb_shard_open_peers(nsb_ctx* c, const uint8_t* handles, nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    if (!c->comm) throw std::invalid_argument("no communicator (nsb_comm_init)");
+    if (!handles) throw std::invalid_argument("null handles");
+    if (c->nranks > 64) throw std::invalid_argument("too many ranks for peer mapping");
+    NSB_CUDA(cudaSetDevice(c->device));
+    for (int r = 0; r < c->nranks; ++r) {
+      if (r == c->rank || c->peers[r]) continue;
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, handles + 64 * r, sizeof h);
+      void* p = nullptr;
+      NSB_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      c->peers[r] = static_cast<double2*>(p);
+    }
+  });
+}
+
+// stream-ordered rendezvous of all ranks (an 8-byte all-gather on the stream)
+void comm_barrier(nsb_ctx* c) {
+  double* buf = c->scratch.ptr + 2 * dev::kReduceBlocks + 8;
+  NSB_NCCL(shard_nccl().all_gather(buf, buf + 1, 1, ncclFloat64,
+                                   static_cast<ncclComm_t>(c->comm), c->stream));
+}
+
+int nsb_shard_swap_p2p(nsb_ctx* c, int32_t global_bit, int32_t local_q, nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    if (!c->comm) throw std::invalid_argument("no communicator (nsb_comm_init)");
+    if (global_bit < 0 || (1 << global_bit) >= c->nranks || local_q < 0 || local_q >= c->n)
+      throw std::invalid_argument("bad shard swap qubits");
+    const int partner = c->rank ^ (1 << global_bit);
+    if (!c->peers[partner]) throw std::invalid_argument("peer shard not mapped (nsb_shard_open_peers)");
+    if (c->scratch.count < size_t(2 * dev::kReduceBlocks + 8 + 1 + c->nranks))
+      throw std::invalid_argument("barrier exceeds scratch");
+    NSB_CUDA(cudaSetDevice(c->device));
+    const int b = (c->rank >> global_bit) & 1;
+    const uint64_t half = c->n_amps >> 1;
+    const int clog = static_cast<int>(std::min<uint64_t>(16, c->n - 1));
+    comm_barrier(c);  // both shards are final before either is touched
+    dev::k_shard_swap_p2p<<<static_cast<unsigned>(c->sm_count * 4), 256, 0, c->stream>>>(
+        c->amps.ptr, c->peers[partner], half, local_q, 1 - b, b, b, clog);
+    NSB_CUDA(cudaGetLastError());
+    comm_barrier(c);  // both halves of the exchange landed before either continues
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
 

@@ -264,6 +264,7 @@ class ShardedState:
         self.dev.call("nsb_state_init", self.nl)
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
         self.dev.call("nsb_comm_init", buf, world, rank)
+        self.peer_swaps = False  # set by from_torch_distributed (IPC-mapped partner shards)
         self.reset()
 
     @staticmethod
@@ -274,16 +275,32 @@ class ShardedState:
         return bytes(buf)
 
     @classmethod
-    def from_torch_distributed(cls, n_qubits: int, device: int | None = None):
-        """Collective: rank 0 makes the NCCL id, torch.distributed broadcasts it."""
+    def from_torch_distributed(cls, n_qubits: int, device: int | None = None,
+                               peer_swaps: bool | None = None):
+        """Collective: rank 0 makes the NCCL id, torch.distributed broadcasts it.
+        With peer_swaps (default: on unless NSB_SWAP_NCCL=1) the ranks also
+        exchange CUDA IPC handles of their shards, and qubit swaps run as one
+        peer-memory kernel over NVLink (nsb_shard_swap_p2p) instead of
+        pack / NCCL send-recv / unpack."""
+        import os
         import torch.distributed as dist
         rank, world = dist.get_rank(), dist.get_world_size()
         box = [cls.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(box, src=0)
         if device is None:
-            import os
             device = int(os.environ.get("LOCAL_RANK", rank))
-        return cls(n_qubits, rank, world, device, box[0])
+        st = cls(n_qubits, rank, world, device, box[0])
+        if peer_swaps is None:
+            peer_swaps = os.environ.get("NSB_SWAP_NCCL", "0") == "0"
+        if peer_swaps and world > 1:
+            h = (ctypes.c_uint8 * 64)()
+            st.dev.call("nsb_shard_ipc_handle", h)
+            handles = [None] * world
+            dist.all_gather_object(handles, bytes(h))
+            buf = (ctypes.c_uint8 * (64 * world)).from_buffer_copy(b"".join(handles))
+            st.dev.call("nsb_shard_open_peers", buf)
+            st.peer_swaps = True
+        return st
 
     def close(self):
         self.dev.close()
@@ -431,7 +448,10 @@ class ShardedProgram:
                     N.check(N.lib().nsb_plan_run_segment(S.dev.handle, h, i, ctypes.byref(st)),
                             st)
             elif s.kind == "swap":
-                S.dev.call("nsb_shard_swap", s.global_bit, s.local_q, chunk_amps)
+                if S.peer_swaps:
+                    S.dev.call("nsb_shard_swap_p2p", s.global_bit, s.local_q)
+                else:
+                    S.dev.call("nsb_shard_swap", s.global_bit, s.local_q, chunk_amps)
             else:
                 p = ctypes.c_double(0.0)
                 S.dev.call("nsb_branch_probability", s.local_q, 0, ctypes.byref(p))

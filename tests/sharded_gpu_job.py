@@ -31,8 +31,10 @@ def main(out):
     dist.init_process_group("gloo")
     rank = dist.get_rank()
     res = {}
-    for tag, ops, params, pool, n in cases():
-        st = S.ShardedState.from_torch_distributed(n, device=int(os.environ["LOCAL_RANK"]))
+    for (tag, ops, params, pool, n), peer in zip(list(cases()) * 2, [True, True, False, False]):
+        tag = tag + ("_p2p" if peer else "_nccl")
+        st = S.ShardedState.from_torch_distributed(n, device=int(os.environ["LOCAL_RANK"]),
+                                                   peer_swaps=peer)
         probs, steps = st.run_mma(ops, params, pool)
         shard = st.download()
         norm = st.norm()
