@@ -408,12 +408,18 @@ void swap_packed_slots(uint8_t& cls, double* v, uint16_t& cols) {
 // largest are zeroed as in pack_matrix).
 using cplx = std::complex<double>;
 
+// plain complex product (std::complex's operator* calls __muldc3 for its
+// NaN/Inf recovery: an order of magnitude slower, and not needed here)
+inline cplx cm(const cplx& a, const cplx& b) {
+  return cplx(a.real() * b.real() - a.imag() * b.imag(), a.real() * b.imag() + a.imag() * b.real());
+}
+
 void apply_octet(const GateOp& op, const double* m2, cplx* x) {
   auto M = [&](int i) { return cplx(m2[2 * i], m2[2 * i + 1]); };
   auto mix = [&](int i, int j, int e) {
     const cplx a = x[i], b = x[j];
-    x[i] = M(e) * a + M(e + 1) * b;
-    x[j] = M(e + 2) * a + M(e + 3) * b;
+    x[i] = cm(M(e), a) + cm(M(e + 1), b);
+    x[j] = cm(M(e + 2), a) + cm(M(e + 3), b);
   };
   const int c = op.cls;
   if (op.pat >= kPat0 && op.pat <= kPat2) {
@@ -421,8 +427,8 @@ void apply_octet(const GateOp& op, const double* m2, cplx* x) {
     for (int b = 0; b < 8; ++b) {
       if (b & A) continue;
       if (c == kDiag1) {
-        x[b] *= M(0);
-        x[b | A] *= M(1);
+        x[b] = cm(M(0), x[b]);
+        x[b | A] = cm(M(1), x[b | A]);
       } else {
         mix(b, b | A, 0);
       }
@@ -445,26 +451,27 @@ void apply_octet(const GateOp& op, const double* m2, cplx* x) {
         const int k = (c == kPairQ || c == kPairQr) ? 0 : (c == kPairP || c == kPairPr) ? 1 : 2;
         static const int kU[3][4] = {{0, 2, 1, 3}, {0, 1, 2, 3}, {0, 3, 1, 2}};
         const int* u = kU[k];
-        out[u[0]] = M(0) * v[u[0]] + M(1) * v[u[1]];
-        out[u[1]] = M(2) * v[u[0]] + M(3) * v[u[1]];
-        out[u[2]] = M(4) * v[u[2]] + M(5) * v[u[3]];
-        out[u[3]] = M(6) * v[u[2]] + M(7) * v[u[3]];
+        out[u[0]] = cm(M(0), v[u[0]]) + cm(M(1), v[u[1]]);
+        out[u[1]] = cm(M(2), v[u[0]]) + cm(M(3), v[u[1]]);
+        out[u[2]] = cm(M(4), v[u[2]]) + cm(M(5), v[u[3]]);
+        out[u[3]] = cm(M(6), v[u[2]]) + cm(M(7), v[u[3]]);
         break;
       }
       case kDiag2:
-        for (int s = 0; s < 4; ++s) out[s] = M(s) * v[s];
+        for (int s = 0; s < 4; ++s) out[s] = cm(M(s), v[s]);
         break;
       case kMono2:
-        for (int s = 0; s < 4; ++s) out[s] = M(s) * v[(op.cols >> (2 * s)) & 3];
+        for (int s = 0; s < 4; ++s) out[s] = cm(M(s), v[(op.cols >> (2 * s)) & 3]);
         break;
       case kSparse2:
         for (int s = 0; s < 4; ++s)
-          out[s] = M(2 * s) * v[(op.cols >> (4 * s)) & 3] +
-                   M(2 * s + 1) * v[(op.cols >> (4 * s + 2)) & 3];
+          out[s] = cm(M(2 * s), v[(op.cols >> (4 * s)) & 3]) +
+                   cm(M(2 * s + 1), v[(op.cols >> (4 * s + 2)) & 3]);
         break;
       default:  // kDense2
         for (int s = 0; s < 4; ++s)
-          out[s] = M(4 * s) * v[0] + M(4 * s + 1) * v[1] + M(4 * s + 2) * v[2] + M(4 * s + 3) * v[3];
+          out[s] = cm(M(4 * s), v[0]) + cm(M(4 * s + 1), v[1]) + cm(M(4 * s + 2), v[2]) +
+                   cm(M(4 * s + 3), v[3]);
         break;
     }
     for (int s = 0; s < 4; ++s) x[idx[s]] = out[s];
@@ -475,8 +482,27 @@ void apply_octet(const GateOp& op, const double* m2, cplx* x) {
 bool fuse_group(const std::vector<GateOp>& ops, const std::vector<double>& mats, GateOp& fused,
                 std::vector<double>& packed) {
   if (ops.size() < 2) return false;
-  for (const GateOp& op : ops)
+  // structural pre-check: the XOR span of the register distances the gates
+  // can couple must be {0} or {0, 2^t}, else the product cannot qualify
+  static const uint8_t kReach2[3] = {1 | 2, 1 | 4, 1 | 8};  // 2q patterns -> slot masks
+  (void)kReach2;
+  uint32_t span = 0;  // bit mask of axis bits that some gate moves amplitudes along
+  for (const GateOp& op : ops) {
     if (op.pat > kPat2) return false;
+    if (op.cls == kDiag1 || op.cls == kDiag2 || op.cls == kPermute) continue;
+    if (op.pat >= kPat0) {
+      span |= 1u << (op.pat - kPat0);
+      continue;
+    }
+    static const int kAx[3][2] = {{0, 1}, {0, 2}, {1, 2}};
+    const uint32_t a = 1u << kAx[op.pat][0], b = 1u << kAx[op.pat][1];
+    switch (op.cls) {
+      case kPairQ: case kPairQr: case kCX01: span |= b; break;   // slot 1 moves
+      case kPairP: case kPairPr: case kCX10: span |= a; break;   // slot 0 moves
+      default: span |= a | b; break;                            // both (or a diagonal move)
+    }
+  }
+  if (__builtin_popcount(span) > 1) return false;
   cplx Mx[8][8];
   for (int j = 0; j < 8; ++j) {
     cplx x[8];
