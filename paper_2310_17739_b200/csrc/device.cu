@@ -315,56 +315,6 @@ __device__ __forceinline__ void mix2r(double2& x, double2& y, const double a0, c
   y = oy;
 }
 
-// The same 2x2 on NI register pairs (ix[i], iy[i]) of each of the NO octets,
-// in operand-shared order: each multiply-add step runs over all instances
-// before the next, so consecutive DFMAs share their matrix operand (the
-// register-reuse order that measured faster for the dense 4x4 sweeps).
-template <int NO, int NI>
-__device__ __forceinline__ void mix2_set(double2 (&xs)[NO][8], const int (&ix)[NI],
-                                         const int (&iy)[NI], const double2 m0, const double2 m1,
-                                         const double2 m2, const double2 m3) {
-  double oxx[NO][NI], oxy[NO][NI], oyx[NO][NI], oyy[NO][NI];
-#define NSB_ALL for (int q = 0; q < NO; ++q) _Pragma("unroll") for (int i = 0; i < NI; ++i)
-#pragma unroll
-  NSB_ALL oxx[q][i] = m0.x * xs[q][ix[i]].x;
-#pragma unroll
-  NSB_ALL oxy[q][i] = m0.x * xs[q][ix[i]].y;
-#pragma unroll
-  NSB_ALL oyx[q][i] = m2.x * xs[q][ix[i]].x;
-#pragma unroll
-  NSB_ALL oyy[q][i] = m2.x * xs[q][ix[i]].y;
-#pragma unroll
-  NSB_ALL oxx[q][i] = fma(-m0.y, xs[q][ix[i]].y, oxx[q][i]);
-#pragma unroll
-  NSB_ALL oxy[q][i] = fma(m0.y, xs[q][ix[i]].x, oxy[q][i]);
-#pragma unroll
-  NSB_ALL oyx[q][i] = fma(-m2.y, xs[q][ix[i]].y, oyx[q][i]);
-#pragma unroll
-  NSB_ALL oyy[q][i] = fma(m2.y, xs[q][ix[i]].x, oyy[q][i]);
-#pragma unroll
-  NSB_ALL oxx[q][i] = fma(m1.x, xs[q][iy[i]].x, oxx[q][i]);
-#pragma unroll
-  NSB_ALL oxy[q][i] = fma(m1.x, xs[q][iy[i]].y, oxy[q][i]);
-#pragma unroll
-  NSB_ALL oyx[q][i] = fma(m3.x, xs[q][iy[i]].x, oyx[q][i]);
-#pragma unroll
-  NSB_ALL oyy[q][i] = fma(m3.x, xs[q][iy[i]].y, oyy[q][i]);
-#pragma unroll
-  NSB_ALL oxx[q][i] = fma(-m1.y, xs[q][iy[i]].y, oxx[q][i]);
-#pragma unroll
-  NSB_ALL oxy[q][i] = fma(m1.y, xs[q][iy[i]].x, oxy[q][i]);
-#pragma unroll
-  NSB_ALL oyx[q][i] = fma(-m3.y, xs[q][iy[i]].y, oyx[q][i]);
-#pragma unroll
-  NSB_ALL oyy[q][i] = fma(m3.y, xs[q][iy[i]].x, oyy[q][i]);
-#pragma unroll
-  NSB_ALL {
-    xs[q][ix[i]] = make_double2(oxx[q][i], oxy[q][i]);
-    xs[q][iy[i]] = make_double2(oyx[q][i], oyy[q][i]);
-  }
-#undef NSB_ALL
-}
-
 __device__ __forceinline__ double2 pick(const double2 x0, const double2 x1, const double2 x2,
                                         const double2 x3, int c) {
   double2 r = x0;
@@ -421,7 +371,6 @@ __device__ __forceinline__ void gate2(double2 (&xs)[NO][8], const GateOp o,
       constexpr int u3 = C == kPairQ ? A | B : (C == kPairP ? A | B : B);
       const double2 m0 = m[0], m1 = m[1], m2 = m[2], m3 = m[3];
       const double2 n0 = m[4], n1 = m[5], n2 = m[6], n3 = m[7];
-#ifdef NSB_MIX_PAIRS
 #pragma unroll
       for (int q = 0; q < NO; ++q)
 #pragma unroll
@@ -429,12 +378,6 @@ __device__ __forceinline__ void gate2(double2 (&xs)[NO][8], const GateOp o,
           mix2(xs[q][h], xs[q][h | u1], m0, m1, m2, m3);
           mix2(xs[q][h | u2], xs[q][h | u3], n0, n1, n2, n3);
         }
-#else
-      constexpr int x1[2] = {0, H}, y1[2] = {u1, H | u1};
-      constexpr int x2[2] = {u2, H | u2}, y2[2] = {u3, H | u3};
-      mix2_set<NO, 2>(xs, x1, y1, m0, m1, m2, m3);
-      mix2_set<NO, 2>(xs, x2, y2, n0, n1, n2, n3);
-#endif
       break;
     }
     case kPairQr:
@@ -596,7 +539,6 @@ __device__ __forceinline__ void gate1(double2 (&xs)[NO][8], const GateOp,
       }
   } else {
     const double2 m0 = m[0], m1 = m[1], m2 = m[2], m3 = m[3];
-#ifdef NSB_MIX_PAIRS
 #pragma unroll
     for (int q = 0; q < NO; ++q)
 #pragma unroll
@@ -604,10 +546,6 @@ __device__ __forceinline__ void gate1(double2 (&xs)[NO][8], const GateOp,
         const int c = ((i & 1) ? L0 : 0) | ((i & 2) ? L1 : 0);
         mix2(xs[q][c], xs[q][c | A], m0, m1, m2, m3);
       }
-#else
-    constexpr int ix[4] = {0, L0, L1, L0 | L1}, iy[4] = {A, L0 | A, L1 | A, L0 | L1 | A};
-    mix2_set<NO, 4>(xs, ix, iy, m0, m1, m2, m3);
-#endif
   }
 }
 
@@ -622,13 +560,8 @@ __device__ __forceinline__ void gate_octet_axis(double2 (&xs)[NO][8],
   for (int b = 0; b < 4; ++b) {
     const int c = ((b & 1) ? L0 : 0) | ((b & 2) ? L1 : 0);
     const double2 m0 = m[4 * b], m1 = m[4 * b + 1], m2 = m[4 * b + 2], m3 = m[4 * b + 3];
-#ifdef NSB_MIX_PAIRS
 #pragma unroll
     for (int q = 0; q < NO; ++q) mix2(xs[q][c], xs[q][c | A], m0, m1, m2, m3);
-#else
-    const int ix[1] = {c}, iy[1] = {c | A};
-    mix2_set<NO, 1>(xs, ix, iy, m0, m1, m2, m3);
-#endif
   }
 }
 
