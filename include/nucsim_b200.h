@@ -37,7 +37,8 @@ enum {
   NSB_EASSERT = 2,   /* FilterAssertionError(step, prob) (engine.py:187-190, errors.py:27-33) */
   NSB_EPROJECT = 3,  /* ProjectionError                (engine.py:177-178) */
   NSB_ERESOURCE = 4, /* ResourceLimitError / out of device memory */
-  NSB_EDEVICE = 5    /* CUDA / NCCL failure -> RuntimeError */
+  NSB_EDEVICE = 5,   /* CUDA / NCCL failure -> RuntimeError */
+  NSB_EQASM = 6      /* QasmError(msg, line = step, col = prob)  (errors.py:14-20) */
 };
 
 typedef struct nsb_status {
@@ -81,6 +82,30 @@ typedef struct nsb_op {
 /* Dense matrix of a named gate, bit-identical to reference gate_matrix
  * (gates.py:283-291).  out: (2^k)^2 complex.  Replaces gates.gate_matrix. */
 int nsb_gate_matrix(int32_t tag, const double* params, int32_t n_params, double* out);
+
+/* ---- OpenQASM 2.0 reader (replaces qasm.parse_qasm, qasm.py:30-347) ------
+ * The reference subset: header + qelib1 include, one qreg (<= 64 qubits
+ * here), named cregs (also before the qreg), the qelib1 gate names, measure /
+ * reset / barrier (indexed or whole register), `//` comments, constant angle
+ * expressions folded to doubles in the reference's order.  Output records
+ * are ready for nsb_fuse / nsb_plan_create.  Barrier records: nq = 0, mask =
+ * the qubit set, param = offset of their operands (first-occurrence order)
+ * in barrier_qubits, cbit = their count.  Errors: NSB_EQASM with the
+ * reference's message, st->step = line, st->prob = column.                */
+typedef struct nsb_qasm {
+  int32_t n_qubits;
+  int32_t n_cregs;
+  nsb_op* ops;              /* library-owned: nsb_qasm_free */
+  int64_t n_ops;
+  double* params;           /* float64 parameter pool referenced by ops[].param */
+  int64_t n_params;
+  int32_t* barrier_qubits;
+  int64_t n_barrier_qubits;
+  char* creg_names;         /* n_cregs NUL-terminated names, declaration order */
+  int64_t* creg_sizes;
+} nsb_qasm;
+int nsb_qasm_parse(const char* text, int64_t len, nsb_qasm* out, nsb_status* st);
+void nsb_qasm_free(nsb_qasm* q);
 
 /* ---- fusion (replaces fusion.fuse_pipeline, fusion.py:240-251) --------- */
 enum { NSB_PASS_MERGE_1Q = 1, NSB_PASS_ABSORB_1Q = 2, NSB_PASS_NORMALIZE_2Q = 4,

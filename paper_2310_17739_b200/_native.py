@@ -14,13 +14,13 @@ from pathlib import Path
 
 import numpy as np
 
-from .errors import FilterAssertionError, ProjectionError, ResourceLimitError
+from .errors import FilterAssertionError, ProjectionError, QasmError, ResourceLimitError
 
 LIB_PATH = Path(__file__).resolve().parent / "libnucsim_b200.so"
 if os.environ.get("NSB_LIB_VARIANT"):  # tuning experiments: an in-tree build variant
     LIB_PATH = LIB_PATH.with_name(f"libnucsim_b200_{os.environ['NSB_LIB_VARIANT']}.so")
 
-NSB_OK, NSB_EINVAL, NSB_EASSERT, NSB_EPROJECT, NSB_ERESOURCE, NSB_EDEVICE = range(6)
+NSB_OK, NSB_EINVAL, NSB_EASSERT, NSB_EPROJECT, NSB_ERESOURCE, NSB_EDEVICE, NSB_EQASM = range(7)
 OP_GATE, OP_MEASURE, OP_RESET, OP_BARRIER = range(4)
 BLAS_CHAIN2, BLAS_FOUR = 1, 2
 PASS_ALL = 15
@@ -43,6 +43,15 @@ class Fused(ctypes.Structure):
                 ("payloads", ctypes.POINTER(ctypes.c_double)), ("n_payload", ctypes.c_int64),
                 ("gates_before", ctypes.c_int64),
                 ("pass_before", ctypes.c_int64 * 4), ("pass_after", ctypes.c_int64 * 4)]
+
+
+class Qasm(ctypes.Structure):
+    _fields_ = [("n_qubits", ctypes.c_int32), ("n_cregs", ctypes.c_int32),
+                ("ops", ctypes.c_void_p), ("n_ops", ctypes.c_int64),
+                ("params", ctypes.POINTER(ctypes.c_double)), ("n_params", ctypes.c_int64),
+                ("barrier_qubits", ctypes.POINTER(ctypes.c_int32)),
+                ("n_barrier_qubits", ctypes.c_int64),
+                ("creg_names", ctypes.c_void_p), ("creg_sizes", ctypes.POINTER(ctypes.c_int64))]
 
 
 class PlanInfo(ctypes.Structure):
@@ -81,6 +90,8 @@ _SIGNATURES = {
                                            ctypes.POINTER(ctypes.POINTER(ctypes.c_double)),
                                            ctypes.POINTER(_I64), _ST]),
     "nsb_free": (None, [_P]),
+    "nsb_qasm_parse": (ctypes.c_int, [ctypes.c_char_p, _I64, ctypes.POINTER(Qasm), _ST]),
+    "nsb_qasm_free": (None, [ctypes.POINTER(Qasm)]),
     "nsb_device_count": (ctypes.c_int, [ctypes.POINTER(_I32)]),
     "nsb_ctx_create": (ctypes.c_int, [_I32, ctypes.POINTER(_P), _ST]),
     "nsb_ctx_destroy": (None, [_P]),
@@ -162,6 +173,8 @@ def check(code: int, st: Status) -> None:
         raise ProjectionError(msg)
     if code == NSB_ERESOURCE:
         raise ResourceLimitError(msg)
+    if code == NSB_EQASM:
+        raise QasmError(msg, int(st.step), int(st.prob))
     raise RuntimeError(f"device error: {msg}")
 
 
