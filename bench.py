@@ -480,7 +480,7 @@ def main():
     ap.add_argument("--config", default="deep21", choices=("deep21", "rand28", "shard"))
     ap.add_argument("--qubits", type=int, default=34, help="--config shard: total qubits")
     ap.add_argument("--trotter", type=int, default=None)
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
