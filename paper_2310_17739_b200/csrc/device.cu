@@ -912,10 +912,21 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
     }
     // split grid barrier: arrive, stage the next pass's descriptors while the
     // other CTAs finish, then wait (co-residency from the cooperative launch)
+#ifdef NSB_FENCE_ALL
     __threadfence();
     __syncthreads();
     ++n_bar;
     if (tid == 0) atomicAdd(p.bar, 1u);
+#else
+    // the CTA barrier orders every thread's stores before thread 0's gpu-scope
+    // fence, which is cumulative (the cooperative-groups grid barrier pattern)
+    __syncthreads();
+    ++n_bar;
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(p.bar, 1u);
+    }
+#endif
     if (pi + 1 < p.pass_end) stage(pi + 1);
     if (tid == 0) {
       const unsigned target = n_bar * gridDim.x;
