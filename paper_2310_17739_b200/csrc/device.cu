@@ -629,14 +629,22 @@ __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
   for (int q = 0; q < NO; ++q)
 #pragma unroll
     for (int c = 0; c < 8; ++c)
+#ifdef NSB_SWEEP_NOMEM  // timing experiment (tools/sweep_exp.sh): gate arithmetic only
+      x[q][c] = make_double2(double(r[q] + c), double(a[q] - c));
+#else
       x[q][c] = src[r[q] ^ ((c & 1) ? r0 : 0) ^ ((c & 2) ? r1 : 0) ^ ((c & 4) ? r2 : 0)];
+#endif
   const int n_ops = G.n_ops;
   auto store = [&]() {
 #pragma unroll
     for (int q = 0; q < NO; ++q)
 #pragma unroll
       for (int c = 0; c < 8; ++c)
+#ifdef NSB_SWEEP_NOMEM
+        if (x[q][c].x == 1234.5678) dst[a[q] ^ c] = x[q][c];
+#else
         dst[a[q] ^ ((c & 1) ? m0 : 0) ^ ((c & 2) ? m1 : 0) ^ ((c & 4) ? m2 : 0)] = x[q][c];
+#endif
   };
   // Gate dispatch: pattern * 16 + class selects straight-line register code.
   // The LAST gate of a group stores its octets from inside its own case, so
@@ -688,7 +696,11 @@ __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
         break;
     }
   };
+#ifdef NSB_SWEEP_NOOPS  // timing experiment (tools/sweep_exp.sh): loads and stores only
+  if (true) {
+#else
   if (n_ops == 0) {
+#endif
     store();
     return;
   }
