@@ -565,6 +565,40 @@ __device__ __forceinline__ void gate_octet_axis(double2 (&xs)[NO][8],
   }
 }
 
+// 4x4 on axes (P, Q) with one block per value of the third axis (whole-octet
+// op of planner group fusion, kPatD*): block hh at m + 16 hh, column-major
+template <int P, int Q, int NO>
+__device__ __forceinline__ void gate_octet_pair(double2 (&xs)[NO][8],
+                                                const double2* __restrict__ m) {
+  constexpr int A = 1 << P, B = 1 << Q, H = 7 ^ A ^ B;
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    const int h = hh ? H : 0;
+    const double2* w = m + 16 * hh;
+    double2 out[NO][4];
+#pragma unroll
+    for (int q = 0; q < NO; ++q)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) out[q][r] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double2 wc = w[4 * r + c];
+        const int cm = h | ((c & 1) ? A : 0) | ((c & 2) ? B : 0);
+#pragma unroll
+        for (int q = 0; q < NO; ++q) cmac(out[q][r], wc, xs[q][cm]);
+      }
+#pragma unroll
+    for (int q = 0; q < NO; ++q) {
+      xs[q][h] = out[q][0];
+      xs[q][h | A] = out[q][1];
+      xs[q][h | B] = out[q][2];
+      xs[q][h | A | B] = out[q][3];
+    }
+  }
+}
+
 template <int NO>
 __device__ __forceinline__ void gate_octet_diag(double2 (&xs)[NO][8],
                                                 const double2* __restrict__ m) {
@@ -683,6 +717,13 @@ __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
     if (last) store();                                                   \
     break;
       NSB_GT(0) NSB_GT(1) NSB_GT(2)
+#define NSB_GD(P, Q, PAT)                                                \
+  case PAT * 16 + kDense2:                                               \
+    gate_octet_pair<P, Q, NO>(x, m);                                     \
+    if (last) store();                                                   \
+    break;
+      NSB_GD(0, 1, kPatD01) NSB_GD(0, 2, kPatD02) NSB_GD(1, 2, kPatD12)
+#undef NSB_GD
       case kPatAll * 16 + kDiag1:
         gate_octet_diag<NO>(x, m);
         if (last) store();

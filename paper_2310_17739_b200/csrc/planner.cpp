@@ -502,7 +502,22 @@ bool fuse_group(const std::vector<GateOp>& ops, const std::vector<double>& mats,
       default: span |= a | b; break;                            // both (or a diagonal move)
     }
   }
-  if (__builtin_popcount(span) > 1) return false;
+  if (__builtin_popcount(span) > 2) return false;
+  // gate cost in multiply-adds per amplitude plus a per-gate overhead (dispatch,
+  // matrix loads, register copies; measured to dominate short gates)
+  auto cost = [](const GateOp& op) {
+    constexpr int kOverhead = 8;
+    switch (op.cls) {
+      case kDense1: return 8 + kOverhead;
+      case kDense2: return 16 + kOverhead;
+      case kSparse2: case kPairQ: case kPairP: case kPairX: return 8 + kOverhead;
+      case kPairQr: case kPairPr: case kPairXr: case kMono2: case kDiag1: case kDiag2:
+        return 4 + kOverhead;
+      default: return kOverhead;
+    }
+  };
+  int cost_in = 0;
+  for (const GateOp& op : ops) cost_in += cost(op);
   cplx Mx[8][8];
   for (int j = 0; j < 8; ++j) {
     cplx x[8];
@@ -535,7 +550,29 @@ bool fuse_group(const std::vector<GateOp>& ops, const std::vector<double>& mats,
     int t = -1;
     for (int a = 0; a < 3; ++a)
       if ((reach & ~(1u | (1u << (1 << a)))) == 0) t = a;
-    if (t < 0) return false;
+    if (t < 0) {
+      // two axes (a < b): a 4x4 on them with one block per value of the third
+      // (32 values); only when cheaper than the gates it replaces
+      static const int kPairs[3][2] = {{0, 1}, {0, 2}, {1, 2}};
+      int pat = -1;
+      for (int k = 0; k < 3; ++k) {
+        const uint32_t A = 1u << kPairs[k][0], B = 1u << kPairs[k][1];
+        const uint32_t ok = (1u << 0) | (1u << A) | (1u << B) | (1u << (A | B));
+        if ((reach & ~ok) == 0) pat = k;
+      }
+      if (pat < 0 || 16 + 8 >= cost_in) return false;
+      const int A = 1 << kPairs[pat][0], B = 1 << kPairs[pat][1], H = 7 ^ A ^ B;
+      for (int hh = 0; hh < 2; ++hh) {
+        const int h = hh ? H : 0;
+        const int idx[4] = {h, h | A, h | B, h | A | B};
+        for (int r = 0; r < 4; ++r)
+          for (int c = 0; c < 4; ++c) put(Mx[idx[r]][idx[c]]);
+      }
+      fused.cls = kDense2;
+      fused.pat = static_cast<uint8_t>(kPatD01 + pat);
+      fused.kind = static_cast<uint8_t>(fused.pat * 16 + fused.cls);
+      return true;
+    }
     const int T = 1 << t;
     const int L0 = t == 0 ? 2 : 1, L1 = t == 2 ? 2 : 4;  // the other two axes
     for (int b = 0; b < 4; ++b) {

@@ -119,7 +119,10 @@ enum AxisPattern : uint8_t {
   // kPatT0..T2 with class kDense1 = a 2x2 on axis t whose matrix depends on
   // the other two axes (four blocks, block index = their bits, lower axis
   // first; 16 complex values); kPatAll with class kDiag1 = 8x8 diagonal (8).
-  kPatT0 = 6, kPatT1 = 7, kPatT2 = 8, kPatAll = 9
+  kPatT0 = 6, kPatT1 = 7, kPatT2 = 8, kPatAll = 9,
+  // kPatD01/D02/D12 with class kDense2: a 4x4 on the two axes (slot 0 the
+  // lower) with one block per value of the third axis (32 complex values)
+  kPatD01 = 10, kPatD02 = 11, kPatD12 = 12
 };
 struct GateOp {           // 8 bytes
   int16_t mat;            // offset (complex elements) in the pass's matrix block

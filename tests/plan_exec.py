@@ -35,6 +35,7 @@ TILE_MAX = 11  # kTileQubitsMax
  PERMUTE, PAIRQR, PAIRPR, PAIRXR) = range(16)
 PATTERNS = {0: (0, 1), 1: (0, 2), 2: (1, 2), 3: (0,), 4: (1,), 5: (2,)}
 PAT_T, PAT_ALL = (6, 7, 8), 9  # whole-octet ops (planner.h kPatT0..T2, kPatAll)
+PAT_D = (10, 11, 12)  # two-axis whole-octet ops (planner.h kPatD01..D12)
 
 
 class HostPlan:
@@ -102,6 +103,18 @@ def _gate(x, op, m):
     if pat == PAT_ALL:  # whole-octet diagonal (planner group fusion)
         for r in range(8):
             x[r] = m[r] * x[r]
+        return
+    if pat in PAT_D:  # 4x4 on two axes, one block per value of the third
+        a, b = PATTERNS[pat - PAT_D[0]]
+        A, B = 1 << a, 1 << b
+        H = 7 ^ A ^ B
+        for hh in (0, 1):
+            h = H if hh else 0
+            idx = [h, h | A, h | B, h | A | B]
+            v = [x[i] for i in idx]
+            w = m[16 * hh: 16 * hh + 16]
+            for r in range(4):
+                x[idx[r]] = sum(w[4 * r + c] * v[c] for c in range(4))
         return
     if pat in PAT_T:  # 2x2 on axis t, one block per value of the other two axes
         t = pat - PAT_T[0]
