@@ -227,7 +227,16 @@ struct Parser {
     }
     return v;
   }
+  int depth = 0;  // expression nesting (the reference would hit Python's recursion limit)
+  struct Nest {
+    Parser& p;
+    explicit Nest(Parser& q) : p(q) {
+      if (++p.depth > 500) p.fail("angle expression nested too deeply");
+    }
+    ~Nest() { --p.depth; }
+  };
   double unary() {
+    Nest guard(*this);
     if (peek().kind == kSym && peek().text == "-") {
       next();
       return -unary();

@@ -67,3 +67,17 @@ def test_large_file_throughput():
     dt = time.perf_counter() - t
     assert len(prog.ops) == 100_000
     assert dt < 5.0
+
+
+def test_deep_nesting_and_garbage_do_not_crash():
+    deep = "OPENQASM 2.0;\nqreg q[1];\nrz(" + "(" * 100000 + "1" + ")" * 100000 + ") q[0];\n"
+    with pytest.raises(QasmError, match="nested too deeply"):
+        parse_qasm(deep)
+    rng = np.random.default_rng(5)
+    alphabet = list("OPENQASM2.0;qregcx[](),->pi+*/ \n\"qelib1.inc\"measurebarrier0123456789")
+    for _ in range(300):
+        text = "".join(rng.choice(alphabet, size=int(rng.integers(0, 200))))
+        try:
+            parse_qasm(text)
+        except QasmError:
+            pass
