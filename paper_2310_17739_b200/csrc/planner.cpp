@@ -1142,23 +1142,42 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
     // warp positions: the pair of tile positions that lets the most
     // consecutive sweeps run warp-locally (kThreadBits + 1 octet-index bits
     // must be tile-local for the warp bits 5, 6 to be C vectors: k >= 10)
-    uint32_t wsel = 0;  // chosen warp positions
-    if (k - 3 >= kThreadBits) {  // the warp bits of the octet index are tile-local C vectors
-      // positions a group keeps out of the warp split: its axes (all of them
-      // when its read map is not the identity -- exact check below)
-      std::vector<uint32_t> blocked(closed.size());
-      for (size_t g = 0; g < closed.size(); ++g)
-        blocked[g] = closed[g].r_id ? closed[g].axm : ~0u;
-      int best = 0;
-      for (uint32_t wm = 1; wm < (1u << k); ++wm) {
-        if (__builtin_popcount(wm) != kWarpBits) continue;
-        int score = 0;
-        for (size_t g = 0; g + 1 < closed.size(); ++g)
-          score += !((blocked[g] | blocked[g + 1]) & wm);
-        if (score > best) {
-          best = score;
-          wsel = wm;
+    // warp positions per group: a run of consecutive groups that share a warp
+    // split (two tile positions outside their axes and read maps) runs with
+    // __syncwarp between its sweeps; the split may change wherever a CTA
+    // barrier is needed anyway.  Dynamic programming over the groups picks
+    // the assignment with the most warp-local sweep transitions.
+    std::vector<uint32_t> wsel(closed.size(), 0u);
+    if (k - 3 >= kThreadBits && !closed.empty()) {  // warp bits of the octet index are tile-local
+      std::vector<uint32_t> cands;
+      for (uint32_t wm = 1; wm < (1u << k); ++wm)
+        if (__builtin_popcount(wm) == kWarpBits) cands.push_back(wm);
+      const size_t G = closed.size(), W = cands.size();
+      std::vector<uint8_t> ok(G * W);
+      for (size_t g = 0; g < G; ++g)
+        for (size_t w = 0; w < W; ++w) ok[g * W + w] = warp_local(closed[g], cands[w]);
+      // S[g][w]: most warp-local transitions among groups 0..g with group g on split w
+      std::vector<int> S(G * W, 0), from(G * W, -1);
+      for (size_t g = 1; g < G; ++g) {
+        int best = -1, arg = 0;
+        for (size_t w = 0; w < W; ++w)
+          if (S[(g - 1) * W + w] > best) best = S[(g - 1) * W + w], arg = static_cast<int>(w);
+        for (size_t w = 0; w < W; ++w) {
+          int v = best, f = arg;  // switch split (a CTA barrier between g-1 and g)
+          if (ok[(g - 1) * W + w] && ok[g * W + w] && S[(g - 1) * W + w] + 1 > v) {
+            v = S[(g - 1) * W + w] + 1;
+            f = static_cast<int>(w);
+          }
+          S[g * W + w] = v;
+          from[g * W + w] = f;
         }
+      }
+      int w = 0;
+      for (size_t x = 1; x < W; ++x)
+        if (S[(G - 1) * W + x] > S[(G - 1) * W + w]) w = static_cast<int>(x);
+      for (size_t g = G; g-- > 0;) {
+        wsel[g] = ok[g * W + w] ? cands[w] : 0u;
+        if (g) w = from[g * W + w];
       }
     }
     // group fusion, within the pass's matrix budget (kMaxPassMats)
@@ -1190,10 +1209,10 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
         gate_ops.push_back(op);
       }
       matrices.insert(matrices.end(), H.mats.begin(), H.mats.end());
-      const bool here = wsel && warp_local(H, wsel);
-      const bool next = g + 1 < closed.size() && wsel && warp_local(closed[g + 1], wsel);
-      finish_group(H, k, d, here ? wsel : 0u);
-      d.sync = (here && next) ? 0 : 1;
+      const uint32_t wm = wsel[g];
+      const bool next = g + 1 < closed.size() && wm && wsel[g + 1] == wm;
+      finish_group(H, k, d, wm);
+      d.sync = next ? 0 : 1;
       if (!d.sync) ++n_warp_syncs;
       groups.push_back(d);
     }
