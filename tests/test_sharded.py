@@ -247,11 +247,14 @@ def _gpu_count():
 
 
 @pytest.mark.gpu
-@pytest.mark.skipif(_gpu_count() < 2, reason="needs two GPUs")
-def test_nccl_sharded_matches_oracle(tmp_path):
+@pytest.mark.parametrize("ranks", [2, 4])
+def test_nccl_sharded_matches_oracle(tmp_path, ranks):
+    if _gpu_count() < ranks:
+        pytest.skip(f"needs {ranks} GPUs")
     port = _free_port()
     out = tmp_path / "sharded.npz"
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={ranks}",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            str(ROOT / "tests" / "sharded_gpu_job.py"), str(out)]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
