@@ -127,3 +127,23 @@ def test_tiny_states_through_the_plan(n):
         want = want.reshape(-1, 2, 1 << q)
         want = np.einsum("ab,rbt->rat", u, want).reshape(-1)
     np.testing.assert_allclose(state.amps, want, atol=1e-13)
+
+
+@pytest.mark.parametrize("n", [25])
+def test_hbm_regime_layered_stream_then_adjoint_is_identity(n):
+    """Above the L2-resident size (tiles hold qubits 0..2, 128-byte runs) the
+    random layered circuit of BASELINE config 4 followed by its adjoint
+    returns |0...0>; 512 MiB state, every pass streams HBM."""
+    wl = W.layered_workload(n, 6, 2310)
+    fops, pool, _ = W.fuse_packed(wl.ops, wl.params, wl.payloads)
+    gates = fops[fops["kind"] == N.OP_GATE]
+    inv, inv_pool = _adjoint(gates, wl.params, pool)
+    state = StateVector(n)
+    fwd = DeviceProgram(state, gates, wl.params, pool)
+    fwd.run_mma()
+    assert abs(state.norm() - 1.0) < 1e-10
+    back = DeviceProgram(state, inv, np.zeros(1), inv_pool)
+    back.run_mma()
+    a = state.amps
+    assert abs(a[0] - 1.0) < 1e-10
+    assert np.linalg.norm(a[1:]) < 1e-10
