@@ -391,6 +391,8 @@ def run_ours(args, rank, world, local):
     e2e_times = []
     rng = np.random.Generator(np.random.Philox(7))
     for _ in range(max(1, args.e2e_steps)):
+        if world > 1:
+            torch.distributed.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         state.restart()
@@ -401,8 +403,12 @@ def run_ours(args, rank, world, local):
         e2e_times.append(time.perf_counter() - t0)
         del p2
     e2e_s = float(np.median(e2e_times))
-    h2d = exe.nbytes + wl.params.nbytes + pool.nbytes
-    d2h = probs.nbytes + 8 * info.n_measures
+    if world > 1:  # whole job: every rank's call, slowest rank's time
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    h2d = (exe.nbytes + wl.params.nbytes + pool.nbytes) * world
+    d2h = (probs.nbytes + 8 * info.n_measures) * world
 
     # roofline of the dominant kernel (k_blocked): algorithmic bytes =
     # passes x (read + write) x 16 B x 2^n per launch
@@ -458,7 +464,7 @@ def run_ours(args, rank, world, local):
             "fp64": {"achieved_tflops": round(fp64_ach, 3), "peak_tflops": round(fp64_peak, 2),
                      "frac": round(fp64_ach / fp64_peak, 4),
                      "flops_per_launch": info.flops},
-            "e2e": {"value": round(wl.input_gates / e2e_s, 1), "unit": UNIT,
+            "e2e": {"value": round(wl.input_gates * world / e2e_s, 1), "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "s_per_step": round(e2e_s, 4)},
             "wall_s": round(wall, 3), "gpu_launches": launches, "clocks": clk}
