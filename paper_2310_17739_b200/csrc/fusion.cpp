@@ -12,6 +12,10 @@
 // at most one pending run in merge_1q and fuse_2q (a gate touching it
 // flushes the others), so the reference's dict scans become array lookups.
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <string>
+#include <thread>
 #include <new>
 #include <stdexcept>
 
@@ -26,18 +30,26 @@ struct Fuser {
   const double* params;
   int variant;
   std::vector<double> pool;  // complex payloads, interleaved
+  // read-only payloads shared by the segments of a parallel fusion; offsets
+  // below n_base index `base`, the rest this fuser's own pool
+  const double* base = nullptr;
+  int64_t n_base = 0;
 
   int64_t push_payload(const double* m, int dim) {
-    const int64_t off = static_cast<int64_t>(pool.size() / 2);
+    const int64_t off = n_base + static_cast<int64_t>(pool.size() / 2);
     pool.insert(pool.end(), m, m + 2 * dim * dim);
     return off;
+  }
+
+  const double* payload(int64_t off) const {
+    return off < n_base ? base + 2 * off : pool.data() + 2 * (off - n_base);
   }
 
   // resolved_matrix (circuit.py:42-46) of a 1- or 2-qubit op
   void matrix(const nsb_op& op, double* out) const {
     const int dim = 1 << op.nq;
     if (op.payload >= 0) {
-      std::memcpy(out, pool.data() + 2 * op.payload, sizeof(double) * 2 * dim * dim);
+      std::memcpy(out, payload(op.payload), sizeof(double) * 2 * dim * dim);
       return;
     }
     CMat m;
@@ -281,6 +293,162 @@ std::vector<nsb_op> fuse_2q(Fuser& F, const std::vector<nsb_op>& in) {
   return out;
 }
 
+using Pass = std::vector<nsb_op> (*)(Fuser&, const std::vector<nsb_op>&);
+const Pass kPasses[4] = {merge_1q, absorb_1q, normalize_2q, fuse_2q};
+
+void run_passes(Fuser& F, std::vector<nsb_op>& cur, int pass_mask, int64_t* before,
+                int64_t* after) {
+  for (int p = 0; p < 4; ++p) {
+    before[p] = count_gates(cur);
+    if (pass_mask & (1 << p)) cur = kPasses[p](F, cur);
+    after[p] = count_gates(cur);
+  }
+}
+
+inline uint64_t op_mask(const nsb_op& o) {
+  uint64_t m = o.mask;
+  if (m == 0)
+    for (int j = 0; j < o.nq; ++j) m |= uint64_t(1) << o.q[j];
+  return m;
+}
+
+// Input record i as the passes see it (checked by validate_input first).
+inline nsb_op input_op(const nsb_op* ops, int64_t i) {
+  nsb_op o = ops[i];
+  o.mask = op_mask(o);
+  o.src = static_cast<int32_t>(i);
+  return o;
+}
+
+// The serial loop's checks, in its order (first bad record wins); returns
+// the union qubit mask and the extent of the input payload pool.
+uint64_t validate_input(const nsb_op* ops, int64_t n_ops, const double* payloads,
+                        int64_t* n_base) {
+  uint64_t all = 0;
+  int64_t ext = 0;
+  for (int64_t i = 0; i < n_ops; ++i) {
+    const nsb_op& o = ops[i];
+    if (o.nq < 0 || o.nq > 5) throw std::invalid_argument("op with bad qubit count");
+    if (o.kind == NSB_OP_GATE && o.payload >= 0) {
+      if (!payloads) throw std::invalid_argument("payload offset without payload pool");
+      ext = std::max<int64_t>(ext, o.payload + (int64_t(1) << (2 * o.nq)));
+    } else if (o.kind == NSB_OP_GATE && o.nq <= 2 && gate_arity(o.tag) != o.nq) {
+      throw std::invalid_argument("gate tag / qubit count mismatch");
+    }
+    all |= op_mask(o);
+  }
+  *n_base = ext;
+  return all;
+}
+
+// Segment boundaries for parallel fusion: just after every barrier whose qubit
+// set covers every qubit of the circuit.  Such a barrier flushes every pending
+// run of merge_1q and fuse_2q and resets absorb_1q's last-op table
+// (fusion.py:127, 149-150, 233), so no pass carries state across it and the
+// segments fuse independently to exactly the sequential result.  Small
+// circuits stay on one segment.
+std::vector<int64_t> segment_cuts(const nsb_op* ops, int64_t n_ops, uint64_t all) {
+  constexpr int64_t kMinSegmentOps = 1 << 15;
+  std::vector<int64_t> cuts{0};
+  if (n_ops >= 2 * kMinSegmentOps)
+    for (int64_t i = 0; i < n_ops; ++i)
+      if (ops[i].kind == NSB_OP_BARRIER && (op_mask(ops[i]) & all) == all &&
+          i + 1 - cuts.back() >= kMinSegmentOps && n_ops - (i + 1) >= kMinSegmentOps)
+        cuts.push_back(i + 1);
+  cuts.push_back(n_ops);
+  return cuts;
+}
+
+// The segments on host threads: each builds its records straight from the
+// input, runs the four passes with its own payload pool over the shared input
+// payloads (offsets below n_base unchanged), and copies its ops and pool into
+// the output at its offset (payload offsets rebased); pass counts summed.
+void fuse_segments(const nsb_op* ops, const double* params, const double* payloads,
+                   int64_t n_base, const std::vector<int64_t>& cuts, int pass_mask,
+                   int variant, nsb_fused* out) {
+  const size_t n_seg = cuts.size() - 1;
+  struct Seg {
+    std::vector<nsb_op> ops;
+    Fuser fz;
+    int64_t before[4], after[4];
+    int64_t op_off = 0, pool_off = 0;  // complex units, after n_base
+    std::string err;
+    bool oom = false;
+  };
+  std::vector<Seg> segs(n_seg);
+  for (Seg& sg : segs) {
+    sg.fz.params = params;
+    sg.fz.variant = variant;
+    sg.fz.base = payloads;
+    sg.fz.n_base = n_base;
+  }
+  const size_t hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  auto parallel = [&](auto&& body) {
+    std::atomic<size_t> next{0};
+    auto worker = [&]() {
+      for (size_t s; (s = next.fetch_add(1)) < n_seg;) {
+        try {
+          body(s);
+        } catch (const std::bad_alloc&) {
+          segs[s].oom = true;
+        } catch (const std::exception& e) {
+          segs[s].err = e.what();
+        }
+      }
+    };
+    std::vector<std::thread> threads;
+    for (size_t t = 1; t < std::min(hw, n_seg); ++t) threads.emplace_back(worker);
+    worker();
+    for (std::thread& t : threads) t.join();
+    for (const Seg& sg : segs) {  // the earliest segment's failure, as the serial order
+      if (sg.oom) throw std::bad_alloc();
+      if (!sg.err.empty()) throw std::runtime_error(sg.err);
+    }
+  };
+  parallel([&](size_t s) {
+    Seg& sg = segs[s];
+    sg.ops.reserve(cuts[s + 1] - cuts[s]);
+    for (int64_t i = cuts[s]; i < cuts[s + 1]; ++i) sg.ops.push_back(input_op(ops, i));
+    run_passes(sg.fz, sg.ops, pass_mask, sg.before, sg.after);
+  });
+  int64_t n_out = 0, n_pool = n_base;
+  for (Seg& sg : segs) {
+    sg.op_off = n_out;
+    sg.pool_off = n_pool;
+    n_out += static_cast<int64_t>(sg.ops.size());
+    n_pool += static_cast<int64_t>(sg.fz.pool.size() / 2);
+  }
+  for (int p = 0; p < 4; ++p) {
+    out->pass_before[p] = out->pass_after[p] = 0;
+    for (const Seg& sg : segs) {
+      out->pass_before[p] += sg.before[p];
+      out->pass_after[p] += sg.after[p];
+    }
+  }
+  out->gates_before = out->pass_before[0];
+  out->n_ops = n_out;
+  out->n_payload = n_pool;
+  out->ops = static_cast<nsb_op*>(std::malloc(sizeof(nsb_op) * std::max<int64_t>(n_out, 1)));
+  out->payloads = static_cast<double*>(std::malloc(sizeof(double) * 2 * std::max<int64_t>(n_pool, 1)));
+  if (!out->ops || !out->payloads) throw std::bad_alloc();
+  if (n_base > 0) std::memcpy(out->payloads, payloads, sizeof(double) * 2 * n_base);
+  parallel([&](size_t s) {
+    Seg& sg = segs[s];
+    const int64_t shift = sg.pool_off - n_base;
+    nsb_op* dst = out->ops + sg.op_off;
+    for (size_t i = 0; i < sg.ops.size(); ++i) {
+      nsb_op o = sg.ops[i];
+      if (o.payload >= n_base) o.payload += shift;
+      dst[i] = o;
+    }
+    if (!sg.fz.pool.empty())
+      std::memcpy(out->payloads + 2 * sg.pool_off, sg.fz.pool.data(),
+                  sizeof(double) * sg.fz.pool.size());
+    std::vector<nsb_op>().swap(sg.ops);
+    std::vector<double>().swap(sg.fz.pool);
+  });
+}
+
 }  // namespace
 
 int fuse(const nsb_op* ops, int64_t n_ops, const double* params, const double* payloads,
@@ -295,6 +463,14 @@ int fuse(const nsb_op* ops, int64_t n_ops, const double* params, const double* p
   }
   std::memset(out, 0, sizeof(*out));
   try {
+    int64_t n_base = 0;
+    const uint64_t all = validate_input(ops, n_ops, payloads, &n_base);
+    const std::vector<int64_t> cuts = segment_cuts(ops, n_ops, all);
+    if (cuts.size() > 2 && !std::getenv("NSB_FUSE_SERIAL")) {  // (serial: parity tests)
+      fuse_segments(ops, params, payloads, n_base, cuts, pass_mask, variant, out);
+      set_status(st, NSB_OK, "");
+      return NSB_OK;
+    }
     Fuser F{params, variant, {}};
     std::vector<nsb_op> cur;
     cur.reserve(n_ops);
@@ -314,13 +490,7 @@ int fuse(const nsb_op* ops, int64_t n_ops, const double* params, const double* p
       cur.push_back(o);
     }
     out->gates_before = count_gates(cur);
-    using Pass = std::vector<nsb_op> (*)(Fuser&, const std::vector<nsb_op>&);
-    const Pass passes[4] = {merge_1q, absorb_1q, normalize_2q, fuse_2q};
-    for (int p = 0; p < 4; ++p) {
-      out->pass_before[p] = count_gates(cur);
-      if (pass_mask & (1 << p)) cur = passes[p](F, cur);
-      out->pass_after[p] = count_gates(cur);
-    }
+    run_passes(F, cur, pass_mask, out->pass_before, out->pass_after);
     out->n_ops = static_cast<int64_t>(cur.size());
     out->ops = static_cast<nsb_op*>(std::malloc(sizeof(nsb_op) * std::max<size_t>(cur.size(), 1)));
     out->n_payload = static_cast<int64_t>(F.pool.size() / 2);

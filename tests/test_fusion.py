@@ -147,3 +147,48 @@ def test_gate_count_excludes_markers():
     c.barrier()
     c.measure(1, 0)
     assert gate_count(c) == 1
+
+
+def test_segment_parallel_fusion_equals_serial_and_oracle(monkeypatch, golden_variant):
+    """Circuits above 2 x 2^15 records fuse on host threads, split after barriers
+    that cover every qubit (csrc/fusion.cpp segment_cuts); the result must be
+    the serial pipeline's, which is the reference's (fusion.py:240-251)."""
+    rng = np.random.default_rng(2310)
+    n = 6
+    c = Circuit(n, [("c", 2)])
+    pool1 = [Gate.H, Gate.RX, Gate.RZ, Gate.U3]
+    pool2 = [Gate.CX, Gate.CZ, Gate.RZZ, Gate.CU3]
+    payload = None
+    for i in range(150_000):
+        if i % 37_000 == 36_999:
+            c.barrier()  # full barrier: a segment boundary
+            continue
+        r = rng.random()
+        if r < 0.45:
+            g = pool1[rng.integers(len(pool1))]
+            c.gate_op(g, (int(rng.integers(n)),), tuple(rng.uniform(-3, 3, g.n_params)))
+        elif r < 0.93:
+            g = pool2[rng.integers(len(pool2))]
+            a, b = rng.choice(n, 2, replace=False)
+            c.gate_op(g, (int(a), int(b)), tuple(rng.uniform(-3, 3, g.n_params)))
+        elif r < 0.95:
+            if payload is None:
+                payload = gate_matrix(Gate.CU3, (0.3, -1.1, 0.7))
+            a, b = rng.choice(n, 2, replace=False)
+            c.fused_2q(payload, int(a), int(b))  # input payload records
+        elif r < 0.96:
+            c.gate_op(Gate.CCX, tuple(int(q) for q in rng.choice(n, 3, replace=False)))
+        elif r < 0.98:
+            c.barrier(*(int(q) for q in rng.choice(n, 2, replace=False)))  # partial: no cut
+        else:
+            q = int(rng.integers(n))
+            c.measure(q, 0)
+            c.reset(q)
+    par, s_par = fuse_pipeline(c)
+    monkeypatch.setenv("NSB_FUSE_SERIAL", "1")
+    ser, s_ser = fuse_pipeline(c)
+    assert s_par == s_ser
+    want = oracle_from_circuit(ser)
+    assert_same(par, want)
+    ref, _ = O.fuse_pipeline(oracle_from_circuit(c), golden_variant)
+    assert_same(par, ref)
