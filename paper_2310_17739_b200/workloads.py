@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -120,13 +121,22 @@ class Workload:
         return ops[:end]
 
 
+def _adopt(ptr, n_bytes: int) -> np.ndarray:
+    """A uint8 array over a library-allocated buffer, released with nsb_free
+    when the last view of it goes (no copy: 10^8-gate plans are GBs)."""
+    addr = ctypes.cast(ptr, ctypes.c_void_p).value
+    buf = (ctypes.c_uint8 * n_bytes).from_address(addr)
+    weakref.finalize(buf, N.lib().nsb_free, ctypes.c_void_p(addr))
+    return np.frombuffer(buf, np.uint8)
+
+
 def _take_fused(f: N.Fused) -> tuple[np.ndarray, np.ndarray]:
-    raw = np.ctypeslib.as_array(ctypes.cast(f.ops, ctypes.POINTER(ctypes.c_uint8)),
-                                shape=(max(f.n_ops, 1) * N.OP_DTYPE.itemsize,))
-    ops = raw.view(N.OP_DTYPE)[: f.n_ops].copy()
+    """Take ownership of nsb_fused's buffers (f's pointers are cleared)."""
+    ops = _adopt(f.ops, max(f.n_ops, 1) * N.OP_DTYPE.itemsize).view(N.OP_DTYPE)[: f.n_ops]
+    f.ops = None
     if f.payloads and f.n_payload > 0:
-        pool = np.ctypeslib.as_array(f.payloads, shape=(2 * f.n_payload,)).copy()
-        pool = pool.view(np.complex128)
+        pool = _adopt(f.payloads, 16 * f.n_payload).view(np.complex128)
+        f.payloads = None
     else:
         pool = np.zeros(1, np.complex128)
     return ops, pool
