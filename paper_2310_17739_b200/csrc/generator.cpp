@@ -4,6 +4,9 @@
 // into the packed op list so 10^8-gate workloads never become Python objects.
 // Parameters are deduplicated: every (filter step, term) pair shares one
 // params-pool slot across its Trotter slices.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <new>
 #include <stdexcept>
 
@@ -13,9 +16,31 @@ namespace nsb {
 namespace {
 
 struct Emitter {
-  std::vector<nsb_op> ops;
+  // the op list is written straight into the malloc'd output buffer (10^8
+  // records are GBs: no second copy); `cap` is an upper bound fixed up front
+  nsb_op* ops = nullptr;
+  size_t n_ops = 0, cap = 0;
   std::vector<double> params;
   int n;  // register width (system + ancilla)
+
+  ~Emitter() { std::free(ops); }
+  void reserve(size_t c) {
+    ops = static_cast<nsb_op*>(std::malloc(sizeof(nsb_op) * std::max<size_t>(c, 1)));
+    if (!ops) throw std::bad_alloc();
+    cap = c;
+  }
+  void push(const nsb_op& o) {
+    if (n_ops == cap) throw std::logic_error("generator op count bound exceeded");
+    ops[n_ops++] = o;
+  }
+  // append `times` copies of records [b, e) (identical Trotter slices)
+  void repeat(size_t b, size_t e, int64_t times) {
+    const size_t len = e - b;
+    if (n_ops + len * static_cast<size_t>(times) > cap)
+      throw std::logic_error("generator op count bound exceeded");
+    for (int64_t r = 0; r < times; ++r, n_ops += len)
+      std::memcpy(ops + n_ops, ops + b, sizeof(nsb_op) * len);
+  }
 
   void gate(int tag, int a, int b = -1, int64_t param = -1) {
     nsb_op o{};
@@ -30,7 +55,7 @@ struct Emitter {
     o.param = param;
     o.payload = -1;
     o.mask = (uint64_t(1) << a) | (b >= 0 ? uint64_t(1) << b : 0);
-    ops.push_back(o);
+    push(o);
   }
   void marker(int kind, int q, int cbit) {
     nsb_op o{};
@@ -46,7 +71,7 @@ struct Emitter {
     o.payload = -1;
     o.mask = kind == NSB_OP_BARRIER ? ((n == 64) ? ~uint64_t(0) : (uint64_t(1) << n) - 1)
                                     : uint64_t(1) << q;
-    ops.push_back(o);
+    push(o);
   }
   int64_t param(double v) {
     params.push_back(v);
@@ -81,7 +106,7 @@ int generate_filter(int n_system, const uint8_t* letters, const double* coeffs, 
       const int m = static_cast<int>(involved[t].size());
       body_gates += m == 0 ? 1 : 2 * m + 5 + 4 * m;
     }
-    E.ops.reserve(static_cast<size_t>(n_steps * (trotter * body_gates + 5) + n_system + 1 + 64));
+    E.reserve(static_cast<size_t>(n_steps * (trotter * body_gates + 5) + n_system + 1 + 64));
     if (trial)
       for (int q = 0; q < n_system; ++q)
         if (trial[q]) E.gate(NSB_GATE_X, q);
@@ -92,7 +117,10 @@ int generate_filter(int n_system, const uint8_t* letters, const double* coeffs, 
         const double theta = coeffs[t] * t_i / static_cast<double>(trotter);
         theta_slot[t] = E.param(2.0 * theta);
       }
-      for (int64_t r = 0; r < trotter; ++r) {
+      // every slice of a step is the same record sequence (the step's
+      // parameter slots are shared): emit one, copy it trotter - 1 times
+      const size_t slice0 = E.n_ops;
+      {
         for (int64_t t = 0; t < n_terms; ++t) {
           const std::vector<int>& inv = involved[t];
           const uint8_t* L = letters + t * n_system;
@@ -126,6 +154,7 @@ int generate_filter(int n_system, const uint8_t* letters, const double* coeffs, 
           }
         }
       }
+      E.repeat(slice0, E.n_ops, trotter - 1);
       E.gate(NSB_GATE_RY, anc, -1, E.param(2.0 * delta));
       E.marker(NSB_OP_MEASURE, anc, i);
       E.marker(NSB_OP_BARRIER, -1, -1);
@@ -133,16 +162,17 @@ int generate_filter(int n_system, const uint8_t* letters, const double* coeffs, 
       E.marker(NSB_OP_BARRIER, -1, -1);
     }
     for (int q = 0; q <= n_system; ++q) E.marker(NSB_OP_MEASURE, q, n_steps + q);
-    out->n_ops = static_cast<int64_t>(E.ops.size());
-    out->ops = static_cast<nsb_op*>(std::malloc(sizeof(nsb_op) * E.ops.size()));
     *params_out = static_cast<double*>(std::malloc(sizeof(double) * std::max<size_t>(1, E.params.size())));
-    if (!out->ops || !*params_out) throw std::bad_alloc();
-    std::memcpy(out->ops, E.ops.data(), sizeof(nsb_op) * E.ops.size());
+    if (!*params_out) throw std::bad_alloc();
     std::memcpy(*params_out, E.params.data(), sizeof(double) * E.params.size());
     *n_params_out = static_cast<int64_t>(E.params.size());
     int64_t g = 0;
-    for (const nsb_op& o : E.ops) g += o.kind == NSB_OP_GATE;
+    for (size_t i = 0; i < E.n_ops; ++i) g += E.ops[i].kind == NSB_OP_GATE;
     out->gates_before = g;
+    out->n_ops = static_cast<int64_t>(E.n_ops);
+    nsb_op* shrunk = static_cast<nsb_op*>(std::realloc(E.ops, sizeof(nsb_op) * std::max<size_t>(E.n_ops, 1)));
+    out->ops = shrunk ? shrunk : E.ops;
+    E.ops = nullptr;  // owned by out
   } catch (const std::bad_alloc&) {
     std::free(out->ops);
     out->ops = nullptr;
