@@ -400,8 +400,8 @@ def run_ours(args, rank, world, local):
         p2.run_mma()
         state.device_call("nsb_probabilities", N.ptr(probs))
         _sample_from(probs, n, 1024, rng)
+        del p2  # the program is released inside the call, as run() does
         e2e_times.append(time.perf_counter() - t0)
-        del p2
     e2e_s = float(np.median(e2e_times))
     if world > 1:  # whole job: every rank's call, slowest rank's time
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)

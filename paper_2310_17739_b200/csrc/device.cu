@@ -25,6 +25,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <thread>
 
 #include "device.cuh"
 #include "planner_host.h"
@@ -1672,6 +1673,15 @@ int nsb_plan_create(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const double* 
 void nsb_plan_destroy(nsb_plan* plan) {
   if (!plan) return;
   if (plan->ctx) cudaSetDevice(plan->ctx->device);
+  // the host-side program (hundreds of MB for long circuits) is released on a
+  // detached thread: returning its pages is off the caller's path
+  HostPlan* host = nullptr;
+  try {
+    host = new HostPlan(std::move(plan->host));
+    std::thread([host] { delete host; }).detach();
+  } catch (...) {
+    delete host;  // no thread: release inline
+  }
   delete plan;
 }
 
