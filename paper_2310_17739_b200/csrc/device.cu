@@ -1102,23 +1102,34 @@ template <class T>
 struct DevBuf {
   T* ptr = nullptr;
   size_t count = 0;
-  void alloc(size_t n) {
+  // non-null: stream-ordered allocation (cudaMallocAsync / cudaFreeAsync on
+  // `stream`), so releasing a plan's buffers does not synchronise the device
+  cudaStream_t stream = nullptr;
+  void alloc(size_t n, cudaStream_t s = nullptr) {
     release();
     if (n == 0) n = 1;
-    cudaError_t e = cudaMalloc(&ptr, n * sizeof(T));
+    cudaError_t e = s ? cudaMallocAsync(reinterpret_cast<void**>(&ptr), n * sizeof(T), s)
+                      : cudaMalloc(&ptr, n * sizeof(T));
     if (e != cudaSuccess) {
       ptr = nullptr;
       throw std::bad_alloc();
     }
+    stream = s;
     count = n;
   }
   void upload(const T* src, size_t n, cudaStream_t s) {
-    alloc(n);
+    alloc(n, s);
     if (n) NSB_CUDA(cudaMemcpyAsync(ptr, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
   }
   void release() {
-    if (ptr) cudaFree(ptr);
+    if (ptr) {
+      if (stream)
+        cudaFreeAsync(ptr, stream);
+      else
+        cudaFree(ptr);
+    }
     ptr = nullptr;
+    stream = nullptr;
     count = 0;
   }
   ~DevBuf() { release(); }
@@ -1162,6 +1173,18 @@ struct nsb_plan {
   DevBuf<unsigned> bar;
   double last_ms = 0.0;
   int64_t last_launches = 0;
+  // the plan's own stream for releasing its buffers: stream-ordered frees
+  // (no device-wide synchronise) that do not depend on the context outliving
+  // the plan; every run synchronises the context stream before returning
+  int device = 0;
+  cudaStream_t rel = nullptr;
+  ~nsb_plan() {
+    if (rel) cudaSetDevice(device);
+    passes.release(); mma_passes.release(); groups.release(); ops.release();
+    mats.release(); dense.release(); record.release(); partials.release();
+    fail.release(); bar.release();
+    if (rel) cudaStreamDestroy(rel);
+  }
 };
 
 namespace {
@@ -1428,6 +1451,13 @@ int nsb_ctx_create(int32_t device, nsb_ctx** out, nsb_status* st) {
     ctx->device = device;
     NSB_CUDA(cudaSetDevice(device));
     NSB_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    {  // plan buffers come from the device's default pool: keep up to 8 GiB
+       // cached across plans instead of returning it at every synchronise
+      cudaMemPool_t pool;
+      NSB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+      uint64_t keep = uint64_t(8) << 30;
+      NSB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     NSB_CUDA(cudaEventCreate(&ctx->ev0));
     NSB_CUDA(cudaEventCreate(&ctx->ev1));
     NSB_CUDA(cudaEventCreate(&ctx->tev0));
@@ -1650,6 +1680,8 @@ int nsb_plan_create(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const double* 
     if (n_ops < 0 || (n_ops > 0 && !ops)) throw std::invalid_argument("bad op list");
     NSB_CUDA(cudaSetDevice(c->device));
     P->ctx = c;
+    P->device = c->device;
+    NSB_CUDA(cudaStreamCreateWithFlags(&P->rel, cudaStreamNonBlocking));
     P->host.build(ops, n_ops, params, payloads, c->n, c->blocked_grid);
     HostPlan& H = P->host;
     P->passes.upload(H.passes.data(), H.passes.size(), c->stream);
@@ -1660,11 +1692,16 @@ int nsb_plan_create(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const double* 
                    c->stream);
     P->dense.upload(reinterpret_cast<const double2*>(H.dense_mats.data()),
                     H.dense_mats.size() / 2, c->stream);
-    P->record.alloc(std::max<int64_t>(H.n_measures, 1));
-    P->partials.alloc(2 * size_t(std::max(c->blocked_grid, 1)));
-    P->fail.alloc(2);
-    P->bar.alloc(1);
+    P->record.alloc(std::max<int64_t>(H.n_measures, 1), c->stream);
+    P->partials.alloc(2 * size_t(std::max(c->blocked_grid, 1)), c->stream);
+    P->fail.alloc(2, c->stream);
+    P->bar.alloc(1, c->stream);
     NSB_CUDA(cudaStreamSynchronize(c->stream));
+    for (cudaStream_t* bs : {&P->passes.stream, &P->mma_passes.stream, &P->groups.stream,
+                             &P->ops.stream, &P->mats.stream, &P->dense.stream,
+                             &P->record.stream, &P->partials.stream, &P->fail.stream,
+                             &P->bar.stream})
+      *bs = P->rel;
   });
   if (rc == NSB_OK) *out = P.release();
   return rc;
@@ -1672,7 +1709,7 @@ int nsb_plan_create(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const double* 
 
 void nsb_plan_destroy(nsb_plan* plan) {
   if (!plan) return;
-  if (plan->ctx) cudaSetDevice(plan->ctx->device);
+  cudaSetDevice(plan->device);
   // the host-side program (hundreds of MB for long circuits) is released on a
   // detached thread: returning its pages is off the caller's path
   HostPlan* host = nullptr;
