@@ -18,7 +18,9 @@ e2e    through the C ABI with host buffers: per step the packed fused op list
        back (D2H) and sampled on the host -- what `run()` does per call.
 cpu_baseline / --impl reference: the oracle port of the reference engine
        (numpy einsum, as nucsim.engine) on a bounded prefix of the same fused
-       gate stream, single-threaded, extrapolated per gate.
+       gate stream, single-threaded, extrapolated per gate.  The reference
+       arm never imports the product: deep21's fused stream is the prefix
+       the unmodified reference produced (tests/golden/deep21.npz).
 
 Multi-GPU (torchrun, N > 1), default configs: replicas -- every rank runs
 the same circuit on its own GPU (no data-path collective), value = total
@@ -149,66 +151,146 @@ class Clocks:
                 "samples": len(sm)}
 
 
-def cpu_reference(exe, pool, params, n, input_per_fused, budget_s=12.0):
-    """Oracle port of nucsim.engine on a prefix of the fused stream."""
+# ---------------------------------------------------------------------------
+# CPU reference arm (--impl reference) and cpu_baseline: the oracle port of the
+# reference engine (oracle/nucsim_oracle.py, numpy einsum exactly as
+# nucsim/engine.py:92-156) on a bounded prefix of the SAME fused stream.  This
+# path never imports paper_2310_17739_b200: the deep21 fused stream comes from
+# tests/golden/deep21.npz (the first 1 500 fused gates the unmodified reference
+# itself produced, make_deep21_golden.py), rand28's from a pure-numpy restatement
+# of workloads.layered_workload fused by the oracle's fuse_pipeline.
+
+
+def host_cpu() -> dict:
+    model = "unknown"
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def _oracle():
     sys.path.insert(0, str(ROOT / "oracle"))
-    import nucsim_oracle as O
-    from paper_2310_17739_b200 import gate_matrix
-    from paper_2310_17739_b200.gates import BY_CODE
+    sys.path.insert(0, str(ROOT / "tests"))
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    import nucsim_oracle as O
+    return O
+
+
+def reference_stream(config: str, trotter: int | None):
+    """(oracle IR prefix of the fused stream, n_qubits, input gates, fused gates)
+    of the bench workload, without the product package."""
+    O = _oracle()
+    if config == "deep21":
+        if trotter not in (None, 18):
+            raise SystemExit("the reference arm's deep21 sample is the Trotter-18 headline")
+        from circuit_io import to_oracle
+        d = dict(np.load(ROOT / "tests" / "golden" / "deep21.npz"))
+        instrs, n = to_oracle(d, "prefix_")
+        return instrs, n, int(d["fused_stats"][0]), int(d["fused_stats"][1])
+    if config == "rand28":  # workloads.layered_workload(28, layers, seed 28), restated
+        import math
+        n, layers = 28, trotter or 20
+        rng = np.random.default_rng(28)
+        instrs = []
+        for _ in range(layers):
+            for q in range(n):
+                instrs.append(("u3", (q,), tuple(float(x) for x in rng.uniform(-math.pi, math.pi, 3)),
+                               None, None))
+            perm = rng.permutation(n)
+            for k in range(0, n - 1, 2):
+                a, b = int(perm[k]), int(perm[k + 1])
+                g = ("cx", "cz", "rzz")[int(rng.integers(3))]
+                ps = (float(rng.uniform(-math.pi, math.pi)),) if g == "rzz" else ()
+                instrs.append((g, (a, b), ps, None, None))
+        fused = O.fuse_pipeline(instrs)[0]
+        return fused, n, len(instrs), O.gate_count(fused)
+    raise SystemExit(f"unknown config {config}")
+
+
+def cpu_sample(instrs, n, input_per_fused, budget_s):
+    """Oracle port on the fused stream from |0...0>, fused gates applied in
+    order until `budget_s` seconds have passed; input gates/s extrapolated."""
+    O = _oracle()
     a = np.zeros(1 << n, np.complex128)
     a[0] = 1.0
     done = 0
     t0 = time.perf_counter()
-    for rec in exe:
-        if rec["kind"] != 0:
-            if rec["kind"] == 1:
-                p0 = O.branch_probability(a, int(rec["q"][0]), 0)
-                O.project(a, int(rec["q"][0]), 0, p0)
+    for ins in instrs:
+        name, qs = ins[0], tuple(ins[1])
+        if name in ("barrier", "reset"):
             continue
-        k = int(rec["nq"])
-        if rec["payload"] >= 0:
-            off = int(rec["payload"])
-            m = pool[off:off + 4 ** k].reshape(2 ** k, 2 ** k)
-        else:
-            g = BY_CODE[int(rec["tag"])]
-            p = tuple(params[int(rec["param"]):int(rec["param"]) + g.n_params]) if g.n_params else ()
-            m = gate_matrix(g, p)
-        a = O.apply_dense(a, m, tuple(int(x) for x in rec["q"][:k]))
+        if name == "measure":
+            p0 = O.branch_probability(a, qs[0], 0)
+            O.project(a, qs[0], 0, p0)
+            continue
+        a = O.apply_dense(a, O.resolved(ins), qs)
         done += 1
         if time.perf_counter() - t0 > budget_s:
             break
     dt = time.perf_counter() - t0
-    return {"value": round(done * input_per_fused / dt, 3), "unit": UNIT, "cores": 1,
-            "kind": "port",
-            "sample": f"first {done} fused gates of the same workload at {n} qubits "
-                      f"({dt:.1f} s, numpy einsum single thread), scaled by input/fused "
-                      f"gate ratio {input_per_fused:.3f}"}
+    return done, dt, done * input_per_fused / dt
+
+
+def cpu_baseline(args, budget_s: float) -> dict:
+    instrs, n, n_in, n_fused = reference_stream(args.config, args.trotter)
+    ratio = n_in / max(n_fused, 1)
+    done, dt, value = cpu_sample(instrs, n, ratio, budget_s)
+    return {"value": round(value, 3), "unit": UNIT, "cores": 1, "kind": "port", **host_cpu(),
+            "sample": f"first {done} fused gates of the same fused stream at {n} qubits "
+                      f"({dt:.1f} s; oracle port of nucsim.engine, numpy einsum, one thread: "
+                      f"the reference's gate kernels are single-threaded), scaled by the "
+                      f"input/fused gate ratio {ratio:.3f}"}
 
 
 def run_reference(args, rank):
+    """--impl reference: rank 0 times the oracle port on bounded samples
+    (each step = fused gates from |0...0> for --ref-step-s seconds)."""
     if rank != 0:
         return
-    wl, exe, pool, stats, host = make_workload(args.config, args.trotter)
-    ratio = wl.input_gates / max(stats["gates_after"], 1)
-    vals = []
-    cb = None
+    instrs, n, n_in, n_fused = reference_stream(args.config, args.trotter)
+    ratio = n_in / max(n_fused, 1)
+    for _ in range(args.warmup):
+        cpu_sample(instrs, n, ratio, 0.2)
+    gates = secs = 0.0
     for _ in range(args.steps):
-        cb = cpu_reference(exe, pool, wl.params, wl.n_qubits, ratio, budget_s=args.ref_budget)
-        vals.append(cb["value"])
-    value = float(np.mean(vals))
-    cb["value"] = value
-    cb["cores"] = 1
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+        done, dt, _ = cpu_sample(instrs, n, ratio, args.ref_step_s)
+        gates += done
+        secs += dt
+    value = gates * ratio / secs
+    line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(secs * 1e3 / args.steps, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": workload_name(args), "n_qubits": wl.n_qubits,
-                       "input_gates": wl.input_gates, "fused_gates": stats["gates_after"]},
-            "cpu_baseline": cb,
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+            "config": workload_config(args, n, n_in, n_fused, args.gpus),
+            "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": 1, "kind": "port",
+                             **host_cpu(),
+                             "sample": f"{args.steps} steps x {args.ref_step_s:.1f} s: "
+                                       f"{int(gates)} fused gates of the same fused stream "
+                                       f"from |0...0> at {n} qubits (oracle port of "
+                                       f"nucsim.engine, numpy einsum, one thread), scaled by "
+                                       f"the input/fused ratio {ratio:.3f}"},
+            "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def workload_config(args, n, input_gates, fused_gates, world) -> dict:
+    """The `config` both arms print (workload identity only)."""
+    c = {"workload": workload_name(args), "n_qubits": n, "input_gates": input_gates,
+         "fused_gates": fused_gates, "parallelism": f"replicas{world}",
+         "l2": "flushed between steps (256 MiB write); state (2^n x 16 B) L2-resident "
+               "within a step when it fits"}
+    if args.config == "deep21":
+        c.update({"trotter": args.trotter or 18, "filter_steps": 8})
+    else:
+        c.update({"layers": args.trotter or 20})
+    return c
 
 
 def workload_name(args) -> str:
@@ -430,20 +512,17 @@ def run_ours(args, rank, world, local):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
             "data": "synthetic",
-            "config": {"workload": workload_name(args), "n_qubits": n,
-                       "input_gates": wl.input_gates, "fused_gates": stats["gates_after"],
-                       "fusion_reduction": round(wl.input_gates / max(stats["gates_after"], 1), 3),
-                       "passes": info.n_passes,
-                       "device_gate_ops": info.n_device_gates,
-                       "octet_sweeps": info.n_sweeps,
-                       "group_fused_ops": info.n_fused_group_ops,
-                       "frame_absorbed_gates": info.n_frame_gates,
-                       "frame_flush_gates": info.n_flush_gates,
-                       "gates_per_pass": round(info.n_gates / max(info.n_passes, 1), 2),
-                       "tile_qubits": info.tile_qubits, "parallelism": f"replicas{world}",
-                       "l2": "flushed between steps (256 MiB write); state (2^n x 16 B) "
-                             "L2-resident within a step when it fits",
-                       **{k: v for k, v in wl.meta.items() if k != "terms"}},
+            "config": workload_config(args, n, wl.input_gates, stats["gates_after"], world),
+            "plan": {"fusion_reduction": round(wl.input_gates / max(stats["gates_after"], 1), 3),
+                     "passes": info.n_passes,
+                     "device_gate_ops": info.n_device_gates,
+                     "octet_sweeps": info.n_sweeps,
+                     "group_fused_ops": info.n_fused_group_ops,
+                     "frame_absorbed_gates": info.n_frame_gates,
+                     "frame_flush_gates": info.n_flush_gates,
+                     "gates_per_pass": round(info.n_gates / max(info.n_passes, 1), 2),
+                     "tile_qubits": info.tile_qubits,
+                     **{k: v for k, v in wl.meta.items() if k != "terms"}},
             "host": host,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
                          "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
@@ -469,8 +548,7 @@ def run_ours(args, rank, world, local):
                     "s_per_step": round(e2e_s, 4)},
             "wall_s": round(wall, 3), "gpu_launches": launches, "clocks": clk}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ratio = wl.input_gates / max(stats["gates_after"], 1)
-        line["cpu_baseline"] = cpu_reference(exe, pool, wl.params, n, ratio, args.ref_budget)
+        line["cpu_baseline"] = cpu_baseline(args, args.ref_budget)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -487,7 +565,10 @@ def main():
     ap.add_argument("--qubits", type=int, default=34, help="--config shard: total qubits")
     ap.add_argument("--trotter", type=int, default=None)
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--ref-budget", type=float, default=12.0)
+    ap.add_argument("--ref-budget", type=float, default=12.0,
+                    help="cpu_baseline sample length (s)")
+    ap.add_argument("--ref-step-s", type=float, default=1.5,
+                    help="--impl reference: seconds of oracle work per timed step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     rank, world, local = dist_env()

@@ -299,7 +299,12 @@ int nsb_timer_stop(nsb_ctx* ctx, double* ms, nsb_status* st);
  * element pairs are split in chunks, this rank swaps the chunks of its
  * parity with one kernel that reads and writes both shards directly (no
  * staging copies, no pack / unpack), between two stream-ordered barriers.
- * Collective: both partners must call it (after nsb_shard_open_peers). */
+ * Collective: both partners must call it (after nsb_shard_open_peers).
+ * Opening checks that every rank's shard has this rank's size and re-maps
+ * shards that were already mapped.  nsb_shard_close_peers (collective):
+ * unmap them and rendezvous, so no rank frees or reallocates its exported
+ * shard while a partner still maps it; nsb_state_init refuses to resize a
+ * shard while peers are mapped. */
 int nsb_comm_unique_id(uint8_t* id, nsb_status* st);
 int nsb_comm_init(nsb_ctx* ctx, const uint8_t* id, int32_t nranks, int32_t rank,
                   nsb_status* st);
@@ -311,6 +316,7 @@ int nsb_shard_allgather(nsb_ctx* ctx, const double* in, int32_t count, double* o
 int nsb_shard_ipc_handle(nsb_ctx* ctx, uint8_t* handle, nsb_status* st);
 int nsb_shard_open_peers(nsb_ctx* ctx, const uint8_t* handles, nsb_status* st);
 int nsb_shard_swap_p2p(nsb_ctx* ctx, int32_t global_bit, int32_t local_q, nsb_status* st);
+int nsb_shard_close_peers(nsb_ctx* ctx, nsb_status* st);
 
 #ifdef __cplusplus
 }

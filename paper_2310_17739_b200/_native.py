@@ -131,6 +131,7 @@ _SIGNATURES = {
     "nsb_shard_allgather": (ctypes.c_int, [_P, _P, _I32, _P, _ST]),
     "nsb_shard_ipc_handle": (ctypes.c_int, [_P, _P, _ST]),
     "nsb_shard_open_peers": (ctypes.c_int, [_P, _P, _ST]),
+    "nsb_shard_close_peers": (ctypes.c_int, [_P, _ST]),
     "nsb_shard_swap_p2p": (ctypes.c_int, [_P, _I32, _I32, _ST]),
 }
 

@@ -18,10 +18,14 @@
 #include <nccl.h>  // types only: libnccl is resolved at run time (shard_nccl)
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <deque>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -1102,13 +1106,15 @@ template <class T>
 struct DevBuf {
   T* ptr = nullptr;
   size_t count = 0;
-  // non-null: stream-ordered allocation (cudaMallocAsync / cudaFreeAsync on
-  // `stream`), so releasing a plan's buffers does not synchronise the device
+  // non-null: stream-ordered allocation from the context's private plan pool
+  // (cudaMallocFromPoolAsync / cudaFreeAsync on `stream`), so releasing a
+  // plan's buffers does not synchronise the device
   cudaStream_t stream = nullptr;
-  void alloc(size_t n, cudaStream_t s = nullptr) {
+  void alloc(size_t n, cudaStream_t s = nullptr, cudaMemPool_t pool = nullptr) {
     release();
     if (n == 0) n = 1;
-    cudaError_t e = s ? cudaMallocAsync(reinterpret_cast<void**>(&ptr), n * sizeof(T), s)
+    cudaError_t e = s ? cudaMallocFromPoolAsync(reinterpret_cast<void**>(&ptr), n * sizeof(T),
+                                                pool, s)
                       : cudaMalloc(&ptr, n * sizeof(T));
     if (e != cudaSuccess) {
       ptr = nullptr;
@@ -1117,8 +1123,8 @@ struct DevBuf {
     stream = s;
     count = n;
   }
-  void upload(const T* src, size_t n, cudaStream_t s) {
-    alloc(n, s);
+  void upload(const T* src, size_t n, cudaStream_t s, cudaMemPool_t pool) {
+    alloc(n, s, pool);
     if (n) NSB_CUDA(cudaMemcpyAsync(ptr, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
   }
   void release() {
@@ -1138,7 +1144,11 @@ struct DevBuf {
 }  // namespace
 
 struct nsb_ctx {
+  // one reference held by the owner (nsb_ctx_destroy drops it) and one by
+  // every live plan, so a plan never outlives the context it runs on
+  std::atomic<int> refs{1};
   int device = 0;
+  cudaMemPool_t plan_pool = nullptr;  // private stream-ordered pool for plan buffers
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t tev0 = nullptr, tev1 = nullptr;  // nsb_timer_start / stop
@@ -1162,7 +1172,8 @@ struct nsb_ctx {
 };
 
 struct nsb_plan {
-  nsb_ctx* ctx = nullptr;
+  nsb_ctx* ctx = nullptr;  // holds a reference (ctx->refs)
+  int n = 0;               // qubit count the plan was built for
   HostPlan host;
   DevBuf<PassDesc> passes, mma_passes;
   DevBuf<GroupDesc> groups;
@@ -1257,8 +1268,13 @@ int fail_status(nsb_status* st, int code, const std::string& msg) {
   return code;
 }
 
+// Runs f, mapping exceptions to status codes.  The return value is the
+// status code whether or not the caller passed a status struct (a NULL st
+// is replaced by a local one, so a failure set inside f is still returned).
 template <class F>
 int guarded(nsb_status* st, F&& f) {
+  nsb_status local;
+  if (!st) st = &local;
   set_status(st, NSB_OK, "");
   try {
     f();
@@ -1271,7 +1287,65 @@ int guarded(nsb_status* st, F&& f) {
   } catch (const std::exception& e) {
     return fail_status(st, NSB_EDEVICE, e.what());
   }
-  return st ? st->code : NSB_OK;
+  return st->code;
+}
+
+void ctx_free(nsb_ctx* ctx);
+void ctx_release(nsb_ctx* ctx) {
+  if (ctx && ctx->refs.fetch_sub(1) == 1) ctx_free(ctx);
+}
+
+// Host programs of destroyed plans (hundreds of MB for long circuits) are
+// released by ONE long-lived worker thread, off the caller's path; small
+// ones inline.  The singleton is never destroyed (no exit-order hazard).
+struct Reclaimer {
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<HostPlan*> queue;
+  Reclaimer() {
+    std::thread([this] {
+      for (;;) {
+        HostPlan* h;
+        {
+          std::unique_lock<std::mutex> lk(mu);
+          cv.wait(lk, [this] { return !queue.empty(); });
+          h = queue.front();
+          queue.pop_front();
+        }
+        delete h;
+      }
+    }).detach();
+  }
+  static Reclaimer& get() {
+    static Reclaimer* r = new Reclaimer();
+    return *r;
+  }
+  void push(HostPlan* h) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      queue.push_back(h);
+    }
+    cv.notify_one();
+  }
+};
+
+size_t host_plan_bytes(const HostPlan& H) {
+  return H.groups.size() * sizeof(GroupDesc) + H.gate_ops.size() * sizeof(GateOp) +
+         (H.matrices.size() + H.packed_all.size() + H.dense_mats.size()) * sizeof(double) +
+         (H.passes.size() + H.mma_passes.size()) * sizeof(PassDesc);
+}
+
+// state vector allocation; on out-of-memory the plan pool's cached blocks
+// are returned to the device and the allocation retried once
+void alloc_state(nsb_ctx* c, uint64_t n_amps) {
+  try {
+    c->amps.alloc(n_amps);
+  } catch (const std::bad_alloc&) {
+    cudaGetLastError();
+    NSB_CUDA(cudaDeviceSynchronize());
+    if (c->plan_pool) NSB_CUDA(cudaMemPoolTrimTo(c->plan_pool, 0));
+    c->amps.alloc(n_amps);
+  }
 }
 
 unsigned grid_for(uint64_t work, int threads, const nsb_ctx* c) {
@@ -1379,7 +1453,7 @@ void apply_matrix(nsb_ctx* c, const double* u, const int32_t* qubits, int k,
     const double2* m = dev_mat;
     DevBuf<double2> tmp;
     if (!m) {
-      tmp.upload(reinterpret_cast<const double2*>(u), size_t(1) << (2 * k), c->stream);
+      tmp.upload(reinterpret_cast<const double2*>(u), size_t(1) << (2 * k), c->stream, c->plan_pool);
       m = tmp.ptr;
     }
     dev::k_applyk<<<grid_for(c->n_amps >> k, 128, c), 128, 0, c->stream>>>(
@@ -1451,12 +1525,16 @@ int nsb_ctx_create(int32_t device, nsb_ctx** out, nsb_status* st) {
     ctx->device = device;
     NSB_CUDA(cudaSetDevice(device));
     NSB_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-    {  // plan buffers come from the device's default pool: keep up to 8 GiB
-       // cached across plans instead of returning it at every synchronise
-      cudaMemPool_t pool;
-      NSB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    {  // plan buffers come from a private stream-ordered pool that keeps up to
+       // 8 GiB cached across plans (the device's default pool is left alone);
+       // state allocations trim it on out-of-memory (alloc_state)
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = device;
+      NSB_CUDA(cudaMemPoolCreate(&ctx->plan_pool, &props));
       uint64_t keep = uint64_t(8) << 30;
-      NSB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+      NSB_CUDA(cudaMemPoolSetAttribute(ctx->plan_pool, cudaMemPoolAttrReleaseThreshold, &keep));
     }
     NSB_CUDA(cudaEventCreate(&ctx->ev0));
     NSB_CUDA(cudaEventCreate(&ctx->ev1));
@@ -1477,8 +1555,12 @@ int nsb_ctx_create(int32_t device, nsb_ctx** out, nsb_status* st) {
   return rc;
 }
 
-void nsb_ctx_destroy(nsb_ctx* ctx) {
-  if (!ctx) return;
+void nsb_ctx_destroy(nsb_ctx* ctx) { ctx_release(ctx); }
+
+}  // extern "C"
+
+namespace {
+void ctx_free(nsb_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->comm) shard_comm_destroy(ctx);
@@ -1499,8 +1581,12 @@ void nsb_ctx_destroy(nsb_ctx* ctx) {
   if (ctx->tev0) cudaEventDestroy(ctx->tev0);
   if (ctx->tev1) cudaEventDestroy(ctx->tev1);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->plan_pool) cudaMemPoolDestroy(ctx->plan_pool);  // deferred by CUDA until freed
   delete ctx;
 }
+}  // namespace
+
+extern "C" {
 
 int nsb_state_init(nsb_ctx* c, int32_t n_qubits, nsb_status* st) {
   if (!c) return fail_status(st, NSB_EINVAL, "null context");
@@ -1510,9 +1596,13 @@ int nsb_state_init(nsb_ctx* c, int32_t n_qubits, nsb_status* st) {
     NSB_CUDA(cudaSetDevice(c->device));
     const uint64_t n_amps = uint64_t(1) << n_qubits;
     if (c->n != n_qubits || !c->amps.ptr) {
+      for (int r = 0; r < 64; ++r)
+        if (c->peers[r])
+          throw std::invalid_argument(
+              "state size change while peer shards are mapped (re-open peers after init)");
       c->amps.release();
       c->n = 0;
-      c->amps.alloc(n_amps);
+      alloc_state(c, n_amps);
       c->n = n_qubits;
       c->n_amps = n_amps;
     }
@@ -1679,23 +1769,24 @@ int nsb_plan_create(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const double* 
     require_state(c);
     if (n_ops < 0 || (n_ops > 0 && !ops)) throw std::invalid_argument("bad op list");
     NSB_CUDA(cudaSetDevice(c->device));
-    P->ctx = c;
     P->device = c->device;
+    P->n = c->n;
     NSB_CUDA(cudaStreamCreateWithFlags(&P->rel, cudaStreamNonBlocking));
     P->host.build(ops, n_ops, params, payloads, c->n, c->blocked_grid);
     HostPlan& H = P->host;
-    P->passes.upload(H.passes.data(), H.passes.size(), c->stream);
-    P->mma_passes.upload(H.mma_passes.data(), H.mma_passes.size(), c->stream);
-    P->groups.upload(H.groups.data(), H.groups.size(), c->stream);
-    P->ops.upload(H.gate_ops.data(), H.gate_ops.size(), c->stream);
+    cudaMemPool_t pool = c->plan_pool;
+    P->passes.upload(H.passes.data(), H.passes.size(), c->stream, pool);
+    P->mma_passes.upload(H.mma_passes.data(), H.mma_passes.size(), c->stream, pool);
+    P->groups.upload(H.groups.data(), H.groups.size(), c->stream, pool);
+    P->ops.upload(H.gate_ops.data(), H.gate_ops.size(), c->stream, pool);
     P->mats.upload(reinterpret_cast<const double2*>(H.matrices.data()), H.matrices.size() / 2,
-                   c->stream);
+                   c->stream, pool);
     P->dense.upload(reinterpret_cast<const double2*>(H.dense_mats.data()),
-                    H.dense_mats.size() / 2, c->stream);
-    P->record.alloc(std::max<int64_t>(H.n_measures, 1), c->stream);
-    P->partials.alloc(2 * size_t(std::max(c->blocked_grid, 1)), c->stream);
-    P->fail.alloc(2, c->stream);
-    P->bar.alloc(1, c->stream);
+                    H.dense_mats.size() / 2, c->stream, pool);
+    P->record.alloc(std::max<int64_t>(H.n_measures, 1), c->stream, pool);
+    P->partials.alloc(2 * size_t(std::max(c->blocked_grid, 1)), c->stream, pool);
+    P->fail.alloc(2, c->stream, pool);
+    P->bar.alloc(1, c->stream, pool);
     NSB_CUDA(cudaStreamSynchronize(c->stream));
     for (cudaStream_t* bs : {&P->passes.stream, &P->mma_passes.stream, &P->groups.stream,
                              &P->ops.stream, &P->mats.stream, &P->dense.stream,
@@ -1703,23 +1794,30 @@ int nsb_plan_create(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const double* 
                              &P->bar.stream})
       *bs = P->rel;
   });
-  if (rc == NSB_OK) *out = P.release();
+  if (rc == NSB_OK) {
+    c->refs.fetch_add(1);
+    P->ctx = c;
+    *out = P.release();
+  }
   return rc;
 }
 
 void nsb_plan_destroy(nsb_plan* plan) {
   if (!plan) return;
   cudaSetDevice(plan->device);
-  // the host-side program (hundreds of MB for long circuits) is released on a
-  // detached thread: returning its pages is off the caller's path
-  HostPlan* host = nullptr;
-  try {
-    host = new HostPlan(std::move(plan->host));
-    std::thread([host] { delete host; }).detach();
-  } catch (...) {
-    delete host;  // no thread: release inline
+  // the host-side program is handed to the reclaimer thread when large
+  if (host_plan_bytes(plan->host) > (size_t(8) << 20)) {
+    HostPlan* host = nullptr;
+    try {
+      host = new HostPlan(std::move(plan->host));
+      Reclaimer::get().push(host);
+    } catch (...) {
+      delete host;  // release inline
+    }
   }
+  nsb_ctx* c = plan->ctx;
   delete plan;
+  ctx_release(c);
 }
 
 int nsb_plan_info_get(const nsb_plan* plan, nsb_plan_info* info) {
@@ -1733,6 +1831,7 @@ int nsb_plan_run_mma(nsb_ctx* c, nsb_plan* P, double eps, double* assert_probs,
   return guarded(st, [&] {
     require_state(c);
     if (!P || P->ctx != c) throw std::invalid_argument("plan belongs to another context");
+    if (P->n != c->n) throw std::invalid_argument("plan was built for another qubit count");
     NSB_CUDA(cudaSetDevice(c->device));
     HostPlan& H = P->host;
     P->last_launches = 0;
@@ -1792,6 +1891,7 @@ int nsb_plan_run_segment(nsb_ctx* c, nsb_plan* P, int64_t seg, nsb_status* st) {
   return guarded(st, [&] {
     require_state(c);
     if (!P || P->ctx != c) throw std::invalid_argument("plan belongs to another context");
+    if (P->n != c->n) throw std::invalid_argument("plan was built for another qubit count");
     if (seg < 0 || seg >= static_cast<int64_t>(P->host.items.size()))
       throw std::invalid_argument("item index out of range");
     NSB_CUDA(cudaSetDevice(c->device));
@@ -1959,8 +2059,27 @@ int nsb_shard_open_peers(nsb_ctx* c, const uint8_t* handles, nsb_status* st) {
     if (!handles) throw std::invalid_argument("null handles");
     if (c->nranks > 64) throw std::invalid_argument("too many ranks for peer mapping");
     NSB_CUDA(cudaSetDevice(c->device));
+    {  // every rank's shard must have this rank's size
+      double* buf = c->scratch.ptr + 2 * dev::kReduceBlocks + 8;
+      if (c->scratch.count < size_t(2 * dev::kReduceBlocks + 8 + 1 + c->nranks))
+        throw std::invalid_argument("rank count exceeds scratch");
+      const double mine = static_cast<double>(c->n_amps);
+      NSB_CUDA(cudaMemcpyAsync(buf, &mine, sizeof mine, cudaMemcpyHostToDevice, c->stream));
+      NSB_NCCL(shard_nccl().all_gather(buf, buf + 1, 1, ncclFloat64,
+                                       static_cast<ncclComm_t>(c->comm), c->stream));
+      std::vector<double> sizes(c->nranks);
+      NSB_CUDA(cudaMemcpyAsync(sizes.data(), buf + 1, sizeof(double) * c->nranks,
+                               cudaMemcpyDeviceToHost, c->stream));
+      NSB_CUDA(cudaStreamSynchronize(c->stream));
+      for (double v : sizes)
+        if (v != mine) throw std::invalid_argument("peer shards differ in size");
+    }
     for (int r = 0; r < c->nranks; ++r) {
-      if (r == c->rank || c->peers[r]) continue;
+      if (r == c->rank) continue;
+      if (c->peers[r]) {  // re-open: the partner may have reallocated its shard
+        NSB_CUDA(cudaIpcCloseMemHandle(c->peers[r]));
+        c->peers[r] = nullptr;
+      }
       cudaIpcMemHandle_t h;
       std::memcpy(&h, handles + 64 * r, sizeof h);
       void* p = nullptr;
@@ -1975,6 +2094,23 @@ void comm_barrier(nsb_ctx* c) {
   double* buf = c->scratch.ptr + 2 * dev::kReduceBlocks + 8;
   NSB_NCCL(shard_nccl().all_gather(buf, buf + 1, 1, ncclFloat64,
                                    static_cast<ncclComm_t>(c->comm), c->stream));
+}
+
+// Collective: unmap the partners' shards, then a rendezvous, so no rank frees
+// (or reallocates) its exported shard while another still maps it.
+int nsb_shard_close_peers(nsb_ctx* c, nsb_status* st) {
+  return guarded(st, [&] {
+    if (!c || !c->comm) throw std::invalid_argument("no communicator (nsb_comm_init)");
+    NSB_CUDA(cudaSetDevice(c->device));
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+    for (double2*& p : c->peers)
+      if (p) {
+        NSB_CUDA(cudaIpcCloseMemHandle(p));
+        p = nullptr;
+      }
+    comm_barrier(c);
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+  });
 }
 
 int nsb_shard_swap_p2p(nsb_ctx* c, int32_t global_bit, int32_t local_q, nsb_status* st) {

@@ -838,6 +838,10 @@ void HostPlan::build_serial(const nsb_op* ops, int64_t n_ops, const double* para
   if (const char* e = std::getenv("NSB_LOW_QUBITS")) low_qubits = std::atoi(e);  // tuning
   if (const char* e = std::getenv("NSB_NO_GROUP_FUSION")) fuse_groups = std::atoi(e) == 0;
   blocked = n >= 6;
+  // NSB_FORCE_PER_OP=1: every gate is its own item executed by the per-op
+  // kernels (k_apply1 / k_apply2 / k_applyk, oracle-tested one by one) -- the
+  // full-size cross-check of the blocked program (tests/test_fullsize_gpu.py)
+  if (const char* e = std::getenv("NSB_FORCE_PER_OP")) blocked = blocked && std::atoi(e) == 0;
   std::vector<PhysGate> run;
   uint64_t col[64];  // frame: physical mask of logical bit j (M e_j)
   uint64_t row[64];  // inverse frame: logical bit j = parity(p & row[j]) (M^-1)

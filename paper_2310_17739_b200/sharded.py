@@ -303,6 +303,11 @@ class ShardedState:
         return st
 
     def close(self):
+        """Collective when peer shards are mapped: every rank unmaps its
+        partners' shards and the ranks rendezvous before any shard is freed."""
+        if getattr(self, "peer_swaps", False) and self.dev.handle:
+            self.dev.call("nsb_shard_close_peers")
+            self.peer_swaps = False
         self.dev.close()
 
     # -- collectives -----------------------------------------------------------

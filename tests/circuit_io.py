@@ -93,3 +93,83 @@ def to_circuit(d, prefix: str = ""):
 def oracle_from_circuit(circuit):
     return [(ins.gate.value, tuple(ins.qubits), tuple(ins.params), ins.matrix, ins.cbit)
             for ins in circuit.instructions]
+
+
+# ---------------------------------------------------------------------------
+# canonical digest of an instruction stream (for lists too large to commit)
+#
+# The stream is reduced to fixed-layout arrays -- gate code (position in the
+# reference's Gate enum, gates.py:30-83), qubit count, qubits (-1 padded),
+# barrier qubit mask, parameter count, parameters (0 padded), classical bit,
+# payload length, and all payloads concatenated in row order (complex128,
+# row-major) -- and sha256 runs over their bytes.  Equal digests mean
+# identical instructions and bit-identical payloads.
+
+
+def _gate_codes():
+    from paper_2310_17739_b200.gates import Gate
+    return {g.value: i for i, g in enumerate(Gate)}
+
+
+def canonical_from_arrays(d: dict, prefix: str = "") -> dict:
+    """Canonical arrays from to_arrays() output (reference circuits)."""
+    g = lambda k: d[prefix + k]
+    codes_of = _gate_codes()
+    names = g("names")
+    uniq, inv = np.unique(names, return_inverse=True)
+    codes = np.array([codes_of[str(u)] for u in uniq], np.int16)[inv]
+    nq = g("nq").astype(np.int8)
+    mats = g("mats")
+    mat_off = g("mat_off")
+    mat_len = np.where(mat_off >= 0, 4 ** nq.astype(np.int64), 0).astype(np.int32)
+    return {"codes": codes, "nq": nq, "qubits": g("qubits").astype(np.int32),
+            "bmask": g("bmask").astype(np.uint64), "npar": g("npar").astype(np.int8),
+            "params": g("params").astype(np.float64), "cbit": g("cbit").astype(np.int32),
+            "mat_len": mat_len, "mats": np.ascontiguousarray(mats, np.complex128)}
+
+
+def canonical_from_packed(ops, params, pool) -> dict:
+    """Canonical arrays from a packed op list (nsb_op records + float64 params
+    + complex payload pool), vectorised (10^6-row lists in about a second)."""
+    from paper_2310_17739_b200 import _native as N
+    from paper_2310_17739_b200.gates import BY_CODE, Gate
+    n = len(ops)
+    kind = ops["kind"].astype(np.int64)
+    tag = ops["tag"].astype(np.int64)
+    codes = tag.astype(np.int16).copy()
+    codes[kind == N.OP_MEASURE] = Gate.MEASURE.code
+    codes[kind == N.OP_RESET] = Gate.RESET.code
+    codes[kind == N.OP_BARRIER] = Gate.BARRIER.code
+    is_bar = kind == N.OP_BARRIER
+    nq = np.where(is_bar, 0, ops["nq"]).astype(np.int8)
+    q = ops["q"].astype(np.int32).copy()
+    q[np.arange(5)[None, :] >= nq[:, None]] = -1
+    bmask = np.where(is_bar, ops["mask"], 0).astype(np.uint64)
+    npar_of = np.array([g.n_params for g in BY_CODE], np.int64)
+    is_gate = kind == N.OP_GATE
+    npar = np.where(is_gate & (ops["param"] >= 0), npar_of[np.clip(tag, 0, len(BY_CODE) - 1)], 0)
+    pm = np.zeros((n, 3), np.float64)
+    for j in range(3):
+        sel = npar > j
+        pm[sel, j] = params[ops["param"][sel] + j]
+    has = is_gate & (ops["payload"] >= 0)
+    mat_len = np.where(has, 4 ** nq.astype(np.int64), 0)
+    starts = np.repeat(ops["payload"][has].astype(np.int64), mat_len[has])
+    within = np.arange(int(mat_len.sum())) - np.repeat(np.cumsum(mat_len[has]) - mat_len[has],
+                                                       mat_len[has])
+    mats = pool[starts + within] if len(starts) else np.zeros(0, np.complex128)
+    cbit = ops["cbit"].astype(np.int32)
+    return {"codes": codes, "nq": nq, "qubits": q, "bmask": bmask, "npar": npar.astype(np.int8),
+            "params": pm, "cbit": cbit, "mat_len": mat_len.astype(np.int32),
+            "mats": np.ascontiguousarray(mats, np.complex128)}
+
+
+def digest(c: dict) -> str:
+    import hashlib
+    h = hashlib.sha256()
+    for k in ("codes", "nq", "qubits", "bmask", "npar", "params", "cbit", "mat_len", "mats"):
+        a = np.ascontiguousarray(c[k])
+        h.update(k.encode())
+        h.update(np.int64(a.size).tobytes())
+        h.update(a.tobytes())
+    return h.hexdigest()

@@ -166,6 +166,13 @@ def _gate(x, op, m):
             x[i] = val
 
 
+def _check() -> bool:
+    """Per-CTA emulation with the partition / warp-locality asserts (default);
+    NSB_PLAN_EXEC_CHECK=0 executes every batch of a pass at once instead
+    (same arithmetic, vectorised over batches: for the larger tests)."""
+    return os.environ.get("NSB_PLAN_EXEC_CHECK", "1") != "0"
+
+
 def _apply_group(B, G, ops, mats, tbases, k, nvalid):
     """One octet sweep over a batch B (nvalid tiles of 2^k stored back to
     back), enumerated exactly as k_blocked's apply_group: swizzled shared-
@@ -190,13 +197,15 @@ def _apply_group(B, G, ops, mats, tbases, k, nvalid):
           for c in range(8)]
     ld = [r ^ (ram[0] if c & 1 else 0) ^ (ram[1] if c & 2 else 0) ^ (ram[2] if c & 4 else 0)
           for c in range(8)]
-    assert len(np.unique(np.concatenate(st))) == 8 * n_act  # octets partition the batch
-    assert len(np.unique(np.concatenate(ld))) == 8 * n_act
     S = B.copy()  # out of place: loads see the pre-sweep batch
-    n_warps = THREADS // 32
-    warp = (t >> 5) & (n_warps - 1)  # octet-index bits 5 .. kThreadBits-1
-    loads = [np.sort(np.concatenate([U(l)[warp == w] for l in ld])) for w in range(n_warps)]
-    stores = [np.sort(np.concatenate([U(s_)[warp == w] for s_ in st])) for w in range(n_warps)]
+    loads = stores = None
+    if _check():
+        assert len(np.unique(np.concatenate(st))) == 8 * n_act  # octets partition the batch
+        assert len(np.unique(np.concatenate(ld))) == 8 * n_act
+        n_warps = THREADS // 32
+        warp = (t >> 5) & (n_warps - 1)  # octet-index bits 5 .. kThreadBits-1
+        loads = [np.sort(np.concatenate([U(l)[warp == w] for l in ld])) for w in range(n_warps)]
+        stores = [np.sort(np.concatenate([U(s_)[warp == w] for s_ in st])) for w in range(n_warps)]
     x = [S[U(l)] for l in ld]
     o0 = int(G["op_begin"])
     for op in ops[o0:o0 + int(G["n_ops"])]:
@@ -206,11 +215,43 @@ def _apply_group(B, G, ops, mats, tbases, k, nvalid):
     return loads, stores
 
 
+def _apply_group_batches(Bs, G, ops, mats, tbs, k, nvalid):
+    """_apply_group on every batch at once: Bs (n_batches, nvalid << k),
+    tbs (n_batches, nvalid) tile bases."""
+    cb = k - 3
+    n_act = nvalid << cb
+    t = np.arange(n_act, dtype=np.int64)
+    a0 = np.zeros(n_act, np.int64)
+    r0 = np.zeros(n_act, np.int64)
+    for b in range(INDEX_BITS):
+        a0 ^= np.where((t >> b) & 1, int(G["tcol"][b]), 0)
+        r0 ^= np.where((t >> b) & 1, int(G["rtcol"][b]), 0)
+    tile = t >> cb
+    am = [int(v) for v in G["am"]]
+    ram = [int(v) for v in G["ram"]]
+    a = np.broadcast_to(a0, (Bs.shape[0], n_act)).copy()
+    r = np.broadcast_to(r0, (Bs.shape[0], n_act)).copy()
+    for i in range(3):
+        kap = _parity(tbs[:, tile].astype(np.uint64) & np.uint64(G["r_out"][i]))
+        a ^= kap * am[i]
+        r ^= kap * ram[i]
+    U = _swz
+    x = [np.take_along_axis(Bs, U(r ^ (ram[0] if c & 1 else 0) ^ (ram[1] if c & 2 else 0)
+                                    ^ (ram[2] if c & 4 else 0)), axis=1) for c in range(8)]
+    o0 = int(G["op_begin"])
+    for op in ops[o0:o0 + int(G["n_ops"])]:
+        _gate(x, op, mats[int(op["mat"]):])
+    for c in range(8):
+        st = a ^ (am[0] if c & 1 else 0) ^ (am[1] if c & 2 else 0) ^ (am[2] if c & 4 else 0)
+        np.put_along_axis(Bs, U(st), x[c], axis=1)
+
+
 def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12, workers=148):
     """Execute a pass list on `state` in place, with k_blocked's per-CTA
     contiguous tile ranges and batches; returns {step: p0} and the carry."""
     n = plan.n
     rec = {}
+    fast = not _check()
     for P in passes:
         k = int(P["k"])
         lidx = _scatter(np.arange(1 << k, dtype=np.int64), P["tq"][:k])
@@ -223,7 +264,17 @@ def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12, workers=1
         assert len(groups) <= 40 and len(pops) <= 40 and len(block) <= 384
         cq = int(P["collapse_q"])
         per, extra = divmod(n_tiles, workers)
-        for cta in range(min(workers, n_tiles)):
+        if fast:  # every batch of nb consecutive tiles at once
+            nv = min(nb, n_tiles)
+            tbs = tb_all.reshape(-1, nv)
+            idx = (tbs[:, :, None] | lidx[None, None, :]).reshape(tbs.shape[0], -1)
+            B = state[idx]
+            if cq >= 0:
+                B = np.where((idx >> cq) & 1, 0.0, B * (1.0 / np.sqrt(carry_p0)))
+            for G in groups:
+                _apply_group_batches(B, G, pops, block, tbs, k, nv)
+            state[idx] = B
+        for cta in range(0 if fast else min(workers, n_tiles)):
             t_begin = cta * per + min(cta, extra)
             t_end = t_begin + per + (1 if cta < extra else 0)
             for t0 in range(t_begin, t_end, nb):
@@ -236,7 +287,7 @@ def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12, workers=1
                 prev = None
                 for G in groups:
                     loads, stores = _apply_group(B, G, pops, block, tbs, k, nvalid)
-                    if prev is not None:  # __syncwarp only: each warp reads its own writes
+                    if prev is not None and loads is not None:  # __syncwarp only: each warp reads its own writes
                         for w in range(len(loads)):
                             assert np.array_equal(loads[w], prev[w])
                     prev = stores if int(G["sync"]) == 0 else None

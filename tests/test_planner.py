@@ -109,3 +109,61 @@ def test_group_fusion_whole_octet_ops(monkeypatch, fusion):
     probs, state = PE.run_mma(plan)
     assert probs == pytest.approx(want_p, abs=1e-12)
     assert np.linalg.norm(state - want) / np.linalg.norm(want) < 1e-10
+
+
+# ---------------------------------------------------------------------------
+# the HBM-regime tile policy (n > 22: every tile holds qubits 0..2) at sizes the
+# oracle finishes quickly, forced with NSB_LOW_QUBITS / NSB_TILE_QUBITS
+
+
+@pytest.mark.parametrize("n,low,tile", [(12, 3, 11), (13, 3, 9), (14, 3, 10), (15, 3, 11),
+                                        (16, 3, 8), (16, 3, 11), (18, 3, 11), (17, 3, 10),
+                                        (14, 1, 9), (13, 0, 7)])
+def test_hbm_tile_policy_filter_workload(monkeypatch, n, low, tile):
+    """Deep-circuit shape (JW shell-model filter, native emitter + fusion) under
+    the tile policy C4/C5 run with: the exported program reproduces the
+    full-state oracle's assertion probabilities and final state."""
+    import shard_exec as SE
+    from paper_2310_17739_b200 import workloads as W
+    monkeypatch.setenv("NSB_LOW_QUBITS", str(low))
+    monkeypatch.setenv("NSB_TILE_QUBITS", str(tile))
+    if n >= 15:  # all batches of a pass at once (same arithmetic, no per-CTA asserts)
+        monkeypatch.setenv("NSB_PLAN_EXEC_CHECK", "0")
+    wl = W.filter_workload(n - 1, trotter=1, n_steps=2, n_scatter=2, hop_range=3,
+                           pair_density=0.1, trial="10" * ((n - 1) // 2) + "1" * ((n - 1) % 2))
+    fops, pool, _ = W.fuse_packed(wl.ops, wl.params, wl.payloads)
+    exe = wl.executable(fops)
+    plan = PE.HostPlan(exe, wl.params, pool, n, 148)
+    assert plan.k == tile
+    for p in plan.mma_passes:
+        tq = set(int(x) for x in p["tq"][: int(p["k"])])
+        assert set(range(low)) <= tq, "tile lacks the always-tiled low qubits"
+    want_p, want = SE.full_mma(exe, wl.params, pool, n)
+    probs, state = PE.run_mma(plan)
+    assert probs == pytest.approx(want_p, abs=1e-12)
+    assert np.linalg.norm(state - want) / np.linalg.norm(want) < 1e-10
+
+
+@pytest.mark.parametrize("n,tile", [(14, 11), (16, 10)])
+def test_hbm_tile_policy_ladders(monkeypatch, n, tile):
+    monkeypatch.setenv("NSB_LOW_QUBITS", "3")
+    monkeypatch.setenv("NSB_TILE_QUBITS", str(tile))
+    rng = np.random.default_rng(900 + n)
+    c = ladder_circuit(rng, n, 14, blocks=2)
+    check(fuse_pipeline(c)[0])
+
+
+def test_default_policy_switches_at_l2_size():
+    """The planner picks the HBM policy (qubits 0..2 tiled) above 22 qubits and
+    the L2 policy (qubits 0, 1) at or below (planner.h kL2ResidentQubits)."""
+    from paper_2310_17739_b200 import workloads as W
+    for n, low in ((21, 2), (22, 2), (23, 3), (24, 3)):
+        wl = W.layered_workload(n, 1, 5)
+        fops, pool, _ = W.fuse_packed(wl.ops, wl.params, wl.payloads)
+        plan = PE.HostPlan(fops, wl.params, pool, n, 296)
+        for p in plan.mma_passes:
+            tq = set(int(x) for x in p["tq"][: int(p["k"])])
+            assert set(range(low)) <= tq
+            if low == 2:
+                continue
+            assert 2 in tq
