@@ -208,6 +208,8 @@ typedef struct nsb_plan_info {
   int64_t n_device_gates;/* gate ops executed on the device per run */
   int64_t n_sweeps;      /* shared-memory octet sweeps (gate groups) per run */
   int64_t n_fused_group_ops; /* gate ops merged away by group fusion (whole-octet ops) */
+  int64_t n_identity_gates;  /* payloads within rounding of the identity, not executed */
+  double identity_error;     /* sum of their ||U - I||_F: bound on the relative L2 change */
 } nsb_plan_info;
 
 /* ops: the executable part of the circuit (sampling block already removed,

@@ -61,7 +61,8 @@ class PlanInfo(ctypes.Structure):
                 ("tile_qubits", ctypes.c_int64), ("n_items", ctypes.c_int64),
                 ("n_frame_gates", ctypes.c_int64), ("n_flush_gates", ctypes.c_int64),
                 ("n_device_gates", ctypes.c_int64), ("n_sweeps", ctypes.c_int64),
-                ("n_fused_group_ops", ctypes.c_int64)]
+                ("n_fused_group_ops", ctypes.c_int64), ("n_identity_gates", ctypes.c_int64),
+                ("identity_error", ctypes.c_double)]
 
 
 class PlanView(ctypes.Structure):

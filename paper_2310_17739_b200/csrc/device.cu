@@ -1268,6 +1268,13 @@ int fail_status(nsb_status* st, int code, const std::string& msg) {
   return code;
 }
 
+// A failed MMA assertion inside a guarded call (-> NSB_EASSERT with step, p0).
+struct AssertFailure {
+  int step;
+  double prob;
+  std::string msg;
+};
+
 // Runs f, mapping exceptions to status codes.  The return value is the
 // status code whether or not the caller passed a status struct (a NULL st
 // is replaced by a local one, so a failure set inside f is still returned).
@@ -1278,6 +1285,9 @@ int guarded(nsb_status* st, F&& f) {
   set_status(st, NSB_OK, "");
   try {
     f();
+  } catch (const AssertFailure& a) {
+    set_status(st, NSB_EASSERT, a.msg, a.step, a.prob);
+    return NSB_EASSERT;
   } catch (const CudaError& e) {
     return fail_status(st, NSB_EDEVICE, e.what());
   } catch (const std::bad_alloc&) {
@@ -1858,7 +1868,7 @@ int nsb_plan_run_mma(nsb_ctx* c, nsb_plan* P, double eps, double* assert_probs,
         char buf[128];
         std::snprintf(buf, sizeof buf, "assertion failed at step %d: P(|0>) = %.3e", fail[1],
                       rec[fail[1]]);
-        set_status(st, NSB_EASSERT, buf, fail[1], rec[fail[1]]);
+        throw AssertFailure{fail[1], rec[fail[1]], buf};
       }
       return;
     }
@@ -1869,8 +1879,7 @@ int nsb_plan_run_mma(nsb_ctx* c, nsb_plan* P, double eps, double* assert_probs,
         if (p0 < eps) {
           char buf[128];
           std::snprintf(buf, sizeof buf, "assertion failed at step %d: P(|0>) = %.3e", it.step, p0);
-          set_status(st, NSB_EASSERT, buf, it.step, p0);
-          break;
+          throw AssertFailure{it.step, p0, buf};
         }
         if (assert_probs) assert_probs[it.step] = p0;
         project(c, it.qubit, 0, p0);

@@ -266,6 +266,26 @@ static inline int lowest_bit(uint64_t m) { return __builtin_ctzll(m); }
 // physical support (bits of ma | mb) above which the frame is flushed first
 constexpr int kMaxSupport = 4;
 
+// ||U - I||_F of a dim x dim complex matrix (interleaved re, im)
+double identity_deviation(const double* m, int dim) {
+  double s = 0.0;
+  for (int r = 0; r < dim; ++r)
+    for (int c = 0; c < dim; ++c) {
+      const double re = m[2 * (r * dim + c)] - (r == c ? 1.0 : 0.0), im = m[2 * (r * dim + c) + 1];
+      s += re * re + im * im;
+    }
+  return std::sqrt(s);
+}
+// a few ulps of 1: products such as H.H or S.Sdg come out as 1 +- 2^-52
+constexpr double kIdentityTol = 1e-15;
+double default_identity_budget() {
+  static const double b = [] {
+    const char* e = std::getenv("NSB_IDENTITY_BUDGET");
+    return e ? std::atof(e) : 3e-11;
+  }();
+  return b;
+}
+
 static int choose_tile_qubits(int n, int workers) {
   if (n <= kTileQubitsMax) return n;
   for (int k = kTileQubitsMax; k >= 9; --k) {
@@ -759,7 +779,9 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
     for (size_t s; (s = next.fetch_add(1)) < n_parts;) {
       int64_t b, e;
       range(s, b, e);
-      try {
+      try {  // the identity budget is shared out in proportion to the part's ops
+        parts[s].identity_budget =
+            default_identity_budget() * static_cast<double>(e - b) / static_cast<double>(n_ops);
         parts[s].build_serial(ops + b, e - b, params, payloads, n, workers);
       } catch (...) {
         errors[s] = std::current_exception();
@@ -804,6 +826,8 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
       items.push_back(it);
     }
     n_gates += H.n_gates;
+    n_identity_gates += H.n_identity_gates;
+    identity_error += H.identity_error;
     n_frame_gates += H.n_frame_gates;
     n_flush_gates += H.n_flush_gates;
     n_frame_flushes += H.n_frame_flushes;
@@ -831,6 +855,7 @@ void HostPlan::build_serial(const nsb_op* ops, int64_t n_ops, const double* para
                             const double* payloads, int n, int workers) {
   n_qubits = n;
   if (n < 1 || n > kMaxQubits) throw std::invalid_argument("qubit count out of range");
+  if (identity_budget < 0.0) identity_budget = default_identity_budget();
   int k = choose_tile_qubits(n, workers);
   if (const char* e = std::getenv("NSB_TILE_QUBITS")) k = std::min(std::atoi(e), n);  // tuning
   tile_qubits = k;
@@ -941,6 +966,14 @@ void HostPlan::build_serial(const nsb_op* ops, int64_t n_ops, const double* para
       throw std::invalid_argument("cannot resolve gate matrix");
     }
     ++n_gates;
+    if (blocked && o.nq <= 2 && identity_budget > 0.0) {
+      const double dev = identity_deviation(mat.v, dim);
+      if (dev <= kIdentityTol && identity_error + dev <= identity_budget) {
+        identity_error += dev;
+        ++n_identity_gates;
+        continue;
+      }
+    }
     if (o.nq >= 3 || !blocked) {
       flush_run();
       Item it;
@@ -1293,6 +1326,8 @@ void HostPlan::build_mma() {
 namespace {
 void fill_info(const nsb::HostPlan& H, nsb_plan_info* info) {
   using nsb::Item;
+  info->n_identity_gates = H.n_identity_gates;
+  info->identity_error = H.identity_error;
   info->n_gates = H.n_gates;
   info->n_measures = H.n_measures;
   int64_t resets = 0, segs = 0;

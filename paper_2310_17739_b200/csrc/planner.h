@@ -27,7 +27,10 @@
 
 namespace nsb {
 
-constexpr int kTileQubitsMax = 11;               // 2048 amplitudes = 32 KiB per buffer
+#ifndef NSB_TILE_MAX
+#define NSB_TILE_MAX 11
+#endif
+constexpr int kTileQubitsMax = NSB_TILE_MAX;     // 2048 amplitudes = 32 KiB per buffer
 constexpr int kTileAmpsMax = 1 << kTileQubitsMax;
 #ifndef NSB_OCTETS
 #define NSB_OCTETS 2

@@ -76,6 +76,15 @@ struct HostPlan {
   int64_t n_warp_syncs = 0;     // sweeps followed by __syncwarp instead of a CTA barrier
   int64_t n_fused_group_ops = 0;  // gate ops removed by group fusion (fuse_group)
   bool fuse_groups = true;      // NSB_NO_GROUP_FUSION=1 turns group fusion off
+  // Gates within rounding of the identity (||U - I||_F <= kIdentityTol, e.g. the
+  // fused H.H / S.Sdg products between consecutive JW terms) are not executed,
+  // while the summed deviation stays within identity_budget: for unitaries
+  // ||U_N..U_1 - U'_N..U'_1|| <= sum ||U_i - U'_i||, so the final state moves by
+  // at most identity_error relative L2 (default budget 3e-11, under a third of the
+  // 1e-10 parity bound; NSB_IDENTITY_BUDGET=0 executes every gate).
+  double identity_budget = -1.0;  // < 0: the default / environment
+  int64_t n_identity_gates = 0;
+  double identity_error = 0.0;
   int64_t flops = 0;
   int64_t class_count[kNumClasses] = {};
 

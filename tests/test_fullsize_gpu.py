@@ -147,3 +147,53 @@ def test_hbm_regime_layered_stream_then_adjoint_is_identity(n):
     a = state.amps
     assert abs(a[0] - 1.0) < 1e-10
     assert np.linalg.norm(a[1:]) < 1e-10
+
+
+def test_state_released_before_its_programs():
+    """Python may collect a StateVector (its nsb_ctx) before the DeviceProgram
+    built on it: the plan holds a reference on the context, so destroying the
+    plan afterwards is safe (regression: segfault in nsb_plan_destroy during
+    garbage collection, round 1)."""
+    import gc
+    wl = W.filter_workload(11, trotter=1, n_steps=2, trial="10" * 5 + "1")
+    fops, pool, _ = W.fuse_packed(wl.ops, wl.params, wl.payloads)
+    exe = wl.executable(fops)
+    state = StateVector(12)
+    progs = [DeviceProgram(state, exe, wl.params, pool) for _ in range(3)]
+    progs[0].run_mma()
+    state._dev.close()  # the owner's reference goes first
+    del state
+    gc.collect()
+    for p in progs:
+        p.__del__()
+    gc.collect()
+
+
+def test_plan_rejects_a_resized_state():
+    """A plan is bound to the qubit count it was built for (no out-of-bounds
+    run after nsb_state_init changes the state size)."""
+    wl = W.layered_workload(12, 2, 3)
+    fops, pool, _ = W.fuse_packed(wl.ops, wl.params, wl.payloads)
+    state = StateVector(12)
+    prog = DeviceProgram(state, fops, wl.params, pool)
+    state._dev.call("nsb_state_init", 10)
+    with pytest.raises(ValueError):
+        prog.run_mma()
+
+
+def test_null_status_still_reports_assertion_failure():
+    """nsb_plan_run_mma returns NSB_EASSERT when the caller passes no status."""
+    import ctypes
+    c = np.zeros(4, N.OP_DTYPE)
+    c["cbit"], c["src"], c["param"], c["payload"] = -1, -1, -1, -1
+    c["q"] = -1
+    c[0]["kind"], c[0]["tag"], c[0]["nq"], c[0]["q"][0] = N.OP_GATE, Gate.X.code, 1, 3
+    c[1]["kind"], c[1]["nq"], c[1]["q"][0] = N.OP_MEASURE, 1, 3
+    c[2]["kind"], c[2]["nq"], c[2]["q"][0] = N.OP_RESET, 1, 3
+    c[3]["kind"], c[3]["tag"], c[3]["nq"], c[3]["q"][0] = N.OP_GATE, Gate.H.code, 1, 0
+    state = StateVector(8)
+    prog = DeviceProgram(state, c, np.zeros(1), np.zeros(1, np.complex128))
+    probs = np.zeros(1)
+    code = N.lib().nsb_plan_run_mma(state._dev.handle, prog.handle, ctypes.c_double(1e-12),
+                                    N.ptr(probs), None)
+    assert code == 2  # NSB_EASSERT
