@@ -98,6 +98,13 @@ def make_workload(config: str, trotter: int | None):
         wl = W.filter_workload(20, trotter=r, n_steps=8, n_scatter=8, trial="10" * 10)
     elif config == "rand28":
         wl = W.layered_workload(28, layers=trotter or 20)
+    elif config in SMALL:
+        d = small_fixture(config)
+        terms = [("".join("IXYZ"[c] for c in row), float(cf))
+                 for row, cf in zip(d["term_letters"], d["term_coeffs"])]
+        wl = W.filter_workload(d["term_letters"].shape[1], int(d["trotter"]), terms=terms,
+                               steps=[tuple(map(float, x)) for x in d["steps"]],
+                               trial="".join(str(int(b)) for b in d["trial"]))
     else:
         raise SystemExit(f"unknown config {config}")
     t_gen = time.perf_counter() - t0
@@ -161,6 +168,17 @@ class Clocks:
 # of workloads.layered_workload fused by the oracle's fuse_pipeline.
 
 
+# BASELINE configs 1 and 2: the filter circuits the reference generated for the
+# golden fixtures (tests/golden/make_golden.py): C1 `ucc8` = 7-mode shell
+# model + ancilla, 10 554 gates; C2 `mcm16` = 15-site chain + ancilla,
+# 39 676 gates, 4 mid-circuit assertions each
+SMALL = {"ucc8": "filter8", "mcm16": "filter16"}
+
+
+def small_fixture(config: str) -> dict:
+    return dict(np.load(ROOT / "tests" / "golden" / f"{SMALL[config]}.npz"))
+
+
 def host_cpu() -> dict:
     model = "unknown"
     try:
@@ -191,6 +209,11 @@ def reference_stream(config: str, trotter: int | None):
         from circuit_io import to_oracle
         d = dict(np.load(ROOT / "tests" / "golden" / "deep21.npz"))
         instrs, n = to_oracle(d, "prefix_")
+        return instrs, n, int(d["fused_stats"][0]), int(d["fused_stats"][1])
+    if config in SMALL:  # the reference's own fused list of the whole circuit
+        from circuit_io import to_oracle
+        d = small_fixture(config)
+        instrs, n = to_oracle(d, "fused_")
         return instrs, n, int(d["fused_stats"][0]), int(d["fused_stats"][1])
     if config == "rand28":  # workloads.layered_workload(28, layers, seed 28), restated
         import math
@@ -288,12 +311,21 @@ def workload_config(args, n, input_gates, fused_gates, world) -> dict:
                "within a step when it fits"}
     if args.config == "deep21":
         c.update({"trotter": args.trotter or 18, "filter_steps": 8})
+    elif args.config in SMALL:
+        d = small_fixture(args.config)
+        c.update({"trotter": int(d["trotter"]), "filter_steps": int(len(d["steps"]))})
     else:
         c.update({"layers": args.trotter or 20})
     return c
 
 
 def workload_name(args) -> str:
+    if args.config == "ucc8":
+        return ("ucc8 (BASELINE config 1): 7-mode shell-model projection filter + ancilla "
+                "(8 qubits), 4 filter steps, MMA mode")
+    if args.config == "mcm16":
+        return ("mcm16 (BASELINE config 2): 15-site transverse-field chain projection filter + "
+                "ancilla (16 qubits), 4 mid-circuit assertions, MMA mode")
     if args.config == "deep21":
         return (f"deep21: 20-mode JW shell-model projection filter + ancilla (21 qubits), "
                 f"8 filter steps x {args.trotter or 18} Trotter slices (paper P9 shape), MMA mode")
@@ -561,7 +593,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--config", default="deep21", choices=("deep21", "rand28", "shard"))
+    ap.add_argument("--config", default="deep21",
+                    choices=("deep21", "rand28", "ucc8", "mcm16", "shard"))
     ap.add_argument("--qubits", type=int, default=34, help="--config shard: total qubits")
     ap.add_argument("--trotter", type=int, default=None)
     ap.add_argument("--e2e-steps", type=int, default=3)

@@ -217,6 +217,13 @@ typedef struct nsb_plan_info {
  * (nsb_gate_matrix), C1/C2/k-qubit payloads from `payloads`. */
 int nsb_plan_create(nsb_ctx* ctx, const nsb_op* ops, int64_t n_ops, const double* params,
                     const double* payloads, nsb_plan** out, nsb_status* st);
+/* nsb_plan_create with flags: NSB_PLAN_EXACT executes every gate, including
+ * those within rounding of a scalar identity (for callers that measure the
+ * state between nsb_plan_run_segment calls themselves: rejection mode, the
+ * sharded schedule). */
+enum { NSB_PLAN_EXACT = 1 };
+int nsb_plan_create_ex(nsb_ctx* ctx, const nsb_op* ops, int64_t n_ops, const double* params,
+                       const double* payloads, int32_t flags, nsb_plan** out, nsb_status* st);
 void nsb_plan_destroy(nsb_plan* plan);
 /* Host-only dry run of the planner (no device needed): the schedule that
  * nsb_plan_create would upload, summarised.  class_counts (NSB_N_CLASSES
@@ -263,6 +270,13 @@ int nsb_plan_run_mma(nsb_ctx* ctx, nsb_plan* plan, double eps, double* assert_pr
 int nsb_plan_run_segment(nsb_ctx* ctx, nsb_plan* plan, int64_t seg, nsb_status* st);
 int nsb_plan_segment_marker(const nsb_plan* plan, int64_t seg, int32_t* kind, int32_t* qubit,
                             int32_t* step);
+
+/* Factor between the state's P(|0>) at assertion `step` and the reference's
+ * (engine.py:159-161): the product of |s|^2 of the near-scalar gates s I the
+ * plan does not execute since the previous assertion (nsb_plan_info
+ * n_identity_gates).  nsb_plan_run_mma applies it; callers that measure
+ * between nsb_plan_run_segment calls multiply their p0 by it. */
+int nsb_plan_p0_scale(const nsb_plan* plan, int32_t step, double* scale);
 
 /* Device time of the last nsb_plan_run_* call in milliseconds (CUDA events
  * on the launching stream), and the number of kernels it launched. */

@@ -22,6 +22,7 @@ if os.environ.get("NSB_LIB_VARIANT"):  # tuning experiments: an in-tree build va
 
 NSB_OK, NSB_EINVAL, NSB_EASSERT, NSB_EPROJECT, NSB_ERESOURCE, NSB_EDEVICE, NSB_EQASM = range(7)
 OP_GATE, OP_MEASURE, OP_RESET, OP_BARRIER = range(4)
+PLAN_EXACT = 1  # nsb_plan_create_ex flag: execute every gate
 BLAS_CHAIN2, BLAS_FOUR = 1, 2
 PASS_ALL = 15
 
@@ -110,6 +111,8 @@ _SIGNATURES = {
     "nsb_expectation_pauli": (ctypes.c_int, [_P, _P, _P, _P, _I64, ctypes.POINTER(_D),
                                              ctypes.POINTER(_D), _ST]),
     "nsb_plan_create": (ctypes.c_int, [_P, _P, _I64, _P, _P, ctypes.POINTER(_P), _ST]),
+    "nsb_plan_create_ex": (ctypes.c_int, [_P, _P, _I64, _P, _P, ctypes.c_int32,
+                                          ctypes.POINTER(_P), _ST]),
     "nsb_plan_destroy": (None, [_P]),
     "nsb_plan_info_get": (ctypes.c_int, [_P, ctypes.POINTER(PlanInfo)]),
     "nsb_plan_analyze": (ctypes.c_int, [_P, _I64, _P, _P, _I32, ctypes.POINTER(PlanInfo), _P,
@@ -123,6 +126,7 @@ _SIGNATURES = {
     "nsb_plan_segment_marker": (ctypes.c_int, [_P, _I64, ctypes.POINTER(_I32),
                                                ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
     "nsb_plan_last_timing": (ctypes.c_int, [_P, ctypes.POINTER(_D), ctypes.POINTER(_I64)]),
+    "nsb_plan_p0_scale": (ctypes.c_int, [_P, ctypes.c_int32, _P]),
     "nsb_timer_start": (ctypes.c_int, [_P, _ST]),
     "nsb_timer_stop": (ctypes.c_int, [_P, ctypes.POINTER(_D), _ST]),
     "nsb_comm_unique_id": (ctypes.c_int, [_P, _ST]),

@@ -980,13 +980,13 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
     // fence, which is cumulative (the cooperative-groups grid barrier pattern)
     __syncthreads();
     ++n_bar;
-    if (tid == 0) {
+    if (tid == 0 && gridDim.x > 1) {
       __threadfence();
       atomicAdd(p.bar, 1u);
     }
 #endif
     if (pi + 1 < p.pass_end) stage(pi + 1);
-    if (tid == 0) {
+    if (tid == 0 && gridDim.x > 1) {  // one CTA (n <= 11): the CTA barrier suffices
       const unsigned target = n_bar * gridDim.x;
       unsigned seen;
       // relaxed polling (no L1 invalidation per iteration), one acquire fence after
@@ -1174,6 +1174,10 @@ struct nsb_ctx {
 struct nsb_plan {
   nsb_ctx* ctx = nullptr;  // holds a reference (ctx->refs)
   int n = 0;               // qubit count the plan was built for
+  // persistent CTAs of this plan's k_blocked launches: the co-resident grid,
+  // but no more than the tiles of a pass -- a state of one tile (n <= 11) runs
+  // on ONE CTA with no grid barrier at all, a 16-qubit state on 32
+  int grid = 0;
   HostPlan host;
   DevBuf<PassDesc> passes, mma_passes;
   DevBuf<GroupDesc> groups;
@@ -1498,9 +1502,13 @@ void launch_blocked(nsb_ctx* c, nsb_plan* P, const PassDesc* passes, int pb, int
   bp.debug = debug;
   void* args[] = {&bp};
   NSB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::k_blocked),
-                                       dim3(c->blocked_grid), dim3(kPassThreads), args,
+                                       dim3(P->grid), dim3(kPassThreads), args,
                                        dev::kBlockedSmemBytes, c->stream));
   P->last_launches += 1;
+}
+
+double p0_scale(const HostPlan& H, int step) {
+  return step >= 0 && step < static_cast<int>(H.p0_scale.size()) ? H.p0_scale[step] : 1.0;
 }
 
 void run_item(nsb_ctx* c, nsb_plan* P, const Item& it) {
@@ -1772,6 +1780,11 @@ int nsb_expectation_pauli(nsb_ctx* c, const uint64_t* xmask, const uint64_t* zma
 
 int nsb_plan_create(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const double* params,
                     const double* payloads, nsb_plan** out, nsb_status* st) {
+  return nsb_plan_create_ex(c, ops, n_ops, params, payloads, 0, out, st);
+}
+
+int nsb_plan_create_ex(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const double* params,
+                       const double* payloads, int32_t flags, nsb_plan** out, nsb_status* st) {
   if (!out) return fail_status(st, NSB_EINVAL, "null out pointer");
   *out = nullptr;
   auto P = std::make_unique<nsb_plan>();
@@ -1782,8 +1795,15 @@ int nsb_plan_create(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const double* 
     P->device = c->device;
     P->n = c->n;
     NSB_CUDA(cudaStreamCreateWithFlags(&P->rel, cudaStreamNonBlocking));
+    if (flags & NSB_PLAN_EXACT) P->host.identity_budget = 0.0;
     P->host.build(ops, n_ops, params, payloads, c->n, c->blocked_grid);
     HostPlan& H = P->host;
+    {
+      uint64_t tiles = 1;
+      for (const auto* v : {&H.passes, &H.mma_passes})
+        for (const PassDesc& pd : *v) tiles = std::max(tiles, uint64_t(1) << (c->n - pd.k));
+      P->grid = static_cast<int>(std::min<uint64_t>(tiles, uint64_t(c->blocked_grid)));
+    }
     cudaMemPool_t pool = c->plan_pool;
     P->passes.upload(H.passes.data(), H.passes.size(), c->stream, pool);
     P->mma_passes.upload(H.mma_passes.data(), H.mma_passes.size(), c->stream, pool);
@@ -1862,6 +1882,10 @@ int nsb_plan_run_mma(nsb_ctx* c, nsb_plan* P, double eps, double* assert_probs,
       NSB_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
       P->last_ms = ms;
       const int n_ok = fail[0] ? fail[1] : static_cast<int>(H.n_measures);
+      // the reference's P(|0>) includes the norm carried by the near-identity
+      // gates the plan does not execute (planner_host.h p0_scale)
+      for (int s = 0; s < static_cast<int>(H.n_measures) && s < static_cast<int>(rec.size()); ++s)
+        rec[s] *= p0_scale(H, s);
       if (assert_probs)
         for (int s = 0; s < n_ok; ++s) assert_probs[s] = rec[s];
       if (fail[0]) {
@@ -1876,12 +1900,14 @@ int nsb_plan_run_mma(nsb_ctx* c, nsb_plan* P, double eps, double* assert_probs,
     for (const Item& it : H.items) {
       if (it.kind == Item::kMeasure) {
         const double p0 = half_norm(c, it.qubit, 0);
+        const double p0_ref = p0 * p0_scale(H, it.step);
         if (p0 < eps) {
           char buf[128];
-          std::snprintf(buf, sizeof buf, "assertion failed at step %d: P(|0>) = %.3e", it.step, p0);
-          throw AssertFailure{it.step, p0, buf};
+          std::snprintf(buf, sizeof buf, "assertion failed at step %d: P(|0>) = %.3e", it.step,
+                        p0_ref);
+          throw AssertFailure{it.step, p0_ref, buf};
         }
-        if (assert_probs) assert_probs[it.step] = p0;
+        if (assert_probs) assert_probs[it.step] = p0_ref;
         project(c, it.qubit, 0, p0);
         P->last_launches += 3;
       } else if (it.kind != Item::kReset) {
@@ -1919,6 +1945,12 @@ int nsb_plan_segment_marker(const nsb_plan* P, int64_t seg, int32_t* kind, int32
                                     : (it.kind == Item::kReset ? NSB_OP_RESET : NSB_OP_GATE);
   *qubit = it.qubit;
   *step = it.step;
+  return NSB_OK;
+}
+
+int nsb_plan_p0_scale(const nsb_plan* P, int32_t step, double* scale) {
+  if (!P || !scale || step < 0 || step >= P->host.n_measures) return NSB_EINVAL;
+  *scale = p0_scale(P->host, step);
   return NSB_OK;
 }
 

@@ -266,12 +266,16 @@ static inline int lowest_bit(uint64_t m) { return __builtin_ctzll(m); }
 // physical support (bits of ma | mb) above which the frame is flushed first
 constexpr int kMaxSupport = 4;
 
-// ||U - I||_F of a dim x dim complex matrix (interleaved re, im)
-double identity_deviation(const double* m, int dim) {
+// Scalar part s = U_00 of a near-scalar matrix and the residual ||U - s I||_F
+// (dim x dim complex, interleaved re, im)
+double scalar_residual(const double* m, int dim, double& s_re, double& s_im) {
+  s_re = m[0];
+  s_im = m[1];
   double s = 0.0;
   for (int r = 0; r < dim; ++r)
     for (int c = 0; c < dim; ++c) {
-      const double re = m[2 * (r * dim + c)] - (r == c ? 1.0 : 0.0), im = m[2 * (r * dim + c) + 1];
+      const double re = m[2 * (r * dim + c)] - (r == c ? s_re : 0.0);
+      const double im = m[2 * (r * dim + c) + 1] - (r == c ? s_im : 0.0);
       s += re * re + im * im;
     }
   return std::sqrt(s);
@@ -766,6 +770,7 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
     build_mma();
     return;
   }
+  const double total_budget = identity_budget >= 0.0 ? identity_budget : default_identity_budget();
   // parts: [0, m0), [m0 + 1, m1), ..., [m_last + 1, n_ops)
   const size_t n_parts = marks.size() + 1;
   std::vector<HostPlan> parts(n_parts);
@@ -781,7 +786,7 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
       range(s, b, e);
       try {  // the identity budget is shared out in proportion to the part's ops
         parts[s].identity_budget =
-            default_identity_budget() * static_cast<double>(e - b) / static_cast<double>(n_ops);
+            total_budget * static_cast<double>(e - b) / static_cast<double>(n_ops);
         parts[s].build_serial(ops + b, e - b, params, payloads, n, workers);
       } catch (...) {
         errors[s] = std::current_exception();
@@ -797,6 +802,7 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
   // concatenate: each part's items, then the marker that ended it
   build_serial(ops, 0, params, payloads, n, workers);  // header fields, no ops
   int step = 0;
+  double running_scale2 = 1.0, running_tail_error = 0.0;
   for (size_t s = 0; s < n_parts; ++s) {
     HostPlan& H = parts[s];
     const int32_t pass0 = static_cast<int32_t>(passes.size());
@@ -827,7 +833,10 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
     }
     n_gates += H.n_gates;
     n_identity_gates += H.n_identity_gates;
-    identity_error += H.identity_error;
+    // each part added its own tail error (it has no measurement); only the
+    // drift after the circuit's last measurement stays uncompensated
+    identity_error += H.identity_error - H.tail_error_total;
+    running_tail_error += H.tail_error_total;
     n_frame_gates += H.n_frame_gates;
     n_flush_gates += H.n_flush_gates;
     n_frame_flushes += H.n_frame_flushes;
@@ -837,9 +846,15 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
     n_fused_group_ops += H.n_fused_group_ops;
     flops += H.flops;
     for (int c = 0; c < kNumClasses; ++c) class_count[c] += H.class_count[c];
+    running_scale2 *= H.tail_scale2;  // parts hold no measurement (split at markers)
     if (s < marks.size()) {
       const nsb_op& o = ops[marks[s]];
       if (o.q[0] < 0 || o.q[0] >= n) throw std::invalid_argument("qubit out of range in plan");
+      if (o.kind == NSB_OP_MEASURE) {
+        p0_scale.push_back(running_scale2);
+        running_scale2 = 1.0;
+        running_tail_error = 0.0;
+      }
       Item it;
       it.kind = o.kind == NSB_OP_MEASURE ? Item::kMeasure : Item::kReset;
       it.qubit = o.q[0];
@@ -848,6 +863,7 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
     }
   }
   n_measures = step;
+  identity_error += running_tail_error;
   build_mma();
 }
 
@@ -948,6 +964,11 @@ void HostPlan::build_serial(const nsb_op* ops, int64_t n_ops, const double* para
       if (o.q[j] < 0 || o.q[j] >= n) throw std::invalid_argument("qubit out of range in plan");
     if (o.kind == NSB_OP_MEASURE || o.kind == NSB_OP_RESET) {
       flush_run();
+      if (o.kind == NSB_OP_MEASURE) {  // the reference renormalises here
+        p0_scale.push_back(tail_scale2);
+        tail_scale2 = 1.0;
+        tail_error = 0.0;
+      }
       Item it;
       it.kind = o.kind == NSB_OP_MEASURE ? Item::kMeasure : Item::kReset;
       it.qubit = o.q[0];
@@ -967,9 +988,17 @@ void HostPlan::build_serial(const nsb_op* ops, int64_t n_ops, const double* para
     }
     ++n_gates;
     if (blocked && o.nq <= 2 && identity_budget > 0.0) {
-      const double dev = identity_deviation(mat.v, dim);
-      if (dev <= kIdentityTol && identity_error + dev <= identity_budget) {
-        identity_error += dev;
+      double s_re, s_im;
+      const double res = scalar_residual(mat.v, dim, s_re, s_im);
+      const double mod = std::hypot(s_re, s_im);
+      const double phase_err = std::hypot(s_re / mod - 1.0, s_im / mod);
+      const double mod_err = std::fabs(mod - 1.0);  // uncompensated only after the last measurement
+      const double err = res + phase_err;
+      if (res <= kIdentityTol && mod_err <= kIdentityTol && phase_err <= kIdentityTol &&
+          identity_error + err + tail_error + mod_err <= identity_budget) {
+        identity_error += err;
+        tail_error += mod_err;
+        tail_scale2 *= mod * mod;
         ++n_identity_gates;
         continue;
       }
@@ -1031,6 +1060,9 @@ void HostPlan::build_serial(const nsb_op* ops, int64_t n_ops, const double* para
   }
   flush_run();
   n_measures = step;
+  tail_error_total = tail_error;
+  identity_error += tail_error;  // after the last measurement: not compensated
+  tail_error = 0.0;
 }
 
 void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {

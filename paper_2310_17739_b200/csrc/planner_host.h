@@ -76,15 +76,25 @@ struct HostPlan {
   int64_t n_warp_syncs = 0;     // sweeps followed by __syncwarp instead of a CTA barrier
   int64_t n_fused_group_ops = 0;  // gate ops removed by group fusion (fuse_group)
   bool fuse_groups = true;      // NSB_NO_GROUP_FUSION=1 turns group fusion off
-  // Gates within rounding of the identity (||U - I||_F <= kIdentityTol, e.g. the
-  // fused H.H / S.Sdg products between consecutive JW terms) are not executed,
-  // while the summed deviation stays within identity_budget: for unitaries
-  // ||U_N..U_1 - U'_N..U'_1|| <= sum ||U_i - U'_i||, so the final state moves by
-  // at most identity_error relative L2 (default budget 3e-11, under a third of the
-  // 1e-10 parity bound; NSB_IDENTITY_BUDGET=0 executes every gate).
+  // Gates within rounding of a scalar identity s I (e.g. the fused H.H / S.Sdg
+  // products between consecutive JW terms, 1 + 2^-52 on the diagonal) are not
+  // executed.  Their scalar is kept: the reference's state carries the product
+  // of the |s|^2 in its norm until the next measurement renormalises it, so
+  // each reported P(|0>) is multiplied by that product (p0_scale; a real
+  // positive s makes the post-collapse states agree exactly).  What is not
+  // compensated -- the residuals ||U - s I||_F, the phases |s/|s| - 1| and the
+  // norm drift after the last measurement -- is summed in identity_error and
+  // kept within identity_budget: for unitaries ||U_N..U_1 - U'_N..U'_1|| <=
+  // sum ||U_i - U'_i||, so the state moves by at most identity_error relative
+  // L2 (default budget 3e-11, under a third of the 1e-10 parity bound;
+  // NSB_IDENTITY_BUDGET=0 executes every gate).
   double identity_budget = -1.0;  // < 0: the default / environment
   int64_t n_identity_gates = 0;
   double identity_error = 0.0;
+  std::vector<double> p0_scale;   // per assertion step: product of |s|^2 since the last one
+  double tail_scale2 = 1.0;       // product of |s|^2 after the last measurement
+  double tail_error = 0.0;        // sum of | |s| - 1 | after the last measurement
+  double tail_error_total = 0.0;  // its final value (parts of a parallel build)
   int64_t flops = 0;
   int64_t class_count[kNumClasses] = {};
 

@@ -411,9 +411,11 @@ class ShardedProgram:
                     self.plans.append(None)
                     continue
                 h = ctypes.c_void_p()
-                N.check(N.lib().nsb_plan_create(state.dev.handle, N.ptr(s.ops), len(s.ops),
-                                                N.ptr(params), N.ptr(payloads.view(np.float64)),
-                                                ctypes.byref(h), ctypes.byref(st)), st)
+                # exact: assertions are measured between the groups by the host
+                N.check(N.lib().nsb_plan_create_ex(state.dev.handle, N.ptr(s.ops), len(s.ops),
+                                                   N.ptr(params), N.ptr(payloads.view(np.float64)),
+                                                   N.PLAN_EXACT, ctypes.byref(h),
+                                                   ctypes.byref(st)), st)
                 info = N.PlanInfo()
                 N.lib().nsb_plan_info_get(h, ctypes.byref(info))
                 self.plans.append((h, int(info.n_items)))

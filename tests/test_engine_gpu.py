@@ -425,7 +425,7 @@ def test_rejection_replay_equals_explicit_shots(golden):
     packed = E.pack(fused, instrs[:end])
     n_steps = sum(1 for ins in instrs[:end] if ins.gate is E.Gate.MEASURE)
     state = E.StateVector(fused.n_qubits)
-    prog = E.DeviceProgram(state, packed.ops, packed.params, packed.payloads)
+    prog = E.DeviceProgram(state, packed.ops, packed.params, packed.payloads, exact=True)
     items = prog.items()
     assert E._replayable(items)
     fast = E._rejection(state, prog, items, n_steps, 200, E._as_rng(11), False)

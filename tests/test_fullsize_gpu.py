@@ -80,7 +80,7 @@ def test_filter21_mma_launch_matches_item_path():
     for i, (kind, q, step) in enumerate(prog.items()):
         if kind == N.OP_MEASURE:
             p0 = _branch_probability(state, q, 0)
-            p_items.append(p0)
+            p_items.append(p0 * prog.p0_scale(step))
             _project(state, q, 0, p0)
         elif kind == N.OP_GATE:
             prog.run_item(i)
