@@ -1803,6 +1803,7 @@ int nsb_plan_create_ex(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const doubl
       for (const auto* v : {&H.passes, &H.mma_passes})
         for (const PassDesc& pd : *v) tiles = std::max(tiles, uint64_t(1) << (c->n - pd.k));
       P->grid = static_cast<int>(std::min<uint64_t>(tiles, uint64_t(c->blocked_grid)));
+      if (std::getenv("NSB_FULL_GRID")) P->grid = c->blocked_grid;  // A/B: the round-1 grid
     }
     cudaMemPool_t pool = c->plan_pool;
     P->passes.upload(H.passes.data(), H.passes.size(), c->stream, pool);

@@ -145,7 +145,7 @@ def test_sample_shard_edge_draws():
 
 
 # ---------------------------------------------------------------------------
-# world_size-2 gloo: one shard per process, real exchanges
+# world_size-2/4/8 gloo: one shard per process, real exchanges
 
 
 def _free_port():
@@ -216,8 +216,10 @@ def _gloo_worker(rank, world, port, n, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_gloo_world2_matches_full_state(world):
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_gloo_world_matches_full_state(world):
+    """g = 1, 2, 3 global qubits: one shard per process (8 ranks = the 8-GPU
+    layout of BASELINE config 5), real point-to-point exchanges."""
     ops, params, pool, n = _filter()
     want_p, want = SE.full_mma(ops, params, pool, n)
     ctx = mp.get_context("spawn")
