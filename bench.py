@@ -24,7 +24,10 @@ cpu_baseline / --impl reference: the oracle port of the reference engine
 
 Multi-GPU (torchrun, N > 1), default configs: replicas -- every rank runs
 the same circuit on its own GPU (no data-path collective), value = total
-gates / max time over ranks, "scaling": "weak".
+gates / max time over ranks, "scaling": "weak".  Every default line also
+carries "sharded": the multi-GPU design measured at this N -- ONE 32-qubit
+layered circuit split over all N GPUs (strong scaling; 64 GiB state, fits one
+GPU at N = 1) and, from N = 2, the 34-qubit config 5 state (256 GiB).
 
 --config shard [--qubits Q] (BASELINE config 5, default Q = 34): ONE layered
 random circuit whose state is split over the N ranks (sharded.py: 2^(Q-g)
@@ -332,19 +335,18 @@ def workload_name(args) -> str:
     return f"rand28: 28-qubit random layered U3 + {{CX,CZ,RZZ}} circuit, {args.trotter or 20} layers"
 
 
-def run_sharded(args, rank, world, local):
-    """BASELINE config 5: one state split over all ranks (sharded.py)."""
-    import torch
+def sharded_measure(n: int, layers: int, rank: int, world: int, local: int, steps: int,
+                    warmup: int, extras: bool = False) -> dict:
+    """ONE n-qubit layered circuit (BASELINE config 4/5 generator) whose state is
+    split over all `world` ranks (sharded.py: 2^(n-g) amplitudes per GPU, qubit
+    swaps through peer memory over NVLink, collective assertions).  Device time
+    per full execution, max over ranks.  Collective: every rank calls it."""
     import torch.distributed as dist
     from paper_2310_17739_b200 import workloads as W
     from paper_2310_17739_b200.sharded import ShardedState
 
-    n = args.qubits
-    if world > 1:
-        dist.init_process_group("gloo")
-    torch.cuda.set_device(local)
     t0 = time.perf_counter()
-    wl = W.layered_workload(n, layers=args.trotter or 10, seed=34)
+    wl = W.layered_workload(n, layers=layers, seed=34)
     fops, pool, stats = W.fuse_packed(wl.ops, wl.params, wl.payloads)
     host = {"generate_fuse_s": round(time.perf_counter() - t0, 3)}
     if world > 1:
@@ -367,33 +369,20 @@ def run_sharded(args, rank, world, local):
         prog.run()
         return st.timer_stop()
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         one()
     barrier()
-    clocks = Clocks(local)
-    ms = [one() for _ in range(args.steps)]
-    clk = clocks.stop()
+    ms = [one() for _ in range(steps)]
     dev_s = sum(ms) / 1e3
     if world > 1:
         box = [None] * world
         dist.all_gather_object(box, dev_s)
         dev_s = max(box)
-    # one extra profiled execution (per-step device events; outside the timed region)
+    # one profiled execution (per-step device events; outside the timed region)
     st.reset()
     barrier()
     times: dict = {}
     prog.run(times=times)
-    t0 = time.perf_counter()
-    st.reset()
-    p2 = st.compile(fops, wl.params, pool)
-    p2.run()
-    norm = st.norm()
-    e2e_s = time.perf_counter() - t0
-    p2.close()
-    barrier()
-    t0 = time.perf_counter()
-    smp = st.sample(1024, 2310)  # collective sampling of the full 2^n state (sharded.py)
-    sample_s = time.perf_counter() - t0
     nl = st.nl
     pk = peaks()
     gate_bytes = tot["n_passes"] * 32 * (1 << nl)
@@ -401,46 +390,76 @@ def run_sharded(args, rank, world, local):
     gate_s = times.get("gates", 0.0) / 1e3
     swap_s = times.get("swap", 0.0) / 1e3
     achieved = gate_bytes / gate_s / 1e9 if gate_s else 0.0
-    line = {"metric": METRIC, "value": round(wl.input_gates * args.steps / dev_s, 1),
-            "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(dev_s * 1e3 / args.steps, 3), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-            "config": {"workload": f"shard{n}: {n}-qubit random layered U3 + {{CX,CZ,RZZ}} "
-                                   f"circuit, {args.trotter or 10} layers, state split over "
-                                   f"{world} GPU(s)",
-                       "n_qubits": n, "local_qubits": nl, "input_gates": wl.input_gates,
-                       "fused_gates": stats["gates_after"], "passes_per_rank": tot["n_passes"],
-                       "device_gate_ops": tot["n_device_gates"], "octet_sweeps": tot["n_sweeps"],
-                       "qubit_swaps": prog.n_swaps,
-                       "qubit_swap_path": "peer-memory kernel (nsb_shard_swap_p2p)"
-                       if st.peer_swaps else "pack + NCCL send/recv + unpack",
-                       "parallelism": f"shard{world}",
-                       "l2": f"state shard 2^{nl} x 16 B >> L2; no flush needed"},
-            "host": host,
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
-                         "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
-                         "traffic": None, "peak_source": pk["source"],
-                         "note": "k_blocked only: passes x 32 B x 2^local per rank over the "
-                                 "summed gate-group device time of one profiled execution"},
-            "breakdown_ms": {k: round(v, 3) for k, v in times.items()},
-            "nvlink": {"bytes_sent_per_rank": swap_bytes,
-                       "achieved_gbs": round(swap_bytes / swap_s / 1e9, 1) if swap_s else None,
-                       "note": "per qubit swap each rank sends and receives half its shard"},
-            "e2e": {"value": round(wl.input_gates / e2e_s, 1), "unit": UNIT,
-                    "h2d_bytes_per_step": int(fops.nbytes + wl.params.nbytes + pool.nbytes),
-                    "d2h_bytes_per_step": 8, "s_per_step": round(e2e_s, 4),
-                    "note": "schedule + plan upload from host op arrays + run + norm read-back"},
-            "sampling": {"shots": 1024, "s": round(sample_s, 4), "distinct": len(smp),
-                         "note": "ShardedState.sample after the last run: device chunk sums, "
-                                 "one fetched chunk per hit, indices all-gathered"},
-            "norm": norm, "gpu_launches": None, "clocks": clk,
-            "cpu_baseline": {"value": None, "unit": UNIT, "cores": 1, "kind": "port",
-                             "sample": f"infeasible: the reference holds 2 x 2^{n} x 16 B "
-                                       "on one host (engine.py:51, 68-71)"}}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
+    out = {"workload": f"shard{n}: {n}-qubit random layered U3 + {{CX,CZ,RZZ}} circuit, "
+                       f"{layers} layers, state split over {world} GPU(s)",
+           "n_qubits": n, "local_qubits": nl, "input_gates": wl.input_gates,
+           "fused_gates": stats["gates_after"],
+           "value": round(wl.input_gates * steps / dev_s, 1), "unit": UNIT,
+           "ms_per_run": round(dev_s * 1e3 / steps, 3), "steps": steps, "warmup": warmup,
+           "scaling": "strong", "n_gpus": world, "qubit_swaps": prog.n_swaps,
+           "qubit_swap_path": "peer-memory kernel (nsb_shard_swap_p2p)" if st.peer_swaps
+           else "pack + NCCL send/recv + unpack",
+           "passes_per_rank": tot["n_passes"], "device_gate_ops": tot["n_device_gates"],
+           "breakdown_ms": {k: round(v, 3) for k, v in times.items()},
+           "gate_groups_hbm": {"achieved_gbs": round(achieved, 1), "peak": pk["hbm_gbs"],
+                               "frac": round(achieved / pk["hbm_gbs"], 4)},
+           "nvlink": {"bytes_sent_per_rank": swap_bytes,
+                      "achieved_gbs": round(swap_bytes / swap_s / 1e9, 1) if swap_s else None},
+           "host": host}
+    if extras:
+        t0 = time.perf_counter()
+        st.reset()
+        p2 = st.compile(fops, wl.params, pool)
+        p2.run()
+        out["norm"] = st.norm()
+        e2e_s = time.perf_counter() - t0
+        p2.close()
+        out["e2e"] = {"value": round(wl.input_gates / e2e_s, 1), "unit": UNIT,
+                      "h2d_bytes_per_step": int(fops.nbytes + wl.params.nbytes + pool.nbytes),
+                      "d2h_bytes_per_step": 8, "s_per_step": round(e2e_s, 4),
+                      "note": "schedule + plan upload from host op arrays + run + norm read-back"}
+        barrier()
+        t0 = time.perf_counter()
+        smp = st.sample(1024, 2310)  # collective sampling of the full 2^n state (sharded.py)
+        out["sampling"] = {"shots": 1024, "s": round(time.perf_counter() - t0, 4),
+                           "distinct": len(smp)}
     prog.close()
     st.close()
+    return out
+
+
+def run_sharded(args, rank, world, local):
+    """BASELINE config 5: one state split over all ranks (sharded.py)."""
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    torch.cuda.set_device(local)
+    clocks = Clocks(local)
+    m = sharded_measure(args.qubits, args.trotter or 10, rank, world, local, args.steps,
+                        args.warmup, extras=True)
+    clk = clocks.stop()
+    line = {"metric": METRIC, "value": m["value"], "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": m["ms_per_run"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic",
+            "config": {"workload": m["workload"], "n_qubits": m["n_qubits"],
+                       "input_gates": m["input_gates"], "fused_gates": m["fused_gates"],
+                       "parallelism": f"shard{world}",
+                       "l2": f"state shard 2^{m['local_qubits']} x 16 B >> L2; no flush needed"},
+            "sharded": m,
+            "roofline": {"bound": "hbm", "achieved": m["gate_groups_hbm"]["achieved_gbs"],
+                         "peak": m["gate_groups_hbm"]["peak"], "unit": "GB/s",
+                         "frac": m["gate_groups_hbm"]["frac"], "traffic": None,
+                         "note": "k_blocked only: passes x 32 B x 2^local per rank over the "
+                                 "summed gate-group device time of one profiled execution"},
+            "e2e": m["e2e"], "gpu_launches": None, "clocks": clk,
+            "cpu_baseline": {"value": None, "unit": UNIT, "cores": 1, "kind": "port",
+                             "sample": f"infeasible: the reference holds 2 x 2^{args.qubits} "
+                                       "x 16 B on one host (engine.py:51, 68-71)"}}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
@@ -579,6 +598,16 @@ def run_ours(args, rank, world, local):
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "s_per_step": round(e2e_s, 4)},
             "wall_s": round(wall, 3), "gpu_launches": launches, "clocks": clk}
+    if not args.no_sharded and args.config == "deep21":
+        # the multi-GPU design itself (the replicas above need no exchange):
+        # strong scaling of one 32-qubit state split over all N GPUs, and the
+        # 34-qubit config 5 state from N = 2 on
+        del prog, state
+        torch.cuda.empty_cache()
+        sh = [sharded_measure(32, 10, rank, world, local, 2, 1)]
+        if world >= 2:
+            sh.append(sharded_measure(34, 10, rank, world, local, 1, 1))
+        line["sharded"] = sh
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, args.ref_budget)
     if rank == 0:
@@ -603,6 +632,8 @@ def main():
     ap.add_argument("--ref-step-s", type=float, default=1.5,
                     help="--impl reference: seconds of oracle work per timed step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sharded", action="store_true",
+                    help="skip the sharded strong-scaling sub-measurement (shard32 / shard34)")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":

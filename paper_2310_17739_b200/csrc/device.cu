@@ -604,6 +604,20 @@ __device__ __forceinline__ void gate_octet_pair(double2 (&xs)[NO][8],
   }
 }
 
+// Register-axis exchange (four-axis groups): octet position P <-> octet index
+template <int P, int NO>
+__device__ __forceinline__ void swap_axis_q(double2 (&xs)[NO][8]) {
+  static_assert(NO == 2, "the octet index is an axis only with two octets per thread");
+  constexpr int A = 1 << P;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    if (!(c & A)) {
+      const double2 t = xs[0][c | A];
+      xs[0][c | A] = xs[1][c];
+      xs[1][c] = t;
+    }
+}
+
 template <int NO>
 __device__ __forceinline__ void gate_octet_diag(double2 (&xs)[NO][8],
                                                 const double2* __restrict__ m) {
@@ -633,8 +647,9 @@ __device__ __forceinline__ uint32_t thread_table_entry(const GroupDesc& d, int e
 
 // One octet sweep: src -> registers -> dst (different buffers).  Thread t
 // owns octets t + j T (j < kOctets, T = kPassThreads; octet-index bit
-// kThreadBits selects the second octet).  `kap` holds 3 parity bits per
-// tile of the batch (the axes' out-of-tile rows).
+// kThreadBits selects the second octet -- a fourth axis in four-axis
+// groups).  `kap` holds 8 parity bits per tile of the batch (the axes'
+// out-of-tile rows): 4 for the load placement, 4 for the store placement.
 __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
                                             double2* __restrict__ dst, int k, int nvalid,
                                             const GroupDesc& G, const GateOp* __restrict__ ops,
@@ -657,11 +672,16 @@ __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
     const int oi = t + (q << kThreadBits);
     a[q] = (v & 0xffffu) ^ (q ? G.tcol[kThreadBits] : 0);
     r[q] = (v >> 16) ^ (q ? G.rtcol[kThreadBits] : 0);
-    const int sh = 3 * (oi >> cb);  // tiles >= 4 exist only as garbage octets
-    const unsigned kp = sh < 12 ? (kap >> sh) & 7u : 0u;
-    if (kp & 1) { a[q] ^= m0; r[q] ^= r0; }
-    if (kp & 2) { a[q] ^= m1; r[q] ^= r1; }
-    if (kp & 4) { a[q] ^= m2; r[q] ^= r2; }
+    const int sh = 8 * (oi >> cb);  // tiles >= 4 exist only as garbage octets
+    const unsigned kp = sh < 32 ? (kap >> sh) & 0xffu : 0u;
+    if (kp & 1) r[q] ^= r0;
+    if (kp & 2) r[q] ^= r1;
+    if (kp & 4) r[q] ^= r2;
+    if (kp & 8) r[q] ^= G.rtcol[kThreadBits];
+    if (kp & 16) a[q] ^= m0;
+    if (kp & 32) a[q] ^= m1;
+    if (kp & 64) a[q] ^= m2;
+    if (kp & 128) a[q] ^= G.tcol[kThreadBits];
   }
   double2 x[NO][8];
 #pragma unroll
@@ -733,6 +753,15 @@ __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
         gate_octet_diag<NO>(x, m);
         if (last) store();
         break;
+#if NSB_OCTETS == 2
+#define NSB_GQ(P)                                                        \
+  case (kPatQ0 + P) * 16 + kPermute:                                     \
+    swap_axis_q<P, NO>(x);                                               \
+    if (last) store();                                                   \
+    break;
+      NSB_GQ(0) NSB_GQ(1) NSB_GQ(2)
+#undef NSB_GQ
+#endif
 #undef NSB_GT
 #undef NSB_G1
 #undef NSB_G2ALL
@@ -769,7 +798,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // the same pass streams into the other shared-memory buffer with cp.async.
 constexpr size_t kBlockedSmemBytes = sizeof(double2) * (3 * kTileAmpsMax + kMaxPassMats) +
                                      sizeof(GroupDesc) * kMaxPassGates +
-                                     sizeof(GateOp) * kMaxPassGates;
+                                     sizeof(GateOp) * kMaxPassOps;
 
 __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
   // dynamic shared memory: 3 batch buffers (current, gate-sweep target,
@@ -895,8 +924,13 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           if (b < nvalid) {
+            unsigned kl = 0;  // per axis (= load position)
 #pragma unroll
-            for (int i = 0; i < 3; ++i) gm |= (__popcll(tbase[b] & d.r_out[i]) & 1u) << (3 * b + i);
+            for (int i = 0; i < 4; ++i) kl |= (__popcll(tbase[b] & d.r_out[i]) & 1u) << i;
+            unsigned ks = 0;  // per store position: the axis placed there
+#pragma unroll
+            for (int j = 0; j < 4; ++j) ks |= ((kl >> ((d.perm >> (2 * j)) & 3u)) & 1u) << j;
+            gm |= (kl | ks << 4) << (8 * b);
           }
         }
         s_gm[tid] = gm;

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <complex>
 #include <atomic>
 #include <exception>
@@ -622,7 +623,10 @@ struct Axis {
 
 struct OpenGroup {
   int nax = 0;
-  Axis ax[3];
+  int maxax = 3;           // 4: four-axis group (the octet index is the fourth axis)
+  Axis ax[4];
+  int pos[4] = {0, 1, 2, 3};  // axis -> register position (3 = octet index)
+  int at[4] = {0, 1, 2, 3};   // register position -> axis
   uint32_t rcol[16];       // read map of the group's loads
   uint32_t axm = 0;        // union of the (unpadded) axis masks
   bool r_id = true;        // read map is the identity
@@ -632,8 +636,17 @@ struct OpenGroup {
 
 // axis slots of the gate's qubits in the group (adding axes if allowed);
 // false if the gate needs a fourth axis or clashes with the group's frame
+std::atomic<long> g_join_fail[3];  // NSB_PLAN_DEBUG: dual conflict, axis overflow, ok
+struct JoinReport {
+  ~JoinReport() {
+    if (std::getenv("NSB_PLAN_DEBUG"))
+      std::fprintf(stderr, "join: dual %ld overflow %ld ok %ld\n", g_join_fail[0].load(),
+                   g_join_fail[1].load(), g_join_fail[2].load());
+  }
+} g_join_report;
+
 bool join_axes(OpenGroup& G, const Axis* ga, int nq, int* slot) {
-  Axis tmp[3];
+  Axis tmp[4];
   int n = G.nax;
   for (int i = 0; i < n; ++i) tmp[i] = G.ax[i];
   for (int a = 0; a < nq; ++a) {
@@ -642,8 +655,14 @@ bool join_axes(OpenGroup& G, const Axis* ga, int nq, int* slot) {
       if (tmp[i] == ga[a]) found = i;
     if (found < 0) {
       for (int i = 0; i < n; ++i)
-        if (parity32(ga[a].rin & tmp[i].m) || parity32(tmp[i].rin & ga[a].m)) return false;
-      if (n == 3) return false;
+        if (parity32(ga[a].rin & tmp[i].m) || parity32(tmp[i].rin & ga[a].m)) {
+          ++g_join_fail[0];
+          return false;
+        }
+      if (n == G.maxax) {
+        ++g_join_fail[1];
+        return false;
+      }
       tmp[n] = ga[a];
       found = n++;
     }
@@ -651,6 +670,7 @@ bool join_axes(OpenGroup& G, const Axis* ga, int nq, int* slot) {
   }
   for (int i = 0; i < n; ++i) G.ax[i] = tmp[i];
   G.nax = n;
+  ++g_join_fail[2];
   return true;
 }
 
@@ -687,9 +707,10 @@ void finish_group(OpenGroup& G, int k, GroupDesc& d, uint32_t wm) {
       if (G.ax[j].m >> p & 1) a.rin ^= G.ax[j].rin;
     G.ax[G.nax++] = a;
   }
-  uint32_t f[3] = {G.ax[0].rin, G.ax[1].rin, G.ax[2].rin};
-  Basis C = kernel_basis(f, 3, k);
-  if (static_cast<int>(C.size()) != k - 3) throw std::logic_error("group axes are not dual");
+  const int na = G.nax;  // 3, or 4 (the octet index is axis 3)
+  uint32_t f[4] = {G.ax[0].rin, G.ax[1].rin, G.ax[2].rin, na == 4 ? G.ax[3].rin : 0u};
+  Basis C = kernel_basis(f, na, k);
+  if (static_cast<int>(C.size()) != k - na) throw std::logic_error("group axes are not dual");
   uint32_t cw[kWarpBits > 0 ? kWarpBits : 1] = {};
   if (local) {  // index bits 5.. (the warp bits) pick the warp's coset of W
     int wp[kWarpBits], nw = 0;
@@ -742,12 +763,21 @@ void finish_group(OpenGroup& G, int k, GroupDesc& d, uint32_t wm) {
     return out;
   };
   for (int i = 0; i < 3; ++i) {
-    d.am[i] = static_cast<uint16_t>(swz11(G.ax[i].m));
-    d.ram[i] = static_cast<uint16_t>(swz11(rmap(G.ax[i].m)));
-    d.r_out[i] = G.ax[i].rout;
+    d.am[i] = static_cast<uint16_t>(swz11(G.ax[G.at[i]].m));  // final placement
+    d.ram[i] = static_cast<uint16_t>(swz11(rmap(G.ax[i].m)));  // loads: axis i at i
+  }
+  d.perm = 0;
+  for (int j = 0; j < 4; ++j) {
+    d.r_out[j] = j < na ? G.ax[j].rout : 0;
+    d.perm |= static_cast<uint8_t>((na == 4 ? G.at[j] : j) << (2 * j));
   }
   const int cb = k - 3;
   for (int b = 0; b < kIndexBits; ++b) {
+    if (na == 4 && b == kThreadBits) {  // the octet index: axis 3 (load), its final axis (store)
+      d.tcol[b] = static_cast<uint16_t>(swz11(G.ax[G.at[3]].m));
+      d.rtcol[b] = static_cast<uint16_t>(swz11(rmap(G.ax[3].m)));
+      continue;
+    }
     const uint32_t v = b < cb ? C[b] : (1u << (k + b - cb));  // then tile-in-batch bits
     d.tcol[b] = static_cast<uint16_t>(swz11(v));
     d.rtcol[b] = static_cast<uint16_t>(swz11(rmap(v)));
@@ -844,6 +874,7 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
     this->n_ops += H.n_ops;
     n_warp_syncs += H.n_warp_syncs;
     n_fused_group_ops += H.n_fused_group_ops;
+    n_axis_swaps += H.n_axis_swaps;
     flops += H.flops;
     for (int c = 0; c < kNumClasses; ++c) class_count[c] += H.class_count[c];
     running_scale2 *= H.tail_scale2;  // parts hold no measurement (split at markers)
@@ -1078,6 +1109,9 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
     if (popc(masks[i] | low) > k) throw std::logic_error("gate support exceeds the tile");
   }
   std::vector<uint64_t> sets;
+  // four-axis groups: full tiles with two octets per thread (NSB_THREE_AXIS=1: off)
+  static const bool three_axis_env = std::getenv("NSB_THREE_AXIS") != nullptr;
+  const bool four_axis = kOctets == 2 && k == kTileQubitsMax && !three_axis_env;
   // one group slot stays free for a trailing read-map sweep
   auto pass_groups = pack_groups(masks, k, low, all, 256, sets, &deps, &weights,
                                  kMaxPassGates - 1, kMaxPassMats);
@@ -1115,6 +1149,7 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
     };
     auto start = [&]() {
       G = OpenGroup();
+      G.maxax = four_axis ? 4 : 3;
       std::memcpy(G.rcol, rcol, sizeof rcol);
       for (int i = 0; i < 16; ++i) rcol[i] = 1u << i;
       r_identity = true;
@@ -1131,6 +1166,29 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
       }
     };
     auto add_op = [&](const PhysGate& g, int* slot) {
+      // register positions of the gate's axes; a gate on the axis held by the
+      // octet index first exchanges it with a position the gate does not use
+      int p0 = G.pos[slot[0]], p1 = g.nq == 2 ? G.pos[slot[1]] : -1;
+      if (p0 == 3 || p1 == 3) {
+        int f = 0;
+        while (f == p0 || f == p1) ++f;
+        GateOp sw{};
+        sw.cls = kPermute;
+        sw.pat = static_cast<uint8_t>(kPatQ0 + f);
+        sw.mat = static_cast<int16_t>(G.mats.size() / 2);
+        sw.kind = static_cast<uint8_t>(sw.pat * 16 + sw.cls);
+        G.ops.push_back(sw);
+        ++n_axis_swaps;
+        const int a3 = G.at[3], af = G.at[f];
+        G.at[3] = af;
+        G.at[f] = a3;
+        G.pos[a3] = f;
+        G.pos[af] = 3;
+        p0 = G.pos[slot[0]];
+        p1 = g.nq == 2 ? G.pos[slot[1]] : -1;
+      }
+      slot[0] = p0;
+      if (g.nq == 2) slot[1] = p1;
       GateOp op{};
       op.cls = g.cls;
       op.cols = g.cols;
@@ -1254,17 +1312,58 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
       size_t used = 0;
       for (const OpenGroup& H : closed) used += H.mats.size() / 2;
       for (OpenGroup& H : closed) {
-        GateOp f;
-        std::vector<double> pk;
-        if (!fuse_group(H.ops, H.mats, f, pk)) continue;
-        const size_t after = used - H.mats.size() / 2 + pk.size() / 2;
-        if (after > size_t(kMaxPassMats)) continue;
-        used = after;
-        n_fused_group_ops += static_cast<int64_t>(H.ops.size()) - 1;
-        n_ops -= static_cast<int64_t>(H.ops.size()) - 1;
-        f.mat = 0;
-        H.ops.assign(1, f);
-        H.mats = std::move(pk);
+        // runs of gates between register-axis exchanges act on the same
+        // three octet positions: each run is fused on its own
+        std::vector<GateOp> ops_out;
+        std::vector<double> mats_out;
+        size_t i = 0;
+        while (i < H.ops.size()) {
+          if (H.ops[i].pat >= kPatQ0) {
+            GateOp sw = H.ops[i++];
+            sw.mat = static_cast<int16_t>(mats_out.size() / 2);
+            ops_out.push_back(sw);
+            continue;
+          }
+          size_t j = i;
+          while (j < H.ops.size() && H.ops[j].pat < kPatQ0) ++j;
+          std::vector<GateOp> run_ops(H.ops.begin() + i, H.ops.begin() + j);
+          GateOp f;
+          std::vector<double> pk;
+          size_t run_size = 0;  // complex values of the run's own payloads
+          auto op_size = [&](const GateOp& o) -> size_t {
+            static const int kN[kNumClasses] = {4, 2, 16, 8, 4, 4, 0, 0, 8, 8, 8, 0, 0, 8, 8, 8};
+            if (o.pat == kPatAll) return 8;
+            if (o.pat >= kPatT0 && o.pat <= kPatT2) return 16;
+            if (o.pat >= kPatD01 && o.pat <= kPatD12) return 32;
+            return static_cast<size_t>(kN[o.cls]);
+          };
+          for (const GateOp& o : run_ops) run_size += op_size(o);
+          bool fused = false;
+          if (fuse_group(run_ops, H.mats, f, pk)) {
+            const size_t after = used - run_size + pk.size() / 2;
+            if (after <= size_t(kMaxPassMats)) {
+              used = after;
+              n_fused_group_ops += static_cast<int64_t>(run_ops.size()) - 1;
+              n_ops -= static_cast<int64_t>(run_ops.size()) - 1;
+              f.mat = static_cast<int16_t>(mats_out.size() / 2);
+              ops_out.push_back(f);
+              mats_out.insert(mats_out.end(), pk.begin(), pk.end());
+              fused = true;
+            }
+          }
+          if (!fused)
+            for (GateOp o : run_ops) {
+              const size_t nv = op_size(o);
+              const size_t src = static_cast<size_t>(o.mat);
+              o.mat = static_cast<int16_t>(mats_out.size() / 2);
+              mats_out.insert(mats_out.end(), H.mats.begin() + 2 * src,
+                              H.mats.begin() + 2 * (src + nv));
+              ops_out.push_back(o);
+            }
+          i = j;
+        }
+        H.ops = std::move(ops_out);
+        H.mats = std::move(mats_out);
       }
     }
     for (size_t g = 0; g < closed.size(); ++g) {
@@ -1287,6 +1386,8 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
     }
     P.group_end = static_cast<int32_t>(groups.size());
     P.op_end = static_cast<int32_t>(gate_ops.size());
+    if (P.op_end - P.op_begin > kMaxPassOps || P.group_end - P.group_begin > kMaxPassGates)
+      throw std::logic_error("pass exceeds the kernel's op / group capacity");
     P.mat_count = static_cast<int32_t>(matrices.size() / 2) - P.mat_begin;
     passes.push_back(P);
   }

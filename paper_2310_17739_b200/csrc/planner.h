@@ -39,7 +39,7 @@ constexpr int kOctets = NSB_OCTETS;              // octets per thread per sweep 
 constexpr int kThreadBits = kOctets == 2 ? 7 : 8;
 constexpr int kPassThreads = 1 << kThreadBits;  // 4 (8) warps per CTA, two CTAs per SM
 constexpr int kIndexBits = kThreadBits + (kOctets == 2 ? 1 : 0);  // octet-index bits of a batch
-static_assert(kIndexBits <= 9, "GroupDesc holds 9 index-bit offsets");
+static_assert(kIndexBits <= 8, "GroupDesc holds 8 index-bit offsets");
 constexpr int kLowQubits = 3;                    // always-tiled qubits 0..2 (128 B runs)
 // States up to this many qubits stay L2-resident inside a launch: their
 // tiles need not hold qubits 0..2 (sector efficiency matters less than the
@@ -98,17 +98,28 @@ enum GateClass : uint8_t {
 // them in a pass reads its octets through their composition R (a linear map
 // of tile-local indices) and writes in place order, so the r* fields hold
 // the same offsets mapped through R (equal to the plain ones when R = I).
+//
+// Four-axis groups (full 11-qubit tiles): a thread's two octets are the two
+// values of a FOURTH logical axis -- its 16 registers are the coset of a
+// four-dimensional subspace -- so a run of gates touching up to four axes is
+// one sweep.  Gates still address the octet positions 0..2 only: before a
+// gate that needs the fourth axis, a register-axis exchange op (kPermute with
+// pattern kPatQ0..2, straight register moves, no arithmetic) swaps it with a
+// position the gate does not use.  Loads place axis i at position i (axis 3
+// on the octet index); stores use the final placement `perm`.  The
+// out-of-tile parity bits kappa are therefore taken per axis for the loads
+// and permuted for the stores.
 struct GroupDesc {        // 80 bytes
-  uint16_t am[3];         // swizzled axis masks (store side)
-  uint16_t ram[3];        // the same through the read map R (load side)
-  uint16_t tcol[9];       // swizzled offsets of octet-index bits (store side):
-                          // thread bits, then the thread's second-octet bit
-  uint16_t rtcol[9];      // load side
+  uint16_t am[3];         // swizzled masks of the axes at positions 0..2 after the ops (store)
+  uint16_t ram[3];        // axes 0..2 through the read map R (load side)
+  uint16_t tcol[8];       // swizzled offsets of octet-index bits (store side): thread
+                          // bits, then the octet index (a fourth axis, or a free vector)
+  uint16_t rtcol[8];      // load side
   uint8_t op_begin;       // first GateOp (relative to the pass's op_begin)
   uint8_t n_ops;          // 0: a pure read-map sweep
   uint8_t sync;           // 1: CTA barrier after this sweep; 0: warp-local, __syncwarp
-  uint8_t pad[5];
-  uint64_t r_out[3];      // out-of-tile parts of the axes' dual rows
+  uint8_t perm;           // store position j (2 bits each, j = 0..3) -> axis index
+  uint64_t r_out[4];      // out-of-tile parts of the axes' dual rows (axis 3: 0 if none)
 };
 static_assert(sizeof(GroupDesc) == 80, "GroupDesc layout");
 
@@ -125,7 +136,10 @@ enum AxisPattern : uint8_t {
   kPatT0 = 6, kPatT1 = 7, kPatT2 = 8, kPatAll = 9,
   // kPatD01/D02/D12 with class kDense2: a 4x4 on the two axes (slot 0 the
   // lower) with one block per value of the third axis (32 complex values)
-  kPatD01 = 10, kPatD02 = 11, kPatD12 = 12
+  kPatD01 = 10, kPatD02 = 11, kPatD12 = 12,
+  // kPatQ0..Q2 with class kPermute: exchange register position 0..2 with the
+  // octet index (four-axis groups; no matrix)
+  kPatQ0 = 13, kPatQ1 = 14, kPatQ2 = 15
 };
 struct GateOp {           // 8 bytes
   int16_t mat;            // offset (complex elements) in the pass's matrix block
@@ -139,7 +153,8 @@ static_assert(sizeof(GateOp) == 8, "GateOp layout");
 
 // Per pass the kernel stages the group descriptors, gate ops and the pass's
 // own block of packed matrices in shared memory (bounded by these limits).
-constexpr int kMaxPassGates = 40;   // gate ops per pass (and groups per pass)
+constexpr int kMaxPassGates = 40;   // gates per pass (and groups per pass)
+constexpr int kMaxPassOps = 80;     // gate ops per pass, register-axis exchanges included
 constexpr int kMaxPassMats = 384;   // complex elements (6 KiB)
 
 struct PassDesc {         // 112 bytes

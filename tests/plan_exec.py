@@ -22,9 +22,9 @@ PASS_DT = np.dtype([("group_begin", "<i4"), ("group_end", "<i4"), ("op_begin", "
                     ("measure_q", "<i4"), ("measure_slot", "<i4"), ("collapse_q", "<i4"),
                     ("collapse_slot", "<i4"), ("pad", "<i4"), ("tq", "i1", (16,)),
                     ("oq", "i1", (48,))])
-GROUP_DT = np.dtype([("am", "<u2", (3,)), ("ram", "<u2", (3,)), ("tcol", "<u2", (9,)),
-                     ("rtcol", "<u2", (9,)), ("op_begin", "u1"), ("n_ops", "u1"),
-                     ("sync", "u1"), ("pad", "u1", (5,)), ("r_out", "<u8", (3,))], align=True)
+GROUP_DT = np.dtype([("am", "<u2", (3,)), ("ram", "<u2", (3,)), ("tcol", "<u2", (8,)),
+                     ("rtcol", "<u2", (8,)), ("op_begin", "u1"), ("n_ops", "u1"),
+                     ("sync", "u1"), ("perm", "u1"), ("r_out", "<u8", (4,))], align=True)
 OP_DT = np.dtype([("mat", "<i2"), ("cls", "u1"), ("pat", "u1"), ("cols", "<u2"), ("kind", "u1"), ("pad", "u1")])
 OCTETS = 1 if os.environ.get("NSB_LIB_VARIANT") == "o1" else 2  # kOctets (build variant)
 THREAD_BITS = 7 if OCTETS == 2 else 8  # kThreadBits
@@ -36,6 +36,7 @@ TILE_MAX = 11  # kTileQubitsMax
 PATTERNS = {0: (0, 1), 1: (0, 2), 2: (1, 2), 3: (0,), 4: (1,), 5: (2,)}
 PAT_T, PAT_ALL = (6, 7, 8), 9  # whole-octet ops (planner.h kPatT0..T2, kPatAll)
 PAT_D = (10, 11, 12)  # two-axis whole-octet ops (planner.h kPatD01..D12)
+PAT_Q = (13, 14, 15)  # register position 0..2 <-> octet index (four-axis groups)
 
 
 class HostPlan:
@@ -95,11 +96,30 @@ def _swz(l):
     return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7)
 
 
+def _swap_q(x, p, axis=-1):
+    """swap_axis_q: exchange register position p with the octet index, whose
+    bit is octet-index bit THREAD_BITS of the (last) array axis."""
+    A = 1 << p
+    n = x[0].shape[-1]
+    t = np.arange(n)
+    lo = t[((t >> THREAD_BITS) & 1) == 0]
+    hi = lo | (1 << THREAD_BITS)
+    for c in range(8):
+        if c & A:
+            continue
+        a = x[c | A][..., lo].copy()
+        x[c | A][..., lo] = x[c][..., hi]
+        x[c][..., hi] = a
+
+
 def _gate(x, op, m):
     """One GateOp on the octet registers x[0..7] (arrays over threads),
     as gate2 / gate1 in csrc/device.cu."""
     pat = int(op["pat"])
     c = int(op["cls"])
+    if pat in PAT_Q:
+        _swap_q(x, pat - PAT_Q[0])
+        return
     if pat == PAT_ALL:  # whole-octet diagonal (planner group fusion)
         for r in range(8):
             x[r] = m[r] * x[r]
@@ -186,12 +206,14 @@ def _apply_group(B, G, ops, mats, tbases, k, nvalid):
         a ^= np.where((t >> b) & 1, int(G["tcol"][b]), 0)
         r ^= np.where((t >> b) & 1, int(G["rtcol"][b]), 0)
     tile = t >> cb
-    am = [int(v) for v in G["am"]]
-    ram = [int(v) for v in G["ram"]]
-    for i in range(3):
-        kap = _parity(tbases[tile].astype(np.uint64) & np.uint64(G["r_out"][i]))
-        a ^= kap * am[i]
-        r ^= kap * ram[i]
+    am = [int(v) for v in G["am"]] + [int(G["tcol"][THREAD_BITS])]
+    ram = [int(v) for v in G["ram"]] + [int(G["rtcol"][THREAD_BITS])]
+    perm = [(int(G["perm"]) >> (2 * j)) & 3 for j in range(4)]
+    kl = [_parity(tbases[tile].astype(np.uint64) & np.uint64(G["r_out"][i])) for i in range(4)]
+    for i in range(4):  # loads: axis i at position i; stores: axis perm[j] at position j
+        r ^= kl[i] * ram[i]
+        a ^= kl[perm[i]] * am[i]
+    am, ram = am[:3], ram[:3]
     U = _swz
     st = [a ^ (am[0] if c & 1 else 0) ^ (am[1] if c & 2 else 0) ^ (am[2] if c & 4 else 0)
           for c in range(8)]
@@ -227,14 +249,16 @@ def _apply_group_batches(Bs, G, ops, mats, tbs, k, nvalid):
         a0 ^= np.where((t >> b) & 1, int(G["tcol"][b]), 0)
         r0 ^= np.where((t >> b) & 1, int(G["rtcol"][b]), 0)
     tile = t >> cb
-    am = [int(v) for v in G["am"]]
-    ram = [int(v) for v in G["ram"]]
+    am = [int(v) for v in G["am"]] + [int(G["tcol"][THREAD_BITS])]
+    ram = [int(v) for v in G["ram"]] + [int(G["rtcol"][THREAD_BITS])]
+    perm = [(int(G["perm"]) >> (2 * j)) & 3 for j in range(4)]
     a = np.broadcast_to(a0, (Bs.shape[0], n_act)).copy()
     r = np.broadcast_to(r0, (Bs.shape[0], n_act)).copy()
-    for i in range(3):
-        kap = _parity(tbs[:, tile].astype(np.uint64) & np.uint64(G["r_out"][i]))
-        a ^= kap * am[i]
-        r ^= kap * ram[i]
+    kl = [_parity(tbs[:, tile].astype(np.uint64) & np.uint64(G["r_out"][i])) for i in range(4)]
+    for i in range(4):
+        r ^= kl[i] * ram[i]
+        a ^= kl[perm[i]] * am[i]
+    am, ram = am[:3], ram[:3]
     U = _swz
     x = [np.take_along_axis(Bs, U(r ^ (ram[0] if c & 1 else 0) ^ (ram[1] if c & 2 else 0)
                                     ^ (ram[2] if c & 4 else 0)), axis=1) for c in range(8)]
@@ -261,7 +285,7 @@ def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12, workers=1
         block = plan.mats[int(P["mat_begin"]):int(P["mat_begin"]) + int(P["mat_count"])]
         groups = plan.groups[int(P["group_begin"]):int(P["group_end"])]
         pops = plan.ops[int(P["op_begin"]):int(P["op_end"])]
-        assert len(groups) <= 40 and len(pops) <= 40 and len(block) <= 384
+        assert len(groups) <= 40 and len(pops) <= 80 and len(block) <= 384
         cq = int(P["collapse_q"])
         per, extra = divmod(n_tiles, workers)
         if fast:  # every batch of nb consecutive tiles at once
