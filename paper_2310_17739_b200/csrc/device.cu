@@ -618,6 +618,21 @@ __device__ __forceinline__ void swap_axis_q(double2 (&xs)[NO][8]) {
     }
 }
 
+// Register CX (four-axis groups): registers c' = c with bit K ^= bit J over
+// the 16 registers of the two octets (bit 3 = octet index)
+template <int J, int K, int NO>
+__device__ __forceinline__ void reg_cx(double2 (&xs)[NO][8]) {
+  static_assert(NO == 2, "register ops need two octets per thread");
+#pragma unroll
+  for (int c = 0; c < 16; ++c)
+    if ((c >> J & 1) && !(c >> K & 1)) {
+      const int e = c | (1 << K);
+      const double2 t = xs[c >> 3][c & 7];
+      xs[c >> 3][c & 7] = xs[e >> 3][e & 7];
+      xs[e >> 3][e & 7] = t;
+    }
+}
+
 template <int NO>
 __device__ __forceinline__ void gate_octet_diag(double2 (&xs)[NO][8],
                                                 const double2* __restrict__ m) {
@@ -693,7 +708,7 @@ __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
 #else
       x[q][c] = src[r[q] ^ ((c & 1) ? r0 : 0) ^ ((c & 2) ? r1 : 0) ^ ((c & 4) ? r2 : 0)];
 #endif
-  const int n_ops = G.n_ops;
+  const int n_ops = G.n_ops();
   auto store = [&]() {
 #pragma unroll
     for (int q = 0; q < NO; ++q)
@@ -761,6 +776,14 @@ __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
     break;
       NSB_GQ(0) NSB_GQ(1) NSB_GQ(2)
 #undef NSB_GQ
+#define NSB_RCX(J, K)                                                    \
+  case 208 + J * 3 + (K < J ? K : K - 1):                               \
+    reg_cx<J, K, NO>(x);                                                 \
+    if (last) store();                                                   \
+    break;
+      NSB_RCX(0, 1) NSB_RCX(0, 2) NSB_RCX(0, 3) NSB_RCX(1, 0) NSB_RCX(1, 2) NSB_RCX(1, 3)
+      NSB_RCX(2, 0) NSB_RCX(2, 1) NSB_RCX(2, 3) NSB_RCX(3, 0) NSB_RCX(3, 1) NSB_RCX(3, 2)
+#undef NSB_RCX
 #endif
 #undef NSB_GT
 #undef NSB_G1
@@ -927,9 +950,9 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
             unsigned kl = 0;  // per axis (= load position)
 #pragma unroll
             for (int i = 0; i < 4; ++i) kl |= (__popcll(tbase[b] & d.r_out[i]) & 1u) << i;
-            unsigned ks = 0;  // per store position: the axis placed there
+            unsigned ks = 0;  // per store position: parity of the load rows summing to its row
 #pragma unroll
-            for (int j = 0; j < 4; ++j) ks |= ((kl >> ((d.perm >> (2 * j)) & 3u)) & 1u) << j;
+            for (int j = 0; j < 4; ++j) ks |= (__popc(kl & (d.kmat >> (4 * j)) & 15u) & 1u) << j;
             gm |= (kl | ks << 4) << (8 * b);
           }
         }
@@ -958,7 +981,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
 #pragma unroll 1
       for (int g = 0; g < ((p.debug & 1) ? 0 : n_groups); ++g) {
         const GroupDesc& d = s_groups[g];
-        const bool cta_sync = d.sync;  // read before the sweep: no load latency after it
+        const bool cta_sync = d.sync();  // read before the sweep: no load latency after it
         double2* out = smem + spare * kTileAmpsMax;
         apply_group(tile, out, k, nvalid, d, s_ops + d.op_begin, s_mats, s_gm[g], s_ttab[g]);
         const int tmp = cur;

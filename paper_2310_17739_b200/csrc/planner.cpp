@@ -621,12 +621,16 @@ struct Axis {
   bool operator==(const Axis& o) const { return m == o.m && rin == o.rin && rout == o.rout; }
 };
 
+// A group's registers form a dual basis (m_j, r_j) of a <= 4-dimensional
+// subspace V of tile masks and the matching row space R (register position j:
+// 0..2 octet bits, 3 the octet index).  Register ops (kRegCX / kRegSwap:
+// straight register moves) change the basis without moving data in memory;
+// `ax` is the current basis, `ax0` the one the loads use.
 struct OpenGroup {
   int nax = 0;
   int maxax = 3;           // 4: four-axis group (the octet index is the fourth axis)
-  Axis ax[4];
-  int pos[4] = {0, 1, 2, 3};  // axis -> register position (3 = octet index)
-  int at[4] = {0, 1, 2, 3};   // register position -> axis
+  Axis ax[4];              // current register basis
+  Axis ax0[4];             // load basis
   uint32_t rcol[16];       // read map of the group's loads
   uint32_t axm = 0;        // union of the (unpadded) axis masks
   bool r_id = true;        // read map is the identity
@@ -636,40 +640,127 @@ struct OpenGroup {
 
 // axis slots of the gate's qubits in the group (adding axes if allowed);
 // false if the gate needs a fourth axis or clashes with the group's frame
-std::atomic<long> g_join_fail[3];  // NSB_PLAN_DEBUG: dual conflict, axis overflow, ok
+std::atomic<long> g_join_fail[3];  // NSB_PLAN_DEBUG: degenerate, axis overflow, ok
 struct JoinReport {
   ~JoinReport() {
     if (std::getenv("NSB_PLAN_DEBUG"))
-      std::fprintf(stderr, "join: dual %ld overflow %ld ok %ld\n", g_join_fail[0].load(),
+      std::fprintf(stderr, "join: degenerate %ld overflow %ld ok %ld\n", g_join_fail[0].load(),
                    g_join_fail[1].load(), g_join_fail[2].load());
   }
 } g_join_report;
 
-bool join_axes(OpenGroup& G, const Axis* ga, int nq, int* slot) {
-  Axis tmp[4];
-  int n = G.nax;
-  for (int i = 0; i < n; ++i) tmp[i] = G.ax[i];
+inline int dotp(const Axis& row, uint32_t m) { return parity32(row.rin & m); }
+
+// register ops of four-axis groups (dispatch keys outside pat * 16 + cls use)
+constexpr uint8_t kKindRegCX = 208;  // + ordered pair index of (j, k), j != k < 4
+constexpr uint8_t kKindRegSwap[3] = {(kPatQ0 + 0) * 16 + kPermute, (kPatQ0 + 1) * 16 + kPermute,
+                                     (kPatQ0 + 2) * 16 + kPermute};
+inline uint8_t regcx_kind(int j, int k) { return kKindRegCX + j * 3 + (k < j ? k : k - 1); }
+
+// Place a gate's axes in the group: every gate axis (m, r) must lie in
+// V x R or extend both (keeping the basis dual); register ops then bring it
+// to a unit vector at an octet position.  On success the ops are appended
+// and pos[a] holds the gate axis' octet position; on failure G is unchanged.
+bool place_gate(OpenGroup& G, const Axis* ga, int nq, int* pos) {
+  Axis cur[4], load[4];
+  int d = G.nax;
+  for (int j = 0; j < 4; ++j) {
+    cur[j] = G.ax[j];
+    load[j] = G.ax0[j];
+  }
+  std::vector<GateOp> ops;
+  auto cx = [&](int j, int k) {  // registers c' = c with bit k ^= bit j
+    cur[j].m ^= cur[k].m;
+    cur[k].rin ^= cur[j].rin;
+    cur[k].rout ^= cur[j].rout;
+    GateOp o{};
+    o.cls = kPermute;
+    o.pat = kPatQ0;
+    o.kind = regcx_kind(j, k);
+    ops.push_back(o);
+  };
+  auto swap3 = [&](int f) {
+    std::swap(cur[f], cur[3]);
+    GateOp o{};
+    o.cls = kPermute;
+    o.pat = kPatQ0;
+    o.kind = kKindRegSwap[f];
+    ops.push_back(o);
+  };
+  uint32_t used = 0;  // positions taken by the gate's earlier axis
   for (int a = 0; a < nq; ++a) {
-    int found = -1;
-    for (int i = 0; i < n; ++i)
-      if (tmp[i] == ga[a]) found = i;
-    if (found < 0) {
-      for (int i = 0; i < n; ++i)
-        if (parity32(ga[a].rin & tmp[i].m) || parity32(tmp[i].rin & ga[a].m)) {
-          ++g_join_fail[0];
-          return false;
-        }
-      if (n == G.maxax) {
+    const uint32_t m = ga[a].m;
+    uint32_t mv = 0, al = 0, be = 0;
+    Axis rr{};
+    for (int j = 0; j < d; ++j) {
+      if (dotp(cur[j], m)) {
+        al |= 1u << j;
+        mv ^= cur[j].m;
+      }
+      if (dotp(ga[a], cur[j].m)) {
+        be |= 1u << j;
+        rr.rin ^= cur[j].rin;
+        rr.rout ^= cur[j].rout;
+      }
+    }
+    const bool inV = mv == m, inR = rr.rin == ga[a].rin && rr.rout == ga[a].rout;
+    if (!inV || !inR) {
+      if (inV || inR) {
+        ++g_join_fail[0];
+        return false;
+      }
+      if (d == G.maxax) {
         ++g_join_fail[1];
         return false;
       }
-      tmp[n] = ga[a];
-      found = n++;
+      Axis nw;
+      nw.m = m ^ mv;
+      nw.rin = ga[a].rin ^ rr.rin;
+      nw.rout = ga[a].rout ^ rr.rout;
+      if (!dotp(nw, nw.m)) {  // the extended pairing would be degenerate
+        ++g_join_fail[0];
+        return false;
+      }
+      cur[d] = load[d] = nw;
+      al |= 1u << d;
+      be |= 1u << d;
+      ++d;
     }
-    slot[a] = found;
+    // pivot: a free position with al = be = 1 (exists: al . be = 1), octet bits first
+    int p = -1;
+    for (int j = 0; j < d && p < 0; ++j)
+      if (!(used >> j & 1) && (al & be) >> j & 1) p = j;
+    if (p < 0) throw std::logic_error("gate axis has no pivot in the group");
+    for (int k = 0; k < d; ++k)  // masks: clear al outside p
+      if (k != p && (al >> k & 1)) {
+        cx(p, k);
+        al ^= 1u << k;
+        if (be >> k & 1) be ^= 1u << p;  // beta_p ^= beta_k
+      }
+    for (int k = 0; k < d; ++k)  // rows: clear be outside p
+      if (k != p && (be >> k & 1)) {
+        cx(k, p);
+        be ^= 1u << k;
+      }
+    if (p == 3) {
+      int f = 0;
+      while (used >> f & 1) ++f;
+      swap3(f);
+      p = f;
+    }
+    used |= 1u << p;
+    pos[a] = p;
   }
-  for (int i = 0; i < n; ++i) G.ax[i] = tmp[i];
-  G.nax = n;
+  for (int j = 0; j < 4; ++j) {
+    G.ax[j] = cur[j];
+    G.ax0[j] = load[j];
+  }
+  G.nax = d;
+  for (const GateOp& o : ops) {
+    GateOp q = o;
+    q.mat = static_cast<int16_t>(G.mats.size() / 2);
+    G.ops.push_back(q);
+  }
   ++g_join_fail[2];
   return true;
 }
@@ -695,7 +786,7 @@ void finish_group(OpenGroup& G, int k, GroupDesc& d, uint32_t wm) {
   while (G.nax < 3) {  // pad with a free axis of the tile (outside the warp positions)
     uint32_t f[3 + kWarpBits];
     int nf = 0;
-    for (int i = 0; i < G.nax; ++i) f[nf++] = G.ax[i].rin;
+    for (int i = 0; i < G.nax; ++i) f[nf++] = G.ax[i].rin;  // rows span R (either basis)
     for (uint32_t w = wm; w; w &= w - 1) f[nf++] = w & (0u - w);
     Basis ker = kernel_basis(f, nf, k);
     if (ker.empty()) throw std::logic_error("no free axis in the tile");
@@ -705,10 +796,11 @@ void finish_group(OpenGroup& G, int k, GroupDesc& d, uint32_t wm) {
     a.rin = 1u << p;
     for (int j = 0; j < G.nax; ++j)
       if (G.ax[j].m >> p & 1) a.rin ^= G.ax[j].rin;
+    G.ax0[G.nax] = a;  // dual to both bases (orthogonal to V and R)
     G.ax[G.nax++] = a;
   }
   const int na = G.nax;  // 3, or 4 (the octet index is axis 3)
-  uint32_t f[4] = {G.ax[0].rin, G.ax[1].rin, G.ax[2].rin, na == 4 ? G.ax[3].rin : 0u};
+  uint32_t f[4] = {G.ax0[0].rin, G.ax0[1].rin, G.ax0[2].rin, na == 4 ? G.ax0[3].rin : 0u};
   Basis C = kernel_basis(f, na, k);
   if (static_cast<int>(C.size()) != k - na) throw std::logic_error("group axes are not dual");
   uint32_t cw[kWarpBits > 0 ? kWarpBits : 1] = {};
@@ -763,19 +855,23 @@ void finish_group(OpenGroup& G, int k, GroupDesc& d, uint32_t wm) {
     return out;
   };
   for (int i = 0; i < 3; ++i) {
-    d.am[i] = static_cast<uint16_t>(swz11(G.ax[G.at[i]].m));  // final placement
-    d.ram[i] = static_cast<uint16_t>(swz11(rmap(G.ax[i].m)));  // loads: axis i at i
+    d.am[i] = static_cast<uint16_t>(swz11(G.ax[i].m));         // final basis (stores)
+    d.ram[i] = static_cast<uint16_t>(swz11(rmap(G.ax0[i].m)));  // load basis
   }
-  d.perm = 0;
+  // store parity bits: final row j = sum_i M_ji (load row i), M_ji = r_j . m0_i
+  d.kmat = 0;
   for (int j = 0; j < 4; ++j) {
-    d.r_out[j] = j < na ? G.ax[j].rout : 0;
-    d.perm |= static_cast<uint8_t>((na == 4 ? G.at[j] : j) << (2 * j));
+    d.r_out[j] = j < na ? G.ax0[j].rout : 0;
+    for (int i = 0; i < 4; ++i) {
+      const int mji = (j < na && i < na) ? dotp(G.ax[j], G.ax0[i].m) : (i == j ? 1 : 0);
+      d.kmat |= static_cast<uint16_t>(mji << (4 * j + i));
+    }
   }
   const int cb = k - 3;
   for (int b = 0; b < kIndexBits; ++b) {
     if (na == 4 && b == kThreadBits) {  // the octet index: axis 3 (load), its final axis (store)
-      d.tcol[b] = static_cast<uint16_t>(swz11(G.ax[G.at[3]].m));
-      d.rtcol[b] = static_cast<uint16_t>(swz11(rmap(G.ax[3].m)));
+      d.tcol[b] = static_cast<uint16_t>(swz11(G.ax[3].m));
+      d.rtcol[b] = static_cast<uint16_t>(swz11(rmap(G.ax0[3].m)));
       continue;
     }
     const uint32_t v = b < cb ? C[b] : (1u << (k + b - cb));  // then tile-in-batch bits
@@ -1166,29 +1262,6 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
       }
     };
     auto add_op = [&](const PhysGate& g, int* slot) {
-      // register positions of the gate's axes; a gate on the axis held by the
-      // octet index first exchanges it with a position the gate does not use
-      int p0 = G.pos[slot[0]], p1 = g.nq == 2 ? G.pos[slot[1]] : -1;
-      if (p0 == 3 || p1 == 3) {
-        int f = 0;
-        while (f == p0 || f == p1) ++f;
-        GateOp sw{};
-        sw.cls = kPermute;
-        sw.pat = static_cast<uint8_t>(kPatQ0 + f);
-        sw.mat = static_cast<int16_t>(G.mats.size() / 2);
-        sw.kind = static_cast<uint8_t>(sw.pat * 16 + sw.cls);
-        G.ops.push_back(sw);
-        ++n_axis_swaps;
-        const int a3 = G.at[3], af = G.at[f];
-        G.at[3] = af;
-        G.at[f] = a3;
-        G.pos[a3] = f;
-        G.pos[af] = 3;
-        p0 = G.pos[slot[0]];
-        p1 = g.nq == 2 ? G.pos[slot[1]] : -1;
-      }
-      slot[0] = p0;
-      if (g.nq == 2) slot[1] = p1;
       GateOp op{};
       op.cls = g.cls;
       op.cols = g.cols;
@@ -1227,7 +1300,7 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
           Axis ga[2];
           axes_of(g, ga);
           int slot[2] = {0, 0};
-          if (!(dm & blocked) && join_axes(G, ga, g.nq, slot)) {
+          if (!(dm & blocked) && place_gate(G, ga, g.nq, slot)) {
             add_op(g, slot);
           } else {
             blocked |= dm;
@@ -1370,7 +1443,7 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
       OpenGroup& H = closed[g];
       GroupDesc d{};
       d.op_begin = static_cast<uint8_t>(gate_ops.size() - P.op_begin);
-      d.n_ops = static_cast<uint8_t>(H.ops.size());
+      d.n_ops_sync = static_cast<uint8_t>(H.ops.size());
       const int32_t mat0 = static_cast<int32_t>(matrices.size() / 2) - P.mat_begin;
       for (GateOp op : H.ops) {
         op.mat = static_cast<int16_t>(op.mat + mat0);
@@ -1380,8 +1453,9 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
       const uint32_t wm = wsel[g];
       const bool next = g + 1 < closed.size() && wm && wsel[g + 1] == wm;
       finish_group(H, k, d, wm);
-      d.sync = next ? 0 : 1;
-      if (!d.sync) ++n_warp_syncs;
+      if (!next) d.n_ops_sync |= 128;
+      if (next) ++n_warp_syncs;
+      for (const GateOp& o : H.ops) n_axis_swaps += o.cls == kPermute && o.pat == kPatQ0;
       groups.push_back(d);
     }
     P.group_end = static_cast<int32_t>(groups.size());

@@ -25,6 +25,11 @@
 
 #include <cstdint>
 
+#ifndef __CUDACC__
+#define __host__
+#define __device__
+#endif
+
 namespace nsb {
 
 #ifndef NSB_TILE_MAX
@@ -116,10 +121,13 @@ struct GroupDesc {        // 80 bytes
                           // bits, then the octet index (a fourth axis, or a free vector)
   uint16_t rtcol[8];      // load side
   uint8_t op_begin;       // first GateOp (relative to the pass's op_begin)
-  uint8_t n_ops;          // 0: a pure read-map sweep
-  uint8_t sync;           // 1: CTA barrier after this sweep; 0: warp-local, __syncwarp
-  uint8_t perm;           // store position j (2 bits each, j = 0..3) -> axis index
-  uint64_t r_out[4];      // out-of-tile parts of the axes' dual rows (axis 3: 0 if none)
+  uint8_t n_ops_sync;     // bits 0..6: gate ops (0: a pure read-map sweep); bit 7: CTA
+                          // barrier after this sweep (else warp-local, __syncwarp)
+  uint16_t kmat;          // store parity map: bits 4j..4j+3 = the load rows whose sum
+                          // is the final row at position j
+  uint64_t r_out[4];      // out-of-tile parts of the load basis rows (position 3: 0 if none)
+  __host__ __device__ int n_ops() const { return n_ops_sync & 127; }
+  __host__ __device__ bool sync() const { return n_ops_sync >> 7; }
 };
 static_assert(sizeof(GroupDesc) == 80, "GroupDesc layout");
 

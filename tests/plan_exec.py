@@ -23,8 +23,8 @@ PASS_DT = np.dtype([("group_begin", "<i4"), ("group_end", "<i4"), ("op_begin", "
                     ("collapse_slot", "<i4"), ("pad", "<i4"), ("tq", "i1", (16,)),
                     ("oq", "i1", (48,))])
 GROUP_DT = np.dtype([("am", "<u2", (3,)), ("ram", "<u2", (3,)), ("tcol", "<u2", (8,)),
-                     ("rtcol", "<u2", (8,)), ("op_begin", "u1"), ("n_ops", "u1"),
-                     ("sync", "u1"), ("perm", "u1"), ("r_out", "<u8", (4,))], align=True)
+                     ("rtcol", "<u2", (8,)), ("op_begin", "u1"), ("n_ops_sync", "u1"),
+                     ("kmat", "<u2"), ("r_out", "<u8", (4,))], align=True)
 OP_DT = np.dtype([("mat", "<i2"), ("cls", "u1"), ("pat", "u1"), ("cols", "<u2"), ("kind", "u1"), ("pad", "u1")])
 OCTETS = 1 if os.environ.get("NSB_LIB_VARIANT") == "o1" else 2  # kOctets (build variant)
 THREAD_BITS = 7 if OCTETS == 2 else 8  # kThreadBits
@@ -36,7 +36,10 @@ TILE_MAX = 11  # kTileQubitsMax
 PATTERNS = {0: (0, 1), 1: (0, 2), 2: (1, 2), 3: (0,), 4: (1,), 5: (2,)}
 PAT_T, PAT_ALL = (6, 7, 8), 9  # whole-octet ops (planner.h kPatT0..T2, kPatAll)
 PAT_D = (10, 11, 12)  # two-axis whole-octet ops (planner.h kPatD01..D12)
-PAT_Q = (13, 14, 15)  # register position 0..2 <-> octet index (four-axis groups)
+PAT_Q = (13, 14, 15)  # register ops of four-axis groups (kind picks the op)
+KIND_SWAP = {220: 0, 236: 1, 252: 2}  # register position p <-> octet index
+KIND_CX = {208 + j * 3 + (k if k < j else k - 1): (j, k) for j in range(4) for k in range(4)
+           if j != k}  # registers c' = c with bit k ^= bit j (bit 3 = octet index)
 
 
 class HostPlan:
@@ -96,9 +99,27 @@ def _swz(l):
     return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7)
 
 
-def _swap_q(x, p, axis=-1):
-    """swap_axis_q: exchange register position p with the octet index, whose
-    bit is octet-index bit THREAD_BITS of the (last) array axis."""
+def _reg_cx(x, j, k):
+    """reg_cx / swap_axis_q of csrc/device.cu on the 16 registers of a thread:
+    register c (bit 3 = octet index = octet-index bit THREAD_BITS of the last
+    array axis) -- registers c' = c with bit k ^= bit j."""
+    n = x[0].shape[-1]
+    t = np.arange(n)
+    half = [t[((t >> THREAD_BITS) & 1) == q] for q in (0, 1)]
+    get = lambda c: x[c & 7][..., half[c >> 3]]
+
+    def put(c, v):
+        x[c & 7][..., half[c >> 3]] = v
+    for c in range(16):
+        if (c >> j) & 1 and not (c >> k) & 1:
+            e = c | (1 << k)
+            a, b = get(c).copy(), get(e).copy()
+            put(c, b)
+            put(e, a)
+
+
+def _swap_q(x, p):
+    """swap_axis_q: exchange register position p with the octet index."""
     A = 1 << p
     n = x[0].shape[-1]
     t = np.arange(n)
@@ -118,7 +139,11 @@ def _gate(x, op, m):
     pat = int(op["pat"])
     c = int(op["cls"])
     if pat in PAT_Q:
-        _swap_q(x, pat - PAT_Q[0])
+        kind = int(op["kind"])
+        if kind in KIND_SWAP:
+            _swap_q(x, KIND_SWAP[kind])
+        else:
+            _reg_cx(x, *KIND_CX[kind])
         return
     if pat == PAT_ALL:  # whole-octet diagonal (planner group fusion)
         for r in range(8):
@@ -208,11 +233,15 @@ def _apply_group(B, G, ops, mats, tbases, k, nvalid):
     tile = t >> cb
     am = [int(v) for v in G["am"]] + [int(G["tcol"][THREAD_BITS])]
     ram = [int(v) for v in G["ram"]] + [int(G["rtcol"][THREAD_BITS])]
-    perm = [(int(G["perm"]) >> (2 * j)) & 3 for j in range(4)]
+    kmat = int(G["kmat"])
     kl = [_parity(tbases[tile].astype(np.uint64) & np.uint64(G["r_out"][i])) for i in range(4)]
-    for i in range(4):  # loads: axis i at position i; stores: axis perm[j] at position j
-        r ^= kl[i] * ram[i]
-        a ^= kl[perm[i]] * am[i]
+    for j in range(4):  # loads: load basis rows; stores: final row j = sum of kmat's load rows
+        r ^= kl[j] * ram[j]
+        ks = np.zeros_like(kl[0])
+        for i in range(4):
+            if (kmat >> (4 * j + i)) & 1:
+                ks ^= kl[i]
+        a ^= ks * am[j]
     am, ram = am[:3], ram[:3]
     U = _swz
     st = [a ^ (am[0] if c & 1 else 0) ^ (am[1] if c & 2 else 0) ^ (am[2] if c & 4 else 0)
@@ -230,7 +259,7 @@ def _apply_group(B, G, ops, mats, tbases, k, nvalid):
         stores = [np.sort(np.concatenate([U(s_)[warp == w] for s_ in st])) for w in range(n_warps)]
     x = [S[U(l)] for l in ld]
     o0 = int(G["op_begin"])
-    for op in ops[o0:o0 + int(G["n_ops"])]:
+    for op in ops[o0:o0 + (int(G["n_ops_sync"]) & 127)]:
         _gate(x, op, mats[int(op["mat"]):])
     for s, v in zip(st, x):
         B[U(s)] = v
@@ -251,19 +280,23 @@ def _apply_group_batches(Bs, G, ops, mats, tbs, k, nvalid):
     tile = t >> cb
     am = [int(v) for v in G["am"]] + [int(G["tcol"][THREAD_BITS])]
     ram = [int(v) for v in G["ram"]] + [int(G["rtcol"][THREAD_BITS])]
-    perm = [(int(G["perm"]) >> (2 * j)) & 3 for j in range(4)]
+    kmat = int(G["kmat"])
     a = np.broadcast_to(a0, (Bs.shape[0], n_act)).copy()
     r = np.broadcast_to(r0, (Bs.shape[0], n_act)).copy()
     kl = [_parity(tbs[:, tile].astype(np.uint64) & np.uint64(G["r_out"][i])) for i in range(4)]
-    for i in range(4):
-        r ^= kl[i] * ram[i]
-        a ^= kl[perm[i]] * am[i]
+    for j in range(4):
+        r ^= kl[j] * ram[j]
+        ks = np.zeros_like(kl[0])
+        for i in range(4):
+            if (kmat >> (4 * j + i)) & 1:
+                ks ^= kl[i]
+        a ^= ks * am[j]
     am, ram = am[:3], ram[:3]
     U = _swz
     x = [np.take_along_axis(Bs, U(r ^ (ram[0] if c & 1 else 0) ^ (ram[1] if c & 2 else 0)
                                     ^ (ram[2] if c & 4 else 0)), axis=1) for c in range(8)]
     o0 = int(G["op_begin"])
-    for op in ops[o0:o0 + int(G["n_ops"])]:
+    for op in ops[o0:o0 + (int(G["n_ops_sync"]) & 127)]:
         _gate(x, op, mats[int(op["mat"]):])
     for c in range(8):
         st = a ^ (am[0] if c & 1 else 0) ^ (am[1] if c & 2 else 0) ^ (am[2] if c & 4 else 0)
@@ -314,7 +347,7 @@ def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12, workers=1
                     if prev is not None and loads is not None:  # __syncwarp only: each warp reads its own writes
                         for w in range(len(loads)):
                             assert np.array_equal(loads[w], prev[w])
-                    prev = stores if int(G["sync"]) == 0 else None
+                    prev = stores if int(G["n_ops_sync"]) >> 7 == 0 else None
                 state[idx] = B
         mq = int(P["measure_q"])
         if mq >= 0:
