@@ -1205,9 +1205,13 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
     if (popc(masks[i] | low) > k) throw std::logic_error("gate support exceeds the tile");
   }
   std::vector<uint64_t> sets;
-  // four-axis groups: full tiles with two octets per thread (NSB_THREE_AXIS=1: off)
-  static const bool three_axis_env = std::getenv("NSB_THREE_AXIS") != nullptr;
-  const bool four_axis = kOctets == 2 && k == kTileQubitsMax && !three_axis_env;
+  // four-axis groups with a register frame: full tiles, two octets per thread.
+  // Off by default (NSB_FOUR_AXIS=1 turns them on): on deep21 they cut the
+  // sweeps by 35 % but split group fusion into runs between register ops, so
+  // 30 % more gate ops run and the kernel -- bound by per-op latency, not by
+  // shared-memory traffic -- got 31 % slower (832 vs 634 ms).
+  static const bool four_axis_env = std::getenv("NSB_FOUR_AXIS") != nullptr;
+  const bool four_axis = kOctets == 2 && k == kTileQubitsMax && four_axis_env;
   // one group slot stays free for a trailing read-map sweep
   auto pass_groups = pack_groups(masks, k, low, all, 256, sets, &deps, &weights,
                                  kMaxPassGates - 1, kMaxPassMats);
