@@ -595,7 +595,7 @@ bool fuse_group(const std::vector<GateOp>& ops, const std::vector<double>& mats,
       }
       fused.cls = kDense2;
       fused.pat = static_cast<uint8_t>(kPatD01 + pat);
-      fused.kind = static_cast<uint8_t>(fused.pat * 16 + fused.cls);
+      fused.kind = static_cast<uint8_t>(op_kind(fused.pat, fused.cls));
       return true;
     }
     const int T = 1 << t;
@@ -610,7 +610,7 @@ bool fuse_group(const std::vector<GateOp>& ops, const std::vector<double>& mats,
     fused.cls = kDense1;
     fused.pat = static_cast<uint8_t>(kPatT0 + t);
   }
-  fused.kind = static_cast<uint8_t>(fused.pat * 16 + fused.cls);
+  fused.kind = static_cast<uint8_t>(op_kind(fused.pat, fused.cls));
   return true;
 }
 
@@ -651,11 +651,8 @@ struct JoinReport {
 
 inline int dotp(const Axis& row, uint32_t m) { return parity32(row.rin & m); }
 
-// register ops of four-axis groups (dispatch keys outside pat * 16 + cls use)
-constexpr uint8_t kKindRegCX = 208;  // + ordered pair index of (j, k), j != k < 4
-constexpr uint8_t kKindRegSwap[3] = {(kPatQ0 + 0) * 16 + kPermute, (kPatQ0 + 1) * 16 + kPermute,
-                                     (kPatQ0 + 2) * 16 + kPermute};
-inline uint8_t regcx_kind(int j, int k) { return kKindRegCX + j * 3 + (k < j ? k : k - 1); }
+// register ops of register-frame groups (planner.h reg_cx_kind / reg_swap_kind)
+inline uint8_t regcx_kind(int j, int k) { return static_cast<uint8_t>(reg_cx_kind(j, k)); }
 
 // Place a gate's axes in the group: every gate axis (m, r) must lie in
 // V x R or extend both (keeping the basis dual); register ops then bring it
@@ -684,7 +681,7 @@ bool place_gate(OpenGroup& G, const Axis* ga, int nq, int* pos) {
     GateOp o{};
     o.cls = kPermute;
     o.pat = kPatQ0;
-    o.kind = kKindRegSwap[f];
+    o.kind = static_cast<uint8_t>(reg_swap_kind(f));
     ops.push_back(o);
   };
   uint32_t used = 0;  // positions taken by the gate's earlier axis
@@ -1282,7 +1279,7 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
         }
         op.pat = static_cast<uint8_t>(slot[0] == 0 ? (slot[1] == 1 ? kPat01 : kPat02) : kPat12);
       }
-      op.kind = static_cast<uint8_t>(op.pat * 16 + op.cls);
+      op.kind = static_cast<uint8_t>(op_kind(op.pat, op.cls));
       G.ops.push_back(op);
       ++n_ops;
     };

@@ -149,6 +149,27 @@ enum AxisPattern : uint8_t {
   // octet index (four-axis groups; no matrix)
   kPatQ0 = 13, kPatQ1 = 14, kPatQ2 = 15
 };
+// Dense dispatch keys (GateOp::kind): consecutive small integers, so the
+// kernel's switch compiles to one indirect branch through a jump table
+// instead of a compare-and-branch tree over pat * 16 + cls.
+#ifndef NSB_SPARSE_KINDS
+__host__ __device__ constexpr int op_kind(int pat, int cls) {
+  // 2q patterns: 13 classes each (kPermute and the 1q classes never occur there)
+  return pat <= kPat12 ? pat * 13 + (cls < kPermute ? cls - kDense2 : cls - kDense2 - 1)
+       : pat <= kPat2 ? 39 + (pat - kPat0) * 2 + (cls == kDiag1 ? 1 : 0)
+       : pat <= kPatT2 ? 45 + (pat - kPatT0)
+       : pat == kPatAll ? 48
+       : pat <= kPatD12 ? 49 + (pat - kPatD01)
+       : 67;
+}
+__host__ __device__ constexpr int reg_swap_kind(int p) { return 52 + p; }
+__host__ __device__ constexpr int reg_cx_kind(int j, int k) { return 55 + j * 3 + (k < j ? k : k - 1); }
+#else  // A/B: the sparse keys of round 1
+__host__ __device__ constexpr int op_kind(int pat, int cls) { return pat * 16 + cls; }
+__host__ __device__ constexpr int reg_swap_kind(int p) { return (kPatQ0 + p) * 16 + kPermute; }
+__host__ __device__ constexpr int reg_cx_kind(int j, int k) { return 208 + j * 3 + (k < j ? k : k - 1); }
+#endif
+
 struct GateOp {           // 8 bytes
   int16_t mat;            // offset (complex elements) in the pass's matrix block
   uint8_t cls;            // GateClass

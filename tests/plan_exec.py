@@ -37,8 +37,8 @@ PATTERNS = {0: (0, 1), 1: (0, 2), 2: (1, 2), 3: (0,), 4: (1,), 5: (2,)}
 PAT_T, PAT_ALL = (6, 7, 8), 9  # whole-octet ops (planner.h kPatT0..T2, kPatAll)
 PAT_D = (10, 11, 12)  # two-axis whole-octet ops (planner.h kPatD01..D12)
 PAT_Q = (13, 14, 15)  # register ops of four-axis groups (kind picks the op)
-KIND_SWAP = {220: 0, 236: 1, 252: 2}  # register position p <-> octet index
-KIND_CX = {208 + j * 3 + (k if k < j else k - 1): (j, k) for j in range(4) for k in range(4)
+KIND_SWAP = {52 + p: p for p in range(3)}  # register position p <-> octet index (planner.h)
+KIND_CX = {55 + j * 3 + (k if k < j else k - 1): (j, k) for j in range(4) for k in range(4)
            if j != k}  # registers c' = c with bit k ^= bit j (bit 3 = octet index)
 
 
