@@ -555,7 +555,7 @@ def run_ours(args, rank, world, local):
     smem_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
     smem_ach = info.n_sweeps * 32 * (1 << n) / kernel_s / 1e12
     l2_gbs = l2_copy_gbs(16 << n)
-    profile = ROOT / "profiles" / "r01_dram_bytes.json"
+    profile = ROOT / "profiles" / "r02_dram_bytes.json"
     traffic = None
     if profile.exists():
         traffic = json.loads(profile.read_text()).get(args.config)
