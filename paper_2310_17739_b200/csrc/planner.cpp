@@ -5,11 +5,12 @@
 //     sparsity by exact zeros (skipping an exact zero term is bit-identical
 //     to multiplying by it), deduplicate identical payloads by hash;
 //  2. cut the op list into items: gate runs, k>=3 dense gates, MEASURE, RESET;
-//  3. schedule each gate run into passes (tile qubit sets of <= 12 qubits)
-//     with a dependency-respecting greedy look-ahead: a gate joins the open
-//     pass if it fits the tile set and no skipped earlier gate shares a
-//     qubit with it; otherwise it is deferred to a later pass;
-//  4. inside a pass, schedule stages (4-qubit register groups) the same way;
+//  3. schedule each gate run into passes (tile qubit sets of <= 11 qubits,
+//     kTileQubitsMax) with a dependency-respecting greedy look-ahead: a gate
+//     joins the open pass if it fits the tile set and no skipped earlier gate
+//     shares a qubit with it; otherwise it is deferred to a later pass;
+//  4. inside a pass, group gates into octet sweeps (three-axis register
+//     groups with a register frame, planner.h) the same way;
 //  5. for MMA mode, build a single pass list in which each MEASURE becomes
 //     an epilogue reduction of the preceding pass and a collapse prologue of
 //     the next one (engine.py:183-191, 164-167).
