@@ -271,6 +271,24 @@ int nsb_plan_run_segment(nsb_ctx* ctx, nsb_plan* plan, int64_t seg, nsb_status* 
 int nsb_plan_segment_marker(const nsb_plan* plan, int64_t seg, int32_t* kind, int32_t* qubit,
                             int32_t* step);
 
+/* Rejection mode (replaces engine.run(..., "rejection"), engine.py:431-474).
+ * Plan: built with NSB_PLAN_EXACT.  uniforms: the caller's Philox stream
+ * (rng.random() draws, in order; n_uniforms available), consumed in the
+ * reference's order -- one per executed MEASURE and RESET, one per accepted
+ * shot's sample; *consumed returns how many were used (the caller advances
+ * its generator by that many).  Outputs: *accepted, step_rejections
+ * [n_measures], sample_index[shots] (basis index of each accepted shot's
+ * sample, engine.py:207-222; -1 for a rejected shot), first_state (nullable,
+ * 2^n interleaved complex): the first accepted shot's final state (the
+ * reference's energy input).  Filter-shaped circuits are replayed from one
+ * device pass along the accepted path (a reset draw of 1 falls back to an
+ * explicit shot); flags & 1 forces explicit per-shot simulation.
+ * NSB_EINVAL if the stream runs out. */
+int nsb_plan_run_rejection(nsb_ctx* ctx, nsb_plan* plan, const double* uniforms,
+                           int64_t n_uniforms, int64_t shots, int32_t flags, int64_t* consumed,
+                           int64_t* accepted, int64_t* step_rejections, int64_t* sample_index,
+                           double* first_state, nsb_status* st);
+
 /* Factor between the state's P(|0>) at assertion `step` and the reference's
  * (engine.py:159-161): the product of |s|^2 of the near-scalar gates s I the
  * plan does not execute since the previous assertion (nsb_plan_info

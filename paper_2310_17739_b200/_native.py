@@ -127,6 +127,8 @@ _SIGNATURES = {
                                                ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
     "nsb_plan_last_timing": (ctypes.c_int, [_P, ctypes.POINTER(_D), ctypes.POINTER(_I64)]),
     "nsb_plan_p0_scale": (ctypes.c_int, [_P, ctypes.c_int32, _P]),
+    "nsb_plan_run_rejection": (ctypes.c_int, [_P, _P, _P, _I64, _I64, ctypes.c_int32, _P, _P,
+                                              _P, _P, _P, _ST]),
     "nsb_timer_start": (ctypes.c_int, [_P, _ST]),
     "nsb_timer_stop": (ctypes.c_int, [_P, ctypes.POINTER(_D), _ST]),
     "nsb_comm_unique_id": (ctypes.c_int, [_P, _ST]),

@@ -2027,6 +2027,180 @@ int nsb_plan_run_segment(nsb_ctx* c, nsb_plan* P, int64_t seg, nsb_status* st) {
   });
 }
 
+// Rejection mode (engine.py:431-474) through the C ABI.  The caller supplies
+// its Philox uniforms (rng.random() draws in order); they are consumed exactly
+// as the reference consumes them: one per executed MEASURE, one per executed
+// RESET, one per accepted shot's sample (engine.py:443, 452, 462).
+// Filter-shaped circuits (every MEASURE followed by a RESET of the same qubit,
+// every RESET after such a MEASURE) are replayed: ONE device pass along the
+// all-zero path records P(0) at every marker (with the reset's
+// renormalisation, engine.py:455), and the shots are decided on the host from
+// the draws; a reset draw of 1 leaves that path and the shot is simulated
+// explicitly from its forced outcomes on.  Other circuits (or flags & 1) run
+// every shot on the device.
+int nsb_plan_run_rejection(nsb_ctx* c, nsb_plan* P, const double* uniforms, int64_t n_uniforms,
+                           int64_t shots, int32_t flags, int64_t* consumed, int64_t* accepted,
+                           int64_t* step_rejections, int64_t* sample_index, double* first_state,
+                           nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    if (!P || P->ctx != c) throw std::invalid_argument("plan belongs to another context");
+    if (P->n != c->n) throw std::invalid_argument("plan was built for another qubit count");
+    if (shots < 0 || (shots > 0 && (!uniforms || !sample_index)) || !consumed || !accepted)
+      throw std::invalid_argument("bad rejection arguments");
+    NSB_CUDA(cudaSetDevice(c->device));
+    const HostPlan& H = P->host;
+    if (H.n_identity_gates) throw std::invalid_argument("rejection mode needs an exact plan");
+    const std::vector<Item>& items = H.items;
+    int64_t cur = 0;
+    auto draw = [&]() -> double {
+      if (cur >= n_uniforms) throw std::invalid_argument("uniform stream exhausted");
+      return uniforms[cur++];
+    };
+    for (int64_t s = 0; s < H.n_measures; ++s) step_rejections[s] = 0;
+    *accepted = 0;
+    std::vector<double> cum;
+    auto cumsum = [&]() {  // np.cumsum of re*re + im*im (sequential, engine.py:215-216)
+      if (c->probs.count < c->n_amps) c->probs.alloc(c->n_amps);
+      dev::k_probabilities<<<grid_for(c->n_amps, 256, c), 256, 0, c->stream>>>(
+          c->amps.ptr, c->n_amps, c->probs.ptr);
+      NSB_CUDA(cudaGetLastError());
+      cum.resize(c->n_amps);
+      copy_d2h(c, cum.data(), c->probs.ptr, c->n_amps * sizeof(double));
+      for (uint64_t i = 1; i < c->n_amps; ++i) cum[i] = cum[i - 1] + cum[i];
+    };
+    auto sample_one = [&](double u) -> int64_t {  // searchsorted(side="right"), clipped
+      const double x = u * cum.back();
+      int64_t idx = std::upper_bound(cum.begin(), cum.end(), x) - cum.begin();
+      return std::min<int64_t>(idx, static_cast<int64_t>(cum.size()) - 1);
+    };
+    auto restart = [&]() {
+      dev::k_vacuum<<<grid_for(c->n_amps, 256, c), 256, 0, c->stream>>>(c->amps.ptr, c->n_amps);
+      NSB_CUDA(cudaGetLastError());
+    };
+    static const double kX[8] = {0, 0, 1, 0, 1, 0, 0, 0};
+    bool kept = false;
+    auto keep = [&]() {
+      if (first_state && !kept) {
+        copy_d2h(c, first_state, c->amps.ptr, c->n_amps * sizeof(double2));
+        kept = true;
+      }
+    };
+    // one shot on the device from |0...0> (engine.py:436-463); the first
+    // forced.size() marker outcomes are given (their draws were taken)
+    auto explicit_shot = [&](const std::vector<int>& forced, int64_t shot) {
+      restart();
+      size_t j = 0;
+      for (size_t i = 0; i < items.size(); ++i) {
+        const Item& it = items[i];
+        if (it.kind == Item::kMeasure || it.kind == Item::kReset) {
+          const double p0 = half_norm(c, it.qubit, 0);
+          const int outcome = j < forced.size() ? forced[j] : (draw() < p0 ? 0 : 1);
+          ++j;
+          if (it.kind == Item::kMeasure) {
+            if (outcome) {
+              ++step_rejections[it.step];
+              sample_index[shot] = -1;
+              return;
+            }
+            project(c, it.qubit, 0, p0);
+          } else {
+            project(c, it.qubit, outcome, outcome == 0 ? p0 : 1.0 - p0);
+            if (outcome) apply_matrix(c, kX, &it.qubit, 1, nullptr);
+          }
+        } else {
+          run_item(c, P, it);
+        }
+      }
+      ++*accepted;
+      cumsum();
+      sample_index[shot] = sample_one(draw());
+      keep();
+    };
+    bool replay = !(flags & 1);
+    {  // filter-shaped: MEASURE q, RESET q pairs only (engine._replayable)
+      std::vector<const Item*> marks;
+      for (const Item& it : items)
+        if (it.kind == Item::kMeasure || it.kind == Item::kReset) marks.push_back(&it);
+      if (marks.empty() || marks.size() % 2) replay = false;
+      for (size_t i = 0; replay && i < marks.size(); i += 2)
+        replay = marks[i]->kind == Item::kMeasure && marks[i + 1]->kind == Item::kReset &&
+                 marks[i]->qubit == marks[i + 1]->qubit;
+    }
+    if (!replay) {
+      for (int64_t s = 0; s < shots; ++s) explicit_shot({}, s);
+      *consumed = cur;
+      NSB_CUDA(cudaStreamSynchronize(c->stream));
+      return;
+    }
+    // one pass along the accepted path
+    struct Mark {
+      bool measure;
+      int step;
+      double p;
+    };
+    std::vector<Mark> path;
+    bool reachable = true;
+    restart();
+    for (const Item& it : items) {
+      if (it.kind == Item::kMeasure) {
+        const double p0 = half_norm(c, it.qubit, 0);
+        path.push_back({true, it.step, p0});
+        if (p0 <= 0.0) {
+          reachable = false;  // every shot stops here
+          break;
+        }
+        project(c, it.qubit, 0, p0);
+      } else if (it.kind == Item::kReset) {
+        const double p0 = half_norm(c, it.qubit, 0);
+        path.push_back({false, -1, p0});
+        project(c, it.qubit, 0, p0);
+      } else {
+        run_item(c, P, it);
+      }
+    }
+    if (reachable) {
+      cumsum();
+      keep();
+    }
+    std::vector<double> path_cum = cum;
+    for (int64_t s = 0; s < shots; ++s) {
+      std::vector<int> forced;
+      int outcome = -1;  // >= 0: rejected at that step; -2: left the path
+      for (const Mark& m : path) {
+        const double u = draw();
+        if (m.measure) {
+          if (!(u < m.p)) {
+            outcome = m.step;
+            break;
+          }
+          forced.push_back(0);
+        } else if (!(u < m.p)) {  // reset drew 1
+          forced.push_back(1);
+          outcome = -2;
+          break;
+        } else {
+          forced.push_back(0);
+        }
+      }
+      if (outcome >= 0) {
+        ++step_rejections[outcome];
+        sample_index[s] = -1;
+        continue;
+      }
+      if (outcome == -2) {
+        explicit_shot(forced, s);
+        cum = path_cum;
+        continue;
+      }
+      ++*accepted;
+      sample_index[s] = sample_one(draw());
+    }
+    *consumed = cur;
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
 int nsb_plan_segment_marker(const nsb_plan* P, int64_t seg, int32_t* kind, int32_t* qubit,
                             int32_t* step) {
   if (!P || seg < 0 || seg >= static_cast<int64_t>(P->host.items.size()) || !kind || !qubit ||

@@ -415,8 +415,9 @@ def test_relabeling_frame_against_oracle(n, terms):
 
 @pytest.mark.gpu
 def test_rejection_replay_equals_explicit_shots(golden):
-    """The replay fast path gives the same tallies, samples and accepted
-    count as simulating every shot (same seed, same Philox stream)."""
+    """The replay fast path of nsb_plan_run_rejection gives the same tallies,
+    samples, accepted count and consumed draws as simulating every shot
+    (same seed, same Philox stream), and both equal the reference's goldens."""
     from paper_2310_17739_b200 import engine as E
     d = golden("filter8")
     fused = to_circuit(d, "fused_")
@@ -426,17 +427,15 @@ def test_rejection_replay_equals_explicit_shots(golden):
     n_steps = sum(1 for ins in instrs[:end] if ins.gate is E.Gate.MEASURE)
     state = E.StateVector(fused.n_qubits)
     prog = E.DeviceProgram(state, packed.ops, packed.params, packed.payloads, exact=True)
-    items = prog.items()
-    assert E._replayable(items)
-    fast = E._rejection(state, prog, items, n_steps, 200, E._as_rng(11), False)
-    # explicit path: force the non-replay branch
-    saved = E._replayable
-    try:
-        E._replayable = lambda items: False
-        slow = E._rejection(state, prog, items, n_steps, 200, E._as_rng(11), False)
-    finally:
-        E._replayable = saved
-    assert fast[0] == slow[0] and fast[2] == slow[2] and fast[1] == slow[1]
+    r1, r2 = E._as_rng(int(d["seeds"][0])), E._as_rng(int(d["seeds"][0]))
+    shots = int(d["rej_shots"])
+    fast = E._rejection(state, prog, n_steps, shots, r1, False)
+    slow = E._rejection(state, prog, n_steps, shots, r2, False, explicit=True)
+    assert fast[:3] == slow[:3]
+    assert r1.random() == r2.random()  # both generators advanced by the same draws
+    assert fast[0] == int(d["rej_accepted"])
+    assert fast[2] == list(d["rej_steps"])
+    assert fast[1] == golden_samples(d, "rej_")
 
 
 @pytest.mark.parametrize("env", [{}, {"NSB_NO_GROUP_FUSION": "1"}, {"NSB_EXACT_CLASSES": "1"}])
