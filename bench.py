@@ -14,8 +14,9 @@ value  device-resident: the fused plan is already in HBM; timed with CUDA
        after W warm-ups; L2 flushed (256 MiB write) between steps because the
        21-qubit state (32 MiB) would otherwise stay L2-resident across steps.
 e2e    through the C ABI with host buffers: per step the packed fused op list
-       (host) is planned + uploaded, executed, and the probabilities are read
-       back (D2H) and sampled on the host -- what `run()` does per call.
+       (host) is planned + uploaded + executed (nsb_run_mma_streamed: part s+1
+       planned while part s runs), and the probabilities are read back (D2H)
+       and sampled on the host -- what `run()` does per call.
 cpu_baseline / --impl reference: the oracle port of the reference engine
        (numpy einsum, as nucsim.engine) on a bounded prefix of the same fused
        gate stream, single-threaded, extrapolated per gate.  The reference
@@ -473,7 +474,8 @@ def run_ours(args, rank, world, local):
     torch.cuda.set_device(local)
     os.environ["NUCSIM_DEVICE"] = str(local)
     from paper_2310_17739_b200 import _native as N
-    from paper_2310_17739_b200.engine import DeviceProgram, StateVector, _sample_from
+    from paper_2310_17739_b200.engine import (DeviceProgram, StateVector, _sample_from,
+                                              _streamable, run_mma_streamed)
 
     wl, exe, pool, stats, host = make_workload(args.config, args.trotter)
     n = wl.n_qubits
@@ -529,11 +531,14 @@ def run_ours(args, rank, world, local):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         state.restart()
-        p2 = DeviceProgram(state, exe, wl.params, pool)
-        p2.run_mma()
+        if _streamable(exe, n):  # run()'s MMA path: planning streamed behind execution
+            run_mma_streamed(state, exe, wl.params, pool)
+        else:
+            p2 = DeviceProgram(state, exe, wl.params, pool)
+            p2.run_mma()
+            del p2  # the program is released inside the call, as run() does
         state.device_call("nsb_probabilities", N.ptr(probs))
         _sample_from(probs, n, 1024, rng)
-        del p2  # the program is released inside the call, as run() does
         e2e_times.append(time.perf_counter() - t0)
     e2e_s = float(np.median(e2e_times))
     if world > 1:  # whole job: every rank's call, slowest rank's time

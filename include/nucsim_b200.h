@@ -271,6 +271,18 @@ int nsb_plan_run_segment(nsb_ctx* ctx, nsb_plan* plan, int64_t seg, nsb_status* 
 int nsb_plan_segment_marker(const nsb_plan* plan, int64_t seg, int32_t* kind, int32_t* qubit,
                             int32_t* step);
 
+/* MMA run with planning streamed behind execution (replaces engine.run(...,
+ * "mma")'s gate loop, engine.py:414-423): the op list is cut at its MEASURE /
+ * RESET markers, a host thread plans the parts in order and part s runs on
+ * the device (one cooperative launch) while part s+1 is planned.  Same
+ * outputs and errors as nsb_plan_create + nsb_plan_run_mma (n_measures: the
+ * number of assertion probabilities written; device_ms, nullable: device
+ * time of the launches).  1q / 2q gates and >= 6 qubits only (else
+ * NSB_EINVAL: use the plan calls). */
+int nsb_run_mma_streamed(nsb_ctx* ctx, const nsb_op* ops, int64_t n_ops, const double* params,
+                         const double* payloads, double eps, double* assert_probs,
+                         int64_t* n_measures, double* device_ms, nsb_status* st);
+
 /* Rejection mode (replaces engine.run(..., "rejection"), engine.py:431-474).
  * Plan: built with NSB_PLAN_EXACT.  uniforms: the caller's Philox stream
  * (rng.random() draws, in order; n_uniforms available), consumed in the

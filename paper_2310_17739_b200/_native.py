@@ -127,6 +127,7 @@ _SIGNATURES = {
                                                ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
     "nsb_plan_last_timing": (ctypes.c_int, [_P, ctypes.POINTER(_D), ctypes.POINTER(_I64)]),
     "nsb_plan_p0_scale": (ctypes.c_int, [_P, ctypes.c_int32, _P]),
+    "nsb_run_mma_streamed": (ctypes.c_int, [_P, _P, _I64, _P, _P, _D, _P, _P, _P, _ST]),
     "nsb_plan_run_rejection": (ctypes.c_int, [_P, _P, _P, _I64, _I64, ctypes.c_int32, _P, _P,
                                               _P, _P, _P, _ST]),
     "nsb_timer_start": (ctypes.c_int, [_P, _ST]),

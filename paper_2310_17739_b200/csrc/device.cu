@@ -912,7 +912,11 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
     }
     __syncthreads();
   };
+  if (p.eps >= 0.0 && p.fail[0]) return;  // an earlier launch of this MMA run failed its assertion
   if (p.pass_begin < p.pass_end) stage(p.pass_begin);
+  // a launch that starts with a collapse (streamed MMA runs: one launch per
+  // part between assertions) takes p0 from the record the previous launch wrote
+  if (p.pass_begin < p.pass_end && sp.collapse_q >= 0) carry_p0 = p.record[sp.collapse_slot];
 
   for (int pi = p.pass_begin; pi < p.pass_end; ++pi) {
     const int k = sp.k;
@@ -2200,6 +2204,220 @@ int nsb_plan_run_rejection(nsb_ctx* c, nsb_plan* P, const double* uniforms, int6
     }
     *consumed = cur;
     NSB_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+// MMA run with planning streamed behind execution (engine.run's MMA path, the
+// reference-facing call): the op list is cut at its MEASURE / RESET markers
+// (the relabeling frame is flushed there, so the parts are independent
+// planning problems); a host thread plans the parts in order, each with all
+// cores on its passes, and the caller's thread uploads part s and launches
+// its passes (one cooperative k_blocked launch per part, pass descriptors with
+// the assertion epilogue / collapse prologue of the markers around it) while
+// part s+1 is being planned.  A launch that starts with a collapse takes p0
+// from the record; a failed assertion makes the later launches return at once.
+// Reported p0 carry the parts' near-identity norm factors as in
+// nsb_plan_run_mma.  Circuits with k >= 3 dense gates or fewer than 6 qubits
+// are not streamed (NSB_EINVAL: use nsb_plan_create + nsb_plan_run_mma).
+int nsb_run_mma_streamed(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const double* params,
+                         const double* payloads, double eps, double* assert_probs,
+                         int64_t* n_measures, double* device_ms, nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    if (n_ops < 0 || (n_ops > 0 && !ops) || !n_measures) throw std::invalid_argument("bad op list");
+    if (c->n < 6) throw std::invalid_argument("streamed MMA runs need >= 6 qubits");
+    NSB_CUDA(cudaSetDevice(c->device));
+    std::vector<int64_t> marks;
+    int64_t n_meas = 0;
+    for (int64_t i = 0; i < n_ops; ++i) {
+      if (ops[i].kind == NSB_OP_MEASURE || ops[i].kind == NSB_OP_RESET) marks.push_back(i);
+      if (ops[i].kind == NSB_OP_MEASURE) ++n_meas;
+      if (ops[i].kind == NSB_OP_GATE && ops[i].nq >= 3)
+        throw std::invalid_argument("streamed MMA runs take 1q / 2q gates only");
+    }
+    *n_measures = n_meas;
+    const size_t n_parts = marks.size() + 1;
+    const double budget = default_identity_budget_value();
+    // producer: parts planned in order on a host thread
+    std::vector<std::unique_ptr<HostPlan>> parts(n_parts);
+    std::vector<std::exception_ptr> errs(n_parts);
+    std::mutex mu;
+    std::condition_variable cv;
+    size_t ready = 0;
+    std::atomic<bool> stop{false};
+    std::thread producer([&] {
+      for (size_t s = 0; s < n_parts && !stop.load(); ++s) {
+        const int64_t b = s == 0 ? 0 : marks[s - 1] + 1, e = s < marks.size() ? marks[s] : n_ops;
+        auto H = std::make_unique<HostPlan>();
+        try {
+          H->identity_budget = n_ops ? budget * static_cast<double>(e - b) / n_ops : 0.0;
+          H->build_segment(ops + b, e - b, params, payloads, c->n, c->blocked_grid);
+        } catch (...) {
+          errs[s] = std::current_exception();
+        }
+        {
+          std::lock_guard<std::mutex> lk(mu);
+          parts[s] = std::move(H);
+          ready = s + 1;
+        }
+        cv.notify_one();
+      }
+    });
+    struct PartDev {
+      DevBuf<PassDesc> passes;
+      DevBuf<GroupDesc> groups;
+      DevBuf<GateOp> ops;
+      DevBuf<double2> mats;
+    };
+    std::vector<PartDev> dev(n_parts + 1);
+    DevBuf<double> record, partials;
+    DevBuf<int> fail;
+    DevBuf<unsigned> bar;
+    cudaMemPool_t pool = c->plan_pool;
+    record.alloc(std::max<int64_t>(n_meas, 1), c->stream, pool);
+    partials.alloc(2 * size_t(std::max(c->blocked_grid, 1)), c->stream, pool);
+    fail.alloc(2, c->stream, pool);
+    bar.alloc(1, c->stream, pool);
+    NSB_CUDA(cudaMemsetAsync(fail.ptr, 0, 2 * sizeof(int), c->stream));
+    NSB_CUDA(cudaEventRecord(c->ev0, c->stream));
+    static const int debug = [] {
+      const char* e = std::getenv("NSB_DEBUG_BLOCKED");
+      return e ? std::atoi(e) : 0;
+    }();
+    int grid = 0;
+    auto launch = [&](PartDev& d, int count) {
+      dev::BlockedParams bp;
+      bp.amps = c->amps.ptr;
+      bp.n = c->n;
+      bp.passes = d.passes.ptr;
+      bp.pass_begin = 0;
+      bp.pass_end = count;
+      bp.groups = d.groups.ptr;
+      bp.ops = d.ops.ptr;
+      bp.mats = d.mats.ptr;
+      bp.partials = partials.ptr;
+      bp.record = record.ptr;
+      bp.fail = fail.ptr;
+      bp.bar = bar.ptr;
+      bp.eps = eps;
+      bp.debug = debug;
+      NSB_CUDA(cudaMemsetAsync(bar.ptr, 0, sizeof(unsigned), c->stream));
+      void* args[] = {&bp};
+      NSB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::k_blocked), dim3(grid),
+                                           dim3(kPassThreads), args, dev::kBlockedSmemBytes,
+                                           c->stream));
+    };
+    std::vector<double> scale(std::max<int64_t>(n_meas, 1), 1.0);
+    double running = 1.0;
+    int pending_q = -1, pending_slot = -1, step = 0;
+    int k_tile = 0;
+    auto fresh = [&]() {
+      PassDesc P{};
+      P.k = k_tile;
+      P.measure_q = P.collapse_q = -1;
+      P.measure_slot = P.collapse_slot = -1;
+      int t = 0, o = 0;
+      for (int q = 0; q < c->n; ++q) {
+        if (q < k_tile)
+          P.tq[t++] = static_cast<int8_t>(q);
+        else
+          P.oq[o++] = static_cast<int8_t>(q);
+      }
+      return P;
+    };
+    try {
+      for (size_t s = 0; s < n_parts; ++s) {
+        {
+          std::unique_lock<std::mutex> lk(mu);
+          cv.wait(lk, [&] { return ready > s; });
+        }
+        if (errs[s]) std::rethrow_exception(errs[s]);
+        HostPlan& H = *parts[s];
+        if (!H.blocked) throw std::invalid_argument("streamed MMA runs need a blocked plan");
+        for (const Item& it : H.items)
+          if (it.kind == Item::kDense) throw std::invalid_argument("dense k-qubit item in a stream");
+        if (!grid) {
+          k_tile = H.tile_qubits;
+          grid = static_cast<int>(std::min<uint64_t>(uint64_t(1) << (c->n - k_tile),
+                                                     uint64_t(c->blocked_grid)));
+          if (std::getenv("NSB_FULL_GRID")) grid = c->blocked_grid;
+        }
+        std::vector<PassDesc> mp = H.passes;  // one kGates item at most: all passes in order
+        if (!mp.empty() && pending_q >= 0) {
+          mp.front().collapse_q = pending_q;
+          mp.front().collapse_slot = pending_slot;
+          pending_q = -1;
+        }
+        running *= H.tail_scale2;
+        if (s < marks.size() && ops[marks[s]].kind == NSB_OP_MEASURE) {
+          if (mp.empty() || pending_q >= 0) {
+            PassDesc P = fresh();
+            if (pending_q >= 0) {
+              P.collapse_q = pending_q;
+              P.collapse_slot = pending_slot;
+              pending_q = -1;
+            }
+            mp.push_back(P);
+          }
+          mp.back().measure_q = ops[marks[s]].q[0];
+          mp.back().measure_slot = step;
+          pending_q = ops[marks[s]].q[0];
+          pending_slot = step;
+          scale[step] = running;
+          running = 1.0;
+          ++step;
+        }
+        if (s + 1 == n_parts && pending_q >= 0) {  // the last collapse
+          PassDesc P = fresh();
+          P.collapse_q = pending_q;
+          P.collapse_slot = pending_slot;
+          mp.push_back(P);
+        }
+        if (!mp.empty()) {
+          PartDev& d = dev[s];
+          d.passes.upload(mp.data(), mp.size(), c->stream, pool);
+          d.groups.upload(H.groups.data(), H.groups.size(), c->stream, pool);
+          d.ops.upload(H.gate_ops.data(), H.gate_ops.size(), c->stream, pool);
+          d.mats.upload(reinterpret_cast<const double2*>(H.matrices.data()),
+                        H.matrices.size() / 2, c->stream, pool);
+          launch(d, static_cast<int>(mp.size()));
+        }
+        if (s > 0) {  // planned parts already uploaded: release their host programs
+          std::lock_guard<std::mutex> lk(mu);
+          parts[s - 1].reset();
+        }
+      }
+    } catch (...) {
+      stop = true;
+      producer.join();
+      throw;
+    }
+    producer.join();
+    NSB_CUDA(cudaEventRecord(c->ev1, c->stream));
+    int fl[2] = {0, 0};
+    NSB_CUDA(cudaMemcpyAsync(fl, fail.ptr, sizeof fl, cudaMemcpyDeviceToHost, c->stream));
+    std::vector<double> rec(std::max<int64_t>(n_meas, 1));
+    NSB_CUDA(cudaMemcpyAsync(rec.data(), record.ptr, rec.size() * sizeof(double),
+                             cudaMemcpyDeviceToHost, c->stream));
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+    float ms = 0.f;
+    NSB_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    if (device_ms) *device_ms = ms;
+    for (int64_t i = 0; i < n_meas; ++i) rec[i] *= scale[i];
+    const int64_t n_ok = fl[0] ? fl[1] : n_meas;
+    if (assert_probs)
+      for (int64_t i = 0; i < n_ok; ++i) assert_probs[i] = rec[i];
+    for (PartDev& d : dev) {  // stream-ordered frees on the context stream
+      d.passes.release();
+      d.groups.release();
+      d.ops.release();
+      d.mats.release();
+    }
+    if (fl[0]) {
+      char buf[128];
+      std::snprintf(buf, sizeof buf, "assertion failed at step %d: P(|0>) = %.3e", fl[1], rec[fl[1]]);
+      throw AssertFailure{fl[1], rec[fl[1]], buf};
+    }
   });
 }
 

@@ -1213,7 +1213,16 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
   // one group slot stays free for a trailing read-map sweep
   auto pass_groups = pack_groups(masks, k, low, all, 256, sets, &deps, &weights,
                                  kMaxPassGates - 1, kMaxPassMats);
-  for (size_t pi = 0; pi < pass_groups.size(); ++pi) {
+  // Passes are independent planning problems (each starts from an identity
+  // read map): large runs build them on host threads, then concatenate.
+  struct PassOut {
+    PassDesc P{};
+    std::vector<GroupDesc> groups;
+    std::vector<GateOp> gate_ops;
+    std::vector<double> matrices;
+    int64_t n_ops = 0, n_folded = 0, n_permute = 0, n_fused = 0, n_warp = 0, n_axis = 0;
+  };
+  auto build_pass = [&](size_t pi, PassOut& out) {
     uint64_t tset = sets[pi];
     for (int q = 0; q < n && popc(tset) < k; ++q) tset |= uint64_t(1) << q;
     PassDesc P{};
@@ -1227,9 +1236,9 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
       else
         P.oq[o++] = static_cast<int8_t>(q);
     }
-    P.group_begin = static_cast<int32_t>(groups.size());
-    P.op_begin = static_cast<int32_t>(gate_ops.size());
-    P.mat_begin = static_cast<int32_t>(matrices.size() / 2);
+    P.group_begin = static_cast<int32_t>(out.groups.size());
+    P.op_begin = static_cast<int32_t>(out.gate_ops.size());
+    P.mat_begin = static_cast<int32_t>(out.matrices.size() / 2);
     uint32_t rcol[16];  // pending read map R (tile-local columns), product of CXs
     for (int i = 0; i < 16; ++i) rcol[i] = 1u << i;
     bool r_identity = true;
@@ -1282,7 +1291,7 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
       }
       op.kind = static_cast<uint8_t>(op_kind(op.pat, op.cls));
       G.ops.push_back(op);
-      ++n_ops;
+      ++out.n_ops;
     };
     // Gates between two folded permutations are grouped greedily with
     // look-ahead: a gate may join the open group ahead of skipped gates it
@@ -1329,7 +1338,7 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
           std::swap(rcol[a], rcol[b]);
         }
         r_identity = false;
-        ++n_folded_gates;
+        ++out.n_folded;
         continue;
       }
       seg.push_back(gi);
@@ -1339,7 +1348,7 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
     if (!r_identity) {  // trailing permutation: one sweep through R without gates
       start();
       close();
-      class_count[kPermute]++;
+      ++out.n_permute;
     }
     // warp positions: the pair of tile positions that lets the most
     // consecutive sweeps run warp-locally (kThreadBits + 1 octet-index bits
@@ -1418,8 +1427,8 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
             const size_t after = used - run_size + pk.size() / 2;
             if (after <= size_t(kMaxPassMats)) {
               used = after;
-              n_fused_group_ops += static_cast<int64_t>(run_ops.size()) - 1;
-              n_ops -= static_cast<int64_t>(run_ops.size()) - 1;
+              out.n_fused += static_cast<int64_t>(run_ops.size()) - 1;
+              out.n_ops -= static_cast<int64_t>(run_ops.size()) - 1;
               f.mat = static_cast<int16_t>(mats_out.size() / 2);
               ops_out.push_back(f);
               mats_out.insert(mats_out.end(), pk.begin(), pk.end());
@@ -1444,28 +1453,69 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
     for (size_t g = 0; g < closed.size(); ++g) {
       OpenGroup& H = closed[g];
       GroupDesc d{};
-      d.op_begin = static_cast<uint8_t>(gate_ops.size() - P.op_begin);
+      d.op_begin = static_cast<uint8_t>(out.gate_ops.size() - P.op_begin);
       d.n_ops_sync = static_cast<uint8_t>(H.ops.size());
-      const int32_t mat0 = static_cast<int32_t>(matrices.size() / 2) - P.mat_begin;
+      const int32_t mat0 = static_cast<int32_t>(out.matrices.size() / 2) - P.mat_begin;
       for (GateOp op : H.ops) {
         op.mat = static_cast<int16_t>(op.mat + mat0);
-        gate_ops.push_back(op);
+        out.gate_ops.push_back(op);
       }
-      matrices.insert(matrices.end(), H.mats.begin(), H.mats.end());
+      out.matrices.insert(out.matrices.end(), H.mats.begin(), H.mats.end());
       const uint32_t wm = wsel[g];
       const bool next = g + 1 < closed.size() && wm && wsel[g + 1] == wm;
       finish_group(H, k, d, wm);
       if (!next) d.n_ops_sync |= 128;
-      if (next) ++n_warp_syncs;
-      for (const GateOp& o : H.ops) n_axis_swaps += o.cls == kPermute && o.pat == kPatQ0;
-      groups.push_back(d);
+      if (next) ++out.n_warp;
+      for (const GateOp& o : H.ops) out.n_axis += o.cls == kPermute && o.pat == kPatQ0;
+      out.groups.push_back(d);
     }
-    P.group_end = static_cast<int32_t>(groups.size());
-    P.op_end = static_cast<int32_t>(gate_ops.size());
+    P.group_end = static_cast<int32_t>(out.groups.size());
+    P.op_end = static_cast<int32_t>(out.gate_ops.size());
     if (P.op_end - P.op_begin > kMaxPassOps || P.group_end - P.group_begin > kMaxPassGates)
       throw std::logic_error("pass exceeds the kernel's op / group capacity");
-    P.mat_count = static_cast<int32_t>(matrices.size() / 2) - P.mat_begin;
+    P.mat_count = static_cast<int32_t>(out.matrices.size() / 2) - P.mat_begin;
+    out.P = P;
+    };
+  std::vector<PassOut> outs(pass_groups.size());
+  const size_t np = pass_groups.size();
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const size_t n_threads = np >= 64 && !std::getenv("NSB_PLAN_SERIAL") ? std::min<size_t>(hw, np / 32) : 1;
+  if (n_threads <= 1) {
+    for (size_t pi = 0; pi < np; ++pi) build_pass(pi, outs[pi]);
+  } else {
+    std::atomic<size_t> next{0};
+    std::vector<std::exception_ptr> errs(n_threads);
+    auto work = [&](size_t w) {
+      try {
+        for (size_t pi; (pi = next.fetch_add(1)) < np;) build_pass(pi, outs[pi]);
+      } catch (...) {
+        errs[w] = std::current_exception();
+      }
+    };
+    std::vector<std::thread> pool;
+    for (size_t w = 1; w < n_threads; ++w) pool.emplace_back(work, w);
+    work(0);
+    for (std::thread& t : pool) t.join();
+    for (auto& e : errs)
+      if (e) std::rethrow_exception(e);
+  }
+  for (PassOut& out : outs) {  // concatenate in pass order
+    PassDesc P = out.P;
+    P.group_begin += static_cast<int32_t>(groups.size());
+    P.group_end += static_cast<int32_t>(groups.size());
+    P.op_begin += static_cast<int32_t>(gate_ops.size());
+    P.op_end += static_cast<int32_t>(gate_ops.size());
+    P.mat_begin += static_cast<int32_t>(matrices.size() / 2);
+    groups.insert(groups.end(), out.groups.begin(), out.groups.end());
+    gate_ops.insert(gate_ops.end(), out.gate_ops.begin(), out.gate_ops.end());
+    matrices.insert(matrices.end(), out.matrices.begin(), out.matrices.end());
     passes.push_back(P);
+    n_ops += out.n_ops;
+    n_folded_gates += out.n_folded;
+    class_count[kPermute] += out.n_permute;
+    n_fused_group_ops += out.n_fused;
+    n_warp_syncs += out.n_warp;
+    n_axis_swaps += out.n_axis;
   }
 }
 
@@ -1561,6 +1611,7 @@ void fill_info(const nsb::HostPlan& H, nsb_plan_info* info) {
 
 namespace nsb {
 void plan_info(const HostPlan& H, nsb_plan_info* info) { fill_info(H, info); }
+double default_identity_budget_value() { return default_identity_budget(); }
 }  // namespace nsb
 
 extern "C" int nsb_plan_analyze(const nsb_op* ops, int64_t n_ops, const double* params,

@@ -112,6 +112,12 @@ struct HostPlan {
   // workers: persistent CTAs of the pass kernel (tile-size choice)
   void build(const nsb_op* ops, int64_t n_ops, const double* params, const double* payloads,
              int n, int workers);
+  // one gate run between two markers (no MEASURE / RESET inside): the unit of
+  // the parallel build and of streamed MMA runs (nsb_run_mma_streamed)
+  void build_segment(const nsb_op* ops, int64_t n_ops, const double* params,
+                     const double* payloads, int n, int workers) {
+    build_serial(ops, n_ops, params, payloads, n, workers);
+  }
 
  private:
   void build_serial(const nsb_op* ops, int64_t n_ops, const double* params,
@@ -121,5 +127,6 @@ struct HostPlan {
 };
 
 void plan_info(const HostPlan& H, nsb_plan_info* info);
+double default_identity_budget_value();  // NSB_IDENTITY_BUDGET or 3e-11
 
 }  // namespace nsb

@@ -197,3 +197,65 @@ def test_null_status_still_reports_assertion_failure():
     code = N.lib().nsb_plan_run_mma(state._dev.handle, prog.handle, ctypes.c_double(1e-12),
                                     N.ptr(probs), None)
     assert code == 2  # NSB_EASSERT
+
+
+def test_streamed_mma_run_matches_the_single_launch_program():
+    """nsb_run_mma_streamed (planning of part s+1 behind the device run of part
+    s, one launch per part, p0 carried through the record) reproduces the
+    single-launch MMA program: every p0 and the final state."""
+    from paper_2310_17739_b200.engine import run_mma_streamed
+    wl = W.filter_workload(20, trotter=1, n_steps=8, n_scatter=8, trial="10" * 10)
+    fops, pool, _ = W.fuse_packed(wl.ops, wl.params, wl.payloads)
+    exe = wl.executable(fops)
+    state = StateVector(wl.n_qubits)
+    prog = DeviceProgram(state, exe, wl.params, pool)
+    p_one = prog.run_mma()
+    a_one = state.amps.copy()
+    state.restart()
+    p_str = run_mma_streamed(state, exe, wl.params, pool)
+    assert len(p_str) == 8
+    np.testing.assert_allclose(p_str, p_one, rtol=0, atol=1e-15)
+    assert np.linalg.norm(state.amps - a_one) <= 1e-13
+    assert state.last_device_ms > 0.0
+
+
+def test_streamed_mma_assertion_failure():
+    """A failed assertion in a streamed run stops the later launches and raises
+    FilterAssertionError(step, p0) like the single-launch program."""
+    from paper_2310_17739_b200.engine import run_mma_streamed
+    from paper_2310_17739_b200.errors import FilterAssertionError
+    rng = np.random.default_rng(3)
+    n = 8
+    ops = []
+    params = []
+
+    def gate(tag, qs, ps=()):
+        rec = np.zeros(1, N.OP_DTYPE)[0]
+        rec["kind"], rec["tag"], rec["nq"], rec["cbit"] = N.OP_GATE, tag.code, len(qs), -1
+        rec["q"] = tuple(qs) + (-1,) * (5 - len(qs))
+        rec["src"], rec["payload"] = -1, -1
+        rec["param"] = len(params) if ps else -1
+        params.extend(ps)
+        ops.append(rec)
+
+    def marker(kind, q):
+        rec = np.zeros(1, N.OP_DTYPE)[0]
+        rec["kind"], rec["nq"], rec["cbit"] = kind, 1, -1
+        rec["q"] = (q, -1, -1, -1, -1)
+        rec["src"], rec["param"], rec["payload"] = -1, -1, -1
+        ops.append(rec)
+
+    for step in range(3):
+        for _ in range(20):
+            a, b = (int(x) for x in rng.choice(n - 1, 2, replace=False))
+            gate(Gate.RZZ, (a, b), (float(rng.uniform(-1, 1)),))
+            gate(Gate.U3, (a,), tuple(float(x) for x in rng.uniform(-1, 1, 3)))
+        if step == 1:
+            gate(Gate.X, (n - 1,))  # the ancilla is |1>: P(|0>) = 0 at step 1
+        marker(N.OP_MEASURE, n - 1)
+        marker(N.OP_RESET, n - 1)
+    ops = np.array(ops, N.OP_DTYPE)
+    state = StateVector(n)
+    with pytest.raises(FilterAssertionError) as e:
+        run_mma_streamed(state, ops, np.asarray(params or [0.0]), np.zeros(1, np.complex128))
+    assert e.value.step == 1
