@@ -679,7 +679,9 @@ __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
   // memory, which is cheaper than predicating every load and store -- but a
   // warp none of whose octets is valid (small states: 8 qubits fill 32
   // octets) skips the sweep (valid octets only ever address valid tiles).
+#ifndef NSB_NO_SKIP
   if ((t & ~31) >= (nvalid << cb)) return;
+#endif
   const GateOp first = ops[0];  // (unused by read-map-only sweeps)
   const uint32_t v = ttab[t & 15] ^ ttab[16 + (t >> 4)];
   const int m0 = G.am[0], m1 = G.am[1], m2 = G.am[2];
