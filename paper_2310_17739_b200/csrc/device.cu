@@ -676,12 +676,9 @@ __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
   // Every thread sweeps both of its octets.  Octets past the batch's valid
   // tiles (a short last batch, or k < 8) address the unused part of the
   // 2^11-amplitude buffer: they move garbage that is never stored to global
-  // memory, which is cheaper than predicating every load and store -- but a
-  // warp none of whose octets is valid (small states: 8 qubits fill 32
-  // octets) skips the sweep (valid octets only ever address valid tiles).
-#ifndef NSB_NO_SKIP
-  if ((t & ~31) >= (nvalid << cb)) return;
-#endif
+  // memory, which is cheaper than predicating every load and store (a warp
+  // none of whose octets is valid skips the sweep altogether: see k_blocked).
+
   const GateOp first = ops[0];  // (unused by read-map-only sweeps)
   const uint32_t v = ttab[t & 15] ^ ttab[16 + (t >> 4)];
   const int m0 = G.am[0], m1 = G.am[1], m2 = G.am[2];
@@ -1020,12 +1017,20 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
             }
         __syncthreads();
       }
+      // small states (8 qubits fill 32 octets): warps without a valid octet
+      // skip the sweeps (valid octets only ever address valid tiles)
+#ifndef NSB_NO_SKIP
+      const bool warp_idle = (tid & ~31) >= (nvalid << (k - 3));
+#else
+      const bool warp_idle = false;
+#endif
 #pragma unroll 1
       for (int g = 0; g < ((p.debug & 1) ? 0 : n_groups); ++g) {
         const GroupDesc& d = s_groups[g];
         const bool cta_sync = d.sync();  // read before the sweep: no load latency after it
         double2* out = smem + spare * kTileAmpsMax;
-        apply_group(tile, out, k, nvalid, d, s_ops + d.op_begin, s_mats, s_gm[g], s_ttab[g]);
+        if (!warp_idle)
+          apply_group(tile, out, k, nvalid, d, s_ops + d.op_begin, s_mats, s_gm[g], s_ttab[g]);
         const int tmp = cur;
         cur = spare;
         spare = tmp;

@@ -1082,120 +1082,6 @@ void HostPlan::build_serial(const nsb_op* ops, int64_t n_ops, const double* para
     packed_all.clear();
   };
 
-  // one 1q / 2q gate on logical qubits (a, b) into the frame or the run
-  auto emit = [&](const double* m, int nq, int a, int b) {
-      PhysGate g{};
-      g.nq = nq;
-      g.cls = pack_matrix(m, nq, packed, g.cols);
-      class_count[g.cls]++;
-      // logical CX(c -> t): M <- M C, i.e. column c += column t and, for
-      // M^-1 <- C M^-1, row t += row c
-      if (g.cls == kCX01) {
-        col[a] ^= col[b];
-        row[b] ^= row[a];
-        ++n_frame_gates;
-        return;
-      }
-      if (g.cls == kCX10) {
-        col[b] ^= col[a];
-        row[a] ^= row[b];
-        ++n_frame_gates;
-        return;
-      }
-      if (g.cls == kSwap) {
-        std::swap(col[a], col[b]);
-        std::swap(row[a], row[b]);
-        ++n_frame_gates;
-        return;
-      }
-      if (popc(col[a] | (nq == 2 ? col[b] : 0)) > kMaxSupport) {
-        // keep physical supports small so passes stay dense: reduce just this
-        // gate's columns to unit vectors with physical CXs (row operations)
-        reduce_column(a);
-        if (nq == 2) reduce_column(b);
-        ++n_frame_flushes;
-      }
-      g.ma = col[a];
-      g.mb = nq == 2 ? col[b] : 0;
-      g.ra = row[a];
-      g.rb = nq == 2 ? row[b] : 0;
-      g.mat = static_cast<int32_t>(packed_all.size() / 2);
-      g.n_mat = static_cast<int32_t>(packed.size() / 2);
-      packed_all.insert(packed_all.end(), packed.begin(), packed.end());
-      static const int kNnz[kNumClasses] = {4, 2, 16, 8, 4, 4, 0, 0, 8, 8, 8, 0, 0, 4, 4, 4};
-      flops += 8ll * kNnz[g.cls] * (int64_t(1) << (n - g.nq));
-      run.push_back(g);
-  };
-  // CX-factoring (NSB_FACTOR_CX=1, experiment): a fused 2q payload that is
-  // CX * (A (x) B) or (A (x) B) * CX within rounding goes to the frame as the
-  // exact CX plus the 1q gates A, B (exact identities dropped); the
-  // reconstruction error is charged to the identity budget.
-  static const bool factor_env = std::getenv("NSB_FACTOR_CX") != nullptr;
-  const bool factor_cx = factor_env && blocked;
-  static const double kOne[8] = {1, 0, 0, 0, 0, 0, 1, 0};
-  auto try_factor = [&](const double* u, int qa, int qb) -> bool {
-    // matrix index = bit(slot 0) + 2 bit(slot 1); CX01: slot 0 controls slot 1
-    static const int kPerm[2][4] = {{0, 3, 2, 1}, {0, 1, 3, 2}};  // CX01, CX10 (involutions)
-    for (int which = 0; which < 2; ++which)
-      for (int side = 0; side < 2; ++side) {
-        const int* P = kPerm[which];
-        double M[32];  // side 0: P^-1 U (U = P (A x B)); side 1: U P^-1 (U = (A x B) P)
-        for (int r = 0; r < 4; ++r)
-          for (int c = 0; c < 4; ++c) {
-            const int rr = side == 0 ? P[r] : r, cc = side == 1 ? P[c] : c;
-            M[2 * (4 * r + c)] = u[2 * (4 * rr + cc)];
-            M[2 * (4 * r + c) + 1] = u[2 * (4 * rr + cc) + 1];
-          }
-        // rank-1 split M[(o1,o0),(i1,i0)] = B[o1,i1] A[o0,i0] at the largest entry
-        int best = 0;
-        double bm = -1.0;
-        for (int e = 0; e < 16; ++e) {
-          const double v = std::hypot(M[2 * e], M[2 * e + 1]);
-          if (v > bm) bm = v, best = e;
-        }
-        const int r0 = best >> 2, c0 = best & 3;
-        const int o1s = r0 >> 1, o0s = r0 & 1, i1s = c0 >> 1, i0s = c0 & 1;
-        const cplx mx(M[2 * best], M[2 * best + 1]);
-        double A[8], B[8];
-        for (int o0 = 0; o0 < 2; ++o0)
-          for (int i0 = 0; i0 < 2; ++i0) {
-            const int e = 4 * (2 * o1s + o0) + (2 * i1s + i0);
-            A[2 * (2 * o0 + i0)] = M[2 * e];
-            A[2 * (2 * o0 + i0) + 1] = M[2 * e + 1];
-          }
-        for (int o1 = 0; o1 < 2; ++o1)
-          for (int i1 = 0; i1 < 2; ++i1) {
-            const int e = 4 * (2 * o1 + o0s) + (2 * i1 + i0s);
-            const cplx v = cplx(M[2 * e], M[2 * e + 1]) / mx;
-            B[2 * (2 * o1 + i1)] = v.real();
-            B[2 * (2 * o1 + i1) + 1] = v.imag();
-          }
-        double err = 0.0;
-        for (int r = 0; r < 4; ++r)
-          for (int c = 0; c < 4; ++c) {
-            const cplx b(B[2 * (2 * (r >> 1) + (c >> 1))], B[2 * (2 * (r >> 1) + (c >> 1)) + 1]);
-            const cplx a(A[2 * (2 * (r & 1) + (c & 1))], A[2 * (2 * (r & 1) + (c & 1)) + 1]);
-            const cplx d = cm(b, a) - cplx(M[2 * (4 * r + c)], M[2 * (4 * r + c) + 1]);
-            err += std::norm(d);
-          }
-        err = std::sqrt(err);
-        if (err > kIdentityTol || identity_error + err + tail_error > identity_budget) continue;
-        identity_error += err;
-        ++n_factored;
-        const int ctrl = which == 0 ? qa : qb, targ = which == 0 ? qb : qa;
-        auto cx = [&]() {
-          col[ctrl] ^= col[targ];
-          row[targ] ^= row[ctrl];
-          ++n_frame_gates;
-        };
-        if (side == 1) cx();
-        if (std::memcmp(A, kOne, sizeof A)) emit(A, 1, qa, -1);
-        if (std::memcmp(B, kOne, sizeof B)) emit(B, 1, qb, -1);
-        if (side == 0) cx();
-        return true;
-      }
-    return false;
-  };
   for (int64_t i = 0; i < n_ops; ++i) {
     const nsb_op& o = ops[i];
     if (o.kind == NSB_OP_BARRIER) continue;
@@ -1254,8 +1140,48 @@ void HostPlan::build_serial(const nsb_op* ops, int64_t n_ops, const double* para
       items.push_back(it);
       continue;
     }
-    if (factor_cx && o.nq == 2 && try_factor(mat.v, o.q[0], o.q[1])) continue;
-    emit(mat.v, o.nq, o.q[0], o.nq == 2 ? o.q[1] : -1);
+    PhysGate g{};
+    g.nq = o.nq;
+    g.cls = pack_matrix(mat.v, o.nq, packed, g.cols);
+    class_count[g.cls]++;
+    const int a = o.q[0], b = o.nq == 2 ? o.q[1] : -1;
+    // logical CX(c -> t): M <- M C, i.e. column c += column t and, for
+    // M^-1 <- C M^-1, row t += row c
+    if (g.cls == kCX01) {
+      col[a] ^= col[b];
+      row[b] ^= row[a];
+      ++n_frame_gates;
+      continue;
+    }
+    if (g.cls == kCX10) {
+      col[b] ^= col[a];
+      row[a] ^= row[b];
+      ++n_frame_gates;
+      continue;
+    }
+    if (g.cls == kSwap) {
+      std::swap(col[a], col[b]);
+      std::swap(row[a], row[b]);
+      ++n_frame_gates;
+      continue;
+    }
+    if (popc(col[a] | (o.nq == 2 ? col[b] : 0)) > kMaxSupport) {
+      // keep physical supports small so passes stay dense: reduce just this
+      // gate's columns to unit vectors with physical CXs (row operations)
+      reduce_column(a);
+      if (o.nq == 2) reduce_column(b);
+      ++n_frame_flushes;
+    }
+    g.ma = col[a];
+    g.mb = o.nq == 2 ? col[b] : 0;
+    g.ra = row[a];
+    g.rb = o.nq == 2 ? row[b] : 0;
+    g.mat = static_cast<int32_t>(packed_all.size() / 2);
+    g.n_mat = static_cast<int32_t>(packed.size() / 2);
+    packed_all.insert(packed_all.end(), packed.begin(), packed.end());
+    static const int kNnz[kNumClasses] = {4, 2, 16, 8, 4, 4, 0, 0, 8, 8, 8, 0, 0, 4, 4, 4};
+    flops += 8ll * kNnz[g.cls] * (int64_t(1) << (n - g.nq));
+    run.push_back(g);
   }
   flush_run();
   n_measures = step;

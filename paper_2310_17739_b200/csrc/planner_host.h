@@ -76,7 +76,6 @@ struct HostPlan {
   int64_t n_warp_syncs = 0;     // sweeps followed by __syncwarp instead of a CTA barrier
   int64_t n_fused_group_ops = 0;  // gate ops removed by group fusion (fuse_group)
   int64_t n_axis_swaps = 0;       // register-axis exchanges of four-axis groups
-  int64_t n_factored = 0;         // 2q payloads split into frame CX + 1q gates
   bool fuse_groups = true;      // NSB_NO_GROUP_FUSION=1 turns group fusion off
   // Gates within rounding of a scalar identity s I (e.g. the fused H.H / S.Sdg
   // products between consecutive JW terms, 1 + 2^-52 on the diagonal) are not
