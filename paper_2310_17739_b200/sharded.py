@@ -42,7 +42,7 @@ EPS_MMA = 1e-12
 
 @dataclass
 class Step:
-    kind: str                        # "gates" | "swap" | "measure"
+    kind: str                        # "gates" | "swap" | "measure" | "reset"
     ops: np.ndarray | None = None    # "gates": op records on LOCAL positions
     global_bit: int = -1             # "swap": rank bit that trades places ...
     local_q: int = -1                # ... with this local position
@@ -69,10 +69,13 @@ def _translate(ops: np.ndarray, idx: list[int], pos: list[int]) -> np.ndarray:
     return out
 
 
-def schedule(ops: np.ndarray, n: int, g: int, window: int = 4096) -> list[Step]:
+def schedule(ops: np.ndarray, n: int, g: int, window: int = 4096,
+             keep_resets: bool = False) -> list[Step]:
     """Split an MMA op stream (gates, measures, resets, barriers; no trailing
     sampling block) into local gate groups, qubit swaps and collective
-    measurements for 2^g ranks.  Pure host logic (tested on CPU)."""
+    measurements for 2^g ranks.  Resets are MMA no-ops and dropped, unless
+    `keep_resets` (the rejection-mode path: "reset" steps, ordered like
+    measurements).  Pure host logic (tested on CPU)."""
     if g < 0 or g >= n:
         raise ValueError("need 0 <= g < n")
     nl = n - g
@@ -86,7 +89,7 @@ def schedule(ops: np.ndarray, n: int, g: int, window: int = 4096) -> list[Step]:
             step_of[i] = s
             s += 1
             pending.append(i)
-        elif k == N.OP_GATE:
+        elif k == N.OP_GATE or (k == N.OP_RESET and keep_resets):
             pending.append(i)
         elif k not in (N.OP_RESET, N.OP_BARRIER):
             raise ValueError(f"op {i}: unknown kind {k}")
@@ -117,12 +120,15 @@ def schedule(ops: np.ndarray, n: int, g: int, window: int = 4096) -> list[Step]:
                 waiting.extend(pending[j:])
                 break
             q = qs[i]
-            is_m = int(kinds[i]) == N.OP_MEASURE
+            is_m = int(kinds[i]) in (N.OP_MEASURE, N.OP_RESET)  # markers keep their order
             if (all(pos[x] < nl for x in q) and blocked.isdisjoint(q)
                     and not (is_m and measure_waiting)):
                 if is_m:
                     flush()
-                    steps.append(Step("measure", local_q=pos[q[0]], step=step_of[i]))
+                    if int(kinds[i]) == N.OP_MEASURE:
+                        steps.append(Step("measure", local_q=pos[q[0]], step=step_of[i]))
+                    else:
+                        steps.append(Step("reset", local_q=pos[q[0]]))
                 else:
                     group.append(i)
             else:
@@ -243,6 +249,44 @@ def sample_shard(rank: int, nl: int, draws: np.ndarray, starts: np.ndarray, last
     return out
 
 
+def replayable(ops: np.ndarray) -> bool:
+    """Filter-shaped: every MEASURE is followed by a RESET of the same qubit and
+    every RESET follows such a MEASURE (all accepted rejection-mode shots then
+    take the same path, engine.py:431-474)."""
+    marks = [(int(r["kind"]), int(r["q"][0])) for r in ops
+             if int(r["kind"]) in (N.OP_MEASURE, N.OP_RESET)]
+    if not marks or len(marks) % 2:
+        return False
+    return all(marks[i][0] == N.OP_MEASURE and marks[i + 1] == (N.OP_RESET, marks[i][1])
+               for i in range(0, len(marks), 2))
+
+
+def replay_rejection(path, n_steps: int, shots: int, rng):
+    """Rejection-mode tallies from the accepted path (engine.py:436-463):
+    `path` = [(is_measure, step, p)] of one pass along the all-zero outcomes; the
+    Philox stream is consumed in the reference's order -- one draw per MEASURE and
+    RESET of a shot until it is rejected, one more for an accepted shot's sample.
+    Returns (accepted, step_rejections, unit draws of the accepted shots' samples).
+    A reset draw of 1 (probability ~1e-16 when p < 1) leaves the path: raised."""
+    step_rej = [0] * n_steps
+    draws = []
+    for _ in range(shots):
+        rejected = False
+        for is_m, step, p in path:
+            u = rng.random()
+            if is_m:
+                if not u < p:
+                    step_rej[step] += 1
+                    rejected = True
+                    break
+            elif not u < p:
+                raise NotImplementedError("a reset drew outcome 1: the shot leaves the "
+                                          "accepted path (run it on one GPU)")
+        if not rejected:
+            draws.append(rng.random())
+    return len(draws), step_rej, np.asarray(draws, np.float64)
+
+
 def swap_count(steps: list[Step]) -> int:
     return sum(1 for s in steps if s.kind == "swap")
 
@@ -340,6 +384,15 @@ class ShardedState:
         rng = _as_rng(seed)
         if shots == 0:
             return {}
+        return self.sample_draws(rng.random(shots), chunk_log2)
+
+    def sample_draws(self, units: np.ndarray, chunk_log2: int = 13) -> dict[str, int]:
+        """`sample` for given unit draws (u in [0, 1), scaled by the total mass as
+        engine.py:217 scales rng.random(shots)); collective."""
+        from .engine import bitstring
+        shots = len(units)
+        if shots == 0:
+            return {}
         clog = max(0, min(int(chunk_log2), self.nl))
         sums = np.empty(1 << (self.nl - clog), np.float64)
         self.dev.call("nsb_prob_chunk_sums", clog, N.ptr(sums))
@@ -348,7 +401,7 @@ class ShardedState:
         starts = np.zeros(self.world + 1, np.float64)
         for r in range(self.world):  # rank order on every rank
             starts[r + 1] = starts[r] + totals[r]
-        draws = rng.random(shots) * starts[-1]
+        draws = np.asarray(units, np.float64) * starts[-1]
 
         def fetch(off, count, out):
             self.dev.call("nsb_probabilities_range", off, count, N.ptr(out))
@@ -379,6 +432,31 @@ class ShardedState:
     def compile(self, ops, params, payloads, window: int = 4096) -> "ShardedProgram":
         """Schedule an MMA op stream and upload one device plan per gate group."""
         return ShardedProgram(self, schedule(ops, self.n, self.g, window), params, payloads)
+
+    def run_rejection(self, ops, params, payloads, shots: int, seed, window: int = 4096):
+        """Rejection mode (engine.py:431-474) on the sharded state, for
+        filter-shaped circuits: one collective pass along the accepted path
+        (exact plans: every gate runs), the Philox stream replayed on the host
+        identically on every rank, the accepted shots' samples drawn from the
+        final sharded state.  Returns (accepted, {bitstring: count},
+        step_rejections), the reference's tallies."""
+        from .engine import _as_rng
+        if not replayable(ops):
+            raise NotImplementedError("sharded rejection mode needs a filter-shaped circuit "
+                                      "(each MEASURE followed by a RESET of the same qubit)")
+        rng = _as_rng(seed)
+        n_steps = int(np.count_nonzero(ops["kind"] == N.OP_MEASURE))
+        prog = ShardedProgram(self, schedule(ops, self.n, self.g, window, keep_resets=True),
+                              params, payloads)
+        try:
+            self.reset()
+            path, reachable = prog.run_path()
+        finally:
+            prog.close()
+        del reachable  # a path cut at P(0) = 0 rejects every shot there (u < 0 never holds)
+        accepted, step_rej, units = replay_rejection(path, n_steps, shots, rng)
+        counts = self.sample_draws(units) if accepted else {}
+        return accepted, counts, step_rej
 
     def run_mma(self, ops, params, payloads, eps: float = EPS_MMA, window: int = 4096):
         prog = self.compile(ops, params, payloads, window)
@@ -470,6 +548,36 @@ class ShardedProgram:
             if times is not None:
                 times[s.kind] = times.get(s.kind, 0.0) + S.timer_stop()
         return probs
+
+    def run_path(self) -> tuple[list, bool]:
+        """Rejection mode's accepted path (collective): gates as in run(); at a
+        MEASURE the summed P(0) is recorded and the shards collapse onto 0; at a
+        RESET likewise, with its renormalisation (engine.py:451-455).  Returns
+        ([(is_measure, step, p)], reachable); an outcome-0 probability of 0 ends
+        the path (every shot stops there)."""
+        S = self.state
+        path = []
+        st = N.Status()
+        for s, plan in zip(self.steps, self.plans):
+            if s.kind == "gates":
+                h, n_items = plan
+                for i in range(n_items):
+                    N.check(N.lib().nsb_plan_run_segment(S.dev.handle, h, i, ctypes.byref(st)),
+                            st)
+            elif s.kind == "swap":
+                if S.peer_swaps:
+                    S.dev.call("nsb_shard_swap_p2p", s.global_bit, s.local_q)
+                else:
+                    S.dev.call("nsb_shard_swap", s.global_bit, s.local_q, 0)
+            else:
+                p = ctypes.c_double(0.0)
+                S.dev.call("nsb_branch_probability", s.local_q, 0, ctypes.byref(p))
+                p0 = S._sum(p.value)
+                path.append((s.kind == "measure", s.step, p0))
+                if p0 <= 0.0:
+                    return path, False
+                S.dev.call("nsb_project", s.local_q, 0, p0)
+        return path, True
 
     def plan_totals(self) -> dict:
         """Summed nsb_plan_info counters over the gate groups."""

@@ -102,15 +102,19 @@ def chunk_sums(a: np.ndarray, clog: int) -> np.ndarray:
     return p.reshape(-1, 1 << clog).sum(axis=1)
 
 
-def sample_all(shards, nl, shots, seed, clog):
-    """ShardedState.sample for every rank at once (single-process emulation)."""
+def sample_all(shards, nl, shots, seed, clog, units=None):
+    """ShardedState.sample (or sample_draws with `units`) for every rank at
+    once (single-process emulation)."""
     from paper_2310_17739_b200.sharded import sample_shard
     world = len(shards)
     sums = [chunk_sums(a, clog) for a in shards]
     starts = np.zeros(world + 1)
     for r in range(world):
         starts[r + 1] = starts[r] + float(np.cumsum(sums[r])[-1])
-    draws = O.as_rng(seed).random(shots) * starts[-1]
+    if units is None:
+        units = O.as_rng(seed).random(shots)
+    shots = len(units)
+    draws = np.asarray(units) * starts[-1]
     idx = np.full(shots, -1, np.int64)
     for r, a in enumerate(shards):
         p = a.real ** 2 + a.imag ** 2
@@ -126,3 +130,27 @@ def sample_all(shards, nl, shots, seed, clog):
     np.clip(idx, 0, (1 << n) - 1, out=idx)
     values, counts = np.unique(idx, return_counts=True)
     return {O.bitstring(int(v), n): int(c) for v, c in zip(values, counts)}
+
+
+def run_path_all(steps, params, payloads, n, g):
+    """ShardedProgram.run_path for every rank at once: ([(is_measure, step, p)],
+    shards) along the accepted rejection-mode path."""
+    nl = n - g
+    shards = [np.zeros(1 << nl, np.complex128) for _ in range(1 << g)]
+    shards[0][0] = 1.0
+    path = []
+    for s in steps:
+        if s.kind == "gates":
+            shards = [apply_ops(a, s.ops, params, payloads) for a in shards]
+        elif s.kind == "swap":
+            local_swap_all(shards, s.global_bit, s.local_q, nl)
+        else:
+            p0 = 0.0
+            for a in shards:  # rank order
+                p0 += O.branch_probability(a, s.local_q, 0)
+            path.append((s.kind == "measure", s.step, p0))
+            if p0 <= 0.0:
+                break
+            for a in shards:
+                O.project(a, s.local_q, 0, p0)
+    return path, shards

@@ -39,6 +39,7 @@ def main(out):
         shard = st.download()
         norm = st.norm()
         samples = {clog: st.sample(1024, 2310, chunk_log2=clog) for clog in (4, 13)}
+        rej = st.run_rejection(ops, params, pool, 200, 91) if S.replayable(ops) else None
         st.close()
         shards = [None] * dist.get_world_size()
         dist.all_gather_object(shards, shard)
@@ -50,6 +51,10 @@ def main(out):
             res["wantp_" + tag] = np.asarray(want_p)
             ref = SE.O.sample(res["got_" + tag], n, 1024, 2310)
             res["samples_ok_" + tag] = np.asarray([samples[c] == ref for c in sorted(samples)])
+            if rej is not None:  # sharded rejection mode against the full-state oracle
+                from test_sharded import _oracle_instrs
+                want = SE.O.run_rejection(_oracle_instrs(ops, params, pool), n, 200, 91)
+                res["rejection_ok_" + tag] = np.asarray([tuple(rej) == tuple(want)])
             print(tag, "swaps", S.swap_count(steps), "norm", norm, flush=True)
     if rank == 0:
         np.savez(out, **res)

@@ -268,3 +268,53 @@ def test_nccl_sharded_matches_oracle(tmp_path, ranks):
             _close(d["got_" + tag], d[name])
             assert np.allclose(d["gotp_" + tag], d["wantp_" + tag], rtol=1e-10, atol=1e-14)
             assert d["samples_ok_" + tag].all(), tag  # ShardedState.sample == reference sample
+    rej = [k for k in d.files if k.startswith("rejection_ok_")]
+    assert rej and all(d[k].all() for k in rej), rej  # sharded rejection mode == reference
+
+
+# ---------------------------------------------------------------------------
+# sharded rejection mode: accepted path + host replay (numpy shards)
+
+
+@pytest.mark.parametrize("g", [0, 1, 2])
+def test_sharded_rejection_replay_matches_reference(g):
+    """schedule(keep_resets) + run_path on shards + replay_rejection +
+    sample_draws reproduce the reference's rejection-mode tallies and samples
+    (engine.py:431-474) for the same seed."""
+    ops, params, pool, n = _filter()
+    assert S.replayable(ops)
+    steps = S.schedule(ops, n, g, keep_resets=True)
+    assert sum(1 for s in steps if s.kind == "reset") == 3
+    path, shards = SE.run_path_all(steps, params, pool, n, g)
+    assert [m for m, _, _ in path] == [True, False] * 3
+    n_steps = int(np.count_nonzero(ops["kind"] == N.OP_MEASURE))
+    rng = SE.O.as_rng(77)
+    accepted, step_rej, units = S.replay_rejection(path, n_steps, 300, rng)
+    counts = SE.sample_all(shards, n - g, 0, None, 3, units=units) if accepted else {}
+    want_acc, want_steps, want_counts = SE.O.run_rejection(_oracle_instrs(ops, params, pool), n,
+                                                           300, 77)
+    assert (accepted, step_rej, counts) == (want_acc, want_steps, want_counts)
+
+
+def _oracle_instrs(ops, params, pool):
+    out = []
+    for r in ops:
+        k = int(r["kind"])
+        qs = tuple(int(q) for q in r["q"][: int(r["nq"])])
+        if k == N.OP_MEASURE:
+            out.append(("measure", qs, (), None, int(r["cbit"]) if int(r["cbit"]) >= 0 else 0))
+        elif k == N.OP_RESET:
+            out.append(("reset", qs, (), None, None))
+        elif k == N.OP_GATE:
+            out.append(("c" + str(len(qs)) if len(qs) <= 2 else "dense", qs, (),
+                        SE.op_matrix(r, params, pool), None))
+    return out
+
+
+def test_replayable_and_reset_draw_leaving_the_path():
+    ops, params, pool, n = _filter()
+    assert S.replayable(ops)
+    assert not S.replayable(ops[ops["kind"] != N.OP_RESET])
+    path = [(True, 0, 0.9), (False, -1, 0.0)]  # the reset is certain to draw 1
+    with pytest.raises(NotImplementedError):
+        S.replay_rejection(path, 1, 5, SE.O.as_rng(1))
