@@ -622,9 +622,9 @@ __device__ __forceinline__ void swap_axis_q(double2 (&xs)[NO][8]) {
 // the 16 registers of the two octets (bit 3 = octet index)
 template <int J, int K, int NO>
 __device__ __forceinline__ void reg_cx(double2 (&xs)[NO][8]) {
-  static_assert(NO == 2, "register ops need two octets per thread");
+  static_assert(NO == 2 || (J < 3 && K < 3), "octet-index register ops need two octets");
 #pragma unroll
-  for (int c = 0; c < 16; ++c)
+  for (int c = 0; c < 8 * NO; ++c)
     if ((c >> J & 1) && !(c >> K & 1)) {
       const int e = c | (1 << K);
       const double2 t = xs[c >> 3][c & 7];
@@ -694,11 +694,11 @@ __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
     if (kp & 1) r[q] ^= r0;
     if (kp & 2) r[q] ^= r1;
     if (kp & 4) r[q] ^= r2;
-    if (kp & 8) r[q] ^= G.rtcol[kThreadBits];
+    if (kOctets == 2 && (kp & 8)) r[q] ^= G.rtcol[kOctets == 2 ? kThreadBits : 0];
     if (kp & 16) a[q] ^= m0;
     if (kp & 32) a[q] ^= m1;
     if (kp & 64) a[q] ^= m2;
-    if (kp & 128) a[q] ^= G.tcol[kThreadBits];
+    if (kOctets == 2 && (kp & 128)) a[q] ^= G.tcol[kOctets == 2 ? kThreadBits : 0];
   }
   double2 x[NO][8];
 #pragma unroll
@@ -798,15 +798,17 @@ __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
     break;
       NSB_GQ(0) NSB_GQ(1) NSB_GQ(2)
 #undef NSB_GQ
+#endif
 #define NSB_RCX(J, K)                                                    \
   case reg_cx_kind(J, K):                                                \
     reg_cx<J, K, NO>(x);                                                 \
     if (last) store();                                                   \
     break;
-      NSB_RCX(0, 1) NSB_RCX(0, 2) NSB_RCX(0, 3) NSB_RCX(1, 0) NSB_RCX(1, 2) NSB_RCX(1, 3)
-      NSB_RCX(2, 0) NSB_RCX(2, 1) NSB_RCX(2, 3) NSB_RCX(3, 0) NSB_RCX(3, 1) NSB_RCX(3, 2)
-#undef NSB_RCX
+      NSB_RCX(0, 1) NSB_RCX(0, 2) NSB_RCX(1, 0) NSB_RCX(1, 2) NSB_RCX(2, 0) NSB_RCX(2, 1)
+#if NSB_OCTETS == 2
+      NSB_RCX(0, 3) NSB_RCX(1, 3) NSB_RCX(2, 3) NSB_RCX(3, 0) NSB_RCX(3, 1) NSB_RCX(3, 2)
 #endif
+#undef NSB_RCX
 #undef NSB_GT
 #undef NSB_G1
 #undef NSB_G2ALL

@@ -231,8 +231,10 @@ def _apply_group(B, G, ops, mats, tbases, k, nvalid):
         a ^= np.where((t >> b) & 1, int(G["tcol"][b]), 0)
         r ^= np.where((t >> b) & 1, int(G["rtcol"][b]), 0)
     tile = t >> cb
-    am = [int(v) for v in G["am"]] + [int(G["tcol"][THREAD_BITS])]
-    ram = [int(v) for v in G["ram"]] + [int(G["rtcol"][THREAD_BITS])]
+    q_col = int(G["tcol"][THREAD_BITS]) if THREAD_BITS < 8 else 0  # one octet per thread: none
+    q_rcol = int(G["rtcol"][THREAD_BITS]) if THREAD_BITS < 8 else 0
+    am = [int(v) for v in G["am"]] + [q_col]
+    ram = [int(v) for v in G["ram"]] + [q_rcol]
     kmat = int(G["kmat"])
     kl = [_parity(tbases[tile].astype(np.uint64) & np.uint64(G["r_out"][i])) for i in range(4)]
     for j in range(4):  # loads: load basis rows; stores: final row j = sum of kmat's load rows
@@ -278,8 +280,10 @@ def _apply_group_batches(Bs, G, ops, mats, tbs, k, nvalid):
         a0 ^= np.where((t >> b) & 1, int(G["tcol"][b]), 0)
         r0 ^= np.where((t >> b) & 1, int(G["rtcol"][b]), 0)
     tile = t >> cb
-    am = [int(v) for v in G["am"]] + [int(G["tcol"][THREAD_BITS])]
-    ram = [int(v) for v in G["ram"]] + [int(G["rtcol"][THREAD_BITS])]
+    q_col = int(G["tcol"][THREAD_BITS]) if THREAD_BITS < 8 else 0  # one octet per thread: none
+    q_rcol = int(G["rtcol"][THREAD_BITS]) if THREAD_BITS < 8 else 0
+    am = [int(v) for v in G["am"]] + [q_col]
+    ram = [int(v) for v in G["ram"]] + [q_rcol]
     kmat = int(G["kmat"])
     a = np.broadcast_to(a0, (Bs.shape[0], n_act)).copy()
     r = np.broadcast_to(r0, (Bs.shape[0], n_act)).copy()
