@@ -54,8 +54,8 @@ def main(out):
             if rej is not None:  # sharded rejection mode against the full-state oracle
                 from test_sharded import _oracle_instrs
                 want = SE.O.run_rejection(_oracle_instrs(ops, params, pool), n, 200, 91)
-                acc, counts, steps = rej
-                res["rejection_ok_" + tag] = np.asarray([(acc, steps, counts) == tuple(want)])
+                acc, rcounts, rsteps = rej
+                res["rejection_ok_" + tag] = np.asarray([(acc, rsteps, rcounts) == tuple(want)])
             print(tag, "swaps", S.swap_count(steps), "norm", norm, flush=True)
     if rank == 0:
         np.savez(out, **res)
