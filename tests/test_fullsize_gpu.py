@@ -259,3 +259,61 @@ def test_streamed_mma_assertion_failure():
     with pytest.raises(FilterAssertionError) as e:
         run_mma_streamed(state, ops, np.asarray(params or [0.0]), np.zeros(1, np.complex128))
     assert e.value.step == 1
+
+
+@pytest.mark.parametrize("shape", ["leading_markers", "gates_only", "back_to_back"])
+def test_streamed_mma_edge_shapes(shape):
+    """Parts without gates (markers first, consecutive assertions) and circuits
+    without markers run the same through the streamed call as through the
+    single-launch program."""
+    from paper_2310_17739_b200.engine import run_mma_streamed
+    rng = np.random.default_rng(11)
+    n = 9
+    recs, params = [], []
+
+    def gate(qs):
+        rec = np.zeros(1, N.OP_DTYPE)[0]
+        rec["kind"], rec["tag"], rec["nq"], rec["cbit"] = N.OP_GATE, Gate.U3.code, 1, -1
+        if len(qs) == 2:
+            rec["tag"], rec["nq"] = Gate.CU3.code, 2
+        rec["q"] = tuple(qs) + (-1,) * (5 - len(qs))
+        rec["src"], rec["payload"], rec["param"] = -1, -1, len(params)
+        params.extend(rng.uniform(-0.4, 0.4, 3))
+        recs.append(rec)
+
+    def marker(kind):
+        rec = np.zeros(1, N.OP_DTYPE)[0]
+        rec["kind"], rec["nq"], rec["cbit"] = kind, 1, -1
+        rec["q"] = (n - 1, -1, -1, -1, -1)
+        rec["src"], rec["param"], rec["payload"] = -1, -1, -1
+        recs.append(rec)
+
+    def block(count):
+        for _ in range(count):
+            a, b = (int(x) for x in rng.choice(n, 2, replace=False))
+            gate((a, b) if rng.random() < 0.6 else (a,))
+
+    if shape == "leading_markers":
+        marker(N.OP_MEASURE)
+        marker(N.OP_RESET)
+        block(60)
+        marker(N.OP_MEASURE)
+        marker(N.OP_RESET)
+    elif shape == "gates_only":
+        block(120)
+    else:
+        block(40)
+        marker(N.OP_MEASURE)
+        marker(N.OP_RESET)
+        marker(N.OP_MEASURE)
+        marker(N.OP_RESET)
+        block(40)
+    ops = np.array(recs, N.OP_DTYPE)
+    params = np.asarray(params)
+    state = StateVector(n)
+    want_p = DeviceProgram(state, ops, params, np.zeros(1, np.complex128)).run_mma()
+    want = state.amps.copy()
+    state.restart()
+    got_p = run_mma_streamed(state, ops, params, np.zeros(1, np.complex128))
+    np.testing.assert_allclose(got_p, want_p, rtol=0, atol=1e-14)
+    assert np.linalg.norm(state.amps - want) <= 1e-12
