@@ -2245,7 +2245,32 @@ int nsb_run_mma_streamed(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const dou
         throw std::invalid_argument("streamed MMA runs take 1q / 2q gates only");
     }
     *n_measures = n_meas;
-    const size_t n_parts = marks.size() + 1;
+    // parts: the gate runs between markers; the first run is also cut at 1/16,
+    // 1/8, 1/4 and 1/2 of its length (an exact frame flush at each cut) so the
+    // device starts after a short plan instead of a whole filter step
+    struct Range {
+      int64_t b, e;
+      int64_t mark;  // index of the marker ending the part, -1: an artificial cut
+    };
+    std::vector<Range> ranges;
+    for (size_t s = 0; s <= marks.size(); ++s) {
+      const int64_t b = s == 0 ? 0 : marks[s - 1] + 1, e = s < marks.size() ? marks[s] : n_ops;
+      const int64_t mk = s < marks.size() ? marks[s] : -1;
+      if (s == 0 && e - b >= 4096) {
+        int64_t at = b;
+        for (int64_t div : {16, 8, 4, 2}) {
+          const int64_t cut = b + (e - b) / div;
+          if (cut > at) {
+            ranges.push_back({at, cut, -1});
+            at = cut;
+          }
+        }
+        ranges.push_back({at, e, mk});
+      } else {
+        ranges.push_back({b, e, mk});
+      }
+    }
+    const size_t n_parts = ranges.size();
     const double budget = default_identity_budget_value();
     // producer: parts planned in order on a host thread
     std::vector<std::unique_ptr<HostPlan>> parts(n_parts);
@@ -2256,7 +2281,7 @@ int nsb_run_mma_streamed(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const dou
     std::atomic<bool> stop{false};
     std::thread producer([&] {
       for (size_t s = 0; s < n_parts && !stop.load(); ++s) {
-        const int64_t b = s == 0 ? 0 : marks[s - 1] + 1, e = s < marks.size() ? marks[s] : n_ops;
+        const int64_t b = ranges[s].b, e = ranges[s].e;
         auto H = std::make_unique<HostPlan>();
         try {
           H->identity_budget = n_ops ? budget * static_cast<double>(e - b) / n_ops : 0.0;
@@ -2358,7 +2383,8 @@ int nsb_run_mma_streamed(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const dou
           pending_q = -1;
         }
         running *= H.tail_scale2;
-        if (s < marks.size() && ops[marks[s]].kind == NSB_OP_MEASURE) {
+        const int64_t mk = ranges[s].mark;
+        if (mk >= 0 && ops[mk].kind == NSB_OP_MEASURE) {
           if (mp.empty() || pending_q >= 0) {
             PassDesc P = fresh();
             if (pending_q >= 0) {
@@ -2368,9 +2394,9 @@ int nsb_run_mma_streamed(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const dou
             }
             mp.push_back(P);
           }
-          mp.back().measure_q = ops[marks[s]].q[0];
+          mp.back().measure_q = ops[mk].q[0];
           mp.back().measure_slot = step;
-          pending_q = ops[marks[s]].q[0];
+          pending_q = ops[mk].q[0];
           pending_slot = step;
           scale[step] = running;
           running = 1.0;

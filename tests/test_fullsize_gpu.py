@@ -214,8 +214,10 @@ def test_streamed_mma_run_matches_the_single_launch_program():
     state.restart()
     p_str = run_mma_streamed(state, exe, wl.params, pool)
     assert len(p_str) == 8
-    np.testing.assert_allclose(p_str, p_one, rtol=0, atol=1e-15)
-    assert np.linalg.norm(state.amps - a_one) <= 1e-13
+    # the streamed run cuts the first gate run into shorter parts (exact frame
+    # flushes), so group boundaries -- and roundings -- differ slightly
+    np.testing.assert_allclose(p_str, p_one, rtol=0, atol=1e-12)
+    assert np.linalg.norm(state.amps - a_one) <= 1e-11
     assert state.last_device_ms > 0.0
 
 
