@@ -259,6 +259,12 @@ int nsb_host_plan_build(const nsb_op* ops, int64_t n_ops, const double* params,
                         nsb_status* st);
 int nsb_host_plan_view(const void* plan, nsb_plan_view* view);
 void nsb_host_plan_free(void* plan);
+/* Chunked execution of a gate item (nsb_shard_swap_overlap): the longest
+ * prefix of item `item`'s passes whose tiles all leave `want_bits` local
+ * qubits other than `avoid_q` untouched (fewer bits if none); *cmask = those
+ * qubits (the highest free ones), *n_pass = the prefix length (0: none). */
+int nsb_host_plan_chunk_prefix(const void* plan, int64_t item, int32_t avoid_q,
+                               int32_t want_bits, int32_t* n_pass, uint64_t* cmask);
 
 /* MMA mode (engine.py:414-423): execute the whole plan from the current
  * state; each MEASURE asserts |0> (p0 < eps -> NSB_EASSERT with step/p0),
@@ -270,6 +276,13 @@ int nsb_plan_run_mma(nsb_ctx* ctx, nsb_plan* plan, double eps, double* assert_pr
 int nsb_plan_run_segment(nsb_ctx* ctx, nsb_plan* plan, int64_t seg, nsb_status* st);
 int nsb_plan_segment_marker(const nsb_plan* plan, int64_t seg, int32_t* kind, int32_t* qubit,
                             int32_t* step);
+/* Gate item `seg`, its chunkable pass prefix (nsb_host_plan_chunk_prefix
+ * with avoid_q = -1) run one chunk of 2^chunk_bits at a time, the rest as
+ * usual: the same state as nsb_plan_run_segment (the single-GPU check of
+ * the chunked launches that nsb_shard_swap_overlap pipelines).
+ * *n_chunked = passes run chunk-wise (0: none, the item ran whole). */
+int nsb_plan_run_segment_chunked(nsb_ctx* ctx, nsb_plan* plan, int64_t seg, int32_t chunk_bits,
+                                 int32_t* n_chunked, nsb_status* st);
 
 /* MMA run with planning streamed behind execution (replaces engine.run(...,
  * "mma")'s gate loop, engine.py:414-423): the op list is cut at its MEASURE /
@@ -363,6 +376,21 @@ int nsb_shard_ipc_handle(nsb_ctx* ctx, uint8_t* handle, nsb_status* st);
 int nsb_shard_open_peers(nsb_ctx* ctx, const uint8_t* handles, nsb_status* st);
 int nsb_shard_swap_p2p(nsb_ctx* ctx, int32_t global_bit, int32_t local_q, nsb_status* st);
 int nsb_shard_close_peers(nsb_ctx* ctx, nsb_status* st);
+/* A qubit swap overlapped with the gate item that follows it (north_star:
+ * "qubit-remap ... overlapped with local-gate blocks"; the reference has no
+ * counterpart -- its state is one host array, engine.py:51, 68-71).  The
+ * item's chunkable pass prefix (nsb_host_plan_chunk_prefix, avoid_q =
+ * local_q) runs chunk by chunk on the context stream while the peer-memory
+ * swap (nsb_shard_swap_p2p's exchange) moves the next chunk on a second
+ * stream with `swap_ctas` CTAs (0: default 32); chunk c's passes start once
+ * both partners' halves of chunk c have landed (per-chunk flags written over
+ * NVLink).  The rest of the item then runs on all tiles.  Falls back to
+ * swap-then-item when no pass prefix is chunkable.  Collective: both
+ * partners call it with the same arguments (their plans are the same
+ * schedule step).  *n_chunked = passes overlapped (0: none). */
+int nsb_shard_swap_overlap(nsb_ctx* ctx, int32_t global_bit, int32_t local_q, nsb_plan* plan,
+                           int64_t seg, int32_t chunk_bits, int32_t swap_ctas,
+                           int32_t* n_chunked, nsb_status* st);
 
 #ifdef __cplusplus
 }

@@ -121,8 +121,12 @@ _SIGNATURES = {
                                            _ST]),
     "nsb_host_plan_view": (ctypes.c_int, [_P, ctypes.POINTER(PlanView)]),
     "nsb_host_plan_free": (None, [_P]),
+    "nsb_host_plan_chunk_prefix": (ctypes.c_int, [_P, _I64, _I32, _I32, ctypes.POINTER(_I32),
+                                                  ctypes.POINTER(ctypes.c_uint64)]),
     "nsb_plan_run_mma": (ctypes.c_int, [_P, _P, _D, _P, _ST]),
     "nsb_plan_run_segment": (ctypes.c_int, [_P, _P, _I64, _ST]),
+    "nsb_plan_run_segment_chunked": (ctypes.c_int, [_P, _P, _I64, _I32, ctypes.POINTER(_I32),
+                                                    _ST]),
     "nsb_plan_segment_marker": (ctypes.c_int, [_P, _I64, ctypes.POINTER(_I32),
                                                ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
     "nsb_plan_last_timing": (ctypes.c_int, [_P, ctypes.POINTER(_D), ctypes.POINTER(_I64)]),
@@ -141,6 +145,8 @@ _SIGNATURES = {
     "nsb_shard_open_peers": (ctypes.c_int, [_P, _P, _ST]),
     "nsb_shard_close_peers": (ctypes.c_int, [_P, _ST]),
     "nsb_shard_swap_p2p": (ctypes.c_int, [_P, _I32, _I32, _ST]),
+    "nsb_shard_swap_overlap": (ctypes.c_int, [_P, _I32, _I32, _P, _I64, _I32, _I32,
+                                              ctypes.POINTER(_I32), _ST]),
 }
 
 EXPORTS = tuple(_SIGNATURES)
@@ -158,6 +164,8 @@ def lib() -> ctypes.CDLL:
                 "g.build()'` (there is no CPU fallback for the gate-application path)")
         handle = ctypes.CDLL(str(LIB_PATH), mode=ctypes.RTLD_LOCAL)
         for name, (res, args) in _SIGNATURES.items():
+            if os.environ.get("NSB_LIB_VARIANT") and not hasattr(handle, name):
+                continue  # an older build variant (A/B timing only)
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args

@@ -287,6 +287,11 @@ struct BlockedParams {
   double eps;
   int debug;         // timing experiments only (NSB_DEBUG_BLOCKED): 1 skip sweeps, 2 skip HBM,
                      // 4 no CTA rotation
+  // chunk restriction (overlapped qubit swaps, nsb_shard_swap_overlap): only
+  // the tiles whose physical bits at cmask (out-of-tile qubits of every pass
+  // of the launch) equal cval; cbits = popcount(cmask).  0: every tile.
+  uint64_t cmask, cval;
+  int cbits;
 };
 
 // ---- octet sweeps over a shared-memory batch -------------------------------
@@ -726,7 +731,7 @@ __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
   // The LAST gate of a group stores its octets from inside its own case, so
   // the common one-gate group never merges the 64-register octet pair across
   // the dispatch (the merge costs the allocator a full copy).
-  auto dispatch = [&](const GateOp o, bool last) {
+  auto dispatch = [&](const GateOp o, bool last) __attribute__((always_inline)) {
     const double2* m = mats + o.mat;
 #ifndef NSB_NO_HOTPATH
     // the dominant kinds first (deep21: whole-octet 2x2 51 %, 4x4-per-third-axis
@@ -860,7 +865,12 @@ constexpr size_t kBlockedSmemBytes = sizeof(double2) * (3 * kTileAmpsMax + kMaxP
                                      sizeof(GroupDesc) * kMaxPassGates +
                                      sizeof(GateOp) * kMaxPassOps;
 
+// kChunk: the chunk-restricted instantiation (overlapped swaps); the plain
+// one compiles the restriction away (its address math is the hot loop's).
+template <bool kChunk>
 __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
+  const uint64_t c_mask = kChunk ? p.cmask : 0, c_val = kChunk ? p.cval : 0;
+  const int c_bits = kChunk ? p.cbits : 0;
   // dynamic shared memory: 3 batch buffers (current, gate-sweep target,
   // prefetch) | pass matrices | pass group descriptors | gate ops
   extern __shared__ __align__(128) double2 smem[];
@@ -902,7 +912,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
     if (tid == 0) {
       uint64_t m = 0;
       for (int b = 0; b < p.n - sp.k; ++b) m |= uint64_t(1) << sp.oq[b];
-      s_omask = m;
+      s_omask = m & ~c_mask;
     }
     constexpr int kHi = kTileQubitsMax - kThreadBits;
     if (tid < (1 << kHi)) {
@@ -927,7 +937,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
       if (tid >> b & 1) lo |= uint64_t(1) << sp.tq[b];
     __syncthreads();
     const int n_out = p.n - k;
-    const uint64_t n_tiles = uint64_t(1) << n_out;
+    const uint64_t n_tiles = uint64_t(1) << (n_out - c_bits);
     const int n_j = k > kThreadBits ? 1 << (k - kThreadBits) : 1;
     const bool loader = tid < (1 << lo_bits);
     const double cscale = sp.collapse_q >= 0 ? 1.0 / sqrt(carry_p0) : 1.0;
@@ -936,8 +946,17 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
 
     auto tile_base = [&](uint64_t t) {  // physical index bits of tile t (no tile-local bits)
       uint64_t base = 0;
-      for (int b = 0; b < n_out; ++b)
-        if (t >> b & 1) base |= uint64_t(1) << sp.oq[b];
+      if constexpr (!kChunk) {
+        for (int b = 0; b < n_out; ++b)
+          if (t >> b & 1) base |= uint64_t(1) << sp.oq[b];
+      } else {
+        base = c_val;
+        for (int b = 0, j = 0; b < n_out; ++b) {
+          const uint64_t qb = uint64_t(1) << sp.oq[b];
+          if (c_mask & qb) continue;  // a chunk bit: fixed to cval
+          if (t >> j++ & 1) base |= qb;
+        }
+      }
       return base;
     };
     // contiguous tile range of this CTA, processed in batches of nb tiles
@@ -952,7 +971,10 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
     const uint64_t t_end = t_begin + per + (vb < extra ? 1 : 0);
     // tile t+1's base from tile t's: increment within the out-of-tile mask
     const uint64_t omask = s_omask;
-    auto next_base = [&](uint64_t b) { return ((b | ~omask) + 1) & omask; };
+    auto next_base = [&](uint64_t b) {
+      if constexpr (!kChunk) return ((b | ~omask) + 1) & omask;
+      return (((b | ~omask) + 1) & omask) | c_val;
+    };
     auto issue_batch = [&](uint64_t t0, uint64_t base0, double2* buf) {
       if (!loader || (p.debug & 2)) return;
       uint64_t base = base0 | lo;
@@ -1187,6 +1209,80 @@ __global__ void k_shard_swap_p2p(double2* __restrict__ mine, double2* __restrict
   __threadfence_system();
 }
 
+// One chunk of an overlapped qubit swap (nsb_shard_swap_overlap): the
+// element pairs of k_shard_swap_p2p whose bits at the chunk qubits equal the
+// chunk's value.  Pair index k (the bits other than L and the chunk qubits)
+// is spread by inserting zeros at pos[0..npos) (ascending: the chunk qubits
+// and L), then the fixed bits are set.  Sub-chunks of 2^clog pairs alternate
+// between the two partners as in k_shard_swap_p2p.
+struct SwapChunk {
+  int npos;
+  int pos[8];
+  uint64_t fixed_mine, fixed_peer;  // chunk value | (v << L) on each side
+  uint64_t n_pairs;
+};
+constexpr int kSwapThreads = 256;
+__global__ void __launch_bounds__(kSwapThreads, 2)
+    k_shard_swap_chunk(double2* __restrict__ mine, double2* __restrict__ peer, SwapChunk sc,
+                       int parity, int clog) {
+  const uint64_t clen = uint64_t(1) << clog;
+  const uint64_t n_sub = (sc.n_pairs + clen - 1) >> clog;
+  const uint64_t n_owned = ((n_sub + 1 - parity) >> 1) << clog;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  constexpr int U = 4;
+  for (uint64_t e0 = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e0 < n_owned;
+       e0 += U * stride) {
+    uint64_t km[U], kp[U];
+    double2 x[U], y[U];
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t e = e0 + u * stride;
+      uint64_t k = ((2 * (e >> clog) + parity) << clog) | (e & (clen - 1));
+      ok[u] = e < n_owned && k < sc.n_pairs;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < sc.npos) k = insert_zero(k, sc.pos[i]);
+      km[u] = k | sc.fixed_mine;
+      kp[u] = k | sc.fixed_peer;
+      if (ok[u]) {
+        x[u] = mine[km[u]];
+        y[u] = peer[kp[u]];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (ok[u]) {
+        mine[km[u]] = y[u];
+        peer[kp[u]] = x[u];
+      }
+  }
+}
+
+// Chunk-landed flags of overlapped swaps, in each shard allocation behind its
+// amplitudes (kShardFlagWords words; slot 2 c + side).  The signal runs on
+// the swap stream after the chunk's kernel (whose stores, local and remote,
+// are complete at its end) and writes both partners' copies; the wait holds
+// the gate stream until both sides' kernels for the chunk are done.
+constexpr int kShardFlagWords = 256;
+__global__ void k_flag_signal(unsigned* mine, unsigned* peer, int slot, unsigned epoch) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(mine + slot), "r"(epoch) : "memory");
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(peer + slot), "r"(epoch) : "memory");
+}
+__global__ void k_flag_wait(const unsigned* f, int s0, int s1, unsigned epoch) {
+  if (threadIdx.x == 0) {
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f + s0) : "memory");
+    } while (v < epoch);
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f + s1) : "memory");
+    } while (v < epoch);
+    __threadfence_system();
+  }
+}
+
 }  // namespace dev
 }  // namespace nsb
 
@@ -1275,6 +1371,9 @@ struct nsb_ctx {
   cudaStream_t xfer = nullptr;
   cudaEvent_t ev_packed[2] = {}, ev_moved[2] = {}, ev_unpacked[2] = {};
   DevBuf<double2> stage_send[2], stage_recv[2];
+  // overlapped swaps (nsb_shard_swap_overlap): epoch of the chunk flags
+  unsigned swap_epoch = 0;
+  cudaEvent_t ev_ov0 = nullptr, ev_ov1 = nullptr;
 };
 
 struct nsb_plan {
@@ -1457,15 +1556,22 @@ size_t host_plan_bytes(const HostPlan& H) {
 
 // state vector allocation; on out-of-memory the plan pool's cached blocks
 // are returned to the device and the allocation retried once
+// (plus the zeroed chunk-flag words of overlapped swaps behind the amplitudes)
+constexpr uint64_t kFlagAmps = dev::kShardFlagWords * sizeof(unsigned) / sizeof(double2);
 void alloc_state(nsb_ctx* c, uint64_t n_amps) {
   try {
-    c->amps.alloc(n_amps);
+    c->amps.alloc(n_amps + kFlagAmps);
   } catch (const std::bad_alloc&) {
     cudaGetLastError();
     NSB_CUDA(cudaDeviceSynchronize());
     if (c->plan_pool) NSB_CUDA(cudaMemPoolTrimTo(c->plan_pool, 0));
-    c->amps.alloc(n_amps);
+    c->amps.alloc(n_amps + kFlagAmps);
   }
+  NSB_CUDA(cudaMemsetAsync(c->amps.ptr + n_amps, 0, kFlagAmps * sizeof(double2), c->stream));
+}
+
+unsigned* shard_flags(double2* amps, uint64_t n_amps) {
+  return reinterpret_cast<unsigned*>(amps + n_amps);
 }
 
 unsigned grid_for(uint64_t work, int threads, const nsb_ctx* c) {
@@ -1585,7 +1691,8 @@ void apply_matrix(nsb_ctx* c, const double* u, const int32_t* qubits, int k,
 }
 
 // launch k_blocked over [pb, pe) of `passes` cooperatively
-void launch_blocked(nsb_ctx* c, nsb_plan* P, const PassDesc* passes, int pb, int pe, double eps) {
+void launch_blocked(nsb_ctx* c, nsb_plan* P, const PassDesc* passes, int pb, int pe, double eps,
+                    int grid = 0, uint64_t cmask = 0, uint64_t cval = 0) {
   dev::BlockedParams bp;
   bp.amps = c->amps.ptr;
   bp.n = c->n;
@@ -1606,11 +1713,23 @@ void launch_blocked(nsb_ctx* c, nsb_plan* P, const PassDesc* passes, int pb, int
     return e ? std::atoi(e) : 0;
   }();
   bp.debug = debug;
+  bp.cmask = cmask;
+  bp.cval = cval;
+  bp.cbits = __builtin_popcountll(cmask);
   void* args[] = {&bp};
-  NSB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::k_blocked),
-                                       dim3(P->grid), dim3(kPassThreads), args,
+  NSB_CUDA(cudaLaunchCooperativeKernel(cmask ? reinterpret_cast<void*>(dev::k_blocked<true>)
+                                             : reinterpret_cast<void*>(dev::k_blocked<false>),
+                                       dim3(grid > 0 ? grid : P->grid), dim3(kPassThreads), args,
                                        dev::kBlockedSmemBytes, c->stream));
   P->last_launches += 1;
+}
+
+// bits of v spread over the set bits of mask (ascending)
+uint64_t deposit_bits(uint64_t v, uint64_t mask) {
+  uint64_t out = 0;
+  for (int j = 0; mask; mask &= mask - 1, ++j)
+    if (v >> j & 1) out |= mask & (0 - mask);
+  return out;
 }
 
 double p0_scale(const HostPlan& H, int step) {
@@ -1666,10 +1785,12 @@ int nsb_ctx_create(int32_t device, nsb_ctx** out, nsb_status* st) {
     NSB_CUDA(cudaEventCreate(&ctx->tev1));
     NSB_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
     const int smem = static_cast<int>(dev::kBlockedSmemBytes);
-    NSB_CUDA(cudaFuncSetAttribute(dev::k_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  smem));
+    NSB_CUDA(cudaFuncSetAttribute(dev::k_blocked<false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    NSB_CUDA(cudaFuncSetAttribute(dev::k_blocked<true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int per_sm = 0;
-    NSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_blocked,
+    NSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_blocked<false>,
                                                            kPassThreads, smem));
     if (per_sm < 1) throw std::runtime_error("k_blocked cannot be resident");
     ctx->blocked_grid = per_sm * ctx->sm_count;
@@ -1699,6 +1820,8 @@ void ctx_free(nsb_ctx* ctx) {
     if (ctx->ev_unpacked[b]) cudaEventDestroy(ctx->ev_unpacked[b]);
   }
   if (ctx->xfer) cudaStreamDestroy(ctx->xfer);
+  if (ctx->ev_ov0) cudaEventDestroy(ctx->ev_ov0);
+  if (ctx->ev_ov1) cudaEventDestroy(ctx->ev_ov1);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -2335,9 +2458,11 @@ int nsb_run_mma_streamed(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const dou
       bp.bar = bar.ptr;
       bp.eps = eps;
       bp.debug = debug;
+      bp.cmask = bp.cval = 0;
+      bp.cbits = 0;
       NSB_CUDA(cudaMemsetAsync(bar.ptr, 0, sizeof(unsigned), c->stream));
       void* args[] = {&bp};
-      NSB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::k_blocked), dim3(grid),
+      NSB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::k_blocked<false>), dim3(grid),
                                            dim3(kPassThreads), args, dev::kBlockedSmemBytes,
                                            c->stream));
     };
@@ -2694,6 +2819,125 @@ int nsb_shard_swap_p2p(nsb_ctx* c, int32_t global_bit, int32_t local_q, nsb_stat
         c->amps.ptr, c->peers[partner], half, local_q, 1 - b, b, b, clog);
     NSB_CUDA(cudaGetLastError());
     comm_barrier(c);  // both halves of the exchange landed before either continues
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int nsb_plan_run_segment_chunked(nsb_ctx* c, nsb_plan* P, int64_t seg, int32_t chunk_bits,
+                                 int32_t* n_chunked, nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    if (!P || P->ctx != c) throw std::invalid_argument("plan belongs to another context");
+    if (P->n != c->n) throw std::invalid_argument("plan was built for another qubit count");
+    if (seg < 0 || seg >= static_cast<int64_t>(P->host.items.size()))
+      throw std::invalid_argument("item index out of range");
+    NSB_CUDA(cudaSetDevice(c->device));
+    uint64_t cm = 0;
+    const int np = chunk_prefix(P->host, seg, -1, chunk_bits, &cm);
+    if (n_chunked) *n_chunked = np;
+    const Item& it = P->host.items[static_cast<size_t>(seg)];
+    if (np == 0) {
+      run_item(c, P, it);
+    } else {
+      const int cb = __builtin_popcountll(cm);
+      for (uint64_t ch = 0; ch < (uint64_t(1) << cb); ++ch)
+        launch_blocked(c, P, P->passes.ptr, it.pass_begin, it.pass_begin + np, -1.0, 0, cm,
+                       deposit_bits(ch, cm));
+      if (it.pass_begin + np < it.pass_end)
+        launch_blocked(c, P, P->passes.ptr, it.pass_begin + np, it.pass_end, -1.0);
+    }
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+// Overlapped qubit swap (header): the chunk pipeline.  Swap stream: chunk
+// kernels back to back, each followed by its flag signal; gate stream: per
+// chunk, wait for both partners' flags, then the item's chunkable passes on
+// that chunk (grid reduced by the swap CTAs, which share the SMs); then the
+// rest of the item on every tile.
+int nsb_shard_swap_overlap(nsb_ctx* c, int32_t global_bit, int32_t local_q, nsb_plan* P,
+                           int64_t seg, int32_t chunk_bits, int32_t swap_ctas,
+                           int32_t* n_chunked, nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    if (!c->comm) throw std::invalid_argument("no communicator (nsb_comm_init)");
+    if (global_bit < 0 || (1 << global_bit) >= c->nranks || local_q < 0 || local_q >= c->n)
+      throw std::invalid_argument("bad shard swap qubits");
+    if (!P || P->ctx != c) throw std::invalid_argument("plan belongs to another context");
+    if (P->n != c->n) throw std::invalid_argument("plan was built for another qubit count");
+    if (seg < 0 || seg >= static_cast<int64_t>(P->host.items.size()))
+      throw std::invalid_argument("item index out of range");
+    const int partner = c->rank ^ (1 << global_bit);
+    if (!c->peers[partner]) throw std::invalid_argument("peer shard not mapped (nsb_shard_open_peers)");
+    NSB_CUDA(cudaSetDevice(c->device));
+    uint64_t cm = 0;
+    const int np = chunk_prefix(P->host, seg, local_q, chunk_bits, &cm);
+    if (n_chunked) *n_chunked = np;
+    const Item& it = P->host.items[static_cast<size_t>(seg)];
+    const int b = (c->rank >> global_bit) & 1;
+    const uint64_t half = c->n_amps >> 1;
+    if (np == 0) {  // nothing chunkable: swap, then the item
+      const int clog = static_cast<int>(std::min<uint64_t>(16, c->n - 1));
+      comm_barrier(c);
+      dev::k_shard_swap_p2p<<<static_cast<unsigned>(c->sm_count * 4), 256, 0, c->stream>>>(
+          c->amps.ptr, c->peers[partner], half, local_q, 1 - b, b, b, clog);
+      NSB_CUDA(cudaGetLastError());
+      comm_barrier(c);
+      run_item(c, P, it);
+      NSB_CUDA(cudaStreamSynchronize(c->stream));
+      return;
+    }
+    if (!c->xfer) NSB_CUDA(cudaStreamCreateWithFlags(&c->xfer, cudaStreamNonBlocking));
+    if (!c->ev_ov0) NSB_CUDA(cudaEventCreateWithFlags(&c->ev_ov0, cudaEventDisableTiming));
+    if (!c->ev_ov1) NSB_CUDA(cudaEventCreateWithFlags(&c->ev_ov1, cudaEventDisableTiming));
+    const int cb = __builtin_popcountll(cm);
+    const int n_ch = 1 << cb;
+    if (2 * n_ch > dev::kShardFlagWords) throw std::invalid_argument("too many swap chunks");
+    const int ctas = swap_ctas > 0 ? swap_ctas : 32;
+    const int grid = std::max(1, P->grid - ctas);
+    const unsigned epoch = ++c->swap_epoch;
+    unsigned* f_mine = shard_flags(c->amps.ptr, c->n_amps);
+    unsigned* f_peer = shard_flags(c->peers[partner], c->n_amps);
+    dev::SwapChunk sc{};
+    {
+      std::vector<int> pos;
+      for (uint64_t m = cm | (uint64_t(1) << local_q); m; m &= m - 1) pos.push_back(__builtin_ctzll(m));
+      sc.npos = static_cast<int>(pos.size());
+      for (int i = 0; i < sc.npos; ++i) sc.pos[i] = pos[i];
+      sc.n_pairs = half >> cb;
+    }
+    const int clog = static_cast<int>(std::min<uint64_t>(16, c->n - 1 - cb));
+    // timing experiments only (wrong states): 1 = no swap kernels, 2 = no chunked passes
+    static const int ov_debug = [] {
+      const char* e = std::getenv("NSB_OVERLAP_DEBUG");
+      return e ? std::atoi(e) : 0;
+    }();
+    comm_barrier(c);  // both shards are final before either is touched
+    NSB_CUDA(cudaEventRecord(c->ev_ov0, c->stream));
+    NSB_CUDA(cudaStreamWaitEvent(c->xfer, c->ev_ov0, 0));
+    for (int ch = 0; ch < n_ch; ++ch) {
+      const uint64_t cv = deposit_bits(static_cast<uint64_t>(ch), cm);
+      sc.fixed_mine = cv | (uint64_t(1 - b) << local_q);
+      sc.fixed_peer = cv | (uint64_t(b) << local_q);
+      if (!(ov_debug & 1)) {
+        dev::k_shard_swap_chunk<<<static_cast<unsigned>(ctas), dev::kSwapThreads, 0, c->xfer>>>(
+            c->amps.ptr, c->peers[partner], sc, b, clog);
+        NSB_CUDA(cudaGetLastError());
+      }
+      dev::k_flag_signal<<<1, 1, 0, c->xfer>>>(f_mine, f_peer, 2 * ch + b, epoch);
+      NSB_CUDA(cudaGetLastError());
+    }
+    for (int ch = 0; ch < n_ch; ++ch) {
+      dev::k_flag_wait<<<1, 32, 0, c->stream>>>(f_mine, 2 * ch, 2 * ch + 1, epoch);
+      NSB_CUDA(cudaGetLastError());
+      if (!(ov_debug & 2))
+        launch_blocked(c, P, P->passes.ptr, it.pass_begin, it.pass_begin + np, -1.0, grid, cm,
+                       deposit_bits(static_cast<uint64_t>(ch), cm));
+    }
+    if (it.pass_begin + np < it.pass_end)
+      launch_blocked(c, P, P->passes.ptr, it.pass_begin + np, it.pass_end, -1.0);
+    NSB_CUDA(cudaEventRecord(c->ev_ov1, c->xfer));
+    NSB_CUDA(cudaStreamWaitEvent(c->stream, c->ev_ov1, 0));
     NSB_CUDA(cudaStreamSynchronize(c->stream));
   });
 }

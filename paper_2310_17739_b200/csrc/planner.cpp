@@ -1676,6 +1676,54 @@ extern "C" int nsb_host_plan_build(const nsb_op* ops, int64_t n_ops, const doubl
   return NSB_OK;
 }
 
+namespace nsb {
+// Overlapped qubit swaps (device.cu, nsb_shard_swap_overlap).  A pass never
+// moves data between tiles, so a run of passes that all leave a set B of
+// local qubits out of their tiles can be executed chunk by chunk, one chunk
+// per value of the B bits -- chunk c as soon as chunk c of the swap before it
+// has landed.  This picks the longest prefix of item `item`'s passes that
+// leaves `want_bits` qubits (other than the swapped local qubit `avoid_q`)
+// out of every tile, falling back to fewer bits; B = the highest such
+// qubits.  Returns the prefix length (0: no chunking) and B in *cmask.
+int chunk_prefix(const HostPlan& H, int64_t item, int avoid_q, int want_bits, uint64_t* cmask) {
+  *cmask = 0;
+  if (item < 0 || item >= static_cast<int64_t>(H.items.size())) return 0;
+  const Item& it = H.items[static_cast<size_t>(item)];
+  if (it.kind != Item::kGates || want_bits < 1) return 0;
+  const uint64_t all = H.n_qubits >= 64 ? ~uint64_t(0) : (uint64_t(1) << H.n_qubits) - 1;
+  for (int bits = std::min(want_bits, 6); bits >= 1; --bits) {
+    uint64_t used = avoid_q >= 0 ? uint64_t(1) << avoid_q : 0;
+    int n = 0;
+    for (int pi = it.pass_begin; pi < it.pass_end; ++pi) {
+      const PassDesc& P = H.passes[static_cast<size_t>(pi)];
+      uint64_t u = used;
+      for (int b = 0; b < P.k; ++b) u |= uint64_t(1) << P.tq[b];
+      if (popc(all & ~u) < bits) break;
+      used = u;
+      ++n;
+    }
+    if (n == 0) continue;
+    uint64_t freeq = all & ~used, m = 0;
+    for (int b = 0; b < bits; ++b) {
+      const uint64_t top = uint64_t(1) << (63 - __builtin_clzll(freeq));
+      m |= top;
+      freeq &= ~top;
+    }
+    *cmask = m;
+    return n;
+  }
+  return 0;
+}
+}  // namespace nsb
+
+extern "C" int nsb_host_plan_chunk_prefix(const void* plan, int64_t item, int32_t avoid_q,
+                                          int32_t want_bits, int32_t* n_pass, uint64_t* cmask) {
+  if (!plan || !n_pass || !cmask) return NSB_EINVAL;
+  *n_pass = nsb::chunk_prefix(*static_cast<const nsb::HostPlan*>(plan), item, avoid_q, want_bits,
+                              cmask);
+  return NSB_OK;
+}
+
 extern "C" int nsb_host_plan_view(const void* plan, nsb_plan_view* v) {
   if (!plan || !v) return NSB_EINVAL;
   const auto* H = static_cast<const nsb::HostPlan*>(plan);

@@ -128,5 +128,7 @@ struct HostPlan {
 
 void plan_info(const HostPlan& H, nsb_plan_info* info);
 double default_identity_budget_value();  // NSB_IDENTITY_BUDGET or 3e-11
+// passes of item `item` runnable chunk by chunk over the qubits *cmask (planner.cpp)
+int chunk_prefix(const HostPlan& H, int64_t item, int avoid_q, int want_bits, uint64_t* cmask);
 
 }  // namespace nsb

@@ -29,6 +29,7 @@ mode as in the reference; rejection mode is single-GPU only.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -462,6 +463,7 @@ class ShardedState:
         prog = self.compile(ops, params, payloads, window)
         try:
             probs = prog.run(eps)
+            self.last_overlapped_passes = prog.overlapped_passes
         finally:
             prog.close()
         return [probs[k] for k in sorted(probs)], prog.steps
@@ -501,6 +503,7 @@ class ShardedProgram:
             self.close()
             raise
         self.n_swaps = swap_count(steps)
+        self.overlapped_passes = 0  # gate passes run under a swap (last run)
 
     def close(self):
         for e in self.plans:
@@ -514,29 +517,58 @@ class ShardedProgram:
         except Exception:
             pass
 
+    def _swap(self, i: int, s: Step, chunk_amps: int) -> bool:
+        """Execute swap step i.  With NSB_SWAP_OVERLAP=1 (and peer-memory swaps)
+        the swap is overlapped with the first item of the gate step that
+        follows it (nsb_shard_swap_overlap: that item's chunkable passes run
+        chunk by chunk as the swapped chunks land).  Off by default: measured
+        slower on B200 (the gate passes lose the SMs the swap kernel takes,
+        DESIGN.md section 8).  Returns True when that item has run."""
+        S = self.state
+        nxt = self.plans[i + 1] if i + 1 < len(self.plans) else None
+        if (S.peer_swaps and nxt is not None and nxt[1] > 0
+                and os.environ.get("NSB_SWAP_OVERLAP", "0") == "1"):
+            n = ctypes.c_int32(0)
+            S.dev.call("nsb_shard_swap_overlap", s.global_bit, s.local_q, nxt[0], 0,
+                       int(os.environ.get("NSB_SWAP_CHUNK_BITS", "3")),
+                       int(os.environ.get("NSB_SWAP_CTAS", "0")), ctypes.byref(n))
+            self.overlapped_passes += n.value
+            return True
+        if S.peer_swaps:
+            S.dev.call("nsb_shard_swap_p2p", s.global_bit, s.local_q)
+        else:
+            S.dev.call("nsb_shard_swap", s.global_bit, s.local_q, chunk_amps)
+        return False
+
+    def _gates(self, plan, first: int):
+        h, n_items = plan
+        st = N.Status()
+        for i in range(first, n_items):
+            N.check(N.lib().nsb_plan_run_segment(self.state.dev.handle, h, i, ctypes.byref(st)), st)
+
     def run(self, eps: float = EPS_MMA, chunk_amps: int = 0,
             times: dict | None = None) -> dict[int, float]:
         """Execute on this rank (collective with the other ranks); returns
         {step: p0}.  Raises FilterAssertionError on every rank when a
         post-selection probability falls below eps.  With `times`, each step
         is bracketed by device events and its time (ms) is added under its
-        kind ("gates" / "swap" / "measure")."""
+        kind ("gates" / "swap" / "measure"; an overlapped swap and the gate
+        item under it: "swap+gates")."""
         S = self.state
         probs: dict[int, float] = {}
-        st = N.Status()
-        for s, plan in zip(self.steps, self.plans):
+        self.overlapped_passes = 0
+        done_first = False  # item 0 of this gate step ran under the swap before it
+        for i, (s, plan) in enumerate(zip(self.steps, self.plans)):
             if times is not None:
                 S.timer_start()
+            kind = s.kind
             if s.kind == "gates":
-                h, n_items = plan
-                for i in range(n_items):
-                    N.check(N.lib().nsb_plan_run_segment(S.dev.handle, h, i, ctypes.byref(st)),
-                            st)
+                self._gates(plan, 1 if done_first else 0)
+                done_first = False
             elif s.kind == "swap":
-                if S.peer_swaps:
-                    S.dev.call("nsb_shard_swap_p2p", s.global_bit, s.local_q)
-                else:
-                    S.dev.call("nsb_shard_swap", s.global_bit, s.local_q, chunk_amps)
+                done_first = self._swap(i, s, chunk_amps)
+                if done_first:
+                    kind = "swap+gates"
             else:
                 p = ctypes.c_double(0.0)
                 S.dev.call("nsb_branch_probability", s.local_q, 0, ctypes.byref(p))
@@ -546,7 +578,7 @@ class ShardedProgram:
                     raise FilterAssertionError(s.step, p0)
                 S.dev.call("nsb_project", s.local_q, 0, p0)
             if times is not None:
-                times[s.kind] = times.get(s.kind, 0.0) + S.timer_stop()
+                times[kind] = times.get(kind, 0.0) + S.timer_stop()
         return probs
 
     def run_path(self) -> tuple[list, bool]:
@@ -557,18 +589,13 @@ class ShardedProgram:
         the path (every shot stops there)."""
         S = self.state
         path = []
-        st = N.Status()
-        for s, plan in zip(self.steps, self.plans):
+        done_first = False
+        for i, (s, plan) in enumerate(zip(self.steps, self.plans)):
             if s.kind == "gates":
-                h, n_items = plan
-                for i in range(n_items):
-                    N.check(N.lib().nsb_plan_run_segment(S.dev.handle, h, i, ctypes.byref(st)),
-                            st)
+                self._gates(plan, 1 if done_first else 0)
+                done_first = False
             elif s.kind == "swap":
-                if S.peer_swaps:
-                    S.dev.call("nsb_shard_swap_p2p", s.global_bit, s.local_q)
-                else:
-                    S.dev.call("nsb_shard_swap", s.global_bit, s.local_q, 0)
+                done_first = self._swap(i, s, 0)
             else:
                 p = ctypes.c_double(0.0)
                 S.dev.call("nsb_branch_probability", s.local_q, 0, ctypes.byref(p))

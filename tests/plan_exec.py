@@ -307,9 +307,12 @@ def _apply_group_batches(Bs, G, ops, mats, tbs, k, nvalid):
         np.put_along_axis(Bs, U(st), x[c], axis=1)
 
 
-def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12, workers=148):
+def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12, workers=148,
+               chunk=None):
     """Execute a pass list on `state` in place, with k_blocked's per-CTA
-    contiguous tile ranges and batches; returns {step: p0} and the carry."""
+    contiguous tile ranges and batches; returns {step: p0} and the carry.
+    chunk = (cmask, cval): only the tiles whose bits at cmask equal cval
+    (k_blocked's chunk restriction, nsb_shard_swap_overlap)."""
     n = plan.n
     rec = {}
     fast = not _check()
@@ -318,6 +321,11 @@ def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12, workers=1
         lidx = _scatter(np.arange(1 << k, dtype=np.int64), P["tq"][:k])
         n_tiles = 1 << (n - k)
         tb_all = _scatter(np.arange(n_tiles, dtype=np.int64), P["oq"][:n - k])
+        if chunk is not None:
+            cm, cv = chunk
+            assert not np.any(lidx & cm), "chunk qubits inside a pass's tile"
+            tb_all = tb_all[(tb_all & cm) == cv]
+            n_tiles = len(tb_all)
         nb = 1 if k >= TILE_MAX else min(1 << (TILE_MAX - k), 4)
         block = plan.mats[int(P["mat_begin"]):int(P["mat_begin"]) + int(P["mat_count"])]
         groups = plan.groups[int(P["group_begin"]):int(P["group_end"])]

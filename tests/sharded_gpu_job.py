@@ -25,13 +25,21 @@ def cases():
     wl = W.layered_workload(14, 6, 14)
     fops, pool, _ = W.fuse_packed(wl.ops, wl.params, wl.payloads)
     yield "layered14", fops, wl.params, pool, 14
+    # big enough for chunked overlap of swaps with the gate group after them
+    wl = W.layered_workload(18, 6, 18)
+    fops, pool, _ = W.fuse_packed(wl.ops, wl.params, wl.payloads)
+    yield "layered18", fops, wl.params, pool, 18
 
 
 def main(out):
+    # peer-memory swaps overlapped with the gate group after them (off by
+    # default in ShardedProgram.run; the parity check covers that path too)
+    os.environ["NSB_SWAP_OVERLAP"] = "1"
     dist.init_process_group("gloo")
     rank = dist.get_rank()
     res = {}
-    for (tag, ops, params, pool, n), peer in zip(list(cases()) * 2, [True, True, False, False]):
+    cs = list(cases())
+    for (tag, ops, params, pool, n), peer in zip(cs * 2, [True] * len(cs) + [False] * len(cs)):
         tag = tag + ("_p2p" if peer else "_nccl")
         st = S.ShardedState.from_torch_distributed(n, device=int(os.environ["LOCAL_RANK"]),
                                                    peer_swaps=peer)
@@ -48,6 +56,7 @@ def main(out):
             res["got_" + tag] = np.concatenate(shards)
             res["want_" + tag] = want
             res["gotp_" + tag] = np.asarray(probs)
+            res["overlap_" + tag] = np.asarray([st.last_overlapped_passes])
             res["wantp_" + tag] = np.asarray(want_p)
             ref = SE.O.sample(res["got_" + tag], n, 1024, 2310)
             res["samples_ok_" + tag] = np.asarray([samples[c] == ref for c in sorted(samples)])

@@ -270,6 +270,9 @@ def test_nccl_sharded_matches_oracle(tmp_path, ranks):
             assert d["samples_ok_" + tag].all(), tag  # ShardedState.sample == reference sample
     rej = [k for k in d.files if k.startswith("rejection_ok_")]
     assert rej and all(d[k].all() for k in rej), rej  # sharded rejection mode == reference
+    # peer-memory swaps overlapped with the gate group after them (chunked passes)
+    assert int(d["overlap_layered18_p2p"][0]) > 0
+    assert int(d["overlap_layered18_nccl"][0]) == 0
 
 
 # ---------------------------------------------------------------------------
