@@ -244,7 +244,9 @@ int nsb_plan_info_get(const nsb_plan* plan, nsb_plan_info* info);
  * verify the planner on machines without a GPU. */
 typedef struct nsb_plan_view {
   int32_t n_qubits, tile_qubits, mma_ok, n_measures;
-  int32_t pass_desc_bytes, group_desc_bytes, gate_op_bytes, pad0;
+  int32_t pass_desc_bytes, group_desc_bytes, gate_op_bytes;
+  int32_t tma_edges;       /* 1: tiles move by TMA -- each pass's first group loads and its
+                              last group stores under the 128-byte TMA swizzle */
   int64_t n_passes, n_mma_passes, n_groups, n_gate_ops, n_matrices, n_items;
   const void* passes;      /* plain gate passes (items reference ranges) */
   const void* mma_passes;  /* single-launch MMA program */

@@ -70,7 +70,7 @@ class PlanView(ctypes.Structure):
     _fields_ = [("n_qubits", ctypes.c_int32), ("tile_qubits", ctypes.c_int32),
                 ("mma_ok", ctypes.c_int32), ("n_measures", ctypes.c_int32),
                 ("pass_desc_bytes", ctypes.c_int32), ("group_desc_bytes", ctypes.c_int32),
-                ("gate_op_bytes", ctypes.c_int32), ("pad0", ctypes.c_int32),
+                ("gate_op_bytes", ctypes.c_int32), ("tma_edges", ctypes.c_int32),
                 ("n_passes", ctypes.c_int64), ("n_mma_passes", ctypes.c_int64),
                 ("n_groups", ctypes.c_int64), ("n_gate_ops", ctypes.c_int64),
                 ("n_matrices", ctypes.c_int64), ("n_items", ctypes.c_int64),

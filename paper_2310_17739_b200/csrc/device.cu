@@ -14,6 +14,7 @@
 //       separated by grid-wide barriers.
 // The state is complex128 in HBM as double2 (16-byte vector loads/stores).
 #include <cooperative_groups.h>
+#include <cuda.h>  // CUtensorMap types only: the encoder comes from cudaGetDriverEntryPoint
 #include <dlfcn.h>
 #include <nccl.h>  // types only: libnccl is resolved at run time (shard_nccl)
 
@@ -272,6 +273,120 @@ __global__ void k_sum_fixed2(const double* __restrict__ in, int count, double* _
 // ---------------------------------------------------------------------------
 // blocked gate-stream kernel
 
+// ---- TMA tiles (planner.h "TMA tiles") --------------------------------------
+// Per pass: a tensor map over the whole state whose dims are the tile's qubit
+// runs.  dim 0 = qubits 0..2 as 16 doubles (128 bytes, the swizzle span);
+// dim i >= 1 covers qubits start[i] .. start[i] + ebits[i] - 1 with the box
+// over its lowest run bits (dim 1 starts at qubit 3: a short gap below the
+// first run is a traversal stride, a long one a dim with a box of one); the
+// last dim reaches qubit n - 1, so tile qubits beyond five dims (`left`) are
+// coordinate bits of it, one copy per value, each copy 2^box_bits amplitudes.
+// rank 0: the pass's tiles need too many copies and move by cp.async.
+struct alignas(64) TmaPass {
+  CUtensorMap map;  // 128 bytes
+  uint64_t left;
+  int8_t start[5];
+  int8_t ebits[5];
+  int8_t rank;
+  int8_t box_bits;
+  uint8_t pad[44];
+};
+static_assert(sizeof(TmaPass) == 192, "TmaPass layout");
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred done;\n"
+      "NSB_MBAR_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n"
+      "@!done bra NSB_MBAR_WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared, completion counted on the mbarrier
+__device__ __forceinline__ void tma_load(uint32_t dst, const void* map, uint32_t bar, int rank,
+                                         const int* c) {
+  switch (rank) {
+    case 2:
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst), "l"(map), "r"(bar), "r"(c[0]), "r"(c[1])
+          : "memory");
+      break;
+    case 3:
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst), "l"(map), "r"(bar), "r"(c[0]), "r"(c[1]),
+          "r"(c[2])
+          : "memory");
+      break;
+    case 4:
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst), "l"(map), "r"(bar), "r"(c[0]),
+          "r"(c[1]), "r"(c[2]), "r"(c[3])
+          : "memory");
+      break;
+    default:
+      asm volatile(
+          "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst), "l"(map), "r"(bar), "r"(c[0]),
+          "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4])
+          : "memory");
+      break;
+  }
+}
+// shared -> global, one bulk group per tile (cp.async.bulk.commit_group)
+__device__ __forceinline__ void tma_store(const void* map, uint32_t src, int rank, const int* c) {
+  switch (rank) {
+    case 2:
+      asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];"
+                   ::"l"(map), "r"(src), "r"(c[0]), "r"(c[1]) : "memory");
+      break;
+    case 3:
+      asm volatile(
+          "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];"
+          ::"l"(map), "r"(src), "r"(c[0]), "r"(c[1]), "r"(c[2]) : "memory");
+      break;
+    case 4:
+      asm volatile(
+          "cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];"
+          ::"l"(map), "r"(src), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]) : "memory");
+      break;
+    default:
+      asm volatile(
+          "cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group"
+          " [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(map), "r"(src), "r"(c[0]), "r"(c[1]),
+          "r"(c[2]), "r"(c[3]), "r"(c[4])
+          : "memory");
+      break;
+  }
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_shared() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+// planner.h swz_tma: the 128-byte TMA swizzle in 16-byte slots
+__device__ __forceinline__ int swz_tma(int l) { return l ^ ((l >> 3) & 7); }
+
 struct BlockedParams {
   double2* amps;
   int n;
@@ -292,6 +407,8 @@ struct BlockedParams {
   // of the launch) equal cval; cbits = popcount(cmask).  0: every tile.
   uint64_t cmask, cval;
   int cbits;
+  const TmaPass* tmaps;  // per pass of `passes` (TMA plans, planner.h); else null
+  int tma_store;         // TMA passes store their tiles by TMA (else by the threads)
 };
 
 // ---- octet sweeps over a shared-memory batch -------------------------------
@@ -864,16 +981,28 @@ __device__ __forceinline__ void cp_async_wait() {
 constexpr size_t kBlockedSmemBytes = sizeof(double2) * (3 * kTileAmpsMax + kMaxPassMats) +
                                      sizeof(GroupDesc) * kMaxPassGates +
                                      sizeof(GateOp) * kMaxPassOps;
+// TMA plans: the batch buffers start on a 1024-byte boundary (128-byte swizzle)
+constexpr size_t kBlockedSmemBytesTma = kBlockedSmemBytes + 1024;
 
 // kChunk: the chunk-restricted instantiation (overlapped swaps); the plain
 // one compiles the restriction away (its address math is the hot loop's).
-template <bool kChunk>
+// kTma: a TMA plan (planner.h): tiles hold qubits 0..2, k = kTileQubitsMax,
+// the pass-edge layout is swz_tma.  Without kChunk the tiles move by
+// cp.async.bulk.tensor (one elected thread issues, an mbarrier per buffer
+// counts the bytes in, bulk groups track the stores); the chunk-restricted
+// instantiation keeps per-thread cp.async under the same layout.
+template <bool kChunk, bool kTma>
 __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
+  constexpr bool kHw = kTma && !kChunk;
   const uint64_t c_mask = kChunk ? p.cmask : 0, c_val = kChunk ? p.cval : 0;
   const int c_bits = kChunk ? p.cbits : 0;
   // dynamic shared memory: 3 batch buffers (current, gate-sweep target,
   // prefetch) | pass matrices | pass group descriptors | gate ops
-  extern __shared__ __align__(128) double2 smem[];
+  extern __shared__ __align__(128) double2 smem_raw[];
+  double2* smem = smem_raw;
+  if constexpr (kTma) smem += ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) / sizeof(double2);
+  // shared-memory slot of a tile-local amplitude at the pass edges (loads,
+  // collapse, stores): the TMA layout in a TMA pass (sp.tma) of a TMA plan
   double2* s_mats = smem + 3 * kTileAmpsMax;
   GroupDesc* s_groups = reinterpret_cast<GroupDesc*>(s_mats + kMaxPassMats);
   GateOp* s_ops = reinterpret_cast<GateOp*>(s_groups + kMaxPassGates);
@@ -884,9 +1013,30 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
   __shared__ double red[32];
   __shared__ double s_p0;
   __shared__ uint64_t s_omask;  // physical mask of the pass's out-of-tile qubits
+  __shared__ __align__(8) uint64_t s_mbar[3];  // TMA: bytes landed per batch buffer
+  __shared__ uint64_t s_tleft;                 // TMA: the pass's TmaPass fields
+  __shared__ int8_t s_tstart[5], s_tebits[5], s_trank, s_tbox;
   const int tid = threadIdx.x;
   double carry_p0 = 1.0;  // p0 of the previous pass's assertion (collapse input)
   unsigned n_bar = 0;     // grid barriers passed in this launch
+  unsigned mph = 0;       // TMA: mbarrier phase to wait for, per buffer (bit b)
+  // slot of tile-local amplitude (b << k) + tid + (j << kThreadBits): in a TMA
+  // pass the copy layout permutes the tile bits (PassDesc::tperm) under swz_tma
+  bool etma = false;
+  int k_cur = 0;   // the pass's tile qubits
+  int pi_tid = 0;  // TMA pass: the permuted index of this thread's bits
+  __shared__ int s_pij[1 << (kTileQubitsMax - kThreadBits)];  // ... of j << kThreadBits
+  auto eslot = [&](int b, int j) {
+    if (kTma && etma) return swz_tma(pi_tid ^ s_pij[j]);
+    return swz((b << k_cur) + tid + (j << kThreadBits));
+  };
+  if constexpr (kHw) {
+    if (tid == 0) {
+      for (int b = 0; b < 3; ++b) mbar_init(smem_u32(&s_mbar[b]), 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // (stage() below opens with a CTA barrier)
+  }
 
   // Stage pass pi's descriptors in shared memory.  Called for the next pass
   // right before the grid barrier, so the copy overlaps the wait.
@@ -913,8 +1063,24 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
       uint64_t m = 0;
       for (int b = 0; b < p.n - sp.k; ++b) m |= uint64_t(1) << sp.oq[b];
       s_omask = m & ~c_mask;
+      if constexpr (kHw) {
+        const TmaPass& T = p.tmaps[pi];
+        s_tleft = T.left;
+        for (int i = 0; i < 5; ++i) {
+          s_tstart[i] = T.start[i];
+          s_tebits[i] = T.ebits[i];
+        }
+        s_trank = T.rank;
+        s_tbox = T.box_bits;
+      }
     }
     constexpr int kHi = kTileQubitsMax - kThreadBits;
+    if (kTma && sp.tma && tid < (1 << kHi)) {
+      int v = 0;
+      for (int b = 0; b < kHi; ++b)
+        if (tid >> b & 1) v |= 1 << sp.tperm[kThreadBits + b];
+      s_pij[tid] = v;
+    }
     if (tid < (1 << kHi)) {
       uint64_t h = 0;
       for (int b = 0; b < kHi; ++b)
@@ -943,6 +1109,20 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
     const double cscale = sp.collapse_q >= 0 ? 1.0 / sqrt(carry_p0) : 1.0;
     const int n_groups = sp.group_end - sp.group_begin;
     double msum = 0.0;
+    // TMA plans: this pass's tiles move by TMA (the planner's choice, sp.tma);
+    // the chunk-restricted instantiation moves them by cp.async in that layout
+    etma = kTma && sp.tma;
+    k_cur = k;
+    const bool tp = kHw && etma;
+    // ... and are stored by TMA too (p.tma_store), else by the threads (the
+    // next tile is then requested at the start of a tile, not after its first
+    // sweep: no store is reading the buffer it lands in)
+    const bool ts = tp && p.tma_store;
+    if (kTma && etma) {
+      pi_tid = 0;
+      for (int b = 0; b < kThreadBits; ++b)
+        if (tid >> b & 1) pi_tid |= 1 << sp.tperm[b];
+    }
 
     auto tile_base = [&](uint64_t t) {  // physical index bits of tile t (no tile-local bits)
       uint64_t base = 0;
@@ -983,15 +1163,47 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
         double2* dst = buf;
 #pragma unroll 2
         for (int j = 0; j < n_j; ++j)
-          cp_async16(dst + swz(tid + (j << kThreadBits) + (b << k)), p.amps + (base | s_hi[j]));
+          cp_async16(dst + eslot(b, j), p.amps + (base | s_hi[j]));
         base = next_base(base & omask) | lo;
       }
+    };
+    // TMA (one thread): the tile at physical base `base` <-> buffer bi, one
+    // copy per value of the tile qubits beyond the map's dims
+    auto tma_tile = [&](bool store, uint64_t base, int bi) {
+      const void* map = &p.tmaps[pi].map;
+      const uint64_t left = s_tleft;
+      const int rank = s_trank, box = s_tbox;
+      const uint32_t buf = smem_u32(smem + bi * kTileAmpsMax);
+      const uint32_t bar = smem_u32(&s_mbar[bi]);
+      if (!store) mbar_expect_tx(bar, kTileAmpsMax * sizeof(double2));
+      const int nl = __popcll(left);
+#pragma unroll 1
+      for (int v = 0; v < (1 << nl); ++v) {
+        uint64_t g = base;
+        int j = 0;
+        for (uint64_t m = left; m; m &= m - 1, ++j)
+          if (v >> j & 1) g |= m & (0 - m);
+        int c[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+        for (int i = 1; i < 5; ++i)
+          if (i < rank) c[i] = static_cast<int>((g >> s_tstart[i]) & ((uint64_t(1) << s_tebits[i]) - 1));
+        const uint32_t at = buf + (static_cast<uint32_t>(v) << (box + 4));
+        if (store)
+          tma_store(map, at, rank, c);
+        else
+          tma_load(at, map, bar, rank, c);
+      }
+      if (store) bulk_commit();
     };
 
     int cur = 0, pre = 1, spare = 2;  // buffer roles (rotate)
     uint64_t bnext = t_begin < t_end ? tile_base(t_begin) : 0;  // base of the batch's first tile
-    if (t_begin < t_end) issue_batch(t_begin, bnext, smem);
-    cp_async_commit();
+    if (tp) {
+      if (tid == 0 && t_begin < t_end && !(p.debug & 2)) tma_tile(false, bnext, 0);
+    } else {
+      if (t_begin < t_end) issue_batch(t_begin, bnext, smem);
+      cp_async_commit();
+    }
     for (uint64_t t0 = t_begin; t0 < t_end; t0 += nb) {
       double2* tile = smem + cur * kTileAmpsMax;
       const int nvalid = t_end - t0 < uint64_t(nb) ? static_cast<int>(t_end - t0) : nb;
@@ -1001,9 +1213,25 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
         tbase[b] = b < nvalid ? bnext : 0;
         if (b < nb) bnext = next_base(bnext);  // ends as the next batch's first base
       }
-      if (t0 + nb < t_end) issue_batch(t0 + nb, bnext, smem + pre * kTileAmpsMax);
-      cp_async_commit();
-      cp_async_wait<1>();  // this batch has landed (the next may be in flight)
+      // TMA: the next tile is requested after this tile's first sweep (its
+      // buffer is the one the previous tile's TMA store is still reading)
+      const bool pending = tp && t0 + nb < t_end && !(p.debug & 2);
+      const bool early = !ts || (p.debug & 16);  // request at the tile start
+      auto request_next = [&]() {
+        if (tid == 0) {
+          bulk_wait_read0();
+          tma_tile(false, bnext, pre);
+        }
+      };
+      if (tp) {
+        if (!(p.debug & 2)) mbar_wait(smem_u32(&s_mbar[cur]), (mph >> cur) & 1u);
+        mph ^= 1u << cur;
+        if (pending && early) request_next();
+      } else {
+        if (t0 + nb < t_end) issue_batch(t0 + nb, bnext, smem + pre * kTileAmpsMax);
+        cp_async_commit();
+        cp_async_wait<1>();  // this batch has landed (the next may be in flight)
+      }
       if (tid < n_groups) {  // out-of-tile axis parities per (group, tile of the batch)
         const GroupDesc& d = s_groups[tid];
         unsigned gm = 0;
@@ -1031,7 +1259,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
 #pragma unroll 1
             for (int j = 0; j < n_j && b < nvalid; ++j) {
               const uint64_t g = bb | lo | s_hi[j];
-              double2& v = tile[swz((b << k) + tid + (j << kThreadBits))];
+              double2& v = tile[eslot(b, j)];
               if ((g >> cq) & 1) {
                 v = make_double2(0.0, 0.0);
               } else {
@@ -1055,15 +1283,37 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
         double2* out = smem + spare * kTileAmpsMax;
         if (!warp_idle)
           apply_group(tile, out, k, nvalid, d, s_ops + d.op_begin, s_mats, s_gm[g], s_ttab[g]);
+        if (pending && g == 0 && !early) request_next();
         const int tmp = cur;
         cur = spare;
         spare = tmp;
         tile = out;
-        if (cta_sync)
+        if (cta_sync || (kHw && (p.debug & 8)))
           __syncthreads();
         else
           __syncwarp();  // the next sweep reads only this warp's amplitudes
       }
+      if (ts) {
+        if (pending && !early && (n_groups == 0 || (p.debug & 1))) request_next();
+        // assertion epilogue partial sums from the final buffer, then ONE
+        // thread stores the tile (TMA reads the swz_tma layout)
+        const int mq = sp.measure_q;
+        if (mq >= 0 && !(p.debug & 2)) {
+          const uint64_t base = tbase[0] | lo;
+#pragma unroll 2
+          for (int j = 0; j < n_j; ++j) {
+            const uint64_t g = base | s_hi[j];
+            if (!((g >> mq) & 1)) {
+              const double2 v = tile[eslot(0, j)];
+              msum = fma(v.x, v.x, msum);
+              msum = fma(v.y, v.y, msum);
+            }
+          }
+        }
+        fence_async_shared();  // this thread's sweep stores -> the TMA store's reads
+        __syncthreads();
+        if (tid == 0 && !(p.debug & 2)) tma_tile(true, tbase[0], cur);
+      } else {
       // shared -> global (+ assertion epilogue partial sums)
       if (loader && !(p.debug & 2)) {
         const int mq = sp.measure_q;
@@ -1075,7 +1325,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
 #pragma unroll 2
           for (int j = 0; j < n_j; ++j) {
             const uint64_t g = base | s_hi[j];
-            const double2 v = tile[swz((b << k) + tid + (j << kThreadBits))];
+            const double2 v = tile[eslot(b, j)];
             p.amps[g] = v;
             if (mq >= 0 && !((g >> mq) & 1)) {
               msum = fma(v.x, v.x, msum);
@@ -1085,11 +1335,19 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
         }
       }
       __syncthreads();  // buffer `cur` is free for the batch issued next iteration
+      }
       const int done = cur;  // next batch lives in `pre`; `done` takes the next prefetch
       cur = pre;
       pre = done;
     }
-    cp_async_wait<0>();
+    if (ts) {
+      if (tid == 0) {  // the pass's tile stores are complete before the grid barrier
+        bulk_wait0();
+        fence_async_global();
+      }
+    } else {
+      cp_async_wait<0>();
+    }
     const int mq = sp.measure_q;
     const int mslot = sp.measure_slot;
     if (mq >= 0) {
@@ -1123,6 +1381,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
       } while (seen < target);
       asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
+    if (kHw && tid == 0) fence_async_global();  // other CTAs' stores -> this CTA's TMA loads
     __syncthreads();
     if (mq >= 0) {
       if (tid < 32) {
@@ -1356,6 +1615,7 @@ struct nsb_ctx {
   cudaEvent_t tev0 = nullptr, tev1 = nullptr;  // nsb_timer_start / stop
   int sm_count = 0;
   int blocked_grid = 0;  // co-resident CTAs of k_blocked
+  bool tma_ok = false;   // the TMA instantiation is co-resident on the same grid
   int n = 0;
   uint64_t n_amps = 0;
   DevBuf<double2> amps;
@@ -1391,6 +1651,11 @@ struct nsb_plan {
   DevBuf<double> record, partials;
   DevBuf<int> fail;
   DevBuf<unsigned> bar;
+  // TMA plans: tensor maps per pass of `passes` [0] and `mma_passes` [1],
+  // encoded for the state buffer tm_amps (re-encoded if the state moves)
+  std::vector<dev::TmaPass> tm_host[2];
+  DevBuf<dev::TmaPass> tm_dev[2];
+  const double2* tm_amps[2] = {nullptr, nullptr};
   double last_ms = 0.0;
   int64_t last_launches = 0;
   // the plan's own stream for releasing its buffers: stream-ordered frees
@@ -1403,6 +1668,7 @@ struct nsb_plan {
     passes.release(); mma_passes.release(); groups.release(); ops.release();
     mats.release(); dense.release(); record.release(); partials.release();
     fail.release(); bar.release();
+    tm_dev[0].release(); tm_dev[1].release();
     if (rel) cudaStreamDestroy(rel);
   }
 };
@@ -1690,6 +1956,110 @@ void apply_matrix(nsb_ctx* c, const double* u, const int32_t* qubits, int k,
   NSB_CUDA(cudaGetLastError());
 }
 
+// ---- TMA tensor maps (planner.h "TMA tiles", dev::TmaPass) -----------------
+using TensorMapEncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                          const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                          const cuuint32_t*, CUtensorMapInterleave,
+                                          CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                          CUtensorMapFloatOOBfill);
+TensorMapEncodeTiled tensor_map_encoder() {
+  static TensorMapEncodeTiled fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    NSB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    if (!f || q != cudaDriverEntryPointSuccess)
+      throw std::runtime_error("cuTensorMapEncodeTiled is not available");
+    return reinterpret_cast<TensorMapEncodeTiled>(f);
+  }();
+  return fn;
+}
+
+// L2 sector promotion of the tile copies: the 128-byte rows are whole lines
+// already (NSB_TMA_PROMO = 0 none, 1 64B, 2 128B, 3 256B)
+CUtensorMapL2promotion tma_l2_promotion() {
+  static const int v = [] {
+    const char* e = std::getenv("NSB_TMA_PROMO");
+    return e ? std::atoi(e) : 2;
+  }();
+  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+       : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+       : v == 3 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+}
+
+// TMA passes store their tiles by TMA (1, NSB_TMA_STORE) or by the threads (0)
+int tma_store_mode() {
+  static const int v = [] {
+    const char* e = std::getenv("NSB_TMA_STORE");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
+// the tensor map of pass P over an n-qubit state at `amps` (rank 0: the
+// planner left the pass on cp.async, PassDesc::tma = 0)
+void encode_tma_pass(const PassDesc& P, int n, const double2* amps, dev::TmaPass& T) {
+  std::memset(&T, 0, sizeof T);
+  if (!P.tma) return;
+  TmaLayout L;  // the planner's choice: the dim order whose layout is P.tperm
+  if (!tma_layout(P, n, 0, L)) throw std::logic_error("TMA pass tile is not TMA-shaped");
+  const int n_orders = L.n_orders;
+  int o = 0;
+  while (std::memcmp(L.perm, P.tperm, sizeof L.perm) != 0) {
+    if (++o >= n_orders) throw std::logic_error("TMA pass copy layout not found");
+    tma_layout(P, n, o, L);
+  }
+  T.left = L.left;
+  cuuint64_t dim[5], stride[4];
+  cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
+  dim[0] = 16;  // qubits 0..2 as re/im doubles: 128 bytes
+  box[0] = 16;
+  int box_bits = 3;
+  for (int i = 1; i < L.rank; ++i) {
+    T.start[i] = static_cast<int8_t>(L.start[i]);
+    T.ebits[i] = static_cast<int8_t>(L.ebits[i]);
+    dim[i] = cuuint64_t(1) << L.ebits[i];
+    stride[i - 1] = cuuint64_t(sizeof(double2)) << L.start[i];
+    box[i] = 1u << (L.len[i] + L.gap[i]);
+    estr[i] = 1u << L.gap[i];
+    box_bits += L.len[i];
+  }
+  T.rank = static_cast<int8_t>(L.rank);
+  T.box_bits = static_cast<int8_t>(box_bits);
+  const CUresult r = tensor_map_encoder()(
+      &T.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, static_cast<cuuint32_t>(L.rank),
+      const_cast<double2*>(amps), dim, stride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_128B, tma_l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+}
+
+// device tensor maps of `passes` for the current state (plans: cached per array)
+void encode_tma_passes(const std::vector<PassDesc>& passes, int n, const double2* amps,
+                       std::vector<dev::TmaPass>& out) {
+  out.resize(passes.size());
+  for (size_t i = 0; i < passes.size(); ++i) encode_tma_pass(passes[i], n, amps, out[i]);
+}
+
+const dev::TmaPass* plan_tma(nsb_ctx* c, nsb_plan* P, const PassDesc* passes) {
+  if (!P->host.tma) return nullptr;
+  const int w = passes == P->mma_passes.ptr ? 1 : 0;
+  if (P->tm_amps[w] != c->amps.ptr || !P->tm_dev[w].ptr) {
+    encode_tma_passes(w ? P->host.mma_passes : P->host.passes, c->n, c->amps.ptr, P->tm_host[w]);
+    P->tm_dev[w].upload(P->tm_host[w].data(), P->tm_host[w].size(), c->stream, c->plan_pool);
+    P->tm_dev[w].stream = P->rel;  // released with the plan's other buffers
+    P->tm_amps[w] = c->amps.ptr;
+  }
+  return P->tm_dev[w].ptr;
+}
+
+void* blocked_kernel(bool chunk, bool tma) {
+  return chunk ? (tma ? reinterpret_cast<void*>(dev::k_blocked<true, true>)
+                      : reinterpret_cast<void*>(dev::k_blocked<true, false>))
+               : (tma ? reinterpret_cast<void*>(dev::k_blocked<false, true>)
+                      : reinterpret_cast<void*>(dev::k_blocked<false, false>));
+}
+
 // launch k_blocked over [pb, pe) of `passes` cooperatively
 void launch_blocked(nsb_ctx* c, nsb_plan* P, const PassDesc* passes, int pb, int pe, double eps,
                     int grid = 0, uint64_t cmask = 0, uint64_t cval = 0) {
@@ -1716,11 +2086,13 @@ void launch_blocked(nsb_ctx* c, nsb_plan* P, const PassDesc* passes, int pb, int
   bp.cmask = cmask;
   bp.cval = cval;
   bp.cbits = __builtin_popcountll(cmask);
+  const bool tma = P->host.tma;
+  bp.tmaps = tma && !cmask ? plan_tma(c, P, passes) : nullptr;
+  bp.tma_store = tma_store_mode();
   void* args[] = {&bp};
-  NSB_CUDA(cudaLaunchCooperativeKernel(cmask ? reinterpret_cast<void*>(dev::k_blocked<true>)
-                                             : reinterpret_cast<void*>(dev::k_blocked<false>),
-                                       dim3(grid > 0 ? grid : P->grid), dim3(kPassThreads), args,
-                                       dev::kBlockedSmemBytes, c->stream));
+  NSB_CUDA(cudaLaunchCooperativeKernel(
+      blocked_kernel(cmask != 0, tma), dim3(grid > 0 ? grid : P->grid), dim3(kPassThreads), args,
+      tma ? dev::kBlockedSmemBytesTma : dev::kBlockedSmemBytes, c->stream));
   P->last_launches += 1;
 }
 
@@ -1785,15 +2157,22 @@ int nsb_ctx_create(int32_t device, nsb_ctx** out, nsb_status* st) {
     NSB_CUDA(cudaEventCreate(&ctx->tev1));
     NSB_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
     const int smem = static_cast<int>(dev::kBlockedSmemBytes);
-    NSB_CUDA(cudaFuncSetAttribute(dev::k_blocked<false>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    NSB_CUDA(cudaFuncSetAttribute(dev::k_blocked<true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    int per_sm = 0;
-    NSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_blocked<false>,
+    const int smem_tma = static_cast<int>(dev::kBlockedSmemBytesTma);
+    for (bool chunk : {false, true})
+      for (bool tma : {false, true})
+        NSB_CUDA(cudaFuncSetAttribute(blocked_kernel(chunk, tma),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      tma ? smem_tma : smem));
+    int per_sm = 0, per_sm_tma = 0;
+    NSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_blocked<false, false>,
                                                            kPassThreads, smem));
+    NSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm_tma, dev::k_blocked<false, true>, kPassThreads, smem_tma));
     if (per_sm < 1) throw std::runtime_error("k_blocked cannot be resident");
     ctx->blocked_grid = per_sm * ctx->sm_count;
+    // TMA plans run on the same persistent grid (NSB_TMA=0 or a smaller
+    // residency: per-thread cp.async under the usual layout)
+    ctx->tma_ok = per_sm_tma == per_sm;
     ctx->scratch.alloc(4 * dev::kReduceBlocks + 64);
   });
   if (rc == NSB_OK) *out = ctx.release();
@@ -2025,6 +2404,7 @@ int nsb_plan_create_ex(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const doubl
     P->n = c->n;
     NSB_CUDA(cudaStreamCreateWithFlags(&P->rel, cudaStreamNonBlocking));
     if (flags & NSB_PLAN_EXACT) P->host.identity_budget = 0.0;
+    P->host.allow_tma = c->tma_ok;
     P->host.build(ops, n_ops, params, payloads, c->n, c->blocked_grid);
     HostPlan& H = P->host;
     {
@@ -2408,6 +2788,7 @@ int nsb_run_mma_streamed(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const dou
         auto H = std::make_unique<HostPlan>();
         try {
           H->identity_budget = n_ops ? budget * static_cast<double>(e - b) / n_ops : 0.0;
+          H->allow_tma = c->tma_ok;
           H->build_segment(ops + b, e - b, params, payloads, c->n, c->blocked_grid);
         } catch (...) {
           errs[s] = std::current_exception();
@@ -2421,6 +2802,7 @@ int nsb_run_mma_streamed(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const dou
       }
     });
     struct PartDev {
+      DevBuf<dev::TmaPass> tmaps;  // TMA parts: tensor maps per pass
       DevBuf<PassDesc> passes;
       DevBuf<GroupDesc> groups;
       DevBuf<GateOp> ops;
@@ -2442,7 +2824,7 @@ int nsb_run_mma_streamed(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const dou
       return e ? std::atoi(e) : 0;
     }();
     int grid = 0;
-    auto launch = [&](PartDev& d, int count) {
+    auto launch = [&](PartDev& d, int count, bool tma) {
       dev::BlockedParams bp;
       bp.amps = c->amps.ptr;
       bp.n = c->n;
@@ -2460,11 +2842,13 @@ int nsb_run_mma_streamed(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const dou
       bp.debug = debug;
       bp.cmask = bp.cval = 0;
       bp.cbits = 0;
+      bp.tmaps = tma ? d.tmaps.ptr : nullptr;
+      bp.tma_store = tma_store_mode();
       NSB_CUDA(cudaMemsetAsync(bar.ptr, 0, sizeof(unsigned), c->stream));
       void* args[] = {&bp};
-      NSB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::k_blocked<false>), dim3(grid),
-                                           dim3(kPassThreads), args, dev::kBlockedSmemBytes,
-                                           c->stream));
+      NSB_CUDA(cudaLaunchCooperativeKernel(
+          blocked_kernel(false, tma), dim3(grid), dim3(kPassThreads), args,
+          tma ? dev::kBlockedSmemBytesTma : dev::kBlockedSmemBytes, c->stream));
     };
     std::vector<double> scale(std::max<int64_t>(n_meas, 1), 1.0);
     double running = 1.0;
@@ -2540,7 +2924,12 @@ int nsb_run_mma_streamed(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const dou
           d.ops.upload(H.gate_ops.data(), H.gate_ops.size(), c->stream, pool);
           d.mats.upload(reinterpret_cast<const double2*>(H.matrices.data()),
                         H.matrices.size() / 2, c->stream, pool);
-          launch(d, static_cast<int>(mp.size()));
+          if (H.tma) {
+            std::vector<dev::TmaPass> tm;
+            encode_tma_passes(mp, c->n, c->amps.ptr, tm);
+            d.tmaps.upload(tm.data(), tm.size(), c->stream, pool);
+          }
+          launch(d, static_cast<int>(mp.size()), H.tma);
         }
         if (s > 0) {  // planned parts already uploaded: release their host programs
           std::lock_guard<std::mutex> lk(mu);
@@ -2568,6 +2957,7 @@ int nsb_run_mma_streamed(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const dou
     if (assert_probs)
       for (int64_t i = 0; i < n_ok; ++i) assert_probs[i] = rec[i];
     for (PartDev& d : dev) {  // stream-ordered frees on the context stream
+      d.tmaps.release();
       d.passes.release();
       d.groups.release();
       d.ops.release();

@@ -292,6 +292,84 @@ double default_identity_budget() {
   return b;
 }
 
+bool tma_layout(const PassDesc& P, int n, int order, TmaLayout& L) {
+  L = TmaLayout();
+  if (P.k != kTileQubitsMax || P.tq[0] != 0 || P.tq[1] != 1 || P.tq[2] != 2 || n > kTmaMaxQubits)
+    return false;
+  struct Run {
+    int s, len, pos;  // lowest qubit, length, tile-local position of its lowest bit
+  };
+  Run runs[8];
+  int nr = 0;
+  for (int b = 3; b < P.k;) {
+    int e = b + 1;
+    while (e < P.k && P.tq[e] == P.tq[e - 1] + 1) ++e;
+    runs[nr++] = {P.tq[b], e - b, b};
+    b = e;
+  }
+  // the dims: the longest runs (fewest copies), four, or three and a gap dim
+  int idx[8];
+  for (int i = 0; i < nr; ++i) idx[i] = i;
+  std::stable_sort(idx, idx + nr, [&](int a, int b) { return runs[a].len > runs[b].len; });
+  int nd = std::min(nr, 4);
+  bool gap_dim = false;
+  int stride_gap = 0;
+  for (;;) {
+    int low = 0;
+    for (int i = 1; i < nd; ++i)
+      if (runs[idx[i]].s < runs[idx[low]].s) low = i;
+    const Run& r = runs[idx[low]];
+    gap_dim = r.s > 3 && !(r.s - 3 <= 3 && r.len + r.s - 3 <= 8);
+    stride_gap = r.s > 3 && !gap_dim ? r.s - 3 : 0;
+    if (!gap_dim || nd + 1 <= 4) break;
+    --nd;  // make room for the gap dim
+  }
+  // coordinate ranges (qubit order): dim of run j spans [start_j, next start)
+  int sel[4];
+  for (int i = 0; i < nd; ++i) sel[i] = idx[i];
+  std::sort(sel, sel + nd, [&](int a, int b) { return runs[a].s < runs[b].s; });
+  int cstart[8], cend[8];
+  for (int i = 0; i < nd; ++i) {
+    cstart[sel[i]] = runs[sel[i]].s;
+    cend[sel[i]] = i + 1 < nd ? runs[sel[i + 1]].s : n;
+  }
+  if (stride_gap) cstart[sel[0]] = 3;
+  // dim order in shared memory: permutation `order` of the run dims
+  int ord[4];
+  for (int i = 0; i < nd; ++i) ord[i] = sel[i];
+  L.n_orders = 1;
+  for (int i = 2; i <= nd; ++i) L.n_orders *= i;
+  for (int i = 0; i < order % L.n_orders; ++i) std::next_permutation(ord, ord + nd);
+  L.len[0] = 3;
+  L.rank = 1;
+  for (int b = 0; b < 3; ++b) L.perm[b] = static_cast<int8_t>(b);
+  int pos = 3;
+  for (int i = 0; i < nd; ++i) {
+    const Run& r = runs[ord[i]];
+    L.start[L.rank] = cstart[ord[i]];
+    L.ebits[L.rank] = cend[ord[i]] - cstart[ord[i]];
+    L.len[L.rank] = r.len;
+    L.gap[L.rank] = cstart[ord[i]] < r.s ? r.s - cstart[ord[i]] : 0;
+    ++L.rank;
+    for (int t = 0; t < r.len; ++t) L.perm[r.pos + t] = static_cast<int8_t>(pos++);
+  }
+  if (gap_dim) {  // box of one over qubits 3 .. lowest run - 1
+    L.start[L.rank] = 3;
+    L.ebits[L.rank] = runs[sel[0]].s - 3;
+    L.len[L.rank] = 0;
+    ++L.rank;
+  }
+  bool in_dims[8] = {};
+  for (int i = 0; i < nd; ++i) in_dims[sel[i]] = true;
+  for (int j = 0; j < nr; ++j)  // the other runs: copy index bits, ascending
+    if (!in_dims[j])
+      for (int t = 0; t < runs[j].len; ++t) {
+        L.left |= uint64_t(1) << (runs[j].s + t);
+        L.perm[runs[j].pos + t] = static_cast<int8_t>(pos++);
+      }
+  return true;
+}
+
 static int choose_tile_qubits(int n, int workers) {
   if (n <= kTileQubitsMax) return n;
   for (int k = kTileQubitsMax; k >= 9; --k) {
@@ -308,6 +386,8 @@ namespace {
 
 inline int parity32(uint32_t x) { return __builtin_popcount(x) & 1; }
 inline uint32_t swz11(uint32_t l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u); }
+// the TMA layout of a tile at the pass edges (planner.h, swz_tma)
+inline uint32_t swz_edge(uint32_t l) { return l ^ ((l >> 3) & 7u); }
 
 // basis of {v in GF(2)^k : parity(f_i & v) = 0 for all i}
 struct Basis {
@@ -779,7 +859,19 @@ bool warp_local(const OpenGroup& G, uint32_t wm) {
   return true;
 }
 
-void finish_group(OpenGroup& G, int k, GroupDesc& d, uint32_t wm) {
+// load_edge / store_edge (a TMA pass's copy layout, TmaLayout::perm): the
+// group reads the tile as TMA left it / writes the layout the TMA store reads
+// (swz_tma of the permuted index instead of swz11 on that side)
+void finish_group(OpenGroup& G, int k, GroupDesc& d, uint32_t wm,
+                  const int8_t* load_edge = nullptr, const int8_t* store_edge = nullptr) {
+  auto edge = [k](const int8_t* perm, uint32_t l) {
+    uint32_t x = l & ~((1u << k) - 1);
+    for (int i = 0; i < k; ++i)
+      if (l >> i & 1) x |= 1u << perm[i];
+    return swz_edge(x);
+  };
+  auto swz_ld = [&](uint32_t l) { return load_edge ? edge(load_edge, l) : swz11(l); };
+  auto swz_st = [&](uint32_t l) { return store_edge ? edge(store_edge, l) : swz11(l); };
   const bool local = wm != 0;
   while (G.nax < 3) {  // pad with a free axis of the tile (outside the warp positions)
     uint32_t f[3 + kWarpBits];
@@ -830,31 +922,97 @@ void finish_group(OpenGroup& G, int k, GroupDesc& d, uint32_t wm) {
     for (int i = nw; i < C.n; ++i) K.v[K.n++] = C.v[i];
     C = K;
   }
-  // thread bits 0..2 first: basis vectors whose swizzled bank groups are independent
-  uint32_t phis[3];
-  int placed = 0;
-  for (int j = 0; j < C.n && placed < 3; ++j) {
-    uint32_t ph = swz11(C[j]) & 7u;
-    for (int i = 0; i < placed; ++i)
-      if (ph >> __builtin_ctz(phis[i]) & 1) ph ^= phis[i];
-    if (!ph) continue;
-    for (int i = 0; i < placed; ++i)
-      if (phis[i] >> __builtin_ctz(ph) & 1) phis[i] ^= ph;
-    phis[placed] = ph;
-    std::swap(C[placed], C[j]);
-    ++placed;
-  }
-  if (local)
-    for (int j = kWarpBits - 1; j >= 0; --j) C.insert_at(5, cw[j]);
   auto rmap = [&](uint32_t u) {  // R u on tile-local bits; batch bits pass through
     uint32_t out = u & ~((1u << k) - 1);
     for (int i = 0; i < k; ++i)
       if (u >> i & 1) out ^= G.rcol[i];
     return out;
   };
+  // Thread bits 0..2 first: a quarter-warp (8 lanes of a 128-bit access)
+  // spans their combinations, so it hits 8 distinct 16-byte bank groups iff
+  // their bank images are independent -- on the load side (read map, load
+  // swizzle) and on the store side alike.  Greedy over span(C): the basis
+  // vectors first, then every combination, each pick independent of the
+  // earlier ones on as many sides as possible (round 2; before, the store side
+  // only, which left TMA plans' swz_tma edges with 3x the conflicts).
+  {
+    auto bank_ld = [&](uint32_t v) { return swz_ld(rmap(v)) & 7u; };
+    auto bank_st = [&](uint32_t v) { return swz_st(v) & 7u; };
+    struct Span3 {  // reduced basis of a subspace of GF(2)^3 (pivot = lowest bit)
+      uint32_t r[3];
+      int n = 0;
+      uint32_t reduce(uint32_t x) const {
+        for (int i = 0; i < n; ++i)
+          if (x >> __builtin_ctz(r[i]) & 1) x ^= r[i];
+        return x;
+      }
+      void add(uint32_t x) {
+        x = reduce(x);
+        if (!x) return;
+        for (int i = 0; i < n; ++i)
+          if (r[i] >> __builtin_ctz(x) & 1) r[i] ^= x;
+        r[n++] = x;
+      }
+    } sl, ss;
+    struct SpanK {  // reduced basis of the picked vectors in tile space
+      uint32_t r[16];
+      int n = 0;
+      uint32_t reduce(uint32_t x) const {
+        for (int i = 0; i < n; ++i)
+          if (x >> (31 - __builtin_clz(r[i])) & 1) x ^= r[i];
+        return x;
+      }
+      void add(uint32_t x) {
+        x = reduce(x);
+        if (x) r[n++] = x;
+      }
+    } picked_span;
+    uint32_t picked[3];
+    int np = 0;
+    const int nk = C.n;
+    for (int step = 0; step < 3 && step < nk; ++step) {
+      int best = -1;
+      uint32_t best_v = 0;
+      auto consider = [&](uint32_t v) {
+        if (!v || !picked_span.reduce(v)) return;
+        const int sc = (sl.reduce(bank_ld(v)) ? 1 : 0) + (ss.reduce(bank_st(v)) ? 1 : 0);
+        if (sc > best) {
+          best = sc;
+          best_v = v;
+        }
+      };
+      for (int i = 0; i < nk && best < 2; ++i) consider(C[i]);
+      if (best < 2 && nk <= 8)
+        for (uint32_t m = 1; m < (1u << nk) && best < 2; ++m) {
+          uint32_t v = 0;
+          for (int i = 0; i < nk; ++i)
+            if (m >> i & 1) v ^= C[i];
+          consider(v);
+        }
+      if (best <= 0) break;  // nothing independent on either side
+      picked[np++] = best_v;
+      picked_span.add(best_v);
+      sl.add(bank_ld(best_v));
+      ss.add(bank_st(best_v));
+    }
+    if (np) {  // basis of span(C) that starts with the picks
+      Basis B;
+      SpanK sp = picked_span;
+      for (int i = 0; i < np; ++i) B.v[B.n++] = picked[i];
+      for (int i = 0; i < nk; ++i)
+        if (sp.reduce(C[i])) {
+          sp.add(C[i]);
+          B.v[B.n++] = C[i];
+        }
+      if (B.n != nk) throw std::logic_error("thread basis lost a dimension");
+      C = B;
+    }
+  }
+  if (local)
+    for (int j = kWarpBits - 1; j >= 0; --j) C.insert_at(5, cw[j]);
   for (int i = 0; i < 3; ++i) {
-    d.am[i] = static_cast<uint16_t>(swz11(G.ax[i].m));         // final basis (stores)
-    d.ram[i] = static_cast<uint16_t>(swz11(rmap(G.ax0[i].m)));  // load basis
+    d.am[i] = static_cast<uint16_t>(swz_st(G.ax[i].m));          // final basis (stores)
+    d.ram[i] = static_cast<uint16_t>(swz_ld(rmap(G.ax0[i].m)));  // load basis
   }
   // store parity bits: final row j = sum_i M_ji (load row i), M_ji = r_j . m0_i
   d.kmat = 0;
@@ -868,13 +1026,13 @@ void finish_group(OpenGroup& G, int k, GroupDesc& d, uint32_t wm) {
   const int cb = k - 3;
   for (int b = 0; b < kIndexBits; ++b) {
     if (na == 4 && b == kThreadBits) {  // the octet index: axis 3 (load), its final axis (store)
-      d.tcol[b] = static_cast<uint16_t>(swz11(G.ax[3].m));
-      d.rtcol[b] = static_cast<uint16_t>(swz11(rmap(G.ax0[3].m)));
+      d.tcol[b] = static_cast<uint16_t>(swz_st(G.ax[3].m));
+      d.rtcol[b] = static_cast<uint16_t>(swz_ld(rmap(G.ax0[3].m)));
       continue;
     }
     const uint32_t v = b < cb ? C[b] : (1u << (k + b - cb));  // then tile-in-batch bits
-    d.tcol[b] = static_cast<uint16_t>(swz11(v));
-    d.rtcol[b] = static_cast<uint16_t>(swz11(rmap(v)));
+    d.tcol[b] = static_cast<uint16_t>(swz_st(v));
+    d.rtcol[b] = static_cast<uint16_t>(swz_ld(rmap(v)));
   }
 }
 
@@ -911,6 +1069,7 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
       try {  // the identity budget is shared out in proportion to the part's ops
         parts[s].identity_budget =
             total_budget * static_cast<double>(e - b) / static_cast<double>(n_ops);
+        parts[s].allow_tma = allow_tma;
         parts[s].build_serial(ops + b, e - b, params, payloads, n, workers);
       } catch (...) {
         errors[s] = std::current_exception();
@@ -1003,6 +1162,11 @@ void HostPlan::build_serial(const nsb_op* ops, int64_t n_ops, const double* para
   low_qubits = n <= kL2ResidentQubits ? kLowQubitsL2 : kLowQubits;
   if (const char* e = std::getenv("NSB_LOW_QUBITS")) low_qubits = std::atoi(e);  // tuning
   if (const char* e = std::getenv("NSB_NO_GROUP_FUSION")) fuse_groups = std::atoi(e) == 0;
+  // TMA tiles (planner.h): whenever every tile holds qubits 0..2 at full size
+  // (the HBM policy, n > kL2ResidentQubits, or NSB_LOW_QUBITS >= 3); NSB_TMA=0 off
+  tma = allow_tma && low_qubits >= kLowQubits && k == kTileQubitsMax && n > k &&
+        n <= kTmaMaxQubits;
+  if (const char* e = std::getenv("NSB_TMA")) tma = tma && std::atoi(e) != 0;
   blocked = n >= 6;
   // NSB_FORCE_PER_OP=1: every gate is its own item executed by the per-op
   // kernels (k_apply1 / k_apply2 / k_applyk, oracle-tested one by one) -- the
@@ -1359,6 +1523,7 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
     // barrier is needed anyway.  Dynamic programming over the groups picks
     // the assignment with the most warp-local sweep transitions.
     std::vector<uint32_t> wsel(closed.size(), 0u);
+    bool pt = false;  // this pass's tiles move by TMA (planner.h "TMA tiles")
     if (k - 3 >= kThreadBits && !closed.empty()) {  // warp bits of the octet index are tile-local
       std::vector<uint32_t> cands;
       for (uint32_t wm = 1; wm < (1u << k); ++wm)
@@ -1450,6 +1615,43 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
         H.mats = std::move(mats_out);
       }
     }
+    if (tma) {
+      // the first copy-layout order whose edge sweeps keep all eight bank
+      // groups under swz_tma (thread bits 0..2 independent mod the swizzle);
+      // none, or too many copies: this pass stays on cp.async and swz
+      auto rank3 = [](const uint16_t* v) {
+        uint32_t r[3];
+        int nr = 0;
+        for (int i = 0; i < 3; ++i) {
+          uint32_t x = v[i] & 7u;
+          for (int j = 0; j < nr; ++j)
+            if (x >> __builtin_ctz(r[j]) & 1) x ^= r[j];
+          if (!x) continue;
+          for (int j = 0; j < nr; ++j)
+            if (r[j] >> __builtin_ctz(x) & 1) r[j] ^= x;
+          r[nr++] = x;
+        }
+        return nr;
+      };
+      TmaLayout L;
+      if (tma_layout(P, n, 0, L) && (1 << __builtin_popcountll(L.left)) <= kTmaMaxCopies) {
+        const int n_orders = L.n_orders;
+        for (int o = 0; o < n_orders && !pt; ++o) {
+          tma_layout(P, n, o, L);
+          pt = true;
+          if (!closed.empty()) {
+            const size_t last = closed.size() - 1;
+            OpenGroup f = closed.front(), l = closed.back();
+            GroupDesc df{}, dl{};
+            finish_group(f, k, df, wsel.front(), L.perm, last == 0 ? L.perm : nullptr);
+            finish_group(l, k, dl, wsel.back(), last == 0 ? L.perm : nullptr, L.perm);
+            pt = rank3(df.rtcol) == 3 && rank3(dl.tcol) == 3;
+          }
+          if (pt) std::memcpy(P.tperm, L.perm, sizeof P.tperm);
+        }
+      }
+    }
+    P.tma = pt ? 1 : 0;
     for (size_t g = 0; g < closed.size(); ++g) {
       OpenGroup& H = closed[g];
       GroupDesc d{};
@@ -1462,8 +1664,19 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
       }
       out.matrices.insert(out.matrices.end(), H.mats.begin(), H.mats.end());
       const uint32_t wm = wsel[g];
-      const bool next = g + 1 < closed.size() && wm && wsel[g + 1] == wm;
-      finish_group(H, k, d, wm);
+      // A warp-local transition g -> g+1 needs each warp's slots to stay its
+      // own in BOTH buffers: g+1 overwrites the buffer g read.  Across a TMA
+      // edge (g = first: its loads are in the copy layout, g+1's stores on swz;
+      // g+1 = last: the reverse) the two layouts map a warp's amplitudes to the
+      // same slots only if its split positions are unswizzled (>= 3) and not
+      // moved by the copy layout's permutation.
+      bool split_fixed = true;
+      for (int b = 0; b < k; ++b)
+        if (wm >> b & 1) split_fixed = split_fixed && b >= 3 && P.tperm[b] == b;
+      const bool edge = pt && (g == 0 || g + 2 == closed.size());
+      const bool next = g + 1 < closed.size() && wm && wsel[g + 1] == wm && !(edge && !split_fixed);
+      finish_group(H, k, d, wm, pt && g == 0 ? P.tperm : nullptr,
+                   pt && g + 1 == closed.size() ? P.tperm : nullptr);
       if (!next) d.n_ops_sync |= 128;
       if (next) ++out.n_warp;
       for (const GateOp& o : H.ops) out.n_axis += o.cls == kPermute && o.pat == kPatQ0;
@@ -1730,6 +1943,7 @@ extern "C" int nsb_host_plan_view(const void* plan, nsb_plan_view* v) {
   std::memset(v, 0, sizeof(*v));
   v->n_qubits = H->n_qubits;
   v->tile_qubits = H->tile_qubits;
+  v->tma_edges = H->tma ? 1 : 0;
   v->mma_ok = H->mma_ok;
   v->n_measures = static_cast<int32_t>(H->n_measures);
   v->pass_desc_bytes = sizeof(nsb::PassDesc);

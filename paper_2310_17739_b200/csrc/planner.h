@@ -54,6 +54,22 @@ constexpr int kL2ResidentQubits = 22;
 // still pay: deep21 measured 862 ms with 2, 878 ms with 1, 924 ms with 3.
 constexpr int kLowQubitsL2 = 2;
 constexpr int kMaxQubits = 40;
+// TMA tiles.  When every tile holds qubits 0..2 at full size (the HBM
+// policy), a tile moves between HBM and shared memory by cp.async.bulk.tensor:
+// the tile's qubit runs are the dims of a <= 5-D tensor map (per pass; qubits
+// 0..2 and re/im the 128-byte inner dim, runs beyond five dims as separate
+// copies), landing under the hardware's 128-byte swizzle
+//   swz_tma(l) = l ^ ((l >> 3) & 7)      (16-byte slots, 1024-byte aligned)
+// instead of swz.  Both are linear over XOR, so only the pass edges change:
+// the FIRST group of a pass loads with swz_tma offsets, the LAST one stores
+// with them (the TMA store reads that layout); the sweeps in between keep swz.
+// Coordinates are int32 and a dim spans at most 2^31 values: n <= 34.
+// Per pass, only where it pays: a tile of few copies (a copy costs the TMA
+// unit a fixed few hundred cycles) whose first / last sweep keeps all eight
+// 16-byte bank groups under swz_tma (the hardware swizzle mixes slot bits
+// 3..5 only, so axes on tile bits j and j + 3 alias); else cp.async and swz.
+constexpr int kTmaMaxQubits = 34;
+constexpr int kTmaMaxCopies = 2;
 
 // Payload classes, chosen by exact-zero structure (skipping an exact zero
 // term is bit-identical to multiplying by it).
@@ -195,9 +211,12 @@ struct PassDesc {         // 112 bytes
   int32_t measure_slot;   // index into the probability record
   int32_t collapse_q;     // prologue: collapse onto q=0 using the carried p0
   int32_t collapse_slot;
-  int32_t pad;
+  int32_t tma;            // 1: tiles move by TMA; the first group loads and the last
+                          // group stores under swz_tma (TMA plans, "TMA tiles")
   int8_t tq[16];          // tile-local bit i -> physical qubit (ascending)
-  int8_t oq[48];          // tile-index bit j -> physical qubit (ascending)
+  int8_t oq[32];          // tile-index bit j -> physical qubit (ascending)
+  int8_t tperm[16];       // TMA passes: tile-local bit i -> bit of the copy layout in
+                          // shared memory (before swz_tma); the order of the map's dims
 };
 static_assert(sizeof(PassDesc) == 112, "PassDesc layout");
 

@@ -77,6 +77,10 @@ struct HostPlan {
   int64_t n_fused_group_ops = 0;  // gate ops removed by group fusion (fuse_group)
   int64_t n_axis_swaps = 0;       // register-axis exchanges of four-axis groups
   bool fuse_groups = true;      // NSB_NO_GROUP_FUSION=1 turns group fusion off
+  // tiles move by TMA (planner.h "TMA tiles"): the first group of every pass
+  // loads under swz_tma, the last one stores under it
+  bool tma = false;
+  bool allow_tma = true;  // set by the caller: the device runs the TMA kernel
   // Gates within rounding of a scalar identity s I (e.g. the fused H.H / S.Sdg
   // products between consecutive JW terms, 1 + 2^-52 on the diagonal) are not
   // executed.  Their scalar is kept: the reference's state carries the product
@@ -125,6 +129,26 @@ struct HostPlan {
   void schedule_run(std::vector<PhysGate>& run, int k);
   void build_mma();
 };
+
+// The TMA copy layout of a pass's tile (planner.h "TMA tiles", dev::TmaPass):
+// dim 0 = qubits 0..2; dims 1.. = the (up to four) longest runs of consecutive
+// tile qubits, listed in a chosen order -- the order of their bits in shared
+// memory -- each dim's coordinate spanning its run and the out-of-tile qubits
+// above it (the lowest one starting at qubit 3: a gap of <= 3 qubits below its
+// run is a traversal stride, a longer one takes a dim with a box of one);
+// the other runs are `left`, coordinate bits of the dim below them, one copy
+// per value, their bits on top of the copy layout.  perm: tile-local bit ->
+// bit of the copy layout.  `order` < n_orders picks the order of the run dims.
+// False: the pass's tile is not TMA-shaped (k < kTileQubitsMax, qubits 0..2
+// not all tiled, n > kTmaMaxQubits).
+struct TmaLayout {
+  int rank = 0;                      // dims, dim 0 included
+  int start[5] = {0}, ebits[5] = {0}, len[5] = {0}, gap[5] = {0};
+  uint64_t left = 0;
+  int8_t perm[16] = {0};
+  int n_orders = 0;
+};
+bool tma_layout(const PassDesc& P, int n, int order, TmaLayout& L);
 
 void plan_info(const HostPlan& H, nsb_plan_info* info);
 double default_identity_budget_value();  // NSB_IDENTITY_BUDGET or 3e-11

@@ -20,8 +20,8 @@ from paper_2310_17739_b200 import _native as N
 PASS_DT = np.dtype([("group_begin", "<i4"), ("group_end", "<i4"), ("op_begin", "<i4"),
                     ("op_end", "<i4"), ("mat_begin", "<i4"), ("mat_count", "<i4"), ("k", "<i4"),
                     ("measure_q", "<i4"), ("measure_slot", "<i4"), ("collapse_q", "<i4"),
-                    ("collapse_slot", "<i4"), ("pad", "<i4"), ("tq", "i1", (16,)),
-                    ("oq", "i1", (48,))])
+                    ("collapse_slot", "<i4"), ("tma", "<i4"), ("tq", "i1", (16,)),
+                    ("oq", "i1", (32,)), ("tperm", "i1", (16,))])
 GROUP_DT = np.dtype([("am", "<u2", (3,)), ("ram", "<u2", (3,)), ("tcol", "<u2", (8,)),
                      ("rtcol", "<u2", (8,)), ("op_begin", "u1"), ("n_ops_sync", "u1"),
                      ("kmat", "<u2"), ("r_out", "<u8", (4,))], align=True)
@@ -55,6 +55,7 @@ class HostPlan:
         assert v.pass_desc_bytes == PASS_DT.itemsize
         assert v.group_desc_bytes == GROUP_DT.itemsize and v.gate_op_bytes == OP_DT.itemsize
         self.n, self.k, self.mma_ok, self.n_measures = v.n_qubits, v.tile_qubits, v.mma_ok, v.n_measures
+        self.tma = bool(v.tma_edges)
 
         def arr(p, count, dt):
             if count == 0:
@@ -97,6 +98,13 @@ def _mix2(x, y, m):
 
 def _swz(l):
     return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7)
+
+
+def _swz_edge(l):
+    """planner.h swz_tma: the 128-byte TMA swizzle a tile is loaded / stored
+    under at the pass edges of a TMA plan (first group's loads, last group's
+    stores)."""
+    return l ^ ((l >> 3) & 7)
 
 
 def _reg_cx(x, j, k):
@@ -218,7 +226,7 @@ def _check() -> bool:
     return os.environ.get("NSB_PLAN_EXEC_CHECK", "1") != "0"
 
 
-def _apply_group(B, G, ops, mats, tbases, k, nvalid):
+def _apply_group(B, G, ops, mats, tbases, k, nvalid, u_load=_swz, u_store=_swz):
     """One octet sweep over a batch B (nvalid tiles of 2^k stored back to
     back), enumerated exactly as k_blocked's apply_group: swizzled shared-
     memory addresses, un-swizzled here (swz is an involution) to index B."""
@@ -245,7 +253,6 @@ def _apply_group(B, G, ops, mats, tbases, k, nvalid):
                 ks ^= kl[i]
         a ^= ks * am[j]
     am, ram = am[:3], ram[:3]
-    U = _swz
     st = [a ^ (am[0] if c & 1 else 0) ^ (am[1] if c & 2 else 0) ^ (am[2] if c & 4 else 0)
           for c in range(8)]
     ld = [r ^ (ram[0] if c & 1 else 0) ^ (ram[1] if c & 2 else 0) ^ (ram[2] if c & 4 else 0)
@@ -257,18 +264,19 @@ def _apply_group(B, G, ops, mats, tbases, k, nvalid):
         assert len(np.unique(np.concatenate(ld))) == 8 * n_act
         n_warps = THREADS // 32
         warp = (t >> 5) & (n_warps - 1)  # octet-index bits 5 .. kThreadBits-1
-        loads = [np.sort(np.concatenate([U(l)[warp == w] for l in ld])) for w in range(n_warps)]
-        stores = [np.sort(np.concatenate([U(s_)[warp == w] for s_ in st])) for w in range(n_warps)]
-    x = [S[U(l)] for l in ld]
+        # physical shared-memory slots per warp (the kernel's addresses)
+        loads = [np.sort(np.concatenate([l[warp == w] for l in ld])) for w in range(n_warps)]
+        stores = [np.sort(np.concatenate([s_[warp == w] for s_ in st])) for w in range(n_warps)]
+    x = [S[u_load(l)] for l in ld]
     o0 = int(G["op_begin"])
     for op in ops[o0:o0 + (int(G["n_ops_sync"]) & 127)]:
         _gate(x, op, mats[int(op["mat"]):])
     for s, v in zip(st, x):
-        B[U(s)] = v
+        B[u_store(s)] = v
     return loads, stores
 
 
-def _apply_group_batches(Bs, G, ops, mats, tbs, k, nvalid):
+def _apply_group_batches(Bs, G, ops, mats, tbs, k, nvalid, u_load=_swz, u_store=_swz):
     """_apply_group on every batch at once: Bs (n_batches, nvalid << k),
     tbs (n_batches, nvalid) tile bases."""
     cb = k - 3
@@ -296,15 +304,14 @@ def _apply_group_batches(Bs, G, ops, mats, tbs, k, nvalid):
                 ks ^= kl[i]
         a ^= ks * am[j]
     am, ram = am[:3], ram[:3]
-    U = _swz
-    x = [np.take_along_axis(Bs, U(r ^ (ram[0] if c & 1 else 0) ^ (ram[1] if c & 2 else 0)
+    x = [np.take_along_axis(Bs, u_load(r ^ (ram[0] if c & 1 else 0) ^ (ram[1] if c & 2 else 0)
                                     ^ (ram[2] if c & 4 else 0)), axis=1) for c in range(8)]
     o0 = int(G["op_begin"])
     for op in ops[o0:o0 + (int(G["n_ops_sync"]) & 127)]:
         _gate(x, op, mats[int(op["mat"]):])
     for c in range(8):
         st = a ^ (am[0] if c & 1 else 0) ^ (am[1] if c & 2 else 0) ^ (am[2] if c & 4 else 0)
-        np.put_along_axis(Bs, U(st), x[c], axis=1)
+        np.put_along_axis(Bs, u_store(st), x[c], axis=1)
 
 
 def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12, workers=148,
@@ -316,6 +323,24 @@ def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12, workers=1
     n = plan.n
     rec = {}
     fast = not _check()
+
+    def edges(P, gi, n_groups):
+        """(load, store) slot -> tile-local index maps of group gi: in a TMA pass
+        the first group loads and the last stores in the copy layout, slot =
+        swz_tma(perm(l)) (PassDesc.tperm), un-permuted here."""
+        if not int(P["tma"]):
+            return _swz, _swz
+        k = int(P["k"])
+        perm = [int(x) for x in P["tperm"][:k]]
+
+        def u_edge(x):
+            y = _swz_edge(x)
+            out = y & ~((1 << k) - 1)
+            for i in range(k):
+                out = out | (((y >> perm[i]) & 1) << i)
+            return out
+        return (u_edge if gi == 0 else _swz), (u_edge if gi == n_groups - 1 else _swz)
+
     for P in passes:
         k = int(P["k"])
         lidx = _scatter(np.arange(1 << k, dtype=np.int64), P["tq"][:k])
@@ -340,8 +365,9 @@ def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12, workers=1
             B = state[idx]
             if cq >= 0:
                 B = np.where((idx >> cq) & 1, 0.0, B * (1.0 / np.sqrt(carry_p0)))
-            for G in groups:
-                _apply_group_batches(B, G, pops, block, tbs, k, nv)
+            for gi, G in enumerate(groups):
+                sw = edges(P, gi, len(groups))
+                _apply_group_batches(B, G, pops, block, tbs, k, nv, *sw)
             state[idx] = B
         for cta in range(0 if fast else min(workers, n_tiles)):
             t_begin = cta * per + min(cta, extra)
@@ -353,13 +379,17 @@ def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12, workers=1
                 B = state[idx]
                 if cq >= 0:
                     B = np.where((idx >> cq) & 1, 0.0, B * (1.0 / np.sqrt(carry_p0)))
-                prev = None
-                for G in groups:
-                    loads, stores = _apply_group(B, G, pops, block, tbs, k, nvalid)
-                    if prev is not None and loads is not None:  # __syncwarp only: each warp reads its own writes
+                prev = None  # (loads, stores) of the previous sweep when only __syncwarp follows it
+                for gi, G in enumerate(groups):
+                    sw = edges(P, gi, len(groups))
+                    loads, stores = _apply_group(B, G, pops, block, tbs, k, nvalid, *sw)
+                    if prev is not None and loads is not None:
                         for w in range(len(loads)):
-                            assert np.array_equal(loads[w], prev[w])
-                    prev = stores if int(G["n_ops_sync"]) >> 7 == 0 else None
+                            # each warp reads its own writes (RAW) and overwrites
+                            # only slots it read itself in the other buffer (WAR)
+                            assert np.array_equal(loads[w], prev[1][w])
+                            assert np.array_equal(stores[w], prev[0][w])
+                    prev = (loads, stores) if int(G["n_ops_sync"]) >> 7 == 0 else None
                 state[idx] = B
         mq = int(P["measure_q"])
         if mq >= 0:

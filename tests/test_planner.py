@@ -10,7 +10,7 @@ import pytest
 import nucsim_oracle as O
 import plan_exec as PE
 from circuit_io import oracle_from_circuit, to_circuit
-from paper_2310_17739_b200 import fuse_pipeline
+from paper_2310_17739_b200 import Circuit, Gate, fuse_pipeline
 from paper_2310_17739_b200._pack import pack
 from test_engine_gpu import ladder_circuit, random_filter_like
 
@@ -135,6 +135,8 @@ def test_hbm_tile_policy_filter_workload(monkeypatch, n, low, tile):
     exe = wl.executable(fops)
     plan = PE.HostPlan(exe, wl.params, pool, n, 148)
     assert plan.k == tile
+    # full tiles holding qubits 0..2 move by TMA: pass-edge groups on swz_tma
+    assert plan.tma == (low >= 3 and tile == 11)
     for p in plan.mma_passes:
         tq = set(int(x) for x in p["tq"][: int(p["k"])])
         assert set(range(low)) <= tq, "tile lacks the always-tiled low qubits"
@@ -144,10 +146,12 @@ def test_hbm_tile_policy_filter_workload(monkeypatch, n, low, tile):
     assert np.linalg.norm(state - want) / np.linalg.norm(want) < 1e-10
 
 
-@pytest.mark.parametrize("n,tile", [(14, 11), (16, 10)])
-def test_hbm_tile_policy_ladders(monkeypatch, n, tile):
+@pytest.mark.parametrize("n,tile,tma", [(14, 11, "1"), (14, 11, "0"), (16, 10, "1"),
+                                        (17, 11, "1")])
+def test_hbm_tile_policy_ladders(monkeypatch, n, tile, tma):
     monkeypatch.setenv("NSB_LOW_QUBITS", "3")
     monkeypatch.setenv("NSB_TILE_QUBITS", str(tile))
+    monkeypatch.setenv("NSB_TMA", tma)
     rng = np.random.default_rng(900 + n)
     c = ladder_circuit(rng, n, 14, blocks=2)
     check(fuse_pipeline(c)[0])
@@ -161,9 +165,40 @@ def test_default_policy_switches_at_l2_size():
         wl = W.layered_workload(n, 1, 5)
         fops, pool, _ = W.fuse_packed(wl.ops, wl.params, wl.payloads)
         plan = PE.HostPlan(fops, wl.params, pool, n, 296)
+        assert plan.tma == (low == 3)
         for p in plan.mma_passes:
             tq = set(int(x) for x in p["tq"][: int(p["k"])])
             assert set(range(low)) <= tq
             if low == 2:
                 continue
             assert 2 in tq
+
+
+@pytest.mark.parametrize("pairs", [((4, 6), (8, 10), (12, 14)),
+                                   ((4, 6), (8, 10), (12, 14), (1, 15), (3, 5)),
+                                   ((3, 4), (6, 7), (9, 10), (12, 13))])
+def test_tma_edges_keep_warp_local_sweeps_race_free(monkeypatch, pairs):
+    """TMA plans load the first sweep and store the last one under the TMA
+    swizzle: a warp-local transition across such an edge would let one warp
+    overwrite slots another warp is still reading (the executor asserts, per
+    warp, both read-after-write and write-after-read slot sets)."""
+    monkeypatch.setenv("NSB_LOW_QUBITS", "3")
+    monkeypatch.setenv("NSB_TMA", "1")
+    monkeypatch.setenv("NSB_PLAN_EXEC_CHECK", "1")
+    n = 16
+    c = Circuit(n, [("c", 1)])
+    for a, b in pairs:
+        c.gate_op(Gate.CZ, (a, b), ())
+        c.gate_op(Gate.RZZ, (b, a), (0.3,))
+    pk = executable(c)
+    plan = PE.HostPlan(pk.ops, pk.params, pk.payloads, n, 296)
+    assert plan.tma
+    rng = np.random.default_rng(len(pairs))
+    state = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    want = state.copy()
+    PE.run_passes(plan, plan.mma_passes, state, workers=296)
+    monkeypatch.setenv("NSB_TMA", "0")  # the same circuit planned without TMA edges
+    ref = PE.HostPlan(pk.ops, pk.params, pk.payloads, n, 296)
+    assert not ref.tma
+    PE.run_passes(ref, ref.mma_passes, want, workers=296)
+    assert np.allclose(state, want, rtol=0, atol=1e-12)
