@@ -637,9 +637,13 @@ def run_ours(args, rank, world, local):
         # 34-qubit config 5 state from N = 2 on
         del prog, state
         torch.cuda.empty_cache()
-        sh = [sharded_measure(32, 10, rank, world, local, 2, 1)]
-        if world >= 2:
-            sh.append(sharded_measure(34, 10, rank, world, local, 1, 1))
+        sh = []
+        try:  # a failure here must not cost the headline line (same on every rank)
+            sh.append(sharded_measure(32, 10, rank, world, local, 2, 1))
+            if world >= 2:
+                sh.append(sharded_measure(34, 10, rank, world, local, 1, 1))
+        except Exception as e:  # noqa: BLE001 -- reported in the JSON line
+            sh.append({"error": f"{type(e).__name__}: {e}"[:300]})
         line["sharded"] = sh
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, args.ref_budget)
