@@ -249,8 +249,13 @@ def _gpu_count():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("ranks", [2, 4])
+@pytest.mark.parametrize("ranks", [1, 2, 4])
 def test_nccl_sharded_matches_oracle(tmp_path, ranks):
+    """One rank per GPU over NCCL: sharded MMA runs, ShardedState.sample (device
+    chunk masses + range probabilities, 2^4 and 2^13 chunks) and sharded
+    rejection mode against the full-state oracle and the reference sampler.
+    ranks = 1 runs the same executor, sampler and rejection path on one GPU
+    (g = 0: no qubit swaps), so a one-GPU box covers their device half."""
     if _gpu_count() < ranks:
         pytest.skip(f"needs {ranks} GPUs")
     port = _free_port()
@@ -270,9 +275,9 @@ def test_nccl_sharded_matches_oracle(tmp_path, ranks):
             assert d["samples_ok_" + tag].all(), tag  # ShardedState.sample == reference sample
     rej = [k for k in d.files if k.startswith("rejection_ok_")]
     assert rej and all(d[k].all() for k in rej), rej  # sharded rejection mode == reference
-    # peer-memory swaps overlapped with the gate group after them (chunked passes)
-    assert int(d["overlap_layered18_p2p"][0]) > 0
-    assert int(d["overlap_layered18_nccl"][0]) == 0
+    if ranks > 1:  # peer-memory swaps overlapped with the gate group after them (chunked passes)
+        assert int(d["overlap_layered18_p2p"][0]) > 0
+        assert int(d["overlap_layered18_nccl"][0]) == 0
 
 
 # ---------------------------------------------------------------------------
