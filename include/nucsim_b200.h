@@ -393,6 +393,17 @@ int nsb_shard_close_peers(nsb_ctx* ctx, nsb_status* st);
 int nsb_shard_swap_overlap(nsb_ctx* ctx, int32_t global_bit, int32_t local_q, nsb_plan* plan,
                            int64_t seg, int32_t chunk_bits, int32_t swap_ctas,
                            int32_t* n_chunked, nsb_status* st);
+/* The same overlap with the exchange on the COPY ENGINES (no SMs): per block
+ * of a chunk, each partner pulls the other's half into a staging slot of its
+ * own (a 2-D peer cudaMemcpy over NVLink), tells the partner so (a stream
+ * memory write into the partner's flag word), waits for the partner's word,
+ * and copies the slot into its own half (a local copy-engine copy); chunk c's
+ * passes run at the full grid once its blocks are in.  stage_bytes bounds a
+ * staging slot (two slots; 0: 4 GiB).  Same semantics and collective
+ * contract as nsb_shard_swap_overlap. */
+int nsb_shard_swap_overlap_ce(nsb_ctx* ctx, int32_t global_bit, int32_t local_q,
+                              nsb_plan* plan, int64_t seg, int32_t chunk_bits,
+                              int64_t stage_bytes, int32_t* n_chunked, nsb_status* st);
 
 #ifdef __cplusplus
 }

@@ -147,6 +147,8 @@ _SIGNATURES = {
     "nsb_shard_swap_p2p": (ctypes.c_int, [_P, _I32, _I32, _ST]),
     "nsb_shard_swap_overlap": (ctypes.c_int, [_P, _I32, _I32, _P, _I64, _I32, _I32,
                                               ctypes.POINTER(_I32), _ST]),
+    "nsb_shard_swap_overlap_ce": (ctypes.c_int, [_P, _I32, _I32, _P, _I64, _I32, _I64,
+                                                 ctypes.POINTER(_I32), _ST]),
 }
 
 EXPORTS = tuple(_SIGNATURES)

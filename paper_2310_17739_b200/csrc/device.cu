@@ -1634,6 +1634,12 @@ struct nsb_ctx {
   // overlapped swaps (nsb_shard_swap_overlap): epoch of the chunk flags
   unsigned swap_epoch = 0;
   cudaEvent_t ev_ov0 = nullptr, ev_ov1 = nullptr;
+  // copy-engine swaps (nsb_shard_swap_overlap_ce): two staging slots, one
+  // event per chunk
+  DevBuf<double2> ce_stage;
+  cudaEvent_t ev_chunk[16] = {};
+  cudaStream_t xfer2 = nullptr;  // local copies (pulls on xfer)
+  cudaEvent_t ev_pulled[2] = {}, ev_local[2] = {};  // per staging slot
 };
 
 struct nsb_plan {
@@ -1956,6 +1962,38 @@ void apply_matrix(nsb_ctx* c, const double* u, const int32_t* qubits, int k,
   NSB_CUDA(cudaGetLastError());
 }
 
+// ---- stream memory operations (copy-engine swaps) --------------------------
+// cuStreamWriteValue32 / cuStreamWaitValue32 from the driver: flag words
+// written and awaited by the stream front end, no kernel (no SM) involved
+struct StreamMem {
+  using Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+  Fn write_fn = nullptr, wait_fn = nullptr;
+  void write(cudaStream_t s, unsigned* addr, unsigned v) const {
+    const CUresult r = write_fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v,
+                                0 /* CU_STREAM_WRITE_VALUE_DEFAULT: after a memory barrier */);
+    if (r != CUDA_SUCCESS) throw CudaError("cuStreamWriteValue32 failed (" + std::to_string(int(r)) + ")");
+  }
+  void wait(cudaStream_t s, unsigned* addr, unsigned v) const {
+    const CUresult r = wait_fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v,
+                               CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) throw CudaError("cuStreamWaitValue32 failed (" + std::to_string(int(r)) + ")");
+  }
+};
+const StreamMem& stream_mem() {
+  static const StreamMem sm = [] {
+    StreamMem m;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    NSB_CUDA(cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q));
+    m.write_fn = reinterpret_cast<StreamMem::Fn>(f);
+    NSB_CUDA(cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q));
+    m.wait_fn = reinterpret_cast<StreamMem::Fn>(f);
+    if (!m.write_fn || !m.wait_fn) throw std::runtime_error("stream memory operations unavailable");
+    return m;
+  }();
+  return sm;
+}
+
 // ---- TMA tensor maps (planner.h "TMA tiles", dev::TmaPass) -----------------
 using TensorMapEncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                           const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -2201,6 +2239,14 @@ void ctx_free(nsb_ctx* ctx) {
   if (ctx->xfer) cudaStreamDestroy(ctx->xfer);
   if (ctx->ev_ov0) cudaEventDestroy(ctx->ev_ov0);
   if (ctx->ev_ov1) cudaEventDestroy(ctx->ev_ov1);
+  for (cudaEvent_t& e : ctx->ev_chunk)
+    if (e) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->ev_pulled[i]) cudaEventDestroy(ctx->ev_pulled[i]);
+    if (ctx->ev_local[i]) cudaEventDestroy(ctx->ev_local[i]);
+  }
+  if (ctx->xfer2) cudaStreamDestroy(ctx->xfer2);
+  ctx->ce_stage.release();
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -3327,6 +3373,228 @@ int nsb_shard_swap_overlap(nsb_ctx* c, int32_t global_bit, int32_t local_q, nsb_
     if (it.pass_begin + np < it.pass_end)
       launch_blocked(c, P, P->passes.ptr, it.pass_begin + np, it.pass_end, -1.0);
     NSB_CUDA(cudaEventRecord(c->ev_ov1, c->xfer));
+    NSB_CUDA(cudaStreamWaitEvent(c->stream, c->ev_ov1, 0));
+    NSB_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int nsb_shard_swap_overlap_ce(nsb_ctx* c, int32_t global_bit, int32_t local_q, nsb_plan* P,
+                              int64_t seg, int32_t chunk_bits, int64_t stage_bytes,
+                              int32_t* n_chunked, nsb_status* st) {
+  return guarded(st, [&] {
+    require_state(c);
+    if (!c->comm) throw std::invalid_argument("no communicator (nsb_comm_init)");
+    if (global_bit < 0 || (1 << global_bit) >= c->nranks || local_q < 0 || local_q >= c->n)
+      throw std::invalid_argument("bad shard swap qubits");
+    if (!P || P->ctx != c) throw std::invalid_argument("plan belongs to another context");
+    if (P->n != c->n) throw std::invalid_argument("plan was built for another qubit count");
+    if (seg < 0 || seg >= static_cast<int64_t>(P->host.items.size()))
+      throw std::invalid_argument("item index out of range");
+    const int partner = c->rank ^ (1 << global_bit);
+    if (!c->peers[partner]) throw std::invalid_argument("peer shard not mapped (nsb_shard_open_peers)");
+    NSB_CUDA(cudaSetDevice(c->device));
+    const StreamMem& sm = stream_mem();
+    uint64_t cm = 0;
+    int np = chunk_prefix(P->host, seg, local_q, std::min(chunk_bits, 4), &cm);
+    // The copy engines move about 1.5 G rows per second: regions of short runs
+    // (a low chunk or swap qubit) would take them longer than the SM swap
+    // kernel takes the whole exchange (tools/r2_ce_dbg.sh: 512-byte runs, local
+    // copies at 0.7 TB/s).  Those swaps run on the SMs, not overlapped.
+    static const int min_run_log2 = [] {
+      const char* e = std::getenv("NSB_CE_MIN_RUN");
+      return e ? std::atoi(e) : 12;
+    }();
+    if (np > 0 && __builtin_ctzll(cm | (uint64_t(1) << local_q)) < min_run_log2) np = 0;
+    if (n_chunked) *n_chunked = np;
+    const Item& it = P->host.items[static_cast<size_t>(seg)];
+    const int b = (c->rank >> global_bit) & 1;
+    const uint64_t half = c->n_amps >> 1;
+    if (np == 0) {  // nothing chunkable (or short runs): the SM swap, then the item
+      const int clog = static_cast<int>(std::min<uint64_t>(16, c->n - 1));
+      comm_barrier(c);
+      dev::k_shard_swap_p2p<<<static_cast<unsigned>(c->sm_count * 4), 256, 0, c->stream>>>(
+          c->amps.ptr, c->peers[partner], half, local_q, 1 - b, b, b, clog);
+      NSB_CUDA(cudaGetLastError());
+      comm_barrier(c);
+      run_item(c, P, it);
+      NSB_CUDA(cudaStreamSynchronize(c->stream));
+      return;
+    }
+    if (!c->xfer) NSB_CUDA(cudaStreamCreateWithFlags(&c->xfer, cudaStreamNonBlocking));
+    if (!c->ev_ov0) NSB_CUDA(cudaEventCreateWithFlags(&c->ev_ov0, cudaEventDisableTiming));
+    if (!c->ev_ov1) NSB_CUDA(cudaEventCreateWithFlags(&c->ev_ov1, cudaEventDisableTiming));
+    const int cb = __builtin_popcountll(cm);
+    const int n_ch = 1 << cb;
+    for (int ch = 0; ch < n_ch; ++ch)
+      if (!c->ev_chunk[ch]) NSB_CUDA(cudaEventCreateWithFlags(&c->ev_chunk[ch], cudaEventDisableTiming));
+    if (!c->xfer2) NSB_CUDA(cudaStreamCreateWithFlags(&c->xfer2, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      if (!c->ev_pulled[i]) NSB_CUDA(cudaEventCreateWithFlags(&c->ev_pulled[i], cudaEventDisableTiming));
+      if (!c->ev_local[i]) NSB_CUDA(cudaEventCreateWithFlags(&c->ev_local[i], cudaEventDisableTiming));
+    }
+    // The exchanged region of chunk ch: bits F = cm + local_q fixed (mine:
+    // local_q = 1 - b, the partner's: local_q = b), the other bits free,
+    // paired element for element in one fixed order.  It is a set of runs of
+    // 2^p1 amplitudes (p1 = the lowest fixed bit); the free bits above p1 form
+    // groups of consecutive bits between fixed ones.  One 3-D copy covers the
+    // run, the group right above it as height (rows at twice the run's pitch:
+    // the copy engine reads every other run of one contiguous span) and the
+    // largest group above that as depth; a host loop enumerates the other
+    // groups' bits; copies are split into staging blocks of at most a slot.
+    const uint64_t F = cm | (uint64_t(1) << local_q);
+    const int p1 = __builtin_ctzll(F);
+    struct Group {
+      int lo, bits;
+    };
+    std::vector<Group> groups;
+    for (int q = p1 + 1; q < c->n;) {
+      if (F >> q & 1) {
+        ++q;
+        continue;
+      }
+      int e = q;
+      while (e < c->n && !(F >> e & 1)) ++e;
+      groups.push_back({q, e - q});
+      q = e;
+    }
+    static int max_pitch = 0;
+    if (!max_pitch) NSB_CUDA(cudaDeviceGetAttribute(&max_pitch, cudaDevAttrMaxPitch, c->device));
+    int gh = -1, gd = -1;  // height and depth groups
+    if (!groups.empty() && (uint64_t(sizeof(double2)) << groups[0].lo) <= uint64_t(max_pitch)) gh = 0;
+    for (int i = 0; i < static_cast<int>(groups.size()); ++i)
+      if (i != gh && groups[i].lo > (gh >= 0 ? groups[gh].lo : -1) &&
+          (gd < 0 || groups[i].bits > groups[gd].bits))
+        gd = i;
+    uint64_t other = 0;  // free bits enumerated on the host
+    for (int i = 0; i < static_cast<int>(groups.size()); ++i)
+      if (i != gh && i != gd)
+        for (int t = 0; t < groups[i].bits; ++t) other |= uint64_t(1) << (groups[i].lo + t);
+    const uint64_t run = uint64_t(1) << p1;
+    const uint64_t H = gh >= 0 ? uint64_t(1) << groups[gh].bits : 1;
+    const uint64_t D = gd >= 0 ? uint64_t(1) << groups[gd].bits : 1;
+    // strides (log2 amplitudes); no height group: one run per row (pitch = width)
+    const int hs = gh >= 0 ? groups[gh].lo : p1;
+    const int ds = gd >= 0 ? groups[gd].lo : hs + (gh >= 0 ? groups[gh].bits : 0);
+    const uint64_t n_outer = uint64_t(1) << __builtin_popcountll(other);
+    if (n_outer > 4096) throw std::invalid_argument("swap region too fragmented for copy engines");
+    const uint64_t cap = std::max<uint64_t>(run, (stage_bytes > 0 ? static_cast<uint64_t>(stage_bytes)
+                                                                  : (uint64_t(4) << 30)) / sizeof(double2));
+    const uint64_t chunk_amps = half >> cb;
+    const uint64_t slot = std::min<uint64_t>(chunk_amps, cap);
+    if (c->ce_stage.count < 2 * slot) {
+      c->ce_stage.release();
+      c->ce_stage.alloc(2 * slot);
+    }
+    // one chunk's pieces: (outer value, depth range, height range), each a 3-D
+    // copy of whole runs, in the fixed element order
+    struct Piece {
+      uint64_t outer, d0, nd, h0, nh;
+    };
+    std::vector<Piece> pieces;
+    const uint64_t slice = H * run;  // amplitudes per depth slice
+    for (uint64_t o = 0; o < n_outer; ++o) {
+      if (slice <= slot) {
+        const uint64_t per = slot / slice;  // depth slices per piece
+        for (uint64_t d0 = 0; d0 < D; d0 += per) pieces.push_back({o, d0, std::min(per, D - d0), 0, H});
+      } else {
+        const uint64_t per = std::max<uint64_t>(1, slot / run);  // rows per piece
+        for (uint64_t d0 = 0; d0 < D; ++d0)
+          for (uint64_t h0 = 0; h0 < H; h0 += per) pieces.push_back({o, d0, 1, h0, std::min(per, H - h0)});
+      }
+    }
+    auto copy3d_on = [&](cudaStream_t strm, double2* dst, bool dst_dense, const double2* src,
+                         bool src_dense, const Piece& pc, cudaMemcpyKind kind) {
+      if (run >= (uint64_t(1) << 20)) {  // long runs: plain 1-D copies, run by run
+        const uint64_t sh = uint64_t(1) << hs, sd = uint64_t(1) << ds;
+        uint64_t off = 0;
+        for (uint64_t d = 0; d < pc.nd; ++d)
+          for (uint64_t r = 0; r < pc.nh; ++r, off += run) {
+            const uint64_t strided = d * sd + r * sh;
+            NSB_CUDA(cudaMemcpyAsync(dst + (dst_dense ? off : strided), src + (src_dense ? off : strided),
+                                     run * sizeof(double2), kind, strm));
+          }
+        return;
+      }
+      cudaMemcpy3DParms m{};
+      const size_t wb = run * sizeof(double2);
+      const size_t sp = size_t(sizeof(double2)) << hs;
+      const size_t sy = size_t(1) << (ds - hs);
+      m.srcPtr = src_dense ? make_cudaPitchedPtr(const_cast<double2*>(src), wb, wb, pc.nh)
+                           : make_cudaPitchedPtr(const_cast<double2*>(src), sp, wb, sy);
+      m.dstPtr = dst_dense ? make_cudaPitchedPtr(dst, wb, wb, pc.nh) : make_cudaPitchedPtr(dst, sp, wb, sy);
+      m.extent = make_cudaExtent(wb, pc.nh, pc.nd);
+      m.kind = kind;
+      NSB_CUDA(cudaMemcpy3DAsync(&m, strm));
+    };
+    auto copy3d = [&](double2* dst, bool dst_dense, const double2* src, bool src_dense,
+                      const Piece& pc, cudaMemcpyKind kind) {
+      copy3d_on(c->xfer, dst, dst_dense, src, src_dense, pc, kind);
+    };
+    auto region_off = [&](uint64_t fix, const Piece& pc) {
+      return fix | deposit_bits(pc.outer, other) | (pc.d0 << ds) | (pc.h0 << hs);
+    };
+    // timing experiments only (wrong states): 2 = no chunked passes, 4 = no
+    // flag words, 8 = no local copies, 16 = no peer pulls
+    static const int ov_debug = [] {
+      const char* e = std::getenv("NSB_OVERLAP_DEBUG");
+      return e ? std::atoi(e) : 0;
+    }();
+    const unsigned epoch = ++c->swap_epoch;
+    unsigned* f_mine = shard_flags(c->amps.ptr, c->n_amps);
+    unsigned* f_peer = shard_flags(c->peers[partner], c->n_amps);
+    comm_barrier(c);  // both shards are final before either is touched
+    NSB_CUDA(cudaEventRecord(c->ev_ov0, c->stream));
+    NSB_CUDA(cudaStreamWaitEvent(c->xfer, c->ev_ov0, 0));
+    NSB_CUDA(cudaStreamWaitEvent(c->xfer2, c->ev_ov0, 0));
+    // per block k: pulls on xfer, then the flag word to the partner; local
+    // copies on xfer2 once the pull landed and the partner's word arrived, so
+    // block k's local copy (HBM) runs beside block k+1's pull (NVLink); a
+    // slot is pulled into again only after its local copy (ev_local)
+    int k = 0;  // staging block: flag word, slot k & 1
+    for (int ch = 0; ch < n_ch; ++ch) {
+      const uint64_t cv = deposit_bits(static_cast<uint64_t>(ch), cm);
+      const uint64_t fix_mine = cv | (uint64_t(1 - b) << local_q);
+      const uint64_t fix_peer = cv | (uint64_t(b) << local_q);
+      for (size_t p0 = 0; p0 < pieces.size(); ++k) {
+        if (k >= dev::kShardFlagWords) throw std::invalid_argument("too many swap blocks");
+        double2* sbuf = c->ce_stage.ptr + static_cast<uint64_t>(k & 1) * slot;
+        if (k >= 2) NSB_CUDA(cudaStreamWaitEvent(c->xfer, c->ev_local[k & 1], 0));
+        size_t p = p0;
+        uint64_t used = 0;
+        for (; p < pieces.size(); ++p) {  // pull: the partner's half into the slot
+          const uint64_t amps = pieces[p].nd * pieces[p].nh * run;
+          if (used + amps > slot) break;
+          if (!(ov_debug & 16))
+            copy3d(sbuf + used, true, c->peers[partner] + region_off(fix_peer, pieces[p]), false,
+                   pieces[p], cudaMemcpyDefault);
+          used += amps;
+        }
+        if (!(ov_debug & 4)) sm.write(c->xfer, f_peer + k, epoch);  // "your block k is read"
+        NSB_CUDA(cudaEventRecord(c->ev_pulled[k & 1], c->xfer));
+        NSB_CUDA(cudaStreamWaitEvent(c->xfer2, c->ev_pulled[k & 1], 0));
+        if (!(ov_debug & 4)) sm.wait(c->xfer2, f_mine + k, epoch);  // ... and mine
+        used = 0;
+        for (size_t q = p0; q < p && !(ov_debug & 8); ++q) {  // the slot into my half
+          copy3d_on(c->xfer2, c->amps.ptr + region_off(fix_mine, pieces[q]), false, sbuf + used, true,
+                    pieces[q], cudaMemcpyDeviceToDevice);
+          used += pieces[q].nd * pieces[q].nh * run;
+        }
+        NSB_CUDA(cudaEventRecord(c->ev_local[k & 1], c->xfer2));
+        p0 = p;
+      }
+      NSB_CUDA(cudaEventRecord(c->ev_chunk[ch], c->xfer2));
+    }
+    for (int ch = 0; ch < n_ch; ++ch) {
+      NSB_CUDA(cudaStreamWaitEvent(c->stream, c->ev_chunk[ch], 0));
+      if (!(ov_debug & 2))
+        launch_blocked(c, P, P->passes.ptr, it.pass_begin, it.pass_begin + np, -1.0, 0, cm,
+                       deposit_bits(static_cast<uint64_t>(ch), cm));
+    }
+    if (it.pass_begin + np < it.pass_end)
+      launch_blocked(c, P, P->passes.ptr, it.pass_begin + np, it.pass_end, -1.0);
+    NSB_CUDA(cudaEventRecord(c->ev_ov1, c->xfer));
+    NSB_CUDA(cudaStreamWaitEvent(c->stream, c->ev_ov1, 0));
+    NSB_CUDA(cudaEventRecord(c->ev_ov1, c->xfer2));
     NSB_CUDA(cudaStreamWaitEvent(c->stream, c->ev_ov1, 0));
     NSB_CUDA(cudaStreamSynchronize(c->stream));
   });

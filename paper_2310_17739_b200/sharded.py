@@ -518,20 +518,26 @@ class ShardedProgram:
             pass
 
     def _swap(self, i: int, s: Step, chunk_amps: int) -> bool:
-        """Execute swap step i.  With NSB_SWAP_OVERLAP=1 (and peer-memory swaps)
-        the swap is overlapped with the first item of the gate step that
-        follows it (nsb_shard_swap_overlap: that item's chunkable passes run
-        chunk by chunk as the swapped chunks land).  Off by default: measured
-        slower on B200 (the gate passes lose the SMs the swap kernel takes,
-        DESIGN.md section 8).  Returns True when that item has run."""
+        """Execute swap step i.  With peer-memory swaps the swap is overlapped
+        with the first item of the gate step that follows it: that item's
+        chunkable passes run chunk by chunk as the swapped chunks land.
+        NSB_SWAP_OVERLAP selects how the chunks move: "ce" (default) on the
+        copy engines (nsb_shard_swap_overlap_ce: no SMs taken from the gate
+        passes), "1" with a swap kernel on some SMs (nsb_shard_swap_overlap:
+        measured slower), "0" not overlapped (the swap
+        kernel, then the item).  Returns True when that item has run."""
         S = self.state
         nxt = self.plans[i + 1] if i + 1 < len(self.plans) else None
-        if (S.peer_swaps and nxt is not None and nxt[1] > 0
-                and os.environ.get("NSB_SWAP_OVERLAP", "0") == "1"):
+        mode = os.environ.get("NSB_SWAP_OVERLAP", "ce")
+        if S.peer_swaps and nxt is not None and nxt[1] > 0 and mode in ("1", "ce"):
             n = ctypes.c_int32(0)
-            S.dev.call("nsb_shard_swap_overlap", s.global_bit, s.local_q, nxt[0], 0,
-                       int(os.environ.get("NSB_SWAP_CHUNK_BITS", "3")),
-                       int(os.environ.get("NSB_SWAP_CTAS", "0")), ctypes.byref(n))
+            bits = int(os.environ.get("NSB_SWAP_CHUNK_BITS", "3"))
+            if mode == "ce":
+                S.dev.call("nsb_shard_swap_overlap_ce", s.global_bit, s.local_q, nxt[0], 0, bits,
+                           int(os.environ.get("NSB_SWAP_STAGE_BYTES", "0")), ctypes.byref(n))
+            else:
+                S.dev.call("nsb_shard_swap_overlap", s.global_bit, s.local_q, nxt[0], 0, bits,
+                           int(os.environ.get("NSB_SWAP_CTAS", "0")), ctypes.byref(n))
             self.overlapped_passes += n.value
             return True
         if S.peer_swaps:

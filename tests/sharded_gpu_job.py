@@ -32,15 +32,21 @@ def cases():
 
 
 def main(out):
-    # peer-memory swaps overlapped with the gate group after them (off by
-    # default in ShardedProgram.run; the parity check covers that path too)
-    os.environ["NSB_SWAP_OVERLAP"] = "1"
+    # the copy-engine exchange on every geometry (the library otherwise keeps
+    # short-run regions on the SM swap kernel)
+    os.environ["NSB_CE_MIN_RUN"] = "0"
+    # peer-memory swaps overlapped with the gate group after them: on the copy
+    # engines (the default, "_p2p") and with the SM swap kernel ("_p2psm");
+    # NCCL pack/send/unpack swaps ("_nccl")
     dist.init_process_group("gloo")
     rank = dist.get_rank()
     res = {}
     cs = list(cases())
-    for (tag, ops, params, pool, n), peer in zip(cs * 2, [True] * len(cs) + [False] * len(cs)):
-        tag = tag + ("_p2p" if peer else "_nccl")
+    modes = [(True, "ce", "_p2p"), (True, "1", "_p2psm"), (False, "0", "_nccl")]
+    for (tag, ops, params, pool, n), (peer, mode, suffix) in (
+            (c, m) for m in modes for c in cs):
+        os.environ["NSB_SWAP_OVERLAP"] = mode
+        tag = tag + suffix
         st = S.ShardedState.from_torch_distributed(n, device=int(os.environ["LOCAL_RANK"]),
                                                    peer_swaps=peer)
         probs, steps = st.run_mma(ops, params, pool)

@@ -276,7 +276,8 @@ def test_nccl_sharded_matches_oracle(tmp_path, ranks):
     rej = [k for k in d.files if k.startswith("rejection_ok_")]
     assert rej and all(d[k].all() for k in rej), rej  # sharded rejection mode == reference
     if ranks > 1:  # peer-memory swaps overlapped with the gate group after them (chunked passes)
-        assert int(d["overlap_layered18_p2p"][0]) > 0
+        assert int(d["overlap_layered18_p2p"][0]) > 0    # copy engines
+        assert int(d["overlap_layered18_p2psm"][0]) > 0  # SM swap kernel
         assert int(d["overlap_layered18_nccl"][0]) == 0
 
 
