@@ -87,3 +87,23 @@ def test_tma_filter_circuit_with_assertions(monkeypatch):
     p0, a0 = _run(exe, wl.params, pool, n)
     assert p1 == p0
     assert np.array_equal(a1, a0)
+
+
+def test_streamed_run_on_tma_plans(monkeypatch):
+    """nsb_run_mma_streamed above 22 qubits: parts planned as TMA plans (their
+    own tensor maps per part, fresh marker passes on cp.async) reproduce the
+    single-launch program."""
+    from paper_2310_17739_b200.engine import run_mma_streamed
+    n = 23
+    wl = W.filter_workload(n - 1, trotter=1, n_steps=2, n_scatter=2, hop_range=4,
+                           pair_density=0.05, trial="10" * 11)
+    fops, pool, _ = W.fuse_packed(wl.ops, wl.params, wl.payloads)
+    exe = wl.executable(fops)
+    assert _tma_passes(exe, wl.params, pool, n) > 0
+    state = StateVector(n)
+    p_one = DeviceProgram(state, exe, wl.params, pool).run_mma()
+    a_one = state.amps.copy()
+    state.restart()
+    p_str = run_mma_streamed(state, exe, wl.params, pool)
+    np.testing.assert_allclose(p_str, p_one, rtol=0, atol=1e-12)
+    assert np.linalg.norm(state.amps - a_one) <= 1e-11
