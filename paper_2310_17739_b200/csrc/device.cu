@@ -992,7 +992,7 @@ constexpr size_t kBlockedSmemBytesTma = kBlockedSmemBytes + 1024;
 // counts the bytes in, bulk groups track the stores); the chunk-restricted
 // instantiation keeps per-thread cp.async under the same layout.
 template <bool kChunk, bool kTma>
-__global__ void __launch_bounds__(kPassThreads, 2) k_blocked(BlockedParams p) {
+__global__ void __launch_bounds__(kPassThreads, kCtasPerSm) k_blocked(BlockedParams p) {
   constexpr bool kHw = kTma && !kChunk;
   const uint64_t c_mask = kChunk ? p.cmask : 0, c_val = kChunk ? p.cval : 0;
   const int c_bits = kChunk ? p.cbits : 0;

@@ -299,16 +299,17 @@ bool tma_layout(const PassDesc& P, int n, int order, TmaLayout& L) {
   struct Run {
     int s, len, pos;  // lowest qubit, length, tile-local position of its lowest bit
   };
-  Run runs[8];
+  Run runs[16];
   int nr = 0;
   for (int b = 3; b < P.k;) {
     int e = b + 1;
     while (e < P.k && P.tq[e] == P.tq[e - 1] + 1) ++e;
+    if (e - b > 8) return false;  // a box dim spans at most 256 (12-qubit tile variants)
     runs[nr++] = {P.tq[b], e - b, b};
     b = e;
   }
   // the dims: the longest runs (fewest copies), four, or three and a gap dim
-  int idx[8];
+  int idx[16];
   for (int i = 0; i < nr; ++i) idx[i] = i;
   std::stable_sort(idx, idx + nr, [&](int a, int b) { return runs[a].len > runs[b].len; });
   int nd = std::min(nr, 4);
@@ -328,7 +329,7 @@ bool tma_layout(const PassDesc& P, int n, int order, TmaLayout& L) {
   int sel[4];
   for (int i = 0; i < nd; ++i) sel[i] = idx[i];
   std::sort(sel, sel + nd, [&](int a, int b) { return runs[a].s < runs[b].s; });
-  int cstart[8], cend[8];
+  int cstart[16], cend[16];
   for (int i = 0; i < nd; ++i) {
     cstart[sel[i]] = runs[sel[i]].s;
     cend[sel[i]] = i + 1 < nd ? runs[sel[i + 1]].s : n;
@@ -359,7 +360,7 @@ bool tma_layout(const PassDesc& P, int n, int order, TmaLayout& L) {
     L.len[L.rank] = 0;
     ++L.rank;
   }
-  bool in_dims[8] = {};
+  bool in_dims[16] = {};
   for (int i = 0; i < nd; ++i) in_dims[sel[i]] = true;
   for (int j = 0; j < nr; ++j)  // the other runs: copy index bits, ascending
     if (!in_dims[j])

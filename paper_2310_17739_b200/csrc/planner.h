@@ -41,10 +41,15 @@ constexpr int kTileAmpsMax = 1 << kTileQubitsMax;
 #define NSB_OCTETS 2
 #endif
 constexpr int kOctets = NSB_OCTETS;              // octets per thread per sweep (1 or 2)
-constexpr int kThreadBits = kOctets == 2 ? 7 : 8;
+#ifndef NSB_THREAD_BITS  // build variants: 12-qubit tiles take 256 threads (8 warps, one CTA per SM)
+#define NSB_THREAD_BITS (kOctets == 2 ? 7 : 8)
+#endif
+constexpr int kThreadBits = NSB_THREAD_BITS;
 constexpr int kPassThreads = 1 << kThreadBits;  // 4 (8) warps per CTA, two CTAs per SM
+constexpr int kCtasPerSm = kPassThreads > 128 ? 1 : 2;
 constexpr int kIndexBits = kThreadBits + (kOctets == 2 ? 1 : 0);  // octet-index bits of a batch
-static_assert(kIndexBits <= 8, "GroupDesc holds 8 index-bit offsets");
+constexpr int kIndexSlots = kIndexBits > 8 ? 10 : 8;  // GroupDesc offset slots
+static_assert(kIndexBits <= kIndexSlots, "GroupDesc index-bit offsets");
 constexpr int kLowQubits = 3;                    // always-tiled qubits 0..2 (128 B runs)
 // States up to this many qubits stay L2-resident inside a launch: their
 // tiles need not hold qubits 0..2 (sector efficiency matters less than the
@@ -133,9 +138,9 @@ enum GateClass : uint8_t {
 struct GroupDesc {        // 80 bytes
   uint16_t am[3];         // swizzled masks of the axes at positions 0..2 after the ops (store)
   uint16_t ram[3];        // axes 0..2 through the read map R (load side)
-  uint16_t tcol[8];       // swizzled offsets of octet-index bits (store side): thread
-                          // bits, then the octet index (a fourth axis, or a free vector)
-  uint16_t rtcol[8];      // load side
+  uint16_t tcol[kIndexSlots];   // swizzled offsets of octet-index bits (store side):
+                                // thread bits, then the octet index (a fourth axis, or a free vector)
+  uint16_t rtcol[kIndexSlots];  // load side
   uint8_t op_begin;       // first GateOp (relative to the pass's op_begin)
   uint8_t n_ops_sync;     // bits 0..6: gate ops (0: a pure read-map sweep); bit 7: CTA
                           // barrier after this sweep (else warp-local, __syncwarp)
@@ -145,7 +150,7 @@ struct GroupDesc {        // 80 bytes
   __host__ __device__ int n_ops() const { return n_ops_sync & 127; }
   __host__ __device__ bool sync() const { return n_ops_sync >> 7; }
 };
-static_assert(sizeof(GroupDesc) == 80, "GroupDesc layout");
+static_assert(sizeof(GroupDesc) == (kIndexSlots > 8 ? 88 : 80), "GroupDesc layout");
 
 // One gate of a group: class, axis pattern, payload.  Two-qubit gates are
 // stored with slot 0 on the lower axis (the planner exchanges the slots of

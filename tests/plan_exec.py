@@ -22,15 +22,17 @@ PASS_DT = np.dtype([("group_begin", "<i4"), ("group_end", "<i4"), ("op_begin", "
                     ("measure_q", "<i4"), ("measure_slot", "<i4"), ("collapse_q", "<i4"),
                     ("collapse_slot", "<i4"), ("tma", "<i4"), ("tq", "i1", (16,)),
                     ("oq", "i1", (32,)), ("tperm", "i1", (16,))])
-GROUP_DT = np.dtype([("am", "<u2", (3,)), ("ram", "<u2", (3,)), ("tcol", "<u2", (8,)),
-                     ("rtcol", "<u2", (8,)), ("op_begin", "u1"), ("n_ops_sync", "u1"),
+_VARIANT = os.environ.get("NSB_LIB_VARIANT")  # build variants (csrc/Makefile DEFS)
+OCTETS = 1 if _VARIANT == "o1" else 2  # kOctets
+THREAD_BITS = 8 if OCTETS == 1 or _VARIANT == "t12" else 7  # kThreadBits
+INDEX_BITS = THREAD_BITS + (1 if OCTETS == 2 else 0)  # kIndexBits
+INDEX_SLOTS = 10 if INDEX_BITS > 8 else 8  # kIndexSlots
+THREADS = 1 << THREAD_BITS  # kPassThreads
+TILE_MAX = 12 if _VARIANT == "t12" else 11  # kTileQubitsMax
+GROUP_DT = np.dtype([("am", "<u2", (3,)), ("ram", "<u2", (3,)), ("tcol", "<u2", (INDEX_SLOTS,)),
+                     ("rtcol", "<u2", (INDEX_SLOTS,)), ("op_begin", "u1"), ("n_ops_sync", "u1"),
                      ("kmat", "<u2"), ("r_out", "<u8", (4,))], align=True)
 OP_DT = np.dtype([("mat", "<i2"), ("cls", "u1"), ("pat", "u1"), ("cols", "<u2"), ("kind", "u1"), ("pad", "u1")])
-OCTETS = 1 if os.environ.get("NSB_LIB_VARIANT") == "o1" else 2  # kOctets (build variant)
-THREAD_BITS = 7 if OCTETS == 2 else 8  # kThreadBits
-INDEX_BITS = THREAD_BITS + (1 if OCTETS == 2 else 0)  # kIndexBits
-THREADS = 1 << THREAD_BITS  # kPassThreads
-TILE_MAX = 11  # kTileQubitsMax
 (DENSE1, DIAG1, DENSE2, SPARSE2, MONO2, DIAG2, CX01, CX10, PAIRQ, PAIRP, PAIRX, SWAP,
  PERMUTE, PAIRQR, PAIRPR, PAIRXR) = range(16)
 PATTERNS = {0: (0, 1), 1: (0, 2), 2: (1, 2), 3: (0,), 4: (1,), 5: (2,)}
