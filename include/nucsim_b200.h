@@ -255,6 +255,9 @@ typedef struct nsb_plan_view {
   const double* matrices;  /* complex pool */
   const int32_t* items;    /* n_items x 4: kind (0 gates, 1 measure, 2 reset,
                               3 dense), pass_begin | qubit, pass_end | step, k */
+  int32_t octets;          /* octets per thread of the kernel layout (1: 256 threads, small
+                              states; 2: 128 threads) */
+  int32_t thread_bits;     /* log2 threads per CTA */
 } nsb_plan_view;
 int nsb_host_plan_build(const nsb_op* ops, int64_t n_ops, const double* params,
                         const double* payloads, int32_t n_qubits, int32_t workers, void** out,

@@ -76,7 +76,8 @@ class PlanView(ctypes.Structure):
                 ("n_matrices", ctypes.c_int64), ("n_items", ctypes.c_int64),
                 ("passes", ctypes.c_void_p), ("mma_passes", ctypes.c_void_p),
                 ("groups", ctypes.c_void_p), ("gate_ops", ctypes.c_void_p),
-                ("matrices", ctypes.c_void_p), ("items", ctypes.c_void_p)]
+                ("matrices", ctypes.c_void_p), ("items", ctypes.c_void_p),
+                ("octets", ctypes.c_int32), ("thread_bits", ctypes.c_int32)]
 
 
 _P = ctypes.c_void_p

@@ -727,32 +727,35 @@ __device__ __forceinline__ void gate_octet_pair(double2 (&xs)[NO][8],
 }
 
 // Register-axis exchange (four-axis groups): octet position P <-> octet index
+// (the planner emits these only for the two-octet layout: a no-op otherwise)
 template <int P, int NO>
 __device__ __forceinline__ void swap_axis_q(double2 (&xs)[NO][8]) {
-  static_assert(NO == 2, "the octet index is an axis only with two octets per thread");
-  constexpr int A = 1 << P;
+  if constexpr (NO == 2) {
+    constexpr int A = 1 << P;
 #pragma unroll
-  for (int c = 0; c < 8; ++c)
-    if (!(c & A)) {
-      const double2 t = xs[0][c | A];
-      xs[0][c | A] = xs[1][c];
-      xs[1][c] = t;
-    }
+    for (int c = 0; c < 8; ++c)
+      if (!(c & A)) {
+        const double2 t = xs[0][c | A];
+        xs[0][c | A] = xs[NO - 1][c];
+        xs[NO - 1][c] = t;
+      }
+  }
 }
 
 // Register CX (four-axis groups): registers c' = c with bit K ^= bit J over
 // the 16 registers of the two octets (bit 3 = octet index)
 template <int J, int K, int NO>
 __device__ __forceinline__ void reg_cx(double2 (&xs)[NO][8]) {
-  static_assert(NO == 2 || (J < 3 && K < 3), "octet-index register ops need two octets");
+  if constexpr (NO == 2 || (J < 3 && K < 3)) {  // octet-index bits need two octets
 #pragma unroll
-  for (int c = 0; c < 8 * NO; ++c)
-    if ((c >> J & 1) && !(c >> K & 1)) {
-      const int e = c | (1 << K);
-      const double2 t = xs[c >> 3][c & 7];
-      xs[c >> 3][c & 7] = xs[e >> 3][e & 7];
-      xs[e >> 3][e & 7] = t;
-    }
+    for (int c = 0; c < 8 * NO; ++c)
+      if ((c >> J & 1) && !(c >> K & 1)) {
+        const int e = c | (1 << K);
+        const double2 t = xs[c >> 3][c & 7];
+        xs[c >> 3][c & 7] = xs[e >> 3][e & 7];
+        xs[e >> 3][e & 7] = t;
+      }
+  }
 }
 
 template <int NO>
@@ -787,12 +790,13 @@ __device__ __forceinline__ uint32_t thread_table_entry(const GroupDesc& d, int e
 // kThreadBits selects the second octet -- a fourth axis in four-axis
 // groups).  `kap` holds 8 parity bits per tile of the batch (the axes'
 // out-of-tile rows): 4 for the load placement, 4 for the store placement.
+template <int NO>
 __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
                                             double2* __restrict__ dst, int k, int nvalid,
                                             const GroupDesc& G, const GateOp* __restrict__ ops,
                                             const double2* __restrict__ mats, unsigned kap,
                                             const uint32_t* ttab) {
-  constexpr int NO = kOctets;
+  constexpr int TB = NO == 2 ? 7 : 8;  // thread bits of the layout (planner.cpp)
   const int t = threadIdx.x;
   const int cb = k - 3;
   // Every thread sweeps both of its octets.  Octets past the batch's valid
@@ -808,19 +812,19 @@ __device__ __forceinline__ void apply_group(const double2* __restrict__ src,
   int a[NO], r[NO];
 #pragma unroll
   for (int q = 0; q < NO; ++q) {
-    const int oi = t + (q << kThreadBits);
-    a[q] = (v & 0xffffu) ^ (q ? G.tcol[kThreadBits] : 0);
-    r[q] = (v >> 16) ^ (q ? G.rtcol[kThreadBits] : 0);
+    const int oi = t + (q << TB);
+    a[q] = (v & 0xffffu) ^ (q ? G.tcol[TB] : 0);
+    r[q] = (v >> 16) ^ (q ? G.rtcol[TB] : 0);
     const int sh = 8 * (oi >> cb);  // tiles >= 4 exist only as garbage octets
     const unsigned kp = sh < 32 ? (kap >> sh) & 0xffu : 0u;
     if (kp & 1) r[q] ^= r0;
     if (kp & 2) r[q] ^= r1;
     if (kp & 4) r[q] ^= r2;
-    if (kOctets == 2 && (kp & 8)) r[q] ^= G.rtcol[kOctets == 2 ? kThreadBits : 0];
+    if (NO == 2 && (kp & 8)) r[q] ^= G.rtcol[NO == 2 ? TB : 0];
     if (kp & 16) a[q] ^= m0;
     if (kp & 32) a[q] ^= m1;
     if (kp & 64) a[q] ^= m2;
-    if (kOctets == 2 && (kp & 128)) a[q] ^= G.tcol[kOctets == 2 ? kThreadBits : 0];
+    if (NO == 2 && (kp & 128)) a[q] ^= G.tcol[NO == 2 ? TB : 0];
   }
   double2 x[NO][8];
 #pragma unroll
@@ -991,9 +995,15 @@ constexpr size_t kBlockedSmemBytesTma = kBlockedSmemBytes + 1024;
 // cp.async.bulk.tensor (one elected thread issues, an mbarrier per buffer
 // counts the bytes in, bulk groups track the stores); the chunk-restricted
 // instantiation keeps per-thread cp.async under the same layout.
-template <bool kChunk, bool kTma>
-__global__ void __launch_bounds__(kPassThreads, kCtasPerSm) k_blocked(BlockedParams p) {
+// kOct: the thread layout the plan was laid out for (HostPlan::octets): two
+// octets per thread and 128 threads, or one octet and 256 threads (small
+// states)
+template <bool kChunk, bool kTma, int kOct = kOctets>
+__global__ void __launch_bounds__(kOct == 2 ? (1 << NSB_THREAD_BITS) : 256, kCtasPerSm)
+    k_blocked(BlockedParams p) {
   constexpr bool kHw = kTma && !kChunk;
+  constexpr int kThreadBits = kOct == 2 ? nsb::kThreadBits : 8;  // the layout's (shadows planner.h)
+  constexpr int kPassThreads = 1 << kThreadBits;
   const uint64_t c_mask = kChunk ? p.cmask : 0, c_val = kChunk ? p.cval : 0;
   const int c_bits = kChunk ? p.cbits : 0;
   // dynamic shared memory: 3 batch buffers (current, gate-sweep target,
@@ -1007,7 +1017,7 @@ __global__ void __launch_bounds__(kPassThreads, kCtasPerSm) k_blocked(BlockedPar
   GroupDesc* s_groups = reinterpret_cast<GroupDesc*>(s_mats + kMaxPassMats);
   GateOp* s_ops = reinterpret_cast<GateOp*>(s_groups + kMaxPassGates);
   __shared__ PassDesc sp;
-  __shared__ uint64_t s_hi[1 << (kTileQubitsMax - kThreadBits)];  // offsets of tile bits >= kThreadBits
+  __shared__ uint64_t s_hi[1 << (kTileQubitsMax - 7)];  // offsets of tile bits >= kThreadBits
   __shared__ unsigned s_gm[kMaxPassGates];  // per group: out-of-tile axis parities per batch tile
   __shared__ uint32_t s_ttab[kMaxPassGates][32];  // per group: thread-address tables
   __shared__ double red[32];
@@ -1025,7 +1035,7 @@ __global__ void __launch_bounds__(kPassThreads, kCtasPerSm) k_blocked(BlockedPar
   bool etma = false;
   int k_cur = 0;   // the pass's tile qubits
   int pi_tid = 0;  // TMA pass: the permuted index of this thread's bits
-  __shared__ int s_pij[1 << (kTileQubitsMax - kThreadBits)];  // ... of j << kThreadBits
+  __shared__ int s_pij[1 << (kTileQubitsMax - 7)];  // ... of j << kThreadBits
   auto eslot = [&](int b, int j) {
     if (kTma && etma) return swz_tma(pi_tid ^ s_pij[j]);
     return swz((b << k_cur) + tid + (j << kThreadBits));
@@ -1282,7 +1292,7 @@ __global__ void __launch_bounds__(kPassThreads, kCtasPerSm) k_blocked(BlockedPar
         const bool cta_sync = d.sync();  // read before the sweep: no load latency after it
         double2* out = smem + spare * kTileAmpsMax;
         if (!warp_idle)
-          apply_group(tile, out, k, nvalid, d, s_ops + d.op_begin, s_mats, s_gm[g], s_ttab[g]);
+          apply_group<kOct>(tile, out, k, nvalid, d, s_ops + d.op_begin, s_mats, s_gm[g], s_ttab[g]);
         if (pending && g == 0 && !early) request_next();
         const int tmp = cur;
         cur = spare;
@@ -1616,6 +1626,7 @@ struct nsb_ctx {
   int sm_count = 0;
   int blocked_grid = 0;  // co-resident CTAs of k_blocked
   bool tma_ok = false;   // the TMA instantiation is co-resident on the same grid
+  bool o1_ok = false;    // ... and the one-octet layout
   int n = 0;
   uint64_t n_amps = 0;
   DevBuf<double2> amps;
@@ -2091,12 +2102,18 @@ const dev::TmaPass* plan_tma(nsb_ctx* c, nsb_plan* P, const PassDesc* passes) {
   return P->tm_dev[w].ptr;
 }
 
-void* blocked_kernel(bool chunk, bool tma) {
-  return chunk ? (tma ? reinterpret_cast<void*>(dev::k_blocked<true, true>)
-                      : reinterpret_cast<void*>(dev::k_blocked<true, false>))
-               : (tma ? reinterpret_cast<void*>(dev::k_blocked<false, true>)
-                      : reinterpret_cast<void*>(dev::k_blocked<false, false>));
+template <int O>
+void* blocked_kernel_o(bool chunk, bool tma) {
+  return chunk ? (tma ? reinterpret_cast<void*>(dev::k_blocked<true, true, O>)
+                      : reinterpret_cast<void*>(dev::k_blocked<true, false, O>))
+               : (tma ? reinterpret_cast<void*>(dev::k_blocked<false, true, O>)
+                      : reinterpret_cast<void*>(dev::k_blocked<false, false, O>));
 }
+void* blocked_kernel(bool chunk, bool tma, int octets = 2) {
+  return octets == 1 ? blocked_kernel_o<1>(chunk, tma) : blocked_kernel_o<2>(chunk, tma);
+}
+// threads per CTA of a plan's kernel layout
+unsigned blocked_threads(int octets) { return octets == 1 ? 256u : unsigned(kPassThreads); }
 
 // launch k_blocked over [pb, pe) of `passes` cooperatively
 void launch_blocked(nsb_ctx* c, nsb_plan* P, const PassDesc* passes, int pb, int pe, double eps,
@@ -2128,9 +2145,11 @@ void launch_blocked(nsb_ctx* c, nsb_plan* P, const PassDesc* passes, int pb, int
   bp.tmaps = tma && !cmask ? plan_tma(c, P, passes) : nullptr;
   bp.tma_store = tma_store_mode();
   void* args[] = {&bp};
+  const int oct = P->host.octets;
   NSB_CUDA(cudaLaunchCooperativeKernel(
-      blocked_kernel(cmask != 0, tma), dim3(grid > 0 ? grid : P->grid), dim3(kPassThreads), args,
-      tma ? dev::kBlockedSmemBytesTma : dev::kBlockedSmemBytes, c->stream));
+      blocked_kernel(cmask != 0, tma, oct), dim3(grid > 0 ? grid : P->grid),
+      dim3(blocked_threads(oct)), args, tma ? dev::kBlockedSmemBytesTma : dev::kBlockedSmemBytes,
+      c->stream));
   P->last_launches += 1;
 }
 
@@ -2196,11 +2215,12 @@ int nsb_ctx_create(int32_t device, nsb_ctx** out, nsb_status* st) {
     NSB_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
     const int smem = static_cast<int>(dev::kBlockedSmemBytes);
     const int smem_tma = static_cast<int>(dev::kBlockedSmemBytesTma);
-    for (bool chunk : {false, true})
-      for (bool tma : {false, true})
-        NSB_CUDA(cudaFuncSetAttribute(blocked_kernel(chunk, tma),
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      tma ? smem_tma : smem));
+    for (int oct : {1, 2})
+      for (bool chunk : {false, true})
+        for (bool tma : {false, true})
+          NSB_CUDA(cudaFuncSetAttribute(blocked_kernel(chunk, tma, oct),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        tma ? smem_tma : smem));
     int per_sm = 0, per_sm_tma = 0;
     NSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::k_blocked<false, false>,
                                                            kPassThreads, smem));
@@ -2211,6 +2231,10 @@ int nsb_ctx_create(int32_t device, nsb_ctx** out, nsb_status* st) {
     // TMA plans run on the same persistent grid (NSB_TMA=0 or a smaller
     // residency: per-thread cp.async under the usual layout)
     ctx->tma_ok = per_sm_tma == per_sm;
+    int per_sm_o1 = 0;  // the one-octet layout (256 threads) on the same grid
+    NSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm_o1, dev::k_blocked<false, false, 1>, 256, smem));
+    ctx->o1_ok = per_sm_o1 == per_sm;
     ctx->scratch.alloc(4 * dev::kReduceBlocks + 64);
   });
   if (rc == NSB_OK) *out = ctx.release();
@@ -2451,6 +2475,7 @@ int nsb_plan_create_ex(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const doubl
     NSB_CUDA(cudaStreamCreateWithFlags(&P->rel, cudaStreamNonBlocking));
     if (flags & NSB_PLAN_EXACT) P->host.identity_budget = 0.0;
     P->host.allow_tma = c->tma_ok;
+    P->host.octets = c->o1_ok ? plan_octets(c->n) : 2;
     P->host.build(ops, n_ops, params, payloads, c->n, c->blocked_grid);
     HostPlan& H = P->host;
     {
@@ -2842,6 +2867,7 @@ int nsb_run_mma_streamed(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const dou
         try {
           H->identity_budget = n_ops ? budget * static_cast<double>(e - b) / n_ops : 0.0;
           H->allow_tma = c->tma_ok;
+          H->octets = c->o1_ok ? plan_octets(c->n) : 2;
           H->build_segment(ops + b, e - b, params, payloads, c->n, c->blocked_grid);
         } catch (...) {
           errs[s] = std::current_exception();
@@ -2877,7 +2903,7 @@ int nsb_run_mma_streamed(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const dou
       return e ? std::atoi(e) : 0;
     }();
     int grid = 0;
-    auto launch = [&](PartDev& d, int count, bool tma) {
+    auto launch = [&](PartDev& d, int count, bool tma, int oct) {
       dev::BlockedParams bp;
       bp.amps = c->amps.ptr;
       bp.n = c->n;
@@ -2900,7 +2926,7 @@ int nsb_run_mma_streamed(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const dou
       NSB_CUDA(cudaMemsetAsync(bar.ptr, 0, sizeof(unsigned), c->stream));
       void* args[] = {&bp};
       NSB_CUDA(cudaLaunchCooperativeKernel(
-          blocked_kernel(false, tma), dim3(grid), dim3(kPassThreads), args,
+          blocked_kernel(false, tma, oct), dim3(grid), dim3(blocked_threads(oct)), args,
           tma ? dev::kBlockedSmemBytesTma : dev::kBlockedSmemBytes, c->stream));
     };
     std::vector<double> scale(std::max<int64_t>(n_meas, 1), 1.0);
@@ -2983,7 +3009,7 @@ int nsb_run_mma_streamed(nsb_ctx* c, const nsb_op* ops, int64_t n_ops, const dou
             encode_tma_passes(mp, c->n, c->amps.ptr, tm);
             d.tmaps.upload(tm.data(), tm.size(), c->stream, pool);
           }
-          launch(d, static_cast<int>(mp.size()), H.tma);
+          launch(d, static_cast<int>(mp.size()), H.tma, H.octets);
         }
         if (s > 0) {  // planned parts already uploaded: release their host programs
           std::lock_guard<std::mutex> lk(mu);

@@ -292,6 +292,15 @@ double default_identity_budget() {
   return b;
 }
 
+int plan_octets(int n) {
+  static const int forced = [] {
+    const char* e = std::getenv("NSB_PLAN_OCTETS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced == 1 || forced == 2) return forced;
+  return n <= kSmallStateQubits ? 1 : 2;
+}
+
 bool tma_layout(const PassDesc& P, int n, int order, TmaLayout& L) {
   L = TmaLayout();
   if (P.k != kTileQubitsMax || P.tq[0] != 0 || P.tq[1] != 1 || P.tq[2] != 2 || n > kTmaMaxQubits)
@@ -844,11 +853,14 @@ bool place_gate(OpenGroup& G, const Axis* ga, int nq, int* pos) {
   return true;
 }
 
-// Warp-local sweeps: with warp positions W (kWarpBits tile positions, mask
-// wm) a group whose axes avoid them (and whose read map keeps them) can give
-// warp w exactly the amplitudes whose bits at W spell w -- its octets never
-// leave that set, so consecutive warp-local sweeps need only __syncwarp.
-constexpr int kWarpBits = kThreadBits - 5;
+// Warp-local sweeps: with warp positions W (warp-bit count tile positions,
+// mask wm) a group whose axes avoid them (and whose read map keeps them) can
+// give warp w exactly the amplitudes whose bits at W spell w -- its octets
+// never leave that set, so consecutive warp-local sweeps need only __syncwarp.
+// Thread layouts (HostPlan::octets): two octets per thread -> 128 threads, 7
+// thread bits, 2 warp bits; one octet -> 256 threads, 8 thread bits, 3 warp bits.
+constexpr int kMaxWarpBits = 3;
+inline int thread_bits_of(int octets) { return plan_thread_bits(octets); }
 
 bool warp_local(const OpenGroup& G, uint32_t wm) {
   if (G.axm & wm) return false;
@@ -863,8 +875,11 @@ bool warp_local(const OpenGroup& G, uint32_t wm) {
 // load_edge / store_edge (a TMA pass's copy layout, TmaLayout::perm): the
 // group reads the tile as TMA left it / writes the layout the TMA store reads
 // (swz_tma of the permuted index instead of swz11 on that side)
-void finish_group(OpenGroup& G, int k, GroupDesc& d, uint32_t wm,
+void finish_group(OpenGroup& G, int k, GroupDesc& d, uint32_t wm, int octets,
                   const int8_t* load_edge = nullptr, const int8_t* store_edge = nullptr) {
+  const int tb = thread_bits_of(octets);             // thread bits
+  const int ib = tb + (octets == 2 ? 1 : 0);         // octet-index bits
+  const int warp_bits = tb - 5;
   auto edge = [k](const int8_t* perm, uint32_t l) {
     uint32_t x = l & ~((1u << k) - 1);
     for (int i = 0; i < k; ++i)
@@ -875,7 +890,7 @@ void finish_group(OpenGroup& G, int k, GroupDesc& d, uint32_t wm,
   auto swz_st = [&](uint32_t l) { return store_edge ? edge(store_edge, l) : swz11(l); };
   const bool local = wm != 0;
   while (G.nax < 3) {  // pad with a free axis of the tile (outside the warp positions)
-    uint32_t f[3 + kWarpBits];
+    uint32_t f[3 + kMaxWarpBits];
     int nf = 0;
     for (int i = 0; i < G.nax; ++i) f[nf++] = G.ax[i].rin;  // rows span R (either basis)
     for (uint32_t w = wm; w; w &= w - 1) f[nf++] = w & (0u - w);
@@ -894,9 +909,9 @@ void finish_group(OpenGroup& G, int k, GroupDesc& d, uint32_t wm,
   uint32_t f[4] = {G.ax0[0].rin, G.ax0[1].rin, G.ax0[2].rin, na == 4 ? G.ax0[3].rin : 0u};
   Basis C = kernel_basis(f, na, k);
   if (static_cast<int>(C.size()) != k - na) throw std::logic_error("group axes are not dual");
-  uint32_t cw[kWarpBits > 0 ? kWarpBits : 1] = {};
+  uint32_t cw[kMaxWarpBits] = {};
   if (local) {  // index bits 5.. (the warp bits) pick the warp's coset of W
-    int wp[kWarpBits], nw = 0;
+    int wp[kMaxWarpBits], nw = 0;
     for (uint32_t w = wm; w; w &= w - 1) wp[nw++] = __builtin_ctz(w);
     auto phi = [&](uint32_t v) {
       uint32_t o = 0;
@@ -1010,7 +1025,7 @@ void finish_group(OpenGroup& G, int k, GroupDesc& d, uint32_t wm,
     }
   }
   if (local)
-    for (int j = kWarpBits - 1; j >= 0; --j) C.insert_at(5, cw[j]);
+    for (int j = warp_bits - 1; j >= 0; --j) C.insert_at(5, cw[j]);
   for (int i = 0; i < 3; ++i) {
     d.am[i] = static_cast<uint16_t>(swz_st(G.ax[i].m));          // final basis (stores)
     d.ram[i] = static_cast<uint16_t>(swz_ld(rmap(G.ax0[i].m)));  // load basis
@@ -1025,8 +1040,8 @@ void finish_group(OpenGroup& G, int k, GroupDesc& d, uint32_t wm,
     }
   }
   const int cb = k - 3;
-  for (int b = 0; b < kIndexBits; ++b) {
-    if (na == 4 && b == kThreadBits) {  // the octet index: axis 3 (load), its final axis (store)
+  for (int b = 0; b < ib; ++b) {
+    if (na == 4 && b == tb) {  // the octet index: axis 3 (load), its final axis (store)
       d.tcol[b] = static_cast<uint16_t>(swz_st(G.ax[3].m));
       d.rtcol[b] = static_cast<uint16_t>(swz_ld(rmap(G.ax0[3].m)));
       continue;
@@ -1071,6 +1086,7 @@ void HostPlan::build(const nsb_op* ops, int64_t n_ops, const double* params,
         parts[s].identity_budget =
             total_budget * static_cast<double>(e - b) / static_cast<double>(n_ops);
         parts[s].allow_tma = allow_tma;
+        parts[s].octets = octets;
         parts[s].build_serial(ops + b, e - b, params, payloads, n, workers);
       } catch (...) {
         errors[s] = std::current_exception();
@@ -1374,7 +1390,8 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
   // 30 % more gate ops run and the kernel -- bound by per-op latency, not by
   // shared-memory traffic -- got 31 % slower (832 vs 634 ms).
   static const bool four_axis_env = std::getenv("NSB_FOUR_AXIS") != nullptr;
-  const bool four_axis = kOctets == 2 && k == kTileQubitsMax && four_axis_env;
+  const bool four_axis = octets == 2 && k == kTileQubitsMax && four_axis_env;
+  const int tb = thread_bits_of(octets), warp_bits = tb - 5;
   // one group slot stays free for a trailing read-map sweep
   auto pass_groups = pack_groups(masks, k, low, all, 256, sets, &deps, &weights,
                                  kMaxPassGates - 1, kMaxPassMats);
@@ -1525,10 +1542,10 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
     // the assignment with the most warp-local sweep transitions.
     std::vector<uint32_t> wsel(closed.size(), 0u);
     bool pt = false;  // this pass's tiles move by TMA (planner.h "TMA tiles")
-    if (k - 3 >= kThreadBits && !closed.empty()) {  // warp bits of the octet index are tile-local
+    if (k - 3 >= tb && !closed.empty()) {  // warp bits of the octet index are tile-local
       std::vector<uint32_t> cands;
       for (uint32_t wm = 1; wm < (1u << k); ++wm)
-        if (__builtin_popcount(wm) == kWarpBits) cands.push_back(wm);
+        if (__builtin_popcount(wm) == warp_bits) cands.push_back(wm);
       const size_t G = closed.size(), W = cands.size();
       std::vector<uint8_t> ok(G * W);
       for (size_t g = 0; g < G; ++g)
@@ -1644,8 +1661,8 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
             const size_t last = closed.size() - 1;
             OpenGroup f = closed.front(), l = closed.back();
             GroupDesc df{}, dl{};
-            finish_group(f, k, df, wsel.front(), L.perm, last == 0 ? L.perm : nullptr);
-            finish_group(l, k, dl, wsel.back(), last == 0 ? L.perm : nullptr, L.perm);
+            finish_group(f, k, df, wsel.front(), octets, L.perm, last == 0 ? L.perm : nullptr);
+            finish_group(l, k, dl, wsel.back(), octets, last == 0 ? L.perm : nullptr, L.perm);
             pt = rank3(df.rtcol) == 3 && rank3(dl.tcol) == 3;
           }
           if (pt) std::memcpy(P.tperm, L.perm, sizeof P.tperm);
@@ -1676,7 +1693,7 @@ void HostPlan::schedule_run(std::vector<PhysGate>& run, int k) {
         if (wm >> b & 1) split_fixed = split_fixed && b >= 3 && P.tperm[b] == b;
       const bool edge = pt && (g == 0 || g + 2 == closed.size());
       const bool next = g + 1 < closed.size() && wm && wsel[g + 1] == wm && !(edge && !split_fixed);
-      finish_group(H, k, d, wm, pt && g == 0 ? P.tperm : nullptr,
+      finish_group(H, k, d, wm, octets, pt && g == 0 ? P.tperm : nullptr,
                    pt && g + 1 == closed.size() ? P.tperm : nullptr);
       if (!next) d.n_ops_sync |= 128;
       if (next) ++out.n_warp;
@@ -1837,6 +1854,7 @@ extern "C" int nsb_plan_analyze(const nsb_op* ops, int64_t n_ops, const double* 
   }
   try {
     nsb::HostPlan H;
+    H.octets = nsb::plan_octets(n_qubits);
     H.build(ops, n_ops, params, payloads, n_qubits, 296);  // 2 CTAs x 148 SMs (B200)
     fill_info(H, info);
     if (class_counts)
@@ -1863,6 +1881,7 @@ extern "C" int nsb_host_plan_build(const nsb_op* ops, int64_t n_ops, const doubl
   *out = nullptr;
   try {
     auto* H = new nsb::HostPlan();
+    H->octets = nsb::plan_octets(n_qubits);
     try {
       H->build(ops, n_ops, params, payloads, n_qubits, workers);
     } catch (...) {
@@ -1945,6 +1964,8 @@ extern "C" int nsb_host_plan_view(const void* plan, nsb_plan_view* v) {
   v->n_qubits = H->n_qubits;
   v->tile_qubits = H->tile_qubits;
   v->tma_edges = H->tma ? 1 : 0;
+  v->octets = H->octets;
+  v->thread_bits = nsb::plan_thread_bits(H->octets);
   v->mma_ok = H->mma_ok;
   v->n_measures = static_cast<int32_t>(H->n_measures);
   v->pass_desc_bytes = sizeof(nsb::PassDesc);

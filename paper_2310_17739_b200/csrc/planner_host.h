@@ -81,6 +81,9 @@ struct HostPlan {
   // loads under swz_tma, the last one stores under it
   bool tma = false;
   bool allow_tma = true;  // set by the caller: the device runs the TMA kernel
+  // octets per thread of the blocked kernel this plan is laid out for (set by
+  // the caller, plan_octets): 2 (128 threads) or 1 (256 threads: small states)
+  int octets = kOctets;
   // Gates within rounding of a scalar identity s I (e.g. the fused H.H / S.Sdg
   // products between consecutive JW terms, 1 + 2^-52 on the diagonal) are not
   // executed.  Their scalar is kept: the reference's state carries the product
@@ -151,6 +154,13 @@ struct TmaLayout {
 bool tma_layout(const PassDesc& P, int n, int order, TmaLayout& L);
 
 void plan_info(const HostPlan& H, nsb_plan_info* info);
+// the thread layout for an n-qubit state: one octet per thread up to
+// kSmallStateQubits (more warps on the few tiles of a small state: ucc8 0.51
+// vs 0.83 ms, mcm16 4.77 vs 5.45 ms), two above (deep21 602 vs 636 ms);
+// NSB_PLAN_OCTETS overrides
+constexpr int kSmallStateQubits = 17;
+int plan_octets(int n);
+inline int plan_thread_bits(int octets) { return octets == 2 ? 7 : 8; }
 double default_identity_budget_value();  // NSB_IDENTITY_BUDGET or 3e-11
 // passes of item `item` runnable chunk by chunk over the qubits *cmask (planner.cpp)
 int chunk_prefix(const HostPlan& H, int64_t item, int avoid_q, int want_bits, uint64_t* cmask);

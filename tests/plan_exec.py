@@ -58,6 +58,8 @@ class HostPlan:
         assert v.group_desc_bytes == GROUP_DT.itemsize and v.gate_op_bytes == OP_DT.itemsize
         self.n, self.k, self.mma_ok, self.n_measures = v.n_qubits, v.tile_qubits, v.mma_ok, v.n_measures
         self.tma = bool(v.tma_edges)
+        # the kernel thread layout the plan is laid out for (planner.cpp)
+        self.octets, self.thread_bits = v.octets, v.thread_bits
 
         def arr(p, count, dt):
             if count == 0:
@@ -228,7 +230,8 @@ def _check() -> bool:
     return os.environ.get("NSB_PLAN_EXEC_CHECK", "1") != "0"
 
 
-def _apply_group(B, G, ops, mats, tbases, k, nvalid, u_load=_swz, u_store=_swz):
+def _apply_group(B, G, ops, mats, tbases, k, nvalid, u_load=_swz, u_store=_swz, tb=THREAD_BITS,
+                 octets=OCTETS):
     """One octet sweep over a batch B (nvalid tiles of 2^k stored back to
     back), enumerated exactly as k_blocked's apply_group: swizzled shared-
     memory addresses, un-swizzled here (swz is an involution) to index B."""
@@ -237,12 +240,13 @@ def _apply_group(B, G, ops, mats, tbases, k, nvalid, u_load=_swz, u_store=_swz):
     t = np.arange(n_act, dtype=np.int64)
     a = np.zeros(n_act, np.int64)
     r = np.zeros(n_act, np.int64)
-    for b in range(INDEX_BITS):
+    ib = tb + (1 if octets == 2 else 0)
+    for b in range(ib):
         a ^= np.where((t >> b) & 1, int(G["tcol"][b]), 0)
         r ^= np.where((t >> b) & 1, int(G["rtcol"][b]), 0)
     tile = t >> cb
-    q_col = int(G["tcol"][THREAD_BITS]) if THREAD_BITS < 8 else 0  # one octet per thread: none
-    q_rcol = int(G["rtcol"][THREAD_BITS]) if THREAD_BITS < 8 else 0
+    q_col = int(G["tcol"][tb]) if octets == 2 else 0  # one octet per thread: none
+    q_rcol = int(G["rtcol"][tb]) if octets == 2 else 0
     am = [int(v) for v in G["am"]] + [q_col]
     ram = [int(v) for v in G["ram"]] + [q_rcol]
     kmat = int(G["kmat"])
@@ -264,7 +268,7 @@ def _apply_group(B, G, ops, mats, tbases, k, nvalid, u_load=_swz, u_store=_swz):
     if _check():
         assert len(np.unique(np.concatenate(st))) == 8 * n_act  # octets partition the batch
         assert len(np.unique(np.concatenate(ld))) == 8 * n_act
-        n_warps = THREADS // 32
+        n_warps = (1 << tb) // 32
         warp = (t >> 5) & (n_warps - 1)  # octet-index bits 5 .. kThreadBits-1
         # physical shared-memory slots per warp (the kernel's addresses)
         loads = [np.sort(np.concatenate([l[warp == w] for l in ld])) for w in range(n_warps)]
@@ -278,7 +282,8 @@ def _apply_group(B, G, ops, mats, tbases, k, nvalid, u_load=_swz, u_store=_swz):
     return loads, stores
 
 
-def _apply_group_batches(Bs, G, ops, mats, tbs, k, nvalid, u_load=_swz, u_store=_swz):
+def _apply_group_batches(Bs, G, ops, mats, tbs, k, nvalid, u_load=_swz, u_store=_swz,
+                         tb=THREAD_BITS, octets=OCTETS):
     """_apply_group on every batch at once: Bs (n_batches, nvalid << k),
     tbs (n_batches, nvalid) tile bases."""
     cb = k - 3
@@ -286,12 +291,13 @@ def _apply_group_batches(Bs, G, ops, mats, tbs, k, nvalid, u_load=_swz, u_store=
     t = np.arange(n_act, dtype=np.int64)
     a0 = np.zeros(n_act, np.int64)
     r0 = np.zeros(n_act, np.int64)
-    for b in range(INDEX_BITS):
+    ib = tb + (1 if octets == 2 else 0)
+    for b in range(ib):
         a0 ^= np.where((t >> b) & 1, int(G["tcol"][b]), 0)
         r0 ^= np.where((t >> b) & 1, int(G["rtcol"][b]), 0)
     tile = t >> cb
-    q_col = int(G["tcol"][THREAD_BITS]) if THREAD_BITS < 8 else 0  # one octet per thread: none
-    q_rcol = int(G["rtcol"][THREAD_BITS]) if THREAD_BITS < 8 else 0
+    q_col = int(G["tcol"][tb]) if octets == 2 else 0  # one octet per thread: none
+    q_rcol = int(G["rtcol"][tb]) if octets == 2 else 0
     am = [int(v) for v in G["am"]] + [q_col]
     ram = [int(v) for v in G["ram"]] + [q_rcol]
     kmat = int(G["kmat"])
@@ -369,7 +375,8 @@ def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12, workers=1
                 B = np.where((idx >> cq) & 1, 0.0, B * (1.0 / np.sqrt(carry_p0)))
             for gi, G in enumerate(groups):
                 sw = edges(P, gi, len(groups))
-                _apply_group_batches(B, G, pops, block, tbs, k, nv, *sw)
+                _apply_group_batches(B, G, pops, block, tbs, k, nv, *sw, tb=plan.thread_bits,
+                                     octets=plan.octets)
             state[idx] = B
         for cta in range(0 if fast else min(workers, n_tiles)):
             t_begin = cta * per + min(cta, extra)
@@ -384,7 +391,8 @@ def run_passes(plan: HostPlan, passes, state, carry_p0=1.0, eps=1e-12, workers=1
                 prev = None  # (loads, stores) of the previous sweep when only __syncwarp follows it
                 for gi, G in enumerate(groups):
                     sw = edges(P, gi, len(groups))
-                    loads, stores = _apply_group(B, G, pops, block, tbs, k, nvalid, *sw)
+                    loads, stores = _apply_group(B, G, pops, block, tbs, k, nvalid, *sw,
+                                                 tb=plan.thread_bits, octets=plan.octets)
                     if prev is not None and loads is not None:
                         for w in range(len(loads)):
                             # each warp reads its own writes (RAW) and overwrites
