@@ -155,10 +155,11 @@ bool tma_layout(const PassDesc& P, int n, int order, TmaLayout& L);
 
 void plan_info(const HostPlan& H, nsb_plan_info* info);
 // the thread layout for an n-qubit state: one octet per thread up to
-// kSmallStateQubits (more warps on the few tiles of a small state: ucc8 0.51
-// vs 0.83 ms, mcm16 4.77 vs 5.45 ms), two above (deep21 602 vs 636 ms);
-// NSB_PLAN_OCTETS overrides
-constexpr int kSmallStateQubits = 17;
+// kSmallStateQubits (more warps on the few tiles of a small state; filter
+// circuits, tools/oct_sweep.py: 16 q 4.78 vs 4.91 ms, 18 q 6.51 vs 8.15 ms,
+// 19 q 8.74 vs 8.62 ms, 21 q 30.8 vs 29.5 ms), two above; NSB_PLAN_OCTETS
+// overrides
+constexpr int kSmallStateQubits = 18;
 int plan_octets(int n);
 inline int plan_thread_bits(int octets) { return octets == 2 ? 7 : 8; }
 double default_identity_budget_value();  // NSB_IDENTITY_BUDGET or 3e-11
