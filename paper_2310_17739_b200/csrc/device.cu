@@ -3443,7 +3443,7 @@ int nsb_shard_swap_overlap_ce(nsb_ctx* c, int32_t global_bit, int32_t local_q, n
     const Item& it = P->host.items[static_cast<size_t>(seg)];
     const int b = (c->rank >> global_bit) & 1;
     const uint64_t half = c->n_amps >> 1;
-    if (np == 0) {  // nothing chunkable (or short runs): the SM swap, then the item
+    auto sm_swap_then_item = [&]() {
       const int clog = static_cast<int>(std::min<uint64_t>(16, c->n - 1));
       comm_barrier(c);
       dev::k_shard_swap_p2p<<<static_cast<unsigned>(c->sm_count * 4), 256, 0, c->stream>>>(
@@ -3452,6 +3452,10 @@ int nsb_shard_swap_overlap_ce(nsb_ctx* c, int32_t global_bit, int32_t local_q, n
       comm_barrier(c);
       run_item(c, P, it);
       NSB_CUDA(cudaStreamSynchronize(c->stream));
+      if (n_chunked) *n_chunked = 0;
+    };
+    if (np == 0) {  // nothing chunkable (or short runs): the SM swap, then the item
+      sm_swap_then_item();
       return;
     }
     if (!c->xfer) NSB_CUDA(cudaStreamCreateWithFlags(&c->xfer, cudaStreamNonBlocking));
@@ -3510,7 +3514,10 @@ int nsb_shard_swap_overlap_ce(nsb_ctx* c, int32_t global_bit, int32_t local_q, n
     const int hs = gh >= 0 ? groups[gh].lo : p1;
     const int ds = gd >= 0 ? groups[gd].lo : hs + (gh >= 0 ? groups[gh].bits : 0);
     const uint64_t n_outer = uint64_t(1) << __builtin_popcountll(other);
-    if (n_outer > 4096) throw std::invalid_argument("swap region too fragmented for copy engines");
+    if (n_outer > 4096) {  // too many copies to enqueue (both partners decide alike)
+      sm_swap_then_item();
+      return;
+    }
     const uint64_t cap = std::max<uint64_t>(run, (stage_bytes > 0 ? static_cast<uint64_t>(stage_bytes)
                                                                   : (uint64_t(4) << 30)) / sizeof(double2));
     const uint64_t chunk_amps = half >> cb;
