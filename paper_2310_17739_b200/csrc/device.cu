@@ -3543,6 +3543,23 @@ int nsb_shard_swap_overlap_ce(nsb_ctx* c, int32_t global_bit, int32_t local_q, n
           for (uint64_t h0 = 0; h0 < H; h0 += per) pieces.push_back({o, d0, 1, h0, std::min(per, H - h0)});
       }
     }
+    {  // staging blocks per swap (one flag word each): else the SM swap
+      int blocks = 0;
+      for (size_t p0 = 0; p0 < pieces.size(); ++blocks) {
+        uint64_t used = 0;
+        size_t q = p0;
+        for (; q < pieces.size(); ++q) {
+          const uint64_t amps = pieces[q].nd * pieces[q].nh * run;
+          if (used + amps > slot) break;
+          used += amps;
+        }
+        p0 = q;
+      }
+      if (blocks * n_ch > dev::kShardFlagWords) {
+        sm_swap_then_item();
+        return;
+      }
+    }
     auto copy3d_on = [&](cudaStream_t strm, double2* dst, bool dst_dense, const double2* src,
                          bool src_dense, const Piece& pc, cudaMemcpyKind kind) {
       if (run >= (uint64_t(1) << 20)) {  // long runs: plain 1-D copies, run by run
